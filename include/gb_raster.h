@@ -1,0 +1,223 @@
+/*
+ * gb_raster.h -- C-ABI of the B200-native Gaussian Billboards rasterizer.
+ *
+ * This is the drop-in boundary for the reference's rasterizer API
+ * (/root/reference/proj/include/gbil).  The reference has no FFI: its
+ * boundary is the C++ header API listed below, and each entry point here
+ * replaces one of those functions (file:line cited at each declaration).
+ * Plain pointers and sizes only; every device pointer is fp32/int32 CUDA
+ * global memory owned by the caller unless stated.  All calls are
+ * stream-ordered on the context's stream and asynchronous unless stated.
+ * A context is not thread-safe: use one per host thread / GPU.
+ *
+ * Error model: every reference throw site maps to a status code
+ * (std::invalid_argument -> GB_INVALID_ARGUMENT / GB_MISMATCH,
+ * adam's std::runtime_error -> GB_NONFINITE); the message of the last failure
+ * on the calling thread is returned by gb_last_error_string().  NaNs in the
+ * inputs propagate silently, as in the reference.
+ */
+#ifndef GB_RASTER_H
+#define GB_RASTER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GB_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define GB_API __attribute__((visibility("default")))
+#else
+#define GB_API
+#endif
+
+typedef enum {
+    GB_OK = 0,
+    GB_INVALID_ARGUMENT = 1, /* validate() throws: core.hpp:36-41, 109-115; raster.hpp:28-31 */
+    GB_MISMATCH = 2,         /* fingerprint / size guards: raster.hpp:204-205, 280-287 */
+    GB_CUDA_ERROR = 3,
+    GB_OOM = 4,
+    GB_NONFINITE = 5, /* adam_step non-finite gradient: optim.hpp:81-83 */
+    GB_NOT_SUPPORTED = 6
+} gb_status;
+
+#define GB_MODE_ORTHO 0   /* the reference's ImagePlaneCamera (core.hpp:102-116) */
+#define GB_MODE_PINHOLE 1 /* perspective 2DGS extension (no reference) */
+
+typedef struct gb_context gb_context;
+typedef struct gb_binning gb_binning;
+
+/* ColorGridConfig (core.hpp:29-42) */
+typedef struct {
+    int32_t n;
+    int32_t _pad;
+    double sigma;
+} gb_grid_config;
+
+/* SplatSet (core.hpp:53-87), structure-of-arrays, fp32 device pointers.
+ * ortho  : position 2K (x,y), depth_key K, theta K
+ * pinhole: position 3K world mean (x,y,z), quat 4K (w,x,y,z), unnormalised
+ * both   : log_scale 2K (u,v), opacity_logit K, grid K*n*n*3 in
+ *          (i_u, i_v, channel) order (core.hpp:44-48). */
+typedef struct {
+    int64_t count;
+    gb_grid_config grid;
+    const float *position;
+    const float *depth_key;
+    const float *theta;
+    const float *quat;
+    const float *log_scale;
+    const float *opacity_logit;
+    const float *grid_values;
+} gb_splats;
+
+/* GradientBuffer (core.hpp:140-178) with the same layout as gb_splats.
+ * Backward ACCUMULATES into it (caller zeroes), so several views can sum
+ * into one buffer.  depth_key never receives a gradient. */
+typedef struct {
+    float *position;
+    float *depth_key;
+    float *theta;
+    float *quat;
+    float *log_scale;
+    float *opacity_logit;
+    float *grid_values;
+} gb_grads;
+
+/* ImagePlaneCamera (core.hpp:104-116) plus the pinhole extension:
+ * OpenCV convention, x_pix = fx*X/Z + cx with pixel centres at i + 0.5,
+ * world->camera [rot | trans]. */
+typedef struct {
+    int32_t mode;
+    int32_t width;
+    int32_t height;
+    int32_t _pad;
+    double background[3];
+    double fx, fy, cx, cy;
+    double rot[9];
+    double trans[3];
+    double near_plane;
+} gb_camera;
+
+/* RasterConfig (raster.hpp:21-32).  `threads` is accepted and ignored
+ * (the GPU parallelises over tiles).  tile_size must be in [1, 16] on the GPU path. */
+typedef struct {
+    int32_t tile_size;
+    int32_t threads;
+    double cutoff_radius;
+    double alpha_skip;
+    double early_stop_transmittance;
+} gb_raster_config;
+
+/* RenderOutput (core.hpp:123-136), caller-owned device buffers; the
+ * fingerprint fields are written by gb_render_forward. */
+typedef struct {
+    int32_t width;
+    int32_t height;
+    float *color;               /* W*H*3, HWC, unclamped */
+    float *final_transmittance; /* W*H */
+    int32_t *last_rank;         /* W*H, -1 if nothing composited */
+    int64_t splat_count;
+    int32_t grid_n;
+    int32_t tile_size;
+} gb_render_out;
+
+/* LearningRates / AdamConfig / AdamState (optim.hpp:17-72).  The pinhole
+ * rotation quaternion uses the `theta` (rotation) rate. */
+typedef struct {
+    double position, theta, log_scale, opacity_logit, color_grid, position_gamma;
+} gb_learning_rates;
+
+typedef struct {
+    int64_t t;
+    double beta1, beta2, epsilon;
+    gb_grads m; /* first moments, same layout as the gradients, zero-initialised */
+    gb_grads v; /* second moments */
+} gb_adam_state;
+
+/* ---- context ------------------------------------------------------------ */
+GB_API int gb_abi_version(void);
+GB_API const char *gb_last_error_string(void);
+GB_API gb_status gb_context_create(int device, gb_context **out);
+GB_API gb_status gb_context_destroy(gb_context *ctx);
+/* Run all subsequent work on `stream` (a cudaStream_t; NULL = the legacy default stream).
+ * A fresh context uses its own non-blocking stream. */
+GB_API gb_status gb_context_set_stream(gb_context *ctx, void *stream);
+GB_API void *gb_context_stream(gb_context *ctx);
+GB_API gb_status gb_sync(gb_context *ctx);
+/* Number of kernels this context has launched (for the bench's gpu_launches claim). */
+GB_API int64_t gb_context_launch_count(const gb_context *ctx);
+
+/* ---- binning: TileBinning + build_binning (raster.hpp:105-147) ------------ */
+GB_API gb_status gb_binning_create(gb_context *ctx, gb_binning **out);
+GB_API gb_status gb_binning_destroy(gb_binning *b);
+/* Replaces build_binning(const SplatSet&, const ImagePlaneCamera&, const RasterConfig&)
+ * (raster.hpp:116-117).  Device-resident result, reused by forward and
+ * backward; also caches the per-primitive screen headers (K1).  Blocks once
+ * on the stream to learn the pair count P. */
+GB_API gb_status gb_build_binning(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_raster_config *cfg,
+                           gb_binning *b);
+GB_API gb_status gb_binning_info(const gb_binning *b, int32_t *tiles_x, int32_t *tiles_y, int64_t *total);
+/* Synchronous test hook: per-tile lists as CSR on the host
+ * (offsets[tiles+1], values[total]) -- TileBinning::tiles. */
+GB_API gb_status gb_binning_copy_to_host(gb_context *ctx, const gb_binning *b, int64_t *offsets, int32_t *values);
+
+/* ---- render ---------------------------------------------------------------- */
+/* Replaces render_forward(const SplatSet&, const ImagePlaneCamera&, const TileBinning&)
+ * (raster.hpp:201-202). */
+GB_API gb_status gb_render_forward(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_binning *b,
+                            gb_render_out *out);
+/* Replaces render_backward(..., const RenderOutput&, const std::vector<double>& image_grad)
+ * (raster.hpp:277-279).  image_grad is W*H*3 on the device; gradients are
+ * accumulated into *g. */
+GB_API gb_status gb_render_backward(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_binning *b,
+                             const gb_render_out *out, const float *image_grad, gb_grads *g);
+/* Replaces render(const SplatSet&, const ImagePlaneCamera&, const RasterConfig&)
+ * (raster.hpp:389-392); `scratch` receives the binning. */
+GB_API gb_status gb_render(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_raster_config *cfg,
+                    gb_binning *scratch, gb_render_out *out);
+
+/* ---- losses (train.hpp:120-133; L1 is the BASELINE configs' loss) --------- */
+/* grad[i] = scale*sign(color-target) (sign(0) = 0); *loss += scale*sum|color-target|. */
+GB_API gb_status gb_l1_loss(gb_context *ctx, const float *color, const float *target, int64_t n, float scale, float *grad,
+                     float *loss);
+/* grad[i] = 2*scale*(color-target); *loss += scale*sum (color-target)^2. */
+GB_API gb_status gb_mse_loss(gb_context *ctx, const float *color, const float *target, int64_t n, float scale, float *grad,
+                      float *loss);
+
+/* ---- optimiser: adam_step (optim.hpp:96-117) ------------------------------ */
+/* params uses the gb_grads layout (mutable parameter arrays).  Increments
+ * state->t.  Non-finite gradients are detected on the device first; if any is
+ * found no parameter is updated and gb_adam_check() reports GB_NONFINITE with
+ * the group and index. */
+GB_API gb_status gb_adam_step(gb_context *ctx, int32_t mode, int64_t count, int32_t n, gb_grads *params, const gb_grads *g,
+                       gb_adam_state *state, const gb_learning_rates *lrs);
+/* Synchronous.  group: 0 position, 1 theta/quat, 2 log_scale, 3 opacity, 4 grid. */
+GB_API gb_status gb_adam_check(gb_context *ctx, int32_t *group, int64_t *index);
+
+/* ---- seeded synthetic inputs (rng.hpp:12-46 semantics), host-only ---------- */
+typedef struct {
+    int32_t mode;
+    int32_t n;
+    int64_t count;
+    uint64_t seed;
+    double mean_lo, mean_hi; /* pinhole: uniform means in [lo,hi)^3 when mean_sigma <= 0 */
+    double mean_sigma;       /* pinhole: N(0, mean_sigma^2) means when > 0 */
+    double log_scale_lo, log_scale_hi;
+    int32_t width, height; /* ortho: positions uniform over the image */
+} gb_scene_spec;
+/* Geometry from Rng(seed), textures from Rng(seed+1).  Host fp32 buffers. */
+GB_API gb_status gb_scene_generate(const gb_scene_spec *spec, float *position, float *depth_key, float *theta, float *quat,
+                            float *log_scale, float *opacity_logit, float *grid_values);
+/* n uniforms in [0,1) from Rng(seed), rounded to fp32 (targets use seed+2+view). */
+GB_API gb_status gb_uniform_fill(uint64_t seed, int64_t n, float *out);
+/* Raw Rng streams in fp64, for parity with rng.hpp. */
+GB_API gb_status gb_rng_uniform(uint64_t seed, int64_t n, double *out);
+GB_API gb_status gb_rng_normal(uint64_t seed, int64_t n, double mean, double stddev, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

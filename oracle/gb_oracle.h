@@ -1,0 +1,147 @@
+/*
+ * gb_oracle.h -- TEST INFRASTRUCTURE ONLY (not product code).
+ *
+ * CPU fp64 restatement of the Gaussian Billboards rasterizer hot path of the
+ * reference (/root/reference/proj/include/gbil), used as the parity checker
+ * for the CUDA path.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load it.  The product library
+ * (paper_2412_12734_b200/libgb_raster.so) never links or calls it.
+ *
+ * Two geometry modes:
+ *   ORC_MODE_ORTHO   -- the reference's image-plane camera, restated
+ *                       operation-for-operation (raster.hpp:36-387,
+ *                       texture.hpp:27-111, core.hpp:21-100).  Pinned
+ *                       bit-exactly against the compiled reference
+ *                       (oracle/_ref/libgbil_ref.so) by tests/test_oracle_ref.py.
+ *   ORC_MODE_PINHOLE -- the perspective 2DGS extension the BASELINE configs
+ *                       need.  The reference has no perspective path
+ *                       (SPEC.md:279), so only the intersection, the cull box
+ *                       and the projection Jacobian are new; binning,
+ *                       compositing, thresholds, bilinear texture and the
+ *                       back-to-front adjoint are the reference's.  Geometry
+ *                       parity is pinned by finite differences and
+ *                       naive-vs-tiled checks (tests/test_oracle_pinhole.py),
+ *                       not by a reference test ("geometry parity unpinned").
+ */
+#ifndef GB_ORACLE_H
+#define GB_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_MODE_ORTHO 0
+#define ORC_MODE_PINHOLE 1
+
+#define ORC_OK 0
+#define ORC_INVALID_ARGUMENT 1
+#define ORC_MISMATCH 2
+#define ORC_OOM 4
+
+typedef struct {
+    int32_t mode;
+    int32_t width;
+    int32_t height;
+    int32_t _pad;
+    double background[3];
+    /* pinhole only */
+    double fx, fy, cx, cy;
+    double rot[9];   /* world->camera rotation, row-major */
+    double trans[3]; /* world->camera translation */
+    double near_plane;
+} orc_camera;
+
+typedef struct {
+    int32_t tile_size;
+    int32_t threads;
+    double cutoff_radius;
+    double alpha_skip;
+    double early_stop;
+} orc_config;
+
+typedef struct {
+    int64_t count;
+    int32_t n;
+    int32_t _pad;
+    double sigma;
+    const double *position;      /* ortho: 2K (x,y); pinhole: 3K world mean */
+    const double *depth_key;     /* ortho: K */
+    const double *theta;         /* ortho: K */
+    const double *quat;          /* pinhole: 4K (w,x,y,z), unnormalised */
+    const double *log_scale;     /* 2K */
+    const double *opacity_logit; /* K */
+    const double *grid;          /* K*n*n*3, (i_u, i_v, ch) order */
+} orc_splats;
+
+typedef struct {
+    double *position; /* same shapes as orc_splats */
+    double *depth_key;
+    double *theta;
+    double *quat;
+    double *log_scale;
+    double *opacity_logit;
+    double *grid;
+} orc_grads;
+
+typedef struct {
+    int32_t tiles_x;
+    int32_t tiles_y;
+    int64_t total;
+    int64_t *offsets; /* tiles_x*tiles_y + 1 */
+    int32_t *values;  /* total */
+} orc_binning;
+
+/* Kink margins for the parity protocol. */
+typedef struct {
+    double alpha_rel; /* |alpha - alpha_skip| <= alpha_rel*alpha_skip, same vs 0.999 cap */
+    double trans_rel; /* |T - early_stop| <= trans_rel*early_stop at any composite */
+    double grid_abs;  /* |u' - k| <= grid_abs for an interior texel boundary k; ||u|-sigma| <= grid_abs*2sigma/(n-1) */
+    double cond_min;  /* pinhole: |c_z| <= cond_min*|a||b| (grazing ray) */
+} orc_kink;
+
+int orc_build_binning(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, orc_binning *out);
+void orc_binning_free(orc_binning *b);
+
+/* Per-primitive binning geometry: depth key (fp32-rounded for pinhole), and
+ * the pixel range [x0,x1]x[y0,y1] or x0=-1 when culled. */
+int orc_project(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, double *depth, int32_t *rect);
+
+int orc_render_forward(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, const orc_binning *b,
+                       double *color, double *trans, int32_t *last, uint8_t *kink_px, const orc_kink *kink);
+
+/* kink_px (nullable): per-pixel flags from orc_render_forward (bit0 decision kink, bit1 early-stop kink).
+ * mag / slack (nullable): per-entry sum of |terms| and the kink slack (see gb_oracle.c). */
+int orc_render_backward(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, const orc_binning *b,
+                        const double *trans, const int32_t *last, const double *image_grad, orc_grads *g,
+                        const uint8_t *kink_px, orc_grads *mag, orc_grads *slack, const orc_kink *kink);
+
+int orc_render_naive(const orc_splats *s, const orc_camera *cam, double *color, double *trans);
+
+/* Central finite differences of L = sum(weights * render_naive(...).color)
+ * over every raw parameter (reference.hpp:66-105). */
+int orc_gradient_fd(const orc_splats *s, const orc_camera *cam, const double *weights, double step, orc_grads *g);
+
+/* Unit-level restatements for the SPEC known-answer tests. */
+void orc_uv_to_grid(double u, double v, int n, double sigma, int32_t *iu, int32_t *iv, double *fu, double *fv);
+void orc_bilinear(double u, double v, int n, double sigma, const double *grid, double *c);
+void orc_adj_bilinear(double u, double v, int n, double sigma, const double *grid, const double *c_hat,
+                      double *grid_grad, double *u_hat, double *v_hat);
+void orc_intersect_ortho(double px, double py, double x, double y, double theta, double log_su, double log_sv,
+                         double *u, double *v);
+int orc_intersect_pinhole(const orc_camera *cam, const double *mean, const double *quat, const double *log_scale,
+                          double px, double py, double *u, double *v);
+
+/* Adam for one parameter group (optim.hpp:76-90); returns index+1 of the first
+ * non-finite gradient, 0 if none. */
+int64_t orc_adam_group(double *p, const double *g, double *m, double *v, int64_t n, double lr, double beta1,
+                       double beta2, double eps, double bias1, double bias2);
+
+/* L1 loss: value = scale*sum|c-t|, grad = scale*sign(c-t) (sign(0)=0). */
+double orc_l1_loss(const double *c, const double *t, int64_t n, double scale, double *grad);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,530 @@
+// gb_capi.cu -- the extern "C" boundary (include/gb_raster.h) and the host
+// orchestration of K1..K7 on the context's CUDA stream.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gb_internal.cuh"
+
+namespace gb {
+size_t scan_temp_bytes(int64_t K);
+size_t sort_temp_bytes(int64_t P);
+cudaError_t launch_scan(void* temp, size_t temp_bytes, const uint32_t* counts, uint32_t* offsets, int64_t K,
+                        cudaStream_t st);
+cudaError_t launch_duplicate(int64_t K, int tiles_x, const uint32_t* offsets, const uint2* rects,
+                             const uint32_t* depth_bits, uint64_t* keys, int32_t* values, cudaStream_t st);
+cudaError_t launch_sort(void* temp, size_t temp_bytes, uint64_t* keys_in, uint64_t* keys_out, int32_t* vals_in,
+                        int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st);
+cudaError_t launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, int n_tiles, cudaStream_t st);
+cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                           const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                           float* color, float* trans, int32_t* last, cudaStream_t st);
+cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                            const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                            const float* trans, const int32_t* last, const float* image_grad, float* accum,
+                            float* grid_grad, cudaStream_t st);
+cudaError_t launch_loss(int kind, const float* color, const float* target, int64_t n, float scale, float* grad,
+                        float* loss, int sm_count, cudaStream_t st);
+cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned long long* bad, int sm_count,
+                              cudaStream_t st);
+cudaError_t launch_adam_update(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                               float eps, float inv_bias1, float inv_bias2, const unsigned long long* bad,
+                               int sm_count, cudaStream_t st);
+}  // namespace gb
+
+namespace {
+
+thread_local std::string g_last_error;
+
+gb_status fail(gb_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+#define GB_CUDA(call)                                                                                   \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess) {                                                                        \
+            if (e_ == cudaErrorMemoryAllocation)                                                        \
+                return fail(GB_OOM, "%s:%d: %s", __FILE__, __LINE__, cudaGetErrorString(e_));           \
+            return fail(GB_CUDA_ERROR, "%s:%d: %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+        }                                                                                               \
+    } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) {
+            cudaError_t e = cudaFree(p);
+            if (e != cudaSuccess) return e;
+            p = nullptr;
+            cap = 0;
+        }
+        size_t want = bytes < 256 ? 256 : bytes + bytes / 8;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            return e;
+        }
+        cap = want;
+        return cudaSuccess;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+struct gb_context {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, accum, adam_bad;
+    uint32_t* pinned_total = nullptr;
+};
+
+struct gb_binning {
+    gb_context* ctx = nullptr;
+    bool built = false;
+    int mode = 0;
+    int width = 0, height = 0;
+    gb_raster_config cfg{};
+    int tiles_x = 0, tiles_y = 0;
+    int64_t K = 0;
+    int n = 0;
+    int64_t P = 0;
+    DevBuf headers, rects, counts, offsets, depth, keys, values, ranges;
+};
+
+namespace {
+
+gb_status set_device(gb_context* ctx) {
+    GB_CUDA(cudaSetDevice(ctx->device));
+    return GB_OK;
+}
+
+gb_status validate_camera(const gb_camera* cam) {
+    if (!cam) return fail(GB_INVALID_ARGUMENT, "camera is null");
+    if (cam->width < 1 || cam->height < 1)
+        return fail(GB_INVALID_ARGUMENT, "ImagePlaneCamera: width and height must be >= 1");
+    for (int i = 0; i < 3; ++i)
+        if (!(cam->background[i] >= 0.0 && cam->background[i] <= 1.0))
+            return fail(GB_INVALID_ARGUMENT, "ImagePlaneCamera: background must be in [0,1]");
+    if (cam->mode != GB_MODE_ORTHO && cam->mode != GB_MODE_PINHOLE)
+        return fail(GB_INVALID_ARGUMENT, "camera mode must be GB_MODE_ORTHO or GB_MODE_PINHOLE");
+    if (cam->mode == GB_MODE_PINHOLE && !(cam->fx != 0.0 && cam->fy != 0.0 && std::isfinite(cam->fx) &&
+                                          std::isfinite(cam->fy)))
+        return fail(GB_INVALID_ARGUMENT, "pinhole camera: fx and fy must be finite and non-zero");
+    if (cam->width > 65535 * 16 || cam->height > 65535 * 16)
+        return fail(GB_NOT_SUPPORTED, "image too large");
+    return GB_OK;
+}
+
+gb_status validate_config(const gb_raster_config* cfg) {
+    if (!cfg) return fail(GB_INVALID_ARGUMENT, "config is null");
+    if (cfg->tile_size < 1) return fail(GB_INVALID_ARGUMENT, "RasterConfig: tile_size must be >= 1");
+    if (cfg->threads < 1) return fail(GB_INVALID_ARGUMENT, "RasterConfig: threads must be >= 1");
+    if (cfg->tile_size > 16) return fail(GB_NOT_SUPPORTED, "RasterConfig: tile_size > 16 is not supported on the GPU path");
+    return GB_OK;
+}
+
+gb_status validate_splats(const gb_splats* s, int mode) {
+    if (!s) return fail(GB_INVALID_ARGUMENT, "splats is null");
+    if (s->count < 0) return fail(GB_INVALID_ARGUMENT, "splat count must be >= 0");
+    if (s->count >= (int64_t)1 << 31) return fail(GB_NOT_SUPPORTED, "splat count must be < 2^31");
+    if (s->grid.n < 1) return fail(GB_INVALID_ARGUMENT, "ColorGridConfig: n must be >= 1");
+    if (!(s->grid.sigma > 0.0)) return fail(GB_INVALID_ARGUMENT, "ColorGridConfig: sigma must be > 0");
+    if (s->grid.n > 64) return fail(GB_NOT_SUPPORTED, "ColorGridConfig: n > 64 is not supported");
+    if (s->count == 0) return GB_OK;
+    if (!s->position || !s->log_scale || !s->opacity_logit || !s->grid_values)
+        return fail(GB_INVALID_ARGUMENT, "splats: position/log_scale/opacity_logit/grid_values must be non-null");
+    if (mode == GB_MODE_ORTHO && (!s->depth_key || !s->theta))
+        return fail(GB_INVALID_ARGUMENT, "ortho splats need depth_key and theta");
+    if (mode == GB_MODE_PINHOLE && !s->quat) return fail(GB_INVALID_ARGUMENT, "pinhole splats need quat");
+    if ((s->grid.n % 2) == 0 && (reinterpret_cast<uintptr_t>(s->grid_values) & 15))
+        return fail(GB_INVALID_ARGUMENT, "grid_values must be 16-byte aligned");
+    return GB_OK;
+}
+
+gb::CamConst make_cam_const(const gb_camera* cam) {
+    gb::CamConst cc;
+    cc.width = cam->width;
+    cc.height = cam->height;
+    cc.inv_fx = cam->mode == GB_MODE_PINHOLE ? (float)(1.0 / cam->fx) : 0.0f;
+    cc.inv_fy = cam->mode == GB_MODE_PINHOLE ? (float)(1.0 / cam->fy) : 0.0f;
+    for (int i = 0; i < 3; ++i) cc.bg[i] = (float)cam->background[i];
+    return cc;
+}
+
+gb::RasterConst make_raster_const(const gb_binning* b, int n, double sigma) {
+    gb::RasterConst rc;
+    rc.tile_size = b->cfg.tile_size;
+    rc.tiles_x = b->tiles_x;
+    rc.tiles_y = b->tiles_y;
+    rc.alpha_skip = (float)b->cfg.alpha_skip;
+    rc.early_stop = (float)b->cfg.early_stop_transmittance;
+    rc.tex_scale = (float)((double)(n - 1) / (2.0 * sigma));
+    rc.tex_offset = (float)((double)(n - 1) * 0.5);
+    rc.sigma = (float)sigma;
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gb_abi_version(void) { return GB_ABI_VERSION; }
+
+const char* gb_last_error_string(void) { return g_last_error.c_str(); }
+
+gb_status gb_context_create(int device, gb_context** out) {
+    if (!out) return fail(GB_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    int count = 0;
+    GB_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) return fail(GB_INVALID_ARGUMENT, "device %d out of range (%d)", device, count);
+    GB_CUDA(cudaSetDevice(device));
+    gb_context* ctx = new gb_context();
+    ctx->device = device;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) ctx->sm_count = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned_total, sizeof(uint32_t));
+    if (e != cudaSuccess) {
+        if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+        delete ctx;
+        return fail(GB_CUDA_ERROR, "context setup: %s", cudaGetErrorString(e));
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return GB_OK;
+}
+
+gb_status gb_context_destroy(gb_context* ctx) {
+    if (!ctx) return GB_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->scan_temp.release();
+    ctx->sort_temp.release();
+    ctx->keys_tmp.release();
+    ctx->vals_tmp.release();
+    ctx->accum.release();
+    ctx->adam_bad.release();
+    if (ctx->pinned_total) cudaFreeHost(ctx->pinned_total);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return GB_OK;
+}
+
+gb_status gb_context_set_stream(gb_context* ctx, void* stream) {
+    if (!ctx) return fail(GB_INVALID_ARGUMENT, "ctx is null");
+    ctx->stream = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
+    return GB_OK;
+}
+
+void* gb_context_stream(gb_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+gb_status gb_sync(gb_context* ctx) {
+    if (!ctx) return fail(GB_INVALID_ARGUMENT, "ctx is null");
+    if (gb_status s = set_device(ctx)) return s;
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GB_OK;
+}
+
+int64_t gb_context_launch_count(const gb_context* ctx) { return ctx ? ctx->launches : 0; }
+
+gb_status gb_binning_create(gb_context* ctx, gb_binning** out) {
+    if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
+    *out = new gb_binning();
+    (*out)->ctx = ctx;
+    return GB_OK;
+}
+
+gb_status gb_binning_destroy(gb_binning* b) {
+    if (!b) return GB_OK;
+    cudaSetDevice(b->ctx->device);
+    cudaStreamSynchronize(b->ctx->stream);
+    b->headers.release();
+    b->rects.release();
+    b->counts.release();
+    b->offsets.release();
+    b->depth.release();
+    b->keys.release();
+    b->values.release();
+    b->ranges.release();
+    delete b;
+    return GB_OK;
+}
+
+gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera* cam, const gb_raster_config* cfg,
+                           gb_binning* b) {
+    if (!ctx || !b) return fail(GB_INVALID_ARGUMENT, "null context or binning");
+    if (gb_status st = validate_camera(cam)) return st;
+    if (gb_status st = validate_config(cfg)) return st;
+    if (gb_status st = validate_splats(s, cam->mode)) return st;
+    if (gb_status st = set_device(ctx)) return st;
+    cudaStream_t stream = ctx->stream;
+    const int64_t K = s->count;
+    b->built = false;
+    b->mode = cam->mode;
+    b->width = cam->width;
+    b->height = cam->height;
+    b->cfg = *cfg;
+    b->tiles_x = (cam->width + cfg->tile_size - 1) / cfg->tile_size;
+    b->tiles_y = (cam->height + cfg->tile_size - 1) / cfg->tile_size;
+    b->K = K;
+    b->n = s->grid.n;
+    const int n_tiles = b->tiles_x * b->tiles_y;
+    const int64_t Kc = K > 0 ? K : 1;
+    GB_CUDA(b->headers.ensure(sizeof(gb::ScreenHeader) * Kc));
+    GB_CUDA(b->rects.ensure(sizeof(uint2) * Kc));
+    GB_CUDA(b->counts.ensure(sizeof(uint32_t) * Kc));
+    GB_CUDA(b->offsets.ensure(sizeof(uint32_t) * (Kc + 1)));
+    GB_CUDA(b->depth.ensure(sizeof(uint32_t) * Kc));
+    GB_CUDA(b->ranges.ensure(sizeof(uint2) * (n_tiles > 0 ? n_tiles : 1)));
+    const size_t scan_bytes = gb::scan_temp_bytes(Kc);
+    GB_CUDA(ctx->scan_temp.ensure(scan_bytes));
+
+    // K1
+    gb::ProjParams pp = gb::make_proj_params(s, cam, cfg, b->tiles_x, b->tiles_y);
+    GB_CUDA(gb::launch_project(pp, b->headers.as<gb::ScreenHeader>(), b->rects.as<uint2>(),
+                               b->counts.as<uint32_t>(), b->depth.as<uint32_t>(), stream));
+    ctx->launches += K > 0;
+    // K2a scan -> P
+    GB_CUDA(gb::launch_scan(ctx->scan_temp.p, ctx->scan_temp.cap, b->counts.as<uint32_t>(),
+                            b->offsets.as<uint32_t>(), K, stream));
+    ctx->launches += K > 0 ? 1 : 0;
+    GB_CUDA(cudaMemcpyAsync(ctx->pinned_total, b->offsets.as<uint32_t>() + K, sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, stream));
+    GB_CUDA(cudaStreamSynchronize(stream));
+    const int64_t P = *ctx->pinned_total;
+    b->P = P;
+    const int64_t Pc = P > 0 ? P : 1;
+    GB_CUDA(b->keys.ensure(sizeof(uint64_t) * Pc));
+    GB_CUDA(b->values.ensure(sizeof(int32_t) * Pc));
+    GB_CUDA(ctx->keys_tmp.ensure(sizeof(uint64_t) * Pc));
+    GB_CUDA(ctx->vals_tmp.ensure(sizeof(int32_t) * Pc));
+    GB_CUDA(ctx->sort_temp.ensure(gb::sort_temp_bytes(Pc)));
+    // K2b duplicate, K2c sort, K2d ranges
+    GB_CUDA(gb::launch_duplicate(K, b->tiles_x, b->offsets.as<uint32_t>(), b->rects.as<uint2>(),
+                                 b->depth.as<uint32_t>(), ctx->keys_tmp.as<uint64_t>(), ctx->vals_tmp.as<int32_t>(),
+                                 stream));
+    GB_CUDA(gb::launch_sort(ctx->sort_temp.p, ctx->sort_temp.cap, ctx->keys_tmp.as<uint64_t>(),
+                            b->keys.as<uint64_t>(), ctx->vals_tmp.as<int32_t>(), b->values.as<int32_t>(), P, n_tiles,
+                            stream));
+    GB_CUDA(gb::launch_ranges(P, b->keys.as<uint64_t>(), b->ranges.as<uint2>(), n_tiles, stream));
+    ctx->launches += (K > 0) + (P > 0 ? 2 : 0);
+    b->built = true;
+    return GB_OK;
+}
+
+gb_status gb_binning_info(const gb_binning* b, int32_t* tiles_x, int32_t* tiles_y, int64_t* total) {
+    if (!b || !b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    if (tiles_x) *tiles_x = b->tiles_x;
+    if (tiles_y) *tiles_y = b->tiles_y;
+    if (total) *total = b->P;
+    return GB_OK;
+}
+
+gb_status gb_binning_copy_to_host(gb_context* ctx, const gb_binning* b, int64_t* offsets, int32_t* values) {
+    if (!ctx || !b || !b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    if (gb_status st = set_device(ctx)) return st;
+    const int n_tiles = b->tiles_x * b->tiles_y;
+    std::string tmp(sizeof(uint2) * (size_t)n_tiles, '\0');
+    uint2* ranges = reinterpret_cast<uint2*>(&tmp[0]);
+    GB_CUDA(cudaMemcpyAsync(ranges, b->ranges.p, sizeof(uint2) * n_tiles, cudaMemcpyDeviceToHost, ctx->stream));
+    if (b->P > 0 && values)
+        GB_CUDA(cudaMemcpyAsync(values, b->values.p, sizeof(int32_t) * b->P, cudaMemcpyDeviceToHost, ctx->stream));
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    // ranges are contiguous and in tile order; empty tiles have start == end == 0
+    int64_t o = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+        offsets[t] = o;
+        if (ranges[t].y > ranges[t].x) {
+            if ((int64_t)ranges[t].x != o) return fail(GB_CUDA_ERROR, "binning ranges are not contiguous");
+            o = ranges[t].y;
+        }
+    }
+    offsets[n_tiles] = o;
+    if (o != b->P) return fail(GB_CUDA_ERROR, "binning ranges do not cover all pairs");
+    return GB_OK;
+}
+
+gb_status gb_render_forward(gb_context* ctx, const gb_splats* s, const gb_camera* cam, const gb_binning* b,
+                            gb_render_out* out) {
+    if (!ctx || !b || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = validate_camera(cam)) return st;
+    if (gb_status st = validate_splats(s, cam->mode)) return st;
+    if (!b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    if (b->width != cam->width || b->height != cam->height || b->mode != cam->mode)
+        return fail(GB_MISMATCH, "render_forward: binning built for different image size");
+    if (b->K != s->count || b->n != s->grid.n)
+        return fail(GB_MISMATCH, "render_forward: binning built for a different splat set");
+    if (out->width != cam->width || out->height != cam->height)
+        return fail(GB_MISMATCH, "render_forward: output buffers sized for a different image");
+    if (!out->color || !out->final_transmittance || !out->last_rank)
+        return fail(GB_INVALID_ARGUMENT, "render_forward: null output buffer");
+    if (gb_status st = set_device(ctx)) return st;
+    const gb::CamConst cc = make_cam_const(cam);
+    const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+    GB_CUDA(gb::launch_forward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
+                               b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
+                               s->grid_values, cc, rc, out->color, out->final_transmittance, out->last_rank,
+                               ctx->stream));
+    ctx->launches += 1;
+    out->splat_count = s->count;
+    out->grid_n = s->grid.n;
+    out->tile_size = b->cfg.tile_size;
+    return GB_OK;
+}
+
+gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camera* cam, const gb_binning* b,
+                             const gb_render_out* out, const float* image_grad, gb_grads* g) {
+    if (!ctx || !b || !out || !g) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = validate_camera(cam)) return st;
+    if (gb_status st = validate_splats(s, cam->mode)) return st;
+    if (!b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    // raster.hpp:280-287
+    if (out->splat_count != s->count || out->grid_n != s->grid.n || out->tile_size != b->cfg.tile_size)
+        return fail(GB_MISMATCH, "render_backward: output does not match forward inputs");
+    if (out->width != cam->width || out->height != cam->height || b->width != cam->width ||
+        b->height != cam->height || b->mode != cam->mode || b->K != s->count)
+        return fail(GB_MISMATCH, "render_backward: image size mismatch");
+    if (!image_grad) return fail(GB_MISMATCH, "render_backward: image_grad size mismatch");
+    if (s->count == 0) return GB_OK;
+    if (!g->position || !g->log_scale || !g->opacity_logit || !g->grid_values ||
+        (cam->mode == GB_MODE_ORTHO && !g->theta) || (cam->mode == GB_MODE_PINHOLE && !g->quat))
+        return fail(GB_INVALID_ARGUMENT, "render_backward: null gradient buffer");
+    if (gb_status st = set_device(ctx)) return st;
+    cudaStream_t stream = ctx->stream;
+    const int64_t K = s->count;
+    GB_CUDA(ctx->accum.ensure(sizeof(float) * gb::kAccumStride * K));
+    GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(float) * gb::kAccumStride * K, stream));
+    const gb::CamConst cc = make_cam_const(cam);
+    const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+    GB_CUDA(gb::launch_backward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
+                                b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
+                                s->grid_values, cc, rc, out->final_transmittance, out->last_rank, image_grad,
+                                ctx->accum.as<float>(), g->grid_values, stream));
+    gb::ProjParams pp = gb::make_proj_params(s, cam, &b->cfg, b->tiles_x, b->tiles_y);
+    GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
+    ctx->launches += 2;
+    return GB_OK;
+}
+
+gb_status gb_render(gb_context* ctx, const gb_splats* s, const gb_camera* cam, const gb_raster_config* cfg,
+                    gb_binning* scratch, gb_render_out* out) {
+    if (gb_status st = gb_build_binning(ctx, s, cam, cfg, scratch)) return st;
+    return gb_render_forward(ctx, s, cam, scratch, out);
+}
+
+gb_status gb_l1_loss(gb_context* ctx, const float* color, const float* target, int64_t n, float scale, float* grad,
+                     float* loss) {
+    if (!ctx || (n > 0 && (!color || !target || !grad))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(gb::launch_loss(0, color, target, n, scale, grad, loss, ctx->sm_count, ctx->stream));
+    ctx->launches += n > 0;
+    return GB_OK;
+}
+
+gb_status gb_mse_loss(gb_context* ctx, const float* color, const float* target, int64_t n, float scale, float* grad,
+                      float* loss) {
+    if (!ctx || (n > 0 && (!color || !target || !grad))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(gb::launch_loss(1, color, target, n, scale, grad, loss, ctx->sm_count, ctx->stream));
+    ctx->launches += n > 0;
+    return GB_OK;
+}
+
+gb_status gb_adam_step(gb_context* ctx, int32_t mode, int64_t count, int32_t n, gb_grads* params, const gb_grads* g,
+                       gb_adam_state* state, const gb_learning_rates* lrs) {
+    if (!ctx || !params || !g || !state || !lrs) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (mode != GB_MODE_ORTHO && mode != GB_MODE_PINHOLE) return fail(GB_INVALID_ARGUMENT, "bad mode");
+    // optim.hpp:33-39
+    if (!(lrs->position > 0.0 && lrs->theta > 0.0 && lrs->log_scale > 0.0 && lrs->opacity_logit > 0.0 &&
+          lrs->color_grid > 0.0))
+        return fail(GB_INVALID_ARGUMENT, "LearningRates: all rates must be positive");
+    if (!(lrs->position_gamma > 0.0 && lrs->position_gamma <= 1.0))
+        return fail(GB_INVALID_ARGUMENT, "LearningRates: position_gamma must be in (0, 1]");
+    if (count < 0 || n < 1) return fail(GB_INVALID_ARGUMENT, "adam_step: gradient shape mismatch");
+    if (gb_status st = set_device(ctx)) return st;
+    cudaStream_t stream = ctx->stream;
+    GB_CUDA(ctx->adam_bad.ensure(sizeof(unsigned long long)));
+    GB_CUDA(cudaMemsetAsync(ctx->adam_bad.p, 0xff, sizeof(unsigned long long), stream));
+    state->t += 1;
+    const double bias1 = 1.0 - std::pow(state->beta1, (double)state->t);
+    const double bias2 = 1.0 - std::pow(state->beta2, (double)state->t);
+    const double pos_lr = lrs->position * std::pow(lrs->position_gamma, (double)(state->t - 1));
+    struct Group {
+        float *p, *g, *m, *v;
+        int64_t len;
+        double lr;
+    };
+    const bool ortho = mode == GB_MODE_ORTHO;
+    const int64_t tex = count * (int64_t)n * n * 3;
+    Group groups[5] = {
+        {params->position, g->position, state->m.position, state->v.position, count * (ortho ? 2 : 3), pos_lr},
+        {ortho ? params->theta : params->quat, ortho ? g->theta : g->quat, ortho ? state->m.theta : state->m.quat,
+         ortho ? state->v.theta : state->v.quat, count * (ortho ? 1 : 4), lrs->theta},
+        {params->log_scale, g->log_scale, state->m.log_scale, state->v.log_scale, count * 2, lrs->log_scale},
+        {params->opacity_logit, g->opacity_logit, state->m.opacity_logit, state->v.opacity_logit, count,
+         lrs->opacity_logit},
+        {params->grid_values, g->grid_values, state->m.grid_values, state->v.grid_values, tex, lrs->color_grid}};
+    auto* bad = ctx->adam_bad.as<unsigned long long>();
+    for (int i = 0; i < 5; ++i) {
+        if (groups[i].len == 0) continue;
+        if (!groups[i].p || !groups[i].g || !groups[i].m || !groups[i].v)
+            return fail(GB_INVALID_ARGUMENT, "adam_step: null buffer in group %d", i);
+        GB_CUDA(gb::launch_adam_check(groups[i].g, groups[i].len, i, bad, ctx->sm_count, stream));
+        ctx->launches++;
+    }
+    for (int i = 0; i < 5; ++i) {
+        if (groups[i].len == 0) continue;
+        GB_CUDA(gb::launch_adam_update(groups[i].p, groups[i].g, groups[i].m, groups[i].v, groups[i].len,
+                                       (float)groups[i].lr, (float)state->beta1, (float)state->beta2,
+                                       (float)state->epsilon, (float)(1.0 / bias1), (float)(1.0 / bias2), bad,
+                                       ctx->sm_count, stream));
+        ctx->launches++;
+    }
+    return GB_OK;
+}
+
+gb_status gb_adam_check(gb_context* ctx, int32_t* group, int64_t* index) {
+    if (!ctx) return fail(GB_INVALID_ARGUMENT, "ctx is null");
+    if (!ctx->adam_bad.p) return GB_OK;
+    if (gb_status st = set_device(ctx)) return st;
+    unsigned long long v = 0;
+    GB_CUDA(cudaMemcpyAsync(&v, ctx->adam_bad.p, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream));
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (v == ~0ull) return GB_OK;
+    static const char* names[5] = {"position", "theta", "log_scale", "opacity_logit", "color_grid"};
+    const int grp = (int)(v >> 48);
+    const int64_t idx = (int64_t)(v & ((1ull << 48) - 1));
+    if (group) *group = grp;
+    if (index) *index = idx;
+    return fail(GB_NONFINITE, "adam_step: non-finite gradient in group '%s' at index %lld", names[grp & 7],
+                (long long)idx);
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// gb_internal.cuh -- shared device-side definitions for the sm_100a kernels.
+//
+// Data layout in HBM (all fp32 unless noted):
+//   params   : the caller's SplatSet SoA (gb_splats)                       40 B + 12n^2 B / primitive
+//   headers  : ScreenHeader[K], 48 B, written by K1 for binned primitives
+//   rects    : uint2[K] packed tile rectangle (tx0|ty0<<16, tx1|ty1<<16)
+//   counts   : uint32[K] tiles per primitive, scanned in place to offsets
+//   keys     : uint64[P] (tile << 32 | orderable fp32 depth bits), sorted
+//   values   : int32[P] primitive index per (tile, primitive) pair, sorted
+//   ranges   : uint2[tiles] [start, end) into values per tile
+//   accum    : float[K*12] per-primitive screen-space gradient sums (K4 -> K5)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gb_raster.h"
+
+namespace gb {
+
+constexpr int kAccumStride = 12;  // floats per primitive in the K4 -> K5 accumulator
+constexpr float kMaxAlphaF = 0.999f;
+
+// Per-primitive screen header (48 B, three float4).
+//   ortho  : h0 = (x, y, cos t, sin t)   h1 = (1/s_u, 1/s_v, alpha_k, 0)   h2 = 0
+//   pinhole: the ray-splat intersection as a linear-fractional map of the
+//            pixel offset (dx, dy) from the projected centre:
+//              (u, v, 1) ~ (X.x dx + Y.x dy,  X.y dx + Y.y dy,  1 + X.z dx + Y.z dy)
+//            with X = Cx/(E_z fx), Y = Cy/(E_z fy) precomputed in fp64 (K1):
+//            h0 = (X.x, X.y, X.z, Y.x)  h1 = (Y.y, Y.z, alpha_k, hx)
+//            h2 = (hy, int cxi, int cyi, 0); dx = (x - cxi) + hx, dy = (y - cyi) + hy.
+struct __align__(16) ScreenHeader {
+    float4 h0, h1, h2;
+};
+
+// Per-launch camera constants for the fp32 compositor.
+struct CamConst {
+    int width, height;
+    float inv_fx, inv_fy;
+    float bg[3];
+};
+
+// Raster constants shared by K3/K4.
+struct RasterConst {
+    int tile_size;
+    int tiles_x, tiles_y;
+    float alpha_skip;      // <= 0 disables
+    float early_stop;      // <= 0 disables
+    float tex_scale;       // (n-1)/(2 sigma)
+    float tex_offset;      // (n-1)/2
+    float sigma;
+};
+
+// Thread -> pixel mapping inside a tile.  For tile sizes that are multiples
+// of 8 with ts*ts a multiple of 32, each warp covers an 8x4 pixel block
+// (better texel/activity coherence); otherwise row-major.
+__device__ __forceinline__ void tile_pixel(int tid, int ts, int& lx, int& ly) {
+    if ((ts & 7) == 0) {
+        const int warp = tid >> 5, lane = tid & 31;
+        const int wx = ts >> 3;  // warps per row of 8-wide blocks
+        lx = (warp % wx) * 8 + (lane & 7);
+        ly = (warp / wx) * 4 + (lane >> 3);
+    } else {
+        lx = tid % ts;
+        ly = tid / ts;
+    }
+}
+
+// ---- the per-(pixel, entry) evaluation shared bit-for-bit by K3 and K4 ------
+// Explicit _rn intrinsics pin the rounding sequence so forward and backward
+// make identical alpha-skip decisions (the reference needs
+// -ffp-contract=off for the same reason, CMakeLists.txt:12-15).
+
+struct PinholeTerms {  // kept for the backward chain
+    float dx, dy, cz;
+};
+
+// raster.hpp:36-42 (ortho) -- returns true (always a hit).
+__device__ __forceinline__ bool eval_uv_ortho(const ScreenHeader& h, int x, int y, float& u, float& v) {
+    const float dx = __fsub_rn(__fadd_rn((float)x, 0.5f), h.h0.x);
+    const float dy = __fsub_rn(__fadd_rn((float)y, 0.5f), h.h0.y);
+    const float c = h.h0.z, s = h.h0.w;
+    u = __fmul_rn(__fmaf_rn(c, dx, __fmul_rn(s, dy)), h.h1.x);
+    v = __fmul_rn(__fmaf_rn(-s, dx, __fmul_rn(c, dy)), h.h1.y);
+    return true;
+}
+
+// Pinhole 2DGS ray-splat intersection in the centred
+// linear-fractional form above.  A miss (ray parallel to the plane, or the
+// plane hit behind the camera: c_z <= 0 after the K1 normalisation) is skipped.
+__device__ __forceinline__ bool eval_uv_pinhole(const ScreenHeader& h, int x, int y, float& u, float& v,
+                                                PinholeTerms& p) {
+    const int cxi = __float_as_int(h.h2.y), cyi = __float_as_int(h.h2.z);
+    p.dx = __fadd_rn((float)(x - cxi), h.h1.w);
+    p.dy = __fadd_rn((float)(y - cyi), h.h2.x);
+    const float cx = __fmaf_rn(p.dx, h.h0.x, __fmul_rn(p.dy, h.h0.w));
+    const float cy = __fmaf_rn(p.dx, h.h0.y, __fmul_rn(p.dy, h.h1.x));
+    p.cz = __fmaf_rn(p.dx, h.h0.z, __fmaf_rn(p.dy, h.h1.y, 1.0f));
+    const float iz = __frcp_rn(p.cz);
+    u = __fmul_rn(cx, iz);
+    v = __fmul_rn(cy, iz);
+    return p.cz > 0.0f;
+}
+
+// G = exp(-(u^2+v^2)/2)  (raster.hpp:52)
+__device__ __forceinline__ float gauss_weight(float u, float v) {
+    return __expf(__fmul_rn(-0.5f, __fmaf_rn(u, u, __fmul_rn(v, v))));
+}
+
+// uv -> (i, f) on one axis, texture.hpp:27-37, with N fixed at compile time.
+template <int N>
+__device__ __forceinline__ void grid_coord(float u, const RasterConst& rc, int& i, float& f) {
+    float s = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
+    s = fminf(fmaxf(s, 0.0f), (float)(N - 1));
+    i = min((int)floorf(s), N - 2);
+    f = __fsub_rn(s, (float)i);
+}
+
+// K1/K5 parameters (fp64 camera and config), passed by value.
+struct ProjParams {
+    int mode;
+    int n;
+    int64_t K;
+    const float* position;
+    const float* depth_key;
+    const float* theta;
+    const float* quat;
+    const float* log_scale;
+    const float* opacity;
+    int W, H;
+    double fx, fy, cx, cy;
+    double R[9];
+    double t[3];
+    double near_plane;
+    int ts, tiles_x, tiles_y;
+    double cutoff, alpha_skip;
+};
+
+ProjParams make_proj_params(const gb_splats* s, const gb_camera* cam, const gb_raster_config* cfg, int tiles_x,
+                            int tiles_y);
+cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, uint2* rects, uint32_t* counts,
+                           uint32_t* depth_bits, cudaStream_t st);
+cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
+                         cudaStream_t st);
+
+__device__ __forceinline__ uint32_t float_order_key(float d) {
+    uint32_t b = __float_as_uint(d == 0.0f ? 0.0f : d);  // -0 sorts as +0 (double compare)
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+}  // namespace gb

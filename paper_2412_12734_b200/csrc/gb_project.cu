@@ -1,0 +1,384 @@
+// gb_project.cu -- K1 (per-primitive projection + cull + tile rectangle) and
+// K5 (per-primitive gradient chain to the raw parameters).
+//
+// Both run in fp64 and this translation unit is compiled with -fmad=false so
+// the binning decisions (opacity cull, 3-sigma box, pixel-centre coverage,
+// raster.hpp:61-101) replay the fp64 operation sequence of the reference
+// (ortho) and of the oracle's pinhole extension exactly; that is what makes
+// the tile lists bit-exact.  Only CUDA's exp/sin/cos may differ
+// from glibc by an ulp, which moves a box edge by ~1e-16 relative.
+//
+// HBM traffic: K1 reads 40 B of parameters and writes 48 B header + 8 B rect
+// + 4 B count + 4 B depth key per binned primitive; K5 reads the parameters
+// and the 48 B accumulator and read-modify-writes 40 B of gradients.
+#include <math.h>
+
+#include "gb_internal.cuh"
+
+namespace gb {
+
+
+
+struct Geom {
+    bool valid;
+    double alpha_k, s_u, s_v;
+    bool su_clamped, sv_clamped;
+    double cos_t, sin_t;  // ortho
+    double qn[4], qnorm;  // pinhole
+    double tuc[3], tvc[3];
+    double M[9];
+    double depth;
+};
+
+__device__ __forceinline__ double dmax_(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double dmin_(double a, double b) { return (b < a) ? b : a; }
+
+// core.hpp:95-100 + raster.hpp:157-175 (ortho); SURVEY Appendix C (pinhole).
+// Operation order mirrors oracle/gb_oracle.c build_geom().
+__device__ void build_geom(const ProjParams& p, int64_t k, Geom& g) {
+    g.valid = false;
+    g.alpha_k = 1.0 / (1.0 + exp(-(double)p.opacity[k]));
+    const double eu = exp((double)p.log_scale[2 * k + 0]);
+    const double ev = exp((double)p.log_scale[2 * k + 1]);
+    g.s_u = dmax_(eu, 1e-8);
+    g.s_v = dmax_(ev, 1e-8);
+    g.su_clamped = eu < 1e-8;
+    g.sv_clamped = ev < 1e-8;
+    if (p.mode == GB_MODE_ORTHO) {
+        g.valid = true;
+        const double th = (double)p.theta[k];
+        g.cos_t = cos(th);
+        g.sin_t = sin(th);
+        g.depth = (double)p.depth_key[k];
+        return;
+    }
+    const double q0 = p.quat[4 * k + 0], q1 = p.quat[4 * k + 1], q2 = p.quat[4 * k + 2], q3 = p.quat[4 * k + 3];
+    const double nn = q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3;
+    g.qnorm = sqrt(nn);
+    if (!(g.qnorm > 0.0)) return;
+    g.qn[0] = q0 / g.qnorm;
+    g.qn[1] = q1 / g.qnorm;
+    g.qn[2] = q2 / g.qnorm;
+    g.qn[3] = q3 / g.qnorm;
+    const double w = g.qn[0], x = g.qn[1], y = g.qn[2], z = g.qn[3];
+    double tu[3], tv[3];
+    tu[0] = 1.0 - 2.0 * (y * y + z * z);
+    tu[1] = 2.0 * (x * y + w * z);
+    tu[2] = 2.0 * (x * z - w * y);
+    tv[0] = 2.0 * (x * y - w * z);
+    tv[1] = 1.0 - 2.0 * (x * x + z * z);
+    tv[2] = 2.0 * (y * z + w * x);
+    const double m0 = p.position[3 * k + 0], m1 = p.position[3 * k + 1], m2 = p.position[3 * k + 2];
+    double pc[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        pc[r] = p.R[3 * r + 0] * m0 + p.R[3 * r + 1] * m1 + p.R[3 * r + 2] * m2 + p.t[r];
+        g.tuc[r] = p.R[3 * r + 0] * tu[0] + p.R[3 * r + 1] * tu[1] + p.R[3 * r + 2] * tu[2];
+        g.tvc[r] = p.R[3 * r + 0] * tv[0] + p.R[3 * r + 1] * tv[1] + p.R[3 * r + 2] * tv[2];
+        g.M[3 * r + 0] = g.s_u * g.tuc[r];
+        g.M[3 * r + 1] = g.s_v * g.tvc[r];
+        g.M[3 * r + 2] = pc[r];
+    }
+    g.depth = (double)(float)pc[2];
+    g.valid = pc[2] > p.near_plane;
+}
+
+// raster.hpp:61-86 + 93-101 (and the pinhole dual-conic box).  Writes the
+// inclusive pixel range; returns false when culled.
+__device__ bool cull_rect(const ProjParams& p, int64_t k, const Geom& g, int& x0, int& x1, int& y0, int& y1) {
+    if (p.alpha_skip > 0.0 && 1.0 / (1.0 + exp(-(double)p.opacity[k])) < p.alpha_skip) return false;
+    double min_x, max_x, min_y, max_y;
+    if (p.cutoff > 0.0) {
+        if (p.mode == GB_MODE_ORTHO) {
+            const double th = (double)p.theta[k];
+            const double suc = g.s_u * cos(th);
+            const double sus = g.s_u * sin(th);
+            const double svc = g.s_v * cos(th);
+            const double svs = g.s_v * sin(th);
+            const double hx = p.cutoff * sqrt(suc * suc + svs * svs);
+            const double hy = p.cutoff * sqrt(sus * sus + svc * svc);
+            const double x = (double)p.position[2 * k];
+            const double y = (double)p.position[2 * k + 1];
+            min_x = x - hx;
+            max_x = x + hx;
+            min_y = y - hy;
+            max_y = y + hy;
+        } else {
+            if (!g.valid) return false;
+            const double r = p.cutoff;
+            const double* M = g.M;
+            const double lat = sqrt(M[6] * M[6] + M[7] * M[7]);
+            if (!(M[8] - r * lat > p.near_plane)) return false;
+            double H0[3], H1[3], H2[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                H0[j] = p.fx * M[j] + p.cx * M[6 + j];
+                H1[j] = p.fy * M[3 + j] + p.cy * M[6 + j];
+                H2[j] = M[6 + j];
+            }
+            const double r2 = r * r;
+            const double C00 = r2 * (H0[0] * H0[0] + H0[1] * H0[1]) - H0[2] * H0[2];
+            const double C02 = r2 * (H0[0] * H2[0] + H0[1] * H2[1]) - H0[2] * H2[2];
+            const double C11 = r2 * (H1[0] * H1[0] + H1[1] * H1[1]) - H1[2] * H1[2];
+            const double C12 = r2 * (H1[0] * H2[0] + H1[1] * H2[1]) - H1[2] * H2[2];
+            const double C22 = r2 * (H2[0] * H2[0] + H2[1] * H2[1]) - H2[2] * H2[2];
+            const double dx = C02 * C02 - C00 * C22;
+            const double dy = C12 * C12 - C11 * C22;
+            if (!(dx >= 0.0) || !(dy >= 0.0)) return false;
+            const double sx = sqrt(dx), sy = sqrt(dy);
+            const double xa = (C02 - sx) / C22, xb = (C02 + sx) / C22;
+            const double ya = (C12 - sy) / C22, yb = (C12 + sy) / C22;
+            min_x = dmin_(xa, xb);
+            max_x = dmax_(xa, xb);
+            min_y = dmin_(ya, yb);
+            max_y = dmax_(ya, yb);
+        }
+    } else {
+        if (!g.valid) return false;
+        min_x = 0.0;
+        max_x = (double)p.W;
+        min_y = 0.0;
+        max_y = (double)p.H;
+    }
+    min_x = dmax_(min_x, 0.0);
+    min_y = dmax_(min_y, 0.0);
+    max_x = dmin_(max_x, (double)p.W);
+    max_y = dmin_(max_y, (double)p.H);
+    if (!(min_x < max_x) || !(min_y < max_y)) return false;
+    x0 = max(0, (int)ceil(min_x - 0.5));
+    y0 = max(0, (int)ceil(min_y - 0.5));
+    x1 = min(p.W - 1, (int)floor(max_x - 0.5));
+    y1 = min(p.H - 1, (int)floor(max_y - 0.5));
+    if (x0 > x1 || y0 > y1) return false;
+    return true;
+}
+
+// Effective projected centre used by the fp32 compositor (see ScreenHeader).
+__device__ __forceinline__ void pinhole_centre(const ProjParams& p, const Geom& g, int& cxi, int& cyi, float& hx,
+                                               float& hy, double& dxe, double& dye) {
+    const double pz = g.M[8];
+    const double cxp = p.fx * (g.M[2] / pz) + p.cx;
+    const double cyp = p.fy * (g.M[5] / pz) + p.cy;
+    const double fxi = floor(cxp), fyi = floor(cyp);
+    cxi = (int)fxi;
+    cyi = (int)fyi;
+    hx = (float)(0.5 - (cxp - fxi));
+    hy = (float)(0.5 - (cyp - fyi));
+    const double c0x = fxi + 0.5 - (double)hx;
+    const double c0y = fyi + 0.5 - (double)hy;
+    dxe = (c0x - p.cx) / p.fx;
+    dye = (c0y - p.cy) / p.fy;
+}
+
+// c = a x b with a = M0 - dxn M2, b = M1 - dyn M2 is exactly linear in the
+// normalised pixel offset: c = C0 + dxn Cx + dyn Cy, C0 = M0 x M1,
+// Cx = M1 x M2, Cy = M2 x M0 (the dxn*dyn term is M2 x M2 = 0).  Centred at
+// the compositor's centre (dxe, dye): E = C0 + dxe Cx + dye Cy.
+struct PinholeCoeffs {
+    double C0[3], Cx[3], Cy[3], E[3];
+};
+
+__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+__device__ __forceinline__ void pinhole_coeffs(const Geom& g, double dxe, double dye, PinholeCoeffs& pc) {
+    const double* M0 = g.M;
+    const double* M1 = g.M + 3;
+    const double* M2 = g.M + 6;
+    cross3(M0, M1, pc.C0);
+    cross3(M1, M2, pc.Cx);
+    cross3(M2, M0, pc.Cy);
+    for (int j = 0; j < 3; ++j) pc.E[j] = pc.C0[j] + dxe * pc.Cx[j] + dye * pc.Cy[j];
+}
+
+// K1: one thread per primitive.
+__global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeader* __restrict__ hdr,
+                                                 uint2* __restrict__ rects, uint32_t* __restrict__ counts,
+                                                 uint32_t* __restrict__ depth_bits) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p.K) return;
+    Geom g;
+    build_geom(p, k, g);
+    int x0, x1, y0, y1;
+    if (!cull_rect(p, k, g, x0, x1, y0, y1)) {
+        counts[k] = 0;
+        return;
+    }
+    const int tx0 = x0 / p.ts, tx1 = x1 / p.ts, ty0 = y0 / p.ts, ty1 = y1 / p.ts;
+    counts[k] = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    rects[k] = make_uint2((uint32_t)tx0 | ((uint32_t)ty0 << 16), (uint32_t)tx1 | ((uint32_t)ty1 << 16));
+    depth_bits[k] = float_order_key((float)g.depth);
+    ScreenHeader h;
+    if (p.mode == GB_MODE_ORTHO) {
+        h.h0 = make_float4(p.position[2 * k], p.position[2 * k + 1], (float)g.cos_t, (float)g.sin_t);
+        h.h1 = make_float4((float)(1.0 / g.s_u), (float)(1.0 / g.s_v), (float)g.alpha_k, 0.0f);
+        h.h2 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    } else {
+        int cxi, cyi;
+        float hx, hy;
+        double dxe, dye;
+        pinhole_centre(p, g, cxi, cyi, hx, hy, dxe, dye);
+        PinholeCoeffs pc;
+        pinhole_coeffs(g, dxe, dye, pc);
+        const double sx = 1.0 / (pc.E[2] * p.fx), sy = 1.0 / (pc.E[2] * p.fy);
+        const bool ok = pc.E[2] != 0.0 && isfinite(sx) && isfinite(sy);
+        const float nan = __int_as_float(0x7fc00000);
+        // X = Cx/(E_z fx), Y = Cy/(E_z fy); a degenerate plane (through the camera centre) misses everywhere
+        h.h0 = ok ? make_float4((float)(pc.Cx[0] * sx), (float)(pc.Cx[1] * sx), (float)(pc.Cx[2] * sx),
+                                (float)(pc.Cy[0] * sy))
+                  : make_float4(0.f, 0.f, nan, 0.f);
+        h.h1 = ok ? make_float4((float)(pc.Cy[1] * sy), (float)(pc.Cy[2] * sy), (float)g.alpha_k, hx)
+                  : make_float4(0.f, nan, (float)g.alpha_k, hx);
+        h.h2 = make_float4(hy, __int_as_float(cxi), __int_as_float(cyi), 0.0f);
+    }
+    hdr[k] = h;
+}
+
+// K5: chain the K4 screen-space sums to the raw parameters and ADD into the
+// gradient buffer.  Ortho: raster.hpp:350-360 with the per-eval products
+// (u_hat*u, ...) summed by K4.  Pinhole: dL/dM from (S_A, S_B, S_D) then the
+// camera/quaternion chain (oracle pinhole_chain()).
+__global__ void __launch_bounds__(256) k_chain(const ProjParams p, const uint32_t* __restrict__ counts,
+                                               const float* __restrict__ accum, gb_grads g_out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p.K) return;
+    if (counts[k] == 0) return;
+    const float4* a4 = reinterpret_cast<const float4*>(accum + k * kAccumStride);
+    const float4 A = a4[0], B = a4[1], C = a4[2];
+    Geom g;
+    build_geom(p, k, g);
+    if (p.mode == GB_MODE_ORTHO) {
+        const double su = A.x, sv = A.y, suv = A.z, svu = A.w, suu = B.x, svv = B.y, sop = B.z;
+        const double inv_su = 1.0 / g.s_u, inv_sv = 1.0 / g.s_v;
+        g_out.position[2 * k + 0] += (float)(su * (-g.cos_t * inv_su) + sv * (g.sin_t * inv_sv));
+        g_out.position[2 * k + 1] += (float)(su * (-g.sin_t * inv_su) + sv * (-g.cos_t * inv_sv));
+        g_out.theta[k] += (float)(suv * (g.s_v * inv_su) - svu * (g.s_u * inv_sv));
+        if (!g.su_clamped) g_out.log_scale[2 * k + 0] += (float)(-suu);
+        if (!g.sv_clamped) g_out.log_scale[2 * k + 1] += (float)(-svv);
+        g_out.opacity_logit[k] += (float)(sop * (g.alpha_k * (1.0 - g.alpha_k)));
+        return;
+    }
+    if (!g.valid) return;
+    int cxi, cyi;
+    float hx, hy;
+    double dxe, dye;
+    pinhole_centre(p, g, cxi, cyi, hx, hy, dxe, dye);
+    // K4 sums over pixels of gc' = dL/dc' (c' = c / E_z):  S_E = sum gc', S_X = sum dx gc', S_Y = sum dy gc'
+    PinholeCoeffs pc;
+    pinhole_coeffs(g, dxe, dye, pc);
+    if (!(pc.E[2] != 0.0)) return;
+    const double iez = 1.0 / pc.E[2];
+    const double SE[3] = {A.x, A.y, A.z}, SX[3] = {A.w, B.x, B.y}, SY[3] = {B.z, B.w, C.x};
+    const double sop = C.y;
+    double gC0[3], gCx[3], gCy[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const double gE = SE[j] * iez;  // dL/dc = dL/dc' / E_z (u, v are scale invariant)
+        gC0[j] = gE;
+        gCx[j] = SX[j] * iez / p.fx + dxe * gE;
+        gCy[j] = SY[j] * iez / p.fy + dye * gE;
+    }
+    // C0 = M0 x M1, Cx = M1 x M2, Cy = M2 x M0  ->  dL/dM (rows)
+    const double* M0 = g.M;
+    const double* M1 = g.M + 3;
+    const double* M2 = g.M + 6;
+    double t0[3], t1[3], dM[9];
+    cross3(M1, gC0, t0);
+    cross3(gCy, M2, t1);
+    for (int j = 0; j < 3; ++j) dM[j] = t0[j] + t1[j];
+    cross3(gC0, M0, t0);
+    cross3(M2, gCx, t1);
+    for (int j = 0; j < 3; ++j) dM[3 + j] = t0[j] + t1[j];
+    cross3(gCx, M1, t0);
+    cross3(M0, gCy, t1);
+    for (int j = 0; j < 3; ++j) dM[6 + j] = t0[j] + t1[j];
+    double g_col0[3], g_col1[3], g_pc[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        g_col0[r] = dM[3 * r + 0];
+        g_col1[r] = dM[3 * r + 1];
+        g_pc[r] = dM[3 * r + 2];
+    }
+    double g_su = 0.0, g_sv = 0.0, g_tu[3], g_tv[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        g_su += g_col0[r] * g.tuc[r];
+        g_sv += g_col1[r] * g.tvc[r];
+    }
+    const double* R = p.R;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        g_out.position[3 * k + j] += (float)(R[0 + j] * g_pc[0] + R[3 + j] * g_pc[1] + R[6 + j] * g_pc[2]);
+        g_tu[j] = g.s_u * (R[0 + j] * g_col0[0] + R[3 + j] * g_col0[1] + R[6 + j] * g_col0[2]);
+        g_tv[j] = g.s_v * (R[0 + j] * g_col1[0] + R[3 + j] * g_col1[1] + R[6 + j] * g_col1[2]);
+    }
+    if (!g.su_clamped) g_out.log_scale[2 * k + 0] += (float)(g_su * g.s_u);
+    if (!g.sv_clamped) g_out.log_scale[2 * k + 1] += (float)(g_sv * g.s_v);
+    const double w = g.qn[0], x = g.qn[1], y = g.qn[2], z = g.qn[3];
+    double gq[4];
+    gq[0] = g_tu[1] * 2 * z - g_tu[2] * 2 * y - g_tv[0] * 2 * z + g_tv[2] * 2 * x;
+    gq[1] = g_tu[1] * 2 * y + g_tu[2] * 2 * z + g_tv[0] * 2 * y - g_tv[1] * 4 * x + g_tv[2] * 2 * w;
+    gq[2] = -g_tu[0] * 4 * y + g_tu[1] * 2 * x - g_tu[2] * 2 * w + g_tv[0] * 2 * x + g_tv[2] * 2 * z;
+    gq[3] = -g_tu[0] * 4 * z + g_tu[1] * 2 * w + g_tu[2] * 2 * x - g_tv[0] * 2 * w - g_tv[1] * 4 * z + g_tv[2] * 2 * y;
+    const double dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) g_out.quat[4 * k + i] += (float)((gq[i] - g.qn[i] * dot) / g.qnorm);
+    g_out.opacity_logit[k] += (float)(sop * (g.alpha_k * (1.0 - g.alpha_k)));
+}
+
+}  // namespace gb
+
+// ---- host launchers (called from gb_capi.cu) -------------------------------
+namespace gb {
+
+ProjParams make_proj_params(const gb_splats* s, const gb_camera* cam, const gb_raster_config* cfg, int tiles_x,
+                            int tiles_y) {
+    ProjParams p;
+    p.mode = cam->mode;
+    p.n = s->grid.n;
+    p.K = s->count;
+    p.position = s->position;
+    p.depth_key = s->depth_key;
+    p.theta = s->theta;
+    p.quat = s->quat;
+    p.log_scale = s->log_scale;
+    p.opacity = s->opacity_logit;
+    p.W = cam->width;
+    p.H = cam->height;
+    p.fx = cam->fx;
+    p.fy = cam->fy;
+    p.cx = cam->cx;
+    p.cy = cam->cy;
+    for (int i = 0; i < 9; ++i) p.R[i] = cam->rot[i];
+    for (int i = 0; i < 3; ++i) p.t[i] = cam->trans[i];
+    p.near_plane = cam->near_plane;
+    p.ts = cfg->tile_size;
+    p.tiles_x = tiles_x;
+    p.tiles_y = tiles_y;
+    p.cutoff = cfg->cutoff_radius;
+    p.alpha_skip = cfg->alpha_skip;
+    return p;
+}
+
+cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, uint2* rects, uint32_t* counts,
+                           uint32_t* depth_bits, cudaStream_t st) {
+    if (p.K == 0) return cudaSuccess;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((p.K + threads - 1) / threads);
+    k_project<<<blocks, threads, 0, st>>>(p, hdr, rects, counts, depth_bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
+                         cudaStream_t st) {
+    if (p.K == 0) return cudaSuccess;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((p.K + threads - 1) / threads);
+    k_chain<<<blocks, threads, 0, st>>>(p, counts, accum, g);
+    return cudaGetLastError();
+}
+
+}  // namespace gb

@@ -1,0 +1,506 @@
+"""Reference-shaped host API over the C-ABI (include/gb_raster.h).
+
+Mirrors the reference's rasterizer interface (/root/reference/proj/include/gbil)
+name for name -- ``ColorGridConfig``, ``SplatSet``, ``ImagePlaneCamera``,
+``RasterConfig``, ``TileBinning``, ``RenderOutput``, ``GradientBuffer``,
+``build_binning``, ``render_forward``, ``render_backward``, ``render``,
+``adam_step`` -- with fp32 CUDA tensors in place of ``std::vector<double>``.
+Errors follow the reference's throw sites: ``std::invalid_argument`` becomes
+:class:`InvalidArgument` / :class:`Mismatch` (both ``ValueError``), adam's
+non-finite ``std::runtime_error`` becomes :class:`NonFinite`.
+
+Every compute call goes through ``libgb_raster.so``; PyTorch only provides
+device memory and the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import GBError, InvalidArgument, Mismatch, NonFinite, check, lib
+
+MODE_ORTHO = _lib.MODE_ORTHO
+MODE_PINHOLE = _lib.MODE_PINHOLE
+K_MAX_ALPHA = 0.999  # core.hpp:16
+K_MIN_SCALE = 1e-8  # core.hpp:19
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    if t.dtype not in (torch.float32, torch.int32):
+        raise TypeError(f"expected fp32/int32 tensor, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+# --------------------------------------------------------------------------------------------
+# context
+# --------------------------------------------------------------------------------------------
+class _Context:
+    _by_device: dict = {}
+
+    def __init__(self, device: int):
+        h = C.c_void_p()
+        check(lib.gb_context_create(device, C.byref(h)), "gb_context_create")
+        self.handle = h
+        self.device = device
+
+    @classmethod
+    def get(cls, device: torch.device) -> "_Context":
+        if device.type != "cuda":
+            raise ValueError(f"tensors must live on a CUDA device (got {device}); there is no CPU path")
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        ctx = cls._by_device.get(idx)
+        if ctx is None:
+            ctx = cls(idx)
+            cls._by_device[idx] = ctx
+        with torch.cuda.device(idx):
+            stream = torch.cuda.current_stream(idx).cuda_stream
+        check(lib.gb_context_set_stream(ctx.handle, C.c_void_p(stream)), "gb_context_set_stream")
+        return ctx
+
+    def launches(self) -> int:
+        return int(lib.gb_context_launch_count(self.handle))
+
+
+def context(device=None) -> _Context:
+    return _Context.get(torch.device(device) if device is not None else torch.device("cuda"))
+
+
+# --------------------------------------------------------------------------------------------
+# configs and cameras
+# --------------------------------------------------------------------------------------------
+@dataclass
+class ColorGridConfig:
+    """core.hpp:29-42"""
+
+    n: int = 1
+    sigma: float = 0.5
+    channels: int = 3
+
+    def texels_per_splat(self) -> int:
+        return self.n * self.n * 3
+
+    def validate(self) -> None:
+        if self.n < 1:
+            raise ValueError("ColorGridConfig: n must be >= 1")
+        if not self.sigma > 0.0:
+            raise ValueError("ColorGridConfig: sigma must be > 0")
+
+
+@dataclass
+class RasterConfig:
+    """raster.hpp:21-32"""
+
+    tile_size: int = 16
+    cutoff_radius: float = 3.0
+    alpha_skip: float = 1.0 / 255.0
+    early_stop_transmittance: float = 1e-4
+    threads: int = 1
+
+    def to_c(self) -> _lib.RasterConfigC:
+        return _lib.RasterConfigC(self.tile_size, self.threads, self.cutoff_radius, self.alpha_skip,
+                                  self.early_stop_transmittance)
+
+
+@dataclass
+class ImagePlaneCamera:
+    """Orthographic fitting camera (core.hpp:104-116): pixel (i,j) samples (i+0.5, j+0.5)."""
+
+    width: int = 0
+    height: int = 0
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+    mode: int = field(default=MODE_ORTHO, init=False)
+
+    def to_c(self) -> _lib.Camera:
+        c = _lib.Camera()
+        c.mode = MODE_ORTHO
+        c.width, c.height = self.width, self.height
+        for i in range(3):
+            c.background[i] = float(self.background[i])
+        c.fx = c.fy = 1.0
+        return c
+
+
+@dataclass
+class PinholeCamera:
+    """Perspective 2DGS camera (builder extension).
+
+    OpenCV convention: x right, y down, +z forward; x_pix = fx*X/Z + cx with
+    pixel centres at i + 0.5; ``rot``/``trans`` map world -> camera.
+    """
+
+    width: int
+    height: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    rot: np.ndarray
+    trans: np.ndarray
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+    near_plane: float = 0.01
+    mode: int = field(default=MODE_PINHOLE, init=False)
+
+    @staticmethod
+    def look_at(eye, target, width, height, fx, fy, cx, cy, up=(0.0, 1.0, 0.0), background=(0.0, 0.0, 0.0),
+                near_plane=0.01) -> "PinholeCamera":
+        """z_cam = normalize(target - eye), x_cam = normalize(up x z_cam), y_cam = z_cam x x_cam.
+
+        With eye=(0,0,-d) looking at the origin this gives rot = I, trans = (0,0,d).
+        """
+        eye = np.asarray(eye, dtype=np.float64)
+        f = np.asarray(target, dtype=np.float64) - eye
+        f /= np.linalg.norm(f)
+        r = np.cross(np.asarray(up, dtype=np.float64), f)
+        r /= np.linalg.norm(r)
+        d = np.cross(f, r)
+        rot = np.stack([r, d, f])
+        trans = -rot @ eye
+        return PinholeCamera(width, height, fx, fy, cx, cy, rot, trans, background, near_plane)
+
+    @staticmethod
+    def from_spec(spec) -> "PinholeCamera":
+        """From a scenes.CameraSpec."""
+        return PinholeCamera(spec.width, spec.height, spec.fx, spec.fy, spec.cx, spec.cy, spec.rot, spec.trans,
+                             tuple(spec.background), spec.near_plane)
+
+    def to_c(self) -> _lib.Camera:
+        c = _lib.Camera()
+        c.mode = MODE_PINHOLE
+        c.width, c.height = self.width, self.height
+        for i in range(3):
+            c.background[i] = float(self.background[i])
+        c.fx, c.fy, c.cx, c.cy = self.fx, self.fy, self.cx, self.cy
+        rot = np.asarray(self.rot, dtype=np.float64).reshape(9)
+        for i in range(9):
+            c.rot[i] = float(rot[i])
+        tr = np.asarray(self.trans, dtype=np.float64).reshape(3)
+        for i in range(3):
+            c.trans[i] = float(tr[i])
+        c.near_plane = self.near_plane
+        return c
+
+
+# --------------------------------------------------------------------------------------------
+# splats and gradients
+# --------------------------------------------------------------------------------------------
+_FIELDS = ("position", "depth_key", "theta", "quat", "log_scale", "opacity_logit", "grid")
+
+
+class SplatSet:
+    """K primitives, structure of arrays, fp32 on one CUDA device (core.hpp:53-87).
+
+    ortho : position (K,2), depth_key (K,), theta (K,)
+    pinhole: position (K,3) world mean, quat (K,4) (w,x,y,z)
+    both  : log_scale (K,2), opacity_logit (K,), grid (K, n*n*3) in (i_u, i_v, ch) order
+    """
+
+    def __init__(self, mode: int, grid_config: ColorGridConfig, **arrays):
+        grid_config.validate()
+        self.mode = mode
+        self.grid_config = grid_config
+        for f in _FIELDS:
+            setattr(self, f, arrays.get(f))
+        self.count = int(self.opacity_logit.shape[0])
+
+    @staticmethod
+    def from_numpy(mode: int, grid_config: ColorGridConfig, device="cuda", **arrays) -> "SplatSet":
+        t = {k: torch.as_tensor(np.ascontiguousarray(v, dtype=np.float32), device=device) for k, v in arrays.items()
+             if v is not None}
+        return SplatSet(mode, grid_config, **t)
+
+    @property
+    def device(self) -> torch.device:
+        return self.opacity_logit.device
+
+    def tensors(self) -> dict:
+        return {f: getattr(self, f) for f in _FIELDS if getattr(self, f) is not None}
+
+    def to_c(self) -> _lib.Splats:
+        s = _lib.Splats()
+        s.count = self.count
+        s.grid = _lib.GridConfig(self.grid_config.n, 0, self.grid_config.sigma)
+        s.position = _ptr(self.position)
+        s.depth_key = _ptr(self.depth_key)
+        s.theta = _ptr(self.theta)
+        s.quat = _ptr(self.quat)
+        s.log_scale = _ptr(self.log_scale)
+        s.opacity_logit = _ptr(self.opacity_logit)
+        s.grid_values = _ptr(self.grid)
+        return s
+
+
+class GradientBuffer:
+    """Gradients w.r.t. the raw parameters, mirroring SplatSet (core.hpp:140-178).
+
+    All groups live in one flat fp32 tensor (``flat``) so the multi-GPU step can
+    all-reduce them with a single collective; the per-group tensors are views.
+    """
+
+    def __init__(self, like: SplatSet):
+        self.mode = like.mode
+        self.count = like.count
+        self.grid_config = like.grid_config
+        shapes = [(f, tuple(getattr(like, f).shape)) for f in _FIELDS if getattr(like, f) is not None]
+        # keep every group 16-byte aligned (vector red.global.add on the texel grads)
+        pad = lambda n: (n + 3) & ~3
+        total = sum(pad(int(np.prod(s))) for _, s in shapes)
+        self.flat = torch.zeros(total, dtype=torch.float32, device=like.device)
+        o = 0
+        for f in _FIELDS:
+            setattr(self, f, None)
+        for f, s in shapes:
+            n = int(np.prod(s))
+            setattr(self, f, self.flat[o:o + n].view(s))
+            o += pad(n)
+
+    def zero_(self) -> "GradientBuffer":
+        self.flat.zero_()
+        return self
+
+    def tensors(self) -> dict:
+        return {f: getattr(self, f) for f in _FIELDS if getattr(self, f) is not None}
+
+    def to_c(self) -> _lib.Grads:
+        g = _lib.Grads()
+        g.position = _ptr(self.position)
+        g.depth_key = _ptr(self.depth_key)
+        g.theta = _ptr(self.theta)
+        g.quat = _ptr(self.quat)
+        g.log_scale = _ptr(self.log_scale)
+        g.opacity_logit = _ptr(self.opacity_logit)
+        g.grid_values = _ptr(self.grid)
+        return g
+
+
+# --------------------------------------------------------------------------------------------
+# binning / render
+# --------------------------------------------------------------------------------------------
+class TileBinning:
+    """Device-resident per-tile sorted lists (raster.hpp:105-114)."""
+
+    def __init__(self, device=None):
+        self.ctx = context(device)
+        h = C.c_void_p()
+        check(lib.gb_binning_create(self.ctx.handle, C.byref(h)), "gb_binning_create")
+        self.handle = h
+        self.config: Optional[RasterConfig] = None
+        self.width = self.height = 0
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            lib.gb_binning_destroy(h)
+            self.handle = None
+
+    def info(self):
+        tx, ty, total = C.c_int32(), C.c_int32(), C.c_int64()
+        check(lib.gb_binning_info(self.handle, C.byref(tx), C.byref(ty), C.byref(total)), "gb_binning_info")
+        return tx.value, ty.value, total.value
+
+    @property
+    def tiles_x(self) -> int:
+        return self.info()[0]
+
+    @property
+    def tiles_y(self) -> int:
+        return self.info()[1]
+
+    def tile_count(self) -> int:
+        tx, ty, _ = self.info()
+        return tx * ty
+
+    @property
+    def total(self) -> int:
+        return self.info()[2]
+
+    def csr(self):
+        """(offsets[tiles+1] int64, values[total] int32) on the host."""
+        tx, ty, total = self.info()
+        offsets = np.zeros(tx * ty + 1, dtype=np.int64)
+        values = np.zeros(max(total, 1), dtype=np.int32)
+        check(lib.gb_binning_copy_to_host(self.ctx.handle, self.handle, offsets.ctypes.data, values.ctypes.data),
+              "gb_binning_copy_to_host")
+        return offsets, values[:total]
+
+    @property
+    def tiles(self):
+        offsets, values = self.csr()
+        return [values[offsets[i]:offsets[i + 1]] for i in range(len(offsets) - 1)]
+
+
+def build_binning(splats: SplatSet, camera, config: RasterConfig = None, out: TileBinning = None) -> TileBinning:
+    """raster.hpp:116-147"""
+    config = config or RasterConfig()
+    b = out if out is not None else TileBinning(splats.device)
+    ctx = context(splats.device)
+    s, cam, cfg = splats.to_c(), camera.to_c(), config.to_c()
+    check(lib.gb_build_binning(ctx.handle, C.byref(s), C.byref(cam), C.byref(cfg), b.handle), "build_binning")
+    b.config = config
+    b.width, b.height = camera.width, camera.height
+    return b
+
+
+class RenderOutput:
+    """core.hpp:123-136 -- color (H,W,3), final_transmittance (H,W), last_rank (H,W)."""
+
+    def __init__(self, width: int, height: int, device):
+        self.width, self.height = width, height
+        self.color = torch.empty((height, width, 3), dtype=torch.float32, device=device)
+        self.final_transmittance = torch.empty((height, width), dtype=torch.float32, device=device)
+        self.last_rank = torch.empty((height, width), dtype=torch.int32, device=device)
+        self._c = _lib.RenderOut(width, height, self.color.data_ptr(), self.final_transmittance.data_ptr(),
+                                 self.last_rank.data_ptr(), 0, 0, 0)
+
+    @property
+    def splat_count(self):
+        return self._c.splat_count
+
+    @property
+    def grid_n(self):
+        return self._c.grid_n
+
+    @property
+    def tile_size(self):
+        return self._c.tile_size
+
+    @property
+    def alpha(self) -> torch.Tensor:
+        """Accumulated alpha 1 - T (the BASELINE configs' second output)."""
+        return 1.0 - self.final_transmittance
+
+
+def render_forward(splats: SplatSet, camera, binning: TileBinning, out: RenderOutput = None) -> RenderOutput:
+    """raster.hpp:201-261"""
+    ctx = context(splats.device)
+    out = out if out is not None else RenderOutput(camera.width, camera.height, splats.device)
+    s, cam = splats.to_c(), camera.to_c()
+    check(lib.gb_render_forward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(out._c)),
+          "render_forward")
+    return out
+
+
+def render_backward(splats: SplatSet, camera, binning: TileBinning, output: RenderOutput,
+                    image_grad: torch.Tensor, grads: GradientBuffer = None) -> GradientBuffer:
+    """raster.hpp:277-387.  Accumulates into ``grads`` (a fresh zeroed buffer by default)."""
+    ctx = context(splats.device)
+    if grads is None:
+        grads = GradientBuffer(splats)
+    if image_grad.numel() != output.color.numel():
+        raise ValueError("render_backward: image_grad size mismatch")
+    image_grad = image_grad.contiguous()
+    s, cam, g = splats.to_c(), camera.to_c(), grads.to_c()
+    check(lib.gb_render_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(output._c),
+                                 _ptr(image_grad), C.byref(g)), "render_backward")
+    return grads
+
+
+def render(splats: SplatSet, camera, config: RasterConfig = None) -> RenderOutput:
+    """raster.hpp:389-392"""
+    b = build_binning(splats, camera, config)
+    return render_forward(splats, camera, b)
+
+
+# --------------------------------------------------------------------------------------------
+# losses and Adam
+# --------------------------------------------------------------------------------------------
+def l1_loss(color: torch.Tensor, target: torch.Tensor, scale: float = None, grad: torch.Tensor = None,
+            loss: torch.Tensor = None):
+    """L1 photometric loss: returns (loss (device scalar), dL/dC).  scale defaults to 1/numel (mean)."""
+    if color.shape != target.shape:
+        raise ValueError("l1_loss: dimension mismatch")
+    ctx = context(color.device)
+    n = color.numel()
+    scale = 1.0 / n if scale is None else scale
+    grad = torch.empty_like(color) if grad is None else grad
+    if loss is None:
+        loss = torch.zeros((), dtype=torch.float32, device=color.device)
+    check(lib.gb_l1_loss(ctx.handle, _ptr(color.contiguous()), _ptr(target.contiguous()), n, scale, _ptr(grad),
+                         _ptr(loss)), "l1_loss")
+    return loss, grad
+
+
+def mse_loss(color: torch.Tensor, target: torch.Tensor, scale: float = None, grad: torch.Tensor = None,
+             loss: torch.Tensor = None):
+    """train.hpp:120-133: mean squared error, gradient 2(c - t)/n."""
+    if color.shape != target.shape:
+        raise ValueError("mse_loss: dimension mismatch")
+    ctx = context(color.device)
+    n = color.numel()
+    scale = 1.0 / n if scale is None else scale
+    grad = torch.empty_like(color) if grad is None else grad
+    if loss is None:
+        loss = torch.zeros((), dtype=torch.float32, device=color.device)
+    check(lib.gb_mse_loss(ctx.handle, _ptr(color.contiguous()), _ptr(target.contiguous()), n, scale, _ptr(grad),
+                          _ptr(loss)), "mse_loss")
+    return loss, grad
+
+
+@dataclass
+class LearningRates:
+    """optim.hpp:17-40 (pinhole quaternions use the ``theta`` rate)."""
+
+    position: float = 1.6e-4
+    theta: float = 1e-3
+    log_scale: float = 5e-3
+    opacity_logit: float = 5e-2
+    color_grid: float = 2.5e-3
+    position_gamma: float = 1.0
+
+    @staticmethod
+    def scaled_for_image(width: int, height: int) -> "LearningRates":
+        lrs = LearningRates()
+        lrs.position *= max(width, height)
+        return lrs
+
+    def to_c(self):
+        return _lib.LearningRatesC(self.position, self.theta, self.log_scale, self.opacity_logit, self.color_grid,
+                                   self.position_gamma)
+
+
+@dataclass
+class AdamConfig:
+    """optim.hpp:42-46"""
+
+    beta1: float = 0.9
+    beta2: float = 0.999
+    epsilon: float = 1e-8
+
+
+class AdamState:
+    """optim.hpp:50-72: zero moments with the gradient layout, t counts completed steps."""
+
+    def __init__(self, like: SplatSet, config: AdamConfig = None):
+        self.config = config or AdamConfig()
+        self.t = 0
+        self.m = GradientBuffer(like)
+        self.v = GradientBuffer(like)
+
+
+def adam_step(params: SplatSet, grads: GradientBuffer, state: AdamState, lrs: LearningRates,
+              check_finite: bool = True) -> None:
+    """optim.hpp:96-117.  With check_finite, synchronises and raises NonFinite like the reference."""
+    if grads.count != params.count or grads.grid.numel() != params.grid.numel():
+        raise ValueError("adam_step: gradient shape mismatch")
+    ctx = context(params.device)
+    p = _lib.Grads(_ptr(params.position), _ptr(params.depth_key), _ptr(params.theta), _ptr(params.quat),
+                   _ptr(params.log_scale), _ptr(params.opacity_logit), _ptr(params.grid))
+    g = grads.to_c()
+    st = _lib.AdamStateC(state.t, state.config.beta1, state.config.beta2, state.config.epsilon, state.m.to_c(),
+                         state.v.to_c())
+    c_lrs = lrs.to_c()
+    check(lib.gb_adam_step(ctx.handle, params.mode, params.count, params.grid_config.n, C.byref(p), C.byref(g),
+                           C.byref(st), C.byref(c_lrs)), "adam_step")
+    state.t = st.t
+    if check_finite:
+        grp, idx = C.c_int32(), C.c_int64()
+        check(lib.gb_adam_check(ctx.handle, C.byref(grp), C.byref(idx)), "adam_step")

@@ -1,0 +1,137 @@
+"""Regenerate the golden fixtures from the COMPILED REFERENCE (oracle/_ref/libgbil_ref.so).
+
+Run in the build container, where /root/reference exists:
+    make -C oracle && python tests/golden/make_golden.py
+
+Writes (small, committed):
+  ortho_cases.npz -- seeded ortho scenes (fp32 inputs) with the reference's
+                     build_binning CSR, render_forward outputs and
+                     render_backward gradients for a fixed +-1 image_grad
+  naive_fd.npz    -- reference render_naive + gradient_fd on a tiny scene
+  rng.npz         -- reference Rng uniform()/normal() streams
+  kat.json        -- SPEC known-answer examples evaluated by the reference
+The fixtures travel to the GPU box; nothing there reads /root/reference.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle as O  # noqa: E402
+import paper_2412_12734_b200.scenes as sc  # noqa: E402
+
+# (name, K, n, W, H, seed, scale_lo, scale_hi, tile, cutoff, skip, early_stop, background)
+CASES = [
+    ("n1", 150, 1, 64, 48, 101, 0.7, 6.0, 16, 3.0, 1 / 255, 1e-4, (0.0, 0.0, 0.0)),
+    ("n2", 150, 2, 64, 48, 102, 0.7, 6.0, 16, 3.0, 1 / 255, 1e-4, (0.2, 0.4, 0.6)),
+    ("n3", 120, 3, 50, 37, 103, 0.7, 6.0, 16, 3.0, 1 / 255, 1e-4, (0.1, 0.1, 0.1)),
+    ("n4", 150, 4, 64, 48, 104, 0.7, 6.0, 16, 3.0, 1 / 255, 1e-4, (1.0, 1.0, 1.0)),
+    ("n8", 150, 8, 64, 48, 105, 0.7, 6.0, 16, 3.0, 1 / 255, 1e-4, (0.0, 0.5, 0.0)),
+    ("n4_tile5", 120, 4, 41, 29, 106, 0.7, 5.0, 5, 3.0, 1 / 255, 1e-4, (0.3, 0.3, 0.3)),
+    ("n4_nothresh", 60, 4, 32, 24, 107, 1.0, 5.0, 16, 0.0, 0.0, 0.0, (0.5, 0.2, 0.9)),
+    ("n2_dense", 400, 2, 48, 32, 108, 1.0, 10.0, 8, 3.0, 1 / 255, 1e-4, (0.0, 0.0, 0.0)),
+]
+
+
+def ortho_cases():
+    out = {}
+    for name, K, n, W, H, seed, lo, hi, ts, cut, skip, es, bg in CASES:
+        arr = sc.generate(O.MODE_ORTHO, K, n, seed, width=W, height=H, scale_lo=lo, scale_hi=hi)
+        scene = O.Scene64(arr, n)
+        cam = O.Cam(O.MODE_ORTHO, W, H, bg)
+        cfg = O.Cfg(tile_size=ts, cutoff_radius=cut, alpha_skip=skip, early_stop=es, threads=3)
+        ig = np.random.default_rng(seed).choice(np.array([-1.0, 0.0, 1.0]), size=(H, W, 3))
+        r = O.ref_render(scene, cam, cfg, ig)
+        meta = dict(K=K, n=n, W=W, H=H, tile=ts, cutoff=cut, skip=skip, early_stop=es, bg=list(bg))
+        out[f"{name}/meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+        for k in ("position", "depth_key", "theta", "log_scale", "opacity_logit", "grid"):
+            out[f"{name}/in_{k}"] = arr[k]
+        out[f"{name}/image_grad"] = ig.astype(np.int8)
+        for k in ("offsets", "values", "color", "trans", "last"):
+            out[f"{name}/{k}"] = r[k]
+        for k, v in r["grads"].items():
+            out[f"{name}/g_{k}"] = v
+    np.savez_compressed(os.path.join(HERE, "ortho_cases.npz"), **out)
+
+
+def naive_fd():
+    arr = sc.generate(O.MODE_ORTHO, 5, 2, 7, width=16, height=16, scale_lo=1.5, scale_hi=4.0)
+    scene = O.Scene64(arr, 2)
+    cam = O.Cam(O.MODE_ORTHO, 16, 16, (0.1, 0.2, 0.3))
+    w = np.random.default_rng(7).standard_normal((16, 16, 3))
+    color, trans = O.ref_render_naive(scene, cam)
+    g = O.ref_gradient_fd(scene, cam, w, 1e-6)
+    out = {f"in_{k}": arr[k] for k in ("position", "depth_key", "theta", "log_scale", "opacity_logit", "grid")}
+    out.update(weights=w, color=color, trans=trans, **{f"g_{k}": v for k, v in g.items() if v is not None})
+    np.savez_compressed(os.path.join(HERE, "naive_fd.npz"), **out)
+
+
+def rng_streams():
+    L = O.ref_lib()
+    out = {}
+    for seed in (0, 1, 2, 12345, 2 ** 63 + 5):
+        u = np.zeros(1000)
+        L.ref_rng_uniform(seed, 1000, u.ctypes.data)
+        nrm = np.zeros(1001)
+        L.ref_rng_normal(seed, 1001, 0.0, 1.0, nrm.ctypes.data)
+        out[f"uniform_{seed}"] = u
+        out[f"normal_{seed}"] = nrm
+    np.savez_compressed(os.path.join(HERE, "rng.npz"), **out)
+
+
+def kat():
+    import ctypes as C
+
+    L = O.ref_lib()
+    res = {}
+
+    def uv(u, v, n, s):
+        iu, iv, fu, fv = C.c_int32(), C.c_int32(), C.c_double(), C.c_double()
+        L.ref_uv_to_grid(u, v, n, s, C.byref(iu), C.byref(iv), C.byref(fu), C.byref(fv))
+        return [iu.value, iv.value, fu.value, fv.value]
+
+    res["uv_to_grid"] = [[u, v, n, s, uv(u, v, n, s)] for (u, v, n, s) in
+                         [(-0.5, -0.5, 4, 0.5), (0.0, 0.0, 2, 0.5), (5.0, 0.0, 4, 0.5), (0.13, -0.31, 8, 0.5),
+                          (-7.0, 7.0, 8, 2.0), (0.25, 0.25, 1, 0.5)]]
+    grid2 = np.array([0, 0, 0, 0, 0, 1, 1, 0, 0, 1, 0, 1], np.float64)  # C[0,0],C[0,1],C[1,0],C[1,1]
+
+    def bil(u, v, n, s, g):
+        c = np.zeros(3)
+        L.ref_bilinear(u, v, n, s, g.ctypes.data, c.ctypes.data)
+        return c.tolist()
+
+    res["bilinear"] = [[u, v, bil(u, v, 2, 0.5, grid2)] for (u, v) in [(0.0, 0.0), (5.0, 0.0), (-0.2, 0.3)]]
+    rng = np.random.default_rng(3)
+    g8 = rng.random(8 * 8 * 3)
+    adj = []
+    for (u, v) in [(0.11, -0.23), (0.6, 0.1), (-0.49, 0.49), (0.0, 0.0)]:
+        ch = np.array([0.3, -0.7, 1.1])
+        gg = np.zeros_like(g8)
+        uh, vh = C.c_double(), C.c_double()
+        L.ref_adj_bilinear(u, v, 8, 0.5, g8.ctypes.data, ch.ctypes.data, gg.ctypes.data, C.byref(uh), C.byref(vh))
+        adj.append([u, v, ch.tolist(), gg.tolist(), uh.value, vh.value])
+    res["adj_bilinear_grid8"] = g8.tolist()
+    res["adj_bilinear"] = adj
+    p = np.array([1.0, -2.0, 0.5]); g = np.array([1.0, 1.0, -3.0]); m = np.zeros(3); v = np.zeros(3)
+    L.ref_adam_group(p.ctypes.data, g.ctypes.data, m.ctypes.data, v.ctypes.data, 3, 0.1, 0.9, 0.999, 1e-8,
+                     1 - 0.9, 1 - 0.999)
+    res["adam_first_step"] = dict(p0=[1.0, -2.0, 0.5], g=[1.0, 1.0, -3.0], lr=0.1, p1=p.tolist(), m=m.tolist(),
+                                  v=v.tolist())
+    with open(os.path.join(HERE, "kat.json"), "w") as fh:
+        json.dump(res, fh, indent=1)
+
+
+if __name__ == "__main__":
+    if not O.ref_available():
+        O.build()
+    ortho_cases()
+    naive_fd()
+    rng_streams()
+    kat()
+    for f in sorted(os.listdir(HERE)):
+        print(f, os.path.getsize(os.path.join(HERE, f)))

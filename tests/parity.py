@@ -1,0 +1,117 @@
+"""Shared parity helpers: run one scene through the CUDA path (C-ABI via the
+package) and through the fp64 oracle, and compare them with the protocol of
+SURVEY.md §8(c):
+
+* tile lists (offsets + values): bit-exact;
+* images: |d| <= atol + rtol*|ref| on RGB and alpha = 1 - T, exact last_rank,
+  except pixels the oracle flags as within fp32 error of a threshold kink;
+* gradients (same image_grad fed to both sides): |d| <= atol + rtol*|ref| +
+  slack, where slack is the oracle's |terms| from kink-adjacent evaluations.
+  A second, error-model check adds C*eps32*mag (mag = sum of |terms|), the
+  rounding-error scale of fp32 accumulation; both counts are reported.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from oracle import oracle as O  # noqa: E402
+
+RTOL = 1e-4  # north_star tolerance (fp32)
+ATOL = 1e-5
+EPS32 = 2.0 ** -24
+MODEL_C = 64.0  # error-model multiple of eps32*mag
+
+GRAD_FIELDS = ("position", "theta", "quat", "log_scale", "opacity_logit", "grid")
+
+
+def run_gpu(arrays: dict, mode: int, n: int, cam_spec, cfg: "O.Cfg", image_grad=None, sigma=0.5, device="cuda"):
+    """Binning + forward (+ backward with the given image_grad) through libgb_raster.so."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+
+    splats = gb.SplatSet.from_numpy(mode, gb.ColorGridConfig(n, sigma), device=device, **arrays)
+    if mode == O.MODE_ORTHO:
+        camera = gb.ImagePlaneCamera(cam_spec.width, cam_spec.height, tuple(cam_spec.background))
+    else:
+        camera = gb.PinholeCamera.from_spec(cam_spec)
+    rc = gb.RasterConfig(cfg.tile_size, cfg.cutoff_radius, cfg.alpha_skip, cfg.early_stop, 1)
+    binning = gb.build_binning(splats, camera, rc)
+    out = gb.render_forward(splats, camera, binning)
+    res = {}
+    res["offsets"], res["values"] = binning.csr()
+    grads = None
+    if image_grad is not None:
+        ig = torch.as_tensor(np.ascontiguousarray(image_grad, np.float32), device=device)
+        grads = gb.render_backward(splats, camera, binning, out, ig)
+    torch.cuda.synchronize()
+    res["color"] = out.color.cpu().numpy().astype(np.float64)
+    res["trans"] = out.final_transmittance.cpu().numpy().astype(np.float64)
+    res["last"] = out.last_rank.cpu().numpy()
+    if grads is not None:
+        res["grads"] = {k: v.cpu().numpy().astype(np.float64) for k, v in grads.tensors().items()}
+    return res
+
+
+def run_oracle(arrays: dict, n: int, cam: "O.Cam", cfg: "O.Cfg", image_grad=None, sigma=0.5):
+    scene = O.Scene64(arrays, n, sigma)
+    b = O.build_binning(scene, cam, cfg)
+    f = O.render_forward(scene, cam, cfg, b)
+    res = dict(offsets=b[0], values=b[1], color=f["color"], trans=f["trans"], last=f["last"], kink=f["kink"])
+    if image_grad is not None:
+        g, mag, slack = O.render_backward(scene, cam, cfg, b, f, np.asarray(image_grad, np.float64))
+        res.update(grads=g, mag=mag, slack=slack)
+    return res
+
+
+def compare_binning(gpu: dict, orc: dict) -> dict:
+    return dict(offsets_equal=bool(np.array_equal(gpu["offsets"], orc["offsets"])),
+                values_equal=bool(np.array_equal(gpu["values"], orc["values"])),
+                pairs=int(len(orc["values"])))
+
+
+def compare_image(gpu: dict, orc: dict, rtol=RTOL, atol=ATOL) -> dict:
+    ok_px = orc["kink"] == 0
+    dc = np.abs(gpu["color"] - orc["color"])
+    bad_c = (dc > atol + rtol * np.abs(orc["color"])).any(axis=-1)
+    a_g, a_o = 1.0 - gpu["trans"], 1.0 - orc["trans"]
+    bad_a = np.abs(a_g - a_o) > atol + rtol * np.abs(a_o)
+    bad_l = gpu["last"] != orc["last"]
+    return dict(pixels=int(ok_px.size), kink_pixels=int((~ok_px).sum()),
+                color_violations=int((bad_c & ok_px).sum()), alpha_violations=int((bad_a & ok_px).sum()),
+                last_rank_mismatch=int((bad_l & ok_px).sum()),
+                max_abs_color=float(dc[ok_px].max()) if ok_px.any() else 0.0)
+
+
+def compare_grads(gpu: dict, orc: dict, rtol=RTOL, atol=ATOL, model_c=MODEL_C) -> dict:
+    out = {}
+    for f in GRAD_FIELDS:
+        ref = orc["grads"].get(f)
+        if ref is None or f not in gpu["grads"]:
+            continue
+        got = gpu["grads"][f].reshape(ref.shape)
+        d = np.abs(got - ref)
+        slack = orc["slack"][f]
+        mag = orc["mag"][f]
+        strict = d > atol + rtol * np.abs(ref) + slack
+        model = d > atol + rtol * np.abs(ref) + slack + model_c * EPS32 * mag
+        scale = float(np.abs(ref).max()) if ref.size else 0.0
+        tol = atol + rtol * np.abs(ref) + slack
+        ratio = (d / tol).ravel()
+        worst = []
+        for i in np.argsort(ratio)[-3:][::-1]:
+            if ratio[i] > 1.0:
+                worst.append(dict(index=int(i), got=float(got.ravel()[i]), ref=float(ref.ravel()[i]),
+                                  slack=float(slack.ravel()[i]), mag=float(mag.ravel()[i]), ratio=float(ratio[i])))
+        out[f] = dict(entries=int(ref.size), strict_violations=int(strict.sum()), worst=worst,
+                      model_violations=int(model.sum()), kink_entries=int((slack > 0).sum()),
+                      max_abs_err=float(d.max()) if d.size else 0.0,
+                      max_rel_to_scale=float(d.max() / scale) if scale > 0 else 0.0)
+    return out

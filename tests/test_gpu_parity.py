@@ -1,0 +1,163 @@
+"""CUDA path vs the fp64 oracle (parity proper; needs a B200).
+
+Ortho scenes are pinned by the compiled reference (the oracle is bit-exact
+against it, tests/test_oracle_ref.py); pinhole scenes use the oracle's
+perspective extension.  Every case checks: bit-exact tile lists, image within
+rtol 1e-4 / atol 1e-5 (kink pixels excluded and counted), exact last_rank, and
+gradients from the same image_grad within rtol 1e-4 / atol 1e-5 + kink slack.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from parity import ATOL, RTOL, O, compare_binning, compare_grads, compare_image, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+OUT_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+# fraction of gradient entries allowed outside rtol/atol + kink slack (fp32 accumulation of
+# heavily cancelling sums); the error-model check (+64 eps32 * sum|terms|) must have none.
+STRICT_FRACTION = 2e-4
+
+
+def _record(name, stats):
+    os.makedirs(OUT_DIR, exist_ok=True)
+    with open(os.path.join(OUT_DIR, f"parity_{name}.json"), "w") as fh:
+        json.dump(stats, fh, indent=1)
+
+
+def _image_grad(seed, h, w):
+    # the oracle's sign(C - target) in sum reduction: +-1 per channel
+    rng = np.random.default_rng(seed)
+    return rng.choice(np.array([-1.0, 1.0]), size=(h, w, 3))
+
+
+def _check(name, arrays, mode, n, cam, cfg, backward=True, grad_seed=0):
+    ig = _image_grad(grad_seed, cam.height, cam.width) if backward else None
+    gpu = run_gpu(arrays, mode, n, cam, cfg, ig)
+    orc = run_oracle(arrays, n, cam, cfg, ig)
+    stats = dict(binning=compare_binning(gpu, orc), image=compare_image(gpu, orc))
+    if backward:
+        stats["grads"] = compare_grads(gpu, orc)
+    _record(name, stats)
+    print(name, json.dumps(stats))
+    assert stats["binning"]["offsets_equal"] and stats["binning"]["values_equal"], "tile lists must be bit-exact"
+    im = stats["image"]
+    assert im["color_violations"] == 0 and im["alpha_violations"] == 0, im
+    assert im["last_rank_mismatch"] == 0, im
+    if backward:
+        for f, st in stats["grads"].items():
+            assert st["model_violations"] == 0, (f, st)
+            assert st["strict_violations"] <= STRICT_FRACTION * st["entries"] + 1, (f, st)
+    return stats
+
+
+# ---------------------------------------------------------------------------------------------
+# ortho (the reference's own camera)
+# ---------------------------------------------------------------------------------------------
+def _ortho_scene(K, n, seed, W, H, lo=0.5, hi=8.0):
+    import paper_2412_12734_b200.scenes as sc
+
+    return sc.generate(O.MODE_ORTHO, K, n, seed, width=W, height=H, scale_lo=lo, scale_hi=hi)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8, 16])
+def test_ortho_random(n):
+    W, H = 320, 240
+    arrays = _ortho_scene(6000, n, 10 + n, W, H)
+    cam = O.Cam(O.MODE_ORTHO, W, H, (0.1, 0.3, 0.7))
+    _check(f"ortho_n{n}", arrays, O.MODE_ORTHO, n, cam, O.Cfg())
+
+
+@pytest.mark.parametrize("ts", [8, 5, 1])
+def test_ortho_tile_sizes(ts):
+    W, H = 101, 67  # ragged: not a multiple of any tile size
+    arrays = _ortho_scene(800, 4, 3, W, H)
+    cam = O.Cam(O.MODE_ORTHO, W, H, (0.0, 0.0, 0.0))
+    _check(f"ortho_ts{ts}", arrays, O.MODE_ORTHO, 4, cam, O.Cfg(tile_size=ts))
+
+
+def test_ortho_thresholds_disabled():
+    W, H = 64, 48
+    arrays = _ortho_scene(300, 4, 5, W, H, 1.0, 6.0)
+    cam = O.Cam(O.MODE_ORTHO, W, H, (0.5, 0.5, 0.5))
+    _check("ortho_nothresh", arrays, O.MODE_ORTHO, 4, cam,
+           O.Cfg(cutoff_radius=0.0, alpha_skip=0.0, early_stop=0.0))
+
+
+def test_ortho_empty_and_culled():
+    W, H = 40, 30
+    cam = O.Cam(O.MODE_ORTHO, W, H, (0.2, 0.4, 0.6))
+    empty = {k: (None if v is None else v[:0]) for k, v in _ortho_scene(1, 2, 0, W, H).items()}
+    st = _check("ortho_empty", empty, O.MODE_ORTHO, 2, cam, O.Cfg())
+    assert st["binning"]["pairs"] == 0
+    culled = _ortho_scene(50, 2, 1, W, H)
+    culled["opacity_logit"][:] = -10.0  # sigmoid(-10) < 1/255: opacity cull (SPEC cull example 3)
+    st = _check("ortho_culled", culled, O.MODE_ORTHO, 2, cam, O.Cfg())
+    assert st["binning"]["pairs"] == 0
+
+
+def test_ortho_single_splat_kat():
+    """SPEC render_forward example 2: centred splat, constant grid c, alpha 0.9 -> 0.9 c, T = 0.1."""
+    import paper_2412_12734_b200 as gb
+    import torch
+
+    W = H = 16
+    c = np.array([0.3, 0.6, 0.9], np.float32)
+    arrays = dict(position=np.array([[8.5, 8.5]], np.float32), depth_key=np.zeros(1, np.float32),
+                  theta=np.zeros(1, np.float32), log_scale=np.zeros((1, 2), np.float32),
+                  opacity_logit=np.array([np.log(0.9 / 0.1)], np.float32), grid=np.tile(c, 4)[None, :])
+    cam = O.Cam(O.MODE_ORTHO, W, H)
+    gpu = run_gpu(arrays, O.MODE_ORTHO, 2, cam, O.Cfg())
+    np.testing.assert_allclose(gpu["color"][8, 8], 0.9 * c, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(gpu["trans"][8, 8], 0.1, rtol=1e-5)
+    assert gpu["last"][8, 8] == 0
+
+
+# ---------------------------------------------------------------------------------------------
+# pinhole (BASELINE configs; perspective extension of the reference algorithm)
+# ---------------------------------------------------------------------------------------------
+def _config(idx, **kw):
+    import paper_2412_12734_b200.scenes as sc
+
+    return sc.baseline_config(idx, **kw)
+
+
+@pytest.mark.parametrize("n", [1, 4, 8, 16])
+def test_pinhole_small(n):
+    cfgs = _config(0, count=20_000, n=n)
+    cam_spec = cfgs.cameras[0]
+    cam = O.Cam.from_spec(cam_spec)
+    _check(f"pinhole_small_n{n}", cfgs.arrays(), O.MODE_PINHOLE, n, cam, O.Cfg())
+
+
+def test_configs0_forward_full():
+    """configs[0]: 100k surfels, 4x4 textures, 800x800 -- forward only."""
+    c = _config(0)
+    cam = O.Cam.from_spec(c.cameras[0])
+    _check("configs0_forward", c.arrays(), O.MODE_PINHOLE, c.n, cam, O.Cfg(), backward=False)
+
+
+def test_configs1_forward_backward_full():
+    """configs[1]: configs[0] scene, forward + backward with the same image_grad on both sides."""
+    c = _config(1)
+    cam = O.Cam.from_spec(c.cameras[0])
+    _check("configs1_fwd_bwd", c.arrays(), O.MODE_PINHOLE, c.n, cam, O.Cfg())
+
+
+def test_pinhole_ragged_and_offcentre():
+    import paper_2412_12734_b200.scenes as sc
+
+    spec = sc.look_at((1.5, -0.7, -3.2), (0.1, 0.0, 0.2), 333, 217, 400.0, 380.0, 170.3, 101.9)
+    arrays = sc.generate(O.MODE_PINHOLE, 5000, 4, 9, mean_lo=-1.2, mean_hi=1.2, scale_lo=0.01, scale_hi=0.2)
+    _check("pinhole_ragged", arrays, O.MODE_PINHOLE, 4, O.Cam.from_spec(spec), O.Cfg(tile_size=16))
+
+
+@pytest.mark.slow
+def test_configs2_full():
+    """configs[2]: 1M surfels, 8x8 textures, 1600x1064 (minutes of oracle CPU time)."""
+    c = _config(2)
+    cam = O.Cam.from_spec(c.cameras[0])
+    _check("configs2_fwd_bwd", c.arrays(), O.MODE_PINHOLE, c.n, cam, O.Cfg())
