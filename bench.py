@@ -1,0 +1,376 @@
+"""Benchmark of the Gaussian Billboards hot path on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[3], weak scaling): 1,000,000 textured surfels
+with 8x8 RGB fp32 textures, 64 Fibonacci-sphere cameras (radius 6) at
+1600x1064; every GPU renders and backpropagates its own 8 views per step (L1
+loss against seeded-noise targets), gradients are summed by one NCCL
+all-reduce (N > 1) and Adam updates the replicated primitives.  One "step" is
+that whole training step; value = megapixels/s over all GPUs.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference algorithm's CPU implementation on the
+host cores (rank 0 only): the compiled reference has no perspective camera
+(SPEC.md:279), so the workload runs through the fp64 C restatement
+(oracle/gb_oracle.c, bit-exact with the reference on its own ortho path),
+one full view per step with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "fwd+bwd ms/view and megapixels/sec at 1/2/4/8 B200; % HBM roofline"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--views-per-gpu", type=int, default=8)
+    ap.add_argument("--count", type=int, default=1_000_000)
+    ap.add_argument("--n", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, p[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU legs (oracle = test infrastructure; only the cpu_baseline and --impl reference legs use it)
+# ---------------------------------------------------------------------------------------------
+def cpu_view(scene64, cam, target, step_frac_adam=0.125):
+    """One view of the workload on the host: binning + forward + L1 + backward (+ 1/8 of Adam)."""
+    from oracle import oracle as O
+
+    cfg = O.Cfg()
+    b = O.build_binning(scene64, cam, cfg)
+    f = O.render_forward(scene64, cam, cfg, b, kink=None)
+    _, ig = O.l1_loss(f["color"], target, 1.0 / f["color"].size)
+    g, _, _ = O.render_backward(scene64, cam, cfg, b, f, ig.reshape(f["color"].shape), kink=None, want_mag=False)
+    # the step's Adam over the replicated parameters, amortised over its 8 views
+    flat = np.concatenate([v.ravel() for v in g.values() if v is not None])
+    m = int(flat.size * step_frac_adam)
+    O.adam_group(np.zeros(m), flat[:m], np.zeros(m), np.zeros(m), 1e-3, 0.9, 0.999, 1e-8, 0.1, 0.001)
+    return len(b[1])
+
+
+def cpu_setup(args, cfg3):
+    from oracle import oracle as O
+
+    arrays = cfg3.arrays()
+    scene64 = O.Scene64(arrays, cfg3.n)
+    return O, scene64
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import paper_2412_12734_b200.scenes as sc
+
+    cfg3 = sc.baseline_config(3, count=args.count, n=args.n)
+    O, scene64 = cpu_setup(args, cfg3)
+    cores = os.cpu_count() or 1
+    times = []
+    views = list(range(len(cfg3.cameras)))
+    for it in range(args.warmup + args.steps):
+        v = views[it % len(views)]
+        cam = O.Cam.from_spec(cfg3.cameras[v])
+        tgt = cfg3.target(v)
+        t0 = time.perf_counter()
+        cpu_view(scene64, cam, tgt)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    W, H = cfg3.cameras[0].width, cfg3.cameras[0].height
+    step_s = sum(times) / len(times)
+    mps = W * H / 1e6 / step_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(mps, 4), "unit": "MP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
+        "ms_per_view": round(step_s * 1e3, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[3] shapes)",
+        "config": {"workload": "configs[3] view: 1M surfels, 8x8 fp32 textures, 1600x1064, fwd+bwd+L1 (+1/8 Adam)",
+                   "views_per_step": 1},
+        "cpu_baseline": {"value": round(mps, 4), "unit": "MP/s", "cores": cores, "kind": "port",
+                         "sample": "one full configs[3] view per step (binning + forward + L1 + backward + 1/8 "
+                                   "Adam), fp64 C restatement of the reference algorithm (oracle/gb_oracle.c), "
+                                   f"{cores} threads; the compiled reference has no perspective path"},
+        "e2e": {"value": round(mps, 4), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+        local = 0
+    device = torch.device("cuda", local)
+
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+    from paper_2412_12734_b200.train import ViewShardedTrainer, shard_views
+
+    cfg3 = sc.baseline_config(3, count=args.count, n=args.n)
+    arrays = cfg3.arrays()
+    splats = gb.SplatSet.from_numpy(cfg3.mode, gb.ColorGridConfig(cfg3.n), device=device, **arrays)
+    cams = [gb.PinholeCamera.from_spec(c) for c in cfg3.cameras]
+    views = shard_views(len(cams), rank, world, per_rank=args.views_per_gpu)
+    lrs = gb.LearningRates()
+    lrs.position *= 6.0  # position LR x scene extent
+    trainer = ViewShardedTrainer(splats, cams, views, lrs=lrs)
+    W, H = cams[0].width, cams[0].height
+    host_targets = [torch.from_numpy(cfg3.target(v)).pin_memory() for v in views]
+    dev_targets = [t.to(device) for t in host_targets]
+    ctx = gb.raster.context(device)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (untimed) ----
+    for _ in range(args.warmup):
+        trainer.step(dev_targets)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region: inputs resident in HBM (working set >> 126 MB L2) ----
+    stream = torch.cuda.current_stream(device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trainer.pairs.clear()
+    launches0 = ctx.launches()
+    ctx.profile(True)
+    ctx.profile_read()  # reset
+    with ClockSampler(torch.cuda.current_device() if world == 1 else local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            trainer.step(dev_targets)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ctx.profile(False)
+    prof = ctx.profile_read()
+    launches = ctx.launches() - launches0
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    step_ms = elapsed_ms / args.steps
+    views_total = world * len(views)
+    mpix = views_total * W * H / 1e6
+    value = mpix / (step_ms / 1e3)
+    pairs = list(trainer.pairs)
+
+    # ---- end to end: pinned host targets in, per-view losses out, every step ----
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            trainer.step_host(host_targets)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev2.record(stream)
+        for _ in range(args.steps):
+            trainer.step_host(host_targets)
+        ev3.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e2e_ms = max_over_ranks(max(ev2.elapsed_time(ev3), wall * 1e3)) / args.steps
+        h2d = sum(t.numel() * 4 for t in host_targets)
+        e2e = {"value": round(mpix / (e2e_ms / 1e3), 3), "unit": "MP/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": len(views) * 4, "ms_per_step": round(e2e_ms, 3)}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (algorithmic bytes, SURVEY §8d with this build's 48 B header) ----
+    peak, peak_src = hbm_peak()
+    n = cfg3.n
+    Bh, Bt = 48, 12 * n * n
+    tiles = ((W + 15) // 16) * ((H + 15) // 16)
+    npx = W * H
+    model = {
+        "backward": lambda P: P * (4 + 2 * Bh + 2 * Bt) + 8 * tiles + 20 * npx,
+        "forward": lambda P: P * (4 + Bh + Bt) + 8 * tiles + 20 * npx,
+    }
+    dom = max(("forward", "backward"), key=lambda k: prof[k][0])
+    total_ms, count = prof[dom]
+    bytes_per_launch = sum(model[dom](P) for P in pairs) / max(1, len(pairs))
+    avg_ms = total_ms / max(1, count)
+    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
+    traffic = None
+    ncu_sum = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(ncu_sum):
+        try:
+            traffic = json.load(open(ncu_sum)).get(dom, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items() if v[1]}
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "MP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 3),
+        "ms_per_view": round(step_ms / len(views), 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded Rng, BASELINE configs[3] shapes; random-init surfels, noise targets)",
+        "config": {"workload": "configs[3] view-sharded training step: 1M surfels, 8x8 fp32 RGB textures, "
+                               f"{args.views_per_gpu} Fibonacci-sphere views/GPU at 1600x1064, L1, "
+                               "NCCL all-reduce + Adam",
+                   "views_per_gpu": len(views), "surfels": cfg3.count, "texture": f"{n}x{n}",
+                   "image": f"{W}x{H}", "tile": 16, "mean_pairs_per_view": int(np.mean(pairs)) if pairs else 0,
+                   "l2": "working set (0.8 GB textures + 0.8 GB grads + 1.6 GB Adam) >> 126 MB L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": int(bytes_per_launch), "avg_launch_ms": round(avg_ms, 4),
+                     "peak_source": peak_src},
+        "kernel_ms_per_step": kernel_ms,
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            O, scene64 = cpu_setup(args, cfg3)
+            cam0 = O.Cam.from_spec(cfg3.cameras[views[0]])
+            t0 = time.perf_counter()
+            cpu_view(scene64, cam0, cfg3.target(views[0]))
+            dt = time.perf_counter() - t0
+            cores = os.cpu_count() or 1
+            line["cpu_baseline"] = {
+                "value": round(W * H / 1e6 / dt, 4), "unit": "MP/s", "cores": cores, "kind": "port",
+                "sample": f"1 view of the workload (binning+forward+L1+backward+1/8 Adam) in {dt:.1f} s, fp64 C "
+                          f"restatement of the reference algorithm (oracle/gb_oracle.c), {cores} threads"}
+        except Exception as e:  # the baseline never blocks the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "MP/s", "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"failed: {e}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -150,6 +150,23 @@ GB_API gb_status gb_sync(gb_context *ctx);
 /* Number of kernels this context has launched (for the bench's gpu_launches claim). */
 GB_API int64_t gb_context_launch_count(const gb_context *ctx);
 
+/* Per-kernel CUDA-event timing on the context's stream (bench roofline).  While
+ * enabled, every launch site is bracketed by two events; _read synchronises,
+ * returns total milliseconds and launch counts per kernel id, and resets. */
+#define GB_K_PROJECT 0   /* K1  per-primitive projection + cull + tile rect */
+#define GB_K_SCAN 1      /* K2a tile-count scan (CUB) */
+#define GB_K_DUPLICATE 2 /* K2b (tile|depth) key duplication */
+#define GB_K_SORT 3      /* K2c radix sort (CUB) */
+#define GB_K_RANGES 4    /* K2d per-tile ranges */
+#define GB_K_FORWARD 5   /* K3  forward compositor */
+#define GB_K_BACKWARD 6  /* K4  backward compositor */
+#define GB_K_CHAIN 7     /* K5  per-primitive gradient chain */
+#define GB_K_LOSS 8      /* K6  photometric loss */
+#define GB_K_ADAM 9      /* K7  Adam */
+#define GB_NUM_KERNEL_IDS 10
+GB_API gb_status gb_context_profile(gb_context *ctx, int enable);
+GB_API gb_status gb_context_profile_read(gb_context *ctx, double *total_ms, int64_t *counts, int n);
+
 /* ---- binning: TileBinning + build_binning (raster.hpp:105-147) ------------ */
 GB_API gb_status gb_binning_create(gb_context *ctx, gb_binning **out);
 GB_API gb_status gb_binning_destroy(gb_binning *b);

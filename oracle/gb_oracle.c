@@ -157,9 +157,12 @@ typedef struct {
     double tuc[3], tvc[3], pc[3];
     double M[9]; /* camera-space plane map, row-major: columns (s_u tuc, s_v tvc, pc) */
     double depth;
-    /* z components of C0 = M0 x M1, Cx = M1 x M2, Cy = M2 x M0 and the projected
-     * centre (dxc, dyc): only for the parity protocol's conditioning measure */
-    double c0z, cxz, cyz, dxc, dyc;
+    /* Parity-protocol only: the linear-fractional form the fp32 compositor
+     * evaluates, (u, v, 1) ~ (X.x dx + Y.x dy, X.y dx + Y.y dy, 1 + X.z dx + Y.z dy)
+     * with (dx, dy) the pixel offset from the projected centre (cpx, cpy),
+     * X = Cx/(E_z fx), Y = Cy/(E_z fy), Cx = M1 x M2, Cy = M2 x M0. Used to
+     * estimate the fp32 error of (u, v) and the GPU's accumulation magnitudes. */
+    double X[3], Y[3], cpx, cpy, ez, dxc, dyc;
 } geom_t;
 
 /* Unit quaternion (w,x,y,z) -> rotation columns t_u, t_v (2DGS convention,
@@ -217,11 +220,18 @@ static void build_geom(const orc_splats *s, const orc_camera *cam, int64_t k, ge
     g->depth = (double)(float)g->pc[2];
     g->valid = g->pc[2] > cam->near_plane;
     const double *M0 = g->M, *M1 = g->M + 3, *M2 = g->M + 6;
-    g->c0z = M0[0] * M1[1] - M0[1] * M1[0];
-    g->cxz = M1[0] * M2[1] - M1[1] * M2[0];
-    g->cyz = M2[0] * M0[1] - M2[1] * M0[0];
+    const double C0z = M0[0] * M1[1] - M0[1] * M1[0];
+    const double Cx[3] = {M1[1] * M2[2] - M1[2] * M2[1], M1[2] * M2[0] - M1[0] * M2[2], M1[0] * M2[1] - M1[1] * M2[0]};
+    const double Cy[3] = {M2[1] * M0[2] - M2[2] * M0[1], M2[2] * M0[0] - M2[0] * M0[2], M2[0] * M0[1] - M2[1] * M0[0]};
     g->dxc = g->pc[0] / g->pc[2];
     g->dyc = g->pc[1] / g->pc[2];
+    g->cpx = cam->fx * g->dxc + cam->cx;
+    g->cpy = cam->fy * g->dyc + cam->cy;
+    g->ez = C0z + g->dxc * Cx[2] + g->dyc * Cy[2];
+    for (int j = 0; j < 3; ++j) {
+        g->X[j] = Cx[j] / (g->ez * cam->fx);
+        g->Y[j] = Cy[j] / (g->ez * cam->fy);
+    }
 }
 
 /* raster.hpp:36-42 */
@@ -552,16 +562,34 @@ static int eval_uv(const raster_ctx_t *c, const geom_t *g, double px, double py,
     return intersect_pinhole_g(g, c->cam, px, py, u, v, a, b, cz);
 }
 
-/* fp32 conditioning of the pinhole intersection: c_z = C0z + dxn Cxz + dyn Cyz
- * evaluated centred on the projected centre; small |c_z| relative to its
- * terms means the ray grazes the plane and fp32 (u, v) lose digits. */
-static int cond_kink(const raster_ctx_t *c, const geom_t *g, double px, double py, double cz) {
-    if (c->cam->mode != ORC_MODE_PINHOLE || !c->kink) return 0;
-    const double dxn = (px - c->cam->cx) / c->cam->fx - g->dxc;
-    const double dyn = (py - c->cam->cy) / c->cam->fy - g->dyc;
-    const double ez = g->c0z + g->dxc * g->cxz + g->dyc * g->cyz;
-    const double terms = fabs(ez) + fabs(dxn * g->cxz) + fabs(dyn * g->cyz);
-    return fabs(cz) <= c->kink->cond_min * terms;
+/* Estimated absolute fp32 error of (u, v) as the compositor evaluates them
+ * (coefficients and products rounded once each), in texel-grid units
+ * (x (n-1)/(2 sigma) when n > 1).  An evaluation whose estimate exceeds
+ * kink->cond_min is "sensitive": its fp32 result is intrinsically uncertain
+ * beyond the tolerance (thin, grazing splats), so it is treated like a kink. */
+static const double kEps32 = 5.9604644775390625e-08;
+
+static double uv_error32(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
+    double eu, ev;
+    if (c->cam->mode == ORC_MODE_ORTHO) {
+        const double dx = px - g->x, dy = py - g->y;
+        eu = 4.0 * kEps32 * (fabs(g->cos_t * dx) + fabs(g->sin_t * dy)) * g->inv_su + 2.0 * kEps32 * fabs(u);
+        ev = 4.0 * kEps32 * (fabs(g->sin_t * dx) + fabs(g->cos_t * dy)) * g->inv_sv + 2.0 * kEps32 * fabs(v);
+    } else {
+        const double dx = px - g->cpx, dy = py - g->cpy;
+        const double czt = 1.0 + fabs(g->X[2] * dx) + fabs(g->Y[2] * dy);
+        const double cz = fabs(1.0 + g->X[2] * dx + g->Y[2] * dy);
+        eu = 4.0 * kEps32 * (fabs(g->X[0] * dx) + fabs(g->Y[0] * dy) + fabs(u) * czt + fabs(g->X[0]) + fabs(g->Y[0])) / cz;
+        ev = 4.0 * kEps32 * (fabs(g->X[1] * dx) + fabs(g->Y[1] * dy) + fabs(v) * czt + fabs(g->X[1]) + fabs(g->Y[1])) / cz;
+    }
+    const int n = c->s->n;
+    const double grid = n > 1 ? (double)(n - 1) / (2.0 * c->s->sigma) : 1.0;
+    const double e = (eu > ev ? eu : ev);
+    return e * (grid > 1.0 ? grid : 1.0);
+}
+
+static int sensitive(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
+    return c->kink && c->kink->cond_min > 0.0 && uv_error32(c, g, px, py, u, v) > c->kink->cond_min;
 }
 
 static void forward_tile(void *vctx, int tile) {
@@ -593,7 +621,7 @@ static void forward_tile(void *vctx, int tile) {
                     if (cfg->alpha_skip > 0.0 && fabs(alpha - cfg->alpha_skip) <= kk->alpha_rel * cfg->alpha_skip)
                         flag |= 1;
                     if (fabs(alpha_raw - kMaxAlpha) <= kk->alpha_rel * kMaxAlpha) flag |= 1;
-                    if (alpha >= cfg->alpha_skip && cond_kink(c, g, px, py, cz)) flag |= 1;
+                    if (alpha >= cfg->alpha_skip && sensitive(c, g, px, py, u, v)) flag |= 4;
                 }
                 if (alpha < cfg->alpha_skip) continue;
                 double col[3];
@@ -678,16 +706,17 @@ static void geo_abs(const raster_ctx_t *c, const geom_t *g, double u, double v, 
         out[5] = op;
         return;
     }
+    /* magnitudes in the compositor's decomposition: c = E + dxn Cx + dyn Cy
+     * centred on the projected centre, sums of |gc|, |dxn gc|, |dyn gc| */
+    (void)a;
+    (void)b;
     const double iz = 1.0 / fabs(cz);
-    const double gc0 = uh * iz, gc1 = vh * iz, gc2 = (uh * fabs(u) + vh * fabs(v)) * iz;
-    const double ga[3] = {fabs(b[1]) * gc2 + fabs(b[2]) * gc1, fabs(b[2]) * gc0 + fabs(b[0]) * gc2,
-                          fabs(b[0]) * gc1 + fabs(b[1]) * gc0};
-    const double gb[3] = {gc1 * fabs(a[2]) + gc2 * fabs(a[1]), gc2 * fabs(a[0]) + gc0 * fabs(a[2]),
-                          gc0 * fabs(a[1]) + gc1 * fabs(a[0])};
+    const double gc[3] = {uh * iz, vh * iz, (uh * fabs(u) + vh * fabs(v)) * iz};
+    const double ddx = fabs(dxn - g->dxc), ddy = fabs(dyn - g->dyc);
     for (int j = 0; j < 3; ++j) {
-        out[j] = ga[j];
-        out[3 + j] = gb[j];
-        out[6 + j] = fabs(dxn) * ga[j] + fabs(dyn) * gb[j];
+        out[j] = gc[j];
+        out[3 + j] = ddx * gc[j];
+        out[6 + j] = ddy * gc[j];
     }
     out[9] = op;
 }
@@ -726,6 +755,34 @@ static void uv_hat_tex_abs(int n, double sigma, double u, double v, const double
     const double scale = (double)(n - 1) / (2.0 * sigma);
     if (u > -sigma && u < sigma) *uh = scale * su;
     if (v > -sigma && v < sigma) *vh = scale * sv;
+}
+
+/* |terms| of one evaluation (composited with transmittance t in front of it)
+ * added to an abs record: the geometry slots and the four touched texels. */
+static void add_abs_terms(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v,
+                          double alpha, double weight, double t, const double *gacc, const double *behind,
+                          const double *gridk, const double *a, const double *b, double cz, double *dst) {
+    const int n = c->s->n;
+    const double sigma = c->s->sigma;
+    const size_t gs = geom_slots(c->cam);
+    const int pin = c->cam->mode == ORC_MODE_PINHOLE;
+    double col[3];
+    orc_bilinear(u, v, n, sigma, gridk, col);
+    const double c_hat[3] = {alpha * t * gacc[0], alpha * t * gacc[1], alpha * t * gacc[2]};
+    double uh_t, vh_t;
+    uv_hat_tex_abs(n, sigma, u, v, gridk, c_hat, &uh_t, &vh_t);
+    double ah = 0.0;
+    for (int ch = 0; ch < 3; ++ch) ah += fabs(gacc[ch]) * t * (fabs(col[ch]) + fabs(behind[ch]));
+    const int gated = g->alpha_k * weight < kMaxAlpha;
+    const double op_abs = gated ? ah * weight * (g->alpha_k * (1.0 - g->alpha_k)) : 0.0;
+    const double uh = uh_t + (gated ? ah * alpha * fabs(u) : 0.0);
+    const double vh = vh_t + (gated ? ah * alpha * fabs(v) : 0.0);
+    const double dxn = pin ? (px - c->cam->cx) / c->cam->fx : 0.0;
+    const double dyn = pin ? (py - c->cam->cy) / c->cam->fy : 0.0;
+    double d[10];
+    geo_abs(c, g, u, v, uh, vh, op_abs, a, b, cz, dxn, dyn, d);
+    for (size_t j = 0; j < gs; ++j) dst[j] += d[j];
+    tex_abs(n, sigma, u, v, c_hat, dst + gs);
 }
 
 static void backward_tile(void *vctx, int tile) {
@@ -773,9 +830,16 @@ static void backward_tile(void *vctx, int tile) {
                 const double weight = gaussian_weight(u, v);
                 const double alpha_raw = g->alpha_k * weight;
                 const double alpha = dmin(alpha_raw, kMaxAlpha);
-                if (alpha < cfg->alpha_skip) continue;
-                t /= 1.0 - alpha;
                 const double *gridk = c->s->grid + (size_t)id * tex_stride;
+                if (alpha < cfg->alpha_skip) {
+                    /* an entry skipped just below the threshold may be composited in fp32 */
+                    if (pslk && (px_flag & 1) && kk &&
+                        fabs(alpha - cfg->alpha_skip) <= kk->alpha_rel * cfg->alpha_skip)
+                        add_abs_terms(c, g, px, py, u, v, alpha, weight, t, gacc, behind, gridk, a, b, cz,
+                                      pslk + (size_t)rank * stride);
+                    continue;
+                }
+                t /= 1.0 - alpha;
                 double col[3];
                 orc_bilinear(u, v, n, sigma, gridk, col);
                 double *rec = partial + (size_t)rank * stride;
@@ -829,13 +893,16 @@ static void backward_tile(void *vctx, int tile) {
                     }
                     if (pslk) {
                         double *rs = pslk + (size_t)rank * stride;
-                        if (px_flag) {
+                        const double err = kk ? uv_error32(c, g, px, py, u, v) : 0.0;
+                        const double margin = grid_margin > 3.0 * err ? grid_margin : 3.0 * err;
+                        if ((px_flag & 3) || sensitive(c, g, px, py, u, v)) {
+                            /* decision kink in this pixel, or an fp32-ill-conditioned evaluation */
                             for (size_t j = 0; j < gs; ++j) rs[j] += d[j];
                             tex_abs(n, sigma, u, v, c_hat, rs + gs);
-                        } else if (grid_kink(u, n, sigma, grid_margin) || grid_kink(v, n, sigma, grid_margin)) {
+                        } else if (grid_kink(u, n, sigma, margin) || grid_kink(v, n, sigma, margin)) {
                             /* only the texture part of (u_hat, v_hat) jumps across a texel
                              * boundary: bound the jump by both sides' magnitudes */
-                            const double du = 2.0 * grid_margin * (2.0 * sigma) / (n - 1);
+                            const double du = 2.0 * margin * (2.0 * sigma) / (n - 1);
                             double uh_s = 0.0, vh_s = 0.0, t1, t2;
                             const double sh[4][2] = {{-du, 0.0}, {du, 0.0}, {0.0, -du}, {0.0, du}};
                             for (int q = 0; q < 4; ++q) {
@@ -981,8 +1048,39 @@ static void reduce_records(const orc_camera *cam, const orc_binning *b, const ge
     if (pin) {
         for (int64_t k = 0; k < K; ++k) {
             if (!geom[k].valid) continue;
-            pinhole_chain(cam, &geom[k], dM + 9 * k, gr->position + 3 * k, gr->quat + 4 * k, gr->log_scale + 2 * k,
-                          absolute);
+            double *d = dM + 9 * k;
+            if (absolute) {
+                /* (|E|, |X|, |Y|) sums of the compositor's decomposition -> |dL/dM|:
+                 * C0 = M0 x M1, Cx = M1 x M2, Cy = M2 x M0 with |cross| bounds */
+                const geom_t *g = &geom[k];
+                double aM[9], gC0[3], gCx[3], gCy[3], out[9];
+                for (int j = 0; j < 9; ++j) aM[j] = fabs(g->M[j]);
+                for (int j = 0; j < 3; ++j) {
+                    gC0[j] = d[j];
+                    gCx[j] = d[3 + j] + fabs(g->dxc) * d[j];
+                    gCy[j] = d[6 + j] + fabs(g->dyc) * d[j];
+                }
+                const double *A0 = aM, *A1 = aM + 3, *A2 = aM + 6;
+#define ACROSS(a, b, o)                                \
+    do {                                               \
+        (o)[0] = (a)[1] * (b)[2] + (a)[2] * (b)[1];    \
+        (o)[1] = (a)[2] * (b)[0] + (a)[0] * (b)[2];    \
+        (o)[2] = (a)[0] * (b)[1] + (a)[1] * (b)[0];    \
+    } while (0)
+                double t0[3], t1[3];
+                ACROSS(A1, gC0, t0);
+                ACROSS(gCy, A2, t1);
+                for (int j = 0; j < 3; ++j) out[j] = t0[j] + t1[j];
+                ACROSS(gC0, A0, t0);
+                ACROSS(A2, gCx, t1);
+                for (int j = 0; j < 3; ++j) out[3 + j] = t0[j] + t1[j];
+                ACROSS(gCx, A1, t0);
+                ACROSS(A0, gCy, t1);
+                for (int j = 0; j < 3; ++j) out[6 + j] = t0[j] + t1[j];
+#undef ACROSS
+                memcpy(d, out, sizeof(out));
+            }
+            pinhole_chain(cam, &geom[k], d, gr->position + 3 * k, gr->quat + 4 * k, gr->log_scale + 2 * k, absolute);
         }
         free(dM);
     }

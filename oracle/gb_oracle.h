@@ -98,7 +98,7 @@ typedef struct {
     double alpha_rel; /* |alpha - alpha_skip| <= alpha_rel*alpha_skip, same vs 0.999 cap */
     double trans_rel; /* |T - early_stop| <= trans_rel*early_stop at any composite */
     double grid_abs;  /* |u' - k| <= grid_abs for an interior texel boundary k; ||u|-sigma| <= grid_abs*2sigma/(n-1) */
-    double cond_min;  /* pinhole: |c_z| <= cond_min*|a||b| (grazing ray) */
+    double cond_min;  /* fp32 sensitivity: estimated |error| of (u,v) in texel units above this */
 } orc_kink;
 
 int orc_build_binning(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, orc_binning *out);
@@ -111,7 +111,8 @@ int orc_project(const orc_splats *s, const orc_camera *cam, const orc_config *cf
 int orc_render_forward(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, const orc_binning *b,
                        double *color, double *trans, int32_t *last, uint8_t *kink_px, const orc_kink *kink);
 
-/* kink_px (nullable): per-pixel flags from orc_render_forward (bit0 decision kink, bit1 early-stop kink).
+/* kink_px (nullable): per-pixel flags from orc_render_forward (bit0 decision kink, bit1 early-stop kink,
+ * bit2 an fp32-ill-conditioned evaluation).
  * mag / slack (nullable): per-entry sum of |terms| and the kink slack (see gb_oracle.c). */
 int orc_render_backward(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, const orc_binning *b,
                         const double *trans, const int32_t *last, const double *image_grad, orc_grads *g,

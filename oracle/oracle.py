@@ -67,7 +67,7 @@ class OrcKink(C.Structure):
                 ("cond_min", C.c_double)]
 
 
-DEFAULT_KINK = (2e-5, 1e-3, 1e-4, 1e-3)
+DEFAULT_KINK = (2e-5, 1e-3, 1e-4, 1e-4)
 
 _oracle = None
 _ref = None

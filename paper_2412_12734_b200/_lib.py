@@ -24,6 +24,8 @@ GB_NOT_SUPPORTED = 6
 MODE_ORTHO = 0
 MODE_PINHOLE = 1
 
+KERNEL_NAMES = ("project", "scan", "duplicate", "sort", "ranges", "forward", "backward", "chain", "loss", "adam")
+
 
 class GridConfig(C.Structure):
     _fields_ = [("n", C.c_int32), ("_pad", C.c_int32), ("sigma", C.c_double)]
@@ -144,6 +146,8 @@ _SIGS = {
     "gb_context_stream": (P, [P]),
     "gb_sync": (C.c_int, [P]),
     "gb_context_launch_count": (C.c_int64, [P]),
+    "gb_context_profile": (C.c_int, [P, C.c_int]),
+    "gb_context_profile_read": (C.c_int, [P, P, P, C.c_int]),
     "gb_binning_create": (C.c_int, [P, C.POINTER(P)]),
     "gb_binning_destroy": (C.c_int, [P]),
     "gb_build_binning": (C.c_int, [P, C.POINTER(Splats), C.POINTER(Camera), C.POINTER(RasterConfigC), P]),

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "gb_internal.cuh"
 
@@ -94,6 +95,11 @@ struct DevBuf {
 
 }  // namespace
 
+struct ProfRec {
+    int id;
+    cudaEvent_t start, stop;
+};
+
 struct gb_context {
     int device = 0;
     int sm_count = 148;
@@ -102,7 +108,43 @@ struct gb_context {
     int64_t launches = 0;
     DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, accum, adam_bad;
     uint32_t* pinned_total = nullptr;
+    bool prof = false;
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> prof_pool;
 };
+
+namespace {
+cudaEvent_t prof_event(gb_context* ctx) {
+    if (!ctx->prof_pool.empty()) {
+        cudaEvent_t e = ctx->prof_pool.back();
+        ctx->prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one launch site with CUDA events on the context stream when profiling.
+struct ProfScope {
+    gb_context* ctx;
+    int id;
+    cudaEvent_t start = nullptr;
+    ProfScope(gb_context* c, int i) : ctx(c), id(i) {
+        if (ctx->prof) {
+            start = prof_event(ctx);
+            cudaEventRecord(start, ctx->stream);
+        }
+    }
+    ~ProfScope() {
+        if (start) {
+            cudaEvent_t stop = prof_event(ctx);
+            cudaEventRecord(stop, ctx->stream);
+            ctx->prof_recs.push_back({id, start, stop});
+        }
+    }
+};
+}  // namespace
 
 struct gb_binning {
     gb_context* ctx = nullptr;
@@ -232,6 +274,11 @@ gb_status gb_context_destroy(gb_context* ctx) {
     ctx->accum.release();
     ctx->adam_bad.release();
     if (ctx->pinned_total) cudaFreeHost(ctx->pinned_total);
+    for (const ProfRec& r : ctx->prof_recs) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return GB_OK;
@@ -253,6 +300,34 @@ gb_status gb_sync(gb_context* ctx) {
 }
 
 int64_t gb_context_launch_count(const gb_context* ctx) { return ctx ? ctx->launches : 0; }
+
+gb_status gb_context_profile(gb_context* ctx, int enable) {
+    if (!ctx) return fail(GB_INVALID_ARGUMENT, "ctx is null");
+    ctx->prof = enable != 0;
+    return GB_OK;
+}
+
+gb_status gb_context_profile_read(gb_context* ctx, double* total_ms, int64_t* counts, int n) {
+    if (!ctx || n < 0) return fail(GB_INVALID_ARGUMENT, "bad argument");
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < n; ++i) {
+        if (total_ms) total_ms[i] = 0.0;
+        if (counts) counts[i] = 0;
+    }
+    for (const ProfRec& r : ctx->prof_recs) {
+        float ms = 0.0f;
+        GB_CUDA(cudaEventElapsedTime(&ms, r.start, r.stop));
+        if (r.id < n) {
+            if (total_ms) total_ms[r.id] += ms;
+            if (counts) counts[r.id] += 1;
+        }
+        ctx->prof_pool.push_back(r.start);
+        ctx->prof_pool.push_back(r.stop);
+    }
+    ctx->prof_recs.clear();
+    return GB_OK;
+}
 
 gb_status gb_binning_create(gb_context* ctx, gb_binning** out) {
     if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
@@ -308,12 +383,18 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
 
     // K1
     gb::ProjParams pp = gb::make_proj_params(s, cam, cfg, b->tiles_x, b->tiles_y);
-    GB_CUDA(gb::launch_project(pp, b->headers.as<gb::ScreenHeader>(), b->rects.as<uint2>(),
-                               b->counts.as<uint32_t>(), b->depth.as<uint32_t>(), stream));
+    {
+        ProfScope ps(ctx, GB_K_PROJECT);
+        GB_CUDA(gb::launch_project(pp, b->headers.as<gb::ScreenHeader>(), b->rects.as<uint2>(),
+                                   b->counts.as<uint32_t>(), b->depth.as<uint32_t>(), stream));
+    }
     ctx->launches += K > 0;
     // K2a scan -> P
-    GB_CUDA(gb::launch_scan(ctx->scan_temp.p, ctx->scan_temp.cap, b->counts.as<uint32_t>(),
-                            b->offsets.as<uint32_t>(), K, stream));
+    {
+        ProfScope ps(ctx, GB_K_SCAN);
+        GB_CUDA(gb::launch_scan(ctx->scan_temp.p, ctx->scan_temp.cap, b->counts.as<uint32_t>(),
+                                b->offsets.as<uint32_t>(), K, stream));
+    }
     ctx->launches += K > 0 ? 1 : 0;
     GB_CUDA(cudaMemcpyAsync(ctx->pinned_total, b->offsets.as<uint32_t>() + K, sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, stream));
@@ -327,13 +408,22 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
     GB_CUDA(ctx->vals_tmp.ensure(sizeof(int32_t) * Pc));
     GB_CUDA(ctx->sort_temp.ensure(gb::sort_temp_bytes(Pc)));
     // K2b duplicate, K2c sort, K2d ranges
-    GB_CUDA(gb::launch_duplicate(K, b->tiles_x, b->offsets.as<uint32_t>(), b->rects.as<uint2>(),
-                                 b->depth.as<uint32_t>(), ctx->keys_tmp.as<uint64_t>(), ctx->vals_tmp.as<int32_t>(),
-                                 stream));
-    GB_CUDA(gb::launch_sort(ctx->sort_temp.p, ctx->sort_temp.cap, ctx->keys_tmp.as<uint64_t>(),
-                            b->keys.as<uint64_t>(), ctx->vals_tmp.as<int32_t>(), b->values.as<int32_t>(), P, n_tiles,
-                            stream));
-    GB_CUDA(gb::launch_ranges(P, b->keys.as<uint64_t>(), b->ranges.as<uint2>(), n_tiles, stream));
+    {
+        ProfScope ps(ctx, GB_K_DUPLICATE);
+        GB_CUDA(gb::launch_duplicate(K, b->tiles_x, b->offsets.as<uint32_t>(), b->rects.as<uint2>(),
+                                     b->depth.as<uint32_t>(), ctx->keys_tmp.as<uint64_t>(),
+                                     ctx->vals_tmp.as<int32_t>(), stream));
+    }
+    {
+        ProfScope ps(ctx, GB_K_SORT);
+        GB_CUDA(gb::launch_sort(ctx->sort_temp.p, ctx->sort_temp.cap, ctx->keys_tmp.as<uint64_t>(),
+                                b->keys.as<uint64_t>(), ctx->vals_tmp.as<int32_t>(), b->values.as<int32_t>(), P,
+                                n_tiles, stream));
+    }
+    {
+        ProfScope ps(ctx, GB_K_RANGES);
+        GB_CUDA(gb::launch_ranges(P, b->keys.as<uint64_t>(), b->ranges.as<uint2>(), n_tiles, stream));
+    }
     ctx->launches += (K > 0) + (P > 0 ? 2 : 0);
     b->built = true;
     return GB_OK;
@@ -388,6 +478,7 @@ gb_status gb_render_forward(gb_context* ctx, const gb_splats* s, const gb_camera
     if (gb_status st = set_device(ctx)) return st;
     const gb::CamConst cc = make_cam_const(cam);
     const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+    ProfScope ps(ctx, GB_K_FORWARD);
     GB_CUDA(gb::launch_forward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
                                b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
                                s->grid_values, cc, rc, out->color, out->final_transmittance, out->last_rank,
@@ -423,12 +514,19 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
     GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(float) * gb::kAccumStride * K, stream));
     const gb::CamConst cc = make_cam_const(cam);
     const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
-    GB_CUDA(gb::launch_backward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
-                                b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
-                                s->grid_values, cc, rc, out->final_transmittance, out->last_rank, image_grad,
-                                ctx->accum.as<float>(), g->grid_values, stream));
+    {
+        ProfScope ps(ctx, GB_K_BACKWARD);
+        GB_CUDA(gb::launch_backward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
+                                    b->ranges.as<uint2>(), b->values.as<int32_t>(),
+                                    b->headers.as<gb::ScreenHeader>(), s->grid_values, cc, rc,
+                                    out->final_transmittance, out->last_rank, image_grad, ctx->accum.as<float>(),
+                                    g->grid_values, stream));
+    }
     gb::ProjParams pp = gb::make_proj_params(s, cam, &b->cfg, b->tiles_x, b->tiles_y);
-    GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
+    {
+        ProfScope ps(ctx, GB_K_CHAIN);
+        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
+    }
     ctx->launches += 2;
     return GB_OK;
 }
@@ -443,6 +541,7 @@ gb_status gb_l1_loss(gb_context* ctx, const float* color, const float* target, i
                      float* loss) {
     if (!ctx || (n > 0 && (!color || !target || !grad))) return fail(GB_INVALID_ARGUMENT, "null argument");
     if (gb_status st = set_device(ctx)) return st;
+    ProfScope ps(ctx, GB_K_LOSS);
     GB_CUDA(gb::launch_loss(0, color, target, n, scale, grad, loss, ctx->sm_count, ctx->stream));
     ctx->launches += n > 0;
     return GB_OK;
@@ -452,6 +551,7 @@ gb_status gb_mse_loss(gb_context* ctx, const float* color, const float* target, 
                       float* loss) {
     if (!ctx || (n > 0 && (!color || !target || !grad))) return fail(GB_INVALID_ARGUMENT, "null argument");
     if (gb_status st = set_device(ctx)) return st;
+    ProfScope ps(ctx, GB_K_LOSS);
     GB_CUDA(gb::launch_loss(1, color, target, n, scale, grad, loss, ctx->sm_count, ctx->stream));
     ctx->launches += n > 0;
     return GB_OK;
@@ -492,6 +592,7 @@ gb_status gb_adam_step(gb_context* ctx, int32_t mode, int64_t count, int32_t n, 
          lrs->opacity_logit},
         {params->grid_values, g->grid_values, state->m.grid_values, state->v.grid_values, tex, lrs->color_grid}};
     auto* bad = ctx->adam_bad.as<unsigned long long>();
+    ProfScope ps(ctx, GB_K_ADAM);
     for (int i = 0; i < 5; ++i) {
         if (groups[i].len == 0) continue;
         if (!groups[i].p || !groups[i].g || !groups[i].m || !groups[i].v)

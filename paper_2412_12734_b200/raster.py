@@ -70,6 +70,19 @@ class _Context:
     def launches(self) -> int:
         return int(lib.gb_context_launch_count(self.handle))
 
+    def profile(self, enable: bool) -> None:
+        check(lib.gb_context_profile(self.handle, int(enable)), "gb_context_profile")
+
+    def profile_read(self) -> dict:
+        """{kernel: (total_ms, launches)} since the last read (synchronises)."""
+        import numpy as _np
+
+        n = len(_lib.KERNEL_NAMES)
+        ms = _np.zeros(n, _np.float64)
+        cnt = _np.zeros(n, _np.int64)
+        check(lib.gb_context_profile_read(self.handle, ms.ctypes.data, cnt.ctypes.data, n), "gb_context_profile_read")
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(_lib.KERNEL_NAMES)}
+
 
 def context(device=None) -> _Context:
     return _Context.get(torch.device(device) if device is not None else torch.device("cuda"))
