@@ -167,6 +167,14 @@ GB_API int64_t gb_context_launch_count(const gb_context *ctx);
 GB_API gb_status gb_context_profile(gb_context *ctx, int enable);
 GB_API gb_status gb_context_profile_read(gb_context *ctx, double *total_ms, int64_t *counts, int n);
 
+/* ---- device memory helpers (so a C/C++ host needs no CUDA headers) -------- */
+GB_API gb_status gb_device_alloc(gb_context *ctx, uint64_t bytes, void **out);
+GB_API gb_status gb_device_free(gb_context *ctx, void *ptr);
+/* Stream-ordered copies on the context stream; pass sync = 1 to block until done. */
+GB_API gb_status gb_copy_h2d(gb_context *ctx, void *dst_device, const void *src_host, uint64_t bytes, int sync);
+GB_API gb_status gb_copy_d2h(gb_context *ctx, void *dst_host, const void *src_device, uint64_t bytes, int sync);
+GB_API gb_status gb_memset_device(gb_context *ctx, void *dst_device, int value, uint64_t bytes);
+
 /* ---- binning: TileBinning + build_binning (raster.hpp:105-147) ------------ */
 GB_API gb_status gb_binning_create(gb_context *ctx, gb_binning **out);
 GB_API gb_status gb_binning_destroy(gb_binning *b);

@@ -148,6 +148,11 @@ _SIGS = {
     "gb_context_launch_count": (C.c_int64, [P]),
     "gb_context_profile": (C.c_int, [P, C.c_int]),
     "gb_context_profile_read": (C.c_int, [P, P, P, C.c_int]),
+    "gb_device_alloc": (C.c_int, [P, C.c_uint64, C.POINTER(P)]),
+    "gb_device_free": (C.c_int, [P, P]),
+    "gb_copy_h2d": (C.c_int, [P, P, P, C.c_uint64, C.c_int]),
+    "gb_copy_d2h": (C.c_int, [P, P, P, C.c_uint64, C.c_int]),
+    "gb_memset_device": (C.c_int, [P, P, C.c_int, C.c_uint64]),
     "gb_binning_create": (C.c_int, [P, C.POINTER(P)]),
     "gb_binning_destroy": (C.c_int, [P]),
     "gb_build_binning": (C.c_int, [P, C.POINTER(Splats), C.POINTER(Camera), C.POINTER(RasterConfigC), P]),

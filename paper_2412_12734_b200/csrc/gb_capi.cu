@@ -329,6 +329,45 @@ gb_status gb_context_profile_read(gb_context* ctx, double* total_ms, int64_t* co
     return GB_OK;
 }
 
+gb_status gb_device_alloc(gb_context* ctx, uint64_t bytes, void** out) {
+    if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(cudaMalloc(out, bytes > 0 ? bytes : 1));
+    return GB_OK;
+}
+
+gb_status gb_device_free(gb_context* ctx, void* ptr) {
+    if (!ctx) return fail(GB_INVALID_ARGUMENT, "ctx is null");
+    if (!ptr) return GB_OK;
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(cudaFree(ptr));
+    return GB_OK;
+}
+
+gb_status gb_copy_h2d(gb_context* ctx, void* dst, const void* src, uint64_t bytes, int sync) {
+    if (!ctx || (bytes && (!dst || !src))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    if (bytes) GB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (sync) GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GB_OK;
+}
+
+gb_status gb_copy_d2h(gb_context* ctx, void* dst, const void* src, uint64_t bytes, int sync) {
+    if (!ctx || (bytes && (!dst || !src))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    if (bytes) GB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (sync) GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GB_OK;
+}
+
+gb_status gb_memset_device(gb_context* ctx, void* dst, int value, uint64_t bytes) {
+    if (!ctx || (bytes && !dst)) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    if (bytes) GB_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+    return GB_OK;
+}
+
 gb_status gb_binning_create(gb_context* ctx, gb_binning** out) {
     if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
     *out = new gb_binning();

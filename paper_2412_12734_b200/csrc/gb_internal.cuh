@@ -29,8 +29,12 @@ constexpr float kMaxAlphaF = 0.999f;
 //            with X = Cx/(E_z fx), Y = Cy/(E_z fy) precomputed in fp64 (K1):
 //            h0 = (X.x, X.y, X.z, Y.x)  h1 = (Y.y, Y.z, alpha_k, hx)
 //            h2 = (hy, int cxi, int cyi, 0); dx = (x - cxi) + hx, dy = (y - cyi) + hy.
+//   both   : h3 = (x0, x1, y0, y1) the inclusive pixel box outside which
+//            alpha < alpha_skip for certain (fp64 AABB of the alpha-skip
+//            ellipse, enlarged by a safety margin); the compositors skip a
+//            warp's 8x4 pixel block for this entry when it misses the box.
 struct __align__(16) ScreenHeader {
-    float4 h0, h1, h2;
+    float4 h0, h1, h2, h3;
 };
 
 // Per-launch camera constants for the fp32 compositor.

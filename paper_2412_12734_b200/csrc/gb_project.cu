@@ -153,6 +153,58 @@ __device__ bool cull_rect(const ProjParams& p, int64_t k, const Geom& g, int& x0
     return true;
 }
 
+// Pixel box outside which alpha < alpha_skip is certain: the AABB of the uv
+// ellipse u^2 + v^2 <= 2 ln(alpha_k / alpha_skip) (radius enlarged by 1e-3
+// relative + 0.05 px), so the fp32 evaluation there sits > 0.1% below the
+// threshold and skipping it cannot change a decision.  Whole image when the
+// threshold is disabled or the ellipse is not entirely in front of the camera.
+__device__ float4 alpha_box(const ProjParams& p, int64_t k, const Geom& g) {
+    const float4 all = make_float4(-1e30f, 1e30f, -1e30f, 1e30f);
+    if (!(p.alpha_skip > 0.0)) return all;
+    const double ak = 1.0 / (1.0 + exp(-(double)p.opacity[k]));
+    if (!(ak > p.alpha_skip)) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never composited
+    const double r = sqrt(2.0 * log(ak / p.alpha_skip)) * 1.001 + 1e-3;
+    double min_x, max_x, min_y, max_y;
+    if (p.mode == GB_MODE_ORTHO) {
+        const double th = (double)p.theta[k];
+        const double suc = g.s_u * cos(th), sus = g.s_u * sin(th), svc = g.s_v * cos(th), svs = g.s_v * sin(th);
+        const double hx = r * sqrt(suc * suc + svs * svs), hy = r * sqrt(sus * sus + svc * svc);
+        min_x = (double)p.position[2 * k] - hx;
+        max_x = (double)p.position[2 * k] + hx;
+        min_y = (double)p.position[2 * k + 1] - hy;
+        max_y = (double)p.position[2 * k + 1] + hy;
+    } else {
+        const double* M = g.M;
+        const double lat = sqrt(M[6] * M[6] + M[7] * M[7]);
+        if (!(M[8] - r * lat > 0.0)) return all;
+        double H0[3], H1[3], H2[3];
+        for (int j = 0; j < 3; ++j) {
+            H0[j] = p.fx * M[j] + p.cx * M[6 + j];
+            H1[j] = p.fy * M[3 + j] + p.cy * M[6 + j];
+            H2[j] = M[6 + j];
+        }
+        const double r2 = r * r;
+        const double C00 = r2 * (H0[0] * H0[0] + H0[1] * H0[1]) - H0[2] * H0[2];
+        const double C02 = r2 * (H0[0] * H2[0] + H0[1] * H2[1]) - H0[2] * H2[2];
+        const double C11 = r2 * (H1[0] * H1[0] + H1[1] * H1[1]) - H1[2] * H1[2];
+        const double C12 = r2 * (H1[0] * H2[0] + H1[1] * H2[1]) - H1[2] * H2[2];
+        const double C22 = r2 * (H2[0] * H2[0] + H2[1] * H2[1]) - H2[2] * H2[2];
+        const double dx = C02 * C02 - C00 * C22, dy = C12 * C12 - C11 * C22;
+        if (!(dx >= 0.0) || !(dy >= 0.0) || !(C22 < 0.0)) return all;
+        const double sx = sqrt(dx), sy = sqrt(dy);
+        const double xa = (C02 - sx) / C22, xb = (C02 + sx) / C22;
+        const double ya = (C12 - sy) / C22, yb = (C12 + sy) / C22;
+        min_x = dmin_(xa, xb);
+        max_x = dmax_(xa, xb);
+        min_y = dmin_(ya, yb);
+        max_y = dmax_(ya, yb);
+    }
+    const double m = 0.05;  // px
+    if (!(min_x == min_x && max_x == max_x && min_y == min_y && max_y == max_y)) return all;
+    return make_float4((float)fmax(-1e30, ceil(min_x - 0.5 - m)), (float)fmin(1e30, floor(max_x - 0.5 + m)),
+                       (float)fmax(-1e30, ceil(min_y - 0.5 - m)), (float)fmin(1e30, floor(max_y - 0.5 + m)));
+}
+
 // Effective projected centre used by the fp32 compositor (see ScreenHeader).
 __device__ __forceinline__ void pinhole_centre(const ProjParams& p, const Geom& g, int& cxi, int& cyi, float& hx,
                                                float& hy, double& dxe, double& dye) {
@@ -234,6 +286,7 @@ __global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeade
                   : make_float4(0.f, nan, (float)g.alpha_k, hx);
         h.h2 = make_float4(hy, __int_as_float(cxi), __int_as_float(cyi), 0.0f);
     }
+    h.h3 = alpha_box(p, k, g);
     hdr[k] = h;
 }
 

@@ -1,19 +1,25 @@
 // gb_raster.cu -- K3 (per-tile forward compositor) and K4 (per-tile
 // back-to-front backward), fp32, sm_100a.
 //
-// One CTA per 16x16 tile (any tile size 1..32), one thread per pixel.  The
-// tile's sorted list is walked in batches of B entries: each batch's 48 B
-// screen headers and full n x n x 3 textures are staged in shared memory
-// (the texture is the shared-memory cost that forced the
-// A6000 implementation to 8x8 tiles at n=8; a B200 CTA has 227 KB).
+// One CTA per tile (tile size 1..16), one thread per pixel; with 8-multiple
+// tiles each warp owns an 8x4 pixel block.  The tile's sorted list is walked
+// in batches of B entries whose 64 B screen headers and full n x n x 3
+// textures are staged in shared memory (the texture is the
+// shared-memory cost that forced the A6000 implementation to 8x8 tiles at
+// n=8).  Staging is double-buffered and asynchronous: warp 0 issues one TMA
+// bulk copy (cp.async.bulk, UBLKCP) per header and per texture of batch b+1,
+// completing on an mbarrier, while all warps composite batch b.  A warp skips
+// an entry outright when its pixel block misses the entry's alpha-box (K1).
 //
 // K3 restates render_forward (raster.hpp:201-261) + bilinear
 // (texture.hpp:49-66); K4 restates render_backward (raster.hpp:277-387) +
 // adj_bilinear_accum (texture.hpp:77-111).  Instead of the reference's
 // per-(tile, rank) partial records and ordered reduction, K4 reduces each
-// entry's contributions across the warp with shuffles and issues vector
-// red.global.add into (a) the caller's texel gradients and (b) a 48 B
-// per-primitive screen-space accumulator that K5 chains to the raw params.
+// entry's per-pixel contributions across the warp with a reduce-scatter
+// (transpose) butterfly -- V values cost V-1 shuffles instead of 5V -- and
+// issues red.global.add from the lanes that end up owning each sum, into
+// (a) the caller's texel gradients and (b) a 48 B per-primitive
+// screen-space accumulator that K5 chains to the raw parameters.
 #include "gb_internal.cuh"
 
 namespace gb {
@@ -31,7 +37,6 @@ struct Bilin {
     float w00, w10, w01, w11;
 };
 
-template <int NT>
 __device__ __forceinline__ void bilin_setup(float u, float v, int N, const RasterConst& rc, Bilin& b) {
     int iu, iv;
     float s = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
@@ -51,42 +56,107 @@ __device__ __forceinline__ void bilin_setup(float u, float v, int N, const Raste
 }
 
 // ---------------------------------------------------------------------------
-// shared-memory batch staging
+// asynchronous batch staging: TMA bulk copies (n even) or cp.async (n odd)
 // ---------------------------------------------------------------------------
-template <int NT>
-__device__ __forceinline__ void stage_batch(const int32_t* __restrict__ values, const ScreenHeader* __restrict__ hdr,
-                                            const float* __restrict__ tex, int64_t first, int nb, int N,
-                                            ScreenHeader* s_hdr, int* s_id, float* s_tex) {
-    const int nthr = blockDim.x;
-    const int tid = threadIdx.x;
-    for (int i = tid; i < nb; i += nthr) {
-        const int id = values[first + i];
-        s_id[i] = id;
-        s_hdr[i] = hdr[id];
-    }
-    __syncthreads();
-    const int F = 3 * N * N;
-    if ((F & 3) == 0) {
-        const int F4 = F >> 2;
-        const float4* __restrict__ t4 = reinterpret_cast<const float4*>(tex);
-        float4* s4 = reinterpret_cast<float4*>(s_tex);
-        for (int i = tid; i < nb * F4; i += nthr) {
-            const int e = i / F4;
-            const int o = i - e * F4;
-            s4[i] = __ldg(&t4[(size_t)s_id[e] * F4 + o]);
-        }
-    } else {
-        for (int i = tid; i < nb * F; i += nthr) {
-            const int e = i / F;
-            const int o = i - e * F;
-            s_tex[i] = __ldg(&tex[(size_t)s_id[e] * F + o]);
-        }
-    }
-    __syncthreads();
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
-__host__ __device__ inline size_t batch_smem_bytes(int B, int N) {
-    return (size_t)B * (sizeof(ScreenHeader) + sizeof(int) + sizeof(float) * 3 * N * N);
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// One staging buffer: B headers, B ids, B textures.
+struct Stage {
+    ScreenHeader* hdr;
+    float* tex;
+    int* id;
+};
+
+__host__ __device__ inline size_t stage_bytes(int B, int N) {  // rounded so the second buffer stays 128 B aligned
+    return ((size_t)B * (sizeof(ScreenHeader) + sizeof(float) * 3 * N * N + sizeof(int)) + 127) & ~(size_t)127;
+}
+
+__device__ __forceinline__ Stage stage_at(unsigned char* base, int buf, int B, int N) {
+    unsigned char* p = base + (size_t)buf * stage_bytes(B, N);
+    Stage s;
+    s.hdr = reinterpret_cast<ScreenHeader*>(p);
+    s.tex = reinterpret_cast<float*>(p + (size_t)B * sizeof(ScreenHeader));
+    s.id = reinterpret_cast<int*>(p + (size_t)B * (sizeof(ScreenHeader) + sizeof(float) * 3 * N * N));
+    return s;
+}
+
+// Issued by warp 0 only: entries [first, first + nb) of the tile list.  Bulk
+// path (n even: 12 n^2 B is a multiple of 16): lane 0 arms the barrier with
+// the batch's byte count, then the lanes each issue bulk copies.  cp.async
+// path (n odd): the whole warp copies 4-byte words and arrives on the barrier
+// when they land (cp.async.mbarrier.arrive.noinc).
+__device__ __forceinline__ void issue_batch(const int32_t* __restrict__ values, const ScreenHeader* __restrict__ hdr,
+                                            const float* __restrict__ tex, int64_t first, int nb, int N,
+                                            const Stage& s, uint64_t* bar) {
+    const int lane = threadIdx.x & 31;
+    const int F = 3 * N * N;
+    // make the generic-proxy reads of this buffer (previous batch) ordered before the async writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if ((F & 3) == 0) {
+        if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)nb * (uint32_t)(sizeof(ScreenHeader) + 4 * F));
+        __syncwarp();
+        for (int i = lane; i < nb; i += 32) {
+            const int id = values[first + i];
+            s.id[i] = id;
+            bulk_g2s(&s.hdr[i], &hdr[id], sizeof(ScreenHeader), bar);
+            bulk_g2s(s.tex + (size_t)i * F, tex + (size_t)id * F, 4u * F, bar);
+        }
+    } else {
+        for (int i = lane; i < nb; i += 32) s.id[i] = values[first + i];
+        __syncwarp();
+        for (int i = lane; i < nb * 4; i += 32) {
+            const int e = i >> 2, q = i & 3;
+            cp_async16(reinterpret_cast<float4*>(&s.hdr[e]) + q, reinterpret_cast<const float4*>(&hdr[s.id[e]]) + q);
+        }
+        for (int i = lane; i < nb * F; i += 32) {
+            const int e = i / F, o = i - e * F;
+            cp_async4(s.tex + i, tex + (size_t)s.id[e] * F + o);
+        }
+        // every lane's copies arrive on the barrier (count 32) when they complete
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+    }
+}
+
+__device__ __forceinline__ bool box_miss(const float4& box, float bx0, float bx1, float by0, float by1) {
+    return box.y < bx0 || box.x > bx1 || box.w < by0 || box.z > by1;
 }
 
 // ---------------------------------------------------------------------------
@@ -98,12 +168,11 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
                                                  const CamConst cc, const RasterConst rc, int n_rt, int B,
                                                  float* __restrict__ out_color, float* __restrict__ out_trans,
                                                  int32_t* __restrict__ out_last) {
-    extern __shared__ float4 smem4[];
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[2];
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
-    ScreenHeader* s_hdr = reinterpret_cast<ScreenHeader*>(smem4);
-    float* s_tex = reinterpret_cast<float*>(s_hdr + B);
-    int* s_id = reinterpret_cast<int*>(s_tex + (size_t)B * F);
+    const bool bulk = (F & 3) == 0;
 
     const int tile = blockIdx.x;
     const int ts = rc.tile_size;
@@ -113,19 +182,45 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
     const int x = tx * ts + lx, y = ty * ts + ly;
     const bool inside = (int)threadIdx.x < ts * ts && x < cc.width && y < cc.height;
     const uint2 range = ranges[tile];
+    const int warp = threadIdx.x >> 5;
+    // this warp's pixel block (as pixel indices)
+    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
+    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], bulk ? 1 : 32);
+        mbar_init(&bars[1], bulk ? 1 : 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
 
     float T = 1.0f;
     float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
     int last = -1;
     bool done = !inside;
-
-    for (uint32_t base = range.x; base < range.y; base += B) {
+    const int total = (int)(range.y - range.x);
+    const int nbatch = (total + B - 1) / B;
+    uint32_t phases = 0u;  // mbarrier parity per buffer (bit b)
+    if (nbatch > 0 && warp == 0)
+        issue_batch(values, hdr, tex, range.x, min(B, total), N, stage_at(smem, 0, B, N), &bars[0]);
+    int bi = 0;
+    for (; bi < nbatch; ++bi) {
+        // all warps finished batch bi-1 (its buffer is free again); stop once every pixel is done
         if (__syncthreads_count(!done) == 0) break;
-        const int nb = (int)min((uint32_t)B, range.y - base);
-        stage_batch<NT>(values, hdr, tex, base, nb, N, s_hdr, s_id, s_tex);
+        const int buf = bi & 1;
+        if (bi + 1 < nbatch && warp == 0) {
+            const int first = (bi + 1) * B;
+            issue_batch(values, hdr, tex, (int64_t)range.x + first, min(B, total - first), N,
+                        stage_at(smem, buf ^ 1, B, N), &bars[buf ^ 1]);
+        }
+        mbar_wait(&bars[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        const Stage s = stage_at(smem, buf, B, N);
+        const int nb = min(B, total - bi * B);
         if (!done) {
             for (int j = 0; j < nb; ++j) {
-                const ScreenHeader h = s_hdr[j];
+                const ScreenHeader h = s.hdr[j];
+                if (box_miss(h.h3, bx0, bx1, by0, by1)) continue;  // warp-uniform
                 float u, v;
                 bool hit;
                 if (MODE == GB_MODE_ORTHO) {
@@ -135,11 +230,10 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
                     hit = eval_uv_pinhole(h, x, y, u, v, pt);
                 }
                 if (!hit) continue;
-                const float alpha_k = h.h1.z;
                 const float G = gauss_weight(u, v);
-                const float alpha = fminf(__fmul_rn(alpha_k, G), kMaxAlphaF);
+                const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);
                 if (alpha < rc.alpha_skip) continue;
-                const float* t = s_tex + (size_t)j * F;
+                const float* t = s.tex + (size_t)j * F;
                 float c0, c1, c2;
                 if (N == 1) {
                     c0 = t[0];
@@ -147,7 +241,7 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
                     c2 = t[2];
                 } else {
                     Bilin b;
-                    bilin_setup<NT>(u, v, N, rc, b);
+                    bilin_setup(u, v, N, rc, b);
                     const float* p00 = t + b.o00;
                     const float* p10 = p00 + 3 * N;
                     c0 = p00[0] * b.w00 + p10[0] * b.w10 + p00[3] * b.w01 + p10[3] * b.w11;
@@ -159,7 +253,7 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
                 acc1 = fmaf(c1, w, acc1);
                 acc2 = fmaf(c2, w, acc2);
                 T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                last = (int)(base - range.x) + j;
+                last = bi * B + j;
                 if (rc.early_stop > 0.0f && T < rc.early_stop) {
                     done = true;
                     break;
@@ -167,6 +261,8 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
             }
         }
     }
+    // after an early exit batch bi was issued but never consumed: drain it before the CTA retires
+    if (bi < nbatch) mbar_wait(&bars[bi & 1], (phases >> (bi & 1)) & 1u);
     if (inside) {
         const size_t p = (size_t)y * cc.width + x;
         out_color[p * 3 + 0] = fmaf(T, cc.bg[0], acc0);
@@ -178,18 +274,44 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
 }
 
 // ---------------------------------------------------------------------------
-// K4 backward
+// warp reduce-scatter: V = 2^M values per lane -> after the call, lane l holds
+// the warp sum of value index (l >> (5 - M)); V - 1 + (5 - M) shuffles.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float warp_sum(float v) {
+template <int V>
+__device__ __forceinline__ float reduce_scatter(float (&a)[V], int lane) {
+    static_assert(V >= 1 && V <= 32 && (V & (V - 1)) == 0, "V must be a power of two <= 32");
+    constexpr int M = V == 1 ? 0 : V == 2 ? 1 : V == 4 ? 2 : V == 8 ? 3 : V == 16 ? 4 : 5;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    return v;
+    for (int k = 0; k < M; ++k) {
+        const int off = 16 >> k;
+        const bool up = (lane & off) != 0;
+        const int S = V >> k;
+#pragma unroll
+        for (int j = 0; j < S / 2; ++j) {
+            const float send = up ? a[j] : a[j + S / 2];
+            const float keep = up ? a[j + S / 2] : a[j];
+            a[j] = keep + __shfl_xor_sync(kFull, send, off);
+        }
+    }
+    float r = a[0];
+#pragma unroll
+    for (int off = 16 >> M; off > 0; off >>= 1) r += __shfl_xor_sync(kFull, r, off);
+    return r;
 }
 
 __device__ __forceinline__ void red_add(float* p, float v) {
     if (v != 0.0f) atomicAdd(p, v);
 }
 
+// texel corner k (0..3 = 00, 10, 01, 11) channel c -> float offset from the base texel
+__device__ __forceinline__ int corner_offset(int i, int N) {
+    const int k = i / 3, c = i - 3 * (i / 3);
+    return ((k & 1) ? 3 * N : 0) + ((k & 2) ? 3 : 0) + c;
+}
+
+// ---------------------------------------------------------------------------
+// K4 backward
+// ---------------------------------------------------------------------------
 template <int MODE, int NT>
 __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ ranges, const int32_t* __restrict__ values,
                                                   const ScreenHeader* __restrict__ hdr, const float* __restrict__ tex,
@@ -198,13 +320,13 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
                                                   const int32_t* __restrict__ in_last,
                                                   const float* __restrict__ image_grad, float* __restrict__ accum,
                                                   float* __restrict__ grid_grad) {
-    extern __shared__ float4 smem4[];
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[2];
     __shared__ int s_maxlast;
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
-    ScreenHeader* s_hdr = reinterpret_cast<ScreenHeader*>(smem4);
-    float* s_tex = reinterpret_cast<float*>(s_hdr + B);
-    int* s_id = reinterpret_cast<int*>(s_tex + (size_t)B * F);
+    const bool bulk = (F & 3) == 0;
+    constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
 
     const int tile = blockIdx.x;
     const int ts = rc.tile_size;
@@ -215,6 +337,9 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
     const bool inside = (int)threadIdx.x < ts * ts && x < cc.width && y < cc.height;
     const uint2 range = ranges[tile];
     const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
+    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
 
     // raster.hpp:313-322: skip pixels with nothing composited or zero cotangent
     int last = -1;
@@ -229,23 +354,45 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
         if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) last = -1;
     }
     float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
-    if (threadIdx.x == 0) s_maxlast = -1;
+    if (threadIdx.x == 0) {
+        s_maxlast = -1;
+        mbar_init(&bars[0], bulk ? 1 : 32);
+        mbar_init(&bars[1], bulk ? 1 : 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     const int wmax = __reduce_max_sync(kFull, last);
     if (lane == 0 && wmax >= 0) atomicMax(&s_maxlast, wmax);
     __syncthreads();
-    const int count = s_maxlast + 1;
+    const int count = s_maxlast + 1;  // entries [0, count) are walked back to front
+    const int wlast = wmax;           // this warp never needs ranks above its own max
     const float sigma = rc.sigma;
-
-    for (int bend = count; bend > 0; bend -= B) {
-        const int bstart = max(0, bend - B);
-        const int nb = bend - bstart;
-        __syncthreads();  // previous batch fully consumed
-        stage_batch<NT>(values, hdr, tex, (int64_t)range.x + bstart, nb, N, s_hdr, s_id, s_tex);
+    const int nbatch = (count + B - 1) / B;
+    uint32_t phases = 0u;
+    // batch q covers ranks [max(0, count - (q+1) B), count - q B)
+    if (nbatch > 0 && warp == 0) {
+        const int f = max(0, count - B);
+        issue_batch(values, hdr, tex, (int64_t)range.x + f, count - f, N, stage_at(smem, 0, B, N), &bars[0]);
+    }
+    for (int q = 0; q < nbatch; ++q) {
+        __syncthreads();  // batch q-1's buffer is free
+        const int buf = q & 1;
+        const int bstart = max(0, count - (q + 1) * B);
+        if (q + 1 < nbatch && warp == 0) {
+            const int f = max(0, count - (q + 2) * B);
+            issue_batch(values, hdr, tex, (int64_t)range.x + f, bstart - f, N, stage_at(smem, buf ^ 1, B, N),
+                        &bars[buf ^ 1]);
+        }
+        mbar_wait(&bars[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        const Stage s = stage_at(smem, buf, B, N);
+        const int nb = count - q * B - bstart;
         for (int j = nb - 1; j >= 0; --j) {
             const int rank = bstart + j;
+            if (rank > wlast) continue;  // warp-uniform
+            const ScreenHeader h = s.hdr[j];
+            if (box_miss(h.h3, bx0, bx1, by0, by1)) continue;  // warp-uniform
             bool on = rank <= last;
-            const ScreenHeader h = s_hdr[j];
             float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
             PinholeTerms pt;
             if (on) {
@@ -256,9 +403,8 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
                     hit = eval_uv_pinhole(h, x, y, u, v, pt);
                 }
                 if (hit) {
-                    const float alpha_k = h.h1.z;
                     G = gauss_weight(u, v);
-                    araw = __fmul_rn(alpha_k, G);
+                    araw = __fmul_rn(h.h1.z, G);
                     alpha = fminf(araw, kMaxAlphaF);
                     on = !(alpha < rc.alpha_skip);
                 } else {
@@ -268,16 +414,17 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
             const unsigned act = __ballot_sync(kFull, on);
             if (act == 0) continue;
 
-            float sg[10];
+            // red[0..NS): screen-space sums; red[16..28): texel contributions of the first group
+            float red[32];
 #pragma unroll
-            for (int i = 0; i < 10; ++i) sg[i] = 0.0f;
+            for (int i = 0; i < 32; ++i) red[i] = 0.0f;
             float tg[12];
 #pragma unroll
             for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
             int tbase = -1;
             if (on) {
                 T = __fdiv_rn(T, __fsub_rn(1.0f, alpha));  // raster.hpp:333
-                const float* t = s_tex + (size_t)j * F;
+                const float* t = s.tex + (size_t)j * F;
                 float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
                 const float aT = alpha * T;
                 const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
@@ -291,7 +438,7 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
                     tbase = 0;
                 } else {
                     Bilin b;
-                    bilin_setup<NT>(u, v, N, rc, b);
+                    bilin_setup(u, v, N, rc, b);
                     const float* p00 = t + b.o00;
                     const float* p10 = p00 + 3 * N;
                     const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
@@ -327,27 +474,27 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
                     v_hat -= aa * v;
                 }
                 if (MODE == GB_MODE_ORTHO) {
-                    sg[0] = u_hat;
-                    sg[1] = v_hat;
-                    sg[2] = u_hat * v;
-                    sg[3] = v_hat * u;
-                    sg[4] = u_hat * u;
-                    sg[5] = v_hat * v;
-                    sg[6] = op;
+                    red[0] = u_hat;
+                    red[1] = v_hat;
+                    red[2] = u_hat * v;
+                    red[3] = v_hat * u;
+                    red[4] = u_hat * u;
+                    red[5] = v_hat * v;
+                    red[6] = op;
                 } else {
                     // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
                     const float iz = 1.0f / pt.cz;
                     const float gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
-                    sg[0] = gc0;
-                    sg[1] = gc1;
-                    sg[2] = gc2;
-                    sg[3] = pt.dx * gc0;
-                    sg[4] = pt.dx * gc1;
-                    sg[5] = pt.dx * gc2;
-                    sg[6] = pt.dy * gc0;
-                    sg[7] = pt.dy * gc1;
-                    sg[8] = pt.dy * gc2;
-                    sg[9] = op;
+                    red[0] = gc0;
+                    red[1] = gc1;
+                    red[2] = gc2;
+                    red[3] = pt.dx * gc0;
+                    red[4] = pt.dx * gc1;
+                    red[5] = pt.dx * gc2;
+                    red[6] = pt.dy * gc0;
+                    red[7] = pt.dy * gc1;
+                    red[8] = pt.dy * gc2;
+                    red[9] = op;
                 }
                 // raster.hpp:362
                 const float om = 1.0f - alpha;
@@ -355,50 +502,38 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
                 bh1 = alpha * c1 + om * bh1;
                 bh2 = alpha * c2 + om * bh2;
             }
-            const int id = s_id[j];
-            // screen-space sums -> accum (one vector red per 4 floats)
-            constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;
-#pragma unroll
-            for (int i = 0; i < NS; ++i) sg[i] = warp_sum(sg[i]);
-            if (lane == 0) {
-                float4* a4 = reinterpret_cast<float4*>(accum + (size_t)id * kAccumStride);
-                atomicAdd(&a4[0], make_float4(sg[0], sg[1], sg[2], sg[3]));
-                atomicAdd(&a4[1], make_float4(sg[4], sg[5], sg[6], MODE == GB_MODE_ORTHO ? 0.0f : sg[7]));
-                if (MODE != GB_MODE_ORTHO) atomicAdd(reinterpret_cast<float2*>(&a4[2]), make_float2(sg[8], sg[9]));
-            }
-            // texel gradients: one warp reduction per distinct bilinear base
+            const int id = s.id[j];
             float* gg = grid_grad + (size_t)id * F;
-            unsigned pending = act;
-            while (pending) {
-                const int leader = __ffs(pending) - 1;
-                const int b = __shfl_sync(kFull, tbase, leader);
-                const bool mine = on && tbase == b;
-                pending &= ~__ballot_sync(kFull, mine);
-                if (N == 1) {
-                    float s0 = warp_sum(mine ? tg[0] : 0.0f);
-                    float s1 = warp_sum(mine ? tg[1] : 0.0f);
-                    float s2 = warp_sum(mine ? tg[2] : 0.0f);
-                    if (lane == leader) {
-                        red_add(gg + 0, s0);
-                        red_add(gg + 1, s1);
-                        red_add(gg + 2, s2);
-                    }
-                } else {
-                    float s[12];
+            float* acc = accum + (size_t)id * kAccumStride;
+            // first texel group rides along with the screen-space sums in one 32-value reduce-scatter
+            int leader = __ffs(act) - 1;
+            int b0 = __shfl_sync(kFull, tbase, leader);
+            bool mine = on && tbase == b0;
+            unsigned pending = act & ~__ballot_sync(kFull, mine);
+            if (mine) {
 #pragma unroll
-                    for (int i = 0; i < 12; ++i) s[i] = warp_sum(mine ? tg[i] : 0.0f);
-                    if (lane == leader) {
-                        float* p00 = gg + b;
-                        float* p10 = p00 + 3 * N;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            red_add(p00 + c, s[c]);
-                            red_add(p10 + c, s[3 + c]);
-                            red_add(p00 + 3 + c, s[6 + c]);
-                            red_add(p10 + 3 + c, s[9 + c]);
-                        }
-                    }
+                for (int i = 0; i < 12; ++i) red[16 + i] = tg[i];
+            }
+            {
+                const float r = reduce_scatter<32>(red, lane);  // lane l owns value l
+                if (lane < NS) red_add(acc + lane, r);
+                else if (lane >= 16 && lane < 28) {
+                    const int i = lane - 16;
+                    if (N > 1 || i < 3) red_add(gg + b0 + corner_offset(i, N), r);
                 }
+            }
+            while (pending) {  // further distinct bilinear cells in this warp
+                leader = __ffs(pending) - 1;
+                b0 = __shfl_sync(kFull, tbase, leader);
+                mine = on && tbase == b0;
+                pending &= ~__ballot_sync(kFull, mine);
+                float t16[16];
+#pragma unroll
+                for (int i = 0; i < 12; ++i) t16[i] = mine ? tg[i] : 0.0f;
+#pragma unroll
+                for (int i = 12; i < 16; ++i) t16[i] = 0.0f;
+                const float r = reduce_scatter<16>(t16, lane);  // lane l owns value l >> 1
+                if ((lane & 1) == 0 && lane < 24) red_add(gg + b0 + corner_offset(lane >> 1, N), r);
             }
         }
     }
@@ -407,13 +542,12 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-int pick_batch(int N, int tile_threads) {
-    const size_t per = batch_smem_bytes(1, N);
-    int B = (int)(49152 / per);
-    if (B > 256) B = 256;
-    B &= ~3;  // keep the smem carve-up 16 B aligned
+int pick_batch(int N) {
+    // two staging buffers within ~48 KB keeps 4+ CTAs of 256 threads resident per SM
+    const size_t per = stage_bytes(1, N);
+    int B = (int)(24576 / per);
+    if (B > 128) B = 128;
     if (B < 4) B = 4;
-    (void)tile_threads;
     return B;
 }
 
@@ -460,8 +594,8 @@ cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* rang
                            float* color, float* trans, int32_t* last, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
     const int threads = ((ts * ts + 31) / 32) * 32;
-    const int B = pick_batch(n, threads);
-    const size_t smem = batch_smem_bytes(B, n);
+    const int B = pick_batch(n);
+    const size_t smem = 2 * stage_bytes(B, n);
     if (mode == GB_MODE_ORTHO) {
         GB_DISPATCH_N(fwd_t, GB_MODE_ORTHO, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B, color,
                       trans, last)
@@ -477,8 +611,8 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
                             float* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
     const int threads = ((ts * ts + 31) / 32) * 32;
-    const int B = pick_batch(n, threads);
-    const size_t smem = batch_smem_bytes(B, n);
+    const int B = pick_batch(n);
+    const size_t smem = 2 * stage_bytes(B, n);
     if (mode == GB_MODE_ORTHO) {
         GB_DISPATCH_N(bwd_t, GB_MODE_ORTHO, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B, trans,
                       last, image_grad, accum, grid_grad)

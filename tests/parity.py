@@ -27,9 +27,9 @@ RTOL = 1e-4  # north_star tolerance (fp32)
 ATOL = 1e-5
 EPS32 = 2.0 ** -24
 MODEL_C = 64.0  # error-model multiple of eps32*mag
-# rtol is attainable in fp32 only where the sum does not cancel by more than ~1/(rtol*16 eps32):
-# entries with sum|terms| > CANCEL_MAX*|ref| are judged by the error model alone (and counted).
-CANCEL_MAX = 1000.0
+# rtol is attainable in fp32 only where the sum does not cancel by more than rtol/(MODEL_C eps32)
+# (~26): entries with sum|terms| > CANCEL_MAX*|ref| are judged by the error model alone (and counted).
+CANCEL_MAX = RTOL / (MODEL_C * EPS32)
 
 GRAD_FIELDS = ("position", "theta", "quat", "log_scale", "opacity_logit", "grid")
 
