@@ -159,67 +159,119 @@ __device__ __forceinline__ bool box_miss(const float4& box, float bx0, float bx1
     return box.y < bx0 || box.x > bx1 || box.w < by0 || box.z > by1;
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised staging pipeline shared by K3/K4.
+//   warp `cw` (the last warp; cw = number of consumer warps) is the producer:
+//   for each batch r it waits until every consumer released stage r % S
+//   (empty[s]) and issues the batch's bulk copies completing on full[s];
+//   consumer warps wait full[s], composite, arrive empty[s].  Consumers never
+//   meet at a CTA barrier, so a warp with little work runs up to S-1 batches
+//   ahead instead of idling at a per-batch __syncthreads.  Warps stay in the
+//   pipeline until the last batch (no phase is ever skipped); once every
+//   consumer has finished early (forward), the producer stops copying and just
+//   completes the remaining full[] phases so the finished warps drain through.
+// ---------------------------------------------------------------------------
+constexpr int kStages = 4;
+
+struct Pipe {
+    uint64_t full[kStages];
+    uint64_t empty[kStages];
+    int active;  // consumer warps still compositing (forward early termination)
+};
+
+__device__ __forceinline__ void pipe_init(Pipe& p, int consumers, bool bulk) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&p.full[s], bulk ? 1 : 32);
+            mbar_init(&p.empty[s], consumers);
+        }
+        p.active = consumers;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+}
+
+// Producer loop over `nbatch` batches; batch r covers list entries
+// [first(r), first(r) + count(r)) relative to the tile's range start.
+template <typename FirstFn>
+__device__ __forceinline__ void produce(Pipe& p, const int32_t* __restrict__ values,
+                                        const ScreenHeader* __restrict__ hdr, const float* __restrict__ tex,
+                                        int64_t base, int nbatch, int B, int N, unsigned char* smem, FirstFn span) {
+    const bool bulk = ((3 * N * N) & 3) == 0;
+    const int lane = threadIdx.x & 31;
+    for (int r = 0; r < nbatch; ++r) {
+        const int s = r % kStages;
+        if (r >= kStages) mbar_wait(&p.empty[s], ((r / kStages) - 1) & 1);
+        if (*(volatile int*)&p.active == 0) {  // nobody needs the data: complete the phase without copies
+            if (!bulk || lane == 0) mbar_arrive(&p.full[s]);
+            continue;
+        }
+        int first, cnt;
+        span(r, first, cnt);
+        issue_batch(values, hdr, tex, base + first, cnt, N, stage_at(smem, s, B, N), &p.full[s]);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3 forward
 // ---------------------------------------------------------------------------
 template <int MODE, int NT>
-__global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ ranges, const int32_t* __restrict__ values,
+__global__ void __launch_bounds__(288) k_forward(const uint2* __restrict__ ranges, const int32_t* __restrict__ values,
                                                  const ScreenHeader* __restrict__ hdr, const float* __restrict__ tex,
                                                  const CamConst cc, const RasterConst rc, int n_rt, int B,
                                                  float* __restrict__ out_color, float* __restrict__ out_trans,
                                                  int32_t* __restrict__ out_last) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) Pipe pipe;
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
-    const bool bulk = (F & 3) == 0;
-
-    const int tile = blockIdx.x;
     const int ts = rc.tile_size;
+    const int consumers = (ts * ts + 31) >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x;
+    const uint2 range = ranges[tile];
+    const int total = (int)(range.y - range.x);
+    const int nbatch = (total + B - 1) / B;
+    pipe_init(pipe, consumers, (F & 3) == 0);
+    __syncthreads();
+
+    if (warp == consumers) {  // producer warp
+        produce(pipe, values, hdr, tex, range.x, nbatch, B, N, smem, [&](int r, int& first, int& cnt) {
+            first = r * B;
+            cnt = min(B, total - first);
+        });
+        return;
+    }
+
     const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
     int lx, ly;
     tile_pixel(threadIdx.x, ts, lx, ly);
     const int x = tx * ts + lx, y = ty * ts + ly;
     const bool inside = (int)threadIdx.x < ts * ts && x < cc.width && y < cc.height;
-    const uint2 range = ranges[tile];
-    const int warp = threadIdx.x >> 5;
     // this warp's pixel block (as pixel indices)
     const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
     const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
-
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], bulk ? 1 : 32);
-        mbar_init(&bars[1], bulk ? 1 : 32);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
 
     float T = 1.0f;
     float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
     int last = -1;
     bool done = !inside;
-    const int total = (int)(range.y - range.x);
-    const int nbatch = (total + B - 1) / B;
-    uint32_t phases = 0u;  // mbarrier parity per buffer (bit b)
-    if (nbatch > 0 && warp == 0)
-        issue_batch(values, hdr, tex, range.x, min(B, total), N, stage_at(smem, 0, B, N), &bars[0]);
-    int bi = 0;
-    for (; bi < nbatch; ++bi) {
-        // all warps finished batch bi-1 (its buffer is free again); stop once every pixel is done
-        if (__syncthreads_count(!done) == 0) break;
-        const int buf = bi & 1;
-        if (bi + 1 < nbatch && warp == 0) {
-            const int first = (bi + 1) * B;
-            issue_batch(values, hdr, tex, (int64_t)range.x + first, min(B, total - first), N,
-                        stage_at(smem, buf ^ 1, B, N), &bars[buf ^ 1]);
+    bool warp_done = false;
+    for (int r = 0; r < nbatch; ++r) {
+        const int s = r % kStages;
+        if (!warp_done && __all_sync(kFull, done)) {  // every pixel of this warp terminated early
+            warp_done = true;
+            if (lane == 0) atomicSub(&pipe.active, 1);
         }
-        mbar_wait(&bars[buf], (phases >> buf) & 1u);
-        phases ^= 1u << buf;
-        const Stage s = stage_at(smem, buf, B, N);
-        const int nb = min(B, total - bi * B);
-        if (!done) {
+        mbar_wait(&pipe.full[s], (r / kStages) & 1);
+        const Stage st = stage_at(smem, s, B, N);
+        const int nb = min(B, total - r * B);
+        if (!warp_done && !done) {
             for (int j = 0; j < nb; ++j) {
-                const ScreenHeader h = s.hdr[j];
+                const ScreenHeader h = st.hdr[j];
                 if (box_miss(h.h3, bx0, bx1, by0, by1)) continue;  // warp-uniform
                 float u, v;
                 bool hit;
@@ -233,7 +285,7 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
                 const float G = gauss_weight(u, v);
                 const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);
                 if (alpha < rc.alpha_skip) continue;
-                const float* t = s.tex + (size_t)j * F;
+                const float* t = st.tex + (size_t)j * F;
                 float c0, c1, c2;
                 if (N == 1) {
                     c0 = t[0];
@@ -253,16 +305,16 @@ __global__ void __launch_bounds__(256) k_forward(const uint2* __restrict__ range
                 acc1 = fmaf(c1, w, acc1);
                 acc2 = fmaf(c2, w, acc2);
                 T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                last = bi * B + j;
+                last = r * B + j;
                 if (rc.early_stop > 0.0f && T < rc.early_stop) {
                     done = true;
                     break;
                 }
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pipe.empty[s]);
     }
-    // after an early exit batch bi was issued but never consumed: drain it before the CTA retires
-    if (bi < nbatch) mbar_wait(&bars[bi & 1], (phases >> (bi & 1)) & 1u);
     if (inside) {
         const size_t p = (size_t)y * cc.width + x;
         out_color[p * 3 + 0] = fmaf(T, cc.bg[0], acc0);
@@ -313,7 +365,7 @@ __device__ __forceinline__ int corner_offset(int i, int N) {
 // K4 backward
 // ---------------------------------------------------------------------------
 template <int MODE, int NT>
-__global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ ranges, const int32_t* __restrict__ values,
+__global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ ranges, const int32_t* __restrict__ values,
                                                   const ScreenHeader* __restrict__ hdr, const float* __restrict__ tex,
                                                   const CamConst cc, const RasterConst rc, int n_rt, int B,
                                                   const float* __restrict__ in_trans,
@@ -321,15 +373,14 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
                                                   const float* __restrict__ image_grad, float* __restrict__ accum,
                                                   float* __restrict__ grid_grad) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) Pipe pipe;
     __shared__ int s_maxlast;
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
-    const bool bulk = (F & 3) == 0;
     constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
-
-    const int tile = blockIdx.x;
     const int ts = rc.tile_size;
+    const int consumers = (ts * ts + 31) >> 5;
+    const int tile = blockIdx.x;
     const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
     int lx, ly;
     tile_pixel(threadIdx.x, ts, lx, ly);
@@ -338,8 +389,6 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
     const uint2 range = ranges[tile];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
-    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
 
     // raster.hpp:313-322: skip pixels with nothing composited or zero cotangent
     int last = -1;
@@ -353,44 +402,39 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
         T = in_trans[p];
         if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) last = -1;
     }
-    float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
-    if (threadIdx.x == 0) {
-        s_maxlast = -1;
-        mbar_init(&bars[0], bulk ? 1 : 32);
-        mbar_init(&bars[1], bulk ? 1 : 32);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    if (threadIdx.x == 0) s_maxlast = -1;
+    pipe_init(pipe, consumers, (F & 3) == 0);
     __syncthreads();
     const int wmax = __reduce_max_sync(kFull, last);
     if (lane == 0 && wmax >= 0) atomicMax(&s_maxlast, wmax);
     __syncthreads();
     const int count = s_maxlast + 1;  // entries [0, count) are walked back to front
-    const int wlast = wmax;           // this warp never needs ranks above its own max
-    const float sigma = rc.sigma;
     const int nbatch = (count + B - 1) / B;
-    uint32_t phases = 0u;
-    // batch q covers ranks [max(0, count - (q+1) B), count - q B)
-    if (nbatch > 0 && warp == 0) {
-        const int f = max(0, count - B);
-        issue_batch(values, hdr, tex, (int64_t)range.x + f, count - f, N, stage_at(smem, 0, B, N), &bars[0]);
+    // batch r covers ranks [max(0, count - (r+1) B), count - r B)
+
+    if (warp == consumers) {  // producer warp
+        produce(pipe, values, hdr, tex, range.x, nbatch, B, N, smem, [&](int r, int& first, int& cnt) {
+            first = max(0, count - (r + 1) * B);
+            cnt = count - r * B - first;
+        });
+        return;
     }
-    for (int q = 0; q < nbatch; ++q) {
-        __syncthreads();  // batch q-1's buffer is free
-        const int buf = q & 1;
-        const int bstart = max(0, count - (q + 1) * B);
-        if (q + 1 < nbatch && warp == 0) {
-            const int f = max(0, count - (q + 2) * B);
-            issue_batch(values, hdr, tex, (int64_t)range.x + f, bstart - f, N, stage_at(smem, buf ^ 1, B, N),
-                        &bars[buf ^ 1]);
-        }
-        mbar_wait(&bars[buf], (phases >> buf) & 1u);
-        phases ^= 1u << buf;
-        const Stage s = stage_at(smem, buf, B, N);
-        const int nb = count - q * B - bstart;
-        for (int j = nb - 1; j >= 0; --j) {
+
+    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
+    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
+    const int wlast = wmax;  // this warp never needs ranks above its own max
+    float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
+    const float sigma = rc.sigma;
+
+    for (int r = 0; r < nbatch; ++r) {
+        const int s = r % kStages;
+        const int bstart = max(0, count - (r + 1) * B);
+        const int nb = count - r * B - bstart;
+        mbar_wait(&pipe.full[s], (r / kStages) & 1);
+        const Stage st = stage_at(smem, s, B, N);
+        for (int j = min(nb - 1, wlast - bstart); j >= 0; --j) {
             const int rank = bstart + j;
-            if (rank > wlast) continue;  // warp-uniform
-            const ScreenHeader h = s.hdr[j];
+            const ScreenHeader h = st.hdr[j];
             if (box_miss(h.h3, bx0, bx1, by0, by1)) continue;  // warp-uniform
             bool on = rank <= last;
             float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
@@ -414,17 +458,16 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
             const unsigned act = __ballot_sync(kFull, on);
             if (act == 0) continue;
 
-            // red[0..NS): screen-space sums; red[16..28): texel contributions of the first group
-            float red[32];
+            float red[16];  // screen-space sums (NS of 16 slots)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) red[i] = 0.0f;
+            for (int i = 0; i < 16; ++i) red[i] = 0.0f;
             float tg[12];
 #pragma unroll
             for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
             int tbase = -1;
             if (on) {
                 T = __fdiv_rn(T, __fsub_rn(1.0f, alpha));  // raster.hpp:333
-                const float* t = s.tex + (size_t)j * F;
+                const float* t = st.tex + (size_t)j * F;
                 float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
                 const float aT = alpha * T;
                 const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
@@ -502,40 +545,31 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
                 bh1 = alpha * c1 + om * bh1;
                 bh2 = alpha * c2 + om * bh2;
             }
-            const int id = s.id[j];
+            const int id = st.id[j];
+            {  // screen-space sums: lane l owns value l >> 1
+                const float r2 = reduce_scatter<16>(red, lane);
+                if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
+            }
+            // texel gradients: one 16-value reduce-scatter per distinct bilinear cell in the warp
             float* gg = grid_grad + (size_t)id * F;
-            float* acc = accum + (size_t)id * kAccumStride;
-            // first texel group rides along with the screen-space sums in one 32-value reduce-scatter
-            int leader = __ffs(act) - 1;
-            int b0 = __shfl_sync(kFull, tbase, leader);
-            bool mine = on && tbase == b0;
-            unsigned pending = act & ~__ballot_sync(kFull, mine);
-            if (mine) {
-#pragma unroll
-                for (int i = 0; i < 12; ++i) red[16 + i] = tg[i];
-            }
-            {
-                const float r = reduce_scatter<32>(red, lane);  // lane l owns value l
-                if (lane < NS) red_add(acc + lane, r);
-                else if (lane >= 16 && lane < 28) {
-                    const int i = lane - 16;
-                    if (N > 1 || i < 3) red_add(gg + b0 + corner_offset(i, N), r);
-                }
-            }
-            while (pending) {  // further distinct bilinear cells in this warp
-                leader = __ffs(pending) - 1;
-                b0 = __shfl_sync(kFull, tbase, leader);
-                mine = on && tbase == b0;
+            unsigned pending = act;
+            while (pending) {
+                const int leader = __ffs(pending) - 1;
+                const int b0 = __shfl_sync(kFull, tbase, leader);
+                const bool mine = on && tbase == b0;
                 pending &= ~__ballot_sync(kFull, mine);
                 float t16[16];
 #pragma unroll
                 for (int i = 0; i < 12; ++i) t16[i] = mine ? tg[i] : 0.0f;
 #pragma unroll
                 for (int i = 12; i < 16; ++i) t16[i] = 0.0f;
-                const float r = reduce_scatter<16>(t16, lane);  // lane l owns value l >> 1
-                if ((lane & 1) == 0 && lane < 24) red_add(gg + b0 + corner_offset(lane >> 1, N), r);
+                const float r2 = reduce_scatter<16>(t16, lane);  // lane l owns value l >> 1
+                if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
+                    red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pipe.empty[s]);
     }
 }
 
@@ -543,11 +577,11 @@ __global__ void __launch_bounds__(256) k_backward(const uint2* __restrict__ rang
 // host launchers
 // ---------------------------------------------------------------------------
 int pick_batch(int N) {
-    // two staging buffers within ~48 KB keeps 4+ CTAs of 256 threads resident per SM
+    // kStages staging buffers within ~52 KB keeps 4 CTAs resident per SM
     const size_t per = stage_bytes(1, N);
-    int B = (int)(24576 / per);
-    if (B > 128) B = 128;
-    if (B < 4) B = 4;
+    int B = (int)(13312 / per);
+    if (B > 64) B = 64;
+    if (B < 2) B = 2;
     return B;
 }
 
@@ -593,9 +627,9 @@ cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* rang
                            const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
                            float* color, float* trans, int32_t* last, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
-    const int threads = ((ts * ts + 31) / 32) * 32;
+    const int threads = ((ts * ts + 31) / 32) * 32 + 32;  // + the producer warp
     const int B = pick_batch(n);
-    const size_t smem = 2 * stage_bytes(B, n);
+    const size_t smem = kStages * stage_bytes(B, n);
     if (mode == GB_MODE_ORTHO) {
         GB_DISPATCH_N(fwd_t, GB_MODE_ORTHO, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B, color,
                       trans, last)
@@ -610,9 +644,9 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
                             const float* trans, const int32_t* last, const float* image_grad, float* accum,
                             float* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
-    const int threads = ((ts * ts + 31) / 32) * 32;
+    const int threads = ((ts * ts + 31) / 32) * 32 + 32;  // + the producer warp
     const int B = pick_batch(n);
-    const size_t smem = 2 * stage_bytes(B, n);
+    const size_t smem = kStages * stage_bytes(B, n);
     if (mode == GB_MODE_ORTHO) {
         GB_DISPATCH_N(bwd_t, GB_MODE_ORTHO, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B, trans,
                       last, image_grad, accum, grid_grad)
