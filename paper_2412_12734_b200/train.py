@@ -31,6 +31,13 @@ def shard_views(n_views: int, rank: int, world: int, per_rank: Optional[int] = N
     return list(range(lo, hi))
 
 
+def reduce_gradients(grads: GradientBuffer, process_group=None) -> None:
+    """The step's one collective: sum the flat gradient buffer over all ranks (NCCL on GPUs)."""
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        if torch.distributed.get_world_size(process_group) > 1:
+            torch.distributed.all_reduce(grads.flat, op=torch.distributed.ReduceOp.SUM, group=process_group)
+
+
 class ViewShardedTrainer:
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False):
@@ -75,9 +82,7 @@ class ViewShardedTrainer:
         render_backward(self.splats, cam, self.binning, out, gimg, self.grads)
 
     def _finish(self) -> None:
-        if self.pg is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
-            if torch.distributed.get_world_size(self.pg) > 1:
-                torch.distributed.all_reduce(self.grads.flat, op=torch.distributed.ReduceOp.SUM, group=self.pg)
+        reduce_gradients(self.grads, self.pg)
         adam_step(self.splats, self.grads, self.state, self.lrs, check_finite=self.check_finite)
 
     def step(self, targets: Sequence[torch.Tensor]) -> torch.Tensor:
