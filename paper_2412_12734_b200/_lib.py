@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgb_raster.so")
+LIB_PATH = os.environ.get("GB_LIB_PATH") or os.path.join(_HERE, "libgb_raster.so")  # override: debug builds only
 
 GB_OK = 0
 GB_INVALID_ARGUMENT = 1

@@ -26,6 +26,23 @@ namespace gb {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+#ifdef GB_DEBUG_COUNTERS
+// development counters (not built by default): [0] warp-entries tested, [1] passing the box,
+// [2] with an active lane, [3] active lanes, [4] texel groups, [5] corner-only groups
+__device__ unsigned long long g_dbg[8];
+#define GB_DBG(i, v) atomicAdd(&g_dbg[i], (unsigned long long)(v))
+extern "C" __attribute__((visibility("default"))) int gb_debug_counters(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_dbg, sizeof(g_dbg));
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+    }
+    return 0;
+}
+#else
+#define GB_DBG(i, v)
+#endif
+
 template <int NT>
 __device__ __forceinline__ int tex_n(int n_rt) {
     return NT ? NT : n_rt;
@@ -80,6 +97,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+
+// producer-side wait: sleep between polls so the spinning warp does not take
+// issue slots from the consumer warps
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2; selp.u32 %0, 1, 0, P1; }"
+                 : "=r"(done)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+    while (!done) {
+        __nanosleep(64);
+        asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2; selp.u32 %0, 1, 0, P1; }"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+    }
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -204,7 +238,7 @@ __device__ __forceinline__ void produce(Pipe& p, const int32_t* __restrict__ val
     const int lane = threadIdx.x & 31;
     for (int r = 0; r < nbatch; ++r) {
         const int s = r % kStages;
-        if (r >= kStages) mbar_wait(&p.empty[s], ((r / kStages) - 1) & 1);
+        if (r >= kStages) mbar_wait_backoff(&p.empty[s], ((r / kStages) - 1) & 1);
         if (*(volatile int*)&p.active == 0) {  // nobody needs the data: complete the phase without copies
             if (!bulk || lane == 0) mbar_arrive(&p.full[s]);
             continue;
@@ -351,8 +385,43 @@ __device__ __forceinline__ float reduce_scatter(float (&a)[V], int lane) {
     return r;
 }
 
+// Warp sum of NV <= 16 per-lane values through a per-warp shared-memory
+// transpose (scratch: kRedRows x kRedStride floats): lane l writes value i
+// to row i, column l; lane l then sums half (l & 1) of row l >> 1 with four
+// conflict-free 128-bit loads and one shuffle.  ~NV + 22 instructions
+// versus ~4 NV for a shuffle butterfly.  Returns the row l >> 1 total.
+constexpr int kRedRows = 16;
+constexpr int kRedStride = 36;  // 32 lanes + 4 pad: rows land in distinct bank quads
+
+template <int NV>
+__device__ __forceinline__ float smem_reduce(const float (&v)[NV], float* scratch, int lane) {
+    __syncwarp();  // previous readers of the scratch are done
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[i * kRedStride + lane] = v[i];
+    __syncwarp();
+    const int row = lane >> 1;
+    float acc = 0.0f;
+    if (row < NV) {
+        const float4* q = reinterpret_cast<const float4*>(scratch + row * kRedStride + (lane & 1) * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float4 a = q[k];
+            acc += (a.x + a.y) + (a.z + a.w);
+        }
+    }
+    return acc + __shfl_xor_sync(kFull, acc, 1);
+}
+
 __device__ __forceinline__ void red_add(float* p, float v) {
     if (v != 0.0f) atomicAdd(p, v);
+}
+
+// p[0..2] += (a, b, c) with one 8-byte vector red and one scalar red (branch-free on alignment)
+__device__ __forceinline__ void red3(float* p, float a, float b, float c) {
+    const bool even = (reinterpret_cast<uintptr_t>(p) & 7) == 0;
+    float2* pv = reinterpret_cast<float2*>(even ? p : p + 1);
+    atomicAdd(pv, even ? make_float2(a, b) : make_float2(b, c));
+    atomicAdd(even ? p + 2 : p, even ? c : a);
 }
 
 // texel corner k (0..3 = 00, 10, 01, 11) channel c -> float offset from the base texel
@@ -423,6 +492,8 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
     const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
     const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
     const int wlast = wmax;  // this warp never needs ranks above its own max
+    // per-warp reduction scratch after the staging ring
+    float* wscratch = reinterpret_cast<float*>(smem + kStages * stage_bytes(B, N)) + warp * kRedRows * kRedStride;
     float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
     const float sigma = rc.sigma;
 
@@ -435,7 +506,9 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
         for (int j = min(nb - 1, wlast - bstart); j >= 0; --j) {
             const int rank = bstart + j;
             const ScreenHeader h = st.hdr[j];
+            if (lane == 0) GB_DBG(0, 1);
             if (box_miss(h.h3, bx0, bx1, by0, by1)) continue;  // warp-uniform
+            if (lane == 0) GB_DBG(1, 1);
             bool on = rank <= last;
             float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
             PinholeTerms pt;
@@ -457,6 +530,7 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
             }
             const unsigned act = __ballot_sync(kFull, on);
             if (act == 0) continue;
+            if (lane == 0) { GB_DBG(2, 1); GB_DBG(3, __popc(act)); }
 
             float red[16];  // screen-space sums (NS of 16 slots)
 #pragma unroll
@@ -547,25 +621,32 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
             }
             const int id = st.id[j];
             {  // screen-space sums: lane l owns value l >> 1
-                const float r2 = reduce_scatter<16>(red, lane);
+                float sv[NS];
+#pragma unroll
+                for (int i = 0; i < NS; ++i) sv[i] = red[i];
+                const float r2 = smem_reduce<NS>(sv, wscratch, lane);
                 if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
             }
-            // texel gradients: one 16-value reduce-scatter per distinct bilinear cell in the warp
+            // texel gradients: one warp reduction when every active lane shares a bilinear cell;
+            // otherwise each lane adds its (at most four) non-zero texels straight to HBM with
+            // one float2 + one float red per texel -- cheaper than a reduction per distinct cell
             float* gg = grid_grad + (size_t)id * F;
-            unsigned pending = act;
-            while (pending) {
-                const int leader = __ffs(pending) - 1;
-                const int b0 = __shfl_sync(kFull, tbase, leader);
-                const bool mine = on && tbase == b0;
-                pending &= ~__ballot_sync(kFull, mine);
-                float t16[16];
-#pragma unroll
-                for (int i = 0; i < 12; ++i) t16[i] = mine ? tg[i] : 0.0f;
-#pragma unroll
-                for (int i = 12; i < 16; ++i) t16[i] = 0.0f;
-                const float r2 = reduce_scatter<16>(t16, lane);  // lane l owns value l >> 1
+            const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
+            if (__all_sync(kFull, !on || tbase == b0)) {
+                if (lane == 0) GB_DBG(4, 1);
+                const float r2 = smem_reduce<12>(tg, wscratch, lane);
                 if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
                     red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
+            } else if (on) {
+                if (lane == 0) GB_DBG(5, 1);
+                if (N == 1) {
+                    red3(gg, tg[0], tg[1], tg[2]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (tg[3 * k] != 0.0f || tg[3 * k + 1] != 0.0f || tg[3 * k + 2] != 0.0f)
+                            red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
+                }
             }
         }
         __syncwarp();
@@ -576,10 +657,10 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-int pick_batch(int N) {
-    // kStages staging buffers within ~52 KB keeps 4 CTAs resident per SM
+int pick_batch(int N, int stage_budget = 13312) {
+    // kStages staging buffers within ~52 KB (K3) / ~37 KB + reduction scratch (K4) keep 4 CTAs per SM
     const size_t per = stage_bytes(1, N);
-    int B = (int)(13312 / per);
+    int B = (int)(stage_budget / per);
     if (B > 64) B = 64;
     if (B < 2) B = 2;
     return B;
@@ -645,8 +726,8 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
                             float* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
     const int threads = ((ts * ts + 31) / 32) * 32 + 32;  // + the producer warp
-    const int B = pick_batch(n);
-    const size_t smem = kStages * stage_bytes(B, n);
+    const int B = pick_batch(n, 9216);
+    const size_t smem = kStages * stage_bytes(B, n) + (size_t)(threads / 32 - 1) * kRedRows * kRedStride * 4;
     if (mode == GB_MODE_ORTHO) {
         GB_DISPATCH_N(bwd_t, GB_MODE_ORTHO, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B, trans,
                       last, image_grad, accum, grid_grad)
