@@ -87,33 +87,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// Blocking wait on an mbarrier phase.  try_wait with a suspend-time hint lets
+// the hardware park the warp until the phase flips instead of spinning on
+// issue slots the compositing warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)
         : "memory");
-}
-
-// producer-side wait: sleep between polls so the spinning warp does not take
-// issue slots from the consumer warps
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2; selp.u32 %0, 1, 0, P1; }"
-                 : "=r"(done)
-                 : "r"(smem_u32(bar)), "r"(parity)
-                 : "memory");
-    while (!done) {
-        __nanosleep(64);
-        asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2; selp.u32 %0, 1, 0, P1; }"
-                     : "=r"(done)
-                     : "r"(smem_u32(bar)), "r"(parity)
-                     : "memory");
-    }
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -238,7 +224,7 @@ __device__ __forceinline__ void produce(Pipe& p, const int32_t* __restrict__ val
     const int lane = threadIdx.x & 31;
     for (int r = 0; r < nbatch; ++r) {
         const int s = r % kStages;
-        if (r >= kStages) mbar_wait_backoff(&p.empty[s], ((r / kStages) - 1) & 1);
+        if (r >= kStages) mbar_wait(&p.empty[s], ((r / kStages) - 1) & 1);
         if (*(volatile int*)&p.active == 0) {  // nobody needs the data: complete the phase without copies
             if (!bulk || lane == 0) mbar_arrive(&p.full[s]);
             continue;
@@ -303,47 +289,57 @@ __global__ void __launch_bounds__(288) k_forward(const uint2* __restrict__ range
         mbar_wait(&pipe.full[s], (r / kStages) & 1);
         const Stage st = stage_at(smem, s, B, N);
         const int nb = min(B, total - r * B);
-        if (!warp_done && !done) {
-            for (int j = 0; j < nb; ++j) {
-                const ScreenHeader h = st.hdr[j];
-                if (box_miss(h.h3, bx0, bx1, by0, by1)) continue;  // warp-uniform
-                float u, v;
-                bool hit;
-                if (MODE == GB_MODE_ORTHO) {
-                    hit = eval_uv_ortho(h, x, y, u, v);
-                } else {
-                    PinholeTerms pt;
-                    hit = eval_uv_pinhole(h, x, y, u, v, pt);
+        if (!warp_done) {
+            // one ballot per 32 entries finds the entries whose alpha-box meets this warp's block;
+            // the loop stays warp-uniform (finished lanes ride along idle)
+            for (int c0 = 0; c0 < nb; c0 += 32) {
+                unsigned mask =
+                    __ballot_sync(kFull, c0 + lane < nb && !box_miss(st.hdr[c0 + lane].h3, bx0, bx1, by0, by1));
+                while (mask) {
+                    const int j = c0 + __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    if (!done) {
+                        const ScreenHeader h = st.hdr[j];
+                        float u, v;
+                        bool hit;
+                        if (MODE == GB_MODE_ORTHO) {
+                            hit = eval_uv_ortho(h, x, y, u, v);
+                        } else {
+                            PinholeTerms pt;
+                            hit = eval_uv_pinhole(h, x, y, u, v, pt);
+                        }
+                        if (hit) {
+                            const float G = gauss_weight(u, v);
+                            const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);
+                            if (!(alpha < rc.alpha_skip)) {
+                                const float* t = st.tex + (size_t)j * F;
+                                float c0_, c1_, c2_;
+                                if (N == 1) {
+                                    c0_ = t[0];
+                                    c1_ = t[1];
+                                    c2_ = t[2];
+                                } else {
+                                    Bilin b;
+                                    bilin_setup(u, v, N, rc, b);
+                                    const float* p00 = t + b.o00;
+                                    const float* p10 = p00 + 3 * N;
+                                    c0_ = p00[0] * b.w00 + p10[0] * b.w10 + p00[3] * b.w01 + p10[3] * b.w11;
+                                    c1_ = p00[1] * b.w00 + p10[1] * b.w10 + p00[4] * b.w01 + p10[4] * b.w11;
+                                    c2_ = p00[2] * b.w00 + p10[2] * b.w10 + p00[5] * b.w01 + p10[5] * b.w11;
+                                }
+                                const float w = alpha * T;
+                                acc0 = fmaf(c0_, w, acc0);
+                                acc1 = fmaf(c1_, w, acc1);
+                                acc2 = fmaf(c2_, w, acc2);
+                                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                                last = r * B + j;
+                                if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;
+                            }
+                        }
+                    }
+                    if (__all_sync(kFull, done)) break;
                 }
-                if (!hit) continue;
-                const float G = gauss_weight(u, v);
-                const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);
-                if (alpha < rc.alpha_skip) continue;
-                const float* t = st.tex + (size_t)j * F;
-                float c0, c1, c2;
-                if (N == 1) {
-                    c0 = t[0];
-                    c1 = t[1];
-                    c2 = t[2];
-                } else {
-                    Bilin b;
-                    bilin_setup(u, v, N, rc, b);
-                    const float* p00 = t + b.o00;
-                    const float* p10 = p00 + 3 * N;
-                    c0 = p00[0] * b.w00 + p10[0] * b.w10 + p00[3] * b.w01 + p10[3] * b.w11;
-                    c1 = p00[1] * b.w00 + p10[1] * b.w10 + p00[4] * b.w01 + p10[4] * b.w11;
-                    c2 = p00[2] * b.w00 + p10[2] * b.w10 + p00[5] * b.w01 + p10[5] * b.w11;
-                }
-                const float w = alpha * T;
-                acc0 = fmaf(c0, w, acc0);
-                acc1 = fmaf(c1, w, acc1);
-                acc2 = fmaf(c2, w, acc2);
-                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                last = r * B + j;
-                if (rc.early_stop > 0.0f && T < rc.early_stop) {
-                    done = true;
-                    break;
-                }
+                if (__all_sync(kFull, done)) break;
             }
         }
         __syncwarp();
@@ -503,12 +499,18 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
         const int nb = count - r * B - bstart;
         mbar_wait(&pipe.full[s], (r / kStages) & 1);
         const Stage st = stage_at(smem, s, B, N);
-        for (int j = min(nb - 1, wlast - bstart); j >= 0; --j) {
+        const int jmax = min(nb - 1, wlast - bstart);
+        for (int c0 = jmax & ~31; c0 >= 0; c0 -= 32) {
+          // one ballot per 32 entries: in rank range for this warp and alpha-box meets its block
+          unsigned mask = __ballot_sync(kFull, c0 + lane <= jmax &&
+                                                   !box_miss(st.hdr[c0 + lane].h3, bx0, bx1, by0, by1));
+          if (lane == 0) GB_DBG(1, __popc(mask));
+          while (mask) {
+            const int bit = 31 - __clz(mask);
+            mask &= ~(1u << bit);
+            const int j = c0 + bit;
             const int rank = bstart + j;
             const ScreenHeader h = st.hdr[j];
-            if (lane == 0) GB_DBG(0, 1);
-            if (box_miss(h.h3, bx0, bx1, by0, by1)) continue;  // warp-uniform
-            if (lane == 0) GB_DBG(1, 1);
             bool on = rank <= last;
             float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
             PinholeTerms pt;
@@ -648,6 +650,7 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
                             red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
                 }
             }
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&pipe.empty[s]);
