@@ -20,6 +20,8 @@
 // issues red.global.add from the lanes that end up owning each sum, into
 // (a) the caller's texel gradients and (b) a 48 B per-primitive
 // screen-space accumulator that K5 chains to the raw parameters.
+#include <cstdlib>
+
 #include "gb_internal.cuh"
 
 namespace gb {
@@ -100,6 +102,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(0x989680)
         : "memory");
+}
+
+// Producer-side wait: the producer runs up to kStages batches ahead and then
+// waits on the slowest consumer; poll with an exponential nanosleep back-off so
+// it does not steal issue slots from the compositing warps.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred P1; mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2; selp.u32 %0, 1, 0, P1; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ns = 32;
+    while (!mbar_test(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < 512 ? ns * 2 : 512;
+    }
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -224,7 +247,7 @@ __device__ __forceinline__ void produce(Pipe& p, const int32_t* __restrict__ val
     const int lane = threadIdx.x & 31;
     for (int r = 0; r < nbatch; ++r) {
         const int s = r % kStages;
-        if (r >= kStages) mbar_wait(&p.empty[s], ((r / kStages) - 1) & 1);
+        if (r >= kStages) mbar_wait_sleep(&p.empty[s], ((r / kStages) - 1) & 1);
         if (*(volatile int*)&p.active == 0) {  // nobody needs the data: complete the phase without copies
             if (!bulk || lane == 0) mbar_arrive(&p.full[s]);
             continue;
@@ -429,6 +452,156 @@ __device__ __forceinline__ int corner_offset(int i, int N) {
 // ---------------------------------------------------------------------------
 // K4 backward
 // ---------------------------------------------------------------------------
+// One backward entry for the calling warp: evaluate, update the pixel's
+// rewind state, reduce and scatter the gradients (raster.hpp:324-363).
+template <int MODE, int NT>
+__device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __restrict__ t, int id, int rank,
+                                          int last, int x, int y, float& T, float g0, float g1, float g2,
+                                          float& bh0, float& bh1, float& bh2, const RasterConst& rc, int N,
+                                          int lane, float* wscratch, float* __restrict__ accum,
+                                          float* __restrict__ grid_grad) {
+    constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
+    const int F = 3 * N * N;
+    const float sigma = rc.sigma;
+            bool on = rank <= last;
+            float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
+            PinholeTerms pt;
+            if (on) {
+                bool hit;
+                if (MODE == GB_MODE_ORTHO) {
+                    hit = eval_uv_ortho(h, x, y, u, v);
+                } else {
+                    hit = eval_uv_pinhole(h, x, y, u, v, pt);
+                }
+                if (hit) {
+                    G = gauss_weight(u, v);
+                    araw = __fmul_rn(h.h1.z, G);
+                    alpha = fminf(araw, kMaxAlphaF);
+                    on = !(alpha < rc.alpha_skip);
+                } else {
+                    on = false;
+                }
+            }
+            const unsigned act = __ballot_sync(kFull, on);
+            if (act == 0) return;
+            if (lane == 0) { GB_DBG(2, 1); GB_DBG(3, __popc(act)); }
+
+            float red[16];  // screen-space sums (NS of 16 slots)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) red[i] = 0.0f;
+            float tg[12];
+#pragma unroll
+            for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
+            int tbase = -1;
+            if (on) {
+                T = __fdiv_rn(T, __fsub_rn(1.0f, alpha));  // raster.hpp:333
+                float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
+                const float aT = alpha * T;
+                const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
+                if (N == 1) {
+                    c0 = t[0];
+                    c1 = t[1];
+                    c2 = t[2];
+                    tg[0] = ch0;
+                    tg[1] = ch1;
+                    tg[2] = ch2;
+                    tbase = 0;
+                } else {
+                    Bilin b;
+                    bilin_setup(u, v, N, rc, b);
+                    const float* p00 = t + b.o00;
+                    const float* p10 = p00 + 3 * N;
+                    const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
+                    float cc_[3];
+                    const float chat[3] = {ch0, ch1, ch2};
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
+                        cc_[c] = c00 * b.w00 + c10 * b.w10 + c01 * b.w01 + c11 * b.w11;
+                        tg[c] = chat[c] * b.w00;
+                        tg[3 + c] = chat[c] * b.w10;
+                        tg[6 + c] = chat[c] * b.w01;
+                        tg[9 + c] = chat[c] * b.w11;
+                        fu_hat = fmaf(chat[c], (c10 - c00) * gv + (c11 - c01) * b.fv, fu_hat);
+                        fv_hat = fmaf(chat[c], (c01 - c00) * gu + (c11 - c10) * b.fu, fv_hat);
+                    }
+                    c0 = cc_[0];
+                    c1 = cc_[1];
+                    c2 = cc_[2];
+                    tbase = b.o00;
+                }
+                // texture.hpp:106-109 (strict mask)
+                float u_hat = (N > 1 && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
+                float v_hat = (N > 1 && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
+                // raster.hpp:344-346
+                const float gT0 = g0 * T, gT1 = g1 * T, gT2 = g2 * T;
+                const float alpha_hat = gT0 * (c0 - bh0) + gT1 * (c1 - bh1) + gT2 * (c2 - bh2);
+                float op = 0.0f;
+                if (araw < kMaxAlphaF) {  // raster.hpp:350-354
+                    op = alpha_hat * G;
+                    const float aa = alpha_hat * alpha;
+                    u_hat -= aa * u;
+                    v_hat -= aa * v;
+                }
+                if (MODE == GB_MODE_ORTHO) {
+                    red[0] = u_hat;
+                    red[1] = v_hat;
+                    red[2] = u_hat * v;
+                    red[3] = v_hat * u;
+                    red[4] = u_hat * u;
+                    red[5] = v_hat * v;
+                    red[6] = op;
+                } else {
+                    // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
+                    const float iz = 1.0f / pt.cz;
+                    const float gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
+                    red[0] = gc0;
+                    red[1] = gc1;
+                    red[2] = gc2;
+                    red[3] = pt.dx * gc0;
+                    red[4] = pt.dx * gc1;
+                    red[5] = pt.dx * gc2;
+                    red[6] = pt.dy * gc0;
+                    red[7] = pt.dy * gc1;
+                    red[8] = pt.dy * gc2;
+                    red[9] = op;
+                }
+                // raster.hpp:362
+                const float om = 1.0f - alpha;
+                bh0 = alpha * c0 + om * bh0;
+                bh1 = alpha * c1 + om * bh1;
+                bh2 = alpha * c2 + om * bh2;
+            }
+            {  // screen-space sums: lane l owns value l >> 1
+                float sv[NS];
+#pragma unroll
+                for (int i = 0; i < NS; ++i) sv[i] = red[i];
+                const float r2 = smem_reduce<NS>(sv, wscratch, lane);
+                if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
+            }
+            // texel gradients: one warp reduction when every active lane shares a bilinear cell;
+            // otherwise each lane adds its (at most four) non-zero texels straight to HBM with
+            // one float2 + one float red per texel -- cheaper than a reduction per distinct cell
+            float* gg = grid_grad + (size_t)id * F;
+            const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
+            if (__all_sync(kFull, !on || tbase == b0)) {
+                if (lane == 0) GB_DBG(4, 1);
+                const float r2 = smem_reduce<12>(tg, wscratch, lane);
+                if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
+                    red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
+            } else if (on) {
+                if (lane == 0) GB_DBG(5, 1);
+                if (N == 1) {
+                    red3(gg, tg[0], tg[1], tg[2]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (tg[3 * k] != 0.0f || tg[3 * k + 1] != 0.0f || tg[3 * k + 2] != 0.0f)
+                            red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
+                }
+            }
+}
+
 template <int MODE, int NT>
 __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ ranges, const int32_t* __restrict__ values,
                                                   const ScreenHeader* __restrict__ hdr, const float* __restrict__ tex,
@@ -510,146 +683,8 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
             mask &= ~(1u << bit);
             const int j = c0 + bit;
             const int rank = bstart + j;
-            const ScreenHeader h = st.hdr[j];
-            bool on = rank <= last;
-            float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
-            PinholeTerms pt;
-            if (on) {
-                bool hit;
-                if (MODE == GB_MODE_ORTHO) {
-                    hit = eval_uv_ortho(h, x, y, u, v);
-                } else {
-                    hit = eval_uv_pinhole(h, x, y, u, v, pt);
-                }
-                if (hit) {
-                    G = gauss_weight(u, v);
-                    araw = __fmul_rn(h.h1.z, G);
-                    alpha = fminf(araw, kMaxAlphaF);
-                    on = !(alpha < rc.alpha_skip);
-                } else {
-                    on = false;
-                }
-            }
-            const unsigned act = __ballot_sync(kFull, on);
-            if (act == 0) continue;
-            if (lane == 0) { GB_DBG(2, 1); GB_DBG(3, __popc(act)); }
-
-            float red[16];  // screen-space sums (NS of 16 slots)
-#pragma unroll
-            for (int i = 0; i < 16; ++i) red[i] = 0.0f;
-            float tg[12];
-#pragma unroll
-            for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
-            int tbase = -1;
-            if (on) {
-                T = __fdiv_rn(T, __fsub_rn(1.0f, alpha));  // raster.hpp:333
-                const float* t = st.tex + (size_t)j * F;
-                float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
-                const float aT = alpha * T;
-                const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
-                if (N == 1) {
-                    c0 = t[0];
-                    c1 = t[1];
-                    c2 = t[2];
-                    tg[0] = ch0;
-                    tg[1] = ch1;
-                    tg[2] = ch2;
-                    tbase = 0;
-                } else {
-                    Bilin b;
-                    bilin_setup(u, v, N, rc, b);
-                    const float* p00 = t + b.o00;
-                    const float* p10 = p00 + 3 * N;
-                    const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
-                    float cc_[3];
-                    const float chat[3] = {ch0, ch1, ch2};
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
-                        cc_[c] = c00 * b.w00 + c10 * b.w10 + c01 * b.w01 + c11 * b.w11;
-                        tg[c] = chat[c] * b.w00;
-                        tg[3 + c] = chat[c] * b.w10;
-                        tg[6 + c] = chat[c] * b.w01;
-                        tg[9 + c] = chat[c] * b.w11;
-                        fu_hat = fmaf(chat[c], (c10 - c00) * gv + (c11 - c01) * b.fv, fu_hat);
-                        fv_hat = fmaf(chat[c], (c01 - c00) * gu + (c11 - c10) * b.fu, fv_hat);
-                    }
-                    c0 = cc_[0];
-                    c1 = cc_[1];
-                    c2 = cc_[2];
-                    tbase = b.o00;
-                }
-                // texture.hpp:106-109 (strict mask)
-                float u_hat = (N > 1 && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
-                float v_hat = (N > 1 && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
-                // raster.hpp:344-346
-                const float gT0 = g0 * T, gT1 = g1 * T, gT2 = g2 * T;
-                const float alpha_hat = gT0 * (c0 - bh0) + gT1 * (c1 - bh1) + gT2 * (c2 - bh2);
-                float op = 0.0f;
-                if (araw < kMaxAlphaF) {  // raster.hpp:350-354
-                    op = alpha_hat * G;
-                    const float aa = alpha_hat * alpha;
-                    u_hat -= aa * u;
-                    v_hat -= aa * v;
-                }
-                if (MODE == GB_MODE_ORTHO) {
-                    red[0] = u_hat;
-                    red[1] = v_hat;
-                    red[2] = u_hat * v;
-                    red[3] = v_hat * u;
-                    red[4] = u_hat * u;
-                    red[5] = v_hat * v;
-                    red[6] = op;
-                } else {
-                    // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
-                    const float iz = 1.0f / pt.cz;
-                    const float gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
-                    red[0] = gc0;
-                    red[1] = gc1;
-                    red[2] = gc2;
-                    red[3] = pt.dx * gc0;
-                    red[4] = pt.dx * gc1;
-                    red[5] = pt.dx * gc2;
-                    red[6] = pt.dy * gc0;
-                    red[7] = pt.dy * gc1;
-                    red[8] = pt.dy * gc2;
-                    red[9] = op;
-                }
-                // raster.hpp:362
-                const float om = 1.0f - alpha;
-                bh0 = alpha * c0 + om * bh0;
-                bh1 = alpha * c1 + om * bh1;
-                bh2 = alpha * c2 + om * bh2;
-            }
-            const int id = st.id[j];
-            {  // screen-space sums: lane l owns value l >> 1
-                float sv[NS];
-#pragma unroll
-                for (int i = 0; i < NS; ++i) sv[i] = red[i];
-                const float r2 = smem_reduce<NS>(sv, wscratch, lane);
-                if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
-            }
-            // texel gradients: one warp reduction when every active lane shares a bilinear cell;
-            // otherwise each lane adds its (at most four) non-zero texels straight to HBM with
-            // one float2 + one float red per texel -- cheaper than a reduction per distinct cell
-            float* gg = grid_grad + (size_t)id * F;
-            const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
-            if (__all_sync(kFull, !on || tbase == b0)) {
-                if (lane == 0) GB_DBG(4, 1);
-                const float r2 = smem_reduce<12>(tg, wscratch, lane);
-                if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
-                    red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
-            } else if (on) {
-                if (lane == 0) GB_DBG(5, 1);
-                if (N == 1) {
-                    red3(gg, tg[0], tg[1], tg[2]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (tg[3 * k] != 0.0f || tg[3 * k + 1] != 0.0f || tg[3 * k + 2] != 0.0f)
-                            red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
-                }
-            }
+            bwd_entry<MODE, NT>(st.hdr[j], st.tex + (size_t)j * F, st.id[j], rank, last, x, y, T, g0, g1, g2, bh0,
+                                bh1, bh2, rc, N, lane, wscratch, accum, grid_grad);
           }
         }
         __syncwarp();
@@ -658,8 +693,171 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
 }
 
 // ---------------------------------------------------------------------------
+// Direct variants (no shared-memory staging): each warp walks the tile list on
+// its own, reading ids, headers and texels through L1 (__ldg).  No producer,
+// no CTA-level synchronisation; warps finish independently.
+// ---------------------------------------------------------------------------
+template <int MODE, int NT>
+__global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict__ ranges,
+                                                        const int32_t* __restrict__ values,
+                                                        const ScreenHeader* __restrict__ hdr,
+                                                        const float* __restrict__ tex, const CamConst cc,
+                                                        const RasterConst rc, int n_rt, float* __restrict__ out_color,
+                                                        float* __restrict__ out_trans, int32_t* __restrict__ out_last) {
+    const int N = tex_n<NT>(n_rt);
+    const int F = 3 * N * N;
+    const int ts = rc.tile_size;
+    const int lane = threadIdx.x & 31;
+    const int tile = blockIdx.x;
+    const uint2 range = ranges[tile];
+    const int total = (int)(range.y - range.x);
+    const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
+    int lx, ly;
+    tile_pixel(threadIdx.x, ts, lx, ly);
+    const int x = tx * ts + lx, y = ty * ts + ly;
+    const bool inside = (int)threadIdx.x < ts * ts && x < cc.width && y < cc.height;
+    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
+    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
+    float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
+    int last = -1;
+    bool done = !inside;
+    for (int c0 = 0; c0 < total && !__all_sync(kFull, done); c0 += 32) {
+        int idl = -1;
+        bool pass = false;
+        if (c0 + lane < total) {
+            idl = __ldg(&values[range.x + c0 + lane]);
+            pass = !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+        }
+        unsigned mask = __ballot_sync(kFull, pass);
+        while (mask) {
+            const int bit = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int id = __shfl_sync(kFull, idl, bit);
+            if (!done) {
+                ScreenHeader h;
+                h.h0 = __ldg(&hdr[id].h0);
+                h.h1 = __ldg(&hdr[id].h1);
+                h.h2 = __ldg(&hdr[id].h2);
+                float u, v;
+                bool hit;
+                if (MODE == GB_MODE_ORTHO) {
+                    hit = eval_uv_ortho(h, x, y, u, v);
+                } else {
+                    PinholeTerms pt;
+                    hit = eval_uv_pinhole(h, x, y, u, v, pt);
+                }
+                if (hit) {
+                    const float G = gauss_weight(u, v);
+                    const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);
+                    if (!(alpha < rc.alpha_skip)) {
+                        const float* t = tex + (size_t)id * F;
+                        float c0_, c1_, c2_;
+                        if (N == 1) {
+                            c0_ = __ldg(t);
+                            c1_ = __ldg(t + 1);
+                            c2_ = __ldg(t + 2);
+                        } else {
+                            Bilin b;
+                            bilin_setup(u, v, N, rc, b);
+                            const float* p00 = t + b.o00;
+                            const float* p10 = p00 + 3 * N;
+                            c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 + __ldg(p10 + 3) * b.w11;
+                            c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
+                                  __ldg(p10 + 4) * b.w11;
+                            c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
+                                  __ldg(p10 + 5) * b.w11;
+                        }
+                        const float w = alpha * T;
+                        acc0 = fmaf(c0_, w, acc0);
+                        acc1 = fmaf(c1_, w, acc1);
+                        acc2 = fmaf(c2_, w, acc2);
+                        T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                        last = c0 + bit;
+                        if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;
+                    }
+                }
+            }
+            if (__all_sync(kFull, done)) break;
+        }
+    }
+    if (inside) {
+        const size_t p = (size_t)y * cc.width + x;
+        out_color[p * 3 + 0] = fmaf(T, cc.bg[0], acc0);
+        out_color[p * 3 + 1] = fmaf(T, cc.bg[1], acc1);
+        out_color[p * 3 + 2] = fmaf(T, cc.bg[2], acc2);
+        out_trans[p] = T;
+        out_last[p] = last;
+    }
+}
+
+template <int MODE, int NT>
+__global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict__ ranges,
+                                                         const int32_t* __restrict__ values,
+                                                         const ScreenHeader* __restrict__ hdr,
+                                                         const float* __restrict__ tex, const CamConst cc,
+                                                         const RasterConst rc, int n_rt,
+                                                         const float* __restrict__ in_trans,
+                                                         const int32_t* __restrict__ in_last,
+                                                         const float* __restrict__ image_grad,
+                                                         float* __restrict__ accum, float* __restrict__ grid_grad) {
+    extern __shared__ __align__(16) float red_scratch[];
+    const int N = tex_n<NT>(n_rt);
+    const int F = 3 * N * N;
+    const int ts = rc.tile_size;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x;
+    const uint2 range = ranges[tile];
+    const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
+    int lx, ly;
+    tile_pixel(threadIdx.x, ts, lx, ly);
+    const int x = tx * ts + lx, y = ty * ts + ly;
+    const bool inside = (int)threadIdx.x < ts * ts && x < cc.width && y < cc.height;
+    int last = -1;
+    float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
+    if (inside) {  // raster.hpp:313-322
+        const size_t p = (size_t)y * cc.width + x;
+        last = in_last[p];
+        g0 = image_grad[p * 3 + 0];
+        g1 = image_grad[p * 3 + 1];
+        g2 = image_grad[p * 3 + 2];
+        T = in_trans[p];
+        if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) last = -1;
+    }
+    float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
+    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
+    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
+    const int wlast = __reduce_max_sync(kFull, last);
+    float* wscratch = red_scratch + warp * kRedRows * kRedStride;
+    for (int c0 = wlast & ~31; c0 >= 0; c0 -= 32) {
+        int idl = -1;
+        bool pass = false;
+        if (c0 + lane <= wlast) {
+            idl = __ldg(&values[range.x + c0 + lane]);
+            pass = !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+        }
+        unsigned mask = __ballot_sync(kFull, pass);
+        while (mask) {
+            const int bit = 31 - __clz(mask);
+            mask &= ~(1u << bit);
+            const int id = __shfl_sync(kFull, idl, bit);
+            ScreenHeader h;
+            h.h0 = __ldg(&hdr[id].h0);
+            h.h1 = __ldg(&hdr[id].h1);
+            h.h2 = __ldg(&hdr[id].h2);
+            bwd_entry<MODE, NT>(h, tex + (size_t)id * F, id, c0 + bit, last, x, y, T, g0, g1, g2, bh0, bh1, bh2, rc,
+                                N, lane, wscratch, accum, grid_grad);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+static int tune_env(const char* name, int dflt) {  // development knob: GB_TUNE_* overrides
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 int pick_batch(int N, int stage_budget = 13312) {
     // kStages staging buffers within ~52 KB (K3) / ~37 KB + reduction scratch (K4) keep 4 CTAs per SM
     const size_t per = stage_bytes(1, N);
@@ -707,12 +905,41 @@ static cudaError_t bwd_t(int tiles, int threads, size_t smem, cudaStream_t st, c
         default: return FN<MODE, 0>(__VA_ARGS__);       \
     }
 
+template <int MODE, int NT>
+static cudaError_t fwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
+                          const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc, int n,
+                          float* color, float* trans, int32_t* last) {
+    k_forward_direct<MODE, NT><<<tiles, threads, 0, st>>>(ranges, values, hdr, tex, cc, rc, n, color, trans, last);
+    return cudaGetLastError();
+}
+
+template <int MODE, int NT>
+static cudaError_t bwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
+                          const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc, int n,
+                          const float* trans, const int32_t* last, const float* image_grad, float* accum,
+                          float* grid_grad) {
+    const size_t smem = (size_t)(threads / 32) * kRedRows * kRedStride * 4;
+    k_backward_direct<MODE, NT><<<tiles, threads, smem, st>>>(ranges, values, hdr, tex, cc, rc, n, trans, last,
+                                                               image_grad, accum, grid_grad);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                            const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
                            float* color, float* trans, int32_t* last, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
+    if (tune_env("GB_TUNE_DIRECT", 0) & 1) {
+        const int threads = ((ts * ts + 31) / 32) * 32;
+        if (mode == GB_MODE_ORTHO) {
+            GB_DISPATCH_N(fwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, color,
+                          trans, last)
+        } else {
+            GB_DISPATCH_N(fwdd_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, color,
+                          trans, last)
+        }
+    }
     const int threads = ((ts * ts + 31) / 32) * 32 + 32;  // + the producer warp
-    const int B = pick_batch(n);
+    const int B = pick_batch(n, tune_env("GB_TUNE_FWD_BUDGET", 13312));
     const size_t smem = kStages * stage_bytes(B, n);
     if (mode == GB_MODE_ORTHO) {
         GB_DISPATCH_N(fwd_t, GB_MODE_ORTHO, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B, color,
@@ -728,8 +955,18 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
                             const float* trans, const int32_t* last, const float* image_grad, float* accum,
                             float* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
+    if (tune_env("GB_TUNE_DIRECT", 0) & 2) {
+        const int threads = ((ts * ts + 31) / 32) * 32;
+        if (mode == GB_MODE_ORTHO) {
+            GB_DISPATCH_N(bwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, trans, last,
+                          image_grad, accum, grid_grad)
+        } else {
+            GB_DISPATCH_N(bwdd_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, trans,
+                          last, image_grad, accum, grid_grad)
+        }
+    }
     const int threads = ((ts * ts + 31) / 32) * 32 + 32;  // + the producer warp
-    const int B = pick_batch(n, 9216);
+    const int B = pick_batch(n, tune_env("GB_TUNE_BWD_BUDGET", 9216));
     const size_t smem = kStages * stage_bytes(B, n) + (size_t)(threads / 32 - 1) * kRedRows * kRedStride * 4;
     if (mode == GB_MODE_ORTHO) {
         GB_DISPATCH_N(bwd_t, GB_MODE_ORTHO, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B, trans,
