@@ -40,7 +40,7 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--views-per-gpu", type=int, default=8)
@@ -67,7 +67,7 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -81,7 +81,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE,
+                                          "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -333,7 +333,8 @@ def run_ours(args):
                                f"{args.views_per_gpu} Fibonacci-sphere views/GPU at 1600x1064, L1, "
                                "NCCL all-reduce + Adam",
                    "views_per_gpu": len(views), "surfels": cfg3.count, "texture": f"{n}x{n}",
-                   "image": f"{W}x{H}", "tile": 16, "mean_pairs_per_view": int(np.mean(pairs)) if pairs else 0,
+                   "image": f"{W}x{H}", "tile": 16,
+                   "compositor": os.environ.get("GB_COMPOSITOR", "direct"), "mean_pairs_per_view": int(np.mean(pairs)) if pairs else 0,
                    "l2": "working set (0.8 GB textures + 0.8 GB grads + 1.6 GB Adam) >> 126 MB L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,

@@ -1,13 +1,19 @@
-// gb_binning.cu -- K2: tile binning (build_binning, raster.hpp:116-147).
+// gb_binning.cu -- K2: tile binning (build_binning, raster.hpp:116-147) as a
+// two-level stable sort.
 //
-//   counts (K1) --CUB inclusive scan--> offsets
-//   k_duplicate : one (tile << 32 | depth_bits, k) pair per overlapped tile,
-//                 emitted in primitive-index order
-//   CUB stable radix sort on the low 32 + ceil(log2 tiles) key bits
-//   k_ranges    : per-tile [start, end) into the sorted values
+//   depth_bits (K1) --CUB stable radix sort, 32 bits--> perm  (primitives in
+//                      (depth, index) order; culled ones carry ~0 and sort last)
+//   k_gather_counts  : counts in that order, CUB inclusive scan -> offsets
+//   k_duplicate      : one (tile id, primitive) pair per overlapped tile,
+//                      emitted in (depth, index) order
+//   CUB stable radix sort on the ceil(log2 tiles) tile-id bits only
+//   k_ranges         : per-tile [start, end) into the sorted values
 //
-// Stability + index-ordered emission reproduce the reference's per-tile
-// order "ascending depth_key, ties by index" (raster.hpp:141-145) exactly.
+// Both sorts are stable, so inside every tile the pairs stay in (depth_key,
+// index) order -- the reference's per-tile order (raster.hpp:141-145) -- and the
+// result equals one sort of 64-bit (tile << 32 | depth) keys, bit for bit.  It
+// replaces that 45-bit sort over P pairs (6 radix passes of 12 B records) with
+// a 32-bit sort over K primitives plus 2 passes of 8 B records over P pairs.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -15,61 +21,45 @@
 
 namespace gb {
 
-__global__ void __launch_bounds__(256) k_duplicate(int64_t K, int tiles_x, const uint32_t* __restrict__ offsets,
-                                                   const uint2* __restrict__ rects,
-                                                   const uint32_t* __restrict__ depth_bits,
-                                                   uint64_t* __restrict__ keys, int32_t* __restrict__ values) {
+__global__ void __launch_bounds__(256) k_iota(int64_t K, int32_t* __restrict__ out) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
-    const uint32_t end = offsets[k + 1];
-    uint32_t o = offsets[k];
+    if (k < K) out[k] = (int32_t)k;
+}
+
+__global__ void __launch_bounds__(256) k_gather_counts(int64_t K, const int32_t* __restrict__ perm,
+                                                       const uint32_t* __restrict__ counts,
+                                                       uint32_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < K) out[i] = counts[perm[i]];
+}
+
+__global__ void __launch_bounds__(256) k_duplicate(int64_t K, int tiles_x, const int32_t* __restrict__ perm,
+                                                   const uint32_t* __restrict__ offsets,
+                                                   const uint2* __restrict__ rects, uint32_t* __restrict__ keys,
+                                                   int32_t* __restrict__ values) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const uint32_t end = offsets[i + 1];
+    uint32_t o = offsets[i];
     if (o == end) return;
+    const int32_t k = perm[i];
     const uint2 r = rects[k];
     const int tx0 = r.x & 0xffff, ty0 = r.x >> 16, tx1 = r.y & 0xffff, ty1 = r.y >> 16;
-    const uint64_t lo = depth_bits[k];
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
-            keys[o] = ((uint64_t)(ty * tiles_x + tx) << 32) | lo;
-            values[o] = (int32_t)k;
+            keys[o] = (uint32_t)(ty * tiles_x + tx);
+            values[o] = k;
             ++o;
         }
 }
 
-__global__ void __launch_bounds__(256) k_ranges(int64_t P, const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(256) k_ranges(int64_t P, const uint32_t* __restrict__ keys,
                                                 uint2* __restrict__ ranges) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P) return;
-    const uint32_t tile = (uint32_t)(keys[i] >> 32);
-    if (i == 0 || (uint32_t)(keys[i - 1] >> 32) != tile) ranges[tile].x = (uint32_t)i;
-    if (i == P - 1 || (uint32_t)(keys[i + 1] >> 32) != tile) ranges[tile].y = (uint32_t)(i + 1);
-}
-
-size_t scan_temp_bytes(int64_t K) {
-    size_t bytes = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)K);
-    return bytes;
-}
-
-size_t sort_temp_bytes(int64_t P) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
-                                    (int32_t*)nullptr, (int)P);
-    return bytes;
-}
-
-// offsets must have K+1 entries; offsets[0] is zeroed here.
-cudaError_t launch_scan(void* temp, size_t temp_bytes, const uint32_t* counts, uint32_t* offsets, int64_t K,
-                        cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(offsets, 0, sizeof(uint32_t), st);
-    if (e != cudaSuccess || K == 0) return e;
-    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, counts, offsets + 1, (int)K, st);
-}
-
-cudaError_t launch_duplicate(int64_t K, int tiles_x, const uint32_t* offsets, const uint2* rects,
-                             const uint32_t* depth_bits, uint64_t* keys, int32_t* values, cudaStream_t st) {
-    if (K == 0) return cudaSuccess;
-    k_duplicate<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, tiles_x, offsets, rects, depth_bits, keys, values);
-    return cudaGetLastError();
+    const uint32_t tile = keys[i];
+    if (i == 0 || keys[i - 1] != tile) ranges[tile].x = (uint32_t)i;
+    if (i == P - 1 || keys[i + 1] != tile) ranges[tile].y = (uint32_t)(i + 1);
 }
 
 static int bits_for(uint32_t v) {
@@ -78,16 +68,66 @@ static int bits_for(uint32_t v) {
     return b;
 }
 
-// Sorts (keys_in, vals_in) into (keys_out, vals_out).
-cudaError_t launch_sort(void* temp, size_t temp_bytes, uint64_t* keys_in, uint64_t* keys_out, int32_t* vals_in,
-                        int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st) {
-    if (P == 0) return cudaSuccess;
-    const int end_bit = 32 + bits_for((uint32_t)n_tiles);
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)P, 0,
-                                           end_bit, st);
+size_t scan_temp_bytes(int64_t K) {
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)K);
+    return bytes;
 }
 
-cudaError_t launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, int n_tiles, cudaStream_t st) {
+size_t sort_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)n);
+    return bytes;
+}
+
+// Radix passes CUB launches for a sort over `bits` key bits (histogram + exclusive sum + one per 8-bit digit).
+int sort_launches(int bits) { return bits > 0 ? 2 + (bits + 7) / 8 : 0; }
+
+// perm = primitive indices in stable (depth_bits, index) order; depth_sorted is scratch.
+cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* depth_bits, uint32_t* depth_sorted,
+                              int32_t* iota, int32_t* perm, int64_t K, cudaStream_t st) {
+    if (K == 0) return cudaSuccess;
+    k_iota<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, iota);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, depth_bits, depth_sorted, iota, perm, (int)K, 0, 32, st);
+}
+
+// offsets (K+1 entries) = exclusive scan of the counts in perm order; offsets[K] = P.
+cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
+                        uint32_t* counts_sorted, uint32_t* offsets, int64_t K, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(offsets, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess || K == 0) return e;
+    k_gather_counts<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, perm, counts, counts_sorted);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, counts_sorted, offsets + 1, (int)K, st);
+}
+
+cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,
+                             uint32_t* keys, int32_t* values, cudaStream_t st) {
+    if (K == 0) return cudaSuccess;
+    k_duplicate<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, tiles_x, perm, offsets, rects, keys, values);
+    return cudaGetLastError();
+}
+
+// Stable sort of (tile id, primitive) pairs on the tile-id bits.
+cudaError_t launch_tile_sort(void* temp, size_t temp_bytes, uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_in,
+                             int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st) {
+    if (P == 0) return cudaSuccess;
+    int end_bit = bits_for((uint32_t)n_tiles);
+    if (end_bit == 0) end_bit = 1;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)P, 0, end_bit,
+                                           st);
+}
+
+int tile_sort_bits(int n_tiles) {
+    const int b = bits_for((uint32_t)n_tiles);
+    return b ? b : 1;
+}
+
+cudaError_t launch_ranges(int64_t P, const uint32_t* keys, uint2* ranges, int n_tiles, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, st);
     if (e != cudaSuccess || P == 0) return e;
     k_ranges<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, keys, ranges);

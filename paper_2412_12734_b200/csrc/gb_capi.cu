@@ -13,14 +13,18 @@
 
 namespace gb {
 size_t scan_temp_bytes(int64_t K);
-size_t sort_temp_bytes(int64_t P);
-cudaError_t launch_scan(void* temp, size_t temp_bytes, const uint32_t* counts, uint32_t* offsets, int64_t K,
-                        cudaStream_t st);
-cudaError_t launch_duplicate(int64_t K, int tiles_x, const uint32_t* offsets, const uint2* rects,
-                             const uint32_t* depth_bits, uint64_t* keys, int32_t* values, cudaStream_t st);
-cudaError_t launch_sort(void* temp, size_t temp_bytes, uint64_t* keys_in, uint64_t* keys_out, int32_t* vals_in,
-                        int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st);
-cudaError_t launch_ranges(int64_t P, const uint64_t* keys, uint2* ranges, int n_tiles, cudaStream_t st);
+size_t sort_temp_bytes(int64_t n);
+int sort_launches(int bits);
+int tile_sort_bits(int n_tiles);
+cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* depth_bits, uint32_t* depth_sorted,
+                              int32_t* iota, int32_t* perm, int64_t K, cudaStream_t st);
+cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
+                        uint32_t* counts_sorted, uint32_t* offsets, int64_t K, cudaStream_t st);
+cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,
+                             uint32_t* keys, int32_t* values, cudaStream_t st);
+cudaError_t launch_tile_sort(void* temp, size_t temp_bytes, uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_in,
+                             int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st);
+cudaError_t launch_ranges(int64_t P, const uint32_t* keys, uint2* ranges, int n_tiles, cudaStream_t st);
 cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                            const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
                            float* color, float* trans, int32_t* last, cudaStream_t st);
@@ -106,7 +110,7 @@ struct gb_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
-    DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, accum, adam_bad;
+    DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, counts_tmp, accum, adam_bad;
     uint32_t* pinned_total = nullptr;
     bool prof = false;
     std::vector<ProfRec> prof_recs;
@@ -156,7 +160,7 @@ struct gb_binning {
     int64_t K = 0;
     int n = 0;
     int64_t P = 0;
-    DevBuf headers, rects, counts, offsets, depth, keys, values, ranges;
+    DevBuf headers, rects, counts, offsets, depth, perm, keys, values, ranges;
 };
 
 namespace {
@@ -271,6 +275,9 @@ gb_status gb_context_destroy(gb_context* ctx) {
     ctx->sort_temp.release();
     ctx->keys_tmp.release();
     ctx->vals_tmp.release();
+    ctx->depth_tmp.release();
+    ctx->iota_tmp.release();
+    ctx->counts_tmp.release();
     ctx->accum.release();
     ctx->adam_bad.release();
     if (ctx->pinned_total) cudaFreeHost(ctx->pinned_total);
@@ -384,6 +391,7 @@ gb_status gb_binning_destroy(gb_binning* b) {
     b->counts.release();
     b->offsets.release();
     b->depth.release();
+    b->perm.release();
     b->keys.release();
     b->values.release();
     b->ranges.release();
@@ -416,9 +424,13 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
     GB_CUDA(b->counts.ensure(sizeof(uint32_t) * Kc));
     GB_CUDA(b->offsets.ensure(sizeof(uint32_t) * (Kc + 1)));
     GB_CUDA(b->depth.ensure(sizeof(uint32_t) * Kc));
+    GB_CUDA(b->perm.ensure(sizeof(int32_t) * Kc));
     GB_CUDA(b->ranges.ensure(sizeof(uint2) * (n_tiles > 0 ? n_tiles : 1)));
-    const size_t scan_bytes = gb::scan_temp_bytes(Kc);
-    GB_CUDA(ctx->scan_temp.ensure(scan_bytes));
+    GB_CUDA(ctx->depth_tmp.ensure(sizeof(uint32_t) * Kc));
+    GB_CUDA(ctx->iota_tmp.ensure(sizeof(int32_t) * Kc));
+    GB_CUDA(ctx->counts_tmp.ensure(sizeof(uint32_t) * Kc));
+    GB_CUDA(ctx->scan_temp.ensure(gb::scan_temp_bytes(Kc)));
+    GB_CUDA(ctx->sort_temp.ensure(gb::sort_temp_bytes(Kc)));
 
     // K1
     gb::ProjParams pp = gb::make_proj_params(s, cam, cfg, b->tiles_x, b->tiles_y);
@@ -428,42 +440,50 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
                                    b->counts.as<uint32_t>(), b->depth.as<uint32_t>(), stream));
     }
     ctx->launches += K > 0;
-    // K2a scan -> P
+    // K2a primitives in (depth, index) order
+    {
+        ProfScope ps(ctx, GB_K_SORT);
+        GB_CUDA(gb::launch_depth_sort(ctx->sort_temp.p, ctx->sort_temp.cap, b->depth.as<uint32_t>(),
+                                      ctx->depth_tmp.as<uint32_t>(), ctx->iota_tmp.as<int32_t>(),
+                                      b->perm.as<int32_t>(), K, stream));
+    }
+    ctx->launches += K > 0 ? 1 + gb::sort_launches(32) : 0;
+    // K2b tile counts in that order, scanned -> P
     {
         ProfScope ps(ctx, GB_K_SCAN);
-        GB_CUDA(gb::launch_scan(ctx->scan_temp.p, ctx->scan_temp.cap, b->counts.as<uint32_t>(),
-                                b->offsets.as<uint32_t>(), K, stream));
+        GB_CUDA(gb::launch_scan(ctx->scan_temp.p, ctx->scan_temp.cap, b->perm.as<int32_t>(), b->counts.as<uint32_t>(),
+                                ctx->counts_tmp.as<uint32_t>(), b->offsets.as<uint32_t>(), K, stream));
     }
-    ctx->launches += K > 0 ? 1 : 0;
+    ctx->launches += K > 0 ? 3 : 0;  // gather + CUB scan (init + scan)
     GB_CUDA(cudaMemcpyAsync(ctx->pinned_total, b->offsets.as<uint32_t>() + K, sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, stream));
     GB_CUDA(cudaStreamSynchronize(stream));
     const int64_t P = *ctx->pinned_total;
     b->P = P;
     const int64_t Pc = P > 0 ? P : 1;
-    GB_CUDA(b->keys.ensure(sizeof(uint64_t) * Pc));
+    GB_CUDA(b->keys.ensure(sizeof(uint32_t) * Pc));
     GB_CUDA(b->values.ensure(sizeof(int32_t) * Pc));
-    GB_CUDA(ctx->keys_tmp.ensure(sizeof(uint64_t) * Pc));
+    GB_CUDA(ctx->keys_tmp.ensure(sizeof(uint32_t) * Pc));
     GB_CUDA(ctx->vals_tmp.ensure(sizeof(int32_t) * Pc));
     GB_CUDA(ctx->sort_temp.ensure(gb::sort_temp_bytes(Pc)));
-    // K2b duplicate, K2c sort, K2d ranges
+    // K2c duplicate in depth order, K2d stable sort on the tile id, K2e ranges
     {
         ProfScope ps(ctx, GB_K_DUPLICATE);
-        GB_CUDA(gb::launch_duplicate(K, b->tiles_x, b->offsets.as<uint32_t>(), b->rects.as<uint2>(),
-                                     b->depth.as<uint32_t>(), ctx->keys_tmp.as<uint64_t>(),
-                                     ctx->vals_tmp.as<int32_t>(), stream));
+        GB_CUDA(gb::launch_duplicate(K, b->tiles_x, b->perm.as<int32_t>(), b->offsets.as<uint32_t>(),
+                                     b->rects.as<uint2>(), ctx->keys_tmp.as<uint32_t>(), ctx->vals_tmp.as<int32_t>(),
+                                     stream));
     }
     {
         ProfScope ps(ctx, GB_K_SORT);
-        GB_CUDA(gb::launch_sort(ctx->sort_temp.p, ctx->sort_temp.cap, ctx->keys_tmp.as<uint64_t>(),
-                                b->keys.as<uint64_t>(), ctx->vals_tmp.as<int32_t>(), b->values.as<int32_t>(), P,
-                                n_tiles, stream));
+        GB_CUDA(gb::launch_tile_sort(ctx->sort_temp.p, ctx->sort_temp.cap, ctx->keys_tmp.as<uint32_t>(),
+                                     b->keys.as<uint32_t>(), ctx->vals_tmp.as<int32_t>(), b->values.as<int32_t>(), P,
+                                     n_tiles, stream));
     }
     {
         ProfScope ps(ctx, GB_K_RANGES);
-        GB_CUDA(gb::launch_ranges(P, b->keys.as<uint64_t>(), b->ranges.as<uint2>(), n_tiles, stream));
+        GB_CUDA(gb::launch_ranges(P, b->keys.as<uint32_t>(), b->ranges.as<uint2>(), n_tiles, stream));
     }
-    ctx->launches += (K > 0) + (P > 0 ? 2 : 0);
+    ctx->launches += (K > 0) + (P > 0 ? 1 + gb::sort_launches(gb::tile_sort_bits(n_tiles)) : 0);
     b->built = true;
     return GB_OK;
 }

@@ -1,0 +1,92 @@
+// gb_compose.cuh -- device helpers shared by the K3/K4 compositor variants
+// (gb_raster.cu: staged + direct one-pixel-per-thread; gb_composite.cu:
+// multi-pixel-per-thread): bilinear set-up (texture.hpp:27-66), warp
+// reductions and the global red helpers of the backward.
+#pragma once
+
+#include "gb_internal.cuh"
+
+namespace gb {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int NT>
+__device__ __forceinline__ int tex_n(int n_rt) {
+    return NT ? NT : n_rt;
+}
+
+struct Bilin {
+    int o00;  // offset of texel (i_u, i_v) channel 0
+    float fu, fv;
+    float w00, w10, w01, w11;
+};
+
+__device__ __forceinline__ void bilin_setup(float u, float v, int N, const RasterConst& rc, Bilin& b) {
+    int iu, iv;
+    float s = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
+    s = fminf(fmaxf(s, 0.0f), (float)(N - 1));
+    iu = min((int)floorf(s), N - 2);
+    b.fu = __fsub_rn(s, (float)iu);
+    float t = __fmaf_rn(v, rc.tex_scale, rc.tex_offset);
+    t = fminf(fmaxf(t, 0.0f), (float)(N - 1));
+    iv = min((int)floorf(t), N - 2);
+    b.fv = __fsub_rn(t, (float)iv);
+    b.o00 = (iu * N + iv) * 3;
+    const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
+    b.w00 = gu * gv;
+    b.w10 = b.fu * gv;
+    b.w01 = gu * b.fv;
+    b.w11 = b.fu * b.fv;
+}
+
+// Warp sum of NV <= 16 per-lane values through a per-warp shared-memory
+// transpose (scratch: kRedRows x kRedStride floats): lane l writes value i
+// to row i, column l; lane l then sums half (l & 1) of row l >> 1 with four
+// conflict-free 128-bit loads and one shuffle.  ~NV + 22 instructions
+// versus ~4 NV for a shuffle butterfly.  Returns the row l >> 1 total.
+constexpr int kRedRows = 16;
+constexpr int kRedStride = 36;  // 32 lanes + 4 pad: rows land in distinct bank quads
+
+template <int NV>
+__device__ __forceinline__ float smem_reduce(const float (&v)[NV], float* scratch, int lane) {
+    __syncwarp();  // previous readers of the scratch are done
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[i * kRedStride + lane] = v[i];
+    __syncwarp();
+    const int row = lane >> 1;
+    float acc = 0.0f;
+    if (row < NV) {
+        const float4* q = reinterpret_cast<const float4*>(scratch + row * kRedStride + (lane & 1) * 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float4 a = q[k];
+            acc += (a.x + a.y) + (a.z + a.w);
+        }
+    }
+    return acc + __shfl_xor_sync(kFull, acc, 1);
+}
+
+__device__ __forceinline__ void red_add(float* p, float v) {
+    if (v != 0.0f) atomicAdd(p, v);
+}
+
+// p[0..2] += (a, b, c) with one 8-byte vector red and one scalar red (branch-free on alignment)
+__device__ __forceinline__ void red3(float* p, float a, float b, float c) {
+    const bool even = (reinterpret_cast<uintptr_t>(p) & 7) == 0;
+    float2* pv = reinterpret_cast<float2*>(even ? p : p + 1);
+    atomicAdd(pv, even ? make_float2(a, b) : make_float2(b, c));
+    atomicAdd(even ? p + 2 : p, even ? c : a);
+}
+
+// texel corner k (0..3 = 00, 10, 01, 11) channel c -> float offset from the base texel
+__device__ __forceinline__ int corner_offset(int i, int N) {
+    const int k = i / 3, c = i - 3 * (i / 3);
+    return ((k & 1) ? 3 * N : 0) + ((k & 2) ? 3 : 0) + c;
+}
+
+// true when the entry's alpha-box misses the warp's pixel block for certain
+__device__ __forceinline__ bool box_miss(const float4& box, float bx0, float bx1, float by0, float by1) {
+    return box.y < bx0 || box.x > bx1 || box.w < by0 || box.z > by1;
+}
+
+}  // namespace gb

@@ -4,9 +4,12 @@
 //   params   : the caller's SplatSet SoA (gb_splats)                       40 B + 12n^2 B / primitive
 //   headers  : ScreenHeader[K], 48 B, written by K1 for binned primitives
 //   rects    : uint2[K] packed tile rectangle (tx0|ty0<<16, tx1|ty1<<16)
-//   counts   : uint32[K] tiles per primitive, scanned in place to offsets
-//   keys     : uint64[P] (tile << 32 | orderable fp32 depth bits), sorted
-//   values   : int32[P] primitive index per (tile, primitive) pair, sorted
+//   counts   : uint32[K] tiles per primitive
+//   depth    : uint32[K] orderable fp32 depth bits (~0 when culled)
+//   perm     : int32[K] primitives in stable (depth, index) order
+//   offsets  : uint32[K+1] exclusive scan of the counts in perm order
+//   keys     : uint32[P] tile id per (tile, primitive) pair, stably sorted
+//   values   : int32[P] primitive index per pair (per tile: depth, index order)
 //   ranges   : uint2[tiles] [start, end) into values per tile
 //   accum    : float[K*12] per-primitive screen-space gradient sums (K4 -> K5)
 #pragma once
@@ -76,8 +79,17 @@ __device__ __forceinline__ void tile_pixel(int tid, int ts, int& lx, int& ly) {
 // -ffp-contract=off for the same reason, CMakeLists.txt:12-15).
 
 struct PinholeTerms {  // kept for the backward chain
-    float dx, dy, cz;
+    float dx, dy, cz, iz;
 };
+
+// Approximate reciprocal (one MUFU.RCP, ~1 ulp).  It is deterministic, so K3
+// and K4 still see identical bits; only the oracle comparison is
+// tolerance-based, and 1 ulp is far inside it.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 // raster.hpp:36-42 (ortho) -- returns true (always a hit).
 __device__ __forceinline__ bool eval_uv_ortho(const ScreenHeader& h, int x, int y, float& u, float& v) {
@@ -91,7 +103,9 @@ __device__ __forceinline__ bool eval_uv_ortho(const ScreenHeader& h, int x, int 
 
 // Pinhole 2DGS ray-splat intersection in the centred
 // linear-fractional form above.  A miss (ray parallel to the plane, or the
-// plane hit behind the camera: c_z <= 0 after the K1 normalisation) is skipped.
+// plane hit behind the camera: c_z <= 0 after the K1 normalisation) is skipped;
+// c_z below FLT_MIN (a hit at ~infinity, G = 0 anyway) counts as a miss so the
+// flush-to-zero reciprocal never sees a denormal.
 __device__ __forceinline__ bool eval_uv_pinhole(const ScreenHeader& h, int x, int y, float& u, float& v,
                                                 PinholeTerms& p) {
     const int cxi = __float_as_int(h.h2.y), cyi = __float_as_int(h.h2.z);
@@ -100,10 +114,10 @@ __device__ __forceinline__ bool eval_uv_pinhole(const ScreenHeader& h, int x, in
     const float cx = __fmaf_rn(p.dx, h.h0.x, __fmul_rn(p.dy, h.h0.w));
     const float cy = __fmaf_rn(p.dx, h.h0.y, __fmul_rn(p.dy, h.h1.x));
     p.cz = __fmaf_rn(p.dx, h.h0.z, __fmaf_rn(p.dy, h.h1.y, 1.0f));
-    const float iz = __frcp_rn(p.cz);
-    u = __fmul_rn(cx, iz);
-    v = __fmul_rn(cy, iz);
-    return p.cz > 0.0f;
+    p.iz = rcp_approx(p.cz);
+    u = __fmul_rn(cx, p.iz);
+    v = __fmul_rn(cy, p.iz);
+    return p.cz > 1.17549435e-38f;
 }
 
 // G = exp(-(u^2+v^2)/2)  (raster.hpp:52)
@@ -146,6 +160,16 @@ cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, uint2* rects,
                            uint32_t* depth_bits, cudaStream_t st);
 cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
                          cudaStream_t st);
+
+// gb_composite.cu: K3/K4 with several pixels per thread (tile sizes 8 and 16)
+bool mp_supported(int ts);
+cudaError_t launch_forward_mp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                              const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                              float* color, float* trans, int32_t* last, cudaStream_t st);
+cudaError_t launch_backward_mp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                               const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                               const float* trans, const int32_t* last, const float* image_grad, float* accum,
+                               float* grid_grad, cudaStream_t st);
 
 __device__ __forceinline__ uint32_t float_order_key(float d) {
     uint32_t b = __float_as_uint(d == 0.0f ? 0.0f : d);  // -0 sorts as +0 (double compare)

@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeade
     int x0, x1, y0, y1;
     if (!cull_rect(p, k, g, x0, x1, y0, y1)) {
         counts[k] = 0;
+        depth_bits[k] = 0xffffffffu;  // culled: sorts after every binned primitive (K2a)
         return;
     }
     const int tx0 = x0 / p.ts, tx1 = x1 / p.ts, ty0 = y0 / p.ts, ty1 = y1 / p.ts;

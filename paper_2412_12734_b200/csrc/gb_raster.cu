@@ -21,16 +21,17 @@
 // (a) the caller's texel gradients and (b) a 48 B per-primitive
 // screen-space accumulator that K5 chains to the raw parameters.
 #include <cstdlib>
+#include <cstring>
 
-#include "gb_internal.cuh"
+#include "gb_compose.cuh"
 
 namespace gb {
 
-constexpr unsigned kFull = 0xffffffffu;
 
 #ifdef GB_DEBUG_COUNTERS
 // development counters (not built by default): [0] warp-entries tested, [1] passing the box,
-// [2] with an active lane, [3] active lanes, [4] texel groups, [5] corner-only groups
+// [2] with an active lane, [3] active lanes, [4] uniform-cell texel groups, [5] per-lane texel groups,
+// [6] active entries with both 4x4 halves active, [7] with both 8x2 halves active
 __device__ unsigned long long g_dbg[8];
 #define GB_DBG(i, v) atomicAdd(&g_dbg[i], (unsigned long long)(v))
 extern "C" __attribute__((visibility("default"))) int gb_debug_counters(unsigned long long* out, int reset) {
@@ -44,35 +45,6 @@ extern "C" __attribute__((visibility("default"))) int gb_debug_counters(unsigned
 #else
 #define GB_DBG(i, v)
 #endif
-
-template <int NT>
-__device__ __forceinline__ int tex_n(int n_rt) {
-    return NT ? NT : n_rt;
-}
-
-struct Bilin {
-    int o00;  // offset of texel (i_u, i_v) channel 0
-    float fu, fv;
-    float w00, w10, w01, w11;
-};
-
-__device__ __forceinline__ void bilin_setup(float u, float v, int N, const RasterConst& rc, Bilin& b) {
-    int iu, iv;
-    float s = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
-    s = fminf(fmaxf(s, 0.0f), (float)(N - 1));
-    iu = min((int)floorf(s), N - 2);
-    b.fu = __fsub_rn(s, (float)iu);
-    float t = __fmaf_rn(v, rc.tex_scale, rc.tex_offset);
-    t = fminf(fmaxf(t, 0.0f), (float)(N - 1));
-    iv = min((int)floorf(t), N - 2);
-    b.fv = __fsub_rn(t, (float)iv);
-    b.o00 = (iu * N + iv) * 3;
-    const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
-    b.w00 = gu * gv;
-    b.w10 = b.fu * gv;
-    b.w01 = gu * b.fv;
-    b.w11 = b.fu * b.fv;
-}
 
 // ---------------------------------------------------------------------------
 // asynchronous batch staging: TMA bulk copies (n even) or cp.async (n odd)
@@ -198,9 +170,6 @@ __device__ __forceinline__ void issue_batch(const int32_t* __restrict__ values, 
     }
 }
 
-__device__ __forceinline__ bool box_miss(const float4& box, float bx0, float bx1, float by0, float by1) {
-    return box.y < bx0 || box.x > bx1 || box.w < by0 || box.z > by1;
-}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -404,51 +373,6 @@ __device__ __forceinline__ float reduce_scatter(float (&a)[V], int lane) {
     return r;
 }
 
-// Warp sum of NV <= 16 per-lane values through a per-warp shared-memory
-// transpose (scratch: kRedRows x kRedStride floats): lane l writes value i
-// to row i, column l; lane l then sums half (l & 1) of row l >> 1 with four
-// conflict-free 128-bit loads and one shuffle.  ~NV + 22 instructions
-// versus ~4 NV for a shuffle butterfly.  Returns the row l >> 1 total.
-constexpr int kRedRows = 16;
-constexpr int kRedStride = 36;  // 32 lanes + 4 pad: rows land in distinct bank quads
-
-template <int NV>
-__device__ __forceinline__ float smem_reduce(const float (&v)[NV], float* scratch, int lane) {
-    __syncwarp();  // previous readers of the scratch are done
-#pragma unroll
-    for (int i = 0; i < NV; ++i) scratch[i * kRedStride + lane] = v[i];
-    __syncwarp();
-    const int row = lane >> 1;
-    float acc = 0.0f;
-    if (row < NV) {
-        const float4* q = reinterpret_cast<const float4*>(scratch + row * kRedStride + (lane & 1) * 16);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float4 a = q[k];
-            acc += (a.x + a.y) + (a.z + a.w);
-        }
-    }
-    return acc + __shfl_xor_sync(kFull, acc, 1);
-}
-
-__device__ __forceinline__ void red_add(float* p, float v) {
-    if (v != 0.0f) atomicAdd(p, v);
-}
-
-// p[0..2] += (a, b, c) with one 8-byte vector red and one scalar red (branch-free on alignment)
-__device__ __forceinline__ void red3(float* p, float a, float b, float c) {
-    const bool even = (reinterpret_cast<uintptr_t>(p) & 7) == 0;
-    float2* pv = reinterpret_cast<float2*>(even ? p : p + 1);
-    atomicAdd(pv, even ? make_float2(a, b) : make_float2(b, c));
-    atomicAdd(even ? p + 2 : p, even ? c : a);
-}
-
-// texel corner k (0..3 = 00, 10, 01, 11) channel c -> float offset from the base texel
-__device__ __forceinline__ int corner_offset(int i, int N) {
-    const int k = i / 3, c = i - 3 * (i / 3);
-    return ((k & 1) ? 3 * N : 0) + ((k & 2) ? 3 : 0) + c;
-}
-
 // ---------------------------------------------------------------------------
 // K4 backward
 // ---------------------------------------------------------------------------
@@ -484,7 +408,12 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
             }
             const unsigned act = __ballot_sync(kFull, on);
             if (act == 0) return;
-            if (lane == 0) { GB_DBG(2, 1); GB_DBG(3, __popc(act)); }
+            if (lane == 0) {
+                GB_DBG(2, 1);
+                GB_DBG(3, __popc(act));
+                GB_DBG(6, (act & 0x0F0F0F0Fu) && (act & 0xF0F0F0F0u));  // both 4x4 halves active
+                GB_DBG(7, (act & 0x0000FFFFu) && (act & 0xFFFF0000u));  // both 8x2 halves active
+            }
 
             float red[16];  // screen-space sums (NS of 16 slots)
 #pragma unroll
@@ -494,7 +423,7 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
             for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
             int tbase = -1;
             if (on) {
-                T = __fdiv_rn(T, __fsub_rn(1.0f, alpha));  // raster.hpp:333
+                T = __fdividef(T, __fsub_rn(1.0f, alpha));  // raster.hpp:333
                 float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
                 const float aT = alpha * T;
                 const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
@@ -553,7 +482,7 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
                     red[6] = op;
                 } else {
                     // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
-                    const float iz = 1.0f / pt.cz;
+                    const float iz = pt.iz;
                     const float gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
                     red[0] = gc0;
                     red[1] = gc1;
@@ -836,6 +765,7 @@ __global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict
             pass = !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
         }
         unsigned mask = __ballot_sync(kFull, pass);
+        if (lane == 0) GB_DBG(1, __popc(mask));
         while (mask) {
             const int bit = 31 - __clz(mask);
             mask &= ~(1u << bit);
@@ -856,6 +786,18 @@ __global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict
 static int tune_env(const char* name, int dflt) {  // development knob: GB_TUNE_* overrides
     const char* v = getenv(name);
     return v ? atoi(v) : dflt;
+}
+
+// Compositor variant: 1 = one pixel per thread reading through L1 (default),
+// 0 = two pixels per thread (gb_composite.cu; tile sizes 8 and 16),
+// 2 = one pixel per thread with TMA bulk-copy staging.  GB_COMPOSITOR=direct|
+// mp|staged selects one explicitly (A/B measurements and parity tests).
+static int compositor_variant() {
+    const char* v = getenv("GB_COMPOSITOR");
+    if (!v) return 1;
+    if (!strcmp(v, "mp")) return 0;
+    if (!strcmp(v, "staged")) return 2;
+    return 1;
 }
 
 int pick_batch(int N, int stage_budget = 13312) {
@@ -928,7 +870,10 @@ cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* rang
                            const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
                            float* color, float* trans, int32_t* last, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
-    if (tune_env("GB_TUNE_DIRECT", 0) & 1) {
+    const int variant = compositor_variant();
+    if (variant == 0 && mp_supported(ts))
+        return launch_forward_mp(mode, n, tiles, ts, ranges, values, hdr, tex, cc, rc, color, trans, last, st);
+    if (variant != 2) {
         const int threads = ((ts * ts + 31) / 32) * 32;
         if (mode == GB_MODE_ORTHO) {
             GB_DISPATCH_N(fwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, color,
@@ -955,7 +900,11 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
                             const float* trans, const int32_t* last, const float* image_grad, float* accum,
                             float* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
-    if (tune_env("GB_TUNE_DIRECT", 0) & 2) {
+    const int variant = compositor_variant();
+    if (variant == 0 && mp_supported(ts))
+        return launch_backward_mp(mode, n, tiles, ts, ranges, values, hdr, tex, cc, rc, trans, last, image_grad,
+                                  accum, grid_grad, st);
+    if (variant != 2) {
         const int threads = ((ts * ts + 31) / 32) * 32;
         if (mode == GB_MODE_ORTHO) {
             GB_DISPATCH_N(bwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, trans, last,

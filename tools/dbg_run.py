@@ -1,6 +1,6 @@
 """Print the K4 development counters for one configs[2]-like view (needs dbg/libgb_raster.so)."""
 import ctypes as C, os, sys
-os.environ["GB_LIB_PATH"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "dbg", "libgb_raster.so")
+os.environ["GB_LIB_PATH"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "_dbg", "libgb_raster.so")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2412_12734_b200 as gb, paper_2412_12734_b200.scenes as sc
@@ -18,4 +18,5 @@ torch.cuda.synchronize()
 _lib.lib.gb_debug_counters(cnt, 0)
 v = list(cnt)
 print("P", b.total, "warp-entries", v[0], "box-pass", v[1], "active", v[2], "active lanes", v[3],
-      "groups", v[4], "lanes/active", v[3] / max(1, v[2]), "groups/active", v[4] / max(1, v[2]))
+      "uniform groups", v[4], "per-lane groups", v[5], "lanes/active", v[3] / max(1, v[2]),
+      "both 4x4 halves", v[6] / max(1, v[2]), "both 8x2 halves", v[7] / max(1, v[2]))

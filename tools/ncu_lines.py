@@ -71,7 +71,7 @@ def main():
         line = lm.get(a - base, (0, ""))[0]
         by_s[line] += s
         by_i[line] += i
-    src = open(os.path.join(ROOT, "paper_2412_12734_b200", "csrc", "gb_raster.cu")).read().splitlines()
+    src = open(os.path.join(ROOT, "paper_2412_12734_b200", "csrc", os.environ.get("SRC", "gb_raster.cu"))).read().splitlines()
     ts, ti = sum(by_s.values()), sum(by_i.values())
     print(f"total stall samples {ts}, warp instructions {ti}")
     for line, i in by_i.most_common(top):
