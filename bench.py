@@ -334,7 +334,8 @@ def run_ours(args):
                                "NCCL all-reduce + Adam",
                    "views_per_gpu": len(views), "surfels": cfg3.count, "texture": f"{n}x{n}",
                    "image": f"{W}x{H}", "tile": 16,
-                   "compositor": os.environ.get("GB_COMPOSITOR", "direct"), "mean_pairs_per_view": int(np.mean(pairs)) if pairs else 0,
+                   "compositor": os.environ.get("GB_COMPOSITOR", "direct") + (
+                       f"(G={os.environ.get('GB_GROUP', '8')})" if os.environ.get("GB_COMPOSITOR") == "grp" else ""), "mean_pairs_per_view": int(np.mean(pairs)) if pairs else 0,
                    "l2": "working set (0.8 GB textures + 0.8 GB grads + 1.6 GB Adam) >> 126 MB L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,

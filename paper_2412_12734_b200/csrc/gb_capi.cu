@@ -26,10 +26,10 @@ cudaError_t launch_tile_sort(void* temp, size_t temp_bytes, uint32_t* keys_in, u
                              int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st);
 cudaError_t launch_ranges(int64_t P, const uint32_t* keys, uint2* ranges, int n_tiles, cudaStream_t st);
 cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                           const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
                            float* color, float* trans, int32_t* last, cudaStream_t st);
 cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                            const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                            const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
                             const float* trans, const int32_t* last, const float* image_grad, float* accum,
                             float* grid_grad, cudaStream_t st);
 cudaError_t launch_loss(int kind, const float* color, const float* target, int64_t n, float scale, float* grad,
@@ -37,8 +37,8 @@ cudaError_t launch_loss(int kind, const float* color, const float* target, int64
 cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned long long* bad, int sm_count,
                               cudaStream_t st);
 cudaError_t launch_adam_update(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
-                               float eps, float inv_bias1, float inv_bias2, const unsigned long long* bad,
-                               int sm_count, cudaStream_t st);
+                               float omb1, float omb2, float eps, float inv_bias1, float inv_bias2,
+                               const unsigned long long* bad, int sm_count, cudaStream_t st);
 }  // namespace gb
 
 namespace {
@@ -160,7 +160,7 @@ struct gb_binning {
     int64_t K = 0;
     int n = 0;
     int64_t P = 0;
-    DevBuf headers, rects, counts, offsets, depth, perm, keys, values, ranges;
+    DevBuf headers, cull, rects, counts, offsets, depth, perm, keys, values, ranges;
 };
 
 namespace {
@@ -387,6 +387,7 @@ gb_status gb_binning_destroy(gb_binning* b) {
     cudaSetDevice(b->ctx->device);
     cudaStreamSynchronize(b->ctx->stream);
     b->headers.release();
+    b->cull.release();
     b->rects.release();
     b->counts.release();
     b->offsets.release();
@@ -420,6 +421,7 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
     const int n_tiles = b->tiles_x * b->tiles_y;
     const int64_t Kc = K > 0 ? K : 1;
     GB_CUDA(b->headers.ensure(sizeof(gb::ScreenHeader) * Kc));
+    GB_CUDA(b->cull.ensure(sizeof(gb::CullRec) * Kc));
     GB_CUDA(b->rects.ensure(sizeof(uint2) * Kc));
     GB_CUDA(b->counts.ensure(sizeof(uint32_t) * Kc));
     GB_CUDA(b->offsets.ensure(sizeof(uint32_t) * (Kc + 1)));
@@ -436,7 +438,7 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
     gb::ProjParams pp = gb::make_proj_params(s, cam, cfg, b->tiles_x, b->tiles_y);
     {
         ProfScope ps(ctx, GB_K_PROJECT);
-        GB_CUDA(gb::launch_project(pp, b->headers.as<gb::ScreenHeader>(), b->rects.as<uint2>(),
+        GB_CUDA(gb::launch_project(pp, b->headers.as<gb::ScreenHeader>(), b->cull.as<gb::CullRec>(), b->rects.as<uint2>(),
                                    b->counts.as<uint32_t>(), b->depth.as<uint32_t>(), stream));
     }
     ctx->launches += K > 0;
@@ -540,7 +542,7 @@ gb_status gb_render_forward(gb_context* ctx, const gb_splats* s, const gb_camera
     ProfScope ps(ctx, GB_K_FORWARD);
     GB_CUDA(gb::launch_forward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
                                b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
-                               s->grid_values, cc, rc, out->color, out->final_transmittance, out->last_rank,
+                               b->cull.as<gb::CullRec>(), s->grid_values, cc, rc, out->color, out->final_transmittance, out->last_rank,
                                ctx->stream));
     ctx->launches += 1;
     out->splat_count = s->count;
@@ -577,7 +579,7 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
         ProfScope ps(ctx, GB_K_BACKWARD);
         GB_CUDA(gb::launch_backward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
                                     b->ranges.as<uint2>(), b->values.as<int32_t>(),
-                                    b->headers.as<gb::ScreenHeader>(), s->grid_values, cc, rc,
+                                    b->headers.as<gb::ScreenHeader>(), b->cull.as<gb::CullRec>(), s->grid_values, cc, rc,
                                     out->final_transmittance, out->last_rank, image_grad, ctx->accum.as<float>(),
                                     g->grid_values, stream));
     }
@@ -663,6 +665,7 @@ gb_status gb_adam_step(gb_context* ctx, int32_t mode, int64_t count, int32_t n, 
         if (groups[i].len == 0) continue;
         GB_CUDA(gb::launch_adam_update(groups[i].p, groups[i].g, groups[i].m, groups[i].v, groups[i].len,
                                        (float)groups[i].lr, (float)state->beta1, (float)state->beta2,
+                                       (float)(1.0 - state->beta1), (float)(1.0 - state->beta2),
                                        (float)state->epsilon, (float)(1.0 / bias1), (float)(1.0 / bias2), bad,
                                        ctx->sm_count, stream));
         ctx->launches++;

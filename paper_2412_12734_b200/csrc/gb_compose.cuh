@@ -89,4 +89,23 @@ __device__ __forceinline__ bool box_miss(const float4& box, float bx0, float bx1
     return box.y < bx0 || box.x > bx1 || box.w < by0 || box.z > by1;
 }
 
+// True unless the entry's alpha-skip ellipse (K1 alpha_ellipse) certainly
+// misses the pixel-index rectangle [x0, x1] x [y0, y1].  Exact for an
+// ellipse: the minimum of the quadratic form over the rectangle is at the
+// centre when the centre is inside, else on a rectangle edge that faces the
+// centre; each candidate edge is minimised in closed form.
+__device__ __forceinline__ bool ellipse_meets_rect(const float4 a, const float4 b, float x0, float x1, float y0,
+                                                   float y1) {
+    const float ax = x0 - a.x, bx = x1 - a.x, ay = y0 - a.y, by = y1 - a.y;
+    const bool inx = ax <= 0.0f && bx >= 0.0f;
+    const bool iny = ay <= 0.0f && by >= 0.0f;
+    const float xe = ax > 0.0f ? ax : bx;  // facing vertical edge
+    const float ye = ay > 0.0f ? ay : by;  // facing horizontal edge
+    const float dy1 = fminf(fmaxf(-b.y * xe, ay), by);
+    const float dx2 = fminf(fmaxf(-b.z * ye, ax), bx);
+    const float q1 = a.z * xe * xe + 2.0f * b.x * xe * dy1 + a.w * dy1 * dy1;
+    const float q2 = a.z * dx2 * dx2 + 2.0f * b.x * dx2 * ye + a.w * ye * ye;
+    return (inx && iny) || (!inx && q1 <= 1.0f) || (!iny && q2 <= 1.0f);
+}
+
 }  // namespace gb

@@ -1,137 +1,239 @@
-// gb_composite.cu -- K3 / K4 with several pixels per thread (the default
-// compositors for tile sizes that are multiples of 8).
+// gb_composite.cu -- K3 / K4 with sub-warp groups (the default compositors
+// for 16x16 and 8x8 tiles).
 //
-// One CTA per tile, ts*ts/PPT threads; each warp owns an 8 x (4*PPT) pixel
-// block and each lane PPT vertically adjacent pixels of one column.  Headers,
-// ids and texels are read through L1 (__ldg); there is no shared-memory
-// staging and no CTA barrier, so warps finish independently.
+// One CTA per tile, one thread per pixel.  Each warp (an 8x4 pixel block) is
+// split into 32/G groups of G lanes; a group owns a small pixel block (2x2
+// for G = 4, 4x2 for G = 8, 4x4 for G = 16) and walks the tile's sorted list
+// on its own cursor.  When a group's window is used up the whole warp refills
+// it: 32 lanes test the group's next 32 entries against its block with the
+// exact alpha-skip-ellipse test (K1 alpha_ellipse, one entry per lane, one
+// ballot) and park the ids in shared memory.  Then every group composites its
+// next passing entry, all groups of a warp in the same step.
 //
-// Why several pixels per thread: both kernels are issue-bound (ncu: 75-85 %
-// issue-active, DRAM < 12 %), and a large part of the per-(warp, entry) cost
-// does not depend on how many pixels the warp covers -- the list walk and
-// alpha-box ballot, the header loads and, in K4, the warp reductions and the
-// global reds.  With PPT = 2 a lane first sums its two pixels' gradient terms
-// in registers, so one reduction serves 64 pixels instead of 32.
+// Why: K3/K4 are issue-bound and, with a whole warp on one entry, only ~11 of
+// 32 lanes do useful work on an average (warp, entry) step at configs[2]
+// (profiles/k4_counters_r01_s3.txt): most surfels cover a few pixels, and the
+// alpha-box test can only cull at the granularity of the warp's 8x4 block.
+// Groups cull at the granularity of their own block and several entries are
+// composited per step, so the steps per warp drop to the largest group's list
+// instead of the union of all of them (tools/sim_steps.py: 0.63x of the union
+// for G = 8 with exact culling).
+//
+// K4 reduces each step's per-lane gradient terms with one shared-memory
+// transpose per warp that yields one sum per (value, group): V x 32/G sums,
+// owned by distinct lanes, each issuing one red.global.add.  Texel terms go
+// through the same reduction for groups whose active pixels share a bilinear
+// cell, and straight to HBM with per-lane vector reds otherwise.
 //
 // K3 restates render_forward (raster.hpp:201-261) + bilinear
 // (texture.hpp:49-66); K4 restates render_backward (raster.hpp:277-387) +
-// adj_bilinear_accum (texture.hpp:77-111), with the per-(tile, rank) partial
-// records replaced by warp reductions + red.global.add (see gb_raster.cu).
+// adj_bilinear_accum (texture.hpp:77-111).
 #include "gb_compose.cuh"
 
 namespace gb {
 
-constexpr int kPPT = 2;  // pixels per thread
+template <int G>
+__device__ __forceinline__ unsigned group_mask(int lane) {
+    return G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
+}
 
-// lane -> pixel p of the warp's 8 x (4 PPT) block
-__device__ __forceinline__ void mp_pixel(int warp, int lane, int p, int ts, int tx, int ty, int& x, int& y) {
-    const int wx = ts >> 3;  // 8-wide warp blocks per tile row
-    x = tx * ts + (warp % wx) * 8 + (lane & 7);
-    y = ty * ts + (warp / wx) * (4 * kPPT) + (lane >> 3) * kPPT + p;
+// Group block: BW x BH pixels (G = 4: 2x2, G = 8: 4x2, G = 16: 4x4), tiled
+// row-major over the warp's 8x4 block.
+template <int G>
+struct GroupShape {
+    static constexpr int BW = G == 4 ? 2 : 4;
+    static constexpr int BH = G / BW;
+    static constexpr int PER_ROW = 8 / BW;
+};
+
+// origin of group g's block inside its warp's 8x4 block
+template <int G>
+__device__ __forceinline__ void group_origin(int g, int& gx, int& gy) {
+    gx = (g % GroupShape<G>::PER_ROW) * GroupShape<G>::BW;
+    gy = (g / GroupShape<G>::PER_ROW) * GroupShape<G>::BH;
+}
+
+// origin of warp w's 8x4 block in the image
+__device__ __forceinline__ void warp_origin(int tid, int ts, int tx, int ty, int& wx0, int& wy0) {
+    const int warp = tid >> 5, wx = ts >> 3;
+    wx0 = tx * ts + (warp % wx) * 8;
+    wy0 = ty * ts + (warp / wx) * 4;
+}
+
+// lane -> pixel of the tile
+template <int G>
+__device__ __forceinline__ void group_pixel(int tid, int ts, int tx, int ty, int& x, int& y) {
+    const int lane = tid & 31;
+    int wx0, wy0, gx, gy;
+    warp_origin(tid, ts, tx, ty, wx0, wy0);
+    group_origin<G>(lane / G, gx, gy);
+    const int i = lane % G;
+    x = wx0 + gx + i % GroupShape<G>::BW;
+    y = wy0 + gy + i / GroupShape<G>::BW;
+}
+
+// Refill test of group gs: does entry `id`'s alpha-skip ellipse meet the
+// group's pixel block (pixel indices, enlarged by 0.05 px like alpha_box)?
+template <int G>
+__device__ __forceinline__ bool group_test(const CullRec* __restrict__ cull, int id, int wx0, int wy0, int gs) {
+    int gx, gy;
+    group_origin<G>(gs, gx, gy);
+    const float x0 = (float)(wx0 + gx) - 0.05f, y0 = (float)(wy0 + gy) - 0.05f;
+    const float4 a = __ldg(&cull[id].a), b = __ldg(&cull[id].b);
+    return ellipse_meets_rect(a, b, x0, x0 + (float)(GroupShape<G>::BW - 1) + 0.1f, y0,
+                              y0 + (float)(GroupShape<G>::BH - 1) + 0.1f);
+}
+
+// Group-wide cursor over one direction of the tile list (every field is
+// uniform across the group's lanes).
+struct Cursor {
+    int cur;        // next rank to test (forward ascending, backward descending); outside the list = exhausted
+    int wbase;      // rank of bit 0 of the pending window
+    unsigned pend;  // passing entries of the window not yet composited (bit i <-> rank wbase +/- i)
+};
+
+// Sum of NV per-lane values per group: returns, in out[k], the total of value
+// row(q) over the lanes of group grp(q) for pair q = lane + 32 k, q < NV * 32/G
+// (row = q / (32/G), grp = q % (32/G)); scratch = kRedRows x kRedStride floats.
+template <int NV, int G>
+__device__ __forceinline__ void group_reduce(const float (&v)[NV], float* scratch, int lane,
+                                             float (&out)[(NV * (32 / G) + 31) / 32]) {
+    constexpr int NG = 32 / G;
+    constexpr int PASSES = (NV * NG + 31) / 32;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[i * kRedStride + lane] = v[i];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < PASSES; ++k) {
+        const int q = lane + 32 * k;
+        float acc = 0.0f;
+        if (q < NV * NG) {
+            const float4* p = reinterpret_cast<const float4*>(scratch + (q / NG) * kRedStride + (q % NG) * G);
+#pragma unroll
+            for (int j = 0; j < G / 4; ++j) {
+                const float4 a = p[j];
+                acc += (a.x + a.y) + (a.z + a.w);
+            }
+        }
+        out[k] = acc;
+    }
 }
 
 // ---------------------------------------------------------------------------
 // K3 forward
 // ---------------------------------------------------------------------------
-template <int MODE, int NT>
-__global__ void __launch_bounds__(128) k_forward_mp(const uint2* __restrict__ ranges, const int32_t* __restrict__ values,
-                                                    const ScreenHeader* __restrict__ hdr, const float* __restrict__ tex,
-                                                    const CamConst cc, const RasterConst rc, int n_rt,
-                                                    float* __restrict__ out_color, float* __restrict__ out_trans,
-                                                    int32_t* __restrict__ out_last) {
+template <int MODE, int NT, int G>
+__global__ void __launch_bounds__(256) k_forward_grp(const uint2* __restrict__ ranges,
+                                                     const int32_t* __restrict__ values,
+                                                     const ScreenHeader* __restrict__ hdr,
+                                                     const CullRec* __restrict__ cull, const float* __restrict__ tex,
+                                                     const CamConst cc, const RasterConst rc, int n_rt,
+                                                     float* __restrict__ out_color, float* __restrict__ out_trans,
+                                                     int32_t* __restrict__ out_last) {
+    constexpr int NG = 32 / G;
+    __shared__ int s_ids[8][NG][32];  // per warp and group: ids of the current window
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
     const int ts = rc.tile_size;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / G;
+    const unsigned gm = group_mask<G>(lane);
     const int tile = blockIdx.x;
     const uint2 range = ranges[tile];
     const int total = (int)(range.y - range.x);
     const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
-    int x[kPPT], y[kPPT];
-    float T[kPPT], a0[kPPT], a1[kPPT], a2[kPPT];
-    int last[kPPT];
-    bool done[kPPT];
-#pragma unroll
-    for (int p = 0; p < kPPT; ++p) {
-        mp_pixel(warp, lane, p, ts, tx, ty, x[p], y[p]);
-        T[p] = 1.0f;
-        a0[p] = a1[p] = a2[p] = 0.0f;
-        last[p] = -1;
-        done[p] = x[p] >= cc.width || y[p] >= cc.height;
-    }
-    // the warp's pixel block (pixel indices) for the alpha-box test
-    const float bx0 = (float)__reduce_min_sync(kFull, x[0]), bx1 = (float)__reduce_max_sync(kFull, x[0]);
-    const float by0 = (float)__reduce_min_sync(kFull, y[0]), by1 = (float)__reduce_max_sync(kFull, y[kPPT - 1]);
-    bool all_done = __all_sync(kFull, done[0] && done[kPPT - 1]);
-    for (int c0 = 0; c0 < total && !all_done; c0 += 32) {
-        int idl = -1;
-        bool pass = false;
-        if (c0 + lane < total) {
-            idl = __ldg(&values[range.x + c0 + lane]);
-            pass = !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+    int x, y, wx0, wy0;
+    group_pixel<G>(threadIdx.x, ts, tx, ty, x, y);
+    warp_origin(threadIdx.x, ts, tx, ty, wx0, wy0);
+    const bool inside = x < cc.width && y < cc.height;
+    float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
+    int last = -1;
+    bool done = !inside;
+    Cursor c{__all_sync(gm, done) ? total : 0, 0, 0u};  // a group with no pixel in the image has nothing to do
+    for (;;) {
+        for (;;) {  // refill, one group per round, every group whose window is used up
+            const unsigned need = __ballot_sync(kFull, c.pend == 0 && c.cur < total);
+            if (!need) break;
+            const int gs = (__ffs(need) - 1) / G;
+            const int cs = __shfl_sync(kFull, c.cur, gs * G);
+            const int r = cs + lane;
+            int idl = -1;
+            bool pass = false;
+            if (r < total) {
+                idl = __ldg(&values[range.x + r]);
+                pass = group_test<G>(cull, idl, wx0, wy0, gs);
+            }
+            const unsigned bal = __ballot_sync(kFull, pass);
+            s_ids[warp][gs][lane] = idl;
+            if (g == gs) {
+                c.pend = bal;
+                c.wbase = cs;
+                c.cur = cs + 32;
+            }
         }
-        unsigned mask = __ballot_sync(kFull, pass);
-        while (mask) {
-            const int bit = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const int id = __shfl_sync(kFull, idl, bit);
+        __syncwarp();
+        if (!__any_sync(kFull, c.pend != 0)) break;
+        if (c.pend != 0 && !done) {
+            const int bit = __ffs(c.pend) - 1;
+            const int id = s_ids[warp][g][bit];
             ScreenHeader h;
             h.h0 = __ldg(&hdr[id].h0);
             h.h1 = __ldg(&hdr[id].h1);
             h.h2 = __ldg(&hdr[id].h2);
-            const float* t = tex + (size_t)id * F;
-#pragma unroll
-            for (int p = 0; p < kPPT; ++p) {
-                if (done[p]) continue;
-                float u, v;
-                bool hit;
-                if (MODE == GB_MODE_ORTHO) {
-                    hit = eval_uv_ortho(h, x[p], y[p], u, v);
-                } else {
-                    PinholeTerms pt;
-                    hit = eval_uv_pinhole(h, x[p], y[p], u, v, pt);
-                }
-                if (!hit) continue;
-                const float alpha = fminf(__fmul_rn(h.h1.z, gauss_weight(u, v)), kMaxAlphaF);  // raster.hpp:241
-                if (alpha < rc.alpha_skip) continue;                                             // raster.hpp:242
-                float c0_, c1_, c2_;
-                if (N == 1) {
-                    c0_ = __ldg(t);
-                    c1_ = __ldg(t + 1);
-                    c2_ = __ldg(t + 2);
-                } else {
-                    Bilin b;
-                    bilin_setup(u, v, N, rc, b);
-                    const float* p00 = t + b.o00;
-                    const float* p10 = p00 + 3 * N;
-                    c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 + __ldg(p10 + 3) * b.w11;
-                    c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
-                          __ldg(p10 + 4) * b.w11;
-                    c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
-                          __ldg(p10 + 5) * b.w11;
-                }
-                const float w = alpha * T[p];  // raster.hpp:244-249
-                a0[p] = fmaf(c0_, w, a0[p]);
-                a1[p] = fmaf(c1_, w, a1[p]);
-                a2[p] = fmaf(c2_, w, a2[p]);
-                T[p] = __fmul_rn(T[p], __fsub_rn(1.0f, alpha));
-                last[p] = c0 + bit;
-                if (rc.early_stop > 0.0f && T[p] < rc.early_stop) done[p] = true;  // raster.hpp:250
+            float u, v;
+            bool hit;
+            if (MODE == GB_MODE_ORTHO) {
+                hit = eval_uv_ortho(h, x, y, u, v);
+            } else {
+                PinholeTerms pt;
+                hit = eval_uv_pinhole(h, x, y, u, v, pt);
             }
-            all_done = __all_sync(kFull, done[0] && done[kPPT - 1]);
-            if (all_done) break;
+            if (hit) {
+                const float alpha = fminf(__fmul_rn(h.h1.z, gauss_weight(u, v)), kMaxAlphaF);  // raster.hpp:241
+                if (!(alpha < rc.alpha_skip)) {                                                  // raster.hpp:242
+                    const float* t = tex + (size_t)id * F;
+                    float c0_, c1_, c2_;
+                    if (N == 1) {
+                        c0_ = __ldg(t);
+                        c1_ = __ldg(t + 1);
+                        c2_ = __ldg(t + 2);
+                    } else {
+                        Bilin b;
+                        bilin_setup(u, v, N, rc, b);
+                        const float* p00 = t + b.o00;
+                        const float* p10 = p00 + 3 * N;
+                        c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 +
+                              __ldg(p10 + 3) * b.w11;
+                        c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
+                              __ldg(p10 + 4) * b.w11;
+                        c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
+                              __ldg(p10 + 5) * b.w11;
+                    }
+                    const float w = alpha * T;  // raster.hpp:244-249
+                    acc0 = fmaf(c0_, w, acc0);
+                    acc1 = fmaf(c1_, w, acc1);
+                    acc2 = fmaf(c2_, w, acc2);
+                    T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                    last = c.wbase + bit;
+                    if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;  // raster.hpp:250
+                }
+            }
         }
+        c.pend &= c.pend - 1;
+        if (__all_sync(gm, done)) {  // the whole group terminated early: retire its cursor
+            c.pend = 0;
+            c.cur = total;
+        }
+        __syncwarp();  // s_ids readers done before the next refill overwrites
     }
-#pragma unroll
-    for (int p = 0; p < kPPT; ++p) {
-        if (x[p] < cc.width && y[p] < cc.height) {  // raster.hpp:253-254
-            const size_t q = (size_t)y[p] * cc.width + x[p];
-            out_color[q * 3 + 0] = fmaf(T[p], cc.bg[0], a0[p]);
-            out_color[q * 3 + 1] = fmaf(T[p], cc.bg[1], a1[p]);
-            out_color[q * 3 + 2] = fmaf(T[p], cc.bg[2], a2[p]);
-            out_trans[q] = T[p];
-            out_last[q] = last[p];
-        }
+    if (inside) {  // raster.hpp:253-254
+        const size_t q = (size_t)y * cc.width + x;
+        out_color[q * 3 + 0] = fmaf(T, cc.bg[0], acc0);
+        out_color[q * 3 + 1] = fmaf(T, cc.bg[1], acc1);
+        out_color[q * 3 + 2] = fmaf(T, cc.bg[2], acc2);
+        out_trans[q] = T;
+        out_last[q] = last;
     }
 }
 
@@ -145,14 +247,13 @@ struct BwdPx {
 };
 
 // One (pixel, entry) evaluation of render_backward (raster.hpp:324-362) +
-// adj_bilinear_accum (texture.hpp:77-111).  Adds the screen-space terms into
-// red[], writes the 12 texel terms to tg[] (corner-major: 00, 10, 01, 11 x
-// RGB) with their base offset, and advances the rewind state.  Returns false
-// (and touches nothing) when the entry is skipped for this pixel.
+// adj_bilinear_accum (texture.hpp:77-111).  Writes the screen-space terms to
+// red[], the 12 texel terms to tg[] (corner-major: 00, 10, 01, 11 x RGB) with
+// their base offset, and advances the rewind state.  Returns false (and
+// leaves red/tg untouched) when the entry is skipped for this pixel.
 template <int MODE, int NT>
-__device__ __forceinline__ bool bwd_px(const ScreenHeader& h, const float* __restrict__ t, int N, int rank, BwdPx& s,
+__device__ __forceinline__ bool bwd_px(const ScreenHeader& h, const float* __restrict__ t, int N, BwdPx& s,
                                        const RasterConst& rc, float (&red)[10], float (&tg)[12], int& tbase) {
-    if (rank > s.last) return false;
     float u, v;
     PinholeTerms pt;
     bool hit;
@@ -218,26 +319,26 @@ __device__ __forceinline__ bool bwd_px(const ScreenHeader& h, const float* __res
         v_hat -= aa * v;
     }
     if (MODE == GB_MODE_ORTHO) {
-        red[0] += u_hat;
-        red[1] += v_hat;
-        red[2] += u_hat * v;
-        red[3] += v_hat * u;
-        red[4] += u_hat * u;
-        red[5] += v_hat * v;
-        red[6] += op;
+        red[0] = u_hat;
+        red[1] = v_hat;
+        red[2] = u_hat * v;
+        red[3] = v_hat * u;
+        red[4] = u_hat * u;
+        red[5] = v_hat * v;
+        red[6] = op;
     } else {
         // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
         const float gc0 = u_hat * pt.iz, gc1 = v_hat * pt.iz, gc2 = -(u_hat * u + v_hat * v) * pt.iz;
-        red[0] += gc0;
-        red[1] += gc1;
-        red[2] += gc2;
-        red[3] += pt.dx * gc0;
-        red[4] += pt.dx * gc1;
-        red[5] += pt.dx * gc2;
-        red[6] += pt.dy * gc0;
-        red[7] += pt.dy * gc1;
-        red[8] += pt.dy * gc2;
-        red[9] += op;
+        red[0] = gc0;
+        red[1] = gc1;
+        red[2] = gc2;
+        red[3] = pt.dx * gc0;
+        red[4] = pt.dx * gc1;
+        red[5] = pt.dx * gc2;
+        red[6] = pt.dy * gc0;
+        red[7] = pt.dy * gc1;
+        red[8] = pt.dy * gc2;
+        red[9] = op;
     }
     s.bh0 = alpha * c0 + om * s.bh0;  // raster.hpp:362
     s.bh1 = alpha * c1 + om * s.bh1;
@@ -245,163 +346,198 @@ __device__ __forceinline__ bool bwd_px(const ScreenHeader& h, const float* __res
     return true;
 }
 
-__device__ __forceinline__ void red_texels(float* gg, int base, int N, const float (&tg)[12]) {
-    if (N == 1) {
-        red3(gg, tg[0], tg[1], tg[2]);
-        return;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (tg[3 * k] != 0.0f || tg[3 * k + 1] != 0.0f || tg[3 * k + 2] != 0.0f)
-            red3(gg + base + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
-}
-
-template <int MODE, int NT>
-__global__ void __launch_bounds__(128) k_backward_mp(const uint2* __restrict__ ranges,
-                                                     const int32_t* __restrict__ values,
-                                                     const ScreenHeader* __restrict__ hdr,
-                                                     const float* __restrict__ tex, const CamConst cc,
-                                                     const RasterConst rc, int n_rt, const float* __restrict__ in_trans,
-                                                     const int32_t* __restrict__ in_last,
-                                                     const float* __restrict__ image_grad, float* __restrict__ accum,
-                                                     float* __restrict__ grid_grad) {
+template <int MODE, int NT, int G>
+__global__ void __launch_bounds__(256, 4) k_backward_grp(const uint2* __restrict__ ranges,
+                                                      const int32_t* __restrict__ values,
+                                                      const ScreenHeader* __restrict__ hdr,
+                                                      const CullRec* __restrict__ cull,
+                                                      const float* __restrict__ tex, const CamConst cc,
+                                                      const RasterConst rc, int n_rt,
+                                                      const float* __restrict__ in_trans,
+                                                      const int32_t* __restrict__ in_last,
+                                                      const float* __restrict__ image_grad, float* __restrict__ accum,
+                                                      float* __restrict__ grid_grad) {
     constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
-    __shared__ __align__(16) float red_scratch[4 * kRedRows * kRedStride];
+    constexpr int NG = 32 / G;                          // groups per warp
+    constexpr int PS = (NS * NG + 31) / 32;             // reduction passes (screen sums)
+    constexpr int PT = (12 * NG + 31) / 32;             // reduction passes (texels)
+    __shared__ __align__(16) float red_scratch[8 * kRedRows * kRedStride];
+    __shared__ int s_ids[8][NG][32];
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
     const int ts = rc.tile_size;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / G;
+    const unsigned gm = group_mask<G>(lane);
     const int tile = blockIdx.x;
     const uint2 range = ranges[tile];
     const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
-    BwdPx px[kPPT];
-    int wl = -1;
-#pragma unroll
-    for (int p = 0; p < kPPT; ++p) {  // raster.hpp:313-322
-        BwdPx& s = px[p];
-        mp_pixel(warp, lane, p, ts, tx, ty, s.x, s.y);
-        s.last = -1;
-        s.T = 1.0f;
-        s.g0 = s.g1 = s.g2 = 0.0f;
-        if (s.x < cc.width && s.y < cc.height) {
-            const size_t q = (size_t)s.y * cc.width + s.x;
-            s.last = in_last[q];
-            s.g0 = image_grad[q * 3 + 0];
-            s.g1 = image_grad[q * 3 + 1];
-            s.g2 = image_grad[q * 3 + 2];
-            s.T = in_trans[q];
-            if (s.g0 == 0.0f && s.g1 == 0.0f && s.g2 == 0.0f) s.last = -1;
-        }
-        s.bh0 = cc.bg[0];
-        s.bh1 = cc.bg[1];
-        s.bh2 = cc.bg[2];
-        wl = max(wl, s.last);
+    int wx0, wy0;
+    warp_origin(threadIdx.x, ts, tx, ty, wx0, wy0);
+    BwdPx s;
+    group_pixel<G>(threadIdx.x, ts, tx, ty, s.x, s.y);
+    s.last = -1;
+    s.T = 1.0f;
+    s.g0 = s.g1 = s.g2 = 0.0f;
+    if (s.x < cc.width && s.y < cc.height) {  // raster.hpp:313-322
+        const size_t q = (size_t)s.y * cc.width + s.x;
+        s.last = in_last[q];
+        s.g0 = image_grad[q * 3 + 0];
+        s.g1 = image_grad[q * 3 + 1];
+        s.g2 = image_grad[q * 3 + 2];
+        s.T = in_trans[q];
+        if (s.g0 == 0.0f && s.g1 == 0.0f && s.g2 == 0.0f) s.last = -1;
     }
-    const float bx0 = (float)__reduce_min_sync(kFull, px[0].x), bx1 = (float)__reduce_max_sync(kFull, px[0].x);
-    const float by0 = (float)__reduce_min_sync(kFull, px[0].y);
-    const float by1 = (float)__reduce_max_sync(kFull, px[kPPT - 1].y);
-    const int wlast = __reduce_max_sync(kFull, wl);  // this warp never needs ranks above it
+    s.bh0 = cc.bg[0];
+    s.bh1 = cc.bg[1];
+    s.bh2 = cc.bg[2];
     float* wscratch = red_scratch + warp * kRedRows * kRedStride;
-    for (int c0 = wlast & ~31; c0 >= 0; c0 -= 32) {
-        int idl = -1;
-        bool pass = false;
-        if (c0 + lane <= wlast) {
-            idl = __ldg(&values[range.x + c0 + lane]);
-            pass = !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+    // each group walks ranks [0, max last of its pixels] back to front
+    Cursor c{__reduce_max_sync(gm, s.last), 0, 0u};
+    for (;;) {
+        for (;;) {  // refill, one group per round, every group whose window is used up
+            const unsigned need = __ballot_sync(kFull, c.pend == 0 && c.cur >= 0);
+            if (!need) break;
+            const int gs = (__ffs(need) - 1) / G;
+            const int cs = __shfl_sync(kFull, c.cur, gs * G);
+            const int r = cs - lane;
+            int idl = -1;
+            bool pass = false;
+            if (r >= 0) {
+                idl = __ldg(&values[range.x + r]);
+                pass = group_test<G>(cull, idl, wx0, wy0, gs);
+            }
+            const unsigned bal = __ballot_sync(kFull, pass);
+            s_ids[warp][gs][lane] = idl;
+            if (g == gs) {
+                c.pend = bal;
+                c.wbase = cs;
+                c.cur = cs - 32;
+            }
         }
-        unsigned mask = __ballot_sync(kFull, pass);
-        while (mask) {
-            const int bit = 31 - __clz(mask);
-            mask &= ~(1u << bit);
-            const int id = __shfl_sync(kFull, idl, bit);
-            const int rank = c0 + bit;
-            ScreenHeader h;
-            h.h0 = __ldg(&hdr[id].h0);
-            h.h1 = __ldg(&hdr[id].h1);
-            h.h2 = __ldg(&hdr[id].h2);
-            const float* t = tex + (size_t)id * F;
-            float red[10];
-#pragma unroll
-            for (int i = 0; i < 10; ++i) red[i] = 0.0f;
-            float tgA[12], tgB[12];
-            int baseA = -1, baseB = -1;
-            bool onA = bwd_px<MODE, NT>(h, t, N, rank, px[0], rc, red, tgA, baseA);
-            bool onB = bwd_px<MODE, NT>(h, t, N, rank, px[1], rc, red, tgB, baseB);
-            if (!__any_sync(kFull, onA || onB)) continue;
-            {  // screen-space sums: lane l owns value l >> 1
-                float sv[NS];
-#pragma unroll
-                for (int i = 0; i < NS; ++i) sv[i] = red[i];
-                const float r2 = smem_reduce<NS>(sv, wscratch, lane);
-                if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
+        __syncwarp();
+        if (!__any_sync(kFull, c.pend != 0)) break;
+        int id = -1;
+        bool on = false;
+        float red[10], tg[12];
+        int tbase = 0;
+        if (c.pend != 0) {
+            const int bit = __ffs(c.pend) - 1;
+            id = s_ids[warp][g][bit];
+            if (c.wbase - bit <= s.last) {
+                ScreenHeader h;
+                h.h0 = __ldg(&hdr[id].h0);
+                h.h1 = __ldg(&hdr[id].h1);
+                h.h2 = __ldg(&hdr[id].h2);
+                on = bwd_px<MODE, NT>(h, tex + (size_t)id * F, N, s, rc, red, tg, tbase);
             }
-            // texel terms: merge the lane's two pixels when they share a bilinear cell
-            if (onB && (!onA || baseB == baseA)) {
+            c.pend &= c.pend - 1;
+        }
+        __syncwarp();  // s_ids readers done before the next refill overwrites
+        const unsigned act = __ballot_sync(kFull, on);
+        if (act == 0) continue;
+        {  // screen-space sums: one per (value, group), owned by distinct lanes
+            float sv[NS];
 #pragma unroll
-                for (int i = 0; i < 12; ++i) tgA[i] = onA ? tgA[i] + tgB[i] : tgB[i];
-                baseA = baseB;
-                onA = true;
-                onB = false;
+            for (int i = 0; i < NS; ++i) sv[i] = on ? red[i] : 0.0f;
+            float r2[PS];
+            group_reduce<NS, G>(sv, wscratch, lane, r2);
+#pragma unroll
+            for (int k = 0; k < PS; ++k) {
+                const int q = lane + 32 * k;
+                const int src = (q % NG) * G;
+                const int gid = __shfl_sync(kFull, id, src);
+                if (q < NS * NG && ((act >> src) & group_mask<G>(0)))
+                    red_add(accum + (size_t)gid * kAccumStride + q / NG, r2[k]);
             }
+        }
+        // texel terms: one reduction for the groups whose active pixels share a bilinear cell
+        const unsigned gact = act & gm;
+        const int b0 = __shfl_sync(kFull, tbase, gact ? __ffs(gact) - 1 : lane);
+        const unsigned mixed = __ballot_sync(kFull, on && tbase != b0);
+        const bool uni = (mixed & gm) == 0 && gact != 0;
+        const unsigned unimask = __ballot_sync(kFull, uni);
+        if (unimask) {
+            float tv[12];
+#pragma unroll
+            for (int i = 0; i < 12; ++i) tv[i] = (uni && on) ? tg[i] : 0.0f;
+            float r2[PT];
+            group_reduce<12, G>(tv, wscratch, lane, r2);
+#pragma unroll
+            for (int k = 0; k < PT; ++k) {
+                const int q = lane + 32 * k;
+                const int src = (q % NG) * G;
+                const int gid = __shfl_sync(kFull, id, src);
+                const int gb0 = __shfl_sync(kFull, b0, src);
+                if (q < 12 * NG && ((unimask >> src) & 1u) && (N > 1 || q / NG < 3))
+                    red_add(grid_grad + (size_t)gid * F + gb0 + corner_offset(q / NG, N), r2[k]);
+            }
+        }
+        if (on && !uni) {  // mixed cells: each lane adds its (at most four) non-zero texels straight to HBM
             float* gg = grid_grad + (size_t)id * F;
-            const unsigned actA = __ballot_sync(kFull, onA);
-            const int b0 = __shfl_sync(kFull, baseA, actA ? __ffs(actA) - 1 : 0);
-            if (__all_sync(kFull, !onB && (!onA || baseA == b0))) {
-                // every active pixel of the warp shares one cell: one warp reduction
-                if (!onA) {
-#pragma unroll
-                    for (int i = 0; i < 12; ++i) tgA[i] = 0.0f;
-                }
-                const float r2 = smem_reduce<12>(tgA, wscratch, lane);
-                if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
-                    red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
+            if (N == 1) {
+                red3(gg, tg[0], tg[1], tg[2]);
             } else {
-                // otherwise each lane adds its (at most 2 x 4) non-zero texels straight to HBM
-                if (onA) red_texels(gg, baseA, N, tgA);
-                if (onB) red_texels(gg, baseB, N, tgB);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (tg[3 * k] != 0.0f || tg[3 * k + 1] != 0.0f || tg[3 * k + 2] != 0.0f)
+                        red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
             }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// launchers (tile sizes that are multiples of 8: 8 -> 1 warp, 16 -> 4 warps)
+// launchers (16x16 tiles: 8 warps; 8x8 tiles: 2 warps)
 // ---------------------------------------------------------------------------
-bool mp_supported(int ts) { return ts == 8 || ts == 16; }
+bool grp_supported(int ts) { return ts == 8 || ts == 16; }
 
-#define GB_MP_DISPATCH(KERNEL, MODE, ...)                                      \
-    switch (n) {                                                               \
-        case 1: KERNEL<MODE, 1><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
-        case 2: KERNEL<MODE, 2><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
-        case 4: KERNEL<MODE, 4><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
-        case 8: KERNEL<MODE, 8><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
-        case 16: KERNEL<MODE, 16><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
-        default: KERNEL<MODE, 0><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
+static int group_size() {  // GB_GROUP=4|8|16 (A/B); default 8
+    const char* v = getenv("GB_GROUP");
+    const int g = v ? atoi(v) : 8;
+    return (g == 4 || g == 16) ? g : 8;
+}
+
+#define GB_GRP_DISPATCH(KERNEL, MODE, G, ...)                                      \
+    switch (n) {                                                                   \
+        case 1: KERNEL<MODE, 1, G><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 2: KERNEL<MODE, 2, G><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 4: KERNEL<MODE, 4, G><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 8: KERNEL<MODE, 8, G><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 16: KERNEL<MODE, 16, G><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
+        default: KERNEL<MODE, 0, G><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;  \
     }
 
-cudaError_t launch_forward_mp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                              const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
-                              float* color, float* trans, int32_t* last, cudaStream_t st) {
-    const int threads = ts * ts / kPPT;
+#define GB_GRP_G(KERNEL, MODE, ...)                                 \
+    switch (group_size()) {                                         \
+        case 4: GB_GRP_DISPATCH(KERNEL, MODE, 4, __VA_ARGS__) break;   \
+        case 16: GB_GRP_DISPATCH(KERNEL, MODE, 16, __VA_ARGS__) break; \
+        default: GB_GRP_DISPATCH(KERNEL, MODE, 8, __VA_ARGS__) break;  \
+    }
+
+cudaError_t launch_forward_grp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                               const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                               const RasterConst& rc, float* color, float* trans, int32_t* last, cudaStream_t st) {
+    const int threads = ts * ts;
     if (mode == GB_MODE_ORTHO) {
-        GB_MP_DISPATCH(k_forward_mp, GB_MODE_ORTHO, ranges, values, hdr, tex, cc, rc, n, color, trans, last)
+        GB_GRP_G(k_forward_grp, GB_MODE_ORTHO, ranges, values, hdr, cull, tex, cc, rc, n, color, trans, last)
     } else {
-        GB_MP_DISPATCH(k_forward_mp, GB_MODE_PINHOLE, ranges, values, hdr, tex, cc, rc, n, color, trans, last)
+        GB_GRP_G(k_forward_grp, GB_MODE_PINHOLE, ranges, values, hdr, cull, tex, cc, rc, n, color, trans, last)
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_backward_mp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                               const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
-                               const float* trans, const int32_t* last, const float* image_grad, float* accum,
-                               float* grid_grad, cudaStream_t st) {
-    const int threads = ts * ts / kPPT;
+cudaError_t launch_backward_grp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                                const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                                const RasterConst& rc, const float* trans, const int32_t* last,
+                                const float* image_grad, float* accum, float* grid_grad, cudaStream_t st) {
+    const int threads = ts * ts;
     if (mode == GB_MODE_ORTHO) {
-        GB_MP_DISPATCH(k_backward_mp, GB_MODE_ORTHO, ranges, values, hdr, tex, cc, rc, n, trans, last, image_grad,
-                       accum, grid_grad)
+        GB_GRP_G(k_backward_grp, GB_MODE_ORTHO, ranges, values, hdr, cull, tex, cc, rc, n, trans, last, image_grad,
+                 accum, grid_grad)
     } else {
-        GB_MP_DISPATCH(k_backward_mp, GB_MODE_PINHOLE, ranges, values, hdr, tex, cc, rc, n, trans, last, image_grad,
-                       accum, grid_grad)
+        GB_GRP_G(k_backward_grp, GB_MODE_PINHOLE, ranges, values, hdr, cull, tex, cc, rc, n, trans, last, image_grad,
+                 accum, grid_grad)
     }
     return cudaGetLastError();
 }

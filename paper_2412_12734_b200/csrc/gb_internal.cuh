@@ -40,6 +40,12 @@ struct __align__(16) ScreenHeader {
     float4 h0, h1, h2, h3;
 };
 
+// Per-primitive alpha-skip ellipse in pixel-index coordinates (K1, alpha_ellipse):
+// a = (e_x, e_y, Q11, Q22), b = (Q12, Q12/Q22, Q12/Q11, 0).
+struct __align__(16) CullRec {
+    float4 a, b;
+};
+
 // Per-launch camera constants for the fp32 compositor.
 struct CamConst {
     int width, height;
@@ -156,20 +162,20 @@ struct ProjParams {
 
 ProjParams make_proj_params(const gb_splats* s, const gb_camera* cam, const gb_raster_config* cfg, int tiles_x,
                             int tiles_y);
-cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, uint2* rects, uint32_t* counts,
+cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, CullRec* cull, uint2* rects, uint32_t* counts,
                            uint32_t* depth_bits, cudaStream_t st);
 cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
                          cudaStream_t st);
 
-// gb_composite.cu: K3/K4 with several pixels per thread (tile sizes 8 and 16)
-bool mp_supported(int ts);
-cudaError_t launch_forward_mp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                              const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
-                              float* color, float* trans, int32_t* last, cudaStream_t st);
-cudaError_t launch_backward_mp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                               const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
-                               const float* trans, const int32_t* last, const float* image_grad, float* accum,
-                               float* grid_grad, cudaStream_t st);
+// gb_composite.cu: K3/K4 with sub-warp groups (tile sizes 8 and 16)
+bool grp_supported(int ts);
+cudaError_t launch_forward_grp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                               const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
+                               float* color, float* trans, int32_t* last, cudaStream_t st);
+cudaError_t launch_backward_grp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                                const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
+                                const float* trans, const int32_t* last, const float* image_grad, float* accum,
+                                float* grid_grad, cudaStream_t st);
 
 __device__ __forceinline__ uint32_t float_order_key(float d) {
     uint32_t b = __float_as_uint(d == 0.0f ? 0.0f : d);  // -0 sorts as +0 (double compare)

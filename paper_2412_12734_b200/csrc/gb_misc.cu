@@ -56,27 +56,61 @@ cudaError_t launch_loss(int kind, const float* color, const float* target, int64
 __global__ void __launch_bounds__(256) k_adam_check(const float* __restrict__ g, int64_t n, int group,
                                                     unsigned long long* __restrict__ bad) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t n4 = ((reinterpret_cast<uintptr_t>(g) & 15) == 0) ? n / 4 : 0;
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const float4 q = g4[i];
+        if (!(isfinite(q.x) && isfinite(q.y) && isfinite(q.z) && isfinite(q.w))) {
+            for (int j = 0; j < 4; ++j)
+                if (!isfinite(g[4 * i + j]))
+                    atomicMin(bad, ((unsigned long long)group << 48) | (unsigned long long)(4 * i + j));
+        }
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         if (!isfinite(g[i])) atomicMin(bad, ((unsigned long long)group << 48) | (unsigned long long)i);
     }
 }
 
+// optim.hpp:84-88 for one element
+// (1 - beta) arrive from the host rounded once from double: 1 - 0.999f in fp32 is 1.3e-5 off.
+__device__ __forceinline__ void adam_one(float& p, float gi, float& m, float& v, float lr, float b1, float b2,
+                                         float omb1, float omb2, float eps, float inv_bias1, float inv_bias2) {
+    const float mi = b1 * m + omb1 * gi;
+    const float vi = b2 * v + omb2 * gi * gi;
+    m = mi;
+    v = vi;
+    p -= lr * (mi * inv_bias1) / (sqrtf(vi * inv_bias2) + eps);
+}
+
+// HBM-bound: 16-byte vector loads/stores when all four arrays are 16-B aligned (the flat gradient / state
+// buffers keep every group 16-B aligned), scalar tail.
 __global__ void __launch_bounds__(256) k_adam_update(float* __restrict__ p, const float* __restrict__ g,
                                                      float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
-                                                     float b1, float b2, float eps, float inv_bias1, float inv_bias2,
+                                                     float b1, float b2, float omb1, float omb2, float eps,
+                                                     float inv_bias1, float inv_bias2,
                                                      const unsigned long long* __restrict__ bad) {
     if (*bad != ~0ull) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const float gi = g[i];
-        const float mi = b1 * m[i] + (1.0f - b1) * gi;
-        const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
-        m[i] = mi;
-        v[i] = vi;
-        const float m_hat = mi * inv_bias1;
-        const float v_hat = vi * inv_bias2;
-        p[i] -= lr * m_hat / (sqrtf(v_hat) + eps);
+    const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                       reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+    const int64_t n4 = vec ? n / 4 : 0;
+    float4* p4 = reinterpret_cast<float4*>(p);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    float4* m4 = reinterpret_cast<float4*>(m);
+    float4* v4 = reinterpret_cast<float4*>(v);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 pp = p4[i], mm = m4[i], vv = v4[i];
+        const float4 gg = g4[i];
+        adam_one(pp.x, gg.x, mm.x, vv.x, lr, b1, b2, omb1, omb2, eps, inv_bias1, inv_bias2);
+        adam_one(pp.y, gg.y, mm.y, vv.y, lr, b1, b2, omb1, omb2, eps, inv_bias1, inv_bias2);
+        adam_one(pp.z, gg.z, mm.z, vv.z, lr, b1, b2, omb1, omb2, eps, inv_bias1, inv_bias2);
+        adam_one(pp.w, gg.w, mm.w, vv.w, lr, b1, b2, omb1, omb2, eps, inv_bias1, inv_bias2);
+        p4[i] = pp;
+        m4[i] = mm;
+        v4[i] = vv;
     }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        adam_one(p[i], g[i], m[i], v[i], lr, b1, b2, omb1, omb2, eps, inv_bias1, inv_bias2);
 }
 
 static unsigned grid_for(int64_t n, int sm_count) {
@@ -95,10 +129,11 @@ cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned lon
 }
 
 cudaError_t launch_adam_update(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
-                               float eps, float inv_bias1, float inv_bias2, const unsigned long long* bad,
-                               int sm_count, cudaStream_t st) {
+                               float omb1, float omb2, float eps, float inv_bias1, float inv_bias2,
+                               const unsigned long long* bad, int sm_count, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    k_adam_update<<<grid_for(n, sm_count), 256, 0, st>>>(p, g, m, v, n, lr, b1, b2, eps, inv_bias1, inv_bias2, bad);
+    k_adam_update<<<grid_for(n, sm_count), 256, 0, st>>>(p, g, m, v, n, lr, b1, b2, omb1, omb2, eps, inv_bias1,
+                                                          inv_bias2, bad);
     return cudaGetLastError();
 }
 

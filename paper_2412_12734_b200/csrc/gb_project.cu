@@ -205,6 +205,80 @@ __device__ float4 alpha_box(const ProjParams& p, int64_t k, const Geom& g) {
                        (float)fmax(-1e30, ceil(min_y - 0.5 - m)), (float)fmin(1e30, floor(max_y - 0.5 + m)));
 }
 
+__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// The same alpha-skip region as a pixel-space ellipse, for the exact
+// block-vs-entry test of the sub-warp compositors (gb_composite.cu):
+// alpha < alpha_skip for certain outside (p - e)^T Q (p - e) <= 1, p in pixel
+// index coordinates (pixel centre at index + 0.5), same radius margin as
+// alpha_box.  Record: a = (e_x, e_y, Q11, Q22), b = (Q12, Q12/Q22, Q12/Q11, 0).
+// All-zero Q passes everything (threshold disabled, or the region reaches
+// behind the camera and is not an ellipse); e = +inf-like passes nothing.
+__device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g) {
+    const CullRec all = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+    const CullRec none = {make_float4(1e30f, 1e30f, 1.f, 1.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+    if (!(p.alpha_skip > 0.0)) return all;
+    const double ak = 1.0 / (1.0 + exp(-(double)p.opacity[k]));
+    if (!(ak > p.alpha_skip)) return none;
+    const double r = sqrt(2.0 * log(ak / p.alpha_skip)) * 1.001 + 1e-3;
+    const double r2 = r * r;
+    double A11, A12, A22, ex, ey;
+    if (p.mode == GB_MODE_ORTHO) {
+        // u^2 + v^2 with u = (c dx + s dy)/s_u, v = (-s dx + c dy)/s_v (raster.hpp:36-42)
+        const double th = (double)p.theta[k];
+        const double c = cos(th), s = sin(th);
+        const double iu2 = 1.0 / (g.s_u * g.s_u), iv2 = 1.0 / (g.s_v * g.s_v);
+        A11 = (c * c * iu2 + s * s * iv2) / r2;
+        A12 = (c * s * (iu2 - iv2)) / r2;
+        A22 = (s * s * iu2 + c * c * iv2) / r2;
+        ex = (double)p.position[2 * k] - 0.5;
+        ey = (double)p.position[2 * k + 1] - 0.5;
+    } else {
+        const double* M = g.M;
+        const double lat = sqrt(M[6] * M[6] + M[7] * M[7]);
+        if (!(M[8] - r * lat > 0.0)) return all;
+        // pixel ~ H (u, v, 1); (u, v, 1) ~ adj(H) pixel; region: w0^2 + w1^2 - r^2 w2^2 <= 0
+        double H0[3], H1[3], H2[3], c0[3], c1[3], c2[3];
+        for (int j = 0; j < 3; ++j) {
+            H0[j] = p.fx * M[j] + p.cx * M[6 + j];
+            H1[j] = p.fy * M[3 + j] + p.cy * M[6 + j];
+            H2[j] = M[6 + j];
+        }
+        cross3(H1, H2, c0);
+        cross3(H2, H0, c1);
+        cross3(H0, H1, c2);
+        // adj(H) has columns c0, c1, c2, so w_m = sum_j p_j c_j[m] and C[j][l] = <c_j, c_l> under diag(1, 1, -r^2)
+        const double* col[3] = {c0, c1, c2};
+        double C[3][3];
+        for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l)
+                C[j][l] = col[j][0] * col[l][0] + col[j][1] * col[l][1] - r2 * col[j][2] * col[l][2];
+        // C is over p = (x, y, 1) with x, y continuous pixel coordinates
+        const double det2 = C[0][0] * C[1][1] - C[0][1] * C[0][1];
+        if (!(C[0][0] > 0.0) || !(det2 > 0.0)) return all;
+        const double cx = -(C[1][1] * C[0][2] - C[0][1] * C[1][2]) / det2;
+        const double cy = -(C[0][0] * C[1][2] - C[0][1] * C[0][2]) / det2;
+        const double kk = -(C[2][2] + C[0][2] * cx + C[1][2] * cy);
+        if (!(kk > 0.0)) return all;
+        A11 = C[0][0] / kk;
+        A12 = C[0][1] / kk;
+        A22 = C[1][1] / kk;
+        ex = cx - 0.5;
+        ey = cy - 0.5;
+    }
+    if (!(isfinite(A11) && isfinite(A12) && isfinite(A22) && isfinite(ex) && isfinite(ey)) || !(A11 > 0.0) ||
+        !(A22 > 0.0) || fabs(ex) > 1e7 || fabs(ey) > 1e7)
+        return all;
+    CullRec out;
+    out.a = make_float4((float)ex, (float)ey, (float)A11, (float)A22);
+    out.b = make_float4((float)A12, (float)(A12 / A22), (float)(A12 / A11), 0.f);
+    return out;
+}
+
 // Effective projected centre used by the fp32 compositor (see ScreenHeader).
 __device__ __forceinline__ void pinhole_centre(const ProjParams& p, const Geom& g, int& cxi, int& cyi, float& hx,
                                                float& hy, double& dxe, double& dye) {
@@ -230,12 +304,6 @@ struct PinholeCoeffs {
     double C0[3], Cx[3], Cy[3], E[3];
 };
 
-__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {
-    c[0] = a[1] * b[2] - a[2] * b[1];
-    c[1] = a[2] * b[0] - a[0] * b[2];
-    c[2] = a[0] * b[1] - a[1] * b[0];
-}
-
 __device__ __forceinline__ void pinhole_coeffs(const Geom& g, double dxe, double dye, PinholeCoeffs& pc) {
     const double* M0 = g.M;
     const double* M1 = g.M + 3;
@@ -248,8 +316,8 @@ __device__ __forceinline__ void pinhole_coeffs(const Geom& g, double dxe, double
 
 // K1: one thread per primitive.
 __global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeader* __restrict__ hdr,
-                                                 uint2* __restrict__ rects, uint32_t* __restrict__ counts,
-                                                 uint32_t* __restrict__ depth_bits) {
+                                                 CullRec* __restrict__ cull, uint2* __restrict__ rects,
+                                                 uint32_t* __restrict__ counts, uint32_t* __restrict__ depth_bits) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= p.K) return;
     Geom g;
@@ -289,6 +357,7 @@ __global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeade
     }
     h.h3 = alpha_box(p, k, g);
     hdr[k] = h;
+    cull[k] = alpha_ellipse(p, k, g);
 }
 
 // K5: chain the K4 screen-space sums to the raw parameters and ADD into the
@@ -417,12 +486,12 @@ ProjParams make_proj_params(const gb_splats* s, const gb_camera* cam, const gb_r
     return p;
 }
 
-cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, uint2* rects, uint32_t* counts,
+cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, CullRec* cull, uint2* rects, uint32_t* counts,
                            uint32_t* depth_bits, cudaStream_t st) {
     if (p.K == 0) return cudaSuccess;
     const int threads = 256;
     const unsigned blocks = (unsigned)((p.K + threads - 1) / threads);
-    k_project<<<blocks, threads, 0, st>>>(p, hdr, rects, counts, depth_bits);
+    k_project<<<blocks, threads, 0, st>>>(p, hdr, cull, rects, counts, depth_bits);
     return cudaGetLastError();
 }
 

@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
 template <int MODE, int NT>
 __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict__ ranges,
                                                         const int32_t* __restrict__ values,
-                                                        const ScreenHeader* __restrict__ hdr,
+                                                        const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                                         const float* __restrict__ tex, const CamConst cc,
                                                         const RasterConst rc, int n_rt, float* __restrict__ out_color,
                                                         float* __restrict__ out_trans, int32_t* __restrict__ out_last) {
@@ -655,7 +655,8 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
         bool pass = false;
         if (c0 + lane < total) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+            pass = ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f, by0 - 0.05f,
+                                         by1 + 0.05f);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         while (mask) {
@@ -722,7 +723,7 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
 template <int MODE, int NT>
 __global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict__ ranges,
                                                          const int32_t* __restrict__ values,
-                                                         const ScreenHeader* __restrict__ hdr,
+                                                         const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                                          const float* __restrict__ tex, const CamConst cc,
                                                          const RasterConst rc, int n_rt,
                                                          const float* __restrict__ in_trans,
@@ -762,7 +763,8 @@ __global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict
         bool pass = false;
         if (c0 + lane <= wlast) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+            pass = ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f, by0 - 0.05f,
+                                         by1 + 0.05f);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         if (lane == 0) GB_DBG(1, __popc(mask));
@@ -788,14 +790,14 @@ static int tune_env(const char* name, int dflt) {  // development knob: GB_TUNE_
     return v ? atoi(v) : dflt;
 }
 
-// Compositor variant: 1 = one pixel per thread reading through L1 (default),
-// 0 = two pixels per thread (gb_composite.cu; tile sizes 8 and 16),
-// 2 = one pixel per thread with TMA bulk-copy staging.  GB_COMPOSITOR=direct|
-// mp|staged selects one explicitly (A/B measurements and parity tests).
+// Compositor variant: 1 = one warp per entry reading through L1 (default),
+// 0 = sub-warp groups (gb_composite.cu; tile sizes 8 and 16), 2 = one warp per
+// entry with TMA bulk-copy staging.  GB_COMPOSITOR=direct|grp|staged selects
+// one explicitly (A/B measurements and parity tests).
 static int compositor_variant() {
     const char* v = getenv("GB_COMPOSITOR");
     if (!v) return 1;
-    if (!strcmp(v, "mp")) return 0;
+    if (!strcmp(v, "grp")) return 0;
     if (!strcmp(v, "staged")) return 2;
     return 1;
 }
@@ -849,37 +851,37 @@ static cudaError_t bwd_t(int tiles, int threads, size_t smem, cudaStream_t st, c
 
 template <int MODE, int NT>
 static cudaError_t fwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
-                          const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc, int n,
+                          const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc, int n,
                           float* color, float* trans, int32_t* last) {
-    k_forward_direct<MODE, NT><<<tiles, threads, 0, st>>>(ranges, values, hdr, tex, cc, rc, n, color, trans, last);
+    k_forward_direct<MODE, NT><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, color, trans, last);
     return cudaGetLastError();
 }
 
 template <int MODE, int NT>
 static cudaError_t bwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
-                          const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc, int n,
+                          const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc, int n,
                           const float* trans, const int32_t* last, const float* image_grad, float* accum,
                           float* grid_grad) {
     const size_t smem = (size_t)(threads / 32) * kRedRows * kRedStride * 4;
-    k_backward_direct<MODE, NT><<<tiles, threads, smem, st>>>(ranges, values, hdr, tex, cc, rc, n, trans, last,
+    k_backward_direct<MODE, NT><<<tiles, threads, smem, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, trans, last,
                                                                image_grad, accum, grid_grad);
     return cudaGetLastError();
 }
 
 cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                           const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
                            float* color, float* trans, int32_t* last, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
     const int variant = compositor_variant();
-    if (variant == 0 && mp_supported(ts))
-        return launch_forward_mp(mode, n, tiles, ts, ranges, values, hdr, tex, cc, rc, color, trans, last, st);
+    if (variant == 0 && grp_supported(ts))
+        return launch_forward_grp(mode, n, tiles, ts, ranges, values, hdr, cull, tex, cc, rc, color, trans, last, st);
     if (variant != 2) {
         const int threads = ((ts * ts + 31) / 32) * 32;
         if (mode == GB_MODE_ORTHO) {
-            GB_DISPATCH_N(fwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, color,
+            GB_DISPATCH_N(fwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, color,
                           trans, last)
         } else {
-            GB_DISPATCH_N(fwdd_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, color,
+            GB_DISPATCH_N(fwdd_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, color,
                           trans, last)
         }
     }
@@ -896,21 +898,21 @@ cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* rang
 }
 
 cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                            const ScreenHeader* hdr, const float* tex, const CamConst& cc, const RasterConst& rc,
+                            const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
                             const float* trans, const int32_t* last, const float* image_grad, float* accum,
                             float* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
     const int variant = compositor_variant();
-    if (variant == 0 && mp_supported(ts))
-        return launch_backward_mp(mode, n, tiles, ts, ranges, values, hdr, tex, cc, rc, trans, last, image_grad,
-                                  accum, grid_grad, st);
+    if (variant == 0 && grp_supported(ts))
+        return launch_backward_grp(mode, n, tiles, ts, ranges, values, hdr, cull, tex, cc, rc, trans, last, image_grad,
+                                   accum, grid_grad, st);
     if (variant != 2) {
         const int threads = ((ts * ts + 31) / 32) * 32;
         if (mode == GB_MODE_ORTHO) {
-            GB_DISPATCH_N(bwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, trans, last,
+            GB_DISPATCH_N(bwdd_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, trans, last,
                           image_grad, accum, grid_grad)
         } else {
-            GB_DISPATCH_N(bwdd_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, tex, cc, rc, n, trans,
+            GB_DISPATCH_N(bwdd_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, trans,
                           last, image_grad, accum, grid_grad)
         }
     }

@@ -1,0 +1,155 @@
+"""The training-step kernels around the compositor, on the GPU, against the oracle.
+
+* K6 L1 loss (the BASELINE configs' loss) and MSE (train.hpp:120-133);
+* K7 Adam (optim.hpp:76-117): three steps against the fp64 oracle's adam_group,
+  and the non-finite guard (optim.hpp:81-83: nothing is updated, the call raises);
+* the view-sharded step (configs[3] shape, scaled down): gradients summed over
+  the views equal the oracle's per-view backward sum, and the post-Adam
+  parameters equal the oracle's Adam on those gradients.
+"""
+import numpy as np
+import pytest
+
+from parity import O, compare_grads
+
+pytestmark = pytest.mark.gpu
+
+
+def test_l1_and_mse_loss():
+    import torch
+
+    import paper_2412_12734_b200 as gb
+
+    rng = np.random.default_rng(1)
+    c = rng.random((40, 56, 3), dtype=np.float32)
+    t = rng.random((40, 56, 3), dtype=np.float32)
+    scale = 1.0 / c.size
+    loss, grad = gb.l1_loss(torch.as_tensor(c).cuda(), torch.as_tensor(t).cuda(), scale)
+    ref_loss, ref_grad = O.l1_loss(c.astype(np.float64), t.astype(np.float64), scale)
+    assert abs(float(loss) - ref_loss) <= 1e-5 * abs(ref_loss)
+    np.testing.assert_array_equal(grad.cpu().numpy(), ref_grad.astype(np.float32))
+    loss, grad = gb.mse_loss(torch.as_tensor(c).cuda(), torch.as_tensor(t).cuda(), scale)
+    d = c.astype(np.float64) - t
+    assert abs(float(loss) - (d * d).sum() * scale) <= 1e-5 * (d * d).sum() * scale
+    np.testing.assert_allclose(grad.cpu().numpy(), 2 * scale * d, rtol=1e-6, atol=1e-12)
+
+
+def _pinhole_scene(K, n, seed):
+    import paper_2412_12734_b200.scenes as sc
+
+    return sc.generate(O.MODE_PINHOLE, K, n, seed, mean_lo=-1.0, mean_hi=1.0, scale_lo=0.01, scale_hi=0.08)
+
+
+def test_adam_three_steps_vs_oracle():
+    import torch
+
+    import paper_2412_12734_b200 as gb
+
+    n, K = 4, 1001  # odd sizes exercise the vector body and the scalar tail
+    arrays = _pinhole_scene(K, n, 3)
+    splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    state = gb.AdamState(splats)
+    lrs = gb.LearningRates(position_gamma=0.9)
+    rng = np.random.default_rng(7)
+    names = {"position": "position", "quat": "quat", "log_scale": "log_scale", "opacity_logit": "opacity_logit",
+             "grid": "grid"}
+    lr_of = {"position": None, "quat": lrs.theta, "log_scale": lrs.log_scale, "opacity_logit": lrs.opacity_logit,
+             "grid": lrs.color_grid}
+    ref_p = {f: splats.tensors()[f].cpu().numpy().astype(np.float64).ravel() for f in names}
+    ref_m = {f: np.zeros_like(v) for f, v in ref_p.items()}
+    ref_v = {f: np.zeros_like(v) for f, v in ref_p.items()}
+    for t in range(1, 4):
+        grads = gb.GradientBuffer(splats)
+        host = {}
+        for f in names:
+            g = grads.tensors()[f]
+            h = (rng.standard_normal(g.numel()) * 10.0 ** rng.uniform(-4, 1, g.numel())).astype(np.float32)
+            g.copy_(torch.as_tensor(h).view_as(g))
+            host[f] = h.astype(np.float64)
+        gb.adam_step(splats, grads, state, lrs)
+        b1, b2 = 1 - 0.9 ** t, 1 - 0.999 ** t
+        for f in names:
+            lr = lrs.position * lrs.position_gamma ** (t - 1) if f == "position" else lr_of[f]
+            ref_p[f], ref_m[f], ref_v[f], bad = O.adam_group(ref_p[f], host[f], ref_m[f], ref_v[f], lr, 0.9, 0.999,
+                                                              1e-8, b1, b2)
+            assert bad == 0, bad
+    torch.cuda.synchronize()
+    assert state.t == 3
+    for f in names:
+        got = splats.tensors()[f].cpu().numpy().astype(np.float64).ravel()
+        lr = lrs.position if f == "position" else lr_of[f]
+        # fp32 parameters and moments: each of the 3 updates (size <= lr) is exact to ~1e-6 relative
+        np.testing.assert_allclose(got, ref_p[f], rtol=2e-6, atol=1e-5 * lr, err_msg=f)
+
+
+def test_adam_nonfinite_gradient_raises_and_updates_nothing():
+    import torch
+
+    import paper_2412_12734_b200 as gb
+
+    arrays = _pinhole_scene(300, 2, 4)
+    splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(2), **arrays)
+    before = {f: v.clone() for f, v in splats.tensors().items() if v is not None}
+    grads = gb.GradientBuffer(splats)
+    grads.tensors()["grid"].fill_(0.5)
+    grads.tensors()["log_scale"].view(-1)[17] = float("nan")
+    state = gb.AdamState(splats)
+    with pytest.raises(Exception, match="log_scale"):
+        gb.adam_step(splats, grads, state, gb.LearningRates())
+    torch.cuda.synchronize()
+    for f, v in before.items():
+        assert torch.equal(splats.tensors()[f], v), f
+
+
+def test_view_sharded_step_vs_oracle():
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+    from paper_2412_12734_b200.train import ViewShardedTrainer
+
+    n, K, W, H = 4, 3000, 96, 80
+    arrays = _pinhole_scene(K, n, 5)
+    specs = [sc.look_at((3.0 * np.cos(a), 0.7, 3.0 * np.sin(a)), (0.0, 0.0, 0.0), W, H, 90.0, 90.0, 48.0, 40.0)
+             for a in (0.3, 2.1)]
+    targets = [sc.uniform_image(100 + v, W, H) for v in range(2)]
+    splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    cams = [gb.PinholeCamera.from_spec(s) for s in specs]
+    lrs = gb.LearningRates()
+    tr = ViewShardedTrainer(splats, cams, [0, 1], lrs=lrs)
+    # the per-view image cotangents the step will use (computed from the same GPU forward)
+    igs = []
+    for v in range(2):
+        b = gb.build_binning(splats, cams[v])
+        out = gb.render_forward(splats, cams[v], b)
+        _, ig = gb.l1_loss(out.color, torch.as_tensor(targets[v]).cuda())
+        igs.append(ig.cpu().numpy().astype(np.float64))
+    p0 = {f: v.cpu().numpy().astype(np.float64).ravel() for f, v in splats.tensors().items() if v is not None}
+    tr.step([torch.as_tensor(t).cuda() for t in targets])
+    torch.cuda.synchronize()
+    # oracle: sum over the views of render_backward with the same cotangents
+    scene = O.Scene64(arrays, n)
+    cfg = O.Cfg()
+    tot = {f: None for f in ("position", "quat", "log_scale", "opacity_logit", "grid")}
+    mag, slack = dict(tot), dict(tot)
+    for v in range(2):
+        cam = O.Cam.from_spec(specs[v])
+        b = O.build_binning(scene, cam, cfg)
+        f = O.render_forward(scene, cam, cfg, b)
+        g, m, s = O.render_backward(scene, cam, cfg, b, f, igs[v])
+        for k in tot:
+            tot[k] = g[k] if tot[k] is None else tot[k] + g[k]
+            mag[k] = m[k] if mag[k] is None else mag[k] + m[k]
+            slack[k] = s[k] if slack[k] is None else slack[k] + s[k]
+    got = {k: v.cpu().numpy().astype(np.float64) for k, v in tr.grads.tensors().items() if k in tot}
+    st = compare_grads(dict(grads=got), dict(grads=tot, mag=mag, slack=slack))
+    for k, s in st.items():
+        assert s["strict_violations_applicable"] == 0 and s["model_violations"] == 0, (k, s)
+    # Adam on exactly those gradients
+    for k in tot:
+        lr = {"position": lrs.position, "quat": lrs.theta, "log_scale": lrs.log_scale,
+              "opacity_logit": lrs.opacity_logit, "grid": lrs.color_grid}[k]
+        ref, _, _, _ = O.adam_group(p0[k], got[k].ravel(), np.zeros_like(p0[k]), np.zeros_like(p0[k]), lr, 0.9,
+                                    0.999, 1e-8, 0.1, 1 - 0.999)
+        np.testing.assert_allclose(splats.tensors()[k].cpu().numpy().astype(np.float64).ravel(), ref, rtol=2e-6,
+                                   atol=1e-5 * lr, err_msg=k)

@@ -17,12 +17,14 @@ if [ "${TESTS:-1}" = 1 ]; then
   timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
   echo "smoke exit $?" >> $O/smoke.log
 fi
+# variant names: grp (default, G=8), grp16 (G=16), direct, staged
+venv() { case $1 in grp16) echo "GB_COMPOSITOR=grp GB_GROUP=16";; grp4) echo "GB_COMPOSITOR=grp GB_GROUP=4";; *) echo "GB_COMPOSITOR=$1";; esac; }
 for v in ${ALT_TESTS:-}; do
-  GB_COMPOSITOR=$v timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "configs1 or pinhole_small or ortho_random or ragged" > $O/pytest_gpu_$v.log 2>&1
+  env $(venv $v) timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "configs1 or pinhole_small or ortho_random or ragged" > $O/pytest_gpu_$v.log 2>&1
   echo "pytest exit $?" >> $O/pytest_gpu_$v.log
 done
 for v in $VARIANTS; do
-  GB_COMPOSITOR=$v timeout 600 python bench.py --no-cpu-baseline > $O/bench_$v.json 2> $O/bench_$v.err
+  env $(venv $v) timeout 600 python bench.py --no-cpu-baseline > $O/bench_$v.json 2> $O/bench_$v.err
   echo "bench exit $?" >> $O/bench_$v.err
 done
 if [ "${DBG:-0}" = 1 ]; then
@@ -33,11 +35,11 @@ if [ "${REF:-0}" = 1 ]; then
   timeout 900 python bench.py > $O/bench_full.json 2> $O/bench_full.err
 fi
 if [ "${NCU:-1}" = 1 ]; then
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  env $(venv ${NCU_VARIANT:-direct}) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_backward -s 8 -c 1 \
+  env $(venv ${NCU_VARIANT:-direct}) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_backward -s 8 -c 1 \
     -o $O/k4_full -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_k4.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_forward -s 8 -c 1 \
+  env $(venv ${NCU_VARIANT:-direct}) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_forward -s 8 -c 1 \
     -o $O/k3_full -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_k3.log 2>&1
 fi
 echo done > $O/DONE
