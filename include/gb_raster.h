@@ -40,7 +40,8 @@ typedef enum {
     GB_CUDA_ERROR = 3,
     GB_OOM = 4,
     GB_NONFINITE = 5, /* adam_step non-finite gradient: optim.hpp:81-83 */
-    GB_NOT_SUPPORTED = 6
+    GB_NOT_SUPPORTED = 6,
+    GB_IO_ERROR = 7 /* SplatIoError (serialize.hpp:23-25) */
 } gb_status;
 
 #define GB_MODE_ORTHO 0   /* the reference's ImagePlaneCamera (core.hpp:102-116) */
@@ -221,6 +222,30 @@ GB_API gb_status gb_adam_step(gb_context *ctx, int32_t mode, int64_t count, int3
                        gb_adam_state *state, const gb_learning_rates *lrs);
 /* Synchronous.  group: 0 position, 1 theta/quat, 2 log_scale, 3 opacity, 4 grid. */
 GB_API gb_status gb_adam_check(gb_context *ctx, int32_t *group, int64_t *index);
+
+/* ---- GBIL splat files (serialize.hpp:15-124) -------------------------------
+ * Header "GBIL", u32 version, u32 K, u32 N, f32 sigma, then K little-endian
+ * fp32 records.  Version 1 is the reference's (ortho) record: x, y, depth_key,
+ * theta, log_su, log_sv, opacity_logit, N*N*3 grid.  Version 2 is this build's
+ * pinhole extension: mean xyz, quat wxyz, log_su, log_sv, opacity_logit, grid.
+ * Errors are GB_IO_ERROR with serialize.hpp's messages ("bad splat file: wrong
+ * magic", "... truncated header", "unsupported splat file version N",
+ * "... invalid grid config", "... truncated at record R", "cannot open splat
+ * file: PATH", "cannot open for writing: PATH", "splat write failed: PATH"). */
+typedef struct {
+    int32_t version;
+    int32_t mode; /* GB_MODE_ORTHO for version 1, GB_MODE_PINHOLE for version 2 */
+    int64_t count;
+    int32_t n;
+    float sigma;
+} gb_splat_file_info;
+/* Header only (host; no device work).  Replaces the header half of load_splats (serialize.hpp:83-101). */
+GB_API gb_status gb_splats_file_info(const char *path, gb_splat_file_info *info);
+/* Replaces save_splats(path, set) (serialize.hpp:56-90): device SoA -> records on the GPU -> file. */
+GB_API gb_status gb_splats_save(gb_context *ctx, const gb_splats *s, int32_t mode, const char *path);
+/* Replaces load_splats(path) (serialize.hpp:92-124) into caller-allocated device buffers (gb_grads layout,
+ * sized from gb_splats_file_info; count/n must match the file, else GB_MISMATCH).  Synchronous. */
+GB_API gb_status gb_splats_load(gb_context *ctx, const char *path, int64_t count, int32_t n, gb_grads *dst);
 
 /* ---- seeded synthetic inputs (rng.hpp:12-46 semantics), host-only ---------- */
 typedef struct {

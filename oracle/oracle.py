@@ -117,6 +117,8 @@ def ref_lib():
         L.ref_render_naive.argtypes = [C.c_int64, i, d, P, P, P, P, P, P, i, i, P, P, P]
         L.ref_gradient_fd.argtypes = [C.c_int64, i, d, P, P, P, P, P, P, i, i, P, P, d, P, P, P, P, P, P]
         L.ref_uv_to_grid.argtypes = [d, d, i, d, P, P, P, P]
+        L.ref_save_splats.argtypes = [C.c_char_p, C.c_int64, i, d, P, P, P, P, P, P, C.c_char_p, i]
+        L.ref_load_splats.argtypes = [C.c_char_p, P, P, P, P, P, P, P, P, P, C.c_char_p, i]
         L.ref_bilinear.argtypes = [d, d, i, d, P, P]
         L.ref_adj_bilinear.argtypes = [d, d, i, d, P, P, P, P, P]
         L.ref_adam_group.argtypes = [P, P, P, P, C.c_int64, d, d, d, d, d, d]
@@ -351,6 +353,34 @@ def ref_render(scene: Scene64, cam: Cam, cfg: Cfg, image_grad=None):
     if ig is not None:
         out["grads"] = g
     return out
+
+
+def ref_save_splats(path: str, scene: Scene64) -> str:
+    """The reference's save_splats (serialize.hpp:83-90); returns '' or the SplatIoError message."""
+    L = ref_lib()
+    a = scene.a
+    msg = C.create_string_buffer(512)
+    rc = L.ref_save_splats(os.fsencode(path), scene.count, scene.n, scene.sigma, a["position"].ctypes.data,
+                           a["depth_key"].ctypes.data, a["theta"].ctypes.data, a["log_scale"].ctypes.data,
+                           a["opacity_logit"].ctypes.data, a["grid"].ctypes.data, msg, 512)
+    return "" if rc == 0 else msg.value.decode()
+
+
+def ref_load_splats(path: str):
+    """The reference's load_splats (serialize.hpp:118-124) -> (arrays dict, n, sigma) or the error message."""
+    L = ref_lib()
+    k, n, sigma = C.c_int64(), C.c_int(), C.c_double()
+    msg = C.create_string_buffer(512)
+    if L.ref_load_splats(os.fsencode(path), C.byref(k), C.byref(n), C.byref(sigma), None, None, None, None, None,
+                         None, msg, 512):
+        return msg.value.decode()
+    K, N = k.value, n.value
+    out = dict(position=np.zeros((K, 2)), depth_key=np.zeros(K), theta=np.zeros(K), log_scale=np.zeros((K, 2)),
+               opacity_logit=np.zeros(K), grid=np.zeros((K, N * N * 3)))
+    L.ref_load_splats(os.fsencode(path), C.byref(k), C.byref(n), C.byref(sigma),
+                      *[out[f].ctypes.data for f in ("position", "depth_key", "theta", "log_scale", "opacity_logit",
+                                                     "grid")], msg, 512)
+    return out, N, sigma.value
 
 
 def ref_render_naive(scene: Scene64, cam: Cam):

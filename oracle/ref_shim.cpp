@@ -11,6 +11,8 @@
 // Only arrays and sizes cross this boundary; the reference's value types are
 // rebuilt on each call.
 #include <cstdint>
+#include <cstdio>
+#include <string>
 #include <cstring>
 #include <stdexcept>
 #include <vector>
@@ -20,6 +22,7 @@
 #include "gbil/raster.hpp"
 #include "gbil/reference.hpp"
 #include "gbil/rng.hpp"
+#include "gbil/serialize.hpp"
 #include "gbil/texture.hpp"
 
 using namespace gbil;
@@ -198,6 +201,43 @@ void ref_rng_uniform(uint64_t seed, int64_t n, double* out) {
 void ref_rng_normal(uint64_t seed, int64_t n, double mean, double stddev, double* out) {
     Rng r(seed);
     for (int64_t i = 0; i < n; ++i) out[i] = r.normal(mean, stddev);
+}
+
+// save_splats(path, set) (serialize.hpp:83-90); 0 on success, 1 on SplatIoError (message in msg).
+int ref_save_splats(const char* path, int64_t k, int n, double sigma, const double* position,
+                    const double* depth_key, const double* theta, const double* log_scale, const double* opacity,
+                    const double* grid, char* msg, int cap) {
+    try {
+        save_splats(std::string(path), make_set(k, n, sigma, position, depth_key, theta, log_scale, opacity, grid));
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 1;
+    }
+}
+
+// load_splats(path) (serialize.hpp:118-124): on success returns 0 and the header values; on
+// SplatIoError returns 1 with its message.  Fields are copied out when the pointers are non-null.
+int ref_load_splats(const char* path, int64_t* k, int* n, double* sigma, double* position, double* depth_key,
+                    double* theta, double* log_scale, double* opacity, double* grid, char* msg, int cap) {
+    try {
+        SplatSet s = load_splats(std::string(path));
+        *k = (int64_t)s.count;
+        *n = s.grid_config.n;
+        *sigma = s.grid_config.sigma;
+        if (position) {
+            std::memcpy(position, s.position.data(), sizeof(double) * s.position.size());
+            std::memcpy(depth_key, s.depth_key.data(), sizeof(double) * s.depth_key.size());
+            std::memcpy(theta, s.theta.data(), sizeof(double) * s.theta.size());
+            std::memcpy(log_scale, s.log_scale.data(), sizeof(double) * s.log_scale.size());
+            std::memcpy(opacity, s.opacity_logit.data(), sizeof(double) * s.opacity_logit.size());
+            std::memcpy(grid, s.grid.data(), sizeof(double) * s.grid.size());
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 1;
+    }
 }
 
 }  // extern "C"

@@ -31,5 +31,6 @@ from .raster import (  # noqa: F401
     render_backward,
     render_forward,
 )
+from .splat_io import SplatIoError, file_info, load_splats, save_splats  # noqa: F401
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -20,6 +20,7 @@ GB_CUDA_ERROR = 3
 GB_OOM = 4
 GB_NONFINITE = 5
 GB_NOT_SUPPORTED = 6
+GB_IO_ERROR = 7
 
 MODE_ORTHO = 0
 MODE_PINHOLE = 1
@@ -55,6 +56,11 @@ class Grads(C.Structure):
         ("opacity_logit", C.c_void_p),
         ("grid_values", C.c_void_p),
     ]
+
+
+class SplatFileInfo(C.Structure):
+    _fields_ = [("version", C.c_int32), ("mode", C.c_int32), ("count", C.c_int64), ("n", C.c_int32),
+                ("sigma", C.c_float)]
 
 
 class Camera(C.Structure):
@@ -172,6 +178,9 @@ _SIGS = {
          C.POINTER(LearningRatesC)],
     ),
     "gb_adam_check": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "gb_splats_file_info": (C.c_int, [C.c_char_p, C.POINTER(SplatFileInfo)]),
+    "gb_splats_save": (C.c_int, [P, C.POINTER(Splats), C.c_int32, C.c_char_p]),
+    "gb_splats_load": (C.c_int, [P, C.c_char_p, C.c_int64, C.c_int32, C.POINTER(Grads)]),
     "gb_scene_generate": (C.c_int, [C.POINTER(SceneSpec), P, P, P, P, P, P, P]),
     "gb_uniform_fill": (C.c_int, [C.c_uint64, C.c_int64, P]),
     "gb_rng_uniform": (C.c_int, [C.c_uint64, C.c_int64, P]),
@@ -216,6 +225,10 @@ class NonFinite(GBError):
     pass
 
 
+class SplatIoError(GBError):
+    """serialize.hpp:23-25"""
+
+
 def check(status: int, where: str) -> None:
     if status == GB_OK:
         return
@@ -225,4 +238,6 @@ def check(status: int, where: str) -> None:
         raise Mismatch(status, where)
     if status == GB_NONFINITE:
         raise NonFinite(status, where)
+    if status == GB_IO_ERROR:
+        raise SplatIoError(status, where)
     raise GBError(status, where)

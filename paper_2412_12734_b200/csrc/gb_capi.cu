@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "gb_internal.cuh"
+#include "gb_io.cuh"
 
 namespace gb {
 size_t scan_temp_bytes(int64_t K);
@@ -586,7 +587,8 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
     gb::ProjParams pp = gb::make_proj_params(s, cam, &b->cfg, b->tiles_x, b->tiles_y);
     {
         ProfScope ps(ctx, GB_K_CHAIN);
-        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
+        GB_CUDA(gb::launch_chain(pp, b->perm.as<int32_t>(), b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g,
+                                 stream));
     }
     ctx->launches += 2;
     return GB_OK;
@@ -688,6 +690,208 @@ gb_status gb_adam_check(gb_context* ctx, int32_t* group, int64_t* index) {
     if (index) *index = idx;
     return fail(GB_NONFINITE, "adam_step: non-finite gradient in group '%s' at index %lld", names[grp & 7],
                 (long long)idx);
+}
+
+// ---- GBIL splat files (serialize.hpp:15-124) --------------------------------------------------
+namespace {
+constexpr size_t kHeaderBytes = 20;           // "GBIL", u32 version, u32 K, u32 N, f32 sigma
+constexpr size_t kChunkBytes = 16u << 20;     // pinned staging half-buffer
+
+struct FileCloser {
+    FILE* f;
+    ~FileCloser() {
+        if (f) std::fclose(f);
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+struct ScopedDev : DevBuf {
+    ~ScopedDev() { release(); }
+};
+
+struct EventPair {
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    cudaError_t create() {
+        for (auto& x : e) {
+            cudaError_t r = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+            if (r != cudaSuccess) return r;
+        }
+        return cudaSuccess;
+    }
+    ~EventPair() {
+        for (auto x : e)
+            if (x) cudaEventDestroy(x);
+    }
+};
+
+int record_fields(int version) { return version == 1 ? 7 : 10; }
+
+// serialize.hpp:83-101 (header checks, same messages); fills info, leaves f after the header
+gb_status read_header(FILE* f, gb_splat_file_info* info) {
+    unsigned char h[kHeaderBytes];
+    if (std::fread(h, 1, 4, f) != 4 || std::memcmp(h, "GBIL", 4) != 0)
+        return fail(GB_IO_ERROR, "bad splat file: wrong magic");
+    if (std::fread(h + 4, 1, 16, f) != 16) return fail(GB_IO_ERROR, "bad splat file: truncated header");
+    uint32_t version, k, n;
+    float sigma;
+    std::memcpy(&version, h + 4, 4);  // little-endian host (x86-64 / aarch64)
+    std::memcpy(&k, h + 8, 4);
+    std::memcpy(&n, h + 12, 4);
+    std::memcpy(&sigma, h + 16, 4);
+    if (version != 1 && version != 2) return fail(GB_IO_ERROR, "unsupported splat file version %u", version);
+    if (n < 1 || !(sigma > 0.0f)) return fail(GB_IO_ERROR, "bad splat file: invalid grid config");
+    info->version = (int32_t)version;
+    info->mode = version == 1 ? GB_MODE_ORTHO : GB_MODE_PINHOLE;
+    info->count = k;
+    info->n = (int32_t)n;
+    info->sigma = sigma;
+    return GB_OK;
+}
+// serialize.hpp:104-117: the first record that is not complete names the truncation
+gb_status check_records(FILE* f, const gb_splat_file_info& info, const char* path) {
+    const size_t rec_bytes = sizeof(float) * ((size_t)record_fields(info.version) + 3u * info.n * info.n);
+    if (std::fseek(f, 0, SEEK_END) != 0) return fail(GB_IO_ERROR, "cannot read splat file: %s", path);
+    const long long size = std::ftell(f);
+    if (size < (long long)kHeaderBytes) return fail(GB_IO_ERROR, "cannot read splat file: %s", path);
+    const size_t avail = (size_t)size - kHeaderBytes;
+    if (avail / rec_bytes < (size_t)info.count)
+        return fail(GB_IO_ERROR, "bad splat file: truncated at record %lld", (long long)(avail / rec_bytes));
+    if (std::fseek(f, (long)kHeaderBytes, SEEK_SET) != 0) return fail(GB_IO_ERROR, "cannot read splat file: %s", path);
+    return GB_OK;
+}
+}  // namespace
+
+gb_status gb_splats_file_info(const char* path, gb_splat_file_info* info) {
+    if (!path || !info) return fail(GB_INVALID_ARGUMENT, "null argument");
+    FileCloser fc{std::fopen(path, "rb")};
+    if (!fc.f) return fail(GB_IO_ERROR, "cannot open splat file: %s", path);
+    if (gb_status st = read_header(fc.f, info)) return st;
+    return check_records(fc.f, *info, path);
+}
+
+gb_status gb_splats_save(gb_context* ctx, const gb_splats* s, int32_t mode, const char* path) {
+    if (!ctx || !s || !path) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = validate_splats(s, mode)) return st;
+    if (gb_status st = set_device(ctx)) return st;
+    const int version = mode == GB_MODE_ORTHO ? 1 : 2;
+    const gb::RecordMap m = gb::record_map(version, s);
+    const size_t rec_bytes = sizeof(float) * (size_t)(gb::record_fields_of(m));
+    const size_t total = rec_bytes * (size_t)s->count;
+    ScopedDev dev;
+    PinnedBuf pin;
+    if (total) {
+        GB_CUDA(dev.ensure(total));
+        GB_CUDA(cudaMallocHost(&pin.p, 2 * kChunkBytes));
+        GB_CUDA(gb::launch_pack(s->count, m, s->grid_values, dev.as<float>(), ctx->sm_count, ctx->stream));
+        ctx->launches += 1;
+    }
+    FileCloser fc{std::fopen(path, "wb")};
+    if (!fc.f) return fail(GB_IO_ERROR, "cannot open for writing: %s", path);
+    unsigned char h[kHeaderBytes];
+    const uint32_t v = (uint32_t)version, k = (uint32_t)s->count, n = (uint32_t)s->grid.n;
+    const float sigma = (float)s->grid.sigma;
+    std::memcpy(h, "GBIL", 4);
+    std::memcpy(h + 4, &v, 4);
+    std::memcpy(h + 8, &k, 4);
+    std::memcpy(h + 12, &n, 4);
+    std::memcpy(h + 16, &sigma, 4);
+    bool ok = std::fwrite(h, 1, kHeaderBytes, fc.f) == kHeaderBytes;
+    // double-buffered: the D2H copy of chunk i+1 overlaps the fwrite of chunk i
+    EventPair evp;
+    if (total) GB_CUDA(evp.create());
+    cudaEvent_t* ev = evp.e;
+    char* hp = static_cast<char*>(pin.p);
+    size_t off = 0;
+    int b = 0;
+    if (total) {
+        const size_t len0 = total < kChunkBytes ? total : kChunkBytes;
+        GB_CUDA(cudaMemcpyAsync(hp, dev.p, len0, cudaMemcpyDeviceToHost, ctx->stream));
+        GB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    }
+    while (off < total) {
+        const size_t len = total - off < kChunkBytes ? total - off : kChunkBytes;
+        const size_t nxt = off + len;
+        if (nxt < total) {
+            const size_t len2 = total - nxt < kChunkBytes ? total - nxt : kChunkBytes;
+            GB_CUDA(cudaMemcpyAsync(hp + (size_t)(b ^ 1) * kChunkBytes, static_cast<char*>(dev.p) + nxt, len2,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            GB_CUDA(cudaEventRecord(ev[b ^ 1], ctx->stream));
+        }
+        GB_CUDA(cudaEventSynchronize(ev[b]));
+        ok = ok && std::fwrite(hp + (size_t)b * kChunkBytes, 1, len, fc.f) == len;
+        off = nxt;
+        b ^= 1;
+    }
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ok = ok && std::fflush(fc.f) == 0;
+    if (!ok) return fail(GB_IO_ERROR, "splat write failed: %s", path);
+    return GB_OK;
+}
+
+gb_status gb_splats_load(gb_context* ctx, const char* path, int64_t count, int32_t n, gb_grads* dst) {
+    if (!ctx || !path || !dst) return fail(GB_INVALID_ARGUMENT, "null argument");
+    FileCloser fc{std::fopen(path, "rb")};
+    if (!fc.f) return fail(GB_IO_ERROR, "cannot open splat file: %s", path);
+    gb_splat_file_info info;
+    if (gb_status st = read_header(fc.f, &info)) return st;
+    if (info.count != count || info.n != n)
+        return fail(GB_MISMATCH, "load_splats: destination sized for K=%lld n=%d, file has K=%lld n=%d",
+                    (long long)count, n, (long long)info.count, info.n);
+    gb_splats s{};
+    s.count = count;
+    s.grid.n = n;
+    s.grid.sigma = info.sigma;
+    s.position = dst->position;
+    s.depth_key = dst->depth_key;
+    s.theta = dst->theta;
+    s.quat = dst->quat;
+    s.log_scale = dst->log_scale;
+    s.opacity_logit = dst->opacity_logit;
+    s.grid_values = dst->grid_values;
+    if (gb_status st = validate_splats(&s, info.mode)) return st;
+    const gb::RecordMap m = gb::record_map(info.version, &s);
+    const size_t rec_bytes = sizeof(float) * (size_t)gb::record_fields_of(m);
+    const size_t total = rec_bytes * (size_t)count;
+    if (gb_status st = check_records(fc.f, info, path)) return st;
+    if (total == 0) return GB_OK;
+    if (gb_status st = set_device(ctx)) return st;
+    ScopedDev dev;
+    PinnedBuf pin;
+    GB_CUDA(dev.ensure(total));
+    GB_CUDA(cudaMallocHost(&pin.p, 2 * kChunkBytes));
+    EventPair evp;
+    GB_CUDA(evp.create());
+    cudaEvent_t* ev = evp.e;
+    char* hp = static_cast<char*>(pin.p);
+    size_t off = 0;
+    int b = 0;
+    bool ok = true, used[2] = {false, false};
+    // double-buffered: the fread of chunk i+1 overlaps the H2D copy of chunk i
+    while (off < total && ok) {
+        const size_t len = total - off < kChunkBytes ? total - off : kChunkBytes;
+        if (used[b]) GB_CUDA(cudaEventSynchronize(ev[b]));
+        ok = std::fread(hp + (size_t)b * kChunkBytes, 1, len, fc.f) == len;
+        if (!ok) break;
+        GB_CUDA(cudaMemcpyAsync(static_cast<char*>(dev.p) + off, hp + (size_t)b * kChunkBytes, len,
+                                cudaMemcpyHostToDevice, ctx->stream));
+        GB_CUDA(cudaEventRecord(ev[b], ctx->stream));
+        used[b] = true;
+        off += len;
+        b ^= 1;
+    }
+    if (ok) {
+        GB_CUDA(gb::launch_unpack(count, m, dst->grid_values, dev.as<float>(), ctx->sm_count, ctx->stream));
+        ctx->launches += 1;
+    }
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!ok) return fail(GB_IO_ERROR, "bad splat file: truncated at record %lld", (long long)(off / rec_bytes));
+    return GB_OK;
 }
 
 }  // extern "C"

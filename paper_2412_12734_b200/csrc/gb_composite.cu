@@ -72,25 +72,87 @@ __device__ __forceinline__ void group_pixel(int tid, int ts, int tx, int ty, int
     y = wy0 + gy + i / GroupShape<G>::BW;
 }
 
-// Refill test of group gs: does entry `id`'s alpha-skip ellipse meet the
-// group's pixel block (pixel indices, enlarged by 0.05 px like alpha_box)?
+// ---------------------------------------------------------------------------
+// The walk: a ring of two shared 32-entry windows per warp.  The warp tests a
+// window's 32 entries (one per lane) against every group's block with the
+// exact alpha-skip-ellipse test and parks the ids and the per-group pass masks
+// in shared memory; each group then consumes its own mask, one entry per step,
+// and moves to the next window as soon as it is done -- at most one window
+// ahead of the slowest group (tools/sim_steps.py "ring2": within 1 % of fully
+// independent group cursors, at one test round per 32 entries for all groups).
+// Forward windows run front to back over [0, total); backward windows back to
+// front over [0, L) with L = 1 + the warp's largest last rank.
+// ---------------------------------------------------------------------------
 template <int G>
-__device__ __forceinline__ bool group_test(const CullRec* __restrict__ cull, int id, int wx0, int wy0, int gs) {
-    int gx, gy;
-    group_origin<G>(gs, gx, gy);
-    const float x0 = (float)(wx0 + gx) - 0.05f, y0 = (float)(wy0 + gy) - 0.05f;
-    const float4 a = __ldg(&cull[id].a), b = __ldg(&cull[id].b);
-    return ellipse_meets_rect(a, b, x0, x0 + (float)(GroupShape<G>::BW - 1) + 0.1f, y0,
-                              y0 + (float)(GroupShape<G>::BH - 1) + 0.1f);
+struct WarpRing {
+    int ids[2][32];
+    unsigned masks[2][32 / G];
+    int glast[32 / G];  // backward: the largest last rank of each group's pixels
+};
+
+// Group walk state (every field uniform across the group's lanes).
+struct GroupWalk {
+    int w;          // absolute index of the window being consumed (-1 before the first)
+    unsigned pend;  // entries of window w still to composite (bit i <-> i-th rank of the window)
+    bool fin;       // group finished (forward: every pixel terminated early)
+};
+
+// Window k: ranks first, first + dir, ... (count of them); dir = +1 forward, -1 backward.
+template <int G, bool BWD>
+__device__ __forceinline__ void ring_fill(WarpRing<G>& ring, int k, int first, int count, const int32_t* values,
+                                          uint32_t base, const CullRec* __restrict__ cull, int wx0, int wy0,
+                                          int lane) {
+    constexpr int NG = 32 / G;
+    const int r = BWD ? first - lane : first + lane;
+    const bool valid = lane < count;
+    int id = -1;
+    float4 ca = make_float4(0.f, 0.f, 0.f, 0.f), cb = ca;
+    if (valid) {
+        id = __ldg(&values[base + r]);
+        ca = __ldg(&cull[id].a);
+        cb = __ldg(&cull[id].b);
+    }
+    ring.ids[k & 1][lane] = id;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        int gx, gy;
+        group_origin<G>(g, gx, gy);
+        const float x0 = (float)(wx0 + gx) - 0.05f, y0 = (float)(wy0 + gy) - 0.05f;
+        const bool pass = valid && (!BWD || r <= ring.glast[g]) &&
+                          ellipse_meets_rect(ca, cb, x0, x0 + (float)(GroupShape<G>::BW - 1) + 0.1f, y0,
+                                             y0 + (float)(GroupShape<G>::BH - 1) + 0.1f);
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (lane == 0) ring.masks[k & 1][g] = m;
+    }
 }
 
-// Group-wide cursor over one direction of the tile list (every field is
-// uniform across the group's lanes).
-struct Cursor {
-    int cur;        // next rank to test (forward ascending, backward descending); outside the list = exhausted
-    int wbase;      // rank of bit 0 of the pending window
-    unsigned pend;  // passing entries of the window not yet composited (bit i <-> rank wbase +/- i)
-};
+// Advance every group whose mask is used up, filling windows as needed.
+// wc = windows filled so far (warp-uniform), nwin = windows in the walk.
+template <int G, bool BWD>
+__device__ __forceinline__ void ring_advance(WarpRing<G>& ring, GroupWalk& gw, int& wc, int nwin, int span,
+                                             const int32_t* values, uint32_t base, const CullRec* __restrict__ cull,
+                                             int wx0, int wy0, int lane) {
+    const int g = lane / G;
+    for (;;) {
+        for (;;) {  // consume filled windows
+            const bool adv = !gw.fin && gw.pend == 0 && gw.w + 1 < wc;
+            if (!__any_sync(kFull, adv)) break;
+            if (adv) {
+                ++gw.w;
+                gw.pend = ring.masks[gw.w & 1][g];
+            }
+        }
+        const bool want = !gw.fin && gw.pend == 0 && gw.w + 1 == wc && wc < nwin;
+        if (!__any_sync(kFull, want)) break;
+        // slot wc & 1 still holds window wc - 2 while a group consumes it
+        if (__reduce_min_sync(kFull, gw.fin ? 0x7fffffff : gw.w) < wc - 1) break;
+        const int first = BWD ? span - 1 - 32 * wc : 32 * wc;
+        __syncwarp();  // readers of the slot being refilled are done
+        ring_fill<G, BWD>(ring, wc, first, min(32, span - 32 * wc), values, base, cull, wx0, wy0, lane);
+        __syncwarp();
+        ++wc;
+    }
+}
 
 // Sum of NV per-lane values per group: returns, in out[k], the total of value
 // row(q) over the lanes of group grp(q) for pair q = lane + 32 k, q < NV * 32/G
@@ -132,12 +194,11 @@ __global__ void __launch_bounds__(256) k_forward_grp(const uint2* __restrict__ r
                                                      float* __restrict__ out_color, float* __restrict__ out_trans,
                                                      int32_t* __restrict__ out_last) {
     constexpr int NG = 32 / G;
-    __shared__ int s_ids[8][NG][32];  // per warp and group: ids of the current window
+    __shared__ WarpRing<G> s_ring[8];
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
     const int ts = rc.tile_size;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane / G;
     const unsigned gm = group_mask<G>(lane);
     const int tile = blockIdx.x;
     const uint2 range = ranges[tile];
@@ -150,82 +211,66 @@ __global__ void __launch_bounds__(256) k_forward_grp(const uint2* __restrict__ r
     float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
     int last = -1;
     bool done = !inside;
-    Cursor c{__all_sync(gm, done) ? total : 0, 0, 0u};  // a group with no pixel in the image has nothing to do
+    WarpRing<G>& ring = s_ring[warp];
+    const int nwin = (total + 31) / 32;
+    int wc = 0;
+    GroupWalk gw{-1, 0u, __all_sync(gm, done) != 0};  // a group with no pixel in the image has nothing to do
     for (;;) {
-        for (;;) {  // refill, one group per round, every group whose window is used up
-            const unsigned need = __ballot_sync(kFull, c.pend == 0 && c.cur < total);
-            if (!need) break;
-            const int gs = (__ffs(need) - 1) / G;
-            const int cs = __shfl_sync(kFull, c.cur, gs * G);
-            const int r = cs + lane;
-            int idl = -1;
-            bool pass = false;
-            if (r < total) {
-                idl = __ldg(&values[range.x + r]);
-                pass = group_test<G>(cull, idl, wx0, wy0, gs);
-            }
-            const unsigned bal = __ballot_sync(kFull, pass);
-            s_ids[warp][gs][lane] = idl;
-            if (g == gs) {
-                c.pend = bal;
-                c.wbase = cs;
-                c.cur = cs + 32;
-            }
-        }
-        __syncwarp();
-        if (!__any_sync(kFull, c.pend != 0)) break;
-        if (c.pend != 0 && !done) {
-            const int bit = __ffs(c.pend) - 1;
-            const int id = s_ids[warp][g][bit];
-            ScreenHeader h;
-            h.h0 = __ldg(&hdr[id].h0);
-            h.h1 = __ldg(&hdr[id].h1);
-            h.h2 = __ldg(&hdr[id].h2);
-            float u, v;
-            bool hit;
-            if (MODE == GB_MODE_ORTHO) {
-                hit = eval_uv_ortho(h, x, y, u, v);
-            } else {
-                PinholeTerms pt;
-                hit = eval_uv_pinhole(h, x, y, u, v, pt);
-            }
-            if (hit) {
-                const float alpha = fminf(__fmul_rn(h.h1.z, gauss_weight(u, v)), kMaxAlphaF);  // raster.hpp:241
-                if (!(alpha < rc.alpha_skip)) {                                                  // raster.hpp:242
-                    const float* t = tex + (size_t)id * F;
-                    float c0_, c1_, c2_;
-                    if (N == 1) {
-                        c0_ = __ldg(t);
-                        c1_ = __ldg(t + 1);
-                        c2_ = __ldg(t + 2);
-                    } else {
-                        Bilin b;
-                        bilin_setup(u, v, N, rc, b);
-                        const float* p00 = t + b.o00;
-                        const float* p10 = p00 + 3 * N;
-                        c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 +
-                              __ldg(p10 + 3) * b.w11;
-                        c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
-                              __ldg(p10 + 4) * b.w11;
-                        c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
-                              __ldg(p10 + 5) * b.w11;
+        ring_advance<G, false>(ring, gw, wc, nwin, total, values, range.x, cull, wx0, wy0, lane);
+        if (!__any_sync(kFull, gw.pend != 0)) break;
+        if (gw.pend != 0) {
+            const int bit = __ffs(gw.pend) - 1;
+            gw.pend &= gw.pend - 1;
+            if (!done) {
+                const int id = ring.ids[gw.w & 1][bit];
+                ScreenHeader h;
+                h.h0 = __ldg(&hdr[id].h0);
+                h.h1 = __ldg(&hdr[id].h1);
+                h.h2 = __ldg(&hdr[id].h2);
+                float u, v;
+                bool hit;
+                if (MODE == GB_MODE_ORTHO) {
+                    hit = eval_uv_ortho(h, x, y, u, v);
+                } else {
+                    PinholeTerms pt;
+                    hit = eval_uv_pinhole(h, x, y, u, v, pt);
+                }
+                if (hit) {
+                    const float alpha = fminf(__fmul_rn(h.h1.z, gauss_weight(u, v)), kMaxAlphaF);  // raster.hpp:241
+                    if (!(alpha < rc.alpha_skip)) {                                                  // raster.hpp:242
+                        const float* t = tex + (size_t)id * F;
+                        float c0_, c1_, c2_;
+                        if (N == 1) {
+                            c0_ = __ldg(t);
+                            c1_ = __ldg(t + 1);
+                            c2_ = __ldg(t + 2);
+                        } else {
+                            Bilin b;
+                            bilin_setup(u, v, N, rc, b);
+                            const float* p00 = t + b.o00;
+                            const float* p10 = p00 + 3 * N;
+                            c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 +
+                                  __ldg(p10 + 3) * b.w11;
+                            c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
+                                  __ldg(p10 + 4) * b.w11;
+                            c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
+                                  __ldg(p10 + 5) * b.w11;
+                        }
+                        const float w = alpha * T;  // raster.hpp:244-249
+                        acc0 = fmaf(c0_, w, acc0);
+                        acc1 = fmaf(c1_, w, acc1);
+                        acc2 = fmaf(c2_, w, acc2);
+                        T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                        last = 32 * gw.w + bit;
+                        if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;  // raster.hpp:250
                     }
-                    const float w = alpha * T;  // raster.hpp:244-249
-                    acc0 = fmaf(c0_, w, acc0);
-                    acc1 = fmaf(c1_, w, acc1);
-                    acc2 = fmaf(c2_, w, acc2);
-                    T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                    last = c.wbase + bit;
-                    if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;  // raster.hpp:250
                 }
             }
         }
-        c.pend &= c.pend - 1;
-        if (__all_sync(gm, done)) {  // the whole group terminated early: retire its cursor
-            c.pend = 0;
-            c.cur = total;
+        if (__all_sync(gm, done)) {  // the whole group terminated early
+            gw.fin = true;
+            gw.pend = 0;
         }
-        __syncwarp();  // s_ids readers done before the next refill overwrites
     }
     if (inside) {  // raster.hpp:253-254
         const size_t q = (size_t)y * cc.width + x;
@@ -362,12 +407,11 @@ __global__ void __launch_bounds__(256, 4) k_backward_grp(const uint2* __restrict
     constexpr int PS = (NS * NG + 31) / 32;             // reduction passes (screen sums)
     constexpr int PT = (12 * NG + 31) / 32;             // reduction passes (texels)
     __shared__ __align__(16) float red_scratch[8 * kRedRows * kRedStride];
-    __shared__ int s_ids[8][NG][32];
+    __shared__ WarpRing<G> s_ring[8];
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
     const int ts = rc.tile_size;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane / G;
     const unsigned gm = group_mask<G>(lane);
     const int tile = blockIdx.x;
     const uint2 range = ranges[tile];
@@ -392,48 +436,34 @@ __global__ void __launch_bounds__(256, 4) k_backward_grp(const uint2* __restrict
     s.bh1 = cc.bg[1];
     s.bh2 = cc.bg[2];
     float* wscratch = red_scratch + warp * kRedRows * kRedStride;
-    // each group walks ranks [0, max last of its pixels] back to front
-    Cursor c{__reduce_max_sync(gm, s.last), 0, 0u};
+    WarpRing<G>& ring = s_ring[warp];
+    // the warp walks ranks [0, span) back to front; a group never needs ranks above its own largest last
+    const int span = __reduce_max_sync(kFull, s.last) + 1;
+    const int nwin = (span + 31) / 32;
+    const int gl = __reduce_max_sync(gm, s.last);
+    if (lane % G == 0) ring.glast[lane / G] = gl;
+    __syncwarp();
+    int wc = 0;
+    GroupWalk gw{-1, 0u, false};
     for (;;) {
-        for (;;) {  // refill, one group per round, every group whose window is used up
-            const unsigned need = __ballot_sync(kFull, c.pend == 0 && c.cur >= 0);
-            if (!need) break;
-            const int gs = (__ffs(need) - 1) / G;
-            const int cs = __shfl_sync(kFull, c.cur, gs * G);
-            const int r = cs - lane;
-            int idl = -1;
-            bool pass = false;
-            if (r >= 0) {
-                idl = __ldg(&values[range.x + r]);
-                pass = group_test<G>(cull, idl, wx0, wy0, gs);
-            }
-            const unsigned bal = __ballot_sync(kFull, pass);
-            s_ids[warp][gs][lane] = idl;
-            if (g == gs) {
-                c.pend = bal;
-                c.wbase = cs;
-                c.cur = cs - 32;
-            }
-        }
-        __syncwarp();
-        if (!__any_sync(kFull, c.pend != 0)) break;
+        ring_advance<G, true>(ring, gw, wc, nwin, span, values, range.x, cull, wx0, wy0, lane);
+        if (!__any_sync(kFull, gw.pend != 0)) break;
         int id = -1;
         bool on = false;
         float red[10], tg[12];
         int tbase = 0;
-        if (c.pend != 0) {
-            const int bit = __ffs(c.pend) - 1;
-            id = s_ids[warp][g][bit];
-            if (c.wbase - bit <= s.last) {
+        if (gw.pend != 0) {
+            const int bit = __ffs(gw.pend) - 1;
+            gw.pend &= gw.pend - 1;
+            id = ring.ids[gw.w & 1][bit];
+            if (span - 1 - 32 * gw.w - bit <= s.last) {
                 ScreenHeader h;
                 h.h0 = __ldg(&hdr[id].h0);
                 h.h1 = __ldg(&hdr[id].h1);
                 h.h2 = __ldg(&hdr[id].h2);
                 on = bwd_px<MODE, NT>(h, tex + (size_t)id * F, N, s, rc, red, tg, tbase);
             }
-            c.pend &= c.pend - 1;
         }
-        __syncwarp();  // s_ids readers done before the next refill overwrites
         const unsigned act = __ballot_sync(kFull, on);
         if (act == 0) continue;
         {  // screen-space sums: one per (value, group), owned by distinct lanes

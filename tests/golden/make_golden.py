@@ -10,6 +10,7 @@ Writes (small, committed):
   naive_fd.npz    -- reference render_naive + gradient_fd on a tiny scene
   rng.npz         -- reference Rng uniform()/normal() streams
   kat.json        -- SPEC known-answer examples evaluated by the reference
+  ref_k9_n3.gbil  -- a GBIL v1 splat file written by the reference's save_splats
 The fixtures travel to the GPU box; nothing there reads /root/reference.
 """
 import json
@@ -126,6 +127,14 @@ def kat():
         json.dump(res, fh, indent=1)
 
 
+def gbil_file():
+    """A small v1 splat file written by the reference itself (serialize.hpp:83-90)."""
+    arrays = sc.generate(O.MODE_ORTHO, 9, 3, 109, width=40, height=30, scale_lo=0.7, scale_hi=6.0)
+    scene = O.Scene64(arrays, 3, 0.375)
+    msg = O.ref_save_splats(os.path.join(HERE, "ref_k9_n3.gbil"), scene)
+    assert msg == "", msg
+
+
 if __name__ == "__main__":
     if not O.ref_available():
         O.build()
@@ -133,5 +142,6 @@ if __name__ == "__main__":
     naive_fd()
     rng_streams()
     kat()
+    gbil_file()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -98,6 +98,29 @@ def main():
                     gid = (lx // 2) + 4 * (ly // 2)
                 ga = np.stack([act[:, gid == g].any(1) for g in np.unique(gid)], 1)  # (entries, groups)
                 tot[name] += ga.sum(0).max()
+                # ring of R shared 32-entry windows: a group may run at most R-1 windows ahead of the slowest
+                for R in (2, 4):
+                    key = f"{name} ring{R}"
+                    n = ga.shape[0]
+                    nw = (n + 31) // 32
+                    ng = ga.shape[1]
+                    lists = [[np.nonzero(ga[w * 32:(w + 1) * 32, gg])[0].tolist() for w in range(nw)] for gg in range(ng)]
+                    wi = [0] * ng
+                    pos = [0] * ng
+                    steps = 0
+                    def norm(gg):
+                        while wi[gg] < nw and pos[gg] >= len(lists[gg][wi[gg]]):
+                            wi[gg] += 1; pos[gg] = 0
+                    for gg in range(ng):
+                        norm(gg)
+                    while any(wi[gg] < nw for gg in range(ng)):
+                        lo = min(wi)
+                        for gg in range(ng):
+                            if wi[gg] < nw and wi[gg] < lo + R:
+                                pos[gg] += 1
+                                norm(gg)
+                        steps += 1
+                    tot[key] = tot.get(key, 0) + steps
                 for ch in (32, 64):
                     key = f"{name} chunk{ch}"
                     n = ga.shape[0]
