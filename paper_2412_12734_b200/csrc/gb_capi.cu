@@ -587,8 +587,7 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
     gb::ProjParams pp = gb::make_proj_params(s, cam, &b->cfg, b->tiles_x, b->tiles_y);
     {
         ProfScope ps(ctx, GB_K_CHAIN);
-        GB_CUDA(gb::launch_chain(pp, b->perm.as<int32_t>(), b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g,
-                                 stream));
+        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
     }
     ctx->launches += 2;
     return GB_OK;

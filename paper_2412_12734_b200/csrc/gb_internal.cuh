@@ -164,8 +164,8 @@ ProjParams make_proj_params(const gb_splats* s, const gb_camera* cam, const gb_r
                             int tiles_y);
 cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, CullRec* cull, uint2* rects, uint32_t* counts,
                            uint32_t* depth_bits, cudaStream_t st);
-cudaError_t launch_chain(const ProjParams& p, const int32_t* perm, const uint32_t* counts, const float* accum,
-                         const gb_grads& g, cudaStream_t st);
+cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
+                         cudaStream_t st);
 
 // gb_composite.cu: K3/K4 with sub-warp groups (tile sizes 8 and 16)
 bool grp_supported(int ts);

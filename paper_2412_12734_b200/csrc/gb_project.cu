@@ -364,15 +364,10 @@ __global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeade
 // gradient buffer.  Ortho: raster.hpp:350-360 with the per-eval products
 // (u_hat*u, ...) summed by K4.  Pinhole: dL/dM from (S_A, S_B, S_D) then the
 // camera/quaternion chain (oracle pinhole_chain()).
-// Threads walk the primitives in the binning's depth order (perm): the culled
-// ones sort last, so whole warps retire at once instead of idling among the
-// binned primitives' fp64 chains.
-__global__ void __launch_bounds__(256) k_chain(const ProjParams p, const int32_t* __restrict__ perm,
-                                               const uint32_t* __restrict__ counts, const float* __restrict__ accum,
-                                               gb_grads g_out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.K) return;
-    const int64_t k = perm[i];
+__global__ void __launch_bounds__(256) k_chain(const ProjParams p, const uint32_t* __restrict__ counts,
+                                               const float* __restrict__ accum, gb_grads g_out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p.K) return;
     if (counts[k] == 0) return;
     const float4* a4 = reinterpret_cast<const float4*>(accum + k * kAccumStride);
     const float4 A = a4[0], B = a4[1], C = a4[2];
@@ -500,12 +495,12 @@ cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, CullRec* cull
     return cudaGetLastError();
 }
 
-cudaError_t launch_chain(const ProjParams& p, const int32_t* perm, const uint32_t* counts, const float* accum,
-                         const gb_grads& g, cudaStream_t st) {
+cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
+                         cudaStream_t st) {
     if (p.K == 0) return cudaSuccess;
     const int threads = 256;
     const unsigned blocks = (unsigned)((p.K + threads - 1) / threads);
-    k_chain<<<blocks, threads, 0, st>>>(p, perm, counts, accum, g);
+    k_chain<<<blocks, threads, 0, st>>>(p, counts, accum, g);
     return cudaGetLastError();
 }
 
