@@ -213,6 +213,16 @@ GB_API gb_status gb_l1_loss(gb_context *ctx, const float *color, const float *ta
 GB_API gb_status gb_mse_loss(gb_context *ctx, const float *color, const float *target, int64_t n, float scale, float *grad,
                       float *loss);
 
+/* ---- image metrics (metrics.hpp) ------------------------------------------- */
+/* ssim (metrics.hpp:183-185) with clamp01 = 1, ssim_with_gradient (metrics.hpp:189-191) with clamp01 = 0:
+ * Wang 2004 SSIM, 11-tap Gaussian window (std 1.5), K1 = 0.01, K2 = 0.03, valid windows, channels averaged,
+ * on HWC fp32 images.  *mean_ssim (a DEVICE double) += the mean SSIM; when grad != NULL (clamp01 = 0 only),
+ * grad += grad_scale * d(mean SSIM)/d(a).  Asynchronous.  W, H >= 11 (else GB_INVALID_ARGUMENT, as the reference). */
+GB_API gb_status gb_ssim(gb_context *ctx, const float *a, const float *b, int32_t width, int32_t height,
+                         int32_t clamp01, double *mean_ssim, float *grad, float grad_scale);
+/* psnr (metrics.hpp:169-179): both images clamped to [0,1], capped at 99 dB.  Synchronous; *out on the host. */
+GB_API gb_status gb_psnr(gb_context *ctx, const float *a, const float *b, int64_t n, double *out);
+
 /* ---- optimiser: adam_step (optim.hpp:96-117) ------------------------------ */
 /* params uses the gb_grads layout (mutable parameter arrays).  Increments
  * state->t.  Non-finite gradients are detected on the device first; if any is
@@ -261,6 +271,10 @@ typedef struct {
 /* Geometry from Rng(seed), textures from Rng(seed+1).  Host fp32 buffers. */
 GB_API gb_status gb_scene_generate(const gb_scene_spec *spec, float *position, float *depth_key, float *theta, float *quat,
                             float *log_scale, float *opacity_logit, float *grid_values);
+/* initialize() of the image-fitting loop (train.hpp:80-111), ortho SplatSet, same Rng draws, fp32 host buffers. */
+GB_API gb_status gb_fit_initialize(int32_t width, int32_t height, int64_t count, int32_t n, uint64_t seed,
+                                   float *position, float *depth_key, float *theta, float *log_scale,
+                                   float *opacity_logit, float *grid_values);
 /* n uniforms in [0,1) from Rng(seed), rounded to fp32 (targets use seed+2+view). */
 GB_API gb_status gb_uniform_fill(uint64_t seed, int64_t n, float *out);
 /* Raw Rng streams in fp64, for parity with rng.hpp. */

@@ -117,6 +117,13 @@ def ref_lib():
         L.ref_render_naive.argtypes = [C.c_int64, i, d, P, P, P, P, P, P, i, i, P, P, P]
         L.ref_gradient_fd.argtypes = [C.c_int64, i, d, P, P, P, P, P, P, i, i, P, P, d, P, P, P, P, P, P]
         L.ref_uv_to_grid.argtypes = [d, d, i, d, P, P, P, P]
+        L.ref_ssim.argtypes = [i, i, P, P, i, P]
+        L.ref_ssim.restype = d
+        L.ref_psnr.argtypes = [i, i, P, P]
+        L.ref_psnr.restype = d
+        L.ref_initialize.argtypes = [i, i, C.c_int64, i, C.c_uint64, P, P, P, P, P, P]
+        L.ref_fit.argtypes = [i, i, P, C.c_int64, i, d, C.c_int64, i, d, C.c_uint64, C.c_int64, i, P, P, P, P, P,
+                              P, P, C.c_int64, P, C.c_char_p, i]
         L.ref_save_splats.argtypes = [C.c_char_p, C.c_int64, i, d, P, P, P, P, P, P, C.c_char_p, i]
         L.ref_load_splats.argtypes = [C.c_char_p, P, P, P, P, P, P, P, P, P, C.c_char_p, i]
         L.ref_bilinear.argtypes = [d, d, i, d, P, P]
@@ -381,6 +388,54 @@ def ref_load_splats(path: str):
                       *[out[f].ctypes.data for f in ("position", "depth_key", "theta", "log_scale", "opacity_logit",
                                                      "grid")], msg, 512)
     return out, N, sigma.value
+
+
+def ref_ssim(a, b, with_grad=False):
+    """metrics.hpp ssim (clamped) or ssim_with_gradient -> value or (value, grad)."""
+    L = ref_lib()
+    a = np.ascontiguousarray(a, np.float64); b = np.ascontiguousarray(b, np.float64)
+    h, w = a.shape[:2]
+    g = np.zeros_like(a)
+    v = L.ref_ssim(w, h, a.ctypes.data, b.ctypes.data, int(with_grad), g.ctypes.data)
+    return (v, g) if with_grad else v
+
+
+def ref_psnr(a, b):
+    L = ref_lib()
+    a = np.ascontiguousarray(a, np.float64); b = np.ascontiguousarray(b, np.float64)
+    return L.ref_psnr(a.shape[1], a.shape[0], a.ctypes.data, b.ctypes.data)
+
+
+def _ref_set(K, n):
+    return dict(position=np.zeros((K, 2)), depth_key=np.zeros(K), theta=np.zeros(K), log_scale=np.zeros((K, 2)),
+                opacity_logit=np.zeros(K), grid=np.zeros((K, n * n * 3)))
+
+
+_SET_FIELDS = ("position", "depth_key", "theta", "log_scale", "opacity_logit", "grid")
+
+
+def ref_initialize(w, h, K, n, seed):
+    """train.hpp:80-111 initialize() -> fp64 arrays."""
+    L = ref_lib()
+    out = _ref_set(K, n)
+    L.ref_initialize(w, h, K, n, seed, *[out[f].ctypes.data for f in _SET_FIELDS])
+    return out
+
+
+def ref_fit(target, K, n, iterations, mse_ssim=False, ssim_weight=0.2, seed=0, log_every=1, sigma=0.5, tile=16):
+    """train.hpp:174-219 fit() -> (final arrays, history (m, 4): iter, loss, psnr, ssim) or the error text."""
+    L = ref_lib()
+    t = np.ascontiguousarray(target, np.float64)
+    h, w = t.shape[:2]
+    out = _ref_set(K, n)
+    hist = np.zeros((iterations + 2, 4))
+    nh = C.c_int64()
+    msg = C.create_string_buffer(512)
+    rc = L.ref_fit(w, h, t.ctypes.data, K, n, sigma, iterations, int(mse_ssim), ssim_weight, seed, log_every, tile,
+                   *[out[f].ctypes.data for f in _SET_FIELDS], hist.ctypes.data, len(hist), C.byref(nh), msg, 512)
+    if rc:
+        return msg.value.decode()
+    return out, hist[: nh.value]
 
 
 def ref_render_naive(scene: Scene64, cam: Cam):

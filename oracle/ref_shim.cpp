@@ -15,6 +15,7 @@
 #include <string>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "gbil/core.hpp"
@@ -23,6 +24,7 @@
 #include "gbil/reference.hpp"
 #include "gbil/rng.hpp"
 #include "gbil/serialize.hpp"
+#include "gbil/train.hpp"  // + metrics.hpp, image.hpp (png.h: oracle/stub, never called)
 #include "gbil/texture.hpp"
 
 using namespace gbil;
@@ -233,6 +235,86 @@ int ref_load_splats(const char* path, int64_t* k, int* n, double* sigma, double*
             std::memcpy(opacity, s.opacity_logit.data(), sizeof(double) * s.opacity_logit.size());
             std::memcpy(grid, s.grid.data(), sizeof(double) * s.grid.size());
         }
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 1;
+    }
+}
+
+// ssim / ssim_with_gradient / psnr (metrics.hpp:169-191) on W x H x 3 images; grad may be null.
+double ref_ssim(int w, int h, const double* a, const double* b, int with_grad, double* grad) {
+    Image ia(w, h), ib(w, h);
+    std::memcpy(ia.data.data(), a, sizeof(double) * ia.data.size());
+    std::memcpy(ib.data.data(), b, sizeof(double) * ib.data.size());
+    if (!with_grad) return ssim(ia, ib);
+    const auto r = ssim_with_gradient(ia, ib);
+    std::memcpy(grad, r.grad_a.data.data(), sizeof(double) * r.grad_a.data.size());
+    return r.value;
+}
+
+double ref_psnr(int w, int h, const double* a, const double* b) {
+    Image ia(w, h), ib(w, h);
+    std::memcpy(ia.data.data(), a, sizeof(double) * ia.data.size());
+    std::memcpy(ib.data.data(), b, sizeof(double) * ib.data.size());
+    return psnr(ia, ib);
+}
+
+// initialize() (train.hpp:80-111) for a W x H target: the fp64 parameters.
+void ref_initialize(int w, int h, int64_t k, int n, uint64_t seed, double* position, double* depth_key,
+                    double* theta, double* log_scale, double* opacity, double* grid) {
+    TrainConfig cfg;
+    cfg.splat_count = (std::size_t)k;
+    cfg.seed = seed;
+    cfg.grid = ColorGridConfig{n, 0.5};
+    cfg.allow_any_n = true;
+    const SplatSet s = initialize(Image(w, h), cfg);
+    std::memcpy(position, s.position.data(), sizeof(double) * s.position.size());
+    std::memcpy(depth_key, s.depth_key.data(), sizeof(double) * s.depth_key.size());
+    std::memcpy(theta, s.theta.data(), sizeof(double) * s.theta.size());
+    std::memcpy(log_scale, s.log_scale.data(), sizeof(double) * s.log_scale.size());
+    std::memcpy(opacity, s.opacity_logit.data(), sizeof(double) * s.opacity_logit.size());
+    std::memcpy(grid, s.grid.data(), sizeof(double) * s.grid.size());
+}
+
+// fit() (train.hpp:174-219) on a W x H x 3 target.  hist receives (iter, loss, psnr, ssim) per logged
+// record (up to hist_cap records, count in *n_hist).  Returns 0, or 1 with FitError/invalid_argument text.
+int ref_fit(int w, int h, const double* target, int64_t k, int n, double sigma, int64_t iterations, int mse_ssim,
+            double ssim_weight, uint64_t seed, int64_t log_every, int tile, double* position, double* depth_key,
+            double* theta, double* log_scale, double* opacity, double* grid, double* hist, int64_t hist_cap,
+            int64_t* n_hist, char* msg, int cap) {
+    try {
+        Image t(w, h);
+        std::memcpy(t.data.data(), target, sizeof(double) * t.data.size());
+        TrainConfig cfg;
+        cfg.splat_count = (std::size_t)k;
+        cfg.iterations = iterations;
+        cfg.loss = mse_ssim ? LossKind::mse_plus_ssim : LossKind::mse;
+        cfg.ssim_weight = ssim_weight;
+        cfg.seed = seed;
+        cfg.grid = ColorGridConfig{n, sigma};
+        cfg.allow_any_n = true;
+        cfg.log_every = log_every;
+        cfg.raster.tile_size = tile;
+        cfg.raster.threads = (int)std::max(1u, std::thread::hardware_concurrency());
+        const FitResult r = fit(t, cfg);
+        const SplatSet& s = r.splats;
+        std::memcpy(position, s.position.data(), sizeof(double) * s.position.size());
+        std::memcpy(depth_key, s.depth_key.data(), sizeof(double) * s.depth_key.size());
+        std::memcpy(theta, s.theta.data(), sizeof(double) * s.theta.size());
+        std::memcpy(log_scale, s.log_scale.data(), sizeof(double) * s.log_scale.size());
+        std::memcpy(opacity, s.opacity_logit.data(), sizeof(double) * s.opacity_logit.size());
+        std::memcpy(grid, s.grid.data(), sizeof(double) * s.grid.size());
+        int64_t m = 0;
+        for (const MetricRecord& rec : r.history) {
+            if (m >= hist_cap) break;
+            hist[4 * m + 0] = (double)rec.iter;
+            hist[4 * m + 1] = rec.loss;
+            hist[4 * m + 2] = rec.psnr;
+            hist[4 * m + 3] = rec.ssim;
+            ++m;
+        }
+        *n_hist = m;
         return 0;
     } catch (const std::exception& e) {
         std::snprintf(msg, cap, "%s", e.what());

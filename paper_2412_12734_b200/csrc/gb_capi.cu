@@ -37,6 +37,9 @@ cudaError_t launch_loss(int kind, const float* color, const float* target, int64
                         float* loss, int sm_count, cudaStream_t st);
 cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned long long* bad, int sm_count,
                               cudaStream_t st);
+cudaError_t launch_ssim(const float* a, const float* b, int W, int H, int clamp, double* sum, float* grad,
+                        float grad_scale, float* dcoef, cudaStream_t st);
+cudaError_t launch_psnr_sum(const float* a, const float* b, int64_t n, double* sum, int sm_count, cudaStream_t st);
 cudaError_t launch_adam_update(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                                float omb1, float omb2, float eps, float inv_bias1, float inv_bias2,
                                const unsigned long long* bad, int sm_count, cudaStream_t st);
@@ -111,7 +114,8 @@ struct gb_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
-    DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, counts_tmp, accum, adam_bad;
+    DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, counts_tmp, accum, adam_bad, ssim_tmp,
+        metric_tmp;
     uint32_t* pinned_total = nullptr;
     bool prof = false;
     std::vector<ProfRec> prof_recs;
@@ -281,6 +285,8 @@ gb_status gb_context_destroy(gb_context* ctx) {
     ctx->counts_tmp.release();
     ctx->accum.release();
     ctx->adam_bad.release();
+    ctx->ssim_tmp.release();
+    ctx->metric_tmp.release();
     if (ctx->pinned_total) cudaFreeHost(ctx->pinned_total);
     for (const ProfRec& r : ctx->prof_recs) {
         cudaEventDestroy(r.start);
@@ -616,6 +622,37 @@ gb_status gb_mse_loss(gb_context* ctx, const float* color, const float* target, 
     ProfScope ps(ctx, GB_K_LOSS);
     GB_CUDA(gb::launch_loss(1, color, target, n, scale, grad, loss, ctx->sm_count, ctx->stream));
     ctx->launches += n > 0;
+    return GB_OK;
+}
+
+gb_status gb_ssim(gb_context* ctx, const float* a, const float* b, int32_t width, int32_t height, int32_t clamp01,
+                  double* mean_ssim, float* grad, float grad_scale) {
+    if (!ctx || !a || !b || !mean_ssim) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (width < 11 || height < 11)
+        return fail(GB_INVALID_ARGUMENT, "ssim: image smaller than the 11x11 window");  // metrics.hpp:103-104
+    if (grad && clamp01) return fail(GB_INVALID_ARGUMENT, "ssim: the gradient is taken on unclamped images");
+    if (gb_status st = set_device(ctx)) return st;
+    if (grad) GB_CUDA(ctx->ssim_tmp.ensure(sizeof(float) * 9 * (size_t)(width - 10) * (height - 10)));
+    ProfScope ps(ctx, GB_K_LOSS);
+    GB_CUDA(gb::launch_ssim(a, b, width, height, clamp01, mean_ssim, grad, grad_scale, ctx->ssim_tmp.as<float>(),
+                            ctx->stream));
+    ctx->launches += grad ? 2 : 1;
+    return GB_OK;
+}
+
+gb_status gb_psnr(gb_context* ctx, const float* a, const float* b, int64_t n, double* out) {
+    if (!ctx || !out || (n > 0 && (!a || !b))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(ctx->metric_tmp.ensure(sizeof(double)));
+    GB_CUDA(cudaMemsetAsync(ctx->metric_tmp.p, 0, sizeof(double), ctx->stream));
+    GB_CUDA(gb::launch_psnr_sum(a, b, n, ctx->metric_tmp.as<double>(), ctx->sm_count, ctx->stream));
+    ctx->launches += n > 0;
+    double sum = 0.0;
+    GB_CUDA(cudaMemcpyAsync(&sum, ctx->metric_tmp.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    // metrics.hpp:176-178
+    const double mse = n > 0 ? sum / (double)n : 0.0;
+    *out = mse == 0.0 ? 99.0 : std::fmin(99.0, 10.0 * std::log10(1.0 / mse));
     return GB_OK;
 }
 

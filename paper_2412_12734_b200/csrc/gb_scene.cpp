@@ -8,7 +8,9 @@
 // the GPU consume identical bits.
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <random>
+#include <unordered_set>
 
 #include "../../include/gb_raster.h"
 
@@ -86,6 +88,40 @@ gb_status gb_scene_generate(const gb_scene_spec* spec, float* position, float* d
     Rng tex(spec->seed + 1);
     const int64_t nt = K * (int64_t)spec->n * spec->n * 3;
     for (int64_t i = 0; i < nt; ++i) grid_values[i] = (float)tex.uniform();
+    return GB_OK;
+}
+
+// train.hpp:80-111 initialize(): uniform positions over the image, uniform
+// orientation, distinct depth keys, scales sized so a splat's 3-unit footprint
+// covers about W*H/K pixels (jittered x[0.5,2] per axis), opacity 0.5, a flat
+// base colour with N(0, 0.05) per-texel variation -- the same Rng draws in the
+// same order, rounded to fp32 once.
+gb_status gb_fit_initialize(int32_t width, int32_t height, int64_t count, int32_t n, uint64_t seed, float* position,
+                            float* depth_key, float* theta, float* log_scale, float* opacity_logit,
+                            float* grid_values) {
+    if (width < 1 || height < 1 || count < 1 || n < 1) return GB_INVALID_ARGUMENT;
+    if (!position || !depth_key || !theta || !log_scale || !opacity_logit || !grid_values) return GB_INVALID_ARGUMENT;
+    const double w = width, h = height;
+    if ((double)count > w * h)
+        std::fprintf(stderr, "warning: %lld splats exceed the %d x %d pixel count\n", (long long)count, width, height);
+    Rng rng(seed);
+    const double s_init = std::sqrt(w * h / (M_PI * (double)count)) / 3.0;
+    std::unordered_set<double> used;
+    const int64_t F = 3LL * n * n;
+    for (int64_t k = 0; k < count; ++k) {
+        position[2 * k + 0] = (float)rng.uniform(0.0, w);
+        position[2 * k + 1] = (float)rng.uniform(0.0, h);
+        theta[k] = (float)rng.uniform(0.0, 2.0 * M_PI);
+        double key = rng.uniform();
+        while (!used.insert(key).second) key = rng.uniform();
+        depth_key[k] = (float)key;
+        log_scale[2 * k + 0] = (float)std::log(s_init * rng.uniform(0.5, 2.0));
+        log_scale[2 * k + 1] = (float)std::log(s_init * rng.uniform(0.5, 2.0));
+        opacity_logit[k] = 0.0f;  // logit(0.5)
+        double base[3];
+        for (double& b : base) b = rng.uniform(0.2, 0.8);
+        for (int64_t i = 0; i < F; ++i) grid_values[k * F + i] = (float)(base[i % 3] + rng.normal(0.0, 0.05));
+    }
     return GB_OK;
 }
 

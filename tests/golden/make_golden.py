@@ -11,6 +11,8 @@ Writes (small, committed):
   rng.npz         -- reference Rng uniform()/normal() streams
   kat.json        -- SPEC known-answer examples evaluated by the reference
   ref_k9_n3.gbil  -- a GBIL v1 splat file written by the reference's save_splats
+  fit_cases.npz   -- the reference's fit() (train.hpp:174-219) on small seeded targets (MSE and
+                     MSE + SSIM) and its ssim / ssim_with_gradient / psnr on seeded image pairs
 The fixtures travel to the GPU box; nothing there reads /root/reference.
 """
 import json
@@ -135,6 +137,40 @@ def gbil_file():
     assert msg == "", msg
 
 
+FIT_CASES = [  # (name, W, H, K, n, iterations, mse_ssim, seed)
+    ("mse_n4", 40, 32, 60, 4, 3, False, 11),
+    ("ssim_n2", 36, 30, 50, 2, 3, True, 12),
+    ("mse_n1", 24, 20, 30, 1, 2, False, 13),
+]
+
+
+def fit_cases():
+    out = {}
+    for name, W, H, K, n, iters, ms, seed in FIT_CASES:
+        target = sc.uniform_image(1000 + seed, W, H).astype(np.float64)
+        res = O.ref_fit(target, K, n, iters, mse_ssim=ms, seed=seed, log_every=1)
+        assert not isinstance(res, str), res
+        arrays, hist = res
+        out[f"{name}/target"] = target.astype(np.float32)
+        out[f"{name}/meta"] = np.array([W, H, K, n, iters, int(ms), seed], np.int64)
+        out[f"{name}/history"] = hist
+        for f, v in arrays.items():
+            out[f"{name}/final/{f}"] = v
+    rng = np.random.default_rng(5)
+    for name, (h, w) in (("img_a", (41, 53)), ("img_b", (11, 11))):
+        a = rng.random((h, w, 3)) * 1.2 - 0.1  # exceeds [0,1] so clamping matters
+        b = rng.random((h, w, 3))
+        a32, b32 = a.astype(np.float32).astype(np.float64), b.astype(np.float32).astype(np.float64)
+        v, g = O.ref_ssim(a32, b32, with_grad=True)
+        out[f"{name}/a"] = a32.astype(np.float32)
+        out[f"{name}/b"] = b32.astype(np.float32)
+        out[f"{name}/ssim_clamped"] = np.array(O.ref_ssim(a32, b32))
+        out[f"{name}/ssim_raw"] = np.array(v)
+        out[f"{name}/ssim_grad"] = g
+        out[f"{name}/psnr"] = np.array(O.ref_psnr(a32, b32))
+    np.savez_compressed(os.path.join(HERE, "fit_cases.npz"), **out)
+
+
 if __name__ == "__main__":
     if not O.ref_available():
         O.build()
@@ -143,5 +179,6 @@ if __name__ == "__main__":
     rng_streams()
     kat()
     gbil_file()
+    fit_cases()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
