@@ -40,7 +40,7 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--views-per-gpu", type=int, default=8)
@@ -291,10 +291,10 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (algorithmic bytes, SURVEY §8d with this build's 48 B header) ----
+    # ---- roofline of the dominant kernel (algorithmic bytes) ----
     peak, peak_src = hbm_peak()
     n = cfg3.n
-    Bh, Bt = 48, 12 * n * n
+    Bh, Bt = 40, 12 * n * n  # SURVEY §8(d) algorithmic header and texture bytes
     tiles = ((W + 15) // 16) * ((H + 15) // 16)
     npx = W * H
     model = {

@@ -123,7 +123,7 @@ def _ssim(a, b, clamp, grad=None, grad_scale=0.0, acc=None):
         raise ValueError("ssim: image size mismatch")
     H, W = a.shape[0], a.shape[1]
     acc = torch.zeros((), dtype=torch.float64, device=a.device) if acc is None else acc
-    check(lib.gb_ssim(context(a.device).handle, _ptr(_img(a)), _ptr(_img(b)), W, H, int(clamp), _ptr(acc),
+    check(lib.gb_ssim(context(a.device).handle, _ptr(_img(a)), _ptr(_img(b)), W, H, int(clamp), acc.data_ptr(),
                       _ptr(grad), float(grad_scale)), "ssim")
     return acc
 
