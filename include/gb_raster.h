@@ -223,6 +223,13 @@ GB_API gb_status gb_ssim(gb_context *ctx, const float *a, const float *b, int32_
 /* psnr (metrics.hpp:169-179): both images clamped to [0,1], capped at 99 dB.  Synchronous; *out on the host. */
 GB_API gb_status gb_psnr(gb_context *ctx, const float *a, const float *b, int64_t n, double *out);
 
+/* ---- texture diagnostics (texture.hpp:128-197) ------------------------------ */
+/* Output size of downsample_grid(n, levels) (texture.hpp:132-166), or GB_INVALID_ARGUMENT with its message. */
+GB_API gb_status gb_downsample_size(int32_t n, int32_t levels, int32_t *n_out);
+/* downsample_set's grids (texture.hpp:169-188): count grids of n x n x 3 -> n_out x n_out x 3 (device). */
+GB_API gb_status gb_downsample_grids(gb_context *ctx, const float *grid, int64_t count, int32_t n, int32_t levels,
+                                     float *out);
+
 /* ---- optimiser: adam_step (optim.hpp:96-117) ------------------------------ */
 /* params uses the gb_grads layout (mutable parameter arrays).  Increments
  * state->t.  Non-finite gradients are detected on the device first; if any is

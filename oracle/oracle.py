@@ -124,6 +124,8 @@ def ref_lib():
         L.ref_initialize.argtypes = [i, i, C.c_int64, i, C.c_uint64, P, P, P, P, P, P]
         L.ref_fit.argtypes = [i, i, P, C.c_int64, i, d, C.c_int64, i, d, C.c_uint64, C.c_int64, i, P, P, P, P, P,
                               P, P, C.c_int64, P, C.c_char_p, i]
+        L.ref_downsample_grid.argtypes = [P, i, i, P, P, C.c_char_p, i]
+        L.ref_randomize_colors.argtypes = [C.c_int64, i, C.c_uint64, P]
         L.ref_save_splats.argtypes = [C.c_char_p, C.c_int64, i, d, P, P, P, P, P, P, C.c_char_p, i]
         L.ref_load_splats.argtypes = [C.c_char_p, P, P, P, P, P, P, P, P, P, C.c_char_p, i]
         L.ref_bilinear.argtypes = [d, d, i, d, P, P]
@@ -388,6 +390,25 @@ def ref_load_splats(path: str):
                       *[out[f].ctypes.data for f in ("position", "depth_key", "theta", "log_scale", "opacity_logit",
                                                      "grid")], msg, 512)
     return out, N, sigma.value
+
+
+def ref_downsample_grid(grid, n, levels):
+    """texture.hpp:132-166 -> (out, n_out) or the invalid_argument text."""
+    L = ref_lib()
+    g = np.ascontiguousarray(grid, np.float64)
+    out = np.zeros(3 * n * n)
+    no = C.c_int()
+    msg = C.create_string_buffer(256)
+    if L.ref_downsample_grid(g.ctypes.data, n, levels, out.ctypes.data, C.byref(no), msg, 256):
+        return msg.value.decode()
+    return out[: 3 * no.value * no.value], no.value
+
+
+def ref_randomize_colors(K, n, seed):
+    L = ref_lib()
+    g = np.zeros(K * n * n * 3)
+    L.ref_randomize_colors(K, n, seed, g.ctypes.data)
+    return g
 
 
 def ref_ssim(a, b, with_grad=False):

@@ -242,6 +242,28 @@ int ref_load_splats(const char* path, int64_t* k, int* n, double* sigma, double*
     }
 }
 
+// downsample_grid (texture.hpp:132-166) of one grid; 0 ok (n_out set), 1 with the invalid_argument text.
+int ref_downsample_grid(const double* grid, int n, int levels, double* out, int* n_out, char* msg, int cap) {
+    try {
+        int no = 0;
+        const std::vector<double> g(grid, grid + 3 * n * n);
+        const std::vector<double> r = downsample_grid(g, n, levels, no);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+        *n_out = no;
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(msg, cap, "%s", e.what());
+        return 1;
+    }
+}
+
+// randomize_colors (texture.hpp:192-197): the replacement grid values.
+void ref_randomize_colors(int64_t k, int n, uint64_t seed, double* grid) {
+    SplatSet s(static_cast<std::size_t>(k), ColorGridConfig{n, 0.5});
+    const SplatSet r = randomize_colors(s, seed);
+    std::memcpy(grid, r.grid.data(), sizeof(double) * r.grid.size());
+}
+
 // ssim / ssim_with_gradient / psnr (metrics.hpp:169-191) on W x H x 3 images; grad may be null.
 double ref_ssim(int w, int h, const double* a, const double* b, int with_grad, double* grad) {
     Image ia(w, h), ib(w, h);

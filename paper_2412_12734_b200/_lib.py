@@ -181,6 +181,8 @@ _SIGS = {
     "gb_ssim": (C.c_int, [P, P, P, C.c_int32, C.c_int32, C.c_int32, P, P, C.c_float]),
     "gb_psnr": (C.c_int, [P, P, P, C.c_int64, C.POINTER(C.c_double)]),
     "gb_fit_initialize": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_uint64, P, P, P, P, P, P]),
+    "gb_downsample_size": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),
+    "gb_downsample_grids": (C.c_int, [P, P, C.c_int64, C.c_int32, C.c_int32, P]),
     "gb_splats_file_info": (C.c_int, [C.c_char_p, C.POINTER(SplatFileInfo)]),
     "gb_splats_save": (C.c_int, [P, C.POINTER(Splats), C.c_int32, C.c_char_p]),
     "gb_splats_load": (C.c_int, [P, C.c_char_p, C.c_int64, C.c_int32, C.POINTER(Grads)]),

@@ -40,6 +40,9 @@ cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned lon
 cudaError_t launch_ssim(const float* a, const float* b, int W, int H, int clamp, double* sum, float* grad,
                         float grad_scale, float* dcoef, cudaStream_t st);
 cudaError_t launch_psnr_sum(const float* a, const float* b, int64_t n, double* sum, int sm_count, cudaStream_t st);
+bool downsample_plan(int n, int levels, int& halvings, int& collapse, int& n_out);
+cudaError_t launch_downsample(int64_t K, int n, int halvings, int collapse, const float* src, float* dst,
+                              int sm_count, cudaStream_t st);
 cudaError_t launch_adam_update(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                                float omb1, float omb2, float eps, float inv_bias1, float inv_bias2,
                                const unsigned long long* bad, int sm_count, cudaStream_t st);
@@ -653,6 +656,30 @@ gb_status gb_psnr(gb_context* ctx, const float* a, const float* b, int64_t n, do
     // metrics.hpp:176-178
     const double mse = n > 0 ? sum / (double)n : 0.0;
     *out = mse == 0.0 ? 99.0 : std::fmin(99.0, 10.0 * std::log10(1.0 / mse));
+    return GB_OK;
+}
+
+gb_status gb_downsample_size(int32_t n, int32_t levels, int32_t* n_out) {
+    if (!n_out) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (levels < 0) return fail(GB_INVALID_ARGUMENT, "downsample_grid: negative level count");  // texture.hpp:133
+    if (n < 1) return fail(GB_INVALID_ARGUMENT, "ColorGridConfig: n must be >= 1");
+    int h, c, out;
+    if (!gb::downsample_plan(n, levels, h, c, out))
+        return fail(GB_INVALID_ARGUMENT, "downsample_grid: grid size not divisible by 2^levels");
+    *n_out = out;
+    return GB_OK;
+}
+
+gb_status gb_downsample_grids(gb_context* ctx, const float* grid, int64_t count, int32_t n, int32_t levels,
+                              float* out) {
+    if (!ctx || (count > 0 && (!grid || !out))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    int32_t n_out;
+    if (gb_status st = gb_downsample_size(n, levels, &n_out)) return st;
+    int h, c, o;
+    gb::downsample_plan(n, levels, h, c, o);
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(gb::launch_downsample(count, n, h, c, grid, out, ctx->sm_count, ctx->stream));
+    ctx->launches += count > 0;
     return GB_OK;
 }
 

@@ -313,7 +313,7 @@ __device__ __forceinline__ bool bwd_px(const ScreenHeader& h, const float* __res
     const float alpha = fminf(araw, kMaxAlphaF);
     if (alpha < rc.alpha_skip) return false;  // raster.hpp:332
     const float om = __fsub_rn(1.0f, alpha);
-    s.T = __fdividef(s.T, om);  // raster.hpp:333
+    s.T = __fmul_rn(s.T, rcp_approx(om));  // raster.hpp:333
     const float aT = alpha * s.T;
     const float ch0 = aT * s.g0, ch1 = aT * s.g1, ch2 = aT * s.g2;  // c_hat, raster.hpp:338-340
     float c0, c1, c2, u_hat = 0.0f, v_hat = 0.0f;

@@ -126,9 +126,13 @@ __device__ __forceinline__ bool eval_uv_pinhole(const ScreenHeader& h, int x, in
     return p.cz > 1.17549435e-38f;
 }
 
-// G = exp(-(u^2+v^2)/2)  (raster.hpp:52)
+// G = exp(-(u^2+v^2)/2)  (raster.hpp:52) as one MUFU.EX2 of -(u^2+v^2) log2(e)/2
+// (ftz: G underflows to 0 far outside the splat, where alpha < alpha_skip anyway).
 __device__ __forceinline__ float gauss_weight(float u, float v) {
-    return __expf(__fmul_rn(-0.5f, __fmaf_rn(u, u, __fmul_rn(v, v))));
+    const float x = __fmul_rn(-0.72134752044448170368f, __fmaf_rn(u, u, __fmul_rn(v, v)));
+    float g;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(x));
+    return g;
 }
 
 // uv -> (i, f) on one axis, texture.hpp:27-37, with N fixed at compile time.

@@ -422,8 +422,9 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
 #pragma unroll
             for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
             int tbase = -1;
+            float wk[4] = {1.0f, 0.0f, 0.0f, 0.0f};  // bilinear corner weights (n = 1: texel 0 only)
             if (on) {
-                T = __fdividef(T, __fsub_rn(1.0f, alpha));  // raster.hpp:333
+                T = __fmul_rn(T, rcp_approx(__fsub_rn(1.0f, alpha)));  // raster.hpp:333
                 float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
                 const float aT = alpha * T;
                 const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
@@ -458,6 +459,10 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
                     c1 = cc_[1];
                     c2 = cc_[2];
                     tbase = b.o00;
+                    wk[0] = b.w00;
+                    wk[1] = b.w10;
+                    wk[2] = b.w01;
+                    wk[3] = b.w11;
                 }
                 // texture.hpp:106-109 (strict mask)
                 float u_hat = (N > 1 && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
@@ -524,8 +529,8 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
                     red3(gg, tg[0], tg[1], tg[2]);
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (tg[3 * k] != 0.0f || tg[3 * k + 1] != 0.0f || tg[3 * k + 2] != 0.0f)
+                    for (int k = 0; k < 4; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
+                        if (wk[k] != 0.0f)
                             red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
                 }
             }

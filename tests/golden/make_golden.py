@@ -11,6 +11,8 @@ Writes (small, committed):
   rng.npz         -- reference Rng uniform()/normal() streams
   kat.json        -- SPEC known-answer examples evaluated by the reference
   ref_k9_n3.gbil  -- a GBIL v1 splat file written by the reference's save_splats
+  diag_cases.npz  -- the reference's downsample_grid on seeded grids (n, levels sweep) and its
+                     randomize_colors stream
   fit_cases.npz   -- the reference's fit() (train.hpp:174-219) on small seeded targets (MSE and
                      MSE + SSIM) and its ssim / ssim_with_gradient / psnr on seeded image pairs
 The fixtures travel to the GPU box; nothing there reads /root/reference.
@@ -171,6 +173,23 @@ def fit_cases():
     np.savez_compressed(os.path.join(HERE, "fit_cases.npz"), **out)
 
 
+DIAG_CASES = [(8, 1), (8, 2), (8, 3), (8, 5), (4, 1), (6, 1), (6, 3), (3, 2), (16, 2), (1, 3), (2, 0)]
+
+
+def diag_cases():
+    out = {}
+    rng = np.random.default_rng(9)
+    for n, levels in DIAG_CASES:
+        grids = rng.random((5, 3 * n * n)).astype(np.float32)
+        res = [O.ref_downsample_grid(g.astype(np.float64), n, levels) for g in grids]
+        assert not isinstance(res[0], str), res[0]
+        out[f"n{n}_l{levels}/in"] = grids
+        out[f"n{n}_l{levels}/out"] = np.stack([r[0] for r in res])
+        out[f"n{n}_l{levels}/n_out"] = np.array(res[0][1])
+    out["randomize/K7_n3_seed5"] = O.ref_randomize_colors(7, 3, 5)
+    np.savez_compressed(os.path.join(HERE, "diag_cases.npz"), **out)
+
+
 if __name__ == "__main__":
     if not O.ref_available():
         O.build()
@@ -180,5 +199,6 @@ if __name__ == "__main__":
     kat()
     gbil_file()
     fit_cases()
+    diag_cases()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
