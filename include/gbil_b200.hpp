@@ -2,8 +2,11 @@
 //
 // Mirrors the value types and free functions of the reference's header API
 // (/root/reference/proj/include/gbil: core.hpp:28-178, raster.hpp:21-400,
-// optim.hpp:17-117) name for name, so a caller of gbil::build_binning /
-// render_forward / render_backward / render / adam_step can switch namespace:
+// texture.hpp:128-197, optim.hpp:17-117, metrics.hpp:12-191,
+// serialize.hpp:15-124, train.hpp:22-219) name for name, so a caller of
+// gbil::build_binning / render_forward / render_backward / render /
+// adam_step / psnr / ssim / fit / save_splats / load_splats can switch
+// namespace:
 //
 //     namespace gbil = gbil_b200;      // was: #include "gbil/raster.hpp"
 //
@@ -20,7 +23,10 @@
 // Header-only; link with -lgb_raster (paper_2412_12734_b200/libgb_raster.so).
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdint>
 #include <memory>
@@ -350,6 +356,488 @@ inline GradientBuffer render_backward(const SplatSet& set, const ImagePlaneCamer
 // raster.hpp:389-392
 inline RenderOutput render(const SplatSet& set, const ImagePlaneCamera& camera, const RasterConfig& config = {}) {
     return render_forward(set, camera, build_binning(set, camera, config));
+}
+
+// ---- texture diagnostics (texture.hpp:128-197, raster.hpp:394-400) ------------------------------
+// downsample_grid: one grid (texture.hpp:132-166), box-filtered on the device.
+inline std::vector<double> downsample_grid(std::span<const double> grid, int n, int levels, int& n_out) {
+    int32_t no = 0;
+    detail::check(gb_downsample_size(n, levels, &no), "downsample_grid");
+    auto src = detail::upload(std::vector<double>(grid.begin(), grid.end()));
+    detail::DeviceBuffer dst(static_cast<std::size_t>(3) * no * no * sizeof(float) + 16);
+    detail::check(gb_downsample_grids(detail::context(), src->f(), 1, n, levels, dst.f()), "downsample_grid");
+    n_out = no;
+    return detail::download(dst, static_cast<std::size_t>(3) * no * no);
+}
+
+// texture.hpp:169-188
+inline SplatSet downsample_set(const SplatSet& set, int levels) {
+    int32_t no = 0;
+    detail::check(gb_downsample_size(set.grid_config.n, levels, &no), "downsample_grid");
+    SplatSet out(set.count, ColorGridConfig{no, set.grid_config.sigma});
+    out.position = set.position;
+    out.depth_key = set.depth_key;
+    out.theta = set.theta;
+    out.log_scale = set.log_scale;
+    out.opacity_logit = set.opacity_logit;
+    auto src = detail::upload(set.grid);
+    detail::DeviceBuffer dst(out.grid.size() * sizeof(float) + 16);
+    detail::check(gb_downsample_grids(detail::context(), src->f(), static_cast<int64_t>(set.count), set.grid_config.n,
+                                      levels, dst.f()),
+                  "downsample_set");
+    out.grid = detail::download(dst, out.grid.size());
+    return out;
+}
+
+// texture.hpp:192-197 (the reference's Rng stream, rounded to fp32 like every device value)
+inline SplatSet randomize_colors(const SplatSet& set, std::uint64_t seed) {
+    SplatSet out = set;
+    std::vector<float> g(out.grid.size());
+    detail::check(gb_uniform_fill(seed, static_cast<int64_t>(g.size()), g.data()), "randomize_colors");
+    out.grid.assign(g.begin(), g.end());
+    return out;
+}
+
+// raster.hpp:396-400
+inline RenderOutput render_random_colors(const SplatSet& set, const ImagePlaneCamera& camera, std::uint64_t seed,
+                                         const RasterConfig& config = {}) {
+    return render(randomize_colors(set, seed), camera, config);
+}
+
+// ---- optimiser (optim.hpp:14-117) ----------------------------------------------------------------
+struct LearningRates {
+    double position = 1.6e-4;
+    double theta = 1e-3;
+    double log_scale = 5e-3;
+    double opacity_logit = 5e-2;
+    double color_grid = 2.5e-3;
+    double position_gamma = 1.0;
+    static LearningRates scaled_for_image(int width, int height) {
+        LearningRates lrs;
+        lrs.position *= std::max(width, height);
+        return lrs;
+    }
+    void validate() const {
+        if (!(position > 0.0 && theta > 0.0 && log_scale > 0.0 && opacity_logit > 0.0 && color_grid > 0.0))
+            throw std::invalid_argument("LearningRates: all rates must be positive");
+        if (!(position_gamma > 0.0 && position_gamma <= 1.0))
+            throw std::invalid_argument("LearningRates: position_gamma must be in (0, 1]");
+    }
+    gb_learning_rates to_c() const {
+        return gb_learning_rates{position, theta, log_scale, opacity_logit, color_grid, position_gamma};
+    }
+};
+
+struct AdamConfig {
+    double beta1 = 0.9;
+    double beta2 = 0.999;
+    double epsilon = 1e-8;
+};
+
+struct AdamState {
+    std::int64_t t = 0;
+    AdamConfig config;
+    std::vector<double> m_position, v_position, m_theta, v_theta, m_log_scale, v_log_scale, m_opacity, v_opacity,
+        m_grid, v_grid;
+    AdamState() = default;
+    explicit AdamState(const SplatSet& like, const AdamConfig& cfg = {}) : config(cfg) {
+        for (auto* p : {&m_position, &v_position}) p->assign(like.position.size(), 0.0);
+        for (auto* p : {&m_theta, &v_theta}) p->assign(like.theta.size(), 0.0);
+        for (auto* p : {&m_log_scale, &v_log_scale}) p->assign(like.log_scale.size(), 0.0);
+        for (auto* p : {&m_opacity, &v_opacity}) p->assign(like.opacity_logit.size(), 0.0);
+        for (auto* p : {&m_grid, &v_grid}) p->assign(like.grid.size(), 0.0);
+    }
+};
+
+struct NonFiniteGradient : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+
+// fp32 device copies of one SoA group set (params, gradients or a moment) for gb_adam_step
+struct DeviceGroups {
+    std::shared_ptr<DeviceBuffer> position, theta, log_scale, opacity, grid;
+    gb_grads view{};
+    DeviceGroups(const std::vector<double>& pos, const std::vector<double>& th, const std::vector<double>& ls,
+                 const std::vector<double>& op, const std::vector<double>& gr) {
+        position = upload(pos);
+        theta = upload(th);
+        log_scale = upload(ls);
+        opacity = upload(op);
+        grid = upload(gr);
+        view = gb_grads{position->f(), nullptr, theta->f(), nullptr, log_scale->f(), opacity->f(), grid->f()};
+    }
+    void store(std::vector<double>& pos, std::vector<double>& th, std::vector<double>& ls, std::vector<double>& op,
+               std::vector<double>& gr) const {
+        pos = download(*position, pos.size());
+        th = download(*theta, th.size());
+        ls = download(*log_scale, ls.size());
+        op = download(*opacity, op.size());
+        gr = download(*grid, gr.size());
+    }
+};
+
+}  // namespace detail
+
+// optim.hpp:96-117 on the device.  A non-finite gradient throws (optim.hpp:81-83) and updates nothing.
+inline void adam_step(SplatSet& params, const GradientBuffer& grads, AdamState& state, const LearningRates& lrs) {
+    if (grads.count != params.count || grads.grid.size() != params.grid.size())
+        throw std::invalid_argument("adam_step: gradient shape mismatch");
+    lrs.validate();
+    detail::DeviceGroups p(params.position, params.theta, params.log_scale, params.opacity_logit, params.grid);
+    detail::DeviceGroups g(grads.position, grads.theta, grads.log_scale, grads.opacity_logit, grads.grid);
+    detail::DeviceGroups m(state.m_position, state.m_theta, state.m_log_scale, state.m_opacity, state.m_grid);
+    detail::DeviceGroups v(state.v_position, state.v_theta, state.v_log_scale, state.v_opacity, state.v_grid);
+    gb_adam_state st{state.t, state.config.beta1, state.config.beta2, state.config.epsilon, m.view, v.view};
+    const gb_learning_rates l = lrs.to_c();
+    detail::check(gb_adam_step(detail::context(), GB_MODE_ORTHO, static_cast<int64_t>(params.count),
+                               params.grid_config.n, &p.view, &g.view, &st, &l),
+                  "adam_step");
+    int32_t grp = 0;
+    int64_t idx = 0;
+    if (gb_adam_check(detail::context(), &grp, &idx) != GB_OK)
+        throw NonFiniteGradient(gb_last_error_string());
+    state.t = st.t;
+    p.store(params.position, params.theta, params.log_scale, params.opacity_logit, params.grid);
+    m.store(state.m_position, state.m_theta, state.m_log_scale, state.m_opacity, state.m_grid);
+    v.store(state.v_position, state.v_theta, state.v_log_scale, state.v_opacity, state.v_grid);
+}
+
+// ---- images and metrics (image.hpp:18-39, metrics.hpp:12-191) -------------------------------------
+struct Image {
+    int width = 0;
+    int height = 0;
+    std::vector<double> data;  // W*H*3, channels innermost
+    Image() = default;
+    Image(int w, int h, double fill = 0.0) : width(w), height(h), data(static_cast<std::size_t>(w) * h * 3, fill) {}
+    double& at(int x, int y, int c) { return data[(static_cast<std::size_t>(y) * width + x) * 3 + c]; }
+    double at(int x, int y, int c) const { return data[(static_cast<std::size_t>(y) * width + x) * 3 + c]; }
+};
+
+inline Image image_from_render(const RenderOutput& out) {
+    Image img(out.width, out.height);
+    img.data = out.color;
+    return img;
+}
+
+inline constexpr double kPsnrCap = 99.0;
+
+namespace detail {
+inline void check_same_size(const Image& a, const Image& b, const char* what) {
+    if (a.width != b.width || a.height != b.height)
+        throw std::invalid_argument(std::string(what) + ": image size mismatch");
+}
+
+struct SsimResult {
+    double value = 0.0;
+    Image grad_a;
+};
+
+inline SsimResult ssim_device(const Image& a, const Image& b, bool clamp, bool want_grad) {
+    check_same_size(a, b, "ssim");
+    if (a.width < 11 || a.height < 11) throw std::invalid_argument("ssim: image smaller than the 11x11 window");
+    auto da = upload(a.data), db = upload(b.data);
+    DeviceBuffer acc(sizeof(double));
+    check(gb_memset_device(context(), acc.ptr, 0, sizeof(double)), "ssim");
+    std::unique_ptr<DeviceBuffer> grad;
+    if (want_grad) {
+        grad = std::make_unique<DeviceBuffer>(a.data.size() * sizeof(float) + 16);
+        check(gb_memset_device(context(), grad->ptr, 0, grad->bytes), "ssim");
+    }
+    check(gb_ssim(context(), da->f(), db->f(), a.width, a.height, clamp ? 1 : 0, static_cast<double*>(acc.ptr),
+                  want_grad ? grad->f() : nullptr, 1.0f),
+          "ssim");
+    SsimResult r;
+    check(gb_copy_d2h(context(), &r.value, acc.ptr, sizeof(double), 1), "ssim");
+    if (want_grad) {
+        r.grad_a = Image(a.width, a.height);
+        r.grad_a.data = download(*grad, a.data.size());
+    }
+    return r;
+}
+}  // namespace detail
+
+// metrics.hpp:169-179
+inline double psnr(const Image& a, const Image& b) {
+    detail::check_same_size(a, b, "psnr");
+    auto da = detail::upload(a.data), db = detail::upload(b.data);
+    double v = 0.0;
+    detail::check(gb_psnr(detail::context(), da->f(), db->f(), static_cast<int64_t>(a.data.size()), &v), "psnr");
+    return v;
+}
+
+// metrics.hpp:183-185
+inline double ssim(const Image& a, const Image& b) { return detail::ssim_device(a, b, true, false).value; }
+
+// metrics.hpp:189-191
+inline detail::SsimResult ssim_with_gradient(const Image& a, const Image& b) {
+    return detail::ssim_device(a, b, false, true);
+}
+
+// ---- splat files (serialize.hpp:15-124) ----------------------------------------------------------
+struct SplatIoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void save_splats(const std::string& path, const SplatSet& set) {
+    detail::DeviceSplats d(set);
+    if (gb_splats_save(detail::context(), &d.view, GB_MODE_ORTHO, path.c_str()) != GB_OK)
+        throw SplatIoError(gb_last_error_string());
+}
+
+inline SplatSet load_splats(const std::string& path) {
+    gb_splat_file_info info{};
+    if (gb_splats_file_info(path.c_str(), &info) != GB_OK) throw SplatIoError(gb_last_error_string());
+    if (info.mode != GB_MODE_ORTHO) throw SplatIoError("unsupported splat file version " + std::to_string(info.version));
+    SplatSet set(static_cast<std::size_t>(info.count), ColorGridConfig{info.n, static_cast<double>(info.sigma)});
+    const std::size_t K = set.count;
+    detail::DeviceBuffer pos(2 * K * 4 + 16), dk(K * 4 + 16), th(K * 4 + 16), ls(2 * K * 4 + 16), op(K * 4 + 16),
+        gr(set.grid.size() * 4 + 16);
+    gb_grads g{pos.f(), dk.f(), th.f(), nullptr, ls.f(), op.f(), gr.f()};
+    if (gb_splats_load(detail::context(), path.c_str(), info.count, info.n, &g) != GB_OK)
+        throw SplatIoError(gb_last_error_string());
+    set.position = detail::download(pos, 2 * K);
+    set.depth_key = detail::download(dk, K);
+    set.theta = detail::download(th, K);
+    set.log_scale = detail::download(ls, 2 * K);
+    set.opacity_logit = detail::download(op, K);
+    set.grid = detail::download(gr, set.grid.size());
+    return set;
+}
+
+// ---- the image-fitting loop (train.hpp:22-219) -----------------------------------------------------
+enum class LossKind { mse, mse_plus_ssim };
+
+struct TrainConfig {
+    std::size_t splat_count = 1000;
+    std::int64_t iterations = 20000;
+    LossKind loss = LossKind::mse;
+    double ssim_weight = 0.2;
+    std::uint64_t seed = 0;
+    ColorGridConfig grid{4, 0.5};
+    LearningRates lrs;
+    bool position_lr_absolute = false;
+    AdamConfig adam;
+    RasterConfig raster;
+    std::array<double, 3> background = {0.0, 0.0, 0.0};
+    std::int64_t log_every = 100;
+    std::int64_t checkpoint_every = 0;
+    std::string checkpoint_dir;
+    bool allow_any_n = false;
+    void validate() const {
+        if (splat_count < 1) throw std::invalid_argument("TrainConfig: splat_count must be >= 1");
+        if (iterations < 1) throw std::invalid_argument("TrainConfig: iterations must be >= 1");
+        grid.validate();
+        if (!allow_any_n && grid.n != 1 && grid.n != 2 && grid.n != 4 && grid.n != 8)
+            throw std::invalid_argument(
+                "TrainConfig: texture resolution must be one of 1, 2, 4, 8 (use the force flag for other values)");
+        lrs.validate();
+        raster.validate();
+        if (log_every < 1) throw std::invalid_argument("TrainConfig: log_every must be >= 1");
+        if (checkpoint_every < 0) throw std::invalid_argument("TrainConfig: negative checkpoint cadence");
+    }
+};
+
+struct FitError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct MetricRecord {
+    std::int64_t iter = 0;
+    double loss = 0.0;
+    double psnr = 0.0;
+    double ssim = 0.0;
+    double wall_ms = 0.0;
+};
+
+struct FitResult {
+    SplatSet splats;
+    std::vector<MetricRecord> history;
+};
+
+// train.hpp:80-111: the reference's Rng draws, rounded to fp32 (host).
+inline SplatSet initialize(const Image& target, const TrainConfig& cfg) {
+    cfg.validate();
+    if (target.width < 1 || target.height < 1) throw std::invalid_argument("initialize: empty target image");
+    const std::size_t K = cfg.splat_count, F = static_cast<std::size_t>(cfg.grid.texels_per_splat());
+    std::vector<float> pos(2 * K), dk(K), th(K), ls(2 * K), op(K), gr(K * F);
+    detail::check(gb_fit_initialize(target.width, target.height, static_cast<int64_t>(K), cfg.grid.n, cfg.seed,
+                                    pos.data(), dk.data(), th.data(), ls.data(), op.data(), gr.data()),
+                  "initialize");
+    SplatSet set(K, cfg.grid);
+    set.position.assign(pos.begin(), pos.end());
+    set.depth_key.assign(dk.begin(), dk.end());
+    set.theta.assign(th.begin(), th.end());
+    set.log_scale.assign(ls.begin(), ls.end());
+    set.opacity_logit.assign(op.begin(), op.end());
+    set.grid.assign(gr.begin(), gr.end());
+    return set;
+}
+
+struct LossResult {
+    double value = 0.0;
+    Image grad;  // d loss / d rendered
+};
+
+// train.hpp:120-133
+inline LossResult mse_loss(const Image& rendered, const Image& target) {
+    detail::check_same_size(rendered, target, "mse_loss");
+    auto dr = detail::upload(rendered.data), dt = detail::upload(target.data);
+    detail::DeviceBuffer grad(rendered.data.size() * sizeof(float) + 16), loss(sizeof(float));
+    detail::check(gb_memset_device(detail::context(), loss.ptr, 0, sizeof(float)), "mse_loss");
+    const int64_t n = static_cast<int64_t>(rendered.data.size());
+    detail::check(gb_mse_loss(detail::context(), dr->f(), dt->f(), n, static_cast<float>(1.0 / n), grad.f(), loss.f()),
+                  "mse_loss");
+    float v = 0.0f;
+    detail::check(gb_copy_d2h(detail::context(), &v, loss.ptr, sizeof(float), 1), "mse_loss");
+    LossResult r;
+    r.value = v;
+    r.grad = Image(rendered.width, rendered.height);
+    r.grad.data = detail::download(grad, rendered.data.size());
+    return r;
+}
+
+// train.hpp:135-145
+inline LossResult photometric_loss(const Image& rendered, const Image& target, const TrainConfig& cfg) {
+    LossResult res = mse_loss(rendered, target);
+    if (cfg.loss == LossKind::mse_plus_ssim) {
+        const auto s = ssim_with_gradient(rendered, target);
+        res.value += cfg.ssim_weight * (1.0 - s.value);
+        for (std::size_t i = 0; i < res.grad.data.size(); ++i) res.grad.data[i] -= cfg.ssim_weight * s.grad_a.data[i];
+    }
+    return res;
+}
+
+namespace detail {
+// train.hpp:149-165
+inline void write_checkpoint(const std::string& dir, std::int64_t iter, const SplatSet& set,
+                             const std::vector<MetricRecord>& history) {
+    char name[64];
+    std::snprintf(name, sizeof(name), "/checkpoint_%06lld", static_cast<long long>(iter));
+    const std::string base = dir + name;
+    try {
+        save_splats(base + ".gbil", set);
+        std::FILE* f = std::fopen((base + ".history.csv").c_str(), "w");
+        if (!f) throw SplatIoError("cannot open " + base + ".history.csv");
+        std::fprintf(f, "iter,loss,psnr\n");
+        for (const auto& r : history)
+            std::fprintf(f, "%lld,%.17g,%.17g\n", static_cast<long long>(r.iter), r.loss, r.psnr);
+        std::fclose(f);
+    } catch (const std::exception& e) {
+        throw FitError(std::string("checkpoint write failed: ") + e.what());
+    }
+}
+}  // namespace detail
+
+// train.hpp:174-219 with the whole iteration on the device: parameters, Adam moments, the target and every
+// intermediate stay resident; per iteration only the loss scalar (the reference's non-finite check) and, on
+// logged iterations, PSNR/SSIM come back to the host.
+inline FitResult fit(const Image& target, const TrainConfig& cfg) {
+    cfg.validate();
+    if (cfg.loss == LossKind::mse_plus_ssim && (target.width < 11 || target.height < 11))
+        throw std::invalid_argument("fit: mse_plus_ssim needs images of at least 11x11");
+    ImagePlaneCamera camera{target.width, target.height, cfg.background};
+    camera.validate();
+    LearningRates lrs = cfg.lrs;
+    if (!cfg.position_lr_absolute) lrs.position *= std::max(target.width, target.height);
+
+    FitResult result;
+    result.splats = initialize(target, cfg);
+    SplatSet& set = result.splats;
+    gb_context* ctx = detail::context();
+    detail::DeviceSplats p(set);  // device parameters (fp32), updated in place by Adam
+    const std::size_t K = set.count, F = static_cast<std::size_t>(set.grid_config.texels_per_splat());
+    const std::size_t npx = static_cast<std::size_t>(target.width) * target.height;
+    const std::vector<double> zero2(2 * K, 0.0), zero1(K, 0.0), zerog(K * F, 0.0);
+    detail::DeviceGroups g(zero2, zero1, zero2, zero1, zerog), m(zero2, zero1, zero2, zero1, zerog),
+        v(zero2, zero1, zero2, zero1, zerog);
+    gb_grads params{const_cast<float*>(p.view.position), const_cast<float*>(p.view.depth_key),
+                    const_cast<float*>(p.view.theta), nullptr, const_cast<float*>(p.view.log_scale),
+                    const_cast<float*>(p.view.opacity_logit), const_cast<float*>(p.view.grid_values)};
+    gb_adam_state st{0, cfg.adam.beta1, cfg.adam.beta2, cfg.adam.epsilon, m.view, v.view};
+    const gb_learning_rates l = lrs.to_c();
+    auto tgt = detail::upload(target.data);
+    detail::DeviceBuffer color(npx * 3 * 4 + 16), trans(npx * 4 + 16), last(npx * 4 + 16), dimg(npx * 3 * 4 + 16),
+        loss(16), ssim_acc(16);
+    gb_render_out out{target.width, target.height, color.f(), trans.f(), static_cast<int32_t*>(last.ptr), 0, 0, 0};
+    detail::BinningHandle bin;
+    const gb_camera cam = detail::to_c(camera);
+    const gb_raster_config rc = detail::to_c(cfg.raster);
+    const auto start = std::chrono::steady_clock::now();
+    for (std::int64_t iter = 1; iter <= cfg.iterations; ++iter) {
+        detail::check(gb_build_binning(ctx, &p.view, &cam, &rc, bin.b), "fit");
+        detail::check(gb_render_forward(ctx, &p.view, &cam, bin.b, &out), "fit");
+        detail::check(gb_memset_device(ctx, loss.ptr, 0, 16), "fit");
+        detail::check(gb_mse_loss(ctx, color.f(), tgt->f(), static_cast<int64_t>(npx * 3),
+                                  static_cast<float>(1.0 / (npx * 3)), dimg.f(), loss.f()),
+                      "fit");
+        double value = 0.0;
+        if (cfg.loss == LossKind::mse_plus_ssim) {
+            detail::check(gb_memset_device(ctx, ssim_acc.ptr, 0, 16), "fit");
+            detail::check(gb_ssim(ctx, color.f(), tgt->f(), target.width, target.height, 0,
+                                  static_cast<double*>(ssim_acc.ptr), dimg.f(), static_cast<float>(-cfg.ssim_weight)),
+                          "fit");
+            double s = 0.0;
+            detail::check(gb_copy_d2h(ctx, &s, ssim_acc.ptr, sizeof(double), 0), "fit");
+            float mse = 0.0f;
+            detail::check(gb_copy_d2h(ctx, &mse, loss.ptr, sizeof(float), 1), "fit");
+            value = mse + cfg.ssim_weight * (1.0 - s);
+        } else {
+            float mse = 0.0f;
+            detail::check(gb_copy_d2h(ctx, &mse, loss.ptr, sizeof(float), 1), "fit");
+            value = mse;
+        }
+        if (!std::isfinite(value))
+            throw FitError("fit: non-finite loss at iteration " + std::to_string(iter) + "; last checkpoint retained");
+        detail::check(gb_memset_device(ctx, g.position->ptr, 0, g.position->bytes), "fit");
+        detail::check(gb_memset_device(ctx, g.theta->ptr, 0, g.theta->bytes), "fit");
+        detail::check(gb_memset_device(ctx, g.log_scale->ptr, 0, g.log_scale->bytes), "fit");
+        detail::check(gb_memset_device(ctx, g.opacity->ptr, 0, g.opacity->bytes), "fit");
+        detail::check(gb_memset_device(ctx, g.grid->ptr, 0, g.grid->bytes), "fit");
+        detail::check(gb_render_backward(ctx, &p.view, &cam, bin.b, &out, dimg.f(), &g.view), "fit");
+        detail::check(gb_adam_step(ctx, GB_MODE_ORTHO, static_cast<int64_t>(K), set.grid_config.n, &params, &g.view,
+                                   &st, &l),
+                      "fit");
+        int32_t grp = 0;
+        int64_t idx = 0;
+        if (gb_adam_check(ctx, &grp, &idx) != GB_OK) throw NonFiniteGradient(gb_last_error_string());
+        const bool log = iter == 1 || iter == cfg.iterations || iter % cfg.log_every == 0;
+        const bool ckpt = cfg.checkpoint_every > 0 && !cfg.checkpoint_dir.empty() &&
+                          (iter % cfg.checkpoint_every == 0 || iter == cfg.iterations);
+        if (log) {
+            MetricRecord rec;
+            rec.iter = iter;
+            rec.loss = value;
+            detail::check(gb_psnr(ctx, color.f(), tgt->f(), static_cast<int64_t>(npx * 3), &rec.psnr), "fit");
+            if (target.width >= 11 && target.height >= 11) {
+                detail::check(gb_memset_device(ctx, ssim_acc.ptr, 0, 16), "fit");
+                detail::check(gb_ssim(ctx, color.f(), tgt->f(), target.width, target.height, 1,
+                                      static_cast<double*>(ssim_acc.ptr), nullptr, 0.0f),
+                              "fit");
+                detail::check(gb_copy_d2h(ctx, &rec.ssim, ssim_acc.ptr, sizeof(double), 1), "fit");
+            } else {
+                rec.ssim = std::nan("");
+            }
+            rec.wall_ms =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+            result.history.push_back(rec);
+        }
+        if (ckpt) {
+            set.position = detail::download(*p.position, 2 * K);
+            set.theta = detail::download(*p.theta, K);
+            set.log_scale = detail::download(*p.log_scale, 2 * K);
+            set.opacity_logit = detail::download(*p.opacity, K);
+            set.grid = detail::download(*p.grid, K * F);
+            detail::write_checkpoint(cfg.checkpoint_dir, iter, set, result.history);
+        }
+    }
+    set.position = detail::download(*p.position, 2 * K);
+    set.theta = detail::download(*p.theta, K);
+    set.log_scale = detail::download(*p.log_scale, 2 * K);
+    set.opacity_logit = detail::download(*p.opacity, K);
+    set.grid = detail::download(*p.grid, K * F);
+    return result;
 }
 
 }  // namespace gbil_b200

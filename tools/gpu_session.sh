@@ -30,6 +30,9 @@ done
 if [ "${DBG:-0}" = 1 ]; then
   GB_COMPOSITOR=direct timeout 600 python tools/dbg_run.py > $O/dbg_counters.txt 2>&1
 fi
+if [ "${SWEEP:-0}" = 1 ]; then
+  timeout 1200 python tools/sweep.py --out $O/sweep > $O/sweep.log 2>&1
+fi
 if [ "${REF:-0}" = 1 ]; then
   timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref.json 2> $O/bench_ref.err
   timeout 900 python bench.py > $O/bench_full.json 2> $O/bench_full.err
