@@ -87,6 +87,15 @@ def main():
             act &= np.arange(wl + 1)[:, None] <= lst[None, :]
             tot_active_lanes += act.sum()
             lx, ly = xs - x0, ys - y0
+            # per-lane batches: within each batch of B consecutive warp-active entries, every lane walks its own
+            # active entries; the warp needs max over lanes of the count
+            wact = act[act.any(1)]  # warp-active entries, in order
+            for B in (4, 8, 16):
+                key = f"lane batches B={B}"
+                n = wact.shape[0]
+                pad = (-n) % B
+                wb = np.concatenate([wact, np.zeros((pad, wact.shape[1]), bool)]).reshape(-1, B, wact.shape[1])
+                tot[key] = tot.get(key, 0) + wb.sum(1).max(1).sum()
             for name, G in lay.items():
                 if G == 32:
                     gid = np.zeros_like(lx)
