@@ -387,153 +387,153 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
     constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
     const int F = 3 * N * N;
     const float sigma = rc.sigma;
-            bool on = rank <= last;
-            float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
-            PinholeTerms pt;
-            if (on) {
-                bool hit;
-                if (MODE == GB_MODE_ORTHO) {
-                    hit = eval_uv_ortho(h, x, y, u, v);
-                } else {
-                    hit = eval_uv_pinhole(h, x, y, u, v, pt);
-                }
-                if (hit) {
-                    G = gauss_weight(u, v);
-                    araw = __fmul_rn(h.h1.z, G);
-                    alpha = fminf(araw, kMaxAlphaF);
-                    on = !(alpha < rc.alpha_skip);
-                } else {
-                    on = false;
-                }
-            }
-            const unsigned act = __ballot_sync(kFull, on);
-            if (act == 0) return;
-            if (lane == 0) {
-                GB_DBG(2, 1);
-                GB_DBG(3, __popc(act));
-                GB_DBG(6, (act & 0x0F0F0F0Fu) && (act & 0xF0F0F0F0u));  // both 4x4 halves active
-                GB_DBG(7, (act & 0x0000FFFFu) && (act & 0xFFFF0000u));  // both 8x2 halves active
-            }
+    bool on = rank <= last;
+    float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
+    PinholeTerms pt;
+    if (on) {
+        bool hit;
+        if (MODE == GB_MODE_ORTHO) {
+            hit = eval_uv_ortho(h, x, y, u, v);
+        } else {
+            hit = eval_uv_pinhole(h, x, y, u, v, pt);
+        }
+        if (hit) {
+            G = gauss_weight(u, v);
+            araw = __fmul_rn(h.h1.z, G);
+            alpha = fminf(araw, kMaxAlphaF);
+            on = !(alpha < rc.alpha_skip);
+        } else {
+            on = false;
+        }
+    }
+    const unsigned act = __ballot_sync(kFull, on);
+    if (act == 0) return;
+    if (lane == 0) {
+        GB_DBG(2, 1);
+        GB_DBG(3, __popc(act));
+        GB_DBG(6, (act & 0x0F0F0F0Fu) && (act & 0xF0F0F0F0u));  // both 4x4 halves active
+        GB_DBG(7, (act & 0x0000FFFFu) && (act & 0xFFFF0000u));  // both 8x2 halves active
+    }
 
-            float red[16];  // screen-space sums (NS of 16 slots)
+    float red[16];  // screen-space sums (NS of 16 slots)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) red[i] = 0.0f;
-            float tg[12];
+    for (int i = 0; i < 16; ++i) red[i] = 0.0f;
+    float tg[12];
 #pragma unroll
-            for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
-            int tbase = -1;
-            float wk[4] = {1.0f, 0.0f, 0.0f, 0.0f};  // bilinear corner weights (n = 1: texel 0 only)
-            if (on) {
-                T = __fmul_rn(T, rcp_approx(__fsub_rn(1.0f, alpha)));  // raster.hpp:333
-                float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
-                const float aT = alpha * T;
-                const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
-                if (N == 1) {
-                    c0 = t[0];
-                    c1 = t[1];
-                    c2 = t[2];
-                    tg[0] = ch0;
-                    tg[1] = ch1;
-                    tg[2] = ch2;
-                    tbase = 0;
-                } else {
-                    Bilin b;
-                    bilin_setup(u, v, N, rc, b);
-                    const float* p00 = t + b.o00;
-                    const float* p10 = p00 + 3 * N;
-                    const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
-                    float cc_[3];
-                    const float chat[3] = {ch0, ch1, ch2};
+    for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
+    int tbase = -1;
+    float wk[4] = {1.0f, 0.0f, 0.0f, 0.0f};  // bilinear corner weights (n = 1: texel 0 only)
+    if (on) {
+        T = __fmul_rn(T, rcp_approx(__fsub_rn(1.0f, alpha)));  // raster.hpp:333
+        float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
+        const float aT = alpha * T;
+        const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
+        if (N == 1) {
+            c0 = t[0];
+            c1 = t[1];
+            c2 = t[2];
+            tg[0] = ch0;
+            tg[1] = ch1;
+            tg[2] = ch2;
+            tbase = 0;
+        } else {
+            Bilin b;
+            bilin_setup(u, v, N, rc, b);
+            const float* p00 = t + b.o00;
+            const float* p10 = p00 + 3 * N;
+            const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
+            float cc_[3];
+            const float chat[3] = {ch0, ch1, ch2};
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
-                        cc_[c] = c00 * b.w00 + c10 * b.w10 + c01 * b.w01 + c11 * b.w11;
-                        tg[c] = chat[c] * b.w00;
-                        tg[3 + c] = chat[c] * b.w10;
-                        tg[6 + c] = chat[c] * b.w01;
-                        tg[9 + c] = chat[c] * b.w11;
-                        fu_hat = fmaf(chat[c], (c10 - c00) * gv + (c11 - c01) * b.fv, fu_hat);
-                        fv_hat = fmaf(chat[c], (c01 - c00) * gu + (c11 - c10) * b.fu, fv_hat);
-                    }
-                    c0 = cc_[0];
-                    c1 = cc_[1];
-                    c2 = cc_[2];
-                    tbase = b.o00;
-                    wk[0] = b.w00;
-                    wk[1] = b.w10;
-                    wk[2] = b.w01;
-                    wk[3] = b.w11;
-                }
-                // texture.hpp:106-109 (strict mask)
-                float u_hat = (N > 1 && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
-                float v_hat = (N > 1 && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
-                // raster.hpp:344-346
-                const float gT0 = g0 * T, gT1 = g1 * T, gT2 = g2 * T;
-                const float alpha_hat = gT0 * (c0 - bh0) + gT1 * (c1 - bh1) + gT2 * (c2 - bh2);
-                float op = 0.0f;
-                if (araw < kMaxAlphaF) {  // raster.hpp:350-354
-                    op = alpha_hat * G;
-                    const float aa = alpha_hat * alpha;
-                    u_hat -= aa * u;
-                    v_hat -= aa * v;
-                }
-                if (MODE == GB_MODE_ORTHO) {
-                    red[0] = u_hat;
-                    red[1] = v_hat;
-                    red[2] = u_hat * v;
-                    red[3] = v_hat * u;
-                    red[4] = u_hat * u;
-                    red[5] = v_hat * v;
-                    red[6] = op;
-                } else {
-                    // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
-                    const float iz = pt.iz;
-                    const float gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
-                    red[0] = gc0;
-                    red[1] = gc1;
-                    red[2] = gc2;
-                    red[3] = pt.dx * gc0;
-                    red[4] = pt.dx * gc1;
-                    red[5] = pt.dx * gc2;
-                    red[6] = pt.dy * gc0;
-                    red[7] = pt.dy * gc1;
-                    red[8] = pt.dy * gc2;
-                    red[9] = op;
-                }
-                // raster.hpp:362
-                const float om = 1.0f - alpha;
-                bh0 = alpha * c0 + om * bh0;
-                bh1 = alpha * c1 + om * bh1;
-                bh2 = alpha * c2 + om * bh2;
+            for (int c = 0; c < 3; ++c) {
+                const float c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
+                cc_[c] = c00 * b.w00 + c10 * b.w10 + c01 * b.w01 + c11 * b.w11;
+                tg[c] = chat[c] * b.w00;
+                tg[3 + c] = chat[c] * b.w10;
+                tg[6 + c] = chat[c] * b.w01;
+                tg[9 + c] = chat[c] * b.w11;
+                fu_hat = fmaf(chat[c], (c10 - c00) * gv + (c11 - c01) * b.fv, fu_hat);
+                fv_hat = fmaf(chat[c], (c01 - c00) * gu + (c11 - c10) * b.fu, fv_hat);
             }
-            {  // screen-space sums: lane l owns value l >> 1
-                float sv[NS];
+            c0 = cc_[0];
+            c1 = cc_[1];
+            c2 = cc_[2];
+            tbase = b.o00;
+            wk[0] = b.w00;
+            wk[1] = b.w10;
+            wk[2] = b.w01;
+            wk[3] = b.w11;
+        }
+        // texture.hpp:106-109 (strict mask)
+        float u_hat = (N > 1 && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
+        float v_hat = (N > 1 && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
+        // raster.hpp:344-346
+        const float gT0 = g0 * T, gT1 = g1 * T, gT2 = g2 * T;
+        const float alpha_hat = gT0 * (c0 - bh0) + gT1 * (c1 - bh1) + gT2 * (c2 - bh2);
+        float op = 0.0f;
+        if (araw < kMaxAlphaF) {  // raster.hpp:350-354
+            op = alpha_hat * G;
+            const float aa = alpha_hat * alpha;
+            u_hat -= aa * u;
+            v_hat -= aa * v;
+        }
+        if (MODE == GB_MODE_ORTHO) {
+            red[0] = u_hat;
+            red[1] = v_hat;
+            red[2] = u_hat * v;
+            red[3] = v_hat * u;
+            red[4] = u_hat * u;
+            red[5] = v_hat * v;
+            red[6] = op;
+        } else {
+            // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
+            const float iz = pt.iz;
+            const float gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
+            red[0] = gc0;
+            red[1] = gc1;
+            red[2] = gc2;
+            red[3] = pt.dx * gc0;
+            red[4] = pt.dx * gc1;
+            red[5] = pt.dx * gc2;
+            red[6] = pt.dy * gc0;
+            red[7] = pt.dy * gc1;
+            red[8] = pt.dy * gc2;
+            red[9] = op;
+        }
+        // raster.hpp:362
+        const float om = 1.0f - alpha;
+        bh0 = alpha * c0 + om * bh0;
+        bh1 = alpha * c1 + om * bh1;
+        bh2 = alpha * c2 + om * bh2;
+    }
+    {  // screen-space sums: lane l owns value l >> 1
+        float sv[NS];
 #pragma unroll
-                for (int i = 0; i < NS; ++i) sv[i] = red[i];
-                const float r2 = smem_reduce<NS>(sv, wscratch, lane);
-                if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
-            }
-            // texel gradients: one warp reduction when every active lane shares a bilinear cell;
-            // otherwise each lane adds its (at most four) non-zero texels straight to HBM with
-            // one float2 + one float red per texel -- cheaper than a reduction per distinct cell
-            float* gg = grid_grad + (size_t)id * F;
-            const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
-            if (__all_sync(kFull, !on || tbase == b0)) {
-                if (lane == 0) GB_DBG(4, 1);
-                const float r2 = smem_reduce<12>(tg, wscratch, lane);
-                if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
-                    red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
-            } else if (on) {
-                if (lane == 0) GB_DBG(5, 1);
-                if (N == 1) {
-                    red3(gg, tg[0], tg[1], tg[2]);
-                } else {
+        for (int i = 0; i < NS; ++i) sv[i] = red[i];
+        const float r2 = smem_reduce<NS>(sv, wscratch, lane);
+        if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
+    }
+    // texel gradients: one warp reduction when every active lane shares a bilinear cell;
+    // otherwise each lane adds its (at most four) non-zero texels straight to HBM with
+    // one float2 + one float red per texel -- cheaper than a reduction per distinct cell
+    float* gg = grid_grad + (size_t)id * F;
+    const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
+    if (__all_sync(kFull, !on || tbase == b0)) {
+        if (lane == 0) GB_DBG(4, 1);
+        const float r2 = smem_reduce<12>(tg, wscratch, lane);
+        if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
+            red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
+    } else if (on) {
+        if (lane == 0) GB_DBG(5, 1);
+        if (N == 1) {
+            red3(gg, tg[0], tg[1], tg[2]);
+        } else {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
-                        if (wk[k] != 0.0f)
-                            red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
-                }
-            }
+            for (int k = 0; k < 4; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
+                if (wk[k] != 0.0f)
+                    red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
+        }
+    }
 }
 
 template <int MODE, int NT>
@@ -549,7 +549,6 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
     __shared__ int s_maxlast;
     const int N = tex_n<NT>(n_rt);
     const int F = 3 * N * N;
-    constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
     const int ts = rc.tile_size;
     const int consumers = (ts * ts + 31) >> 5;
     const int tile = blockIdx.x;
@@ -598,7 +597,6 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
     // per-warp reduction scratch after the staging ring
     float* wscratch = reinterpret_cast<float*>(smem + kStages * stage_bytes(B, N)) + warp * kRedRows * kRedStride;
     float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
-    const float sigma = rc.sigma;
 
     for (int r = 0; r < nbatch; ++r) {
         const int s = r % kStages;

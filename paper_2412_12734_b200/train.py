@@ -72,14 +72,20 @@ class ViewShardedTrainer:
                                               device=self.splats.device)
         return self._outs[key], self._grad_img[key]
 
-    def _view(self, i: int, target: torch.Tensor) -> None:
+    def _view_forward(self, i: int):
         cam = self.cameras[self.views[i]]
         out, gimg = self._out(cam)
         build_binning(self.splats, cam, self.raster, out=self.binning)
         self.pairs.append(self.binning.total)
         render_forward(self.splats, cam, self.binning, out)
+        return cam, out, gimg
+
+    def _view_backward(self, i: int, cam, out, gimg, target: torch.Tensor) -> None:
         l1_loss(out.color, target.view(cam.height, cam.width, 3), grad=gimg, loss=self.losses[i:i + 1])
         render_backward(self.splats, cam, self.binning, out, gimg, self.grads)
+
+    def _view(self, i: int, target: torch.Tensor) -> None:
+        self._view_backward(i, *self._view_forward(i), target)
 
     def _finish(self) -> None:
         reduce_gradients(self.grads, self.pg)
@@ -96,7 +102,8 @@ class ViewShardedTrainer:
 
     def step_host(self, targets_host: Sequence[torch.Tensor]) -> torch.Tensor:
         """End-to-end step from pinned HOST targets: the H2D copy of view i+1 overlaps the
-        compute of view i on a side stream; the per-view losses are read back to the host."""
+        compute of view i on a side stream, and a view's own copy only has to land before its
+        loss (binning and forward do not read the target); the per-view losses are read back."""
         cur = torch.cuda.current_stream(self.splats.device)
         self.grads.zero_()
         self.losses.zero_()
@@ -119,9 +126,9 @@ class ViewShardedTrainer:
             b = i % 2
             if i + 1 < n:
                 issue(i + 1)
+            cam, out, gimg = self._view_forward(i)
             cur.wait_event(self._copy_done[b])
-            cam = self.cameras[self.views[i]]
-            self._view(i, self._target_buf[b].view(-1)[: cam.height * cam.width * 3])
+            self._view_backward(i, cam, out, gimg, self._target_buf[b].view(-1)[: cam.height * cam.width * 3])
             self._buf_free[b].record(cur)
         self._finish()
         self._pinned_losses.copy_(self.losses, non_blocking=True)

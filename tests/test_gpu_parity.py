@@ -160,3 +160,21 @@ def test_configs2_full():
     c = _config(2)
     cam = O.Cam.from_spec(c.cameras[0])
     _check("configs2_fwd_bwd", c.arrays(), O.MODE_PINHOLE, c.n, cam, O.Cfg())
+
+
+# ---------------------------------------------------------------------------------------------
+# the measured alternative compositors (GB_COMPOSITOR, read by the library at every launch)
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("variant,group", [("staged", None), ("grp", "4"), ("grp", "8"), ("grp", "16")])
+def test_alternative_compositors(monkeypatch, variant, group):
+    import paper_2412_12734_b200.scenes as sc
+
+    monkeypatch.setenv("GB_COMPOSITOR", variant)
+    if group:
+        monkeypatch.setenv("GB_GROUP", group)
+    cfgs = _config(0, count=20_000, n=4)
+    _check(f"variant_{variant}{group or ''}_pinhole", cfgs.arrays(), O.MODE_PINHOLE, 4,
+           O.Cam.from_spec(cfgs.cameras[0]), O.Cfg())
+    arrays = sc.generate(O.MODE_ORTHO, 3000, 3, 31, width=120, height=88, scale_lo=0.5, scale_hi=8.0)
+    _check(f"variant_{variant}{group or ''}_ortho_n3", arrays, O.MODE_ORTHO, 3,
+           O.Cam(O.MODE_ORTHO, 120, 88, (0.2, 0.1, 0.3)), O.Cfg(tile_size=8))
