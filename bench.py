@@ -220,7 +220,6 @@ def run_ours(args):
     W, H = cams[0].width, cams[0].height
     host_targets = [torch.from_numpy(cfg3.target(v)).pin_memory() for v in views]
     dev_targets = [t.to(device) for t in host_targets]
-    ctx = gb.raster.context(device)
     torch.cuda.synchronize()
 
     def barrier():
@@ -244,9 +243,11 @@ def run_ours(args):
     stream = torch.cuda.current_stream(device)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     trainer.pairs.clear()
-    launches0 = ctx.launches()
-    ctx.profile(True)
-    ctx.profile_read()  # reset
+    ctxs = gb.raster.all_contexts(device)  # one per view lane (stream)
+    launches0 = trainer.launches()
+    for c in ctxs:
+        c.profile(True)
+        c.profile_read()  # reset
     with ClockSampler(torch.cuda.current_device() if world == 1 else local) as clk:
         barrier()
         torch.cuda.synchronize()
@@ -256,9 +257,13 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    ctx.profile(False)
-    prof = ctx.profile_read()
-    launches = ctx.launches() - launches0
+    prof = {}
+    for c in ctxs:
+        c.profile(False)
+        for k, (ms, cnt) in c.profile_read().items():
+            t, n = prof.get(k, (0.0, 0))
+            prof[k] = (t + ms, n + cnt)
+    launches = trainer.launches() - launches0
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
     step_ms = elapsed_ms / args.steps
     views_total = world * len(views)

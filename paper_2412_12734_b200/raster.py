@@ -45,27 +45,36 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
 # context
 # --------------------------------------------------------------------------------------------
 class _Context:
-    _by_device: dict = {}
+    """One C-ABI context per (device, CUDA stream): a context owns the scratch of the calls it
+    runs, so work issued on different streams (the trainer's two view lanes) never shares it."""
 
-    def __init__(self, device: int):
+    _by_stream: dict = {}
+
+    def __init__(self, device: int, stream: int):
         h = C.c_void_p()
         check(lib.gb_context_create(device, C.byref(h)), "gb_context_create")
         self.handle = h
         self.device = device
+        check(lib.gb_context_set_stream(h, C.c_void_p(stream)), "gb_context_set_stream")
 
     @classmethod
     def get(cls, device: torch.device) -> "_Context":
         if device.type != "cuda":
             raise ValueError(f"tensors must live on a CUDA device (got {device}); there is no CPU path")
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        ctx = cls._by_device.get(idx)
-        if ctx is None:
-            ctx = cls(idx)
-            cls._by_device[idx] = ctx
         with torch.cuda.device(idx):
             stream = torch.cuda.current_stream(idx).cuda_stream
-        check(lib.gb_context_set_stream(ctx.handle, C.c_void_p(stream)), "gb_context_set_stream")
+        ctx = cls._by_stream.get((idx, stream))
+        if ctx is None:
+            ctx = cls(idx, stream)
+            cls._by_stream[(idx, stream)] = ctx
         return ctx
+
+    @classmethod
+    def all(cls, device) -> list:
+        idx = torch.device(device).index
+        idx = torch.cuda.current_device() if idx is None else idx
+        return [c for (d, _), c in cls._by_stream.items() if d == idx]
 
     def launches(self) -> int:
         return int(lib.gb_context_launch_count(self.handle))
@@ -85,7 +94,13 @@ class _Context:
 
 
 def context(device=None) -> _Context:
+    """The context of the current CUDA stream on `device`."""
     return _Context.get(torch.device(device) if device is not None else torch.device("cuda"))
+
+
+def all_contexts(device=None) -> list:
+    """Every context created on `device` (one per stream used)."""
+    return _Context.all(device if device is not None else "cuda")
 
 
 # --------------------------------------------------------------------------------------------

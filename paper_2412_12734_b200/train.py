@@ -18,7 +18,8 @@ from typing import List, Optional, Sequence
 import torch
 
 from .raster import (AdamConfig, AdamState, GradientBuffer, LearningRates, RasterConfig, RenderOutput, SplatSet,
-                     TileBinning, adam_step, build_binning, context, l1_loss, render_backward, render_forward)
+                     TileBinning, adam_step, all_contexts, build_binning, l1_loss, render_backward,
+                     render_forward)
 
 
 def shard_views(n_views: int, rank: int, world: int, per_rank: Optional[int] = None) -> List[int]:
@@ -38,9 +39,29 @@ def reduce_gradients(grads: GradientBuffer, process_group=None) -> None:
             torch.distributed.all_reduce(grads.flat, op=torch.distributed.ReduceOp.SUM, group=process_group)
 
 
+class _Lane:
+    """One view pipeline: a CUDA stream (hence its own C-ABI context and scratch), a binning,
+    output and cotangent buffers.  View i of a step runs on lane i % lanes."""
+
+    def __init__(self, device, stream):
+        self.stream = stream
+        with torch.cuda.stream(stream):
+            self.binning = TileBinning(device)
+        self.outs = {}
+        self.done = torch.cuda.Event()
+
+
 class ViewShardedTrainer:
+    """configs[3] step: per owned view K1..K6 + K4/K5 into one gradient buffer, one all-reduce, Adam.
+
+    Views alternate between `lanes` streams, so the binning of view i+1 (whose pair count
+    the host must read back) and its small sort/scan kernels overlap the compositors of view
+    i instead of leaving the GPU idle at the host synchronisation point.  All lanes add into
+    the same gradient buffer with atomics; the step joins them before the all-reduce."""
+
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
-                 adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False):
+                 adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
+                 lanes: int = 2):
         self.splats = splats
         self.cameras = list(cameras)
         self.views = list(views)
@@ -48,55 +69,75 @@ class ViewShardedTrainer:
         self.raster = raster or RasterConfig()
         self.grads = GradientBuffer(splats)
         self.state = AdamState(splats, adam)
-        self.binning = TileBinning(splats.device)
         self.pg = process_group
         self.check_finite = check_finite
         dev = splats.device
+        main = torch.cuda.current_stream(dev)
+        self._lanes = [_Lane(dev, main if i == 0 else torch.cuda.Stream(device=dev)) for i in range(max(1, lanes))]
+        self.binning = self._lanes[0].binning
         W = max(self.cameras[v].width for v in self.views) if self.views else 1
         H = max(self.cameras[v].height for v in self.views) if self.views else 1
-        self._outs = {}
-        self._grad_img = {}
         self.losses = torch.zeros(max(1, len(self.views)), dtype=torch.float32, device=dev)
         self._pinned_losses = torch.zeros(max(1, len(self.views)), dtype=torch.float32, pin_memory=True)
         self._target_buf = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
         self._copy_stream = torch.cuda.Stream(device=dev)
         self._copy_done = [torch.cuda.Event() for _ in range(2)]
         self._buf_free = [torch.cuda.Event() for _ in range(2)]
+        self._step_start = torch.cuda.Event()
         self.pairs: List[int] = []  # tile/primitive pair count P of every view binned (roofline bytes)
 
-    def _out(self, cam):
+    def _out(self, lane: _Lane, cam):
         key = (cam.width, cam.height)
-        if key not in self._outs:
-            self._outs[key] = RenderOutput(cam.width, cam.height, self.splats.device)
-            self._grad_img[key] = torch.empty((cam.height, cam.width, 3), dtype=torch.float32,
-                                              device=self.splats.device)
-        return self._outs[key], self._grad_img[key]
+        if key not in lane.outs:
+            with torch.cuda.stream(lane.stream):
+                lane.outs[key] = (RenderOutput(cam.width, cam.height, self.splats.device),
+                                  torch.empty((cam.height, cam.width, 3), dtype=torch.float32,
+                                              device=self.splats.device))
+        return lane.outs[key]
+
+    def _lane(self, i: int) -> _Lane:
+        return self._lanes[i % len(self._lanes)]
 
     def _view_forward(self, i: int):
+        lane = self._lane(i)
         cam = self.cameras[self.views[i]]
-        out, gimg = self._out(cam)
-        build_binning(self.splats, cam, self.raster, out=self.binning)
-        self.pairs.append(self.binning.total)
-        render_forward(self.splats, cam, self.binning, out)
+        out, gimg = self._out(lane, cam)
+        build_binning(self.splats, cam, self.raster, out=lane.binning)
+        self.pairs.append(lane.binning.total)
+        render_forward(self.splats, cam, lane.binning, out)
         return cam, out, gimg
 
     def _view_backward(self, i: int, cam, out, gimg, target: torch.Tensor) -> None:
+        lane = self._lane(i)
         l1_loss(out.color, target.view(cam.height, cam.width, 3), grad=gimg, loss=self.losses[i:i + 1])
-        render_backward(self.splats, cam, self.binning, out, gimg, self.grads)
+        render_backward(self.splats, cam, lane.binning, out, gimg, self.grads)
 
-    def _view(self, i: int, target: torch.Tensor) -> None:
-        self._view_backward(i, *self._view_forward(i), target)
+    def _begin(self) -> None:
+        main = self._lanes[0].stream
+        self.grads.zero_()
+        self.losses.zero_()
+        self._step_start.record(main)
+        for lane in self._lanes[1:]:
+            lane.stream.wait_event(self._step_start)  # parameters updated and gradients zeroed
+
+    def _join(self) -> None:
+        main = self._lanes[0].stream
+        for lane in self._lanes[1:]:
+            lane.done.record(lane.stream)
+            main.wait_event(lane.done)
 
     def _finish(self) -> None:
+        self._join()
         reduce_gradients(self.grads, self.pg)
         adam_step(self.splats, self.grads, self.state, self.lrs, check_finite=self.check_finite)
 
     def step(self, targets: Sequence[torch.Tensor]) -> torch.Tensor:
         """One training step with device-resident per-view targets; returns the device loss vector."""
-        self.grads.zero_()
-        self.losses.zero_()
+        self._begin()
         for i in range(len(self.views)):
-            self._view(i, targets[i])
+            with torch.cuda.stream(self._lane(i).stream):
+                cam, out, gimg = self._view_forward(i)
+                self._view_backward(i, cam, out, gimg, targets[i])
         self._finish()
         return self.losses
 
@@ -104,9 +145,8 @@ class ViewShardedTrainer:
         """End-to-end step from pinned HOST targets: the H2D copy of view i+1 overlaps the
         compute of view i on a side stream, and a view's own copy only has to land before its
         loss (binning and forward do not read the target); the per-view losses are read back."""
-        cur = torch.cuda.current_stream(self.splats.device)
-        self.grads.zero_()
-        self.losses.zero_()
+        main = self._lanes[0].stream
+        self._begin()
         n = len(self.views)
 
         def issue(i):
@@ -119,21 +159,24 @@ class ViewShardedTrainer:
                 self._copy_done[b].record(self._copy_stream)
 
         for b in range(2):
-            self._buf_free[b].record(cur)
+            self._buf_free[b].record(main)
         if n:
             issue(0)
         for i in range(n):
             b = i % 2
             if i + 1 < n:
                 issue(i + 1)
-            cam, out, gimg = self._view_forward(i)
-            cur.wait_event(self._copy_done[b])
-            self._view_backward(i, cam, out, gimg, self._target_buf[b].view(-1)[: cam.height * cam.width * 3])
-            self._buf_free[b].record(cur)
+            s = self._lane(i).stream
+            with torch.cuda.stream(s):
+                cam, out, gimg = self._view_forward(i)
+                s.wait_event(self._copy_done[b])
+                self._view_backward(i, cam, out, gimg,
+                                    self._target_buf[b].view(-1)[: cam.height * cam.width * 3])
+                self._buf_free[b].record(s)
         self._finish()
         self._pinned_losses.copy_(self.losses, non_blocking=True)
-        cur.synchronize()
+        main.synchronize()
         return self._pinned_losses
 
     def launches(self) -> int:
-        return context(self.splats.device).launches()
+        return sum(c.launches() for c in all_contexts(self.splats.device))
