@@ -92,9 +92,13 @@ struct PinholeTerms {  // kept for the backward chain
 // and K4 still see identical bits; only the oracle comparison is
 // tolerance-based, and 1 ulp is far inside it.
 __device__ __forceinline__ float rcp_approx(float x) {
+#ifdef GB_PRECISE_EVAL
+    return __frcp_rn(x);
+#else
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
+#endif
 }
 
 // raster.hpp:36-42 (ortho) -- returns true (always a hit).
@@ -130,9 +134,13 @@ __device__ __forceinline__ bool eval_uv_pinhole(const ScreenHeader& h, int x, in
 // (ftz: G underflows to 0 far outside the splat, where alpha < alpha_skip anyway).
 __device__ __forceinline__ float gauss_weight(float u, float v) {
     const float x = __fmul_rn(-0.72134752044448170368f, __fmaf_rn(u, u, __fmul_rn(v, v)));
+#ifdef GB_PRECISE_EVAL
+    return exp2f(x);
+#else
     float g;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(x));
     return g;
+#endif
 }
 
 // uv -> (i, f) on one axis, texture.hpp:27-37, with N fixed at compile time.

@@ -273,6 +273,21 @@ __device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g) 
     if (!(isfinite(A11) && isfinite(A12) && isfinite(A22) && isfinite(ex) && isfinite(ey)) || !(A11 > 0.0) ||
         !(A22 > 0.0) || fabs(ex) > 1e7 || fabs(ey) > 1e7)
         return all;
+    // The kernels evaluate the form in fp32, whose error near the boundary is ~eps32 * cond(Q); past
+    // cond 4096 that would eat the 0.2 % margin (thin, grazing surfels).  Those fall back to the ellipse
+    // circumscribing the alpha-box (axis-aligned, no cancellation).
+    const double tr = 0.5 * (A11 + A22), dq = sqrt(fmax(tr * tr - (A11 * A22 - A12 * A12), 0.0));
+    if (!(tr - dq > 0.0) || (tr + dq) > 4096.0 * (tr - dq)) {
+        const float4 box = alpha_box(p, k, g);
+        if (box.x > box.y || box.z > box.w) return none;
+        if (box.x < -1e29f || box.y > 1e29f || box.z < -1e29f || box.w > 1e29f) return all;
+        const double hx = 0.5 * ((double)box.y - (double)box.x) + 0.5, hy = 0.5 * ((double)box.w - (double)box.z) + 0.5;
+        CullRec out;
+        out.a = make_float4((float)(0.5 * ((double)box.x + (double)box.y)), (float)(0.5 * ((double)box.z + (double)box.w)),
+                            (float)(0.5 / (hx * hx)), (float)(0.5 / (hy * hy)));
+        out.b = make_float4(0.f, 0.f, 0.f, 0.f);
+        return out;
+    }
     CullRec out;
     out.a = make_float4((float)ex, (float)ey, (float)A11, (float)A22);
     out.b = make_float4((float)A12, (float)(A12 / A22), (float)(A12 / A11), 0.f);

@@ -658,8 +658,9 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
         bool pass = false;
         if (c0 + lane < total) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f, by0 - 0.05f,
-                                         by1 + 0.05f);
+            pass = cull ? ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f,
+                                             by0 - 0.05f, by1 + 0.05f)
+                        : !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         while (mask) {
@@ -766,8 +767,9 @@ __global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict
         bool pass = false;
         if (c0 + lane <= wlast) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f, by0 - 0.05f,
-                                         by1 + 0.05f);
+            pass = cull ? ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f,
+                                             by0 - 0.05f, by1 + 0.05f)
+                        : !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         if (lane == 0) GB_DBG(1, __popc(mask));
@@ -856,6 +858,7 @@ template <int MODE, int NT>
 static cudaError_t fwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc, int n,
                           float* color, float* trans, int32_t* last) {
+    if (tune_env("GB_CULL_BOX", 0)) cull = nullptr;  // A/B: alpha-box test instead of the exact ellipse
     k_forward_direct<MODE, NT><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, color, trans, last);
     return cudaGetLastError();
 }
@@ -866,6 +869,7 @@ static cudaError_t bwdd_t(int tiles, int threads, cudaStream_t st, const uint2* 
                           const float* trans, const int32_t* last, const float* image_grad, float* accum,
                           float* grid_grad) {
     const size_t smem = (size_t)(threads / 32) * kRedRows * kRedStride * 4;
+    if (tune_env("GB_CULL_BOX", 0)) cull = nullptr;
     k_backward_direct<MODE, NT><<<tiles, threads, smem, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, trans, last,
                                                                image_grad, accum, grid_grad);
     return cudaGetLastError();
