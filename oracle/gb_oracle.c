@@ -822,6 +822,21 @@ static void backward_tile(void *vctx, int tile) {
             double t = c->trans[p];
             const double t_final = t;
             double behind[3] = {c->cam->background[0], c->cam->background[1], c->cam->background[2]};
+            if (pslk && (px_flag & 1) && kk && cfg->alpha_skip > 0.0 && !(cfg->early_stop > 0.0 && t < cfg->early_stop)) {
+                /* entries skipped just below the threshold AFTER the last composited one: fp32 may composite
+                 * them (then its walk starts there); their own terms are the slack */
+                for (int64_t rank = len - 1; rank > last; --rank) {
+                    const int32_t id = list[rank];
+                    const geom_t *g = &c->geom[id];
+                    double u, v, a[3], b[3], cz = 0.0;
+                    if (!eval_uv(c, g, px, py, &u, &v, a, b, &cz)) continue;
+                    const double weight = gaussian_weight(u, v);
+                    const double alpha = dmin(g->alpha_k * weight, kMaxAlpha);
+                    if (fabs(alpha - cfg->alpha_skip) <= kk->alpha_rel * cfg->alpha_skip)
+                        add_abs_terms(c, g, px, py, u, v, alpha, weight, t, gacc, behind,
+                                      c->s->grid + (size_t)id * tex_stride, a, b, cz, pslk + (size_t)rank * stride);
+                }
+            }
             for (int32_t rank = last; rank >= 0; --rank) {
                 const int32_t id = list[rank];
                 const geom_t *g = &c->geom[id];
