@@ -149,24 +149,10 @@ def cpu_setup(args, cfg3):
     return O, scene64
 
 
-def band_binning(binning, band, nbands):
-    """The CSR binning restricted to tile rows [band*ty/nbands, (band+1)*ty/nbands) (other tiles empty)."""
-    offsets, values, (tx, ty) = binning
-    r0, r1 = band * ty // nbands, (band + 1) * ty // nbands
-    lens = np.diff(offsets)
-    keep = np.zeros(tx * ty, bool)
-    keep[r0 * tx:r1 * tx] = True
-    new_lens = np.where(keep, lens, 0)
-    new_off = np.concatenate([[0], np.cumsum(new_lens)]).astype(np.int64)
-    new_vals = values[offsets[r0 * tx]:offsets[r1 * tx]]
-    return (new_off, new_vals, (tx, ty)), r0, r1
-
-
 def run_reference(args):
-    """The reference algorithm's CPU implementation on all host cores (rank 0 only).  Each step is a
-    bounded sample of the workload: one eighth of a configs[3] view (a band of tile rows: forward +
-    L1 + backward on that band, plus an eighth of the view's binning and of the step's Adam share),
-    so the whole --steps K --warmup W run stays within minutes."""
+    """The reference algorithm's CPU implementation on all host cores (rank 0 only), one full configs[3]
+    view per step.  (Sub-view samples are not representative: every reference call allocates and reduces
+    full-size gradient buffers, so a band of a view costs half a view.)"""
     rank, world, local = dist_env()
     if rank != 0:
         return
@@ -175,46 +161,31 @@ def run_reference(args):
     cfg3 = sc.baseline_config(3, count=args.count, n=args.n)
     O, scene64 = cpu_setup(args, cfg3)
     cores = os.cpu_count() or 1
-    nb = 8
-    cfg = O.Cfg()
-    W, H = cfg3.cameras[0].width, cfg3.cameras[0].height
-    per_view = {}
-    times, pixels = [], []
+    times = []
+    views = list(range(len(cfg3.cameras)))
     for it in range(args.warmup + args.steps):
-        v = (it // nb) % len(cfg3.cameras)
-        band = it % nb
+        v = views[it % len(views)]
         cam = O.Cam.from_spec(cfg3.cameras[v])
-        if v not in per_view:
-            t0 = time.perf_counter()
-            b = O.build_binning(scene64, cam, cfg)  # single-threaded, as raster.hpp:128-146
-            per_view = {v: (b, time.perf_counter() - t0, cfg3.target(v))}
-        b, t_bin, tgt = per_view[v]
-        bb, r0, r1 = band_binning(b, band, nb)
+        tgt = cfg3.target(v)
         t0 = time.perf_counter()
-        f = O.render_forward(scene64, cam, cfg, bb, kink=None)
-        _, ig = O.l1_loss(f["color"], tgt, 1.0 / f["color"].size)
-        g, _, _ = O.render_backward(scene64, cam, cfg, bb, f, ig.reshape(f["color"].shape), kink=None,
-                                    want_mag=False)
-        flat = np.concatenate([x.ravel() for x in g.values() if x is not None])
-        m = flat.size // (8 * nb)  # the step's Adam over the parameters, amortised over 8 views x nb bands
-        O.adam_group(np.zeros(m), flat[:m], np.zeros(m), np.zeros(m), 1e-3, 0.9, 0.999, 1e-8, 0.1, 0.001)
-        dt = time.perf_counter() - t0 + t_bin / nb
+        cpu_view(scene64, cam, tgt)
+        dt = time.perf_counter() - t0
         if it >= args.warmup:
             times.append(dt)
-            pixels.append(W * (min(16 * r1, H) - 16 * r0))
+    W, H = cfg3.cameras[0].width, cfg3.cameras[0].height
     step_s = sum(times) / len(times)
-    mps = sum(pixels) / 1e6 / sum(times)
-    sample = (f"one eighth of a configs[3] view per step (a band of tile rows: forward + L1 + backward, plus 1/8 "
-              f"of the view's binning and of its Adam share), fp64 C restatement of the reference algorithm "
-              f"(oracle/gb_oracle.c), {cores} threads; the compiled reference has no perspective path")
+    mps = W * H / 1e6 / step_s
     line = {
         "impl": "reference", "metric": METRIC, "value": round(mps, 4), "unit": "MP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
-        "ms_per_view": round(step_s * nb * 1e3, 1), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[3] shapes)",
-        "config": {"workload": "configs[3] view: 1M surfels, 8x8 fp32 textures, 1600x1064, fwd+bwd+L1 (+Adam share)",
-                   "views_per_step": 1.0 / nb},
-        "cpu_baseline": {"value": round(mps, 4), "unit": "MP/s", "cores": cores, "kind": "port", "sample": sample},
+        "ms_per_view": round(step_s * 1e3, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[3] shapes)",
+        "config": {"workload": "configs[3] view: 1M surfels, 8x8 fp32 textures, 1600x1064, fwd+bwd+L1 (+1/8 Adam)",
+                   "views_per_step": 1},
+        "cpu_baseline": {"value": round(mps, 4), "unit": "MP/s", "cores": cores, "kind": "port",
+                         "sample": "one full configs[3] view per step (binning + forward + L1 + backward + 1/8 "
+                                   "Adam), fp64 C restatement of the reference algorithm (oracle/gb_oracle.c), "
+                                   f"{cores} threads; the compiled reference has no perspective path"},
         "e2e": {"value": round(mps, 4), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
