@@ -2,24 +2,29 @@
 // back-to-front backward), fp32, sm_100a.
 //
 // One CTA per tile (tile size 1..16), one thread per pixel; with 8-multiple
-// tiles each warp owns an 8x4 pixel block.  The tile's sorted list is walked
-// in batches of B entries whose 64 B screen headers and full n x n x 3
-// textures are staged in shared memory (the texture is the
-// shared-memory cost that forced the A6000 implementation to 8x8 tiles at
-// n=8).  Staging is double-buffered and asynchronous: warp 0 issues one TMA
-// bulk copy (cp.async.bulk, UBLKCP) per header and per texture of batch b+1,
-// completing on an mbarrier, while all warps composite batch b.  A warp skips
-// an entry outright when its pixel block misses the entry's alpha-box (K1).
+// tiles each warp owns an 8x4 pixel block.  Two implementations of the walk:
+//
+//  * direct (k_forward_direct / k_backward_direct, the default): every warp
+//    walks the tile's sorted list on its own through L1.  Per 32 entries it
+//    loads ids and cull records, tests its pixel rectangle against each
+//    entry's exact alpha-skip ellipse (K1 alpha_ellipse) and ballots; then it
+//    composites the passing entries one at a time.  No CTA barrier.
+//  * staged (k_forward / k_backward, GB_COMPOSITOR=staged): a producer warp
+//    streams every entry's 64 B header and full n x n x 3 texture into a
+//    4-stage shared-memory ring with TMA bulk copies (cp.async.bulk, UBLKCP)
+//    and mbarrier full/empty handshakes, the 8 consumer warps composite from
+//    shared memory (PAPER.md:202-206 staged textures the same way).  Measured
+//    slower: it copies whole textures where a pixel needs four
+//    texels and spends issue slots in barrier waits.
 //
 // K3 restates render_forward (raster.hpp:201-261) + bilinear
 // (texture.hpp:49-66); K4 restates render_backward (raster.hpp:277-387) +
 // adj_bilinear_accum (texture.hpp:77-111).  Instead of the reference's
 // per-(tile, rank) partial records and ordered reduction, K4 reduces each
-// entry's per-pixel contributions across the warp with a reduce-scatter
-// (transpose) butterfly -- V values cost V-1 shuffles instead of 5V -- and
-// issues red.global.add from the lanes that end up owning each sum, into
-// (a) the caller's texel gradients and (b) a 48 B per-primitive
-// screen-space accumulator that K5 chains to the raw parameters.
+// entry's per-pixel contributions across the warp (a shared-memory transpose,
+// lane l summing half of row l/2) and issues red.global.add from the lanes
+// that own each sum, into (a) the caller's texel gradients and (b) a 48 B
+// per-primitive screen-space accumulator that K5 chains to the raw parameters.
 #include <cstdlib>
 #include <cstring>
 
