@@ -61,7 +61,9 @@ typedef struct {
  * ortho  : position 2K (x,y), depth_key K, theta K
  * pinhole: position 3K world mean (x,y,z), quat 4K (w,x,y,z), unnormalised
  * both   : log_scale 2K (u,v), opacity_logit K, grid K*n*n*3 in
- *          (i_u, i_v, channel) order (core.hpp:44-48). */
+ *          (i_u, i_v, channel) order (core.hpp:44-48).
+ * Alignment: quat 16 B, log_scale 8 B, grid_values 16 B for even n (any
+ * device allocation is; K1/K3/K4 read them as vectors). */
 typedef struct {
     int64_t count;
     gb_grid_config grid;

@@ -218,6 +218,9 @@ gb_status validate_splats(const gb_splats* s, int mode) {
     if (mode == GB_MODE_PINHOLE && !s->quat) return fail(GB_INVALID_ARGUMENT, "pinhole splats need quat");
     if ((s->grid.n % 2) == 0 && (reinterpret_cast<uintptr_t>(s->grid_values) & 15))
         return fail(GB_INVALID_ARGUMENT, "grid_values must be 16-byte aligned");
+    if (reinterpret_cast<uintptr_t>(s->log_scale) & 7) return fail(GB_INVALID_ARGUMENT, "log_scale must be 8-byte aligned");
+    if (mode == GB_MODE_PINHOLE && (reinterpret_cast<uintptr_t>(s->quat) & 15))
+        return fail(GB_INVALID_ARGUMENT, "quat must be 16-byte aligned");
     return GB_OK;
 }
 

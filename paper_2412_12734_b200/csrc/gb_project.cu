@@ -38,8 +38,11 @@ __device__ __forceinline__ double dmin_(double a, double b) { return (b < a) ? b
 __device__ void build_geom(const ProjParams& p, int64_t k, Geom& g) {
     g.valid = false;
     g.alpha_k = 1.0 / (1.0 + exp(-(double)p.opacity[k]));
-    const double eu = exp((double)p.log_scale[2 * k + 0]);
-    const double ev = exp((double)p.log_scale[2 * k + 1]);
+    // SoA fields are read as one vector per primitive (log-scales 8 B, quaternion 16 B; the C-ABI requires
+    // the caller's buffers to be at least 16-B aligned, as every device allocator provides)
+    const float2 ls = __ldg(reinterpret_cast<const float2*>(p.log_scale) + k);
+    const double eu = exp((double)ls.x);
+    const double ev = exp((double)ls.y);
     g.s_u = dmax_(eu, 1e-8);
     g.s_v = dmax_(ev, 1e-8);
     g.su_clamped = eu < 1e-8;
@@ -52,7 +55,8 @@ __device__ void build_geom(const ProjParams& p, int64_t k, Geom& g) {
         g.depth = (double)p.depth_key[k];
         return;
     }
-    const double q0 = p.quat[4 * k + 0], q1 = p.quat[4 * k + 1], q2 = p.quat[4 * k + 2], q3 = p.quat[4 * k + 3];
+    const float4 q4 = __ldg(reinterpret_cast<const float4*>(p.quat) + k);
+    const double q0 = q4.x, q1 = q4.y, q2 = q4.z, q3 = q4.w;
     const double nn = q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3;
     g.qnorm = sqrt(nn);
     if (!(g.qnorm > 0.0)) return;

@@ -96,6 +96,21 @@ def main():
                 pad = (-n) % B
                 wb = np.concatenate([wact, np.zeros((pad, wact.shape[1]), bool)]).reshape(-1, B, wact.shape[1])
                 tot[key] = tot.get(key, 0) + wb.sum(1).max(1).sum()
+            # consecutive warp-active entries with disjoint active-pixel sets composited in one step
+            for cap in (2, 3, 4):
+                key = f"disjoint groups <= {cap}"
+                steps = 0
+                union = None
+                size = 0
+                for row in wact:
+                    if union is not None and size < cap and not (union & row).any():
+                        union |= row
+                        size += 1
+                    else:
+                        steps += 1
+                        union = row.copy()
+                        size = 1
+                tot[key] = tot.get(key, 0) + steps
             for name, G in lay.items():
                 if G == 32:
                     gid = np.zeros_like(lx)
