@@ -178,3 +178,22 @@ def test_alternative_compositors(monkeypatch, variant, group):
     arrays = sc.generate(O.MODE_ORTHO, 3000, 3, 31, width=120, height=88, scale_lo=0.5, scale_hi=8.0)
     _check(f"variant_{variant}{group or ''}_ortho_n3", arrays, O.MODE_ORTHO, 3,
            O.Cam(O.MODE_ORTHO, 120, 88, (0.2, 0.1, 0.3)), O.Cfg(tile_size=8))
+
+
+def test_pinhole_camera_inside_the_cloud():
+    """Camera at the centre of the cloud: splats behind the camera, crossing the near plane, huge
+    close-up splats covering many tiles, and grazing ones -- the cull and miss rules of SURVEY App. C."""
+    import paper_2412_12734_b200.scenes as sc
+
+    spec = sc.look_at((0.05, -0.02, 0.0), (0.3, 0.1, 1.0), 160, 120, 110.0, 110.0, 80.0, 60.0)
+    arrays = sc.generate(O.MODE_PINHOLE, 4000, 4, 17, mean_lo=-1.0, mean_hi=1.0, scale_lo=0.005, scale_hi=0.08)
+    _check("pinhole_inside_cloud", arrays, O.MODE_PINHOLE, 4, O.Cam.from_spec(spec), O.Cfg())
+
+
+def test_pinhole_few_huge_splats():
+    """A handful of splats much larger than the image: every tile lists them, lists are short."""
+    import paper_2412_12734_b200.scenes as sc
+
+    spec = sc.look_at((0.0, 0.0, -2.0), (0.0, 0.0, 0.0), 96, 80, 90.0, 90.0, 48.0, 40.0)
+    arrays = sc.generate(O.MODE_PINHOLE, 12, 8, 19, mean_lo=-0.3, mean_hi=0.3, scale_lo=0.5, scale_hi=2.0)
+    _check("pinhole_huge", arrays, O.MODE_PINHOLE, 8, O.Cam.from_spec(spec), O.Cfg())
