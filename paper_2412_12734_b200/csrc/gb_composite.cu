@@ -28,6 +28,9 @@
 // K3 restates render_forward (raster.hpp:201-261) + bilinear
 // (texture.hpp:49-66); K4 restates render_backward (raster.hpp:277-387) +
 // adj_bilinear_accum (texture.hpp:77-111).
+#include <cstdlib>
+#include <cstring>
+
 #include "gb_compose.cuh"
 
 namespace gb {
@@ -391,7 +394,7 @@ __device__ __forceinline__ bool bwd_px(const ScreenHeader& h, const float* __res
     return true;
 }
 
-template <int MODE, int NT, int G>
+template <int MODE, int NT, int G, bool UNI>
 __global__ void __launch_bounds__(256, 4) k_backward_grp(const uint2* __restrict__ ranges,
                                                       const int32_t* __restrict__ values,
                                                       const ScreenHeader* __restrict__ hdr,
@@ -450,7 +453,8 @@ __global__ void __launch_bounds__(256, 4) k_backward_grp(const uint2* __restrict
         if (!__any_sync(kFull, gw.pend != 0)) break;
         int id = -1;
         bool on = false;
-        float red[10], tg[12];
+        float red[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // inactive lanes add zeros
+        float tg[12];
         int tbase = 0;
         if (gw.pend != 0) {
             const int bit = __ffs(gw.pend) - 1;
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(256, 4) k_backward_grp(const uint2* __restrict
         {  // screen-space sums: one per (value, group), owned by distinct lanes
             float sv[NS];
 #pragma unroll
-            for (int i = 0; i < NS; ++i) sv[i] = on ? red[i] : 0.0f;
+            for (int i = 0; i < NS; ++i) sv[i] = red[i];
             float r2[PS];
             group_reduce<NS, G>(sv, wscratch, lane, r2);
 #pragma unroll
@@ -481,26 +485,30 @@ __global__ void __launch_bounds__(256, 4) k_backward_grp(const uint2* __restrict
                     red_add(accum + (size_t)gid * kAccumStride + q / NG, r2[k]);
             }
         }
-        // texel terms: one reduction for the groups whose active pixels share a bilinear cell
-        const unsigned gact = act & gm;
-        const int b0 = __shfl_sync(kFull, tbase, gact ? __ffs(gact) - 1 : lane);
-        const unsigned mixed = __ballot_sync(kFull, on && tbase != b0);
-        const bool uni = (mixed & gm) == 0 && gact != 0;
-        const unsigned unimask = __ballot_sync(kFull, uni);
-        if (unimask) {
-            float tv[12];
+        // texel terms (UNI): one reduction for the groups whose active pixels share a bilinear cell;
+        // otherwise (and always without UNI) each lane adds its non-zero texels straight to HBM
+        bool uni = false;
+        if (UNI) {
+            const unsigned gact = act & gm;
+            const int b0 = __shfl_sync(kFull, tbase, gact ? __ffs(gact) - 1 : lane);
+            const unsigned mixed = __ballot_sync(kFull, on && tbase != b0);
+            uni = (mixed & gm) == 0 && gact != 0;
+            const unsigned unimask = __ballot_sync(kFull, uni);
+            if (unimask) {
+                float tv[12];
 #pragma unroll
-            for (int i = 0; i < 12; ++i) tv[i] = (uni && on) ? tg[i] : 0.0f;
-            float r2[PT];
-            group_reduce<12, G>(tv, wscratch, lane, r2);
+                for (int i = 0; i < 12; ++i) tv[i] = (uni && on) ? tg[i] : 0.0f;
+                float r2[PT];
+                group_reduce<12, G>(tv, wscratch, lane, r2);
 #pragma unroll
-            for (int k = 0; k < PT; ++k) {
-                const int q = lane + 32 * k;
-                const int src = (q % NG) * G;
-                const int gid = __shfl_sync(kFull, id, src);
-                const int gb0 = __shfl_sync(kFull, b0, src);
-                if (q < 12 * NG && ((unimask >> src) & 1u) && (N > 1 || q / NG < 3))
-                    red_add(grid_grad + (size_t)gid * F + gb0 + corner_offset(q / NG, N), r2[k]);
+                for (int k = 0; k < PT; ++k) {
+                    const int q = lane + 32 * k;
+                    const int src = (q % NG) * G;
+                    const int gid = __shfl_sync(kFull, id, src);
+                    const int gb0 = __shfl_sync(kFull, b0, src);
+                    if (q < 12 * NG && ((unimask >> src) & 1u) && (N > 1 || q / NG < 3))
+                        red_add(grid_grad + (size_t)gid * F + gb0 + corner_offset(q / NG, N), r2[k]);
+                }
             }
         }
         if (on && !uni) {  // mixed cells: each lane adds its (at most four) non-zero texels straight to HBM
@@ -545,6 +553,31 @@ static int group_size() {  // GB_GROUP=4|8|16 (A/B); default 8
         default: GB_GRP_DISPATCH(KERNEL, MODE, 8, __VA_ARGS__) break;  \
     }
 
+#define GB_GRP_DISPATCH4(KERNEL, MODE, G, UNI, ...)                                      \
+    switch (n) {                                                                         \
+        case 1: KERNEL<MODE, 1, G, UNI><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 2: KERNEL<MODE, 2, G, UNI><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 4: KERNEL<MODE, 4, G, UNI><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 8: KERNEL<MODE, 8, G, UNI><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;   \
+        case 16: KERNEL<MODE, 16, G, UNI><<<tiles, threads, 0, st>>>(__VA_ARGS__); break; \
+        default: KERNEL<MODE, 0, G, UNI><<<tiles, threads, 0, st>>>(__VA_ARGS__); break;  \
+    }
+
+// backward: G and the texel strategy (GB_GRP_TEXEL=uni: shared-cell reductions, default: per-lane reds)
+#define GB_GRP_B(KERNEL, MODE, ...)                                                                      \
+    {                                                                                                    \
+        const char* tv_ = getenv("GB_GRP_TEXEL");                                                         \
+        const bool uni_ = tv_ && !strcmp(tv_, "uni");                                                     \
+        switch (group_size() * 2 + (uni_ ? 1 : 0)) {                                                      \
+            case 8: GB_GRP_DISPATCH4(KERNEL, MODE, 4, false, __VA_ARGS__) break;                          \
+            case 9: GB_GRP_DISPATCH4(KERNEL, MODE, 4, true, __VA_ARGS__) break;                           \
+            case 32: GB_GRP_DISPATCH4(KERNEL, MODE, 16, false, __VA_ARGS__) break;                        \
+            case 33: GB_GRP_DISPATCH4(KERNEL, MODE, 16, true, __VA_ARGS__) break;                         \
+            case 17: GB_GRP_DISPATCH4(KERNEL, MODE, 8, true, __VA_ARGS__) break;                          \
+            default: GB_GRP_DISPATCH4(KERNEL, MODE, 8, false, __VA_ARGS__) break;                         \
+        }                                                                                                \
+    }
+
 cudaError_t launch_forward_grp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                                const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                                const RasterConst& rc, float* color, float* trans, int32_t* last, cudaStream_t st) {
@@ -563,11 +596,11 @@ cudaError_t launch_backward_grp(int mode, int n, int tiles, int ts, const uint2*
                                 const float* image_grad, float* accum, float* grid_grad, cudaStream_t st) {
     const int threads = ts * ts;
     if (mode == GB_MODE_ORTHO) {
-        GB_GRP_G(k_backward_grp, GB_MODE_ORTHO, ranges, values, hdr, cull, tex, cc, rc, n, trans, last, image_grad,
+        GB_GRP_B(k_backward_grp, GB_MODE_ORTHO, ranges, values, hdr, cull, tex, cc, rc, n, trans, last, image_grad,
                  accum, grid_grad)
     } else {
-        GB_GRP_G(k_backward_grp, GB_MODE_PINHOLE, ranges, values, hdr, cull, tex, cc, rc, n, trans, last, image_grad,
-                 accum, grid_grad)
+        GB_GRP_B(k_backward_grp, GB_MODE_PINHOLE, ranges, values, hdr, cull, tex, cc, rc, n, trans, last,
+                 image_grad, accum, grid_grad)
     }
     return cudaGetLastError();
 }

@@ -803,9 +803,10 @@ static int tune_env(const char* name, int dflt) {  // development knob: GB_TUNE_
 // Compositor variant: 1 = one warp per entry reading through L1 (default),
 // 0 = sub-warp groups (gb_composite.cu; tile sizes 8 and 16), 2 = one warp per
 // entry with TMA bulk-copy staging.  GB_COMPOSITOR=direct|grp|staged selects
-// one explicitly (A/B measurements and parity tests).
-static int compositor_variant() {
-    const char* v = getenv("GB_COMPOSITOR");
+// one explicitly (A/B measurements and parity tests); GB_COMPOSITOR_BWD
+// overrides it for the backward only.
+static int compositor_variant(bool backward = false) {
+    const char* v = backward && getenv("GB_COMPOSITOR_BWD") ? getenv("GB_COMPOSITOR_BWD") : getenv("GB_COMPOSITOR");
     if (!v) return 1;
     if (!strcmp(v, "grp")) return 0;
     if (!strcmp(v, "staged")) return 2;
@@ -914,7 +915,7 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
                             const float* trans, const int32_t* last, const float* image_grad, float* accum,
                             float* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
-    const int variant = compositor_variant();
+    const int variant = compositor_variant(true);
     if (variant == 0 && grp_supported(ts))
         return launch_backward_grp(mode, n, tiles, ts, ranges, values, hdr, cull, tex, cc, rc, trans, last, image_grad,
                                    accum, grid_grad, st);
