@@ -18,7 +18,7 @@ if [ "${TESTS:-1}" = 1 ]; then
   echo "smoke exit $?" >> $O/smoke.log
 fi
 # variant names: grp (default, G=8), grp16 (G=16), direct, staged
-venv() { case $1 in grp16) echo "GB_COMPOSITOR=grp GB_GROUP=16";; grp4) echo "GB_COMPOSITOR=grp GB_GROUP=4";; fwd0) echo "GB_FWD_BATCH=0";; fwd12) echo "GB_FWD_BATCH=12";; grp16b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16";; grp16bu) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16 GB_GRP_TEXEL=uni";; grp8b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=8";; *) echo "GB_COMPOSITOR=$1";; esac; }
+venv() { case $1 in grp16) echo "GB_COMPOSITOR=grp GB_GROUP=16";; grp4) echo "GB_COMPOSITOR=grp GB_GROUP=4";; fwd0) echo "GB_FWD_BATCH=0";; fwd12) echo "GB_FWD_BATCH=12";; grp16b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16";; grp16bu) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16 GB_GRP_TEXEL=uni";; grp8b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=8";; perlane) echo "GB_DIRECT_TEXEL=perlane";; *) echo "GB_COMPOSITOR=$1";; esac; }
 for v in ${ALT_TESTS:-}; do
   env $(venv $v) timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "configs1 or pinhole_small or ortho_random or ragged" > $O/pytest_gpu_$v.log 2>&1
   echo "pytest exit $?" >> $O/pytest_gpu_$v.log
