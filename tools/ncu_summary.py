@@ -23,8 +23,13 @@ METRICS = [
     ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1/shared throughput %"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
     ("smsp__inst_executed_op_global_red.sum", "global red instructions"),
-    ("lts__t_requests_op_red.sum", "L2 red requests"),
-    ("lts__t_requests_op_atom.sum", "L2 atom requests"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "global red requests (L1)"),
+    ("l1tex__m_l1tex2xbar_write_sectors_mem_global_op_red.sum", "red sectors sent to L2"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("lts__t_requests_srcunit_tex_op_red.sum", "L2 red requests"),
+    ("lts__t_sectors_srcunit_tex_op_red.sum", "L2 red sectors"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("smsp__inst_executed.sum", "warp instructions"),
