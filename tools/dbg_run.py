@@ -1,4 +1,4 @@
-"""Print the K4 development counters for one configs[2]-like view (needs dbg/libgb_raster.so)."""
+"""Print the K4 development counters for one configs[2]-like view (needs tools/_dbg/libgb_raster.so from tools/dbg_counters.sh)."""
 import ctypes as C, os, sys
 os.environ["GB_LIB_PATH"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "_dbg", "libgb_raster.so")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
