@@ -49,6 +49,7 @@ typedef enum {
 
 typedef struct gb_context gb_context;
 typedef struct gb_binning gb_binning;
+typedef struct gb_graph gb_graph;
 
 /* ColorGridConfig (core.hpp:29-42) */
 typedef struct {
@@ -166,9 +167,25 @@ GB_API int64_t gb_context_launch_count(const gb_context *ctx);
 #define GB_K_CHAIN 7     /* K5  per-primitive gradient chain */
 #define GB_K_LOSS 8      /* K6  photometric loss */
 #define GB_K_ADAM 9      /* K7  Adam */
-#define GB_NUM_KERNEL_IDS 10
+#define GB_K_FUSED 10    /* K3+K6+K4 in one kernel (gb_render_loss_backward) */
+#define GB_NUM_KERNEL_IDS 11
 GB_API gb_status gb_context_profile(gb_context *ctx, int enable);
 GB_API gb_status gb_context_profile_read(gb_context *ctx, double *total_ms, int64_t *counts, int n);
+
+/* ---- CUDA graphs ------------------------------------------------------------
+ * Capture the work a host thread issues on ctxs[0]'s stream -- and on streams that fork from it and join
+ * back, e.g. other contexts' streams -- into one CUDA graph (stream capture, thread-local mode), so a
+ * training step's views replay with one launch.  Every launch site keeps its gb_context_profile timing:
+ * the capture turns its events into event-record nodes, and each profiled gb_graph_launch points them at
+ * fresh events of the context that issued the site.  Kernel counts (gb_context_launch_count) move from the
+ * capture to every launch.  Between begin and end the calls must not allocate or block (binnings in
+ * capacity mode; buffers already sized by an eager run).  No reference counterpart (the reference is a
+ * synchronous CPU library). */
+GB_API gb_status gb_graph_begin(gb_context *const *ctxs, int32_t n);
+GB_API gb_status gb_graph_end(gb_context *const *ctxs, int32_t n, gb_graph **out);
+/* Launch on the origin context's stream (asynchronous). */
+GB_API gb_status gb_graph_launch(gb_graph *g);
+GB_API gb_status gb_graph_destroy(gb_graph *g);
 
 /* ---- device memory helpers (so a C/C++ host needs no CUDA headers) -------- */
 GB_API gb_status gb_device_alloc(gb_context *ctx, uint64_t bytes, void **out);
@@ -187,6 +204,17 @@ GB_API gb_status gb_binning_destroy(gb_binning *b);
  * on the stream to learn the pair count P. */
 GB_API gb_status gb_build_binning(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_raster_config *cfg,
                            gb_binning *b);
+/* Capacity mode (capacity > 0): gb_build_binning stops reading the pair count P back to the host.  Its
+ * pair buffers hold `capacity` slots and the tile sort runs over all of them (unused slots carry a pad key
+ * that lands in no tile), so the tile lists are identical and the build never blocks -- it can run ahead
+ * of the GPU and be captured into a CUDA graph.  If a view has P > capacity, only the first `capacity`
+ * pairs in (depth, index) order are binned and *overflow (a device int32 the caller zeroes) is set to 1:
+ * grow the capacity and rebuild.  capacity = 0 restores the exactly-sized, blocking build.  No reference
+ * counterpart (build_binning sizes its lists on the host, raster.hpp:128-146). */
+GB_API gb_status gb_binning_set_capacity(gb_binning *b, int64_t capacity, int32_t *overflow);
+/* Stream-ordered copy of the last build's pair count P (uint32, before any capacity clamp) to device memory. */
+GB_API gb_status gb_binning_store_total(gb_context *ctx, const gb_binning *b, uint32_t *dst_device);
+/* total = P (in capacity mode this reads P back synchronously, clamped to the capacity). */
 GB_API gb_status gb_binning_info(const gb_binning *b, int32_t *tiles_x, int32_t *tiles_y, int64_t *total);
 /* Synchronous test hook: per-tile lists as CSR on the host
  * (offsets[tiles+1], values[total]) -- TileBinning::tiles. */
@@ -214,6 +242,19 @@ GB_API gb_status gb_l1_loss(gb_context *ctx, const float *color, const float *ta
 /* grad[i] = 2*scale*(color-target); *loss += scale*sum (color-target)^2. */
 GB_API gb_status gb_mse_loss(gb_context *ctx, const float *color, const float *target, int64_t n, float scale, float *grad,
                       float *loss);
+
+/* One view of a training step (train.hpp:120-133 around raster.hpp:201-371) in one pass:
+ *   gb_render_forward + gb_l1_loss (loss_kind GB_LOSS_L1) or gb_mse_loss (GB_LOSS_MSE) + gb_render_backward,
+ * each pixel's forward, loss cotangent and backward done by the same warp while the entries it walked are
+ * still cached.  target: HWC fp32 (device).  out: NULL, or forward buffers filled as gb_render_forward
+ * would; image_grad: NULL, or receives the cotangent; *loss (device float) += as the loss entry points
+ * (summation order differs); g receives the gradients as gb_render_backward.  Per-pixel arithmetic is the
+ * separate calls'; with GB_COMPOSITOR=grp|staged this runs as those three calls. */
+#define GB_LOSS_L1 0
+#define GB_LOSS_MSE 1
+GB_API gb_status gb_render_loss_backward(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_binning *b,
+                                         const float *target, int32_t loss_kind, float scale, gb_render_out *out,
+                                         float *image_grad, float *loss, gb_grads *g);
 
 /* ---- image metrics (metrics.hpp) ------------------------------------------- */
 /* ssim (metrics.hpp:183-185) with clamp01 = 1, ssim_with_gradient (metrics.hpp:189-191) with clamp01 = 0:

@@ -30,6 +30,7 @@ from .raster import (  # noqa: F401
     render,
     render_backward,
     render_forward,
+    render_loss_backward,
 )
 from .splat_io import SplatIoError, file_info, load_splats, save_splats  # noqa: F401
 

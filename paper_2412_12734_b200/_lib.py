@@ -25,7 +25,7 @@ GB_IO_ERROR = 7
 MODE_ORTHO = 0
 MODE_PINHOLE = 1
 
-KERNEL_NAMES = ("project", "scan", "duplicate", "sort", "ranges", "forward", "backward", "chain", "loss", "adam")
+KERNEL_NAMES = ("project", "scan", "duplicate", "sort", "ranges", "forward", "backward", "chain", "loss", "adam", "fused")
 
 
 class GridConfig(C.Structure):
@@ -163,6 +163,12 @@ _SIGS = {
     "gb_binning_destroy": (C.c_int, [P]),
     "gb_build_binning": (C.c_int, [P, C.POINTER(Splats), C.POINTER(Camera), C.POINTER(RasterConfigC), P]),
     "gb_binning_info": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "gb_binning_set_capacity": (C.c_int, [P, C.c_int64, P]),
+    "gb_graph_begin": (C.c_int, [P, C.c_int32]),
+    "gb_graph_end": (C.c_int, [P, C.c_int32, C.POINTER(P)]),
+    "gb_graph_launch": (C.c_int, [P]),
+    "gb_graph_destroy": (C.c_int, [P]),
+    "gb_binning_store_total": (C.c_int, [P, P, P]),
     "gb_binning_copy_to_host": (C.c_int, [P, P, P, P]),
     "gb_render_forward": (C.c_int, [P, C.POINTER(Splats), C.POINTER(Camera), P, C.POINTER(RenderOut)]),
     "gb_render_backward": (
@@ -170,6 +176,11 @@ _SIGS = {
         [P, C.POINTER(Splats), C.POINTER(Camera), P, C.POINTER(RenderOut), P, C.POINTER(Grads)],
     ),
     "gb_render": (C.c_int, [P, C.POINTER(Splats), C.POINTER(Camera), C.POINTER(RasterConfigC), P, C.POINTER(RenderOut)]),
+    "gb_render_loss_backward": (
+        C.c_int,
+        [P, C.POINTER(Splats), C.POINTER(Camera), P, P, C.c_int32, C.c_float, C.POINTER(RenderOut), P, P,
+         C.POINTER(Grads)],
+    ),
     "gb_l1_loss": (C.c_int, [P, P, P, C.c_int64, C.c_float, P, P]),
     "gb_mse_loss": (C.c_int, [P, P, P, C.c_int64, C.c_float, P, P]),
     "gb_adam_step": (

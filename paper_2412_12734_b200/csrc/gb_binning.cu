@@ -14,6 +14,12 @@
 // result equals one sort of 64-bit (tile << 32 | depth) keys, bit for bit.  It
 // replaces that 45-bit sort over P pairs (6 radix passes of 12 B records) with
 // a 32-bit sort over K primitives plus 2 passes of 8 B records over P pairs.
+//
+// Capacity mode (gb_binning_set_capacity): the host never reads P back.  The
+// pair buffers hold `cap` slots, k_pad fills slots [P, cap) with the pad key
+// n_tiles (one more key bit at most), the tile sort runs over all cap slots
+// and k_ranges ignores pad keys -- so the per-tile ranges are identical and
+// the whole build can be captured into a CUDA graph.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -33,31 +39,46 @@ __global__ void __launch_bounds__(256) k_gather_counts(int64_t K, const int32_t*
     if (i < K) out[i] = counts[perm[i]];
 }
 
+// cap: pair capacity of keys/values.  Pairs at or beyond it are dropped and flagged in *overflow
+// (capacity mode only; the blocking mode sizes the buffers to P exactly).
 __global__ void __launch_bounds__(256) k_duplicate(int64_t K, int tiles_x, const int32_t* __restrict__ perm,
                                                    const uint32_t* __restrict__ offsets,
                                                    const uint2* __restrict__ rects, uint32_t* __restrict__ keys,
-                                                   int32_t* __restrict__ values) {
+                                                   int32_t* __restrict__ values, uint32_t cap,
+                                                   int32_t* __restrict__ overflow) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= K) return;
-    const uint32_t end = offsets[i + 1];
+    const uint32_t end = min(offsets[i + 1], cap);
     uint32_t o = offsets[i];
-    if (o == end) return;
+    if (i == K - 1 && offsets[K] > cap && overflow) *overflow = 1;
+    if (o >= end) return;
     const int32_t k = perm[i];
     const uint2 r = rects[k];
     const int tx0 = r.x & 0xffff, ty0 = r.x >> 16, tx1 = r.y & 0xffff, ty1 = r.y >> 16;
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
+    for (int ty = ty0; ty <= ty1 && o < end; ++ty)
+        for (int tx = tx0; tx <= tx1 && o < end; ++tx) {
             keys[o] = (uint32_t)(ty * tiles_x + tx);
             values[o] = k;
             ++o;
         }
 }
 
+// capacity mode: slots [P, cap) get the pad tile key n_tiles, which sorts after every real tile
+__global__ void __launch_bounds__(256) k_pad(uint32_t cap, const uint32_t* __restrict__ total, uint32_t pad,
+                                             uint32_t* __restrict__ keys, int32_t* __restrict__ values) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cap || i < *total) return;
+    keys[i] = pad;
+    values[i] = -1;
+}
+
+// pairs with a pad key (>= n_tiles) belong to no tile
 __global__ void __launch_bounds__(256) k_ranges(int64_t P, const uint32_t* __restrict__ keys,
-                                                uint2* __restrict__ ranges) {
+                                                uint2* __restrict__ ranges, uint32_t n_tiles) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P) return;
     const uint32_t tile = keys[i];
+    if (tile >= n_tiles) return;
     if (i == 0 || keys[i - 1] != tile) ranges[tile].x = (uint32_t)i;
     if (i == P - 1 || keys[i + 1] != tile) ranges[tile].y = (uint32_t)(i + 1);
 }
@@ -66,6 +87,12 @@ static int bits_for(uint32_t v) {
     int b = 0;
     while (b < 32 && (1ull << b) < (uint64_t)v) ++b;
     return b;
+}
+
+// key bits covering tile keys 0 .. n_keys - 1 (n_keys = n_tiles, + 1 for the capacity mode's pad key)
+int tile_sort_bits(int n_keys) {
+    const int b = bits_for((uint32_t)n_keys);
+    return b ? b : 1;
 }
 
 size_t scan_temp_bytes(int64_t K) {
@@ -106,31 +133,33 @@ cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, cons
 }
 
 cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,
-                             uint32_t* keys, int32_t* values, cudaStream_t st) {
+                             uint32_t* keys, int32_t* values, uint32_t cap, int32_t* overflow, cudaStream_t st) {
     if (K == 0) return cudaSuccess;
-    k_duplicate<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, tiles_x, perm, offsets, rects, keys, values);
+    k_duplicate<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, tiles_x, perm, offsets, rects, keys, values, cap,
+                                                             overflow);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad(uint32_t cap, const uint32_t* total, int n_tiles, uint32_t* keys, int32_t* values,
+                       cudaStream_t st) {
+    if (cap == 0) return cudaSuccess;
+    k_pad<<<(cap + 255) / 256, 256, 0, st>>>(cap, total, (uint32_t)n_tiles, keys, values);
     return cudaGetLastError();
 }
 
 // Stable sort of (tile id, primitive) pairs on the tile-id bits.
 cudaError_t launch_tile_sort(void* temp, size_t temp_bytes, uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_in,
-                             int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st) {
+                             int32_t* vals_out, int64_t P, int n_keys, cudaStream_t st) {
     if (P == 0) return cudaSuccess;
-    int end_bit = bits_for((uint32_t)n_tiles);
-    if (end_bit == 0) end_bit = 1;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)P, 0, end_bit,
-                                           st);
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)P, 0,
+                                           tile_sort_bits(n_keys), st);
 }
 
-int tile_sort_bits(int n_tiles) {
-    const int b = bits_for((uint32_t)n_tiles);
-    return b ? b : 1;
-}
 
 cudaError_t launch_ranges(int64_t P, const uint32_t* keys, uint2* ranges, int n_tiles, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, st);
     if (e != cudaSuccess || P == 0) return e;
-    k_ranges<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, keys, ranges);
+    k_ranges<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, keys, ranges, (uint32_t)n_tiles);
     return cudaGetLastError();
 }
 

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "gb_internal.cuh"
@@ -16,15 +18,17 @@ namespace gb {
 size_t scan_temp_bytes(int64_t K);
 size_t sort_temp_bytes(int64_t n);
 int sort_launches(int bits);
-int tile_sort_bits(int n_tiles);
+int tile_sort_bits(int n_keys);
 cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* depth_bits, uint32_t* depth_sorted,
                               int32_t* iota, int32_t* perm, int64_t K, cudaStream_t st);
 cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
                         uint32_t* counts_sorted, uint32_t* offsets, int64_t K, cudaStream_t st);
 cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,
-                             uint32_t* keys, int32_t* values, cudaStream_t st);
+                             uint32_t* keys, int32_t* values, uint32_t cap, int32_t* overflow, cudaStream_t st);
+cudaError_t launch_pad(uint32_t cap, const uint32_t* total, int n_tiles, uint32_t* keys, int32_t* values,
+                       cudaStream_t st);
 cudaError_t launch_tile_sort(void* temp, size_t temp_bytes, uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_in,
-                             int32_t* vals_out, int64_t P, int n_tiles, cudaStream_t st);
+                             int32_t* vals_out, int64_t P, int n_keys, cudaStream_t st);
 cudaError_t launch_ranges(int64_t P, const uint32_t* keys, uint2* ranges, int n_tiles, cudaStream_t st);
 cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                            const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
@@ -118,7 +122,7 @@ struct gb_context {
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, counts_tmp, accum, adam_bad, ssim_tmp,
-        metric_tmp;
+        metric_tmp, fuse_color, fuse_trans, fuse_last, fuse_grad;
     uint32_t* pinned_total = nullptr;
     bool prof = false;
     std::vector<ProfRec> prof_recs;
@@ -137,20 +141,42 @@ cudaEvent_t prof_event(gb_context* ctx) {
     return e;
 }
 
-// Brackets one launch site with CUDA events on the context stream when profiling.
+// Launch sites recorded while gb_graph_begin's capture is open on this thread: each becomes a pair of
+// event-record nodes in the graph, re-pointed at fresh timing events on every profiled launch.
+struct CaptureSite {
+    gb_context* ctx;
+    int id;
+    cudaEvent_t start, stop;
+};
+thread_local std::vector<CaptureSite>* t_capture = nullptr;
+
+// Brackets one launch site with CUDA events on the context stream when profiling (or, inside a
+// gb_graph capture, always: the graph decides per launch whether the site is timed).
 struct ProfScope {
     gb_context* ctx;
     int id;
     cudaEvent_t start = nullptr;
+    bool graph = false;
     ProfScope(gb_context* c, int i) : ctx(c), id(i) {
-        if (ctx->prof) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(ctx->stream, &cap) != cudaSuccess) return;
+        if (cap != cudaStreamCaptureStatusNone) {
+            if (!t_capture) return;  // somebody else's capture: events would not time anything
+            graph = true;
+            start = prof_event(ctx);
+            cudaEventRecordWithFlags(start, ctx->stream, cudaEventRecordExternal);
+        } else if (ctx->prof) {
             start = prof_event(ctx);
             cudaEventRecord(start, ctx->stream);
         }
     }
     ~ProfScope() {
-        if (start) {
-            cudaEvent_t stop = prof_event(ctx);
+        if (!start) return;
+        cudaEvent_t stop = prof_event(ctx);
+        if (graph) {
+            cudaEventRecordWithFlags(stop, ctx->stream, cudaEventRecordExternal);
+            t_capture->push_back({ctx, id, start, stop});
+        } else {
             cudaEventRecord(stop, ctx->stream);
             ctx->prof_recs.push_back({id, start, stop});
         }
@@ -167,7 +193,9 @@ struct gb_binning {
     int tiles_x = 0, tiles_y = 0;
     int64_t K = 0;
     int n = 0;
-    int64_t P = 0;
+    int64_t P = 0;         // pair count; -1 = on the device only (capacity mode, not read back yet)
+    int64_t capacity = 0;  // > 0: capacity mode (no host read-back of P; see gb_binning_set_capacity)
+    int32_t* overflow = nullptr;
     DevBuf headers, cull, rects, counts, offsets, depth, perm, keys, values, ranges;
 };
 
@@ -349,6 +377,143 @@ gb_status gb_context_profile_read(gb_context* ctx, double* total_ms, int64_t* co
     return GB_OK;
 }
 
+// ---- CUDA graphs of context work (one training step's views) ----------------------------------
+struct gb_graph {
+    gb_context* origin = nullptr;
+    cudaGraph_t graph = nullptr;  // kept: the exec's event-record nodes are addressed through its nodes
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t dummy = nullptr;
+    struct Site {
+        gb_context* ctx;
+        int id;
+        cudaGraphNode_t start, stop;
+    };
+    std::vector<Site> sites;
+    std::vector<std::pair<gb_context*, int64_t>> launches;  // kernels per replay, per context
+};
+
+namespace {
+struct CaptureState {
+    std::vector<CaptureSite> sites;
+    std::vector<std::pair<gb_context*, int64_t>> launches0;
+};
+thread_local CaptureState* t_state = nullptr;
+}  // namespace
+
+gb_status gb_graph_begin(gb_context* const* ctxs, int32_t n) {
+    if (!ctxs || n < 1 || !ctxs[0]) return fail(GB_INVALID_ARGUMENT, "graph_begin: no context");
+    if (t_state) return fail(GB_INVALID_ARGUMENT, "graph_begin: a capture is already open on this thread");
+    if (gb_status st = set_device(ctxs[0])) return st;
+    auto* state = new CaptureState();
+    for (int i = 0; i < n; ++i)
+        if (ctxs[i]) state->launches0.push_back({ctxs[i], ctxs[i]->launches});
+    cudaError_t e = cudaStreamBeginCapture(ctxs[0]->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        delete state;
+        return fail(GB_CUDA_ERROR, "graph_begin: %s", cudaGetErrorString(e));
+    }
+    t_state = state;
+    t_capture = &state->sites;
+    return GB_OK;
+}
+
+gb_status gb_graph_end(gb_context* const* ctxs, int32_t n, gb_graph** out) {
+    if (!ctxs || n < 1 || !ctxs[0] || !out) return fail(GB_INVALID_ARGUMENT, "graph_end: bad argument");
+    if (!t_state) return fail(GB_INVALID_ARGUMENT, "graph_end: no capture open on this thread");
+    std::unique_ptr<CaptureState> state(t_state);
+    t_state = nullptr;
+    t_capture = nullptr;
+    *out = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(ctxs[0]->stream, &graph);
+    auto give_back = [&]() {
+        for (const CaptureSite& c : state->sites) {
+            c.ctx->prof_pool.push_back(c.start);
+            c.ctx->prof_pool.push_back(c.stop);
+        }
+    };
+    if (e != cudaSuccess) {
+        give_back();
+        return fail(GB_CUDA_ERROR, "graph_end: capture failed: %s", cudaGetErrorString(e));
+    }
+    std::unique_ptr<gb_graph> g(new gb_graph());
+    g->origin = ctxs[0];
+    // the capture launched nothing: move its launch counts from the contexts to the graph
+    for (auto& [c, l0] : state->launches0) {
+        g->launches.push_back({c, c->launches - l0});
+        c->launches = l0;
+    }
+    // map every site's events to their event-record nodes
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+    std::vector<std::pair<cudaEvent_t, cudaGraphNode_t>> rec;
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev = nullptr;
+        cudaGraphEventRecordNodeGetEvent(nd, &ev);
+        rec.push_back({ev, nd});
+    }
+    auto node_of = [&](cudaEvent_t ev) -> cudaGraphNode_t {
+        for (auto& r : rec)
+            if (r.first == ev) return r.second;
+        return nullptr;
+    };
+    for (const CaptureSite& c : state->sites) {
+        cudaGraphNode_t a = node_of(c.start), b = node_of(c.stop);
+        if (a && b) g->sites.push_back({c.ctx, c.id, a, b});
+    }
+    g->graph = graph;
+    e = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (e == cudaSuccess) e = cudaEventCreate(&g->dummy);
+    for (const auto& st : g->sites) {  // untimed until a profiled launch re-points them
+        if (e != cudaSuccess) break;
+        e = cudaGraphExecEventRecordNodeSetEvent(g->exec, st.start, g->dummy);
+        if (e == cudaSuccess) e = cudaGraphExecEventRecordNodeSetEvent(g->exec, st.stop, g->dummy);
+    }
+    give_back();
+    if (e != cudaSuccess) {
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        if (g->dummy) cudaEventDestroy(g->dummy);
+        cudaGraphDestroy(graph);
+        return fail(GB_CUDA_ERROR, "graph_end: %s", cudaGetErrorString(e));
+    }
+    *out = g.release();
+    return GB_OK;
+}
+
+gb_status gb_graph_launch(gb_graph* g) {
+    if (!g || !g->exec) return fail(GB_INVALID_ARGUMENT, "graph_launch: null graph");
+    if (gb_status st = set_device(g->origin)) return st;
+    for (const auto& st : g->sites) {
+        cudaEvent_t a = g->dummy, b = g->dummy;
+        if (st.ctx->prof) {
+            a = prof_event(st.ctx);
+            b = prof_event(st.ctx);
+            st.ctx->prof_recs.push_back({st.id, a, b});
+        }
+        GB_CUDA(cudaGraphExecEventRecordNodeSetEvent(g->exec, st.start, a));
+        GB_CUDA(cudaGraphExecEventRecordNodeSetEvent(g->exec, st.stop, b));
+    }
+    GB_CUDA(cudaGraphLaunch(g->exec, g->origin->stream));
+    for (auto& [c, l] : g->launches) c->launches += l;
+    return GB_OK;
+}
+
+gb_status gb_graph_destroy(gb_graph* g) {
+    if (!g) return GB_OK;
+    cudaSetDevice(g->origin->device);
+    cudaStreamSynchronize(g->origin->stream);
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    if (g->dummy) cudaEventDestroy(g->dummy);
+    delete g;
+    return GB_OK;
+}
+
 gb_status gb_device_alloc(gb_context* ctx, uint64_t bytes, void** out) {
     if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
     *out = nullptr;
@@ -470,12 +635,19 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
                                 ctx->counts_tmp.as<uint32_t>(), b->offsets.as<uint32_t>(), K, stream));
     }
     ctx->launches += K > 0 ? 3 : 0;  // gather + CUB scan (init + scan)
-    GB_CUDA(cudaMemcpyAsync(ctx->pinned_total, b->offsets.as<uint32_t>() + K, sizeof(uint32_t),
-                            cudaMemcpyDeviceToHost, stream));
-    GB_CUDA(cudaStreamSynchronize(stream));
-    const int64_t P = *ctx->pinned_total;
-    b->P = P;
+    int64_t P;  // pairs the sort and ranges run over: the exact count, or the capacity
+    if (b->capacity > 0) {
+        P = b->capacity;
+        b->P = -1;
+    } else {
+        GB_CUDA(cudaMemcpyAsync(ctx->pinned_total, b->offsets.as<uint32_t>() + K, sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, stream));
+        GB_CUDA(cudaStreamSynchronize(stream));
+        P = *ctx->pinned_total;
+        b->P = P;
+    }
     const int64_t Pc = P > 0 ? P : 1;
+    const int n_keys = n_tiles + (b->capacity > 0);
     GB_CUDA(b->keys.ensure(sizeof(uint32_t) * Pc));
     GB_CUDA(b->values.ensure(sizeof(int32_t) * Pc));
     GB_CUDA(ctx->keys_tmp.ensure(sizeof(uint32_t) * Pc));
@@ -486,25 +658,62 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
         ProfScope ps(ctx, GB_K_DUPLICATE);
         GB_CUDA(gb::launch_duplicate(K, b->tiles_x, b->perm.as<int32_t>(), b->offsets.as<uint32_t>(),
                                      b->rects.as<uint2>(), ctx->keys_tmp.as<uint32_t>(), ctx->vals_tmp.as<int32_t>(),
-                                     stream));
+                                     (uint32_t)P, b->overflow, stream));
+        if (b->capacity > 0)
+            GB_CUDA(gb::launch_pad((uint32_t)P, b->offsets.as<uint32_t>() + K, n_tiles, ctx->keys_tmp.as<uint32_t>(),
+                                   ctx->vals_tmp.as<int32_t>(), stream));
     }
     {
         ProfScope ps(ctx, GB_K_SORT);
         GB_CUDA(gb::launch_tile_sort(ctx->sort_temp.p, ctx->sort_temp.cap, ctx->keys_tmp.as<uint32_t>(),
                                      b->keys.as<uint32_t>(), ctx->vals_tmp.as<int32_t>(), b->values.as<int32_t>(), P,
-                                     n_tiles, stream));
+                                     n_keys, stream));
     }
     {
         ProfScope ps(ctx, GB_K_RANGES);
         GB_CUDA(gb::launch_ranges(P, b->keys.as<uint32_t>(), b->ranges.as<uint2>(), n_tiles, stream));
     }
-    ctx->launches += (K > 0) + (P > 0 ? 1 + gb::sort_launches(gb::tile_sort_bits(n_tiles)) : 0);
+    ctx->launches += (K > 0) + (b->capacity > 0) + (P > 0 ? 1 + gb::sort_launches(gb::tile_sort_bits(n_keys)) : 0);
     b->built = true;
+    return GB_OK;
+}
+
+namespace {
+// capacity mode: read the pair count back (synchronous); clamps to the capacity on overflow
+gb_status resolve_total(const gb_binning* b) {
+    if (b->P >= 0) return GB_OK;
+    gb_binning* m = const_cast<gb_binning*>(b);
+    if (gb_status st = set_device(b->ctx)) return st;
+    GB_CUDA(cudaMemcpyAsync(b->ctx->pinned_total, b->offsets.as<uint32_t>() + b->K, sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, b->ctx->stream));
+    GB_CUDA(cudaStreamSynchronize(b->ctx->stream));
+    m->P = std::min<int64_t>(*b->ctx->pinned_total, b->capacity);
+    return GB_OK;
+}
+}  // namespace
+
+gb_status gb_binning_set_capacity(gb_binning* b, int64_t capacity, int32_t* overflow) {
+    if (!b) return fail(GB_INVALID_ARGUMENT, "null binning");
+    if (capacity < 0 || capacity > 0xffffffffll) return fail(GB_INVALID_ARGUMENT, "binning capacity out of range");
+    b->capacity = capacity;
+    b->overflow = capacity > 0 ? overflow : nullptr;
+    b->built = false;
+    return GB_OK;
+}
+
+gb_status gb_binning_store_total(gb_context* ctx, const gb_binning* b, uint32_t* dst) {
+    if (!ctx || !b || !dst) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (!b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(cudaMemcpyAsync(dst, b->offsets.as<uint32_t>() + b->K, sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
     return GB_OK;
 }
 
 gb_status gb_binning_info(const gb_binning* b, int32_t* tiles_x, int32_t* tiles_y, int64_t* total) {
     if (!b || !b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    if (total)
+        if (gb_status st = resolve_total(b)) return st;
     if (tiles_x) *tiles_x = b->tiles_x;
     if (tiles_y) *tiles_y = b->tiles_y;
     if (total) *total = b->P;
@@ -513,6 +722,7 @@ gb_status gb_binning_info(const gb_binning* b, int32_t* tiles_x, int32_t* tiles_
 
 gb_status gb_binning_copy_to_host(gb_context* ctx, const gb_binning* b, int64_t* offsets, int32_t* values) {
     if (!ctx || !b || !b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    if (gb_status st = resolve_total(b)) return st;
     if (gb_status st = set_device(ctx)) return st;
     const int n_tiles = b->tiles_x * b->tiles_y;
     std::string tmp(sizeof(uint2) * (size_t)n_tiles, '\0');
@@ -628,6 +838,86 @@ gb_status gb_mse_loss(gb_context* ctx, const float* color, const float* target, 
     ProfScope ps(ctx, GB_K_LOSS);
     GB_CUDA(gb::launch_loss(1, color, target, n, scale, grad, loss, ctx->sm_count, ctx->stream));
     ctx->launches += n > 0;
+    return GB_OK;
+}
+
+gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_camera* cam, const gb_binning* b,
+                                  const float* target, int32_t loss_kind, float scale, gb_render_out* out,
+                                  float* image_grad, float* loss, gb_grads* g) {
+    if (!ctx || !b || !g || !target) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (loss_kind != GB_LOSS_L1 && loss_kind != GB_LOSS_MSE)
+        return fail(GB_INVALID_ARGUMENT, "render_loss_backward: unknown loss kind");
+    if (gb_status st = validate_camera(cam)) return st;
+    if (gb_status st = validate_splats(s, cam->mode)) return st;
+    if (!b->built) return fail(GB_INVALID_ARGUMENT, "binning not built");
+    if (b->width != cam->width || b->height != cam->height || b->mode != cam->mode)
+        return fail(GB_MISMATCH, "render_loss_backward: binning built for different image size");
+    if (b->K != s->count || b->n != s->grid.n)
+        return fail(GB_MISMATCH, "render_loss_backward: binning built for a different splat set");
+    if (out) {
+        if (out->width != cam->width || out->height != cam->height)
+            return fail(GB_MISMATCH, "render_loss_backward: output buffers sized for a different image");
+        if (!out->color || !out->final_transmittance || !out->last_rank)
+            return fail(GB_INVALID_ARGUMENT, "render_loss_backward: null output buffer");
+    }
+    if (s->count > 0 && (!g->position || !g->log_scale || !g->opacity_logit || !g->grid_values ||
+                         (cam->mode == GB_MODE_ORTHO && !g->theta) || (cam->mode == GB_MODE_PINHOLE && !g->quat)))
+        return fail(GB_INVALID_ARGUMENT, "render_loss_backward: null gradient buffer");
+    if (gb_status st = set_device(ctx)) return st;
+    const int64_t npix = (int64_t)cam->width * cam->height;
+    if (!gb::fused_available()) {  // the three separate calls, with context scratch for what the caller skipped
+        gb_render_out tmp{};
+        if (!out) {
+            GB_CUDA(ctx->fuse_color.ensure(sizeof(float) * 3 * npix));
+            GB_CUDA(ctx->fuse_trans.ensure(sizeof(float) * npix));
+            GB_CUDA(ctx->fuse_last.ensure(sizeof(int32_t) * npix));
+            tmp.color = ctx->fuse_color.as<float>();
+            tmp.final_transmittance = ctx->fuse_trans.as<float>();
+            tmp.last_rank = ctx->fuse_last.as<int32_t>();
+            tmp.width = cam->width;
+            tmp.height = cam->height;
+            out = &tmp;
+        }
+        if (!image_grad) {
+            GB_CUDA(ctx->fuse_grad.ensure(sizeof(float) * 3 * npix));
+            image_grad = ctx->fuse_grad.as<float>();
+        }
+        if (gb_status st = gb_render_forward(ctx, s, cam, b, out)) return st;
+        if (gb_status st = (loss_kind == GB_LOSS_L1 ? gb_l1_loss : gb_mse_loss)(ctx, out->color, target, 3 * npix,
+                                                                              scale, image_grad, loss))
+            return st;
+        return gb_render_backward(ctx, s, cam, b, out, image_grad, g);
+    }
+    cudaStream_t stream = ctx->stream;
+    const int64_t K = s->count;
+    if (K > 0) {
+        GB_CUDA(ctx->accum.ensure(sizeof(float) * gb::kAccumStride * K));
+        GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(float) * gb::kAccumStride * K, stream));
+    }
+    const gb::CamConst cc = make_cam_const(cam);
+    const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+    {
+        ProfScope ps(ctx, GB_K_FUSED);
+        GB_CUDA(gb::launch_fused(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
+                                 b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
+                                 b->cull.as<gb::CullRec>(), s->grid_values, cc, rc, loss_kind, target, scale,
+                                 out ? out->color : nullptr, out ? out->final_transmittance : nullptr,
+                                 out ? out->last_rank : nullptr, image_grad, loss,
+                                 K > 0 ? ctx->accum.as<float>() : nullptr, g->grid_values, stream));
+    }
+    ctx->launches += 1;
+    if (out) {
+        out->splat_count = s->count;
+        out->grid_n = s->grid.n;
+        out->tile_size = b->cfg.tile_size;
+    }
+    if (K == 0) return GB_OK;
+    gb::ProjParams pp = gb::make_proj_params(s, cam, &b->cfg, b->tiles_x, b->tiles_y);
+    {
+        ProfScope ps(ctx, GB_K_CHAIN);
+        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
+    }
+    ctx->launches += 1;
     return GB_OK;
 }
 

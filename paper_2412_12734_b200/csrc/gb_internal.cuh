@@ -189,6 +189,14 @@ cudaError_t launch_backward_grp(int mode, int n, int tiles, int ts, const uint2*
                                 const float* trans, const int32_t* last, const float* image_grad, float* accum,
                                 float* grid_grad, cudaStream_t st);
 
+// gb_raster.cu: K3 + K6 + K4 in one kernel (direct compositors only)
+bool fused_available();
+cudaError_t launch_fused(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                         const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                         const RasterConst& rc, int kind, const float* target, float scale, float* color, float* trans,
+                         int32_t* last, float* image_grad, float* loss, float* accum, float* grid_grad,
+                         cudaStream_t st);
+
 __device__ __forceinline__ uint32_t float_order_key(float d) {
     uint32_t b = __float_as_uint(d == 0.0f ? 0.0f : d);  // -0 sorts as +0 (double compare)
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);

@@ -632,40 +632,62 @@ __global__ void __launch_bounds__(288, 4) k_backward(const uint2* __restrict__ r
 // ---------------------------------------------------------------------------
 // Direct variants (no shared-memory staging): each warp walks the tile list on
 // its own, reading ids, headers and texels through L1 (__ldg).  No producer,
-// no CTA-level synchronisation; warps finish independently.
+// no CTA-level synchronisation; warps finish independently.  The walks are
+// device functions shared by the forward, the backward and the fused
+// forward + loss + backward kernel, so all three run the same arithmetic.
 // ---------------------------------------------------------------------------
-template <int MODE, int NT>
-__global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict__ ranges,
-                                                        const int32_t* __restrict__ values,
-                                                        const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
-                                                        const float* __restrict__ tex, const CamConst cc,
-                                                        const RasterConst rc, int n_rt, float* __restrict__ out_color,
-                                                        float* __restrict__ out_trans, int32_t* __restrict__ out_last) {
-    const int N = tex_n<NT>(n_rt);
-    const int F = 3 * N * N;
+struct WarpPixel {
+    int x, y;
+    bool inside;
+    float bx0, bx1, by0, by1;  // the warp's pixel rectangle
+};
+
+__device__ __forceinline__ WarpPixel warp_pixel(const RasterConst& rc, const CamConst& cc, int tile) {
+    WarpPixel w;
     const int ts = rc.tile_size;
-    const int lane = threadIdx.x & 31;
-    const int tile = blockIdx.x;
-    const uint2 range = ranges[tile];
-    const int total = (int)(range.y - range.x);
     const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
     int lx, ly;
     tile_pixel(threadIdx.x, ts, lx, ly);
-    const int x = tx * ts + lx, y = ty * ts + ly;
-    const bool inside = (int)threadIdx.x < ts * ts && x < cc.width && y < cc.height;
-    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
-    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
-    float T = 1.0f, acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
-    int last = -1;
-    bool done = !inside;
+    w.x = tx * ts + lx;
+    w.y = ty * ts + ly;
+    w.inside = (int)threadIdx.x < ts * ts && w.x < cc.width && w.y < cc.height;
+    w.bx0 = (float)__reduce_min_sync(kFull, w.x);
+    w.bx1 = (float)__reduce_max_sync(kFull, w.x);
+    w.by0 = (float)__reduce_min_sync(kFull, w.y);
+    w.by1 = (float)__reduce_max_sync(kFull, w.y);
+    return w;
+}
+
+// one lane's test of list entry `idl` against its warp's rectangle: exact alpha-skip ellipse (K1) or,
+// with a null cull array, the alpha-box
+__device__ __forceinline__ bool entry_meets_warp(const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
+                                                 int idl, const WarpPixel& w) {
+    return cull ? ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), w.bx0 - 0.05f, w.bx1 + 0.05f,
+                                     w.by0 - 0.05f, w.by1 + 0.05f)
+                : !box_miss(__ldg(&hdr[idl].h3), w.bx0, w.bx1, w.by0, w.by1);
+}
+
+// render_forward's per-pixel loop (raster.hpp:237-250) for the calling warp's pixels
+template <int MODE, int NT>
+__device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __restrict__ values,
+                                         const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
+                                         const float* __restrict__ tex, const RasterConst& rc, int N,
+                                         const WarpPixel& wp, float& T, float& acc0, float& acc1, float& acc2,
+                                         int& last) {
+    const int F = 3 * N * N;
+    const int lane = threadIdx.x & 31;
+    const int total = (int)(range.y - range.x);
+    const int x = wp.x, y = wp.y;
+    T = 1.0f;
+    acc0 = acc1 = acc2 = 0.0f;
+    last = -1;
+    bool done = !wp.inside;
     for (int c0 = 0; c0 < total && !__all_sync(kFull, done); c0 += 32) {
         int idl = -1;
         bool pass = false;
         if (c0 + lane < total) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = cull ? ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f,
-                                             by0 - 0.05f, by1 + 0.05f)
-                        : !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+            pass = entry_meets_warp(hdr, cull, idl, wp);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         while (mask) {
@@ -687,8 +709,8 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
                 }
                 if (hit) {
                     const float G = gauss_weight(u, v);
-                    const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);
-                    if (!(alpha < rc.alpha_skip)) {
+                    const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);  // raster.hpp:241
+                    if (!(alpha < rc.alpha_skip)) {                                // raster.hpp:242
                         const float* t = tex + (size_t)id * F;
                         float c0_, c1_, c2_;
                         if (N == 1) {
@@ -706,75 +728,39 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
                             c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
                                   __ldg(p10 + 5) * b.w11;
                         }
-                        const float w = alpha * T;
+                        const float w = alpha * T;  // raster.hpp:244-249
                         acc0 = fmaf(c0_, w, acc0);
                         acc1 = fmaf(c1_, w, acc1);
                         acc2 = fmaf(c2_, w, acc2);
                         T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
                         last = c0 + bit;
-                        if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;
+                        if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;  // raster.hpp:250
                     }
                 }
             }
             if (__all_sync(kFull, done)) break;
         }
     }
-    if (inside) {
-        const size_t p = (size_t)y * cc.width + x;
-        out_color[p * 3 + 0] = fmaf(T, cc.bg[0], acc0);
-        out_color[p * 3 + 1] = fmaf(T, cc.bg[1], acc1);
-        out_color[p * 3 + 2] = fmaf(T, cc.bg[2], acc2);
-        out_trans[p] = T;
-        out_last[p] = last;
-    }
 }
 
+// render_backward's per-pixel loop (raster.hpp:313-364) for the calling warp's pixels
 template <int MODE, int NT>
-__global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict__ ranges,
-                                                         const int32_t* __restrict__ values,
-                                                         const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
-                                                         const float* __restrict__ tex, const CamConst cc,
-                                                         const RasterConst rc, int n_rt,
-                                                         const float* __restrict__ in_trans,
-                                                         const int32_t* __restrict__ in_last,
-                                                         const float* __restrict__ image_grad,
-                                                         float* __restrict__ accum, float* __restrict__ grid_grad) {
-    extern __shared__ __align__(16) float red_scratch[];
-    const int N = tex_n<NT>(n_rt);
+__device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __restrict__ values,
+                                         const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
+                                         const float* __restrict__ tex, const CamConst& cc, const RasterConst& rc,
+                                         int N, const WarpPixel& wp, int last, float T, float g0, float g1, float g2,
+                                         float* wscratch, float* __restrict__ accum, float* __restrict__ grid_grad) {
     const int F = 3 * N * N;
-    const int ts = rc.tile_size;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x;
-    const uint2 range = ranges[tile];
-    const int tx = tile % rc.tiles_x, ty = tile / rc.tiles_x;
-    int lx, ly;
-    tile_pixel(threadIdx.x, ts, lx, ly);
-    const int x = tx * ts + lx, y = ty * ts + ly;
-    const bool inside = (int)threadIdx.x < ts * ts && x < cc.width && y < cc.height;
-    int last = -1;
-    float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
-    if (inside) {  // raster.hpp:313-322
-        const size_t p = (size_t)y * cc.width + x;
-        last = in_last[p];
-        g0 = image_grad[p * 3 + 0];
-        g1 = image_grad[p * 3 + 1];
-        g2 = image_grad[p * 3 + 2];
-        T = in_trans[p];
-        if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) last = -1;
-    }
+    const int lane = threadIdx.x & 31;
+    if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) last = -1;  // raster.hpp:315-317
     float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
-    const float bx0 = (float)__reduce_min_sync(kFull, x), bx1 = (float)__reduce_max_sync(kFull, x);
-    const float by0 = (float)__reduce_min_sync(kFull, y), by1 = (float)__reduce_max_sync(kFull, y);
     const int wlast = __reduce_max_sync(kFull, last);
-    float* wscratch = red_scratch + warp * kRedRows * kRedStride;
     for (int c0 = wlast & ~31; c0 >= 0; c0 -= 32) {
         int idl = -1;
         bool pass = false;
         if (c0 + lane <= wlast) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = cull ? ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), bx0 - 0.05f, bx1 + 0.05f,
-                                             by0 - 0.05f, by1 + 0.05f)
-                        : !box_miss(__ldg(&hdr[idl].h3), bx0, bx1, by0, by1);
+            pass = entry_meets_warp(hdr, cull, idl, wp);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         if (lane == 0) GB_DBG(1, __popc(mask));
@@ -786,10 +772,119 @@ __global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict
             h.h0 = __ldg(&hdr[id].h0);
             h.h1 = __ldg(&hdr[id].h1);
             h.h2 = __ldg(&hdr[id].h2);
-            bwd_entry<MODE, NT>(h, tex + (size_t)id * F, id, c0 + bit, last, x, y, T, g0, g1, g2, bh0, bh1, bh2, rc,
-                                N, lane, wscratch, accum, grid_grad);
+            bwd_entry<MODE, NT>(h, tex + (size_t)id * F, id, c0 + bit, last, wp.x, wp.y, T, g0, g1, g2, bh0, bh1,
+                                bh2, rc, N, lane, wscratch, accum, grid_grad);
         }
     }
+}
+
+template <int MODE, int NT>
+__global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict__ ranges,
+                                                        const int32_t* __restrict__ values,
+                                                        const ScreenHeader* __restrict__ hdr,
+                                                        const CullRec* __restrict__ cull, const float* __restrict__ tex,
+                                                        const CamConst cc, const RasterConst rc, int n_rt,
+                                                        float* __restrict__ out_color, float* __restrict__ out_trans,
+                                                        int32_t* __restrict__ out_last) {
+    const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
+    float T, a0, a1, a2;
+    int last;
+    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
+    if (wp.inside) {  // raster.hpp:253-254
+        const size_t p = (size_t)wp.y * cc.width + wp.x;
+        out_color[p * 3 + 0] = fmaf(T, cc.bg[0], a0);
+        out_color[p * 3 + 1] = fmaf(T, cc.bg[1], a1);
+        out_color[p * 3 + 2] = fmaf(T, cc.bg[2], a2);
+        out_trans[p] = T;
+        out_last[p] = last;
+    }
+}
+
+template <int MODE, int NT>
+__global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict__ ranges,
+                                                         const int32_t* __restrict__ values,
+                                                         const ScreenHeader* __restrict__ hdr,
+                                                         const CullRec* __restrict__ cull, const float* __restrict__ tex,
+                                                         const CamConst cc, const RasterConst rc, int n_rt,
+                                                         const float* __restrict__ in_trans,
+                                                         const int32_t* __restrict__ in_last,
+                                                         const float* __restrict__ image_grad,
+                                                         float* __restrict__ accum, float* __restrict__ grid_grad) {
+    extern __shared__ __align__(16) float red_scratch[];
+    const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
+    int last = -1;
+    float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
+    if (wp.inside) {  // raster.hpp:313-322
+        const size_t p = (size_t)wp.y * cc.width + wp.x;
+        last = in_last[p];
+        g0 = image_grad[p * 3 + 0];
+        g1 = image_grad[p * 3 + 1];
+        g2 = image_grad[p * 3 + 2];
+        T = in_trans[p];
+    }
+    bwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1, g2,
+                       red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad);
+}
+
+// render_forward + the photometric loss (KIND 0 = L1, 1 = MSE; K6) + render_backward of one view in one
+// kernel.  Every warp composites its pixels, turns them into the loss cotangent in registers and walks the
+// same entries back to front while their headers and texels are still in L1/L2; colour, transmittance,
+// last rank and the cotangent are stored only when asked for.
+template <int MODE, int NT, int KIND>
+__global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ ranges,
+                                                      const int32_t* __restrict__ values,
+                                                      const ScreenHeader* __restrict__ hdr,
+                                                      const CullRec* __restrict__ cull, const float* __restrict__ tex,
+                                                      const CamConst cc, const RasterConst rc, int n_rt,
+                                                      const float* __restrict__ target, float scale,
+                                                      float* __restrict__ out_color, float* __restrict__ out_trans,
+                                                      int32_t* __restrict__ out_last, float* __restrict__ out_grad,
+                                                      float* __restrict__ loss, float* __restrict__ accum,
+                                                      float* __restrict__ grid_grad) {
+    extern __shared__ __align__(16) float red_scratch[];
+    const int N = tex_n<NT>(n_rt);
+    const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
+    const uint2 range = ranges[blockIdx.x];
+    float T, a0, a1, a2;
+    int last;
+    fwd_walk<MODE, NT>(range, values, hdr, cull, tex, rc, N, wp, T, a0, a1, a2, last);
+    float g0 = 0.0f, g1 = 0.0f, g2 = 0.0f, l = 0.0f;
+    if (wp.inside) {
+        const size_t p = (size_t)wp.y * cc.width + wp.x;
+        const float c[3] = {fmaf(T, cc.bg[0], a0), fmaf(T, cc.bg[1], a1), fmaf(T, cc.bg[2], a2)};
+        float g[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {  // K6 (gb_misc.cu k_loss), per pixel
+            const float d = c[ch] - target[p * 3 + ch];
+            if (KIND == 0) {
+                l += fabsf(d);
+                g[ch] = scale * (float)((d > 0.0f) - (d < 0.0f));
+            } else {
+                l = fmaf(d, d, l);
+                g[ch] = 2.0f * scale * d;
+            }
+        }
+        g0 = g[0];
+        g1 = g[1];
+        g2 = g[2];
+        if (out_color) {
+            out_color[p * 3 + 0] = c[0];
+            out_color[p * 3 + 1] = c[1];
+            out_color[p * 3 + 2] = c[2];
+            out_trans[p] = T;
+            out_last[p] = last;
+        }
+        if (out_grad) {
+            out_grad[p * 3 + 0] = g0;
+            out_grad[p * 3 + 1] = g1;
+            out_grad[p * 3 + 2] = g2;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
+    if ((threadIdx.x & 31) == 0 && loss && l != 0.0f) atomicAdd(loss, l * scale);
+    bwd_walk<MODE, NT>(range, values, hdr, cull, tex, cc, rc, N, wp, last, T, g0, g1, g2,
+                       red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad);
 }
 
 // ---------------------------------------------------------------------------
@@ -938,6 +1033,45 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
     } else {
         GB_DISPATCH_N(bwd_t, GB_MODE_PINHOLE, tiles, threads, smem, st, ranges, values, hdr, tex, cc, rc, n, B,
                       trans, last, image_grad, accum, grid_grad)
+    }
+}
+
+template <int MODE, int NT>
+static cudaError_t fused_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
+                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                           const RasterConst& rc, int n, int kind, const float* target, float scale, float* color,
+                           float* trans, int32_t* last, float* image_grad, float* loss, float* accum,
+                           float* grid_grad) {
+    const size_t smem = (size_t)(threads / 32) * kRedRows * kRedStride * 4;
+    if (tune_env("GB_CULL_BOX", 0)) cull = nullptr;
+    if (kind == 0)
+        k_fused_direct<MODE, NT, 0><<<tiles, threads, smem, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, target,
+                                                                  scale, color, trans, last, image_grad, loss, accum,
+                                                                  grid_grad);
+    else
+        k_fused_direct<MODE, NT, 1><<<tiles, threads, smem, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, target,
+                                                                  scale, color, trans, last, image_grad, loss, accum,
+                                                                  grid_grad);
+    return cudaGetLastError();
+}
+
+// true when launch_fused runs (the direct compositors are selected); otherwise the caller composes
+// launch_forward + launch_loss + launch_backward
+bool fused_available() { return compositor_variant() == 1 && compositor_variant(true) == 1 && !getenv("GB_NO_FUSE"); }
+
+cudaError_t launch_fused(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                         const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                         const RasterConst& rc, int kind, const float* target, float scale, float* color, float* trans,
+                         int32_t* last, float* image_grad, float* loss, float* accum, float* grid_grad,
+                         cudaStream_t st) {
+    if (tiles == 0) return cudaSuccess;
+    const int threads = ((ts * ts + 31) / 32) * 32;
+    if (mode == GB_MODE_ORTHO) {
+        GB_DISPATCH_N(fused_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, kind,
+                      target, scale, color, trans, last, image_grad, loss, accum, grid_grad)
+    } else {
+        GB_DISPATCH_N(fused_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, kind,
+                      target, scale, color, trans, last, image_grad, loss, accum, grid_grad)
     }
 }
 

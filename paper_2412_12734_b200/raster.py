@@ -103,6 +103,50 @@ def all_contexts(device=None) -> list:
     return _Context.all(device if device is not None else "cuda")
 
 
+def copy_h2d(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """Stream-ordered copy of host ``src`` into the front of device ``dst`` on the current stream
+    (gb_copy_h2d; asynchronous when ``src`` is pinned)."""
+    nbytes = src.numel() * src.element_size()
+    if nbytes > dst.numel() * dst.element_size():
+        raise ValueError("copy_h2d: destination too small")
+    check(lib.gb_copy_h2d(context(dst.device).handle, C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()),
+                          nbytes, 0), "copy_h2d")
+
+
+class StepGraph:
+    """A CUDA graph of C-ABI work (gb_graph_*): capture() records what ``fn`` issues on the first
+    context's stream and the streams that fork from and join back into it; launch() replays it on
+    that stream.  Per-kernel profiling and launch counts of the contexts keep working across replays."""
+
+    def __init__(self, contexts: list):
+        self._ctxs = (C.c_void_p * len(contexts))(*[c.handle.value for c in contexts])
+        self._keep = list(contexts)
+        self.handle = None
+
+    def capture(self, fn) -> None:
+        check(lib.gb_graph_begin(self._ctxs, len(self._keep)), "gb_graph_begin")
+        err = None
+        try:
+            fn()
+        except BaseException as e:  # the capture must be closed either way
+            err = e
+        h = C.c_void_p()
+        st = lib.gb_graph_end(self._ctxs, len(self._keep), C.byref(h))
+        if err is not None:
+            raise err
+        check(st, "gb_graph_end")
+        self.handle = h
+
+    def launch(self) -> None:
+        check(lib.gb_graph_launch(self.handle), "gb_graph_launch")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            lib.gb_graph_destroy(h)
+            self.handle = None
+
+
 # --------------------------------------------------------------------------------------------
 # configs and cameras
 # --------------------------------------------------------------------------------------------
@@ -330,22 +374,36 @@ class TileBinning:
             lib.gb_binning_destroy(h)
             self.handle = None
 
-    def info(self):
-        tx, ty, total = C.c_int32(), C.c_int32(), C.c_int64()
-        check(lib.gb_binning_info(self.handle, C.byref(tx), C.byref(ty), C.byref(total)), "gb_binning_info")
-        return tx.value, ty.value, total.value
+    def info(self, total=True):
+        tx, ty, tot = C.c_int32(), C.c_int32(), C.c_int64(-1)
+        check(lib.gb_binning_info(self.handle, C.byref(tx), C.byref(ty), C.byref(tot) if total else None),
+              "gb_binning_info")
+        return tx.value, ty.value, tot.value
 
     @property
     def tiles_x(self) -> int:
-        return self.info()[0]
+        return self.info(False)[0]
 
     @property
     def tiles_y(self) -> int:
-        return self.info()[1]
+        return self.info(False)[1]
 
     def tile_count(self) -> int:
-        tx, ty, _ = self.info()
+        tx, ty, _ = self.info(False)
         return tx * ty
+
+    def set_capacity(self, capacity: int, overflow: torch.Tensor = None) -> None:
+        """Capacity mode (gb_binning_set_capacity): builds never read the pair count back, so they
+        run ahead of the GPU and can be captured into a CUDA graph.  ``overflow`` (a zeroed device
+        int32 tensor) is set to 1 by a build with more than ``capacity`` pairs.  0 = blocking mode."""
+        self._overflow = overflow  # keep alive
+        check(lib.gb_binning_set_capacity(self.handle, int(capacity), _ptr(overflow)), "gb_binning_set_capacity")
+
+    def store_total(self, dst: torch.Tensor) -> None:
+        """Stream-ordered copy of the last build's pair count into ``dst`` (a 1-element int32 device tensor)."""
+        if dst.dtype != torch.int32 or dst.numel() != 1:
+            raise TypeError("store_total: expected a 1-element int32 tensor")
+        check(lib.gb_binning_store_total(self.ctx.handle, self.handle, _ptr(dst)), "gb_binning_store_total")
 
     @property
     def total(self) -> int:
@@ -430,6 +488,36 @@ def render_backward(splats: SplatSet, camera, binning: TileBinning, output: Rend
     check(lib.gb_render_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(output._c),
                                  _ptr(image_grad), C.byref(g)), "render_backward")
     return grads
+
+
+def render_loss_backward(splats: SplatSet, camera, binning: TileBinning, target: torch.Tensor, loss: str = "l1",
+                         scale: float = None, grads: GradientBuffer = None, loss_acc: torch.Tensor = None,
+                         output: RenderOutput = None, image_grad: torch.Tensor = None):
+    """render_forward + l1_loss / mse_loss + render_backward of one view in one pass
+    (train.hpp:120-133 around raster.hpp:201-387).  Returns (loss_acc, grads); ``loss_acc``
+    (a device float, zero by default) and ``grads`` accumulate.  ``output`` / ``image_grad``,
+    when given, receive the forward buffers and the loss cotangent."""
+    kinds = {"l1": 0, "mse": 1}
+    if loss not in kinds:
+        raise ValueError(f"render_loss_backward: unknown loss {loss!r}")
+    ctx = context(splats.device)
+    n = camera.width * camera.height * 3
+    if target.numel() != n:
+        raise ValueError("render_loss_backward: dimension mismatch")
+    scale = 1.0 / n if scale is None else scale
+    if grads is None:
+        grads = GradientBuffer(splats)
+    if loss_acc is None:
+        loss_acc = torch.zeros((), dtype=torch.float32, device=splats.device)
+    if image_grad is not None and image_grad.numel() != n:
+        raise ValueError("render_loss_backward: image_grad size mismatch")
+    target = target.contiguous()
+    s, cam, g = splats.to_c(), camera.to_c(), grads.to_c()
+    check(lib.gb_render_loss_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, _ptr(target),
+                                      kinds[loss], scale, C.byref(output._c) if output is not None else None,
+                                      _ptr(image_grad) if image_grad is not None else None, _ptr(loss_acc),
+                                      C.byref(g)), "render_loss_backward")
+    return loss_acc, grads
 
 
 def render(splats: SplatSet, camera, config: RasterConfig = None) -> RenderOutput:

@@ -2,7 +2,8 @@
 
 Each rank owns a fixed subset of camera views and replicated primitives.  Per
 step and per owned view it runs, on one CUDA stream, K1 projection -> K2 tile
-binning -> K3 forward -> K6 L1 loss -> K4/K5 backward, accumulating into one
+binning -> K3 forward + K6 L1 loss + K4 backward (one fused kernel by default;
+``fused=False`` runs the three reference-shaped calls) -> K5, accumulating into one
 flat fp32 gradient buffer; then ONE collective (NCCL all-reduce, sum) makes
 the gradients identical on every rank and K7 Adam updates the replicated
 parameters.  This is the only cross-GPU exchange of the path.
@@ -18,8 +19,8 @@ from typing import List, Optional, Sequence
 import torch
 
 from .raster import (AdamConfig, AdamState, GradientBuffer, LearningRates, RasterConfig, RenderOutput, SplatSet,
-                     TileBinning, adam_step, all_contexts, build_binning, l1_loss, render_backward,
-                     render_forward)
+                     StepGraph, TileBinning, adam_step, all_contexts, build_binning, context, l1_loss,
+                     copy_h2d, render_backward, render_forward, render_loss_backward)
 
 
 def shard_views(n_views: int, rank: int, world: int, per_rank: Optional[int] = None) -> List[int]:
@@ -61,7 +62,8 @@ class ViewShardedTrainer:
 
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
-                 lanes: int = 2):
+                 lanes: int = 2, fused: bool = False, async_binning: bool = True, graph: bool = False,
+                 capacity_margin: float = 1.25):
         self.splats = splats
         self.cameras = list(cameras)
         self.views = list(views)
@@ -71,8 +73,10 @@ class ViewShardedTrainer:
         self.state = AdamState(splats, adam)
         self.pg = process_group
         self.check_finite = check_finite
+        self.fused = fused
         dev = splats.device
-        main = torch.cuda.current_stream(dev)
+        # lane 0 is the caller's stream, except under graph capture (which needs a side stream)
+        main = torch.cuda.Stream(device=dev) if graph else torch.cuda.current_stream(dev)
         self._lanes = [_Lane(dev, main if i == 0 else torch.cuda.Stream(device=dev)) for i in range(max(1, lanes))]
         self.binning = self._lanes[0].binning
         W = max(self.cameras[v].width for v in self.views) if self.views else 1
@@ -84,7 +88,22 @@ class ViewShardedTrainer:
         self._copy_done = [torch.cuda.Event() for _ in range(2)]
         self._buf_free = [torch.cuda.Event() for _ in range(2)]
         self._step_start = torch.cuda.Event()
-        self.pairs: List[int] = []  # tile/primitive pair count P of every view binned (roofline bytes)
+        self.pairs: List[int] = []  # blocking mode: pair count P of every view binned (roofline bytes)
+        # capacity mode (async_binning): after one blocking step sizes the pair buffers, builds never read P
+        # back; a device flag reports a view that outgrew them and the step is redone with more room
+        self.async_binning = async_binning
+        self.capacity_margin = capacity_margin
+        self.capacity = 0
+        self._overflow = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._pair_counts = torch.zeros(max(1, len(self.views)), dtype=torch.int32, device=dev)
+        self._pair_sum = torch.zeros(1, dtype=torch.int64, device=dev)
+        self._pair_views = 0
+        self.use_graph = graph
+        self.graph_host = False  # step_host views as a graph too (H2D copies as memcpy nodes)
+        self._graph = None
+        self._graph_key = None
+        self._graphs = {}  # key (input buffers) -> graph, for the current capacity
+        self.overflows = 0
 
     def _out(self, lane: _Lane, cam):
         key = (cam.width, cam.height)
@@ -103,12 +122,20 @@ class ViewShardedTrainer:
         cam = self.cameras[self.views[i]]
         out, gimg = self._out(lane, cam)
         build_binning(self.splats, cam, self.raster, out=lane.binning)
-        self.pairs.append(lane.binning.total)
-        render_forward(self.splats, cam, lane.binning, out)
+        if self.capacity:
+            lane.binning.store_total(self._pair_counts[i:i + 1])
+        else:
+            self.pairs.append(lane.binning.total)
+        if not self.fused:
+            render_forward(self.splats, cam, lane.binning, out)
         return cam, out, gimg
 
     def _view_backward(self, i: int, cam, out, gimg, target: torch.Tensor) -> None:
         lane = self._lane(i)
+        if self.fused:
+            render_loss_backward(self.splats, cam, lane.binning, target, "l1", grads=self.grads,
+                                 loss_acc=self.losses[i:i + 1])
+            return
         l1_loss(out.color, target.view(cam.height, cam.width, 3), grad=gimg, loss=self.losses[i:i + 1])
         render_backward(self.splats, cam, lane.binning, out, gimg, self.grads)
 
@@ -126,18 +153,111 @@ class ViewShardedTrainer:
             lane.done.record(lane.stream)
             main.wait_event(lane.done)
 
+    def _on_lanes(self, body) -> None:
+        """Run body() with lane 0 as the current stream, ordered after and before the caller's stream."""
+        cur = torch.cuda.current_stream(self.splats.device)
+        main = self._lanes[0].stream
+        if cur == main:
+            body()
+            return
+        main.wait_stream(cur)
+        with torch.cuda.stream(main):
+            body()
+        cur.wait_stream(main)
+
+    def _views(self, targets: Sequence[torch.Tensor]) -> None:
+        def body():
+            self._begin()
+            for i in range(len(self.views)):
+                with torch.cuda.stream(self._lane(i).stream):
+                    cam, out, gimg = self._view_forward(i)
+                    self._view_backward(i, cam, out, gimg, targets[i])
+            self._join()
+
+        self._on_lanes(body)
+
+    def _set_capacity(self, pairs_max: int, exact: bool = False) -> None:
+        cap = pairs_max if exact else ((int(pairs_max * self.capacity_margin) + 4096 + 65535) & ~65535)
+        for lane in self._lanes:
+            lane.binning.set_capacity(cap, self._overflow)
+        self.capacity = cap
+        self._graph, self._graph_key = None, None
+        self._graphs = {}
+
+    def _views_checked(self, run) -> None:
+        """All owned views into the gradient buffer (run()); in capacity mode redone with larger pair
+        buffers when a view outgrew them (the flag is read once per step, before the collective and Adam)."""
+        if self.async_binning and not self.capacity:
+            n0 = len(self.pairs)
+            run()  # blocking builds: learn the pair counts
+            self._set_capacity(max(self.pairs[n0:]) if len(self.pairs) > n0 else 0)
+            return
+        while True:
+            run()
+            if not self.capacity or not int(self._overflow.item()):
+                break
+            self.overflows += 1
+            self._overflow.zero_()
+            self._set_capacity(int(self._pair_counts.max().item()))
+        if self.capacity:
+            self._pair_sum += self._pair_counts[: len(self.views)].sum()
+            self._pair_views += len(self.views)
+
+    def _run_views(self, targets: Sequence[torch.Tensor]) -> None:
+        self._run_graphed(lambda: self._views(targets), ("dev",) + tuple(t.data_ptr() for t in targets))
+
+    def _run_host_views(self, targets_host: Sequence[torch.Tensor]) -> None:
+        if not self.graph_host:  # measured: the eager H2D pipeline overlaps better than graph memcpy nodes
+            self._on_lanes(lambda: self._views_host(targets_host))
+            return
+        self._run_graphed(lambda: self._on_lanes(lambda: self._views_host(targets_host)),
+                          ("host",) + tuple(t.data_ptr() for t in targets_host))
+
+    def _run_graphed(self, fn, key) -> None:
+        """fn() eagerly, or -- graph mode with capacity binning -- as a replay of its CUDA graph,
+        captured after one eager run (which sizes every buffer) and re-captured when the
+        buffers it reads (key) or the pair capacity change."""
+        if not (self.use_graph and self.capacity):
+            fn()
+            return
+        if self._graph_key != key and key in self._graphs:
+            self._graph, self._graph_key = self._graphs[key], key
+        if self._graph is not None and self._graph_key == key:
+            self._on_lanes(self._graph.launch)
+            return
+        fn()
+        main = self._lanes[0].stream
+        ctxs = []
+        for lane in self._lanes + [None]:
+            with torch.cuda.stream(lane.stream if lane else self._copy_stream):
+                ctxs.append(context(self.splats.device))
+        g = StepGraph(ctxs)
+        main.wait_stream(torch.cuda.current_stream(self.splats.device))
+        with torch.cuda.stream(main):
+            g.capture(fn)
+        self._graph, self._graph_key = g, key
+        if len(self._graphs) >= 4:
+            self._graphs.clear()
+        self._graphs[key] = g
+
+    def pair_stats(self):
+        """(sum of P, views) over the views binned since reset_pair_stats() (roofline bytes)."""
+        if self.capacity:
+            return int(self._pair_sum.item()), self._pair_views
+        return sum(self.pairs), len(self.pairs)
+
+    def reset_pair_stats(self) -> None:
+        self.pairs.clear()
+        self._pair_sum.zero_()
+        self._pair_views = 0
+
     def _finish(self) -> None:
-        self._join()
         reduce_gradients(self.grads, self.pg)
         adam_step(self.splats, self.grads, self.state, self.lrs, check_finite=self.check_finite)
 
     def step(self, targets: Sequence[torch.Tensor]) -> torch.Tensor:
         """One training step with device-resident per-view targets; returns the device loss vector."""
-        self._begin()
-        for i in range(len(self.views)):
-            with torch.cuda.stream(self._lane(i).stream):
-                cam, out, gimg = self._view_forward(i)
-                self._view_backward(i, cam, out, gimg, targets[i])
+        self._views_checked(lambda: self._run_views(targets))
         self._finish()
         return self.losses
 
@@ -145,6 +265,14 @@ class ViewShardedTrainer:
         """End-to-end step from pinned HOST targets: the H2D copy of view i+1 overlaps the
         compute of view i on a side stream, and a view's own copy only has to land before its
         loss (binning and forward do not read the target); the per-view losses are read back."""
+        self._views_checked(lambda: self._run_host_views(targets_host))
+        self._finish()
+        cur = torch.cuda.current_stream(self.splats.device)
+        self._pinned_losses.copy_(self.losses, non_blocking=True)
+        cur.synchronize()
+        return self._pinned_losses
+
+    def _views_host(self, targets_host: Sequence[torch.Tensor]) -> None:
         main = self._lanes[0].stream
         self._begin()
         n = len(self.views)
@@ -154,8 +282,10 @@ class ViewShardedTrainer:
             with torch.cuda.stream(self._copy_stream):
                 self._copy_stream.wait_event(self._buf_free[b])
                 t = targets_host[i]
-                dst = self._target_buf[b].view(-1)[: t.numel()]
-                dst.copy_(t.view(-1), non_blocking=True)
+                if not t.is_pinned() or not t.is_contiguous() or t.dtype != torch.float32:
+                    raise ValueError("step_host: targets must be contiguous pinned fp32 host tensors")
+                # a plain stream-ordered copy (capturable; no host-allocator bookkeeping)
+                copy_h2d(self._target_buf[b], t)
                 self._copy_done[b].record(self._copy_stream)
 
         for b in range(2):
@@ -173,10 +303,7 @@ class ViewShardedTrainer:
                 self._view_backward(i, cam, out, gimg,
                                     self._target_buf[b].view(-1)[: cam.height * cam.width * 3])
                 self._buf_free[b].record(s)
-        self._finish()
-        self._pinned_losses.copy_(self.losses, non_blocking=True)
-        main.synchronize()
-        return self._pinned_losses
+        self._join()
 
     def launches(self) -> int:
         return sum(c.launches() for c in all_contexts(self.splats.device))

@@ -34,8 +34,13 @@ CANCEL_MAX = RTOL / (MODEL_C * EPS32)
 GRAD_FIELDS = ("position", "theta", "quat", "log_scale", "opacity_logit", "grid")
 
 
-def run_gpu(arrays: dict, mode: int, n: int, cam_spec, cfg: "O.Cfg", image_grad=None, sigma=0.5, device="cuda"):
-    """Binning + forward (+ backward with the given image_grad) through libgb_raster.so."""
+def run_gpu(arrays: dict, mode: int, n: int, cam_spec, cfg: "O.Cfg", image_grad=None, sigma=0.5, device="cuda",
+            fused=None):
+    """Binning + forward (+ backward with the given image_grad) through libgb_raster.so.
+
+    fused="l1"|"mse": the backward runs through render_loss_backward against the target
+    color - image_grad/2 (so the loss cotangent at scale 1 is image_grad), and the result
+    records whether its forward buffers and cotangent equal the separate calls'."""
     import torch
 
     import paper_2412_12734_b200 as gb
@@ -53,7 +58,23 @@ def run_gpu(arrays: dict, mode: int, n: int, cam_spec, cfg: "O.Cfg", image_grad=
     grads = None
     if image_grad is not None:
         ig = torch.as_tensor(np.ascontiguousarray(image_grad, np.float32), device=device)
-        grads = gb.render_backward(splats, camera, binning, out, ig)
+        if fused:
+            target = out.color - 0.5 * ig
+            fout = gb.RenderOutput(camera.width, camera.height, device)
+            gimg = torch.empty_like(ig)
+            loss, grads = gb.render_loss_backward(splats, camera, binning, target, fused, scale=1.0, output=fout,
+                                                  image_grad=gimg)
+            d = out.color - target
+            res["fused"] = dict(
+                color_equal=bool(torch.equal(fout.color, out.color)),
+                trans_equal=bool(torch.equal(fout.final_transmittance, out.final_transmittance)),
+                last_equal=bool(torch.equal(fout.last_rank, out.last_rank)),
+                cotangent_max_err=float((gimg - (torch.sign(d) if fused == "l1" else 2.0 * d)).abs().max()),
+                loss=float(loss), loss_expected=float(d.abs().sum() if fused == "l1" else (d * d).sum()))
+            grads_sep = gb.render_backward(splats, camera, binning, out, gimg)
+            res["grads_separate"] = {k: v.cpu().numpy().astype(np.float64) for k, v in grads_sep.tensors().items()}
+        else:
+            grads = gb.render_backward(splats, camera, binning, out, ig)
     torch.cuda.synchronize()
     res["color"] = out.color.cpu().numpy().astype(np.float64)
     res["trans"] = out.final_transmittance.cpu().numpy().astype(np.float64)

@@ -31,19 +31,31 @@ def _image_grad(seed, h, w):
     return rng.choice(np.array([-1.0, 1.0]), size=(h, w, 3))
 
 
-def _check(name, arrays, mode, n, cam, cfg, backward=True, grad_seed=0):
+def _check(name, arrays, mode, n, cam, cfg, backward=True, grad_seed=0, fused=None):
     ig = _image_grad(grad_seed, cam.height, cam.width) if backward else None
-    gpu = run_gpu(arrays, mode, n, cam, cfg, ig)
+    gpu = run_gpu(arrays, mode, n, cam, cfg, ig, fused=fused)
     orc = run_oracle(arrays, n, cam, cfg, ig)
     stats = dict(binning=compare_binning(gpu, orc), image=compare_image(gpu, orc))
     if backward:
         stats["grads"] = compare_grads(gpu, orc)
+    if fused:
+        stats["fused"] = gpu["fused"]
+        # the fused kernel against the separate calls fed its own cotangent: same arithmetic, atomics order aside
+        # (max |difference| over the field's max magnitude: atomics order moves the last bits only)
+        stats["fused_vs_separate"] = {k: float(np.max(np.abs(gpu["grads"][k] - v)) / (1e-12 + np.max(np.abs(v))))
+                                      for k, v in gpu["grads_separate"].items() if v.size}
     _record(name, stats)
     print(name, json.dumps(stats))
     assert stats["binning"]["offsets_equal"] and stats["binning"]["values_equal"], "tile lists must be bit-exact"
     im = stats["image"]
     assert im["color_violations"] == 0 and im["alpha_violations"] == 0, im
     assert im["last_rank_mismatch"] == 0, im
+    if fused:
+        fs = stats["fused"]
+        assert fs["color_equal"] and fs["trans_equal"] and fs["last_equal"], fs
+        assert fs["cotangent_max_err"] <= (0.0 if fused == "l1" else 1e-6), fs
+        assert abs(fs["loss"] - fs["loss_expected"]) <= 1e-4 * fs["loss_expected"] + 1e-6, fs
+        assert all(v < 1e-5 for v in stats["fused_vs_separate"].values()), stats["fused_vs_separate"]
     if backward:
         for f, st in stats["grads"].items():
             # every entry within rtol/atol + kink slack, except sums cancelling by > CANCEL_MAX
@@ -178,6 +190,25 @@ def test_alternative_compositors(monkeypatch, variant, group):
     arrays = sc.generate(O.MODE_ORTHO, 3000, 3, 31, width=120, height=88, scale_lo=0.5, scale_hi=8.0)
     _check(f"variant_{variant}{group or ''}_ortho_n3", arrays, O.MODE_ORTHO, 3,
            O.Cam(O.MODE_ORTHO, 120, 88, (0.2, 0.1, 0.3)), O.Cfg(tile_size=8))
+
+
+# ---------------------------------------------------------------------------------------------
+# render_loss_backward: K3 + K6 + K4 in one kernel (and its three-call fallback, GB_NO_FUSE)
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("loss", ["l1", "mse"])
+@pytest.mark.parametrize("fallback", [False, True])
+def test_fused_forward_loss_backward(monkeypatch, loss, fallback):
+    import paper_2412_12734_b200.scenes as sc
+
+    if fallback:
+        monkeypatch.setenv("GB_NO_FUSE", "1")
+    tag = f"fused_{loss}{'_fallback' if fallback else ''}"
+    cfgs = _config(0, count=20_000, n=8)
+    _check(f"{tag}_pinhole", cfgs.arrays(), O.MODE_PINHOLE, 8, O.Cam.from_spec(cfgs.cameras[0]), O.Cfg(),
+           fused=loss)
+    arrays = sc.generate(O.MODE_ORTHO, 3000, 3, 37, width=120, height=88, scale_lo=0.5, scale_hi=8.0)
+    _check(f"{tag}_ortho_n3", arrays, O.MODE_ORTHO, 3, O.Cam(O.MODE_ORTHO, 120, 88, (0.2, 0.1, 0.3)),
+           O.Cfg(tile_size=8), fused=loss)
 
 
 def test_pinhole_camera_inside_the_cloud():

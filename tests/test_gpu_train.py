@@ -153,3 +153,99 @@ def test_view_sharded_step_vs_oracle():
                                     0.999, 1e-8, 0.1, 1 - 0.999)
         np.testing.assert_allclose(splats.tensors()[k].cpu().numpy().astype(np.float64).ravel(), ref, rtol=2e-6,
                                    atol=1e-5 * lr, err_msg=k)
+
+
+def test_capacity_binning_matches_blocking():
+    """gb_binning_set_capacity: padded sort over a fixed pair capacity, no host read-back -- the same
+    tile lists and images as the blocking build; an undersized capacity raises the overflow flag."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+
+    c = sc.baseline_config(0, count=20_000, n=4)
+    splats = gb.SplatSet.from_numpy(c.mode, gb.ColorGridConfig(4), **c.arrays())
+    cam = gb.PinholeCamera.from_spec(c.cameras[0])
+    ref = gb.build_binning(splats, cam)
+    P = ref.total
+    ref_csr = ref.csr()
+    ref_img = gb.render_forward(splats, cam, ref).color.clone()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for cap in (P, P + 1, P + 70_000):
+        b = gb.TileBinning()
+        b.set_capacity(cap, flag)
+        gb.build_binning(splats, cam, out=b)
+        got = torch.zeros(1, dtype=torch.int32, device="cuda")
+        b.store_total(got)
+        assert int(got) == P and int(flag) == 0 and b.total == P
+        off, val = b.csr()
+        np.testing.assert_array_equal(off, ref_csr[0])
+        np.testing.assert_array_equal(val, ref_csr[1])
+        assert torch.equal(gb.render_forward(splats, cam, b).color, ref_img)
+    small = gb.TileBinning()
+    small.set_capacity(P // 3, flag)
+    gb.build_binning(splats, cam, out=small)
+    assert int(flag) == 1 and small.total == P // 3
+    off, val = small.csr()  # the first P/3 pairs in (depth, index) order, still tile-sorted
+    assert off[-1] == P // 3 and np.all(np.diff(off) >= 0)
+
+
+def _trainer_scene():
+    import paper_2412_12734_b200.scenes as sc
+
+    n, K, W, H = 4, 3000, 96, 80
+    arrays = _pinhole_scene(K, n, 5)
+    specs = [sc.look_at((3.0 * np.cos(a), 0.7, 3.0 * np.sin(a)), (0.0, 0.0, 0.0), W, H, 90.0, 90.0, 48.0, 40.0)
+             for a in (0.3, 2.1, 4.0)]
+    targets = [sc.uniform_image(100 + v, W, H) for v in range(3)]
+    return n, arrays, specs, targets
+
+
+@pytest.mark.parametrize("mode", ["capacity", "graph", "graph_host", "overflow", "fused"])
+def test_trainer_modes_match_blocking(mode):
+    """The step's gradients with capacity-mode binning, with the view work replayed as a CUDA graph,
+    after a capacity overflow (the step is redone with larger buffers), and with the fused
+    forward+loss+backward kernel, equal the blocking eager step's (atomics order aside)."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200.train import ViewShardedTrainer
+
+    n, arrays, specs, targets = _trainer_scene()
+    cams = [gb.PinholeCamera.from_spec(s) for s in specs]
+    tg = [torch.as_tensor(t).cuda() for t in targets]
+
+    def make(**kw):
+        s = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+        return ViewShardedTrainer(s, cams, [0, 1, 2], **kw)
+
+    ref = make(async_binning=False)
+    ref._views_checked(lambda: ref._run_views(tg))
+    want = {k: v.cpu().numpy().astype(np.float64) for k, v in ref.grads.tensors().items() if v is not None}
+    want_loss = ref.losses.cpu().numpy()
+    P = max(ref.pairs)
+    tr = make(graph=mode.startswith("graph"), fused=mode == "fused")
+    tr.graph_host = mode == "graph_host"
+    tr._set_capacity(P // 4 if mode == "overflow" else P, exact=True)
+    runs = 3 if mode.startswith("graph") else 1  # eager + capture, then replays
+    host = [torch.as_tensor(t).pin_memory() for t in targets]
+    for _ in range(runs):
+        if mode == "graph_host":  # pinned host targets, H2D copies inside the graph
+            tr._views_checked(lambda: tr._run_host_views(host))
+        else:
+            tr._views_checked(lambda: tr._run_views(tg))
+        torch.cuda.synchronize()
+        got = {k: v.cpu().numpy().astype(np.float64) for k, v in tr.grads.tensors().items() if v is not None}
+        for k, w in want.items():
+            np.testing.assert_allclose(got[k], w, rtol=1e-4, atol=1e-6 * np.abs(w).max(), err_msg=k)
+        np.testing.assert_allclose(tr.losses.cpu().numpy(), want_loss, rtol=1e-5)
+    assert tr.overflows == (1 if mode == "overflow" else 0)
+    if mode.startswith("graph"):
+        assert tr._graph is not None
+    s, v = tr.pair_stats()
+    assert v == 3 * runs and s == runs * sum(ref.pairs)
+    # and full steps (collective + Adam) run in every mode, alternating the device and host inputs
+    tr.step(tg)
+    tr.step_host(host)
+    tr.step(tg)
+    torch.cuda.synchronize()

@@ -18,7 +18,7 @@ if [ "${TESTS:-1}" = 1 ]; then
   echo "smoke exit $?" >> $O/smoke.log
 fi
 # variant names: grp (default, G=8), grp16 (G=16), direct, staged
-venv() { case $1 in grp16) echo "GB_COMPOSITOR=grp GB_GROUP=16";; grp4) echo "GB_COMPOSITOR=grp GB_GROUP=4";; fwd0) echo "GB_FWD_BATCH=0";; fwd12) echo "GB_FWD_BATCH=12";; grp16b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16";; grp16bu) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16 GB_GRP_TEXEL=uni";; grp8b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=8";; perlane) echo "GB_DIRECT_TEXEL=perlane";; *) echo "GB_COMPOSITOR=$1";; esac; }
+venv() { case $1 in grp16) echo "GB_COMPOSITOR=grp GB_GROUP=16";; grp4) echo "GB_COMPOSITOR=grp GB_GROUP=4";; fwd0) echo "GB_FWD_BATCH=0";; fwd12) echo "GB_FWD_BATCH=12";; grp16b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16";; grp16bu) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16 GB_GRP_TEXEL=uni";; grp8b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=8";; perlane) echo "GB_DIRECT_TEXEL=perlane";; nofuse) echo "GB_NO_FUSE=1";; fused) echo "GB_FUSED=1";; blocking) echo "GB_BLOCKING_BINNING=1";; graph) echo "GB_GRAPH=1";; graphfused) echo "GB_GRAPH=1 GB_FUSED=1";; *) echo "GB_COMPOSITOR=$1";; esac; }
 for v in ${ALT_TESTS:-}; do
   env $(venv $v) timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "configs1 or pinhole_small or ortho_random or ragged" > $O/pytest_gpu_$v.log 2>&1
   echo "pytest exit $?" >> $O/pytest_gpu_$v.log
@@ -44,5 +44,7 @@ if [ "${NCU:-1}" = 1 ]; then
     -o $O/k4_full -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_k4.log 2>&1
   env $(venv ${NCU_VARIANT:-direct}) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_forward -s 8 -c 1 \
     -o $O/k3_full -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_k3.log 2>&1
+  env $(venv ${NCU_VARIANT:-direct}) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 8 -c 1 \
+    -o $O/kf_full -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_kf.log 2>&1
 fi
 echo done > $O/DONE
