@@ -224,6 +224,7 @@ def run_ours(args):
     use_graph = os.environ.get("GB_GRAPH", "1") != "0" and not args.no_graph
     blocking = os.environ.get("GB_BLOCKING_BINNING") == "1"
     trainer = ViewShardedTrainer(splats, cams, views, lrs=lrs, graph=use_graph, async_binning=not blocking,
+                                 lanes=int(os.environ.get("GB_LANES", "2")),
                                  fused=os.environ.get("GB_FUSED") == "1")
     W, H = cams[0].width, cams[0].height
     host_targets = [torch.from_numpy(cfg3.target(v)).pin_memory() for v in views]

@@ -3,7 +3,7 @@
     python tools/ncu_lines.py <report.ncu-rep> <kernel-regex> <mangled-name-substring> [top]
 
 Extracts the cubins of libgb_raster.so (cuobjdump -xelf), maps SASS offsets to
-source lines with `nvdisasm --print-line-info`, and sums ncu's "Instructions
+source file:line (innermost inlined frame) with `nvdisasm --print-line-info`, and sums ncu's "Instructions
 Executed" and warp-stall samples per line (the binary must be the one profiled).
 """
 import collections
@@ -34,9 +34,9 @@ def line_map(mangled_sub):
                 continue
             if sec is None or mangled_sub not in sec:
                 continue
-            f = re.search(r'line (\d+)', ln) if "//##" in ln else None
+            f = re.search(r'File "([^"]+)", line (\d+)', ln) if "//##" in ln else None
             if f:
-                cur = int(f.group(1))
+                cur = (os.path.basename(f.group(1)), int(f.group(2)))
                 continue
             o = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*)", ln)
             if o and cur is not None:
@@ -68,15 +68,23 @@ def main():
     base = min(a for a, _, _ in recs)
     by_s, by_i = collections.Counter(), collections.Counter()
     for a, s, i in recs:
-        line = lm.get(a - base, (0, ""))[0]
+        line = lm.get(a - base, (("?", 0), ""))[0]
         by_s[line] += s
         by_i[line] += i
-    src = open(os.path.join(ROOT, "paper_2412_12734_b200", "csrc", os.environ.get("SRC", "gb_raster.cu"))).read().splitlines()
+    srcs = {}
+
+    def text_of(fl):
+        f, line = fl
+        if f not in srcs:
+            p = os.path.join(ROOT, "paper_2412_12734_b200", "csrc", f)
+            srcs[f] = open(p).read().splitlines() if os.path.exists(p) else []
+        src = srcs[f]
+        return src[line - 1].strip()[:64] if 0 < line <= len(src) else "?"
+
     ts, ti = sum(by_s.values()), sum(by_i.values())
     print(f"total stall samples {ts}, warp instructions {ti}")
-    for line, i in by_i.most_common(top):
-        text = src[line - 1].strip()[:70] if 0 < line <= len(src) else "?"
-        print(f"L{line:4d} instr {i*100/ti:5.1f}%  stall {by_s[line]*100/ts:5.1f}%  {text}")
+    for fl, i in by_i.most_common(top):
+        print(f"{fl[0][:14]:>14}:{fl[1]:<4d} instr {i*100/ti:5.1f}%  stall {by_s[fl]*100/ts:5.1f}%  {text_of(fl)}")
 
 
 if __name__ == "__main__":
