@@ -12,7 +12,8 @@ VARIANTS=${VARIANTS:-direct}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 lscpu > $O/lscpu.txt 2>&1
 if [ "${TESTS:-1}" = 1 ]; then
-  timeout 1200 python -m pytest tests -m gpu -x -q -k "not configs2_full" > $O/pytest_gpu.log 2>&1
+  if [ "${FULL:-0}" = 1 ]; then K=""; else K="not configs2_full"; fi
+  timeout 2400 python -m pytest tests -m gpu -x -q -k "$K" > $O/pytest_gpu.log 2>&1
   echo "pytest exit $?" >> $O/pytest_gpu.log
   timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
   echo "smoke exit $?" >> $O/smoke.log
