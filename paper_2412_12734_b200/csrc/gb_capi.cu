@@ -272,6 +272,10 @@ gb::RasterConst make_raster_const(const gb_binning* b, int n, double sigma) {
     rc.tex_scale = (float)((double)(n - 1) / (2.0 * sigma));
     rc.tex_offset = (float)((double)(n - 1) * 0.5);
     rc.sigma = (float)sigma;
+    // K4 warp-entries with <= 12 active lanes add per lane (measured optimum of 0..32: 0 = always
+    // reduce 575 MP/s, 8 = 605, 12 = 607, 16 = 605, 24 = 586, 32 = 453); GB_K4_DIRECT overrides
+    const char* dl = getenv("GB_K4_DIRECT");
+    rc.direct_lanes = dl ? atoi(dl) : 12;
     return rc;
 }
 

@@ -78,6 +78,11 @@ __device__ __forceinline__ void red3(float* p, float a, float b, float c) {
     atomicAdd(even ? p + 2 : p, even ? c : a);
 }
 
+// p[0..3] += (a, b, c, d) with one 16-byte vector red (p 16-B aligned)
+__device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
+    atomicAdd(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));
+}
+
 // texel corner k (0..3 = 00, 10, 01, 11) channel c -> float offset from the base texel
 __device__ __forceinline__ int corner_offset(int i, int N) {
     const int k = i / 3, c = i - 3 * (i / 3);

@@ -62,6 +62,7 @@ struct RasterConst {
     float tex_scale;       // (n-1)/(2 sigma)
     float tex_offset;      // (n-1)/2
     float sigma;
+    int direct_lanes;      // K4: warp-entries with at most this many active lanes skip the warp reductions
 };
 
 // Thread -> pixel mapping inside a tile.  For tile sizes that are multiples

@@ -511,25 +511,9 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
         bh1 = alpha * c1 + om * bh1;
         bh2 = alpha * c2 + om * bh2;
     }
-    {  // screen-space sums: lane l owns value l >> 1
-        float sv[NS];
-#pragma unroll
-        for (int i = 0; i < NS; ++i) sv[i] = red[i];
-        const float r2 = smem_reduce<NS>(sv, wscratch, lane);
-        if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
-    }
-    // texel gradients: one warp reduction when every active lane shares a bilinear cell;
-    // otherwise each lane adds its (at most four) non-zero texels straight to HBM with
-    // one float2 + one float red per texel -- cheaper than a reduction per distinct cell
     float* gg = grid_grad + (size_t)id * F;
-    const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
-    if (__all_sync(kFull, !on || tbase == b0)) {
-        if (lane == 0) GB_DBG(4, 1);
-        const float r2 = smem_reduce<12>(tg, wscratch, lane);
-        if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
-            red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
-    } else if (on) {
-        if (lane == 0) GB_DBG(5, 1);
+    // this lane's (at most four) non-zero texels straight to memory: one float2 + one float red each
+    auto texel_reds = [&]() {
         if (N == 1) {
             red3(gg, tg[0], tg[1], tg[2]);
         } else {
@@ -538,6 +522,42 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
                 if (wk[k] != 0.0f)
                     red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
         }
+    };
+    if (__popc(act) <= rc.direct_lanes) {
+        // few active lanes: each adds its own terms with vector reds -- ~20 instructions for the warp
+        // instead of two ~35-instruction warp reductions (12 % of warp-entries have one active lane)
+        if (on) {
+            float* a = accum + (size_t)id * kAccumStride;  // 48-B records: 16-B aligned
+            red4(a, red[0], red[1], red[2], red[3]);
+            if (NS == 10) {
+                red4(a + 4, red[4], red[5], red[6], red[7]);
+                atomicAdd(reinterpret_cast<float2*>(a + 8), make_float2(red[8], red[9]));
+            } else {
+                atomicAdd(reinterpret_cast<float2*>(a + 4), make_float2(red[4], red[5]));
+                atomicAdd(a + 6, red[6]);
+            }
+            texel_reds();
+        }
+        return;
+    }
+    {  // screen-space sums: lane l owns value l >> 1
+        float sv[NS];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) sv[i] = red[i];
+        const float r2 = smem_reduce<NS>(sv, wscratch, lane);
+        if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
+    }
+    // texel gradients: one warp reduction when every active lane shares a bilinear cell;
+    // otherwise each lane adds its own texels -- cheaper than a reduction per distinct cell
+    const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
+    if (__all_sync(kFull, !on || tbase == b0)) {
+        if (lane == 0) GB_DBG(4, 1);
+        const float r2 = smem_reduce<12>(tg, wscratch, lane);
+        if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
+            red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
+    } else if (on) {
+        if (lane == 0) GB_DBG(5, 1);
+        texel_reds();
     }
 }
 
