@@ -446,7 +446,6 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
             bilin_setup(u, v, N, rc, b);
             const float* p00 = t + b.o00;
             const float* p10 = p00 + 3 * N;
-            const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
             float cc_[3];
             const float chat[3] = {ch0, ch1, ch2};
 #pragma unroll
@@ -457,8 +456,11 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
                 tg[3 + c] = chat[c] * b.w10;
                 tg[6 + c] = chat[c] * b.w01;
                 tg[9 + c] = chat[c] * b.w11;
-                fu_hat = fmaf(chat[c], (c10 - c00) * gv + (c11 - c01) * b.fv, fu_hat);
-                fv_hat = fmaf(chat[c], (c01 - c00) * gu + (c11 - c10) * b.fu, fv_hat);
+                // texture.hpp:102-103: (C10 - C00)(1 - f_v) + (C11 - C01) f_v = du + f_v e and
+                // (C01 - C00)(1 - f_u) + (C11 - C10) f_u = dv + f_u e, e = C11 - C10 - C01 + C00
+                const float du = c10 - c00, dv = c01 - c00, e = (c11 - c10) - dv;
+                fu_hat = fmaf(chat[c], fmaf(b.fv, e, du), fu_hat);
+                fv_hat = fmaf(chat[c], fmaf(b.fu, e, dv), fv_hat);
             }
             c0 = cc_[0];
             c1 = cc_[1];
@@ -473,8 +475,7 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
         float u_hat = (N > 1 && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
         float v_hat = (N > 1 && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
         // raster.hpp:344-346
-        const float gT0 = g0 * T, gT1 = g1 * T, gT2 = g2 * T;
-        const float alpha_hat = gT0 * (c0 - bh0) + gT1 * (c1 - bh1) + gT2 * (c2 - bh2);
+        const float alpha_hat = T * (g0 * (c0 - bh0) + g1 * (c1 - bh1) + g2 * (c2 - bh2));
         float op = 0.0f;
         if (araw < kMaxAlphaF) {  // raster.hpp:350-354
             op = alpha_hat * G;
