@@ -383,71 +383,60 @@ __device__ __forceinline__ float reduce_scatter(float (&a)[V], int lane) {
 // ---------------------------------------------------------------------------
 // One backward entry for the calling warp: evaluate, update the pixel's
 // rewind state, reduce and scatter the gradients (raster.hpp:324-363).
-template <int MODE, int NT>
-__device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __restrict__ t, int id, int rank,
-                                          int last, int x, int y, float& T, float g0, float g1, float g2,
-                                          float& bh0, float& bh1, float& bh2, const RasterConst& rc, int N,
-                                          int lane, float* wscratch, float* __restrict__ accum,
-                                          float* __restrict__ grid_grad) {
+// Texel footprint class of a warp-entry (texture.hpp:27-47).  A lane whose |u| >= sigma sits where the
+// clamp pins u' to 0 or n-1: f_u is exactly 0 or 1, one texel row carries all the weight and the u
+// adjoint is masked (texture.hpp:106-109); likewise for v.  When no active lane of the warp needs
+// interpolation along u (v), the bilinear cell degenerates to a texel pair or a single texel and the
+// warp skips the loads, products and reductions of the zero-weight corners.  In a configs[3] view 27 %
+// of warp-entries need one texel, 48 % two, 25 % all four (62 % of active pixels are clamped in both).
+enum { kCellFull = 0, kCellU = 1, kCellV = 2, kCellOne = 3 };
+
+template <int CELL>
+struct CellShape {
+    static constexpr int texels = CELL == kCellFull ? 4 : CELL == kCellOne ? 1 : 2;
+};
+
+// offset of reduced texel-gradient value i (corner i / 3, channel i % 3) from the class's base texel
+template <int CELL>
+__device__ __forceinline__ int cell_offset(int i, int N) {
+    if (CELL == kCellFull) return corner_offset(i, N);
+    if (CELL == kCellU) return i < 3 ? i : 3 * N + i - 3;  // (i_u, i_v'), (i_u + 1, i_v')
+    return i;                                              // kCellV: (i_u', i_v), (i_u', i_v + 1); kCellOne
+}
+
+// One backward entry for the calling warp, after the evaluation: rewind the pixel's state, form the
+// adjoints and reduce/scatter the gradients (raster.hpp:324-363).
+template <int MODE, int NT, int CELL>
+__device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, bool on, unsigned act, float u,
+                                          float v, float G, float alpha, float araw, const PinholeTerms& pt,
+                                          float& T, float g0, float g1, float g2, float& bh0, float& bh1,
+                                          float& bh2, const RasterConst& rc, int N, int lane, float* wscratch,
+                                          float* __restrict__ accum, float* __restrict__ grid_grad) {
     constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
+    constexpr int NX = CellShape<CELL>::texels;
     const int F = 3 * N * N;
     const float sigma = rc.sigma;
-    bool on = rank <= last;
-    float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
-    PinholeTerms pt;
-    if (on) {
-        bool hit;
-        if (MODE == GB_MODE_ORTHO) {
-            hit = eval_uv_ortho(h, x, y, u, v);
-        } else {
-            hit = eval_uv_pinhole(h, x, y, u, v, pt);
-        }
-        if (hit) {
-            G = gauss_weight(u, v);
-            araw = __fmul_rn(h.h1.z, G);
-            alpha = fminf(araw, kMaxAlphaF);
-            on = !(alpha < rc.alpha_skip);
-        } else {
-            on = false;
-        }
-    }
-    const unsigned act = __ballot_sync(kFull, on);
-    if (act == 0) return;
-    if (lane == 0) {
-        GB_DBG(2, 1);
-        GB_DBG(3, __popc(act));
-        GB_DBG(6, (act & 0x0F0F0F0Fu) && (act & 0xF0F0F0F0u));  // both 4x4 halves active
-        GB_DBG(7, (act & 0x0000FFFFu) && (act & 0xFFFF0000u));  // both 8x2 halves active
-    }
-
     float red[16];  // screen-space sums (NS of 16 slots)
 #pragma unroll
     for (int i = 0; i < 16; ++i) red[i] = 0.0f;
-    float tg[12];
+    float tg[3 * NX];
 #pragma unroll
-    for (int i = 0; i < 12; ++i) tg[i] = 0.0f;
+    for (int i = 0; i < 3 * NX; ++i) tg[i] = 0.0f;
     int tbase = -1;
-    float wk[4] = {1.0f, 0.0f, 0.0f, 0.0f};  // bilinear corner weights (n = 1: texel 0 only)
+    float wk[NX];  // corner weights
+#pragma unroll
+    for (int k = 0; k < NX; ++k) wk[k] = 0.0f;
     if (on) {
         T = __fmul_rn(T, rcp_approx(__fsub_rn(1.0f, alpha)));  // raster.hpp:333
         float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
         const float aT = alpha * T;
-        const float ch0 = aT * g0, ch1 = aT * g1, ch2 = aT * g2;  // c_hat (raster.hpp:338-340)
-        if (N == 1) {
-            c0 = t[0];
-            c1 = t[1];
-            c2 = t[2];
-            tg[0] = ch0;
-            tg[1] = ch1;
-            tg[2] = ch2;
-            tbase = 0;
-        } else {
+        const float chat[3] = {aT * g0, aT * g1, aT * g2};  // c_hat (raster.hpp:338-340)
+        float cc_[3];
+        if (CELL == kCellFull) {
             Bilin b;
             bilin_setup(u, v, N, rc, b);
             const float* p00 = t + b.o00;
             const float* p10 = p00 + 3 * N;
-            float cc_[3];
-            const float chat[3] = {ch0, ch1, ch2};
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 const float c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
@@ -462,18 +451,54 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
                 fu_hat = fmaf(chat[c], fmaf(b.fv, e, du), fu_hat);
                 fv_hat = fmaf(chat[c], fmaf(b.fu, e, dv), fv_hat);
             }
-            c0 = cc_[0];
-            c1 = cc_[1];
-            c2 = cc_[2];
             tbase = b.o00;
             wk[0] = b.w00;
             wk[1] = b.w10;
             wk[2] = b.w01;
             wk[3] = b.w11;
+        } else if (CELL == kCellU || CELL == kCellV) {
+            // interpolation along one axis; the other sits on texel 0 or n-1
+            const float w = CELL == kCellU ? u : v;
+            float sx = __fmaf_rn(w, rc.tex_scale, rc.tex_offset);
+            sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
+            const int i0 = min((int)floorf(sx), N - 2);
+            const float f = __fsub_rn(sx, (float)i0);
+            const float gf = 1.0f - f;
+            const int other = (CELL == kCellU ? v : u) > 0.0f ? N - 1 : 0;
+            tbase = (CELL == kCellU ? i0 * N + other : other * N + i0) * 3;
+            const float* pa = t + tbase;
+            const float* pb = pa + (CELL == kCellU ? 3 * N : 3);
+            float fh = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float ca = pa[c], cb = pb[c];
+                cc_[c] = fmaf(cb, f, ca * gf);  // = the four-corner blend with two zero weights
+                tg[c] = chat[c] * gf;
+                tg[3 + c] = chat[c] * f;
+                fh = fmaf(chat[c], cb - ca, fh);
+            }
+            if (CELL == kCellU)
+                fu_hat = fh;
+            else
+                fv_hat = fh;
+            wk[0] = gf;
+            wk[1] = f;
+        } else {  // kCellOne (and n = 1): a single texel with weight 1
+            const int iu = N > 1 && u > 0.0f ? N - 1 : 0, iv = N > 1 && v > 0.0f ? N - 1 : 0;
+            tbase = (iu * N + iv) * 3;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                cc_[c] = t[tbase + c];
+                tg[c] = chat[c];
+            }
+            wk[0] = 1.0f;
         }
+        c0 = cc_[0];
+        c1 = cc_[1];
+        c2 = cc_[2];
         // texture.hpp:106-109 (strict mask)
-        float u_hat = (N > 1 && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
-        float v_hat = (N > 1 && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
+        float u_hat = (CELL != kCellV && CELL != kCellOne && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
+        float v_hat = (CELL != kCellU && CELL != kCellOne && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
         // raster.hpp:344-346
         const float alpha_hat = T * (g0 * (c0 - bh0) + g1 * (c1 - bh1) + g2 * (c2 - bh2));
         float op = 0.0f;
@@ -513,16 +538,12 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
         bh2 = alpha * c2 + om * bh2;
     }
     float* gg = grid_grad + (size_t)id * F;
-    // this lane's (at most four) non-zero texels straight to memory: one float2 + one float red each
+    // this lane's non-zero texels straight to memory: one float2 + one float red each
     auto texel_reds = [&]() {
-        if (N == 1) {
-            red3(gg, tg[0], tg[1], tg[2]);
-        } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
-                if (wk[k] != 0.0f)
-                    red3(gg + tbase + corner_offset(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
-        }
+        for (int k = 0; k < NX; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
+            if (wk[k] != 0.0f)
+                red3(gg + tbase + cell_offset<CELL>(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
     };
     if (__popc(act) <= rc.direct_lanes) {
         // few active lanes: each adds its own terms with vector reds -- ~20 instructions for the warp
@@ -548,18 +569,73 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
         const float r2 = smem_reduce<NS>(sv, wscratch, lane);
         if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
     }
-    // texel gradients: one warp reduction when every active lane shares a bilinear cell;
+    // texel gradients: one warp reduction when every active lane has the same base texel;
     // otherwise each lane adds its own texels -- cheaper than a reduction per distinct cell
     const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
     if (__all_sync(kFull, !on || tbase == b0)) {
         if (lane == 0) GB_DBG(4, 1);
-        const float r2 = smem_reduce<12>(tg, wscratch, lane);
-        if ((lane & 1) == 0 && lane < 24 && (N > 1 || lane < 6))
-            red_add(gg + b0 + corner_offset(lane >> 1, N), r2);
+        const float r2 = smem_reduce<3 * NX>(tg, wscratch, lane);
+        if ((lane & 1) == 0 && (lane >> 1) < 3 * NX) red_add(gg + b0 + cell_offset<CELL>(lane >> 1, N), r2);
     } else if (on) {
         if (lane == 0) GB_DBG(5, 1);
         texel_reds();
     }
+}
+
+// One backward entry for the calling warp: evaluate, pick the warp's texel footprint class, then
+// bwd_shade (raster.hpp:324-363).
+template <int MODE, int NT>
+__device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __restrict__ t, int id, int rank,
+                                          int last, int x, int y, float& T, float g0, float g1, float g2,
+                                          float& bh0, float& bh1, float& bh2, const RasterConst& rc, int N,
+                                          int lane, float* wscratch, float* __restrict__ accum,
+                                          float* __restrict__ grid_grad) {
+    const float sigma = rc.sigma;
+    bool on = rank <= last;
+    float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
+    PinholeTerms pt;
+    if (on) {
+        bool hit;
+        if (MODE == GB_MODE_ORTHO) {
+            hit = eval_uv_ortho(h, x, y, u, v);
+        } else {
+            hit = eval_uv_pinhole(h, x, y, u, v, pt);
+        }
+        if (hit) {
+            G = gauss_weight(u, v);
+            araw = __fmul_rn(h.h1.z, G);
+            alpha = fminf(araw, kMaxAlphaF);
+            on = !(alpha < rc.alpha_skip);
+        } else {
+            on = false;
+        }
+    }
+    const unsigned act = __ballot_sync(kFull, on);
+    if (act == 0) return;
+    if (lane == 0) {
+        GB_DBG(2, 1);
+        GB_DBG(3, __popc(act));
+        GB_DBG(6, (act & 0x0F0F0F0Fu) && (act & 0xF0F0F0F0u));  // both 4x4 halves active
+        GB_DBG(7, (act & 0x0000FFFFu) && (act & 0xFFFF0000u));  // both 8x2 halves active
+    }
+#define GB_SHADE(CELL)                                                                                          \
+    bwd_shade<MODE, NT, CELL>(t, id, on, act, u, v, G, alpha, araw, pt, T, g0, g1, g2, bh0, bh1, bh2, rc, N, \
+                              lane, wscratch, accum, grid_grad)
+    if (N == 1) {
+        GB_SHADE(kCellOne);
+        return;
+    }
+    const bool au = __any_sync(kFull, on && u > -sigma && u < sigma);
+    const bool av = __any_sync(kFull, on && v > -sigma && v < sigma);
+    if (au && av)
+        GB_SHADE(kCellFull);
+    else if (au)
+        GB_SHADE(kCellU);
+    else if (av)
+        GB_SHADE(kCellV);
+    else
+        GB_SHADE(kCellOne);
+#undef GB_SHADE
 }
 
 template <int MODE, int NT>
@@ -715,12 +791,13 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             const int bit = __ffs(mask) - 1;
             mask &= mask - 1;
             const int id = __shfl_sync(kFull, idl, bit);
+            bool comp = false;  // this pixel composites the entry
+            float u = 0.0f, v = 0.0f, alpha = 0.0f;
             if (!done) {
                 ScreenHeader h;
                 h.h0 = __ldg(&hdr[id].h0);
                 h.h1 = __ldg(&hdr[id].h1);
                 h.h2 = __ldg(&hdr[id].h2);
-                float u, v;
                 bool hit;
                 if (MODE == GB_MODE_ORTHO) {
                     hit = eval_uv_ortho(h, x, y, u, v);
@@ -730,34 +807,53 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
                 }
                 if (hit) {
                     const float G = gauss_weight(u, v);
-                    const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);  // raster.hpp:241
-                    if (!(alpha < rc.alpha_skip)) {                                // raster.hpp:242
-                        const float* t = tex + (size_t)id * F;
-                        float c0_, c1_, c2_;
-                        if (N == 1) {
-                            c0_ = __ldg(t);
-                            c1_ = __ldg(t + 1);
-                            c2_ = __ldg(t + 2);
-                        } else {
-                            Bilin b;
-                            bilin_setup(u, v, N, rc, b);
-                            const float* p00 = t + b.o00;
-                            const float* p10 = p00 + 3 * N;
-                            c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 + __ldg(p10 + 3) * b.w11;
-                            c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
-                                  __ldg(p10 + 4) * b.w11;
-                            c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
-                                  __ldg(p10 + 5) * b.w11;
-                        }
-                        const float w = alpha * T;  // raster.hpp:244-249
-                        acc0 = fmaf(c0_, w, acc0);
-                        acc1 = fmaf(c1_, w, acc1);
-                        acc2 = fmaf(c2_, w, acc2);
-                        T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                        last = c0 + bit;
-                        if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;  // raster.hpp:250
-                    }
+                    alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);  // raster.hpp:241
+                    comp = !(alpha < rc.alpha_skip);                  // raster.hpp:242
                 }
+            }
+            // texel footprint class of the warp (see bwd_shade): clamped axes read one texel row
+            const float sigma = rc.sigma;
+            const bool au = N > 1 && __any_sync(kFull, comp && u > -sigma && u < sigma);
+            const bool av = N > 1 && __any_sync(kFull, comp && v > -sigma && v < sigma);
+            if (comp) {
+                const float* t = tex + (size_t)id * F;
+                float c0_, c1_, c2_;
+                if (au && av) {
+                    Bilin b;
+                    bilin_setup(u, v, N, rc, b);
+                    const float* p00 = t + b.o00;
+                    const float* p10 = p00 + 3 * N;
+                    c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 + __ldg(p10 + 3) * b.w11;
+                    c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
+                          __ldg(p10 + 4) * b.w11;
+                    c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
+                          __ldg(p10 + 5) * b.w11;
+                } else if (au || av) {  // the four-corner blend with two zero weights
+                    const float w = au ? u : v;
+                    float sx = __fmaf_rn(w, rc.tex_scale, rc.tex_offset);
+                    sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
+                    const int i0 = min((int)floorf(sx), N - 2);
+                    const float f = __fsub_rn(sx, (float)i0);
+                    const float gf = 1.0f - f;
+                    const int other = (au ? v : u) > 0.0f ? N - 1 : 0;
+                    const float* pa = t + (au ? i0 * N + other : other * N + i0) * 3;
+                    const float* pb = pa + (au ? 3 * N : 3);
+                    c0_ = fmaf(__ldg(pb), f, __ldg(pa) * gf);
+                    c1_ = fmaf(__ldg(pb + 1), f, __ldg(pa + 1) * gf);
+                    c2_ = fmaf(__ldg(pb + 2), f, __ldg(pa + 2) * gf);
+                } else {  // one texel (and n = 1)
+                    const float* p = t + (N > 1 ? ((u > 0.0f ? N - 1 : 0) * N + (v > 0.0f ? N - 1 : 0)) * 3 : 0);
+                    c0_ = __ldg(p);
+                    c1_ = __ldg(p + 1);
+                    c2_ = __ldg(p + 2);
+                }
+                const float w = alpha * T;  // raster.hpp:244-249
+                acc0 = fmaf(c0_, w, acc0);
+                acc1 = fmaf(c1_, w, acc1);
+                acc2 = fmaf(c2_, w, acc2);
+                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                last = c0 + bit;
+                if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;  // raster.hpp:250
             }
             if (__all_sync(kFull, done)) break;
         }
