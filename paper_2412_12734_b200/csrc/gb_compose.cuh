@@ -70,13 +70,22 @@ __device__ __forceinline__ void red_add(float* p, float v) {
     if (v != 0.0f) atomicAdd(p, v);
 }
 
-// p[0..2] += (a, b, c) with one 8-byte vector red and one scalar red (branch-free on alignment)
+// p[0..2] += (a, b, c)
+#ifdef GB_RED3_SCALAR
+__device__ __forceinline__ void red3(float* p, float a, float b, float c) {  // experiment: three scalar reds
+    atomicAdd(p, a);
+    atomicAdd(p + 1, b);
+    atomicAdd(p + 2, c);
+}
+#else
+// one 8-byte vector red and one scalar red (branch-free on alignment)
 __device__ __forceinline__ void red3(float* p, float a, float b, float c) {
     const bool even = (reinterpret_cast<uintptr_t>(p) & 7) == 0;
     float2* pv = reinterpret_cast<float2*>(even ? p : p + 1);
     atomicAdd(pv, even ? make_float2(a, b) : make_float2(b, c));
     atomicAdd(even ? p + 2 : p, even ? c : a);
 }
+#endif
 
 // p[0..3] += (a, b, c, d) with one 16-byte vector red (p 16-B aligned)
 __device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {

@@ -90,7 +90,7 @@ __device__ void build_geom(const ProjParams& p, int64_t k, Geom& g) {
 // raster.hpp:61-86 + 93-101 (and the pinhole dual-conic box).  Writes the
 // inclusive pixel range; returns false when culled.
 __device__ bool cull_rect(const ProjParams& p, int64_t k, const Geom& g, int& x0, int& x1, int& y0, int& y1) {
-    if (p.alpha_skip > 0.0 && 1.0 / (1.0 + exp(-(double)p.opacity[k])) < p.alpha_skip) return false;
+    if (p.alpha_skip > 0.0 && g.alpha_k < p.alpha_skip) return false;  // g.alpha_k: the same expression
     double min_x, max_x, min_y, max_y;
     if (p.cutoff > 0.0) {
         if (p.mode == GB_MODE_ORTHO) {
@@ -162,12 +162,15 @@ __device__ bool cull_rect(const ProjParams& p, int64_t k, const Geom& g, int& x0
 // relative + 0.05 px), so the fp32 evaluation there sits > 0.1% below the
 // threshold and skipping it cannot change a decision.  Whole image when the
 // threshold is disabled or the ellipse is not entirely in front of the camera.
-__device__ float4 alpha_box(const ProjParams& p, int64_t k, const Geom& g) {
+// uv radius of the alpha-skip region, enlarged as described above (alpha_box / alpha_ellipse)
+__device__ __forceinline__ double alpha_radius(const ProjParams& p, const Geom& g) {
+    return sqrt(2.0 * log(g.alpha_k / p.alpha_skip)) * 1.001 + 1e-3;
+}
+
+__device__ float4 alpha_box(const ProjParams& p, int64_t k, const Geom& g, double r) {
     const float4 all = make_float4(-1e30f, 1e30f, -1e30f, 1e30f);
     if (!(p.alpha_skip > 0.0)) return all;
-    const double ak = 1.0 / (1.0 + exp(-(double)p.opacity[k]));
-    if (!(ak > p.alpha_skip)) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never composited
-    const double r = sqrt(2.0 * log(ak / p.alpha_skip)) * 1.001 + 1e-3;
+    if (!(g.alpha_k > p.alpha_skip)) return make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never composited
     double min_x, max_x, min_y, max_y;
     if (p.mode == GB_MODE_ORTHO) {
         const double th = (double)p.theta[k];
@@ -222,13 +225,11 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
 // alpha_box.  Record: a = (e_x, e_y, Q11, Q22), b = (Q12, Q12/Q22, Q12/Q11, 0).
 // All-zero Q passes everything (threshold disabled, or the region reaches
 // behind the camera and is not an ellipse); e = +inf-like passes nothing.
-__device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g) {
+__device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g, double r, const float4 box) {
     const CullRec all = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
     const CullRec none = {make_float4(1e30f, 1e30f, 1.f, 1.f), make_float4(0.f, 0.f, 0.f, 0.f)};
     if (!(p.alpha_skip > 0.0)) return all;
-    const double ak = 1.0 / (1.0 + exp(-(double)p.opacity[k]));
-    if (!(ak > p.alpha_skip)) return none;
-    const double r = sqrt(2.0 * log(ak / p.alpha_skip)) * 1.001 + 1e-3;
+    if (!(g.alpha_k > p.alpha_skip)) return none;
     const double r2 = r * r;
     double A11, A12, A22, ex, ey;
     if (p.mode == GB_MODE_ORTHO) {
@@ -247,6 +248,7 @@ __device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g) 
         if (!(M[8] - r * lat > 0.0)) return all;
         // pixel ~ H (u, v, 1); (u, v, 1) ~ adj(H) pixel; region: w0^2 + w1^2 - r^2 w2^2 <= 0
         double H0[3], H1[3], H2[3], c0[3], c1[3], c2[3];
+#pragma unroll
         for (int j = 0; j < 3; ++j) {
             H0[j] = p.fx * M[j] + p.cx * M[6 + j];
             H1[j] = p.fy * M[3 + j] + p.cy * M[6 + j];
@@ -258,7 +260,9 @@ __device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g) 
         // adj(H) has columns c0, c1, c2, so w_m = sum_j p_j c_j[m] and C[j][l] = <c_j, c_l> under diag(1, 1, -r^2)
         const double* col[3] = {c0, c1, c2};
         double C[3][3];
+#pragma unroll
         for (int j = 0; j < 3; ++j)
+#pragma unroll
             for (int l = 0; l < 3; ++l)
                 C[j][l] = col[j][0] * col[l][0] + col[j][1] * col[l][1] - r2 * col[j][2] * col[l][2];
         // C is over p = (x, y, 1) with x, y continuous pixel coordinates
@@ -282,7 +286,6 @@ __device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g) 
     // circumscribing the alpha-box (axis-aligned, no cancellation).
     const double tr = 0.5 * (A11 + A22), dq = sqrt(fmax(tr * tr - (A11 * A22 - A12 * A12), 0.0));
     if (!(tr - dq > 0.0) || (tr + dq) > 4096.0 * (tr - dq)) {
-        const float4 box = alpha_box(p, k, g);
         if (box.x > box.y || box.z > box.w) return none;
         if (box.x < -1e29f || box.y > 1e29f || box.z < -1e29f || box.w > 1e29f) return all;
         const double hx = 0.5 * ((double)box.y - (double)box.x) + 0.5, hy = 0.5 * ((double)box.w - (double)box.z) + 0.5;
@@ -330,6 +333,7 @@ __device__ __forceinline__ void pinhole_coeffs(const Geom& g, double dxe, double
     cross3(M0, M1, pc.C0);
     cross3(M1, M2, pc.Cx);
     cross3(M2, M0, pc.Cy);
+#pragma unroll
     for (int j = 0; j < 3; ++j) pc.E[j] = pc.C0[j] + dxe * pc.Cx[j] + dye * pc.Cy[j];
 }
 
@@ -374,9 +378,10 @@ __global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeade
                   : make_float4(0.f, nan, (float)g.alpha_k, hx);
         h.h2 = make_float4(hy, __int_as_float(cxi), __int_as_float(cyi), 0.0f);
     }
-    h.h3 = alpha_box(p, k, g);
+    const double ar = p.alpha_skip > 0.0 && g.alpha_k > p.alpha_skip ? alpha_radius(p, g) : 0.0;
+    h.h3 = alpha_box(p, k, g, ar);
     hdr[k] = h;
-    cull[k] = alpha_ellipse(p, k, g);
+    cull[k] = alpha_ellipse(p, k, g, ar, h.h3);
 }
 
 // K5: chain the K4 screen-space sums to the raw parameters and ADD into the
