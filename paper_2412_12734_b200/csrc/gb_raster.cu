@@ -779,6 +779,7 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
     acc0 = acc1 = acc2 = 0.0f;
     last = -1;
     bool done = !wp.inside;
+    const float early = rc.early_stop > 0.0f ? rc.early_stop : -1.0f;  // T >= 0: a disabled stop never fires
     for (int c0 = 0; c0 < total && !__all_sync(kFull, done); c0 += 32) {
         int idl = -1;
         bool pass = false;
@@ -853,7 +854,7 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
                 acc2 = fmaf(c2_, w, acc2);
                 T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
                 last = c0 + bit;
-                if (rc.early_stop > 0.0f && T < rc.early_stop) done = true;  // raster.hpp:250
+                if (T < early) done = true;  // raster.hpp:250
             }
             if (__all_sync(kFull, done)) break;
         }
