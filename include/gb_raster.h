@@ -283,6 +283,27 @@ GB_API gb_status gb_adam_step(gb_context *ctx, int32_t mode, int64_t count, int3
 /* Synchronous.  group: 0 position, 1 theta/quat, 2 log_scale, 3 opacity, 4 grid. */
 GB_API gb_status gb_adam_check(gb_context *ctx, int32_t *group, int64_t *index);
 
+/* Adam over explicit segments: the sharded optimiser of the multi-GPU step, where each rank updates its
+ * slice of a flat parameter buffer (optim.hpp:84-88 per element; the group selects the rate and, for
+ * group 0, the position_gamma schedule).  Two phases, so that ranks can agree on the non-finite guard
+ * (optim.hpp:81-83) before anything is updated:
+ *   phase 0: scan the segments' gradients; *flag (a device int64 the caller sets to GB_ADAM_FLAG_CLEAR)
+ *            is lowered to (group << 48) | index-in-segment of a non-finite gradient;
+ *   (the caller may min-reduce *flag across ranks)
+ *   phase 1: state->t += 1 and update every segment, unless *flag shows a non-finite gradient.
+ * Asynchronous; the moments in the segments use the gradient layout. */
+typedef struct {
+    float *param;
+    const float *grad;
+    float *m, *v;
+    int64_t len;
+    int32_t group; /* 0 position, 1 theta/quat, 2 log_scale, 3 opacity_logit, 4 grid */
+    int32_t _pad;
+} gb_adam_segment;
+#define GB_ADAM_FLAG_CLEAR 0x7fffffffffffffffLL
+GB_API gb_status gb_adam_segments(gb_context *ctx, int32_t phase, const gb_adam_segment *seg, int32_t nseg,
+                                  gb_adam_state *state, const gb_learning_rates *lrs, int64_t *flag);
+
 /* ---- GBIL splat files (serialize.hpp:15-124) -------------------------------
  * Header "GBIL", u32 version, u32 K, u32 N, f32 sigma, then K little-endian
  * fp32 records.  Version 1 is the reference's (ortho) record: x, y, depth_key,

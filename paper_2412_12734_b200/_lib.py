@@ -19,6 +19,7 @@ GB_MISMATCH = 2
 GB_CUDA_ERROR = 3
 GB_OOM = 4
 GB_NONFINITE = 5
+ADAM_FLAG_CLEAR = 0x7FFFFFFFFFFFFFFF  # GB_ADAM_FLAG_CLEAR
 GB_NOT_SUPPORTED = 6
 GB_IO_ERROR = 7
 
@@ -43,6 +44,18 @@ class Splats(C.Structure):
         ("log_scale", C.c_void_p),
         ("opacity_logit", C.c_void_p),
         ("grid_values", C.c_void_p),
+    ]
+
+
+class AdamSegment(C.Structure):
+    _fields_ = [
+        ("param", C.c_void_p),
+        ("grad", C.c_void_p),
+        ("m", C.c_void_p),
+        ("v", C.c_void_p),
+        ("len", C.c_int64),
+        ("group", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 
@@ -189,6 +202,10 @@ _SIGS = {
          C.POINTER(LearningRatesC)],
     ),
     "gb_adam_check": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "gb_adam_segments": (
+        C.c_int,
+        [P, C.c_int32, C.POINTER(AdamSegment), C.c_int32, C.POINTER(AdamStateC), C.POINTER(LearningRatesC), P],
+    ),
     "gb_ssim": (C.c_int, [P, P, P, C.c_int32, C.c_int32, C.c_int32, P, P, C.c_float]),
     "gb_psnr": (C.c_int, [P, P, P, C.c_int64, C.POINTER(C.c_double)]),
     "gb_fit_initialize": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_uint64, P, P, P, P, P, P]),
@@ -223,8 +240,9 @@ lib = _load()
 
 
 class GBError(RuntimeError):
-    def __init__(self, status: int, where: str):
-        msg = lib.gb_last_error_string().decode(errors="replace")
+    def __init__(self, status: int, where: str, msg: str = None):
+        if msg is None:
+            msg = lib.gb_last_error_string().decode(errors="replace")
         super().__init__(f"{where}: status {status}: {msg}")
         self.status = status
 

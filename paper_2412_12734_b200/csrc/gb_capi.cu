@@ -1035,6 +1035,51 @@ gb_status gb_adam_step(gb_context* ctx, int32_t mode, int64_t count, int32_t n, 
     return GB_OK;
 }
 
+gb_status gb_adam_segments(gb_context* ctx, int32_t phase, const gb_adam_segment* seg, int32_t nseg,
+                           gb_adam_state* state, const gb_learning_rates* lrs, int64_t* flag) {
+    if (!ctx || (nseg > 0 && !seg) || !state || !lrs || !flag) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (phase != 0 && phase != 1) return fail(GB_INVALID_ARGUMENT, "adam_segments: phase must be 0 or 1");
+    // optim.hpp:33-39
+    if (!(lrs->position > 0.0 && lrs->theta > 0.0 && lrs->log_scale > 0.0 && lrs->opacity_logit > 0.0 &&
+          lrs->color_grid > 0.0))
+        return fail(GB_INVALID_ARGUMENT, "LearningRates: all rates must be positive");
+    if (!(lrs->position_gamma > 0.0 && lrs->position_gamma <= 1.0))
+        return fail(GB_INVALID_ARGUMENT, "LearningRates: position_gamma must be in (0, 1]");
+    for (int i = 0; i < nseg; ++i) {
+        if (seg[i].group < 0 || seg[i].group > 4 || seg[i].len < 0)
+            return fail(GB_INVALID_ARGUMENT, "adam_segments: bad segment %d", i);
+        if (seg[i].len > 0 && (!seg[i].param || !seg[i].grad || !seg[i].m || !seg[i].v))
+            return fail(GB_INVALID_ARGUMENT, "adam_segments: null buffer in segment %d", i);
+    }
+    if (gb_status st = set_device(ctx)) return st;
+    cudaStream_t stream = ctx->stream;
+    auto* bad = reinterpret_cast<unsigned long long*>(flag);
+    ProfScope ps(ctx, GB_K_ADAM);
+    if (phase == 0) {
+        for (int i = 0; i < nseg; ++i) {
+            if (seg[i].len == 0) continue;
+            GB_CUDA(gb::launch_adam_check(seg[i].grad, seg[i].len, seg[i].group, bad, ctx->sm_count, stream));
+            ctx->launches++;
+        }
+        return GB_OK;
+    }
+    state->t += 1;
+    const double bias1 = 1.0 - std::pow(state->beta1, (double)state->t);
+    const double bias2 = 1.0 - std::pow(state->beta2, (double)state->t);
+    const double rate[5] = {lrs->position * std::pow(lrs->position_gamma, (double)(state->t - 1)), lrs->theta,
+                            lrs->log_scale, lrs->opacity_logit, lrs->color_grid};
+    for (int i = 0; i < nseg; ++i) {
+        if (seg[i].len == 0) continue;
+        GB_CUDA(gb::launch_adam_update(seg[i].param, seg[i].grad, seg[i].m, seg[i].v, seg[i].len,
+                                       (float)rate[seg[i].group], (float)state->beta1, (float)state->beta2,
+                                       (float)(1.0 - state->beta1), (float)(1.0 - state->beta2),
+                                       (float)state->epsilon, (float)(1.0 / bias1), (float)(1.0 / bias2), bad,
+                                       ctx->sm_count, stream));
+        ctx->launches++;
+    }
+    return GB_OK;
+}
+
 gb_status gb_adam_check(gb_context* ctx, int32_t* group, int64_t* index) {
     if (!ctx) return fail(GB_INVALID_ARGUMENT, "ctx is null");
     if (!ctx->adam_bad.p) return GB_OK;

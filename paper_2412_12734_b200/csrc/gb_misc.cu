@@ -52,7 +52,7 @@ cudaError_t launch_loss(int kind, const float* color, const float* target, int64
     return cudaGetLastError();
 }
 
-// first non-finite gradient, encoded (group << 48) | index; ~0 = none
+// first non-finite gradient, encoded (group << 48) | index; ~0 (or INT64_MAX, gb_adam_segments) = none
 __global__ void __launch_bounds__(256) k_adam_check(const float* __restrict__ g, int64_t n, int group,
                                                     unsigned long long* __restrict__ bad) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_adam_update(float* __restrict__ p, cons
                                                      float b1, float b2, float omb1, float omb2, float eps,
                                                      float inv_bias1, float inv_bias2,
                                                      const unsigned long long* __restrict__ bad) {
-    if (*bad != ~0ull) return;
+    if (*bad < (1ull << 62)) return;  // a non-finite gradient was found (clear values: ~0 or INT64_MAX)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const bool vec = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
                        reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;

@@ -318,21 +318,25 @@ class GradientBuffer:
     all-reduce them with a single collective; the per-group tensors are views.
     """
 
-    def __init__(self, like: SplatSet):
+    def __init__(self, like: SplatSet, multiple: int = 4):
         self.mode = like.mode
         self.count = like.count
         self.grid_config = like.grid_config
         shapes = [(f, tuple(getattr(like, f).shape)) for f in _FIELDS if getattr(like, f) is not None]
-        # keep every group 16-byte aligned (vector red.global.add on the texel grads)
+        # keep every group 16-byte aligned (vector red.global.add on the texel grads); the total is padded
+        # to `multiple` elements (the sharded optimiser splits the buffer evenly over the ranks)
         pad = lambda n: (n + 3) & ~3
         total = sum(pad(int(np.prod(s))) for _, s in shapes)
+        total = -(-total // multiple) * multiple
         self.flat = torch.zeros(total, dtype=torch.float32, device=like.device)
+        self.offsets = {}
         o = 0
         for f in _FIELDS:
             setattr(self, f, None)
         for f, s in shapes:
             n = int(np.prod(s))
             setattr(self, f, self.flat[o:o + n].view(s))
+            self.offsets[f] = (o, n)
             o += pad(n)
 
     def zero_(self) -> "GradientBuffer":
@@ -593,13 +597,20 @@ class AdamConfig:
 
 
 class AdamState:
-    """optim.hpp:50-72: zero moments with the gradient layout, t counts completed steps."""
+    """optim.hpp:50-72: zero moments with the gradient layout, t counts completed steps.
+    ``moments=False``: step count and config only (the sharded optimiser keeps its own slices)."""
 
-    def __init__(self, like: SplatSet, config: AdamConfig = None):
+    def __init__(self, like: SplatSet, config: AdamConfig = None, moments: bool = True):
         self.config = config or AdamConfig()
         self.t = 0
-        self.m = GradientBuffer(like)
-        self.v = GradientBuffer(like)
+        self.m = GradientBuffer(like) if moments else None
+        self.v = GradientBuffer(like) if moments else None
+
+    def to_c(self) -> _lib.AdamStateC:
+        empty = _lib.Grads()
+        return _lib.AdamStateC(self.t, self.config.beta1, self.config.beta2, self.config.epsilon,
+                               self.m.to_c() if self.m is not None else empty,
+                               self.v.to_c() if self.v is not None else empty)
 
 
 def adam_step(params: SplatSet, grads: GradientBuffer, state: AdamState, lrs: LearningRates,
@@ -611,8 +622,7 @@ def adam_step(params: SplatSet, grads: GradientBuffer, state: AdamState, lrs: Le
     p = _lib.Grads(_ptr(params.position), _ptr(params.depth_key), _ptr(params.theta), _ptr(params.quat),
                    _ptr(params.log_scale), _ptr(params.opacity_logit), _ptr(params.grid))
     g = grads.to_c()
-    st = _lib.AdamStateC(state.t, state.config.beta1, state.config.beta2, state.config.epsilon, state.m.to_c(),
-                         state.v.to_c())
+    st = state.to_c()
     c_lrs = lrs.to_c()
     check(lib.gb_adam_step(ctx.handle, params.mode, params.count, params.grid_config.n, C.byref(p), C.byref(g),
                            C.byref(st), C.byref(c_lrs)), "adam_step")

@@ -1,12 +1,13 @@
 """View-sharded multi-view training step (BASELINE.json configs[3]).
 
 Each rank owns a fixed subset of camera views and replicated primitives.  Per
-step and per owned view it runs, on one CUDA stream, K1 projection -> K2 tile
-binning -> K3 forward + K6 L1 loss + K4 backward (one fused kernel by default;
-``fused=False`` runs the three reference-shaped calls) -> K5, accumulating into one
-flat fp32 gradient buffer; then ONE collective (NCCL all-reduce, sum) makes
-the gradients identical on every rank and K7 Adam updates the replicated
-parameters.  This is the only cross-GPU exchange of the path.
+step and per owned view it runs K1 projection -> K2 tile binning -> K3 forward
+-> K6 L1 loss -> K4 backward -> K5 (``fused=True``: K3+K6+K4 as one kernel),
+accumulating into one flat fp32 gradient buffer.  Then the gradients are
+reduce-scattered (NCCL), each rank runs K7 Adam on its 1/world slice of the
+flat parameter buffer, and the parameters are all-gathered
+(``sharded_adam=False``: one all-reduce and a replicated Adam instead).  These
+collectives are the only cross-GPU exchange of the path.
 
 The reference's driver loop (train.hpp:174-219, ``fit``) is single-image and
 single-process; this step is its multi-view, multi-GPU generalisation for the
@@ -14,9 +15,12 @@ BASELINE configs (L1 loss, Adam with the reference's defaults, optim.hpp).
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import List, Optional, Sequence
 
 import torch
+
+from . import _lib
 
 from .raster import (AdamConfig, AdamState, GradientBuffer, LearningRates, RasterConfig, RenderOutput, SplatSet,
                      StepGraph, TileBinning, adam_step, all_contexts, build_binning, context, l1_loss,
@@ -38,6 +42,96 @@ def reduce_gradients(grads: GradientBuffer, process_group=None) -> None:
     if torch.distributed.is_available() and torch.distributed.is_initialized():
         if torch.distributed.get_world_size(process_group) > 1:
             torch.distributed.all_reduce(grads.flat, op=torch.distributed.ReduceOp.SUM, group=process_group)
+
+
+_ADAM_GROUP = {"position": 0, "theta": 1, "quat": 1, "log_scale": 2, "opacity_logit": 3, "grid": 4}
+
+
+class ShardedAdam:
+    """The step's optimiser over ranks (SURVEY §8(e) variant): reduce-scatter the flat gradient buffer,
+    Adam on this rank's 1/world slice of a flat parameter buffer (gb_adam_segments), all-gather the
+    parameters.  The collective moves the same bytes as one all-reduce, but each rank updates and keeps
+    moments for 1/world of the parameters.  The non-finite guard (optim.hpp:81-83) is agreed across ranks
+    (min-reduced flag) before anything is updated.  At world size 1 it is the grouped Adam on one slice.
+
+    The splats' parameter tensors become views into ``flat`` (same layout as the gradient buffer)."""
+
+    def __init__(self, splats: SplatSet, grads: GradientBuffer, state: AdamState, process_group=None,
+                 segment_update=None):
+        """``segment_update(phase, ranges, state, lrs, flag)``: replaces the gb_adam_segments call --
+        a hook for the multi-process CPU tests only (there is no CPU optimiser in the product)."""
+        dist = torch.distributed
+        self._hook = segment_update
+        self.pg = process_group
+        self.world = dist.get_world_size(process_group) if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank(process_group) if self.world > 1 else 0
+        if grads.flat.numel() % (4 * self.world):
+            raise ValueError("ShardedAdam: gradient buffer not padded to 4 * world elements")
+        self.splats, self.grads, self.state = splats, grads, state
+        self.flat = torch.zeros_like(grads.flat)
+        for f, (o, n) in grads.offsets.items():
+            t = getattr(splats, f)
+            v = self.flat[o:o + n].view(t.shape)
+            v.copy_(t)
+            setattr(splats, f, v)
+        S = self.flat.numel() // self.world
+        self.lo, self.S = self.rank * S, S
+        dev = grads.flat.device
+        self.g_shard = grads.flat if self.world == 1 else torch.empty(S, dtype=torch.float32, device=dev)
+        self.m = torch.zeros(S, dtype=torch.float32, device=dev)
+        self.v = torch.zeros(S, dtype=torch.float32, device=dev)
+        self.flag = torch.empty(1, dtype=torch.int64, device=dev)
+        segs = []
+        self.ranges = []  # (flat lo, flat hi, group) of this rank's slice
+        gbase = self.lo if self.world > 1 else 0  # g_shard: this rank's slice, or (one rank) the whole buffer
+        for f, (o, n) in grads.offsets.items():
+            if f == "depth_key":  # never updated (optim.hpp:95)
+                continue
+            a, b = max(o, self.lo), min(o + n, self.lo + S)
+            if a >= b:
+                continue
+            self.ranges.append((a, b, _ADAM_GROUP[f]))
+            segs.append(_lib.AdamSegment(self.flat.data_ptr() + 4 * a, self.g_shard.data_ptr() + 4 * (a - gbase),
+                                         self.m.data_ptr() + 4 * (a - self.lo), self.v.data_ptr() + 4 * (a - self.lo),
+                                         b - a, _ADAM_GROUP[f], 0))
+        self._segs = (_lib.AdamSegment * max(1, len(segs)))(*segs)
+        self._nseg = len(segs)
+        self._names = [f for f in grads.offsets if f != "depth_key"]
+
+    def step(self, lrs: LearningRates, check_finite: bool = False) -> None:
+        from .raster import context
+        from ._lib import check, lib
+
+        dist = torch.distributed
+        if self.world > 1:
+            dist.reduce_scatter_tensor(self.g_shard, self.grads.flat, op=dist.ReduceOp.SUM, group=self.pg)
+        self.flag.fill_(_lib.ADAM_FLAG_CLEAR)
+        if self._hook is not None:
+            self._hook(0, self, lrs)
+            if self.world > 1:
+                dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
+            self._hook(1, self, lrs)
+        else:
+            ctx = context(self.flat.device)
+            st = self.state.to_c()
+            c_lrs = lrs.to_c()
+            check(lib.gb_adam_segments(ctx.handle, 0, self._segs, self._nseg, C.byref(st), C.byref(c_lrs),
+                                       self.flag.data_ptr()), "adam_step")
+            if self.world > 1:
+                dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
+            check(lib.gb_adam_segments(ctx.handle, 1, self._segs, self._nseg, C.byref(st), C.byref(c_lrs),
+                                       self.flag.data_ptr()), "adam_step")
+            self.state.t = st.t
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.flat, self.flat[self.lo:self.lo + self.S], group=self.pg)
+        if check_finite:
+            v = int(self.flag.item())
+            if v != _lib.ADAM_FLAG_CLEAR:
+                grp = v >> 48
+                names = ("position", "theta", "log_scale", "opacity_logit", "color_grid")
+                raise _lib.NonFinite(_lib.GB_NONFINITE, "adam_step",
+                                     f"non-finite gradient in group '{names[grp & 7]}' "
+                                     f"(segment index {v & ((1 << 48) - 1)}); no parameter was updated")
 
 
 class _Lane:
@@ -63,15 +157,20 @@ class ViewShardedTrainer:
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
                  lanes: int = 2, fused: bool = False, async_binning: bool = True, graph: bool = False,
-                 capacity_margin: float = 1.25):
+                 capacity_margin: float = 1.25, sharded_adam: bool = True):
         self.splats = splats
         self.cameras = list(cameras)
         self.views = list(views)
         self.lrs = lrs or LearningRates()
         self.raster = raster or RasterConfig()
-        self.grads = GradientBuffer(splats)
-        self.state = AdamState(splats, adam)
         self.pg = process_group
+        dist = torch.distributed
+        world = dist.get_world_size(process_group) if dist.is_available() and dist.is_initialized() else 1
+        self.grads = GradientBuffer(splats, multiple=4 * world)
+        # sharded optimiser (reduce-scatter, Adam on 1/world of the parameters, all-gather) or the
+        # replicated one (all-reduce, full Adam on every rank)
+        self.state = AdamState(splats, adam, moments=not sharded_adam)
+        self.opt = ShardedAdam(splats, self.grads, self.state, process_group) if sharded_adam else None
         self.check_finite = check_finite
         self.fused = fused
         dev = splats.device
@@ -252,6 +351,9 @@ class ViewShardedTrainer:
         self._pair_views = 0
 
     def _finish(self) -> None:
+        if self.opt is not None:
+            self.opt.step(self.lrs, check_finite=self.check_finite)
+            return
         reduce_gradients(self.grads, self.pg)
         adam_step(self.splats, self.grads, self.state, self.lrs, check_finite=self.check_finite)
 

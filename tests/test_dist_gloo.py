@@ -114,3 +114,129 @@ def test_shard_views_partitions():
         got = sorted(v for r in range(w) for v in shard_views(n, r, w))
         assert got == list(range(n))
     assert [shard_views(64, r, 8, per_rank=8) for r in range(8)][3] == list(range(24, 32))
+
+
+# ---------------------------------------------------------------------------------------------
+# the sharded optimiser (reduce-scatter -> Adam on 1/world of the flat parameters -> all-gather)
+# ---------------------------------------------------------------------------------------------
+def _cpu_segment_update(phase, opt, lrs):
+    """Test stand-in for gb_adam_segments on CPU tensors: the oracle's Adam per (flat range, group)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+
+    from parity import O
+
+    base = opt.lo if opt.world > 1 else 0
+    if phase == 0:
+        for a, b, grp in opt.ranges:
+            g = opt.g_shard[a - base:b - base].numpy()
+            bad = np.nonzero(~np.isfinite(g))[0]
+            if bad.size:
+                opt.flag[0] = min(int(opt.flag[0]), (grp << 48) | int(bad[0]))
+        return
+    if int(opt.flag[0]) < (1 << 62):
+        opt.state.t += 1
+        return
+    opt.state.t += 1
+    t = opt.state.t
+    rates = [lrs.position * lrs.position_gamma ** (t - 1), lrs.theta, lrs.log_scale, lrs.opacity_logit,
+             lrs.color_grid]
+    c = opt.state.config
+    for a, b, grp in opt.ranges:
+        p = opt.flat[a:b].numpy().astype(np.float64)
+        g = opt.g_shard[a - base:b - base].numpy().astype(np.float64)
+        m = opt.m[a - opt.lo:b - opt.lo].numpy().astype(np.float64)
+        v = opt.v[a - opt.lo:b - opt.lo].numpy().astype(np.float64)
+        p1, m1, v1, _ = O.adam_group(p, g, m, v, rates[grp], c.beta1, c.beta2, c.epsilon, 1 - c.beta1 ** t,
+                                     1 - c.beta2 ** t)
+        opt.flat[a:b] = torch.as_tensor(p1, dtype=torch.float32)
+        opt.m[a - opt.lo:b - opt.lo] = torch.as_tensor(m1, dtype=torch.float32)
+        opt.v[a - opt.lo:b - opt.lo] = torch.as_tensor(v1, dtype=torch.float32)
+
+
+def _sharded_worker(rank, world, port, out_dir, nan_rank):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200.train import ShardedAdam
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    arrays, _ = _scene()
+    splats = gb.SplatSet.from_numpy(gb.raster.MODE_PINHOLE, gb.ColorGridConfig(2), device="cpu", **arrays)
+    grads = gb.GradientBuffer(splats, multiple=4 * world)
+    rng = np.random.default_rng(100 + rank)  # each rank's partial gradient
+    grads.flat.copy_(torch.as_tensor(rng.standard_normal(grads.flat.numel()), dtype=torch.float32))
+    if rank == nan_rank:
+        grads.quat.view(-1)[3] = float("nan")
+    state = gb.AdamState(splats, moments=False)
+    opt = ShardedAdam(splats, grads, state, segment_update=_cpu_segment_update)
+    lrs = gb.LearningRates(position_gamma=0.9)
+    p0 = {f: t.clone() for f, t in splats.tensors().items()}
+    err = ""
+    try:
+        opt.step(lrs, check_finite=True)
+        opt.step(lrs, check_finite=True)
+    except gb.raster.NonFinite as e:
+        err = str(e)
+    np.savez(os.path.join(out_dir, f"sh{rank}.npz"), flat=opt.flat.numpy(), t=state.t, err=err,
+             ranges=np.array([(a, b, g) for a, b, g in opt.ranges] or [(0, 0, -1)]),
+             unchanged=all(torch.equal(p0[f], t) for f, t in splats.tensors().items()),
+             views=all(t.data_ptr() >= opt.flat.data_ptr() for t in splats.tensors().values()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_adam_gloo(tmp_path, world):
+    """Every parameter is updated by exactly one rank, all ranks end with identical parameters, and the
+    result equals a single-process Adam on the summed gradients, two steps in a row."""
+    import torch.multiprocessing as mp
+
+    mp.start_processes(_sharded_worker, args=(world, _free_port(), str(tmp_path), -1), nprocs=world,
+                       start_method="spawn")
+    r = [np.load(tmp_path / f"sh{i}.npz") for i in range(world)]
+    for x in r[1:]:
+        assert np.array_equal(x["flat"], r[0]["flat"])
+    assert all(bool(x["views"]) and int(x["t"]) == 2 and str(x["err"]) == "" for x in r)
+    covered = sorted((int(a), int(b)) for x in r for a, b, g in x["ranges"] if g >= 0)
+    for (a0, b0), (a1, b1) in zip(covered, covered[1:]):
+        assert b0 <= a1  # disjoint
+    # single-process reference: Adam on the sum of the ranks' partial gradients, per group
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from parity import O
+
+    arrays, _ = _scene()
+    splats = gb.SplatSet.from_numpy(gb.raster.MODE_PINHOLE, gb.ColorGridConfig(2), device="cpu", **arrays)
+    grads = gb.GradientBuffer(splats, multiple=4 * world)
+    gsum = sum(np.random.default_rng(100 + k).standard_normal(grads.flat.numel()).astype(np.float32)
+               .astype(np.float64) for k in range(world))
+    lrs = gb.LearningRates(position_gamma=0.9)
+    rates = {"position": [lrs.position, lrs.position * 0.9], "quat": [lrs.theta] * 2,
+             "log_scale": [lrs.log_scale] * 2, "opacity_logit": [lrs.opacity_logit] * 2, "grid": [lrs.color_grid] * 2}
+    for f, (o, n) in grads.offsets.items():
+        p = np.asarray(arrays[f], np.float64).ravel()
+        m = np.zeros_like(p)
+        v = np.zeros_like(p)
+        g = gsum[o:o + n]
+        for t in (1, 2):
+            p, m, v, _ = O.adam_group(p, g, m, v, rates[f][t - 1], 0.9, 0.999, 1e-8, 1 - 0.9 ** t, 1 - 0.999 ** t)
+        np.testing.assert_allclose(r[0]["flat"][o:o + n], p, rtol=1e-5, atol=1e-6, err_msg=f)
+
+
+def test_sharded_adam_nonfinite_agreement(tmp_path):
+    """A non-finite gradient on one rank's input stops the update on every rank (optim.hpp:81-83)."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    mp.start_processes(_sharded_worker, args=(world, _free_port(), str(tmp_path), 1), nprocs=world,
+                       start_method="spawn")
+    r = [np.load(tmp_path / f"sh{i}.npz") for i in range(world)]
+    for x in r:
+        assert bool(x["unchanged"]), "no parameter may change"
+        assert "non-finite gradient in group 'theta'" in str(x["err"])

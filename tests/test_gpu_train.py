@@ -249,3 +249,39 @@ def test_trainer_modes_match_blocking(mode):
     tr.step_host(host)
     tr.step(tg)
     torch.cuda.synchronize()
+
+
+def test_sharded_adam_single_rank_matches_adam_step():
+    """ShardedAdam at world size 1 (gb_adam_segments over the flat parameter buffer) equals gb_adam_step
+    bit for bit, and its non-finite guard raises without updating anything."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200.train import ShardedAdam
+
+    n, K = 4, 1001
+    arrays = _pinhole_scene(K, n, 3)
+    a = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    b = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    ga, gb_ = gb.GradientBuffer(a), gb.GradientBuffer(b, multiple=4)
+    rng = np.random.default_rng(5)
+    g = torch.as_tensor(rng.standard_normal(ga.flat.numel()), dtype=torch.float32).cuda()
+    ga.flat.copy_(g)
+    gb_.flat.copy_(g)
+    lrs = gb.LearningRates(position_gamma=0.9)
+    sa = gb.AdamState(a)
+    sb = gb.AdamState(b, moments=False)
+    opt = ShardedAdam(b, gb_, sb)
+    for _ in range(3):
+        gb.adam_step(a, ga, sa, lrs, check_finite=True)
+        opt.step(lrs, check_finite=True)
+    torch.cuda.synchronize()
+    for f, t in a.tensors().items():
+        assert torch.equal(t, b.tensors()[f]), f
+    assert sa.t == sb.t == 3
+    before = {f: t.clone() for f, t in b.tensors().items()}
+    gb_.log_scale.view(-1)[7] = float("inf")
+    with pytest.raises(gb.raster.NonFinite, match="log_scale"):
+        opt.step(lrs, check_finite=True)
+    for f, t in b.tensors().items():
+        assert torch.equal(t, before[f]), f
