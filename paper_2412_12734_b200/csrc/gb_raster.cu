@@ -19,12 +19,17 @@
 //
 // K3 restates render_forward (raster.hpp:201-261) + bilinear
 // (texture.hpp:49-66); K4 restates render_backward (raster.hpp:277-387) +
-// adj_bilinear_accum (texture.hpp:77-111).  Instead of the reference's
-// per-(tile, rank) partial records and ordered reduction, K4 reduces each
-// entry's per-pixel contributions across the warp (a shared-memory transpose,
-// lane l summing half of row l/2) and issues red.global.add from the lanes
-// that own each sum, into (a) the caller's texel gradients and (b) a 48 B
-// per-primitive screen-space accumulator that K5 chains to the raw parameters.
+// adj_bilinear_accum (texture.hpp:77-111).  In the direct walks each entry is
+// shaded in one of four texel footprint classes (bwd_shade): lanes outside the
+// |u|, |v| < sigma texture square are clamped to one texel row/column, so a warp
+// whose active lanes never interpolate along an axis loads and scatters 1 or 2
+// texels per pixel instead of 4.  Instead of the reference's per-(tile, rank)
+// partial records and ordered reduction, K4 adds each entry's per-pixel
+// contributions with red.global.add into (a) the caller's texel gradients and
+// (b) a 48 B per-primitive screen-space accumulator that K5 chains to the raw
+// parameters: straight from every active lane when at most 12 lanes are active,
+// else after a warp reduction (a shared-memory transpose, lane l summing half
+// of row l/2).
 #include <cstdlib>
 #include <cstring>
 
