@@ -303,6 +303,18 @@ def run_ours(args):
         e2e = {"value": round(mpix / (e2e_ms / 1e3), 3), "unit": "MP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": len(views) * 4, "ms_per_step": round(e2e_ms, 3)}
 
+    # ---- replicas stay in sync: every rank holds bit-identical parameters ----
+    in_sync = True
+    if world > 1:
+        flat = trainer.opt.flat if trainer.opt is not None else torch.cat(
+            [t.reshape(-1) for t in trainer.splats.tensors().values()])
+        h = flat.view(torch.int32).to(torch.int64)
+        digest = torch.stack([(h * (torch.arange(h.numel(), device=h.device) % 1021 + 1)).sum(), h.sum()])
+        lo, hi = digest.clone(), digest.clone()
+        torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+        torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+        in_sync = bool(torch.equal(lo, hi))
+
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -371,6 +383,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "e2e": e2e,
+        "replicas_in_sync": in_sync,
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
