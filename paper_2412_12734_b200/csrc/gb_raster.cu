@@ -574,6 +574,19 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         const float r2 = smem_reduce<NS>(sv, wscratch, lane);
         if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
     }
+    if (CELL == kCellOne && NT != 1 && N > 1) {
+        // one texel per lane, and it is one of the four grid corners (by the signs of u, v): one warp
+        // reduction over the 4 corners x 3 channels instead of up to 32 reds on at most 4 addresses
+        const int q = on ? ((u > 0.0f) ? 2 : 0) + ((v > 0.0f) ? 1 : 0) : -1;
+        float tq[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) tq[i] = (q == i / 3) ? tg[i % 3] : 0.0f;
+        const float r2 = smem_reduce<12>(tq, wscratch, lane);
+        const int row = lane >> 1, qc = row / 3;
+        if ((lane & 1) == 0 && row < 12)
+            red_add(gg + 3 * (((qc >> 1) ? N - 1 : 0) * N + ((qc & 1) ? N - 1 : 0)) + row % 3, r2);
+        return;
+    }
     // texel gradients: one warp reduction when every active lane has the same base texel;
     // otherwise each lane adds its own texels -- cheaper than a reduction per distinct cell
     const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
@@ -923,8 +936,9 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
     }
 }
 
+// <= 64 registers: 4 CTAs (32 warps) per SM
 template <int MODE, int NT>
-__global__ void __launch_bounds__(256) k_backward_direct(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(256, 4) k_backward_direct(const uint2* __restrict__ ranges,
                                                          const int32_t* __restrict__ values,
                                                          const ScreenHeader* __restrict__ hdr,
                                                          const CullRec* __restrict__ cull, const float* __restrict__ tex,
