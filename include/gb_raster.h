@@ -243,10 +243,10 @@ GB_API gb_status gb_l1_loss(gb_context *ctx, const float *color, const float *ta
 GB_API gb_status gb_mse_loss(gb_context *ctx, const float *color, const float *target, int64_t n, float scale, float *grad,
                       float *loss);
 
-/* One view of a training step (train.hpp:120-133 around raster.hpp:201-371) in one pass:
+/* One view of a training step (train.hpp:120-133 around raster.hpp:201-371):
  *   gb_render_forward + gb_l1_loss (loss_kind GB_LOSS_L1) or gb_mse_loss (GB_LOSS_MSE) + gb_render_backward,
- * each pixel's forward, loss cotangent and backward done by the same warp while the entries it walked are
- * still cached.  target: HWC fp32 (device).  out: NULL, or forward buffers filled as gb_render_forward
+ * as the forward compositor with the loss in its epilogue (the image never round-trips through memory)
+ * followed by the backward compositor.  target: HWC fp32 (device).  out: NULL, or forward buffers filled as gb_render_forward
  * would; image_grad: NULL, or receives the cotangent; *loss (device float) += as the loss entry points
  * (summation order differs); g receives the gradients as gb_render_backward.  Per-pixel arithmetic is the
  * separate calls'; with GB_COMPOSITOR=grp|staged this runs as those three calls. */

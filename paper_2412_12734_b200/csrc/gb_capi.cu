@@ -900,16 +900,46 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
     }
     const gb::CamConst cc = make_cam_const(cam);
     const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
-    {
+    const int tiles = b->tiles_x * b->tiles_y;
+    if (gb::fused_single_kernel()) {
         ProfScope ps(ctx, GB_K_FUSED);
-        GB_CUDA(gb::launch_fused(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
-                                 b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
+        GB_CUDA(gb::launch_fused(cam->mode, s->grid.n, tiles, b->cfg.tile_size, b->ranges.as<uint2>(),
+                                 b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
                                  b->cull.as<gb::CullRec>(), s->grid_values, cc, rc, loss_kind, target, scale,
                                  out ? out->color : nullptr, out ? out->final_transmittance : nullptr,
                                  out ? out->last_rank : nullptr, image_grad, loss,
                                  K > 0 ? ctx->accum.as<float>() : nullptr, g->grid_values, stream));
+        ctx->launches += 1;
+    } else {  // K3 with the loss in its epilogue, then K4: no image round trip, no K6 pass
+        float* trans = out ? out->final_transmittance : nullptr;
+        int32_t* last = out ? out->last_rank : nullptr;
+        if (!out) {
+            GB_CUDA(ctx->fuse_trans.ensure(sizeof(float) * npix));
+            GB_CUDA(ctx->fuse_last.ensure(sizeof(int32_t) * npix));
+            trans = ctx->fuse_trans.as<float>();
+            last = ctx->fuse_last.as<int32_t>();
+        }
+        float* grad = image_grad;
+        if (!grad) {
+            GB_CUDA(ctx->fuse_grad.ensure(sizeof(float) * 3 * npix));
+            grad = ctx->fuse_grad.as<float>();
+        }
+        {
+            ProfScope ps(ctx, GB_K_FORWARD);
+            GB_CUDA(gb::launch_forward_loss(cam->mode, s->grid.n, tiles, b->cfg.tile_size, b->ranges.as<uint2>(),
+                                            b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
+                                            b->cull.as<gb::CullRec>(), s->grid_values, cc, rc, loss_kind, target,
+                                            scale, out ? out->color : nullptr, trans, last, grad, loss, stream));
+        }
+        {
+            ProfScope ps(ctx, GB_K_BACKWARD);
+            GB_CUDA(gb::launch_backward(cam->mode, s->grid.n, tiles, b->cfg.tile_size, b->ranges.as<uint2>(),
+                                        b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
+                                        b->cull.as<gb::CullRec>(), s->grid_values, cc, rc, trans, last, grad,
+                                        K > 0 ? ctx->accum.as<float>() : nullptr, g->grid_values, stream));
+        }
+        ctx->launches += 2;
     }
-    ctx->launches += 1;
     if (out) {
         out->splat_count = s->count;
         out->grid_n = s->grid.n;

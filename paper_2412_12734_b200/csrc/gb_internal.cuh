@@ -190,8 +190,13 @@ cudaError_t launch_backward_grp(int mode, int n, int tiles, int ts, const uint2*
                                 const float* trans, const int32_t* last, const float* image_grad, float* accum,
                                 float* grid_grad, cudaStream_t st);
 
-// gb_raster.cu: K3 + K6 + K4 in one kernel (direct compositors only)
+// gb_raster.cu: K3 + K6 + K4 in one kernel (direct compositors only), or K3 + K6 then K4
 bool fused_available();
+bool fused_single_kernel();
+cudaError_t launch_forward_loss(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                                const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                                const RasterConst& rc, int kind, const float* target, float scale, float* color,
+                                float* trans, int32_t* last, float* image_grad, float* loss, cudaStream_t st);
 cudaError_t launch_fused(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                          const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                          const RasterConst& rc, int kind, const float* target, float scale, float* color, float* trans,

@@ -936,6 +936,49 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
     }
 }
 
+// render_forward with the photometric loss (KIND 0 = L1, 1 = MSE; K6) in its epilogue: the pixel's
+// colour turns into the loss cotangent in registers, so the image is written only when asked for and
+// no separate loss pass runs.  T and the last rank are always written (the backward rewinds from them).
+template <int MODE, int NT, int KIND>
+__global__ void __launch_bounds__(256) k_forward_loss(const uint2* __restrict__ ranges,
+                                                      const int32_t* __restrict__ values,
+                                                      const ScreenHeader* __restrict__ hdr,
+                                                      const CullRec* __restrict__ cull, const float* __restrict__ tex,
+                                                      const CamConst cc, const RasterConst rc, int n_rt,
+                                                      const float* __restrict__ target, float scale,
+                                                      float* __restrict__ out_color, float* __restrict__ out_trans,
+                                                      int32_t* __restrict__ out_last, float* __restrict__ out_grad,
+                                                      float* __restrict__ loss) {
+    const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
+    float T, a0, a1, a2;
+    int last;
+    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
+    float l = 0.0f;
+    if (wp.inside) {
+        const size_t p = (size_t)wp.y * cc.width + wp.x;
+        const float c[3] = {fmaf(T, cc.bg[0], a0), fmaf(T, cc.bg[1], a1), fmaf(T, cc.bg[2], a2)};
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {  // K6 (gb_misc.cu k_loss), per pixel
+            const float d = c[ch] - target[p * 3 + ch];
+            float g;
+            if (KIND == 0) {
+                l += fabsf(d);
+                g = scale * (float)((d > 0.0f) - (d < 0.0f));
+            } else {
+                l = fmaf(d, d, l);
+                g = 2.0f * scale * d;
+            }
+            out_grad[p * 3 + ch] = g;
+            if (out_color) out_color[p * 3 + ch] = c[ch];
+        }
+        out_trans[p] = T;
+        out_last[p] = last;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
+    if ((threadIdx.x & 31) == 0 && loss && l != 0.0f) atomicAdd(loss, l * scale);
+}
+
 // <= 64 registers: 4 CTAs (32 warps) per SM
 template <int MODE, int NT>
 __global__ void __launch_bounds__(256, 4) k_backward_direct(const uint2* __restrict__ ranges,
@@ -1191,6 +1234,40 @@ static cudaError_t fused_t(int tiles, int threads, cudaStream_t st, const uint2*
                                                                   grid_grad);
     return cudaGetLastError();
 }
+
+template <int MODE, int NT>
+static cudaError_t fwdl_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
+                          const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                          const RasterConst& rc, int n, int kind, const float* target, float scale, float* color,
+                          float* trans, int32_t* last, float* image_grad, float* loss) {
+    if (tune_env("GB_CULL_BOX", 0)) cull = nullptr;
+    if (kind == 0)
+        k_forward_loss<MODE, NT, 0><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, target,
+                                                               scale, color, trans, last, image_grad, loss);
+    else
+        k_forward_loss<MODE, NT, 1><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, target,
+                                                               scale, color, trans, last, image_grad, loss);
+    return cudaGetLastError();
+}
+
+// K3 + K6 (direct compositor only): trans, last and image_grad are required, color optional
+cudaError_t launch_forward_loss(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
+                                const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
+                                const RasterConst& rc, int kind, const float* target, float scale, float* color,
+                                float* trans, int32_t* last, float* image_grad, float* loss, cudaStream_t st) {
+    if (tiles == 0) return cudaSuccess;
+    const int threads = ((ts * ts + 31) / 32) * 32;
+    if (mode == GB_MODE_ORTHO) {
+        GB_DISPATCH_N(fwdl_t, GB_MODE_ORTHO, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, kind,
+                      target, scale, color, trans, last, image_grad, loss)
+    } else {
+        GB_DISPATCH_N(fwdl_t, GB_MODE_PINHOLE, tiles, threads, st, ranges, values, hdr, cull, tex, cc, rc, n, kind,
+                      target, scale, color, trans, last, image_grad, loss)
+    }
+}
+
+// the single-kernel forward + loss + backward (k_fused_direct) instead of K3+K6 then K4: measured slower
+bool fused_single_kernel() { return tune_env("GB_FUSED_KERNEL", 0) != 0; }
 
 // true when launch_fused runs (the direct compositors are selected); otherwise the caller composes
 // launch_forward + launch_loss + launch_backward
