@@ -30,6 +30,7 @@
 // parameters: straight from every active lane when at most 12 lanes are active,
 // else after a warp reduction (a shared-memory transpose, lane l summing half
 // of row l/2).
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 
@@ -782,6 +783,17 @@ __device__ __forceinline__ bool entry_meets_warp(const ScreenHeader* __restrict_
                 : !box_miss(__ldg(&hdr[idl].h3), w.bx0, w.bx1, w.by0, w.by1);
 }
 
+// The warp rectangle of the lanes still in play (the forward's pixels not yet past early termination):
+// entries that meet only the other pixels change nothing.
+__device__ __forceinline__ WarpPixel live_rect(const WarpPixel& wp, bool live) {
+    WarpPixel r = wp;
+    r.bx0 = (float)__reduce_min_sync(kFull, live ? wp.x : INT_MAX);
+    r.bx1 = (float)__reduce_max_sync(kFull, live ? wp.x : INT_MIN);
+    r.by0 = (float)__reduce_min_sync(kFull, live ? wp.y : INT_MAX);
+    r.by1 = (float)__reduce_max_sync(kFull, live ? wp.y : INT_MIN);
+    return r;
+}
+
 // render_forward's per-pixel loop (raster.hpp:237-250) for the calling warp's pixels
 template <int MODE, int NT>
 __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __restrict__ values,
@@ -799,11 +811,12 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
     bool done = !wp.inside;
     const float early = rc.early_stop > 0.0f ? rc.early_stop : -1.0f;  // T >= 0: a disabled stop never fires
     for (int c0 = 0; c0 < total && !__all_sync(kFull, done); c0 += 32) {
+        const WarpPixel lr = live_rect(wp, !done);
         int idl = -1;
         bool pass = false;
         if (c0 + lane < total) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = entry_meets_warp(hdr, cull, idl, wp);
+            pass = entry_meets_warp(hdr, cull, idl, lr);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         while (mask) {
@@ -892,11 +905,13 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
     float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
     const int wlast = __reduce_max_sync(kFull, last);
     for (int c0 = wlast & ~31; c0 >= 0; c0 -= 32) {
+        // (a live rectangle here -- lanes with last >= c0 -- measured 1 % slower: few entries drop out)
+        const WarpPixel& lr = wp;
         int idl = -1;
         bool pass = false;
         if (c0 + lane <= wlast) {
             idl = __ldg(&values[range.x + c0 + lane]);
-            pass = entry_meets_warp(hdr, cull, idl, wp);
+            pass = entry_meets_warp(hdr, cull, idl, lr);
         }
         unsigned mask = __ballot_sync(kFull, pass);
         if (lane == 0) GB_DBG(1, __popc(mask));
