@@ -2,8 +2,8 @@
 
 Each rank owns a fixed subset of camera views and replicated primitives.  Per
 step and per owned view it runs K1 projection -> K2 tile binning -> K3 forward
-with the L1 loss (K6) in its epilogue -> K4 backward -> K5 (``fused=False``:
-the reference-shaped render_forward / l1_loss / render_backward calls),
+-> K6 L1 loss -> K4 backward -> K5 through the reference-shaped calls
+(``fused=True``: gb_render_loss_backward, K3 with the loss in its epilogue),
 accumulating into one flat fp32 gradient buffer.  Then the gradients are
 reduce-scattered (NCCL), each rank runs K7 Adam on its 1/world slice of the
 flat parameter buffer, and the parameters are all-gathered
@@ -157,7 +157,7 @@ class ViewShardedTrainer:
 
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
-                 lanes: int = 2, fused: bool = True, async_binning: bool = True, graph: bool = False,
+                 lanes: int = 2, fused: bool = False, async_binning: bool = True, graph: bool = False,
                  capacity_margin: float = 1.25, sharded_adam: bool = True):
         self.splats = splats
         self.cameras = list(cameras)
