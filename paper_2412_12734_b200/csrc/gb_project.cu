@@ -388,7 +388,12 @@ __global__ void __launch_bounds__(256) k_project(const ProjParams p, ScreenHeade
 // gradient buffer.  Ortho: raster.hpp:350-360 with the per-eval products
 // (u_hat*u, ...) summed by K4.  Pinhole: dL/dM from (S_A, S_B, S_D) then the
 // camera/quaternion chain (oracle pinhole_chain()).
-__global__ void __launch_bounds__(256) k_chain(const ProjParams p, const uint32_t* __restrict__ counts,
+// 8 CTAs of 128 threads per SM (64 registers, with spills): fp64 latency hides better with more warps
+// (+0.9 % end to end over 96-104 registers at 4-5 CTAs)
+#ifndef GB_K5_MINB
+#define GB_K5_MINB 8
+#endif
+__global__ void __launch_bounds__(128, GB_K5_MINB) k_chain(const ProjParams p, const uint32_t* __restrict__ counts,
                                                const float* __restrict__ accum, gb_grads g_out) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= p.K) return;
