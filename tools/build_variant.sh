@@ -1,6 +1,7 @@
 #!/bin/bash
 # Build an experimental variant of libgb_raster.so with extra nvcc flags into variants/<name>/
-# (travels to the GPU box; select it with GB_LIB_PATH=variants/<name>/libgb_raster.so).
+# (travels to the GPU box; select it with GB_LIB_PATH=variants/<name>/libgb_raster.so).  Delete variants
+# after use: each is ~18 MB and the gpurun snapshot is capped at 512 MiB.
 #   bash tools/build_variant.sh k4pf -DGB_K4_PREFETCH
 set -e
 NAME=$1; shift
