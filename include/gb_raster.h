@@ -171,6 +171,11 @@ GB_API int64_t gb_context_launch_count(const gb_context *ctx);
 #define GB_NUM_KERNEL_IDS 11
 GB_API gb_status gb_context_profile(gb_context *ctx, int enable);
 GB_API gb_status gb_context_profile_read(gb_context *ctx, double *total_ms, int64_t *counts, int n);
+/* The recorded launches of kernel `id` as (start, stop) in ms after `ref_event` (a cudaEvent_t recorded
+ * earlier on any stream of the device): overlapping launches from several contexts can then be merged
+ * into busy time.  Synchronous; leaves the records for gb_context_profile_read.  *n = all matches. */
+GB_API gb_status gb_context_profile_intervals(gb_context *ctx, void *ref_event, int32_t id, double *start_ms,
+                                              double *stop_ms, int64_t cap, int64_t *n);
 
 /* ---- CUDA graphs ------------------------------------------------------------
  * Capture the work a host thread issues on ctxs[0]'s stream -- and on streams that fork from it and join

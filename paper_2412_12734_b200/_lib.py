@@ -177,6 +177,7 @@ _SIGS = {
     "gb_build_binning": (C.c_int, [P, C.POINTER(Splats), C.POINTER(Camera), C.POINTER(RasterConfigC), P]),
     "gb_binning_info": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "gb_binning_set_capacity": (C.c_int, [P, C.c_int64, P]),
+    "gb_context_profile_intervals": (C.c_int, [P, P, C.c_int32, P, P, C.c_int64, C.POINTER(C.c_int64)]),
     "gb_graph_begin": (C.c_int, [P, C.c_int32]),
     "gb_graph_end": (C.c_int, [P, C.c_int32, C.POINTER(P)]),
     "gb_graph_launch": (C.c_int, [P]),

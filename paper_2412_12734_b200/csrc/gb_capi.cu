@@ -518,6 +518,28 @@ gb_status gb_graph_destroy(gb_graph* g) {
     return GB_OK;
 }
 
+gb_status gb_context_profile_intervals(gb_context* ctx, void* ref_event, int32_t id, double* start_ms,
+                                      double* stop_ms, int64_t cap, int64_t* n) {
+    if (!ctx || !ref_event || !n || cap < 0) return fail(GB_INVALID_ARGUMENT, "bad argument");
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaEvent_t ref = reinterpret_cast<cudaEvent_t>(ref_event);
+    int64_t k = 0;
+    for (const ProfRec& r : ctx->prof_recs) {
+        if (r.id != id) continue;
+        if (k < cap) {
+            float a = 0.0f, b = 0.0f;
+            GB_CUDA(cudaEventElapsedTime(&a, ref, r.start));
+            GB_CUDA(cudaEventElapsedTime(&b, ref, r.stop));
+            if (start_ms) start_ms[k] = a;
+            if (stop_ms) stop_ms[k] = b;
+        }
+        ++k;
+    }
+    *n = k;
+    return GB_OK;
+}
+
 gb_status gb_device_alloc(gb_context* ctx, uint64_t bytes, void** out) {
     if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
     *out = nullptr;

@@ -82,6 +82,20 @@ class _Context:
     def profile(self, enable: bool) -> None:
         check(lib.gb_context_profile(self.handle, int(enable)), "gb_context_profile")
 
+    def profile_intervals(self, ref_event, kernel: str):
+        """[(start_ms, stop_ms)] of the recorded launches of `kernel` after torch.cuda.Event `ref_event`."""
+        import numpy as _np
+
+        kid = _lib.KERNEL_NAMES.index(kernel)
+        n = C.c_int64()
+        check(lib.gb_context_profile_intervals(self.handle, C.c_void_p(ref_event.cuda_event), kid, None, None, 0,
+                                               C.byref(n)), "gb_context_profile_intervals")
+        a = _np.zeros(max(1, n.value), _np.float64)
+        b = _np.zeros(max(1, n.value), _np.float64)
+        check(lib.gb_context_profile_intervals(self.handle, C.c_void_p(ref_event.cuda_event), kid, a.ctypes.data,
+                                               b.ctypes.data, n.value, C.byref(n)), "gb_context_profile_intervals")
+        return list(zip(a[: n.value].tolist(), b[: n.value].tolist()))
+
     def profile_read(self) -> dict:
         """{kernel: (total_ms, launches)} since the last read (synchronises)."""
         import numpy as _np
