@@ -285,3 +285,34 @@ def test_sharded_adam_single_rank_matches_adam_step():
         opt.step(lrs, check_finite=True)
     for f, t in b.tensors().items():
         assert torch.equal(t, before[f]), f
+
+
+def test_profile_intervals_cover_the_launches():
+    """gb_context_profile_intervals: one (start, stop) per recorded launch, ordered after the reference event,
+    inside the timed window, and their lengths sum to gb_context_profile_read's total."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200.raster import context
+
+    n, arrays, specs, targets = _trainer_scene()
+    splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    cam = gb.PinholeCamera.from_spec(specs[0])
+    ctx = context(splats.device)
+    ctx.profile(True)
+    ctx.profile_read()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(3):
+        b = gb.build_binning(splats, cam)
+        gb.render_forward(splats, cam, b)
+    ev1.record()
+    torch.cuda.synchronize()
+    iv = ctx.profile_intervals(ev0, "forward")
+    total = ev0.elapsed_time(ev1)
+    assert len(iv) == 3
+    assert all(0.0 <= a <= c <= total + 1e-3 for a, c in iv)
+    assert all(iv[i][1] <= iv[i + 1][0] + 1e-3 for i in range(2))  # one stream: in order
+    ms, cnt = ctx.profile_read()["forward"]
+    ctx.profile(False)
+    assert cnt == 3 and abs(sum(c - a for a, c in iv) - ms) < 1e-3 * max(1.0, ms)
