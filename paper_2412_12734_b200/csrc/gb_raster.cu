@@ -861,15 +861,26 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
                     c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
                           __ldg(p10 + 5) * b.w11;
                 } else if (au || av) {  // the four-corner blend with two zero weights
-                    const float w = au ? u : v;
-                    float sx = __fmaf_rn(w, rc.tex_scale, rc.tex_offset);
-                    sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
-                    const int i0 = min((int)floorf(sx), N - 2);
-                    const float f = __fsub_rn(sx, (float)i0);
+                    // (separate uniform branches: each keeps its index arithmetic free of selects)
+                    const float* pa;
+                    const float* pb;
+                    float f;
+                    if (au) {
+                        float sx = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
+                        sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
+                        const int i0 = min((int)floorf(sx), N - 2);
+                        f = __fsub_rn(sx, (float)i0);
+                        pa = t + (i0 * N + (v > 0.0f ? N - 1 : 0)) * 3;
+                        pb = pa + 3 * N;
+                    } else {
+                        float sx = __fmaf_rn(v, rc.tex_scale, rc.tex_offset);
+                        sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
+                        const int i0 = min((int)floorf(sx), N - 2);
+                        f = __fsub_rn(sx, (float)i0);
+                        pa = t + ((u > 0.0f ? N - 1 : 0) * N + i0) * 3;
+                        pb = pa + 3;
+                    }
                     const float gf = 1.0f - f;
-                    const int other = (au ? v : u) > 0.0f ? N - 1 : 0;
-                    const float* pa = t + (au ? i0 * N + other : other * N + i0) * 3;
-                    const float* pb = pa + (au ? 3 * N : 3);
                     c0_ = fmaf(__ldg(pb), f, __ldg(pa) * gf);
                     c1_ = fmaf(__ldg(pb + 1), f, __ldg(pa + 1) * gf);
                     c2_ = fmaf(__ldg(pb + 2), f, __ldg(pa + 2) * gf);
