@@ -18,8 +18,9 @@ if [ "${TESTS:-1}" = 1 ]; then
   timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
   echo "smoke exit $?" >> $O/smoke.log
 fi
-# variant names: grp (default, G=8), grp16 (G=16), direct, staged
-venv() { case $1 in grp16) echo "GB_COMPOSITOR=grp GB_GROUP=16";; grp4) echo "GB_COMPOSITOR=grp GB_GROUP=4";; fwd0) echo "GB_FWD_BATCH=0";; fwd12) echo "GB_FWD_BATCH=12";; grp16b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16";; grp16bu) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16 GB_GRP_TEXEL=uni";; grp8b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=8";; perlane) echo "GB_DIRECT_TEXEL=perlane";; nofuse) echo "GB_NO_FUSE=1";; fused) echo "GB_FUSED=1";; blocking) echo "GB_BLOCKING_BINNING=1";; graph) echo "GB_GRAPH=1";; graphfused) echo "GB_GRAPH=1 GB_FUSED=1";; *) echo "GB_COMPOSITOR=$1";; esac; }
+# variant names: direct (default), staged, grp (G=8), grp16/grp4, backward-only grp (grp16b, grp16bu, grp8b),
+# fused (gb_render_loss_backward), nofuse, blocking (blocking binning), eager (no CUDA graph), lanes2
+venv() { case $1 in grp16) echo "GB_COMPOSITOR=grp GB_GROUP=16";; grp4) echo "GB_COMPOSITOR=grp GB_GROUP=4";; grp16b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16";; grp16bu) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=16 GB_GRP_TEXEL=uni";; grp8b) echo "GB_COMPOSITOR_BWD=grp GB_GROUP=8";; nofuse) echo "GB_NO_FUSE=1";; fused) echo "GB_FUSED=1";; blocking) echo "GB_BLOCKING_BINNING=1";; eager) echo "GB_GRAPH=0";; lanes2) echo "GB_LANES=2";; *) echo "GB_COMPOSITOR=$1";; esac; }
 for v in ${ALT_TESTS:-}; do
   env $(venv $v) timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "configs1 or pinhole_small or ortho_random or ragged" > $O/pytest_gpu_$v.log 2>&1
   echo "pytest exit $?" >> $O/pytest_gpu_$v.log
