@@ -823,26 +823,23 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             const int bit = __ffs(mask) - 1;
             mask &= mask - 1;
             const int id = __shfl_sync(kFull, idl, bit);
-            bool comp = false;  // this pixel composites the entry
-            float u = 0.0f, v = 0.0f, alpha = 0.0f;
-            if (!done) {
-                ScreenHeader h;
-                h.h0 = __ldg(&hdr[id].h0);
-                h.h1 = __ldg(&hdr[id].h1);
-                h.h2 = __ldg(&hdr[id].h2);
-                bool hit;
-                if (MODE == GB_MODE_ORTHO) {
-                    hit = eval_uv_ortho(h, x, y, u, v);
-                } else {
-                    PinholeTerms pt;
-                    hit = eval_uv_pinhole(h, x, y, u, v, pt);
-                }
-                if (hit) {
-                    const float G = gauss_weight(u, v);
-                    alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);  // raster.hpp:241
-                    comp = !(alpha < rc.alpha_skip);                  // raster.hpp:242
-                }
+            // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not
+            // composite -- no branch around the evaluation
+            float u, v;
+            ScreenHeader h;
+            h.h0 = __ldg(&hdr[id].h0);
+            h.h1 = __ldg(&hdr[id].h1);
+            h.h2 = __ldg(&hdr[id].h2);
+            bool hit;
+            if (MODE == GB_MODE_ORTHO) {
+                hit = eval_uv_ortho(h, x, y, u, v);
+            } else {
+                PinholeTerms pt;
+                hit = eval_uv_pinhole(h, x, y, u, v, pt);
             }
+            const float G = gauss_weight(u, v);
+            const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);  // raster.hpp:241
+            const bool comp = !done && hit && !(alpha < rc.alpha_skip);     // raster.hpp:242
             // texel footprint class of the warp (see bwd_shade): clamped axes read one texel row
             const float sigma = rc.sigma;
             const bool au = N > 1 && __any_sync(kFull, comp && u > -sigma && u < sigma);
