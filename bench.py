@@ -308,6 +308,27 @@ def run_ours(args):
         e2e = {"value": round(mpix / (e2e_ms / 1e3), 3), "unit": "MP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": len(views) * 4, "ms_per_step": round(e2e_ms, 3)}
 
+    # ---- forward only (render: K1 + K2 + K3 per view, one stream), SURVEY §8(d)'s "fwd" figure ----
+    fwd = None
+    if rank == 0:
+        rb = gb.TileBinning(device)
+        rb.set_capacity(trainer.capacity or 0, torch.zeros(1, dtype=torch.int32, device=device))
+        rout = gb.RenderOutput(W, H, device)
+        for v in views[:2]:  # warm-up
+            gb.render_forward(splats, cams[v], gb.build_binning(splats, cams[v], out=rb), rout)
+        torch.cuda.synchronize()
+        evf0, evf1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        evf0.record()
+        for _ in range(reps):
+            for v in views:
+                gb.render_forward(splats, cams[v], gb.build_binning(splats, cams[v], out=rb), rout)
+        evf1.record()
+        torch.cuda.synchronize()
+        f_ms = evf0.elapsed_time(evf1) / (reps * len(views))
+        fwd = {"ms_per_view": round(f_ms, 4), "value": round(W * H / 1e6 / (f_ms / 1e3), 3), "unit": "MP/s",
+               "what": "build_binning + render_forward per view, one stream, CUDA events"}
+
     # ---- replicas stay in sync: every rank holds bit-identical parameters ----
     in_sync = True
     if world > 1:
@@ -395,6 +416,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "e2e": e2e,
         "replicas_in_sync": in_sync,
+        "forward_only": fwd,
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
