@@ -3,7 +3,7 @@
 //
 //   depth_bits (K1) --CUB stable radix sort, 32 bits--> perm  (primitives in
 //                      (depth, index) order; culled ones carry ~0 and sort last)
-//   k_gather_counts  : counts in that order, CUB inclusive scan -> offsets
+//   CUB inclusive scan of the counts read in that order -> offsets
 //   k_duplicate      : one (tile id, primitive) pair per overlapped tile,
 //                      emitted in (depth, index) order
 //   CUB stable radix sort on the ceil(log2 tiles) tile-id bits only
@@ -22,6 +22,8 @@
 // the whole build can be captured into a CUDA graph.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "gb_internal.cuh"
 
@@ -30,13 +32,6 @@ namespace gb {
 __global__ void __launch_bounds__(256) k_iota(int64_t K, int32_t* __restrict__ out) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < K) out[k] = (int32_t)k;
-}
-
-__global__ void __launch_bounds__(256) k_gather_counts(int64_t K, const int32_t* __restrict__ perm,
-                                                       const uint32_t* __restrict__ counts,
-                                                       uint32_t* __restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < K) out[i] = counts[perm[i]];
 }
 
 // cap: pair capacity of keys/values.  Pairs at or beyond it are dropped and flagged in *overflow
@@ -95,9 +90,18 @@ int tile_sort_bits(int n_keys) {
     return b ? b : 1;
 }
 
+// counts[perm[i]]: the tile counts read in depth order straight into the scan (no gather pass)
+struct PermutedCount {
+    const int32_t* perm;
+    const uint32_t* counts;
+    __host__ __device__ uint32_t operator()(int64_t i) const { return counts[perm[i]]; }
+};
+using CountIter = thrust::transform_iterator<PermutedCount, thrust::counting_iterator<int64_t>, uint32_t>;
+
 size_t scan_temp_bytes(int64_t K) {
     size_t bytes = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)K);
+    CountIter it(thrust::counting_iterator<int64_t>(0), PermutedCount{nullptr, nullptr});
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, it, (uint32_t*)nullptr, (int)K);
     return bytes;
 }
 
@@ -123,13 +127,11 @@ cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* dep
 
 // offsets (K+1 entries) = exclusive scan of the counts in perm order; offsets[K] = P.
 cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
-                        uint32_t* counts_sorted, uint32_t* offsets, int64_t K, cudaStream_t st) {
+                        uint32_t* offsets, int64_t K, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(offsets, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess || K == 0) return e;
-    k_gather_counts<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, perm, counts, counts_sorted);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, counts_sorted, offsets + 1, (int)K, st);
+    CountIter it(thrust::counting_iterator<int64_t>(0), PermutedCount{perm, counts});
+    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, it, offsets + 1, (int)K, st);
 }
 
 cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,

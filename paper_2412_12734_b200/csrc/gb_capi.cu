@@ -22,7 +22,7 @@ int tile_sort_bits(int n_keys);
 cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* depth_bits, uint32_t* depth_sorted,
                               int32_t* iota, int32_t* perm, int64_t K, cudaStream_t st);
 cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
-                        uint32_t* counts_sorted, uint32_t* offsets, int64_t K, cudaStream_t st);
+                        uint32_t* offsets, int64_t K, cudaStream_t st);
 cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,
                              uint32_t* keys, int32_t* values, uint32_t cap, int32_t* overflow, cudaStream_t st);
 cudaError_t launch_pad(uint32_t cap, const uint32_t* total, int n_tiles, uint32_t* keys, int32_t* values,
@@ -121,7 +121,7 @@ struct gb_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
-    DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, counts_tmp, accum, adam_bad, ssim_tmp,
+    DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, accum, adam_bad, ssim_tmp,
         metric_tmp, fuse_color, fuse_trans, fuse_last, fuse_grad;
     uint32_t* pinned_total = nullptr;
     bool prof = false;
@@ -320,7 +320,6 @@ gb_status gb_context_destroy(gb_context* ctx) {
     ctx->vals_tmp.release();
     ctx->depth_tmp.release();
     ctx->iota_tmp.release();
-    ctx->counts_tmp.release();
     ctx->accum.release();
     ctx->adam_bad.release();
     ctx->ssim_tmp.release();
@@ -634,7 +633,6 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
     GB_CUDA(b->ranges.ensure(sizeof(uint2) * (n_tiles > 0 ? n_tiles : 1)));
     GB_CUDA(ctx->depth_tmp.ensure(sizeof(uint32_t) * Kc));
     GB_CUDA(ctx->iota_tmp.ensure(sizeof(int32_t) * Kc));
-    GB_CUDA(ctx->counts_tmp.ensure(sizeof(uint32_t) * Kc));
     GB_CUDA(ctx->scan_temp.ensure(gb::scan_temp_bytes(Kc)));
     GB_CUDA(ctx->sort_temp.ensure(gb::sort_temp_bytes(Kc)));
 
@@ -658,9 +656,9 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
     {
         ProfScope ps(ctx, GB_K_SCAN);
         GB_CUDA(gb::launch_scan(ctx->scan_temp.p, ctx->scan_temp.cap, b->perm.as<int32_t>(), b->counts.as<uint32_t>(),
-                                ctx->counts_tmp.as<uint32_t>(), b->offsets.as<uint32_t>(), K, stream));
+                                b->offsets.as<uint32_t>(), K, stream));
     }
-    ctx->launches += K > 0 ? 3 : 0;  // gather + CUB scan (init + scan)
+    ctx->launches += K > 0 ? 2 : 0;  // CUB scan (init + scan) over the permuted counts
     int64_t P;  // pairs the sort and ranges run over: the exact count, or the capacity
     if (b->capacity > 0) {
         P = b->capacity;
