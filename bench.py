@@ -226,6 +226,7 @@ def run_ours(args):
     trainer = ViewShardedTrainer(splats, cams, views, lrs=lrs, graph=use_graph, async_binning=not blocking,
                                  lanes=int(os.environ.get("GB_LANES", "4")),
                                  fused=os.environ.get("GB_FUSED") == "1")
+    trainer.graph_host = os.environ.get("GB_GRAPH_HOST", "0") == "1"
     W, H = cams[0].width, cams[0].height
     host_targets = [torch.from_numpy(cfg3.target(v)).pin_memory() for v in views]
     dev_targets = [t.to(device) for t in host_targets]
