@@ -7,6 +7,8 @@
   the views equal the oracle's per-view backward sum, and the post-Adam
   parameters equal the oracle's Adam on those gradients.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -316,3 +318,53 @@ def test_profile_intervals_cover_the_launches():
     ms, cnt = ctx.profile_read()["forward"]
     ctx.profile(False)
     assert cnt == 3 and abs(sum(c - a for a, c in iv) - ms) < 1e-3 * max(1.0, ms)
+
+
+_FAKE_RANK_SCRIPT = r"""
+import sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+from torch.testing._internal.distributed.fake_pg import FakeStore
+dist.init_process_group('fake', store=FakeStore(), rank=1, world_size=2)
+_rs = dist.reduce_scatter_tensor
+def _reduce_scatter(out, inp, *a, **k):  # the fake collective writes nothing: emulate a zero peer
+    _rs(out, inp, *a, **k)
+    out.copy_(inp[out.numel():2 * out.numel()])
+dist.reduce_scatter_tensor = _reduce_scatter
+import paper_2412_12734_b200 as gb
+from paper_2412_12734_b200.train import ViewShardedTrainer
+from test_gpu_train import _trainer_scene
+from parity import O
+n, arrays, specs, targets = _trainer_scene()
+splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+cams = [gb.PinholeCamera.from_spec(s) for s in specs]
+tr = ViewShardedTrainer(splats, cams, [0, 1, 2], graph=True)
+opt = tr.opt
+assert opt.world == 2 and opt.rank == 1 and opt.lo == opt.S and opt.flat.numel() == 2 * opt.S
+before = opt.flat.clone()
+tg = [torch.as_tensor(t).cuda() for t in targets]
+host = [torch.as_tensor(t).pin_memory() for t in targets]
+for _ in range(2):
+    tr.step(tg)
+tr.step_host(host)
+torch.cuda.synchronize()
+lo, S = opt.lo, opt.S
+assert not torch.equal(opt.flat[lo:lo + S], before[lo:lo + S]), 'own slice must be updated'
+assert torch.isfinite(opt.flat).all()
+assert tr.state.t == 3 and tr._graph is not None
+print('fake-rank ok')
+"""
+
+
+def test_two_rank_code_path_with_fake_process_group(tmp_path):
+    """The multi-GPU step's code path at world size 2 on one GPU, with torch's fake process group (its
+    collectives move no data; the reduce-scatter is emulated with a zero peer): the reduce-scatter /
+    min-all-reduce / in-place all-gather calls, rank 1's slice and segments, graph capture and the
+    host-input step all run, and rank 1's half of the parameters is updated."""
+    import subprocess
+    import sys
+
+    script = tmp_path / "fake_rank.py"
+    script.write_text(_FAKE_RANK_SCRIPT)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "fake-rank ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
