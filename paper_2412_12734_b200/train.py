@@ -292,13 +292,19 @@ class ViewShardedTrainer:
             run()  # blocking builds: learn the pair counts
             self._set_capacity(max(self.pairs[n0:]) if len(self.pairs) > n0 else 0)
             return
-        while True:
+        for attempt in range(4):
             run()
             if not self.capacity or not int(self._overflow.item()):
                 break
             self.overflows += 1
             self._overflow.zero_()
-            self._set_capacity(int(self._pair_counts.max().item()))
+            need = int((self._pair_counts[: len(self.views)].to(torch.int64) & 0xFFFFFFFF).max().item())  # uint32
+            if need >= 2 ** 31:
+                raise RuntimeError(f"view binning needs {need} tile/primitive pairs, more than the 2^31 the "
+                                   "sort supports")
+            self._set_capacity(need)
+        else:
+            raise RuntimeError("view binning kept outgrowing its pair capacity")
         if self.capacity:
             self._pair_sum += self._pair_counts[: len(self.views)].sum()
             self._pair_views += len(self.views)
