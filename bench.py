@@ -297,7 +297,7 @@ def run_ours(args):
     # ---- end to end: pinned host targets in, per-view losses out, every step ----
     e2e = None
     if not args.no_e2e:
-        for _ in range(1):
+        for _ in range(max(3, args.warmup)):  # the same W >= 3 warm-up as the device-input timing
             trainer.step_host(host_targets)
         barrier()
         torch.cuda.synchronize()
