@@ -230,6 +230,7 @@ def run_ours(args):
     blocking = os.environ.get("GB_BLOCKING_BINNING") == "1"
     trainer = ViewShardedTrainer(splats, cams, views, lrs=lrs, graph=use_graph, async_binning=not blocking,
                                  lanes=int(os.environ.get("GB_LANES", "4")),
+                                 overlap_adam=os.environ.get("GB_OVERLAP_ADAM", "1") == "1",
                                  fused=os.environ.get("GB_FUSED") == "1")
     trainer.graph_host = os.environ.get("GB_GRAPH_HOST", "0") == "1"
     W, H = cams[0].width, cams[0].height

@@ -191,6 +191,9 @@ GB_API gb_status gb_graph_end(gb_context *const *ctxs, int32_t n, gb_graph **out
 /* Launch on the origin context's stream (asynchronous). */
 GB_API gb_status gb_graph_launch(gb_graph *g);
 GB_API gb_status gb_graph_destroy(gb_graph *g);
+/* The context's stream waits for `event` (a cudaEvent_t).  external = 1: inside a gb_graph capture the
+ * graph then waits for the event's record made outside it, at every launch (ignored outside a capture). */
+GB_API gb_status gb_stream_wait_event(gb_context *ctx, void *event, int32_t external);
 
 /* ---- device memory helpers (so a C/C++ host needs no CUDA headers) -------- */
 GB_API gb_status gb_device_alloc(gb_context *ctx, uint64_t bytes, void **out);

@@ -181,6 +181,7 @@ _SIGS = {
     "gb_graph_begin": (C.c_int, [P, C.c_int32]),
     "gb_graph_end": (C.c_int, [P, C.c_int32, C.POINTER(P)]),
     "gb_graph_launch": (C.c_int, [P]),
+    "gb_stream_wait_event": (C.c_int, [P, P, C.c_int32]),
     "gb_graph_destroy": (C.c_int, [P]),
     "gb_binning_store_total": (C.c_int, [P, P, P]),
     "gb_binning_copy_to_host": (C.c_int, [P, P, P, P]),

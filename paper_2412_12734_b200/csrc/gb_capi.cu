@@ -539,6 +539,18 @@ gb_status gb_context_profile_intervals(gb_context* ctx, void* ref_event, int32_t
     return GB_OK;
 }
 
+gb_status gb_stream_wait_event(gb_context* ctx, void* event, int32_t external) {
+    if (!ctx || !event) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    GB_CUDA(cudaStreamIsCapturing(ctx->stream, &cap));
+    // the external flag only means something (and is only accepted) inside a capture
+    const bool ext = external && cap == cudaStreamCaptureStatusActive;
+    GB_CUDA(cudaStreamWaitEvent(ctx->stream, reinterpret_cast<cudaEvent_t>(event),
+                                ext ? cudaEventWaitExternal : cudaEventWaitDefault));
+    return GB_OK;
+}
+
 gb_status gb_device_alloc(gb_context* ctx, uint64_t bytes, void** out) {
     if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
     *out = nullptr;

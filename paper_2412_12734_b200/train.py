@@ -22,6 +22,7 @@ from typing import List, Optional, Sequence
 import torch
 
 from . import _lib
+from ._lib import check, lib
 
 from .raster import (AdamConfig, AdamState, GradientBuffer, LearningRates, RasterConfig, RenderOutput, SplatSet,
                      StepGraph, TileBinning, adam_step, all_contexts, build_binning, context, l1_loss,
@@ -97,9 +98,16 @@ class ShardedAdam:
                                          b - a, _ADAM_GROUP[f], 0))
         self._segs = (_lib.AdamSegment * max(1, len(segs)))(*segs)
         self._nseg = len(segs)
+        grid = [sg for sg in segs if sg.group == 4]
+        other = [sg for sg in segs if sg.group != 4]
+        self._grid_segs = (_lib.AdamSegment * len(grid))(*grid) if grid else None
+        self._other_segs = (_lib.AdamSegment * max(1, len(other)))(*other)
         self._names = [f for f in grads.offsets if f != "depth_key"]
 
-    def step(self, lrs: LearningRates, check_finite: bool = False) -> None:
+    def step(self, lrs: LearningRates, check_finite: bool = False, grid_stream=None, grid_done=None) -> None:
+        """One update.  With ``grid_stream`` (world size 1): the texel segment is updated on that stream
+        (after the non-finite scan of every segment) and ``grid_done`` is recorded there -- the next
+        step's binning overlaps the texel update."""
         from .raster import context
         from ._lib import check, lib
 
@@ -120,8 +128,22 @@ class ShardedAdam:
                                        self.flag.data_ptr()), "adam_step")
             if self.world > 1:
                 dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
-            check(lib.gb_adam_segments(ctx.handle, 1, self._segs, self._nseg, C.byref(st), C.byref(c_lrs),
-                                       self.flag.data_ptr()), "adam_step")
+            if grid_stream is None or self.world > 1 or not self._grid_segs:
+                check(lib.gb_adam_segments(ctx.handle, 1, self._segs, self._nseg, C.byref(st), C.byref(c_lrs),
+                                           self.flag.data_ptr()), "adam_step")
+            else:
+                t0 = st.t
+                check(lib.gb_adam_segments(ctx.handle, 1, self._other_segs, len(self._other_segs), C.byref(st),
+                                           C.byref(c_lrs), self.flag.data_ptr()), "adam_step")
+                st_g = self.state.to_c()
+                st_g.t = t0  # the same step number for the texel segment
+                cur = torch.cuda.current_stream(self.flat.device)
+                grid_stream.wait_stream(cur)
+                with torch.cuda.stream(grid_stream):
+                    gctx = context(self.flat.device)
+                    check(lib.gb_adam_segments(gctx.handle, 1, self._grid_segs, len(self._grid_segs),
+                                               C.byref(st_g), C.byref(c_lrs), self.flag.data_ptr()), "adam_step")
+                    grid_done.record(grid_stream)
             self.state.t = st.t
         if self.world > 1:
             dist.all_gather_into_tensor(self.flat, self.flat[self.lo:self.lo + self.S], group=self.pg)
@@ -158,7 +180,7 @@ class ViewShardedTrainer:
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
                  lanes: int = 4, fused: bool = False, async_binning: bool = True, graph: bool = False,
-                 capacity_margin: float = 1.25, sharded_adam: bool = True):
+                 capacity_margin: float = 1.25, sharded_adam: bool = True, overlap_adam: bool = True):
         self.splats = splats
         self.cameras = list(cameras)
         self.views = list(views)
@@ -172,6 +194,16 @@ class ViewShardedTrainer:
         # replicated one (all-reduce, full Adam on every rank)
         self.state = AdamState(splats, adam, moments=not sharded_adam)
         self.opt = ShardedAdam(splats, self.grads, self.state, process_group) if sharded_adam else None
+        # world size 1: the texel half of Adam (90 % of it) runs on a side stream and overlaps the next
+        # step's binning; each lane waits for it (and the texel-gradient zeroing that follows it) before
+        # its first forward compositor.  Texels read on another stream right after step() returns need
+        # torch.cuda.synchronize() or wait_adam().
+        self.overlap_adam = bool(overlap_adam and self.opt is not None and self.opt.world == 1)
+        self._adam_stream = torch.cuda.Stream(device=splats.device) if self.overlap_adam else None
+        self._grid_done = torch.cuda.Event() if self.overlap_adam else None  # texel update finished
+        self._grid_ready = torch.cuda.Event() if self.overlap_adam else None  # ... and its gradients zeroed
+        if self.overlap_adam:
+            self._grid_done.record(self._adam_stream)  # exists (and is complete) before the first wait
         self.check_finite = check_finite
         self.fused = fused
         dev = splats.device
@@ -226,6 +258,9 @@ class ViewShardedTrainer:
             lane.binning.store_total(self._pair_counts[i:i + 1])
         else:
             self.pairs.append(lane.binning.total)
+        if self.overlap_adam and id(lane) not in self._waited:  # texels updated, their gradients zeroed
+            self._waited.add(id(lane))
+            lane.stream.wait_event(self._grid_ready)
         if not self.fused:
             render_forward(self.splats, cam, lane.binning, out)
         return cam, out, gimg
@@ -239,19 +274,41 @@ class ViewShardedTrainer:
         l1_loss(out.color, target.view(cam.height, cam.width, 3), grad=gimg, loss=self.losses[i:i + 1])
         render_backward(self.splats, cam, lane.binning, out, gimg, self.grads)
 
+    def wait_adam(self) -> None:
+        """Order the current stream after the step's texel update (overlap_adam)."""
+        if self.overlap_adam:
+            torch.cuda.current_stream(self.splats.device).wait_event(self._grid_done)
+
     def _begin(self) -> None:
         main = self._lanes[0].stream
-        self.grads.zero_()
+        if self.overlap_adam:
+            o, _ = self.grads.offsets["grid"]
+            self.grads.flat[:o].zero_()
+        else:
+            self.grads.zero_()
         self.losses.zero_()
         self._step_start.record(main)
         for lane in self._lanes[1:]:
             lane.stream.wait_event(self._step_start)  # parameters updated and gradients zeroed
+        if self.overlap_adam:
+            # side stream: after the previous step's texel update (recorded outside any graph), zero the
+            # texel gradients; lanes wait for that only before their first forward compositor
+            a = self._adam_stream
+            a.wait_event(self._step_start)
+            with torch.cuda.stream(a):
+                check(lib.gb_stream_wait_event(context(self.splats.device).handle,
+                                               C.c_void_p(self._grid_done.cuda_event), 1), "gb_stream_wait_event")
+                self.grads.grid.zero_()
+                self._grid_ready.record(a)
+            self._waited = set()
 
     def _join(self) -> None:
         main = self._lanes[0].stream
         for lane in self._lanes[1:]:
             lane.done.record(lane.stream)
             main.wait_event(lane.done)
+        if self.overlap_adam:
+            main.wait_event(self._grid_ready)  # the side stream rejoins (a graph capture needs it)
 
     def _on_lanes(self, body) -> None:
         """Run body() with lane 0 as the current stream, ordered after and before the caller's stream."""
@@ -359,7 +416,8 @@ class ViewShardedTrainer:
 
     def _finish(self) -> None:
         if self.opt is not None:
-            self.opt.step(self.lrs, check_finite=self.check_finite)
+            self.opt.step(self.lrs, check_finite=self.check_finite,
+                          grid_stream=self._adam_stream, grid_done=self._grid_done)
             return
         reduce_gradients(self.grads, self.pg)
         adam_step(self.splats, self.grads, self.state, self.lrs, check_finite=self.check_finite)
