@@ -233,6 +233,8 @@ def run_ours(args):
                                  overlap_adam=os.environ.get("GB_OVERLAP_ADAM", "1") == "1",
                                  fused=os.environ.get("GB_FUSED") == "1")
     trainer.graph_host = os.environ.get("GB_GRAPH_HOST", "0") == "1"
+    if os.environ.get("GB_PRE_ADAM_READ") == "1":
+        trainer.overlap_read = False
     W, H = cams[0].width, cams[0].height
     host_targets = [torch.from_numpy(cfg3.target(v)).pin_memory() for v in views]
     dev_targets = [t.to(device) for t in host_targets]

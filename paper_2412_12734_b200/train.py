@@ -83,6 +83,7 @@ class ShardedAdam:
         self.m = torch.zeros(S, dtype=torch.float32, device=dev)
         self.v = torch.zeros(S, dtype=torch.float32, device=dev)
         self.flag = torch.empty(1, dtype=torch.int64, device=dev)
+        self._veto = torch.full((1,), self.VETO, dtype=torch.int64, device=dev)
         segs = []
         self.ranges = []  # (flat lo, flat hi, group) of this rank's slice
         gbase = self.lo if self.world > 1 else 0  # g_shard: this rank's slice, or (one rank) the whole buffer
@@ -104,7 +105,11 @@ class ShardedAdam:
         self._other_segs = (_lib.AdamSegment * max(1, len(other)))(*other)
         self._names = [f for f in grads.offsets if f != "depth_key"]
 
-    def step(self, lrs: LearningRates, check_finite: bool = False, grid_stream=None, grid_done=None) -> None:
+    VETO = 7 << 48  # flag value of a vetoed step: below every clear value, above every non-finite code
+    # (group <= 4), so a non-finite gradient still wins the min-reduction
+
+    def step(self, lrs: LearningRates, check_finite: bool = False, grid_stream=None, grid_done=None,
+             veto: torch.Tensor = None) -> None:
         """One update.  With ``grid_stream`` (world size 1): the texel segment is updated on that stream
         (after the non-finite scan of every segment) and ``grid_done`` is recorded there -- the next
         step's binning overlaps the texel update."""
@@ -115,8 +120,14 @@ class ShardedAdam:
         if self.world > 1:
             dist.reduce_scatter_tensor(self.g_shard, self.grads.flat, op=dist.ReduceOp.SUM, group=self.pg)
         self.flag.fill_(_lib.ADAM_FLAG_CLEAR)
+
+        def fold_veto():  # veto (a device int32, nonzero = skip the update on every rank)
+            if veto is not None:
+                self.flag.copy_(torch.where(veto.to(torch.int64) != 0, self._veto, self.flag))
+
         if self._hook is not None:
             self._hook(0, self, lrs)
+            fold_veto()
             if self.world > 1:
                 dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
             self._hook(1, self, lrs)
@@ -126,6 +137,7 @@ class ShardedAdam:
             c_lrs = lrs.to_c()
             check(lib.gb_adam_segments(ctx.handle, 0, self._segs, self._nseg, C.byref(st), C.byref(c_lrs),
                                        self.flag.data_ptr()), "adam_step")
+            fold_veto()
             if self.world > 1:
                 dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
             if grid_stream is None or self.world > 1 or not self._grid_segs:
@@ -148,13 +160,16 @@ class ShardedAdam:
         if self.world > 1:
             dist.all_gather_into_tensor(self.flat, self.flat[self.lo:self.lo + self.S], group=self.pg)
         if check_finite:
-            v = int(self.flag.item())
-            if v != _lib.ADAM_FLAG_CLEAR:
-                grp = v >> 48
-                names = ("position", "theta", "log_scale", "opacity_logit", "color_grid")
-                raise _lib.NonFinite(_lib.GB_NONFINITE, "adam_step",
-                                     f"non-finite gradient in group '{names[grp & 7]}' "
-                                     f"(segment index {v & ((1 << 48) - 1)}); no parameter was updated")
+            self.raise_if_nonfinite(int(self.flag.item()))
+
+    @staticmethod
+    def raise_if_nonfinite(v: int) -> None:
+        if v != _lib.ADAM_FLAG_CLEAR and v != ShardedAdam.VETO:
+            grp = v >> 48
+            names = ("position", "theta", "log_scale", "opacity_logit", "color_grid")
+            raise _lib.NonFinite(_lib.GB_NONFINITE, "adam_step",
+                                 f"non-finite gradient in group '{names[grp & 7]}' "
+                                 f"(segment index {v & ((1 << 48) - 1)}); no parameter was updated")
 
 
 class _Lane:
@@ -199,6 +214,7 @@ class ViewShardedTrainer:
         # its first forward compositor.  Texels read on another stream right after step() returns need
         # torch.cuda.synchronize() or wait_adam().
         self.overlap_adam = bool(overlap_adam and self.opt is not None and self.opt.world == 1)
+        self.overlap_read = True  # step(): the overflow read after Adam is queued (overlap_adam only)
         self._adam_stream = torch.cuda.Stream(device=splats.device) if self.overlap_adam else None
         self._grid_done = torch.cuda.Event() if self.overlap_adam else None  # texel update finished
         self._grid_ready = torch.cuda.Event() if self.overlap_adam else None  # ... and its gradients zeroed
@@ -424,9 +440,41 @@ class ViewShardedTrainer:
 
     def step(self, targets: Sequence[torch.Tensor]) -> torch.Tensor:
         """One training step with device-resident per-view targets; returns the device loss vector."""
-        self._views_checked(lambda: self._run_views(targets))
-        self._finish()
+        run = lambda: self._run_views(targets)  # noqa: E731
+        if not (self.opt is not None and self.overlap_adam and self.async_binning and self.capacity
+                and self.overlap_read):
+            self._views_checked(run)
+            self._finish()
+            return self.losses
+        # the step's one host read comes after Adam is queued (its texel half runs on the side stream, so
+        # the read waits only for the scan and the small groups): a view that outgrew its pair buffers
+        # vetoes the update, and the step is redone with larger buffers
+        for _ in range(4):
+            run()
+            self.opt.step(self.lrs, check_finite=False, grid_stream=self._adam_stream, grid_done=self._grid_done,
+                          veto=self._overflow)
+            code = int(self.opt.flag.item())
+            if code != ShardedAdam.VETO:
+                break
+            self.state.t -= 1  # nothing was updated
+            self._grow_after_overflow()
+        else:
+            raise RuntimeError("view binning kept outgrowing its pair capacity")
+        self._pair_sum += self._pair_counts[: len(self.views)].sum()
+        self._pair_views += len(self.views)
+        if self.check_finite:
+            ShardedAdam.raise_if_nonfinite(code)
         return self.losses
+
+    def _grow_after_overflow(self) -> None:
+        self.overflows += 1
+        if int(self._overflow.item()):
+            need = int((self._pair_counts[: len(self.views)].to(torch.int64) & 0xFFFFFFFF).max().item())  # uint32
+            if need >= 2 ** 31:
+                raise RuntimeError(f"view binning needs {need} tile/primitive pairs, more than the 2^31 the "
+                                   "sort supports")
+            self._overflow.zero_()
+            self._set_capacity(need)
 
     def step_host(self, targets_host: Sequence[torch.Tensor]) -> torch.Tensor:
         """End-to-end step from pinned HOST targets: the H2D copy of view i+1 overlaps the

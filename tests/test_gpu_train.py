@@ -368,3 +368,38 @@ def test_two_rank_code_path_with_fake_process_group(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "fake-rank ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_step_overflow_vetoes_adam_and_redoes():
+    """step() with the Adam overlap reads back once, after Adam is queued: a view that outgrows its pair
+    buffers vetoes the update (folded into the sharded optimiser's agreed flag) and the step is redone
+    with larger buffers -- same gradients and step count as an uninterrupted run."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200.train import ViewShardedTrainer
+
+    n, arrays, specs, targets = _trainer_scene()
+    cams = [gb.PinholeCamera.from_spec(s) for s in specs]
+    tg = [torch.as_tensor(t).cuda() for t in targets]
+
+    def make(**kw):
+        s = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+        return ViewShardedTrainer(s, cams, [0, 1, 2], **kw)
+
+    ref, tr = make(async_binning=False), make()
+    assert tr.overlap_adam and tr.overlap_read
+    for t in (ref, tr):
+        t.step(tg)  # tr: blocking first step, then capacity mode
+    P = max(ref.pairs)
+    tr._set_capacity(P // 4, exact=True)
+    ref.step(tg)
+    tr.step(tg)
+    torch.cuda.synchronize()
+    assert tr.overflows == 1 and tr.capacity >= P and tr.state.t == ref.state.t == 2
+    for k, w in ref.grads.tensors().items():
+        w = w.cpu().numpy().astype(np.float64)
+        np.testing.assert_allclose(tr.grads.tensors()[k].cpu().numpy(), w, rtol=1e-3, atol=1e-5 * np.abs(w).max(),
+                                   err_msg=k)
+    for k, w in ref.splats.tensors().items():
+        np.testing.assert_allclose(tr.splats.tensors()[k].cpu().numpy(), w.cpu().numpy(), atol=2e-3, err_msg=k)
