@@ -231,6 +231,7 @@ class ViewShardedTrainer:
         H = max(self.cameras[v].height for v in self.views) if self.views else 1
         self.losses = torch.zeros(max(1, len(self.views)), dtype=torch.float32, device=dev)
         self._pinned_losses = torch.zeros(max(1, len(self.views)), dtype=torch.float32, pin_memory=True)
+        self._pinned_flag = torch.zeros(1, dtype=torch.int64, pin_memory=True)
         self._target_buf = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
         self._copy_stream = torch.cuda.Stream(device=dev)
         self._copy_done = [torch.cuda.Event() for _ in range(2)]
@@ -480,11 +481,34 @@ class ViewShardedTrainer:
         """End-to-end step from pinned HOST targets: the H2D copy of view i+1 overlaps the
         compute of view i on a side stream, and a view's own copy only has to land before its
         loss (binning and forward do not read the target); the per-view losses are read back."""
-        self._views_checked(lambda: self._run_host_views(targets_host))
-        self._finish()
         cur = torch.cuda.current_stream(self.splats.device)
-        self._pinned_losses.copy_(self.losses, non_blocking=True)
-        cur.synchronize()
+        run = lambda: self._run_host_views(targets_host)  # noqa: E731
+        if not (self.opt is not None and self.overlap_adam and self.async_binning and self.capacity
+                and self.overlap_read):
+            self._views_checked(run)
+            self._finish()
+            self._pinned_losses.copy_(self.losses, non_blocking=True)
+            cur.synchronize()
+            return self._pinned_losses
+        # as step(): one read after Adam is queued -- the losses and the optimiser's agreed flag together
+        for _ in range(4):
+            run()
+            self.opt.step(self.lrs, check_finite=False, grid_stream=self._adam_stream, grid_done=self._grid_done,
+                          veto=self._overflow)
+            self._pinned_losses.copy_(self.losses, non_blocking=True)
+            self._pinned_flag.copy_(self.opt.flag, non_blocking=True)
+            cur.synchronize()
+            code = int(self._pinned_flag[0])
+            if code != ShardedAdam.VETO:
+                break
+            self.state.t -= 1  # nothing was updated
+            self._grow_after_overflow()
+        else:
+            raise RuntimeError("view binning kept outgrowing its pair capacity")
+        self._pair_sum += self._pair_counts[: len(self.views)].sum()
+        self._pair_views += len(self.views)
+        if self.check_finite:
+            ShardedAdam.raise_if_nonfinite(code)
         return self._pinned_losses
 
     def _views_host(self, targets_host: Sequence[torch.Tensor]) -> None:

@@ -403,3 +403,32 @@ def test_step_overflow_vetoes_adam_and_redoes():
                                    err_msg=k)
     for k, w in ref.splats.tensors().items():
         np.testing.assert_allclose(tr.splats.tensors()[k].cpu().numpy(), w.cpu().numpy(), atol=2e-3, err_msg=k)
+
+
+def test_host_step_overflow_vetoes_adam_and_redoes():
+    """step_host: the same single read after Adam (losses and the agreed flag together), the same veto."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200.train import ViewShardedTrainer
+
+    n, arrays, specs, targets = _trainer_scene()
+    cams = [gb.PinholeCamera.from_spec(s) for s in specs]
+    host = [torch.as_tensor(t).pin_memory() for t in targets]
+
+    def make(**kw):
+        s = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+        return ViewShardedTrainer(s, cams, [0, 1, 2], **kw)
+
+    ref, tr = make(async_binning=False), make()
+    for t in (ref, tr):
+        t.step_host(host)
+    P = max(ref.pairs)
+    tr._set_capacity(P // 4, exact=True)
+    want = ref.step_host(host).clone()
+    got = tr.step_host(host).clone()
+    torch.cuda.synchronize()
+    assert tr.overflows == 1 and tr.capacity >= P and tr.state.t == ref.state.t == 2
+    np.testing.assert_allclose(got.numpy(), want.numpy(), rtol=1e-5)
+    for k, w in ref.splats.tensors().items():
+        np.testing.assert_allclose(tr.splats.tensors()[k].cpu().numpy(), w.cpu().numpy(), atol=2e-3, err_msg=k)
