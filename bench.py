@@ -403,15 +403,17 @@ def run_ours(args):
         "data": "synthetic (seeded Rng, BASELINE configs[3] shapes; random-init surfels, noise targets)",
         "config": {"workload": "configs[3] view-sharded training step: 1M surfels, 8x8 fp32 RGB textures, "
                                f"{args.views_per_gpu} Fibonacci-sphere views/GPU at 1600x1064, L1, "
-                               "NCCL all-reduce + Adam",
+                               "Adam (N > 1: NCCL reduce-scatter, Adam on the rank's slice, all-gather)",
                    "views_per_gpu": len(views), "surfels": cfg3.count, "texture": f"{n}x{n}",
                    "image": f"{W}x{H}", "tile": 16,
                    "compositor": ("fused " if trainer.fused else "") + os.environ.get("GB_COMPOSITOR", "direct") + (
                        f"(G={os.environ.get('GB_GROUP', '8')})" if os.environ.get("GB_COMPOSITOR") == "grp" else ""),
                    "mean_pairs_per_view": int(mean_pairs),
                    "binning": "blocking" if blocking else "capacity (no host read-back)",
-                   "cuda_graph": ("each step's view work (binning + compositing, both lanes) replayed as one CUDA "
-                                  "graph; collective + Adam eager; e2e step eager") if use_graph else "off",
+                   "cuda_graph": ("each step's view work (binning + compositing on all lanes) replayed as one "
+                                  "CUDA graph; collectives + Adam eager, Adam's texel update overlapped with the "
+                                  "next step's binning; e2e step eager") if use_graph else "off",
+                   "view_lanes": len(trainer._lanes),
                    "l2": "working set (0.8 GB textures + 0.8 GB grads + 1.6 GB Adam) >> 126 MB L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
