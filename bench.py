@@ -231,6 +231,7 @@ def run_ours(args):
     trainer = ViewShardedTrainer(splats, cams, views, lrs=lrs, graph=use_graph, async_binning=not blocking,
                                  lanes=int(os.environ.get("GB_LANES", "4")),
                                  overlap_adam=os.environ.get("GB_OVERLAP_ADAM", "1") == "1",
+                                 capacity_margin=float(os.environ.get("GB_CAP_MARGIN", "1.1")),
                                  fused=os.environ.get("GB_FUSED") == "1")
     trainer.graph_host = os.environ.get("GB_GRAPH_HOST", "0") == "1"
     if os.environ.get("GB_PRE_ADAM_READ") == "1":

@@ -195,7 +195,7 @@ class ViewShardedTrainer:
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
                  lanes: int = 4, fused: bool = False, async_binning: bool = True, graph: bool = False,
-                 capacity_margin: float = 1.25, sharded_adam: bool = True, overlap_adam: bool = True):
+                 capacity_margin: float = 1.1, sharded_adam: bool = True, overlap_adam: bool = True):
         self.splats = splats
         self.cameras = list(cameras)
         self.views = list(views)
