@@ -143,12 +143,12 @@ def cpu_view(scene64, cam, target, step_frac_adam=0.125):
     return len(b[1])
 
 
-def cpu_setup(args, cfg3):
+def cpu_setup(args):
+    """The configs[3] inputs generated by the oracle's own Rng restatement (no product code is loaded)."""
     from oracle import oracle as O
 
-    arrays = cfg3.arrays()
-    scene64 = O.Scene64(arrays, cfg3.n)
-    return O, scene64
+    arrays, cams, target = O.config3_inputs(count=args.count, n=args.n)
+    return O, O.Scene64(arrays, args.n), cams, target
 
 
 def run_reference(args):
@@ -158,23 +158,20 @@ def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
         return
-    import paper_2412_12734_b200.scenes as sc
-
-    cfg3 = sc.baseline_config(3, count=args.count, n=args.n)
-    O, scene64 = cpu_setup(args, cfg3)
+    O, scene64, cams, target = cpu_setup(args)
     cores = os.cpu_count() or 1
     times = []
-    views = list(range(len(cfg3.cameras)))
+    views = list(range(len(cams)))
     for it in range(args.warmup + args.steps):
         v = views[it % len(views)]
-        cam = O.Cam.from_spec(cfg3.cameras[v])
-        tgt = cfg3.target(v)
+        cam = cams[v]
+        tgt = target(v)
         t0 = time.perf_counter()
         cpu_view(scene64, cam, tgt)
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             times.append(dt)
-    W, H = cfg3.cameras[0].width, cfg3.cameras[0].height
+    W, H = cams[0].width, cams[0].height
     step_s = sum(times) / len(times)
     mps = W * H / 1e6 / step_s
     line = {
@@ -407,8 +404,7 @@ def run_ours(args):
                                "Adam (N > 1: NCCL reduce-scatter, Adam on the rank's slice, all-gather)",
                    "views_per_gpu": len(views), "surfels": cfg3.count, "texture": f"{n}x{n}",
                    "image": f"{W}x{H}", "tile": 16,
-                   "compositor": ("fused " if trainer.fused else "") + os.environ.get("GB_COMPOSITOR", "direct") + (
-                       f"(G={os.environ.get('GB_GROUP', '8')})" if os.environ.get("GB_COMPOSITOR") == "grp" else ""),
+                   "compositor": ("fused " if trainer.fused else "") + "direct (one warp per 8x4 pixel block)",
                    "mean_pairs_per_view": int(mean_pairs),
                    "binning": "blocking" if blocking else "capacity (no host read-back)",
                    "cuda_graph": ("each step's view work (binning + compositing on all lanes) replayed as one "
@@ -432,10 +428,9 @@ def run_ours(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            O, scene64 = cpu_setup(args, cfg3)
-            cam0 = O.Cam.from_spec(cfg3.cameras[views[0]])
+            O, scene64, ocams, otarget = cpu_setup(args)
             t0 = time.perf_counter()
-            cpu_view(scene64, cam0, cfg3.target(views[0]))
+            cpu_view(scene64, ocams[views[0]], otarget(views[0]))
             dt = time.perf_counter() - t0
             cores = os.cpu_count() or 1
             line["cpu_baseline"] = {

@@ -79,7 +79,10 @@ typedef struct {
 
 /* GradientBuffer (core.hpp:140-178) with the same layout as gb_splats.
  * Backward ACCUMULATES into it (caller zeroes), so several views can sum
- * into one buffer.  depth_key never receives a gradient. */
+ * into one buffer with atomic adds, so backwards on different streams may
+ * target the same buffer concurrently.  depth_key never receives a gradient.
+ * Alignment (vector atomics): log_scale and the ortho position 8 B, quat and
+ * grid_values (even n) 16 B, else GB_INVALID_ARGUMENT. */
 typedef struct {
     float *position;
     float *depth_key;
@@ -257,7 +260,7 @@ GB_API gb_status gb_mse_loss(gb_context *ctx, const float *color, const float *t
  * followed by the backward compositor.  target: HWC fp32 (device).  out: NULL, or forward buffers filled as gb_render_forward
  * would; image_grad: NULL, or receives the cotangent; *loss (device float) += as the loss entry points
  * (summation order differs); g receives the gradients as gb_render_backward.  Per-pixel arithmetic is the
- * separate calls'; with GB_COMPOSITOR=grp|staged this runs as those three calls. */
+ * separate calls'. */
 #define GB_LOSS_L1 0
 #define GB_LOSS_MSE 1
 GB_API gb_status gb_render_loss_backward(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_binning *b,

@@ -1326,3 +1326,87 @@ double orc_l1_loss(const double *c, const double *t, int64_t n, double scale, do
     }
     return acc * scale;
 }
+
+/* ---- seeded inputs (rng.hpp:12-46) --------------------------------------------
+ * MT19937-64 as published by Matsumoto & Nishimura (the engine std::mt19937_64 names):
+ * w=64, n=312, m=156, r=31, a=0xB5026F5AA96619E9, tempering (u,d)=(29,0x5555555555555555),
+ * (s,b)=(17,0x71D67FFFEDA60000), (t,c)=(37,0xFFF7EEE000000000), l=43, init multiplier f=6364136223846793005. */
+#define ORC_MT_N 312
+#define ORC_MT_M 156
+void orc_rng_seed(orc_rng *r, uint64_t seed) {
+    r->mt[0] = seed;
+    for (int i = 1; i < ORC_MT_N; ++i)
+        r->mt[i] = 6364136223846793005ULL * (r->mt[i - 1] ^ (r->mt[i - 1] >> 62)) + (uint64_t)i;
+    r->idx = ORC_MT_N;
+    r->have_spare = 0;
+    r->spare = 0.0;
+}
+
+uint64_t orc_rng_next(orc_rng *r) {
+    static const uint64_t upper = 0xFFFFFFFF80000000ULL, lower = 0x7FFFFFFFULL, a = 0xB5026F5AA96619E9ULL;
+    if (r->idx >= ORC_MT_N) {
+        for (int i = 0; i < ORC_MT_N; ++i) {
+            const uint64_t x = (r->mt[i] & upper) | (r->mt[(i + 1) % ORC_MT_N] & lower);
+            r->mt[i] = r->mt[(i + ORC_MT_M) % ORC_MT_N] ^ (x >> 1) ^ ((x & 1ULL) ? a : 0ULL);
+        }
+        r->idx = 0;
+    }
+    uint64_t y = r->mt[r->idx++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+}
+
+double orc_rng_uniform(orc_rng *r) { return (double)(orc_rng_next(r) >> 11) * 0x1.0p-53; } /* rng.hpp:20-22 */
+
+static double rng_uniform_in(orc_rng *r, double lo, double hi) { return lo + (hi - lo) * orc_rng_uniform(r); }
+
+double orc_rng_normal(orc_rng *r, double mean, double stddev) { /* rng.hpp:26-40 */
+    if (r->have_spare) {
+        r->have_spare = 0;
+        return mean + stddev * r->spare;
+    }
+    const double u1 = 1.0 - orc_rng_uniform(r);
+    const double u2 = orc_rng_uniform(r);
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.14159265358979323846 * u2; /* M_PI */
+    r->spare = radius * sin(angle);
+    r->have_spare = 1;
+    return mean + stddev * radius * cos(angle);
+}
+
+int orc_scene_generate_pinhole(int64_t count, int32_t n, uint64_t seed, double mean_lo, double mean_hi,
+                               double mean_sigma, double log_scale_lo, double log_scale_hi, float *position,
+                               float *quat, float *log_scale, float *opacity_logit, float *grid) {
+    if (count < 0 || n < 1) return ORC_INVALID_ARGUMENT;
+    orc_rng *geo = (orc_rng *)malloc(sizeof(orc_rng));
+    if (!geo) return ORC_OOM;
+    orc_rng_seed(geo, seed);
+    for (int64_t k = 0; k < count; ++k) {
+        for (int i = 0; i < 3; ++i)
+            position[3 * k + i] = (float)(mean_sigma > 0.0 ? orc_rng_normal(geo, 0.0, mean_sigma)
+                                                           : rng_uniform_in(geo, mean_lo, mean_hi));
+        for (int i = 0; i < 2; ++i) log_scale[2 * k + i] = (float)rng_uniform_in(geo, log_scale_lo, log_scale_hi);
+        double q[4], nn = 0.0;
+        for (int i = 0; i < 4; ++i) {
+            q[i] = orc_rng_normal(geo, 0.0, 1.0);
+            nn += q[i] * q[i];
+        }
+        const double inv = 1.0 / sqrt(nn);
+        for (int i = 0; i < 4; ++i) quat[4 * k + i] = (float)(q[i] * inv);
+        opacity_logit[k] = (float)orc_rng_normal(geo, 0.0, 1.0);
+    }
+    orc_rng_seed(geo, seed + 1);
+    const int64_t nt = count * (int64_t)n * n * 3;
+    for (int64_t i = 0; i < nt; ++i) grid[i] = (float)orc_rng_uniform(geo);
+    free(geo);
+    return ORC_OK;
+}
+
+void orc_uniform_fill(uint64_t seed, int64_t n, float *out) {
+    orc_rng r;
+    orc_rng_seed(&r, seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = (float)orc_rng_uniform(&r);
+}

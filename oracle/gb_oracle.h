@@ -142,6 +142,29 @@ int64_t orc_adam_group(double *p, const double *g, double *m, double *v, int64_t
 /* L1 loss: value = scale*sum|c-t|, grad = scale*sign(c-t) (sign(0)=0). */
 double orc_l1_loss(const double *c, const double *t, int64_t n, double scale, double *grad);
 
+/* Seeded synthetic inputs, restated independently of the product library so that bench.py's
+ * reference arm never loads it.  Rng (rng.hpp:12-46): std::mt19937_64 (restated from its published
+ * definition), uniform() = (x >> 11) * 2^-53, Box-Muller normal() with a cached spare.  Scenes as
+ * geometry from Rng(seed), textures from Rng(seed+1); fp64 draws rounded to fp32 once.
+ * Bit-identity with the product's gb_scene_generate is a CPU test (tests/test_oracle_scene.py). */
+typedef struct {
+    uint64_t mt[312];
+    int32_t idx;
+    int32_t have_spare;
+    double spare;
+} orc_rng;
+void orc_rng_seed(orc_rng *r, uint64_t seed);
+uint64_t orc_rng_next(orc_rng *r);
+double orc_rng_uniform(orc_rng *r);
+double orc_rng_normal(orc_rng *r, double mean, double stddev);
+/* pinhole scene: means N(0, mean_sigma^2) when mean_sigma > 0 else U[mean_lo, mean_hi)^3; log-scales
+ * U[log_scale_lo, log_scale_hi); quaternion = normalised N(0,1)^4; logit N(0,1); texels U[0,1). */
+int orc_scene_generate_pinhole(int64_t count, int32_t n, uint64_t seed, double mean_lo, double mean_hi,
+                               double mean_sigma, double log_scale_lo, double log_scale_hi, float *position,
+                               float *quat, float *log_scale, float *opacity_logit, float *grid);
+/* n uniforms from Rng(seed) rounded to fp32 (the seeded-noise targets use seed + 2 + view). */
+void orc_uniform_fill(uint64_t seed, int64_t n, float *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,13 @@ def oracle_lib():
         L.orc_adam_group.restype = C.c_int64
         L.orc_l1_loss.argtypes = [P, P, C.c_int64, C.c_double, P]
         L.orc_l1_loss.restype = C.c_double
+        L.orc_scene_generate_pinhole.argtypes = [C.c_int64, C.c_int32, C.c_uint64] + [C.c_double] * 5 + [P] * 5
+        L.orc_uniform_fill.argtypes = [C.c_uint64, C.c_int64, P]
+        L.orc_rng_seed.argtypes = [P, C.c_uint64]
+        L.orc_rng_uniform.argtypes = [P]
+        L.orc_rng_uniform.restype = C.c_double
+        L.orc_rng_normal.argtypes = [P, C.c_double, C.c_double]
+        L.orc_rng_normal.restype = C.c_double
         _oracle = L
     return _oracle
 
@@ -484,3 +491,79 @@ def ref_gradient_fd(scene: Scene64, cam: Cam, weights, step):
                              w.ctypes.data, step, gp("position"), gp("depth_key"), gp("theta"), gp("log_scale"),
                              gp("opacity_logit"), gp("grid")), "ref_gradient_fd")
     return g
+
+
+# ----------------------------------------------------------------------------------------------
+# Seeded BASELINE inputs, generated here (not through the product library) so that bench.py's
+# reference arm loads no product code.  Same semantics as paper_2412_12734_b200.scenes;
+# tests/test_oracle_scene.py checks the bits are identical.
+# ----------------------------------------------------------------------------------------------
+class _RngState(C.Structure):
+    _fields_ = [("mt", C.c_uint64 * 312), ("idx", C.c_int32), ("have_spare", C.c_int32), ("spare", C.c_double)]
+
+
+def rng_uniform(seed: int, n: int) -> np.ndarray:
+    L, st = oracle_lib(), _RngState()
+    L.orc_rng_seed(C.byref(st), seed)
+    return np.array([L.orc_rng_uniform(C.byref(st)) for _ in range(n)])
+
+
+def rng_normal(seed: int, n: int, mean=0.0, stddev=1.0) -> np.ndarray:
+    L, st = oracle_lib(), _RngState()
+    L.orc_rng_seed(C.byref(st), seed)
+    return np.array([L.orc_rng_normal(C.byref(st), mean, stddev) for _ in range(n)])
+
+
+def generate_pinhole(count: int, n: int, seed: int, *, mean_lo=-1.0, mean_hi=1.0, mean_sigma=0.0,
+                     scale_lo=0.005, scale_hi=0.05) -> dict:
+    import math
+
+    arr = {"position": np.zeros((count, 3), np.float32), "depth_key": None, "theta": None,
+           "quat": np.zeros((count, 4), np.float32), "log_scale": np.zeros((count, 2), np.float32),
+           "opacity_logit": np.zeros(count, np.float32), "grid": np.zeros((count, n * n * 3), np.float32)}
+    rc = oracle_lib().orc_scene_generate_pinhole(count, n, seed, mean_lo, mean_hi, mean_sigma, math.log(scale_lo),
+                                                 math.log(scale_hi), arr["position"].ctypes.data,
+                                                 arr["quat"].ctypes.data, arr["log_scale"].ctypes.data,
+                                                 arr["opacity_logit"].ctypes.data, arr["grid"].ctypes.data)
+    _check(rc, "orc_scene_generate_pinhole")
+    return arr
+
+
+def uniform_image(seed: int, width: int, height: int) -> np.ndarray:
+    out = np.zeros((height, width, 3), np.float32)
+    oracle_lib().orc_uniform_fill(seed, out.size, out.ctypes.data)
+    return out
+
+
+def look_at(eye, target, width, height, fx, fy, cx, cy, up=(0.0, 1.0, 0.0), near_plane=0.01) -> Cam:
+    """OpenCV look-at (SURVEY §8(d) ⚑): z = normalize(target - eye), x = normalize(up x z), y = z x x."""
+    eye = np.asarray(eye, dtype=np.float64)
+    f = np.asarray(target, dtype=np.float64) - eye
+    f /= np.linalg.norm(f)
+    r = np.cross(np.asarray(up, dtype=np.float64), f)
+    r /= np.linalg.norm(r)
+    d = np.cross(f, r)
+    rot = np.stack([r, d, f])
+    return Cam(MODE_PINHOLE, width, height, (0.0, 0.0, 0.0), fx, fy, cx, cy, rot, -rot @ eye, near_plane)
+
+
+def fibonacci_cameras(count: int, radius: float, width: int, height: int, fx, fy, cx, cy) -> list:
+    """configs[3]: y_i = 1 - 2(i+1/2)/count, r_i = sqrt(1-y_i^2), phi_i = i*pi*(3-sqrt5)."""
+    import math
+
+    cams = []
+    for i in range(count):
+        y = 1.0 - 2.0 * (i + 0.5) / count
+        r = math.sqrt(max(0.0, 1.0 - y * y))
+        phi = i * math.pi * (3.0 - math.sqrt(5.0))
+        cams.append(look_at((radius * r * math.cos(phi), radius * y, radius * r * math.sin(phi)), (0.0, 0.0, 0.0),
+                            width, height, fx, fy, cx, cy))
+    return cams
+
+
+def config3_inputs(count: int = 1_000_000, n: int = 8, views: int = 64, seed: int = 0):
+    """BASELINE configs[3]: (arrays, cameras, target(view)) with N(0, 2^2) means, log-U[0.002, 0.03] scales,
+    64 Fibonacci views at radius 6, 1600x1064, fx = fy = 1000; targets from Rng(seed + 2 + view)."""
+    arrays = generate_pinhole(count, n, seed, mean_sigma=2.0, scale_lo=0.002, scale_hi=0.03)
+    cams = fibonacci_cameras(views, 6.0, 1600, 1064, 1000.0, 1000.0, 800.0, 532.0)
+    return arrays, cams, (lambda v: uniform_image(seed + 2 + v, cams[v].width, cams[v].height))

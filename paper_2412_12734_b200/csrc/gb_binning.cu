@@ -98,10 +98,21 @@ struct PermutedCount {
 };
 using CountIter = thrust::transform_iterator<PermutedCount, thrust::counting_iterator<int64_t>, uint32_t>;
 
+// The scan saturates at kPairLimit = 2^31 - 1 (the sorts index pairs with int): a pair count that would wrap
+// the uint32 offsets reads as the limit instead, which the blocking build rejects and the capacity build
+// flags as an overflow.  min(a + b, L) is associative for a, b <= L, and a + b < 2^32 cannot wrap.
+constexpr uint32_t kPairLimit = 0x7fffffffu;
+struct SatAdd {
+    __host__ __device__ uint32_t operator()(uint32_t a, uint32_t b) const {
+        const uint32_t s = a + b;
+        return s < kPairLimit ? s : kPairLimit;
+    }
+};
+
 size_t scan_temp_bytes(int64_t K) {
     size_t bytes = 0;
     CountIter it(thrust::counting_iterator<int64_t>(0), PermutedCount{nullptr, nullptr});
-    cub::DeviceScan::InclusiveSum(nullptr, bytes, it, (uint32_t*)nullptr, (int)K);
+    cub::DeviceScan::InclusiveScan(nullptr, bytes, it, (uint32_t*)nullptr, SatAdd{}, (int)K);
     return bytes;
 }
 
@@ -125,13 +136,13 @@ cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* dep
     return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, depth_bits, depth_sorted, iota, perm, (int)K, 0, 32, st);
 }
 
-// offsets (K+1 entries) = exclusive scan of the counts in perm order; offsets[K] = P.
+// offsets (K+1 entries) = exclusive scan of the counts in perm order; offsets[K] = P (saturated at 2^31 - 1).
 cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
                         uint32_t* offsets, int64_t K, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(offsets, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess || K == 0) return e;
     CountIter it(thrust::counting_iterator<int64_t>(0), PermutedCount{perm, counts});
-    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, it, offsets + 1, (int)K, st);
+    return cub::DeviceScan::InclusiveScan(temp, temp_bytes, it, offsets + 1, SatAdd{}, (int)K, st);
 }
 
 cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,

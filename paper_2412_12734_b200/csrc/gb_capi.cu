@@ -252,6 +252,19 @@ gb_status validate_splats(const gb_splats* s, int mode) {
     return GB_OK;
 }
 
+// gradient buffers take vector reds (K4/K5): ortho position and log_scale 8-B aligned, quat and even-n grids 16-B
+gb_status validate_grads(const gb_grads* g, int mode, int n, const char* where) {
+    if (!g->position || !g->log_scale || !g->opacity_logit || !g->grid_values ||
+        (mode == GB_MODE_ORTHO && !g->theta) || (mode == GB_MODE_PINHOLE && !g->quat))
+        return fail(GB_INVALID_ARGUMENT, "%s: null gradient buffer", where);
+    const bool bad = (reinterpret_cast<uintptr_t>(g->log_scale) & 7) ||
+                     (mode == GB_MODE_ORTHO && (reinterpret_cast<uintptr_t>(g->position) & 7)) ||
+                     (mode == GB_MODE_PINHOLE && (reinterpret_cast<uintptr_t>(g->quat) & 15)) ||
+                     ((n % 2) == 0 && (reinterpret_cast<uintptr_t>(g->grid_values) & 15));
+    if (bad) return fail(GB_INVALID_ARGUMENT, "%s: misaligned gradient buffer", where);
+    return GB_OK;
+}
+
 gb::CamConst make_cam_const(const gb_camera* cam) {
     gb::CamConst cc;
     cc.width = cam->width;
@@ -272,10 +285,6 @@ gb::RasterConst make_raster_const(const gb_binning* b, int n, double sigma) {
     rc.tex_scale = (float)((double)(n - 1) / (2.0 * sigma));
     rc.tex_offset = (float)((double)(n - 1) * 0.5);
     rc.sigma = (float)sigma;
-    // K4 warp-entries with <= 12 active lanes add per lane (measured optimum of 0..32: 0 = always
-    // reduce 575 MP/s, 8 = 605, 12 = 607, 16 = 605, 24 = 586, 32 = 453); GB_K4_DIRECT overrides
-    const char* dl = getenv("GB_K4_DIRECT");
-    rc.direct_lanes = dl ? atoi(dl) : 12;
     return rc;
 }
 
@@ -680,6 +689,9 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
                                 cudaMemcpyDeviceToHost, stream));
         GB_CUDA(cudaStreamSynchronize(stream));
         P = *ctx->pinned_total;
+        if (P >= 0x7fffffffll)
+            return fail(GB_NOT_SUPPORTED, "build_binning: %lld+ tile/primitive pairs exceed the 2^31 - 1 the sorts index",
+                        (long long)P);
         b->P = P;
     }
     const int64_t Pc = P > 0 ? P : 1;
@@ -730,7 +742,8 @@ gb_status resolve_total(const gb_binning* b) {
 
 gb_status gb_binning_set_capacity(gb_binning* b, int64_t capacity, int32_t* overflow) {
     if (!b) return fail(GB_INVALID_ARGUMENT, "null binning");
-    if (capacity < 0 || capacity > 0xffffffffll) return fail(GB_INVALID_ARGUMENT, "binning capacity out of range");
+    if (capacity < 0 || capacity >= 0x7fffffffll)
+        return fail(GB_INVALID_ARGUMENT, "binning capacity out of range [0, 2^31 - 1)");
     b->capacity = capacity;
     b->overflow = capacity > 0 ? overflow : nullptr;
     b->built = false;
@@ -824,9 +837,7 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
         return fail(GB_MISMATCH, "render_backward: image size mismatch");
     if (!image_grad) return fail(GB_MISMATCH, "render_backward: image_grad size mismatch");
     if (s->count == 0) return GB_OK;
-    if (!g->position || !g->log_scale || !g->opacity_logit || !g->grid_values ||
-        (cam->mode == GB_MODE_ORTHO && !g->theta) || (cam->mode == GB_MODE_PINHOLE && !g->quat))
-        return fail(GB_INVALID_ARGUMENT, "render_backward: null gradient buffer");
+    if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_backward")) return st;
     if (gb_status st = set_device(ctx)) return st;
     cudaStream_t stream = ctx->stream;
     const int64_t K = s->count;
@@ -896,34 +907,10 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
         if (!out->color || !out->final_transmittance || !out->last_rank)
             return fail(GB_INVALID_ARGUMENT, "render_loss_backward: null output buffer");
     }
-    if (s->count > 0 && (!g->position || !g->log_scale || !g->opacity_logit || !g->grid_values ||
-                         (cam->mode == GB_MODE_ORTHO && !g->theta) || (cam->mode == GB_MODE_PINHOLE && !g->quat)))
-        return fail(GB_INVALID_ARGUMENT, "render_loss_backward: null gradient buffer");
+    if (s->count > 0)
+        if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_loss_backward")) return st;
     if (gb_status st = set_device(ctx)) return st;
     const int64_t npix = (int64_t)cam->width * cam->height;
-    if (!gb::fused_available()) {  // the three separate calls, with context scratch for what the caller skipped
-        gb_render_out tmp{};
-        if (!out) {
-            GB_CUDA(ctx->fuse_color.ensure(sizeof(float) * 3 * npix));
-            GB_CUDA(ctx->fuse_trans.ensure(sizeof(float) * npix));
-            GB_CUDA(ctx->fuse_last.ensure(sizeof(int32_t) * npix));
-            tmp.color = ctx->fuse_color.as<float>();
-            tmp.final_transmittance = ctx->fuse_trans.as<float>();
-            tmp.last_rank = ctx->fuse_last.as<int32_t>();
-            tmp.width = cam->width;
-            tmp.height = cam->height;
-            out = &tmp;
-        }
-        if (!image_grad) {
-            GB_CUDA(ctx->fuse_grad.ensure(sizeof(float) * 3 * npix));
-            image_grad = ctx->fuse_grad.as<float>();
-        }
-        if (gb_status st = gb_render_forward(ctx, s, cam, b, out)) return st;
-        if (gb_status st = (loss_kind == GB_LOSS_L1 ? gb_l1_loss : gb_mse_loss)(ctx, out->color, target, 3 * npix,
-                                                                              scale, image_grad, loss))
-            return st;
-        return gb_render_backward(ctx, s, cam, b, out, image_grad, g);
-    }
     cudaStream_t stream = ctx->stream;
     const int64_t K = s->count;
     if (K > 0) {
@@ -933,7 +920,8 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
     const gb::CamConst cc = make_cam_const(cam);
     const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
     const int tiles = b->tiles_x * b->tiles_y;
-    if (gb::fused_single_kernel()) {
+#ifdef GB_FUSED_SINGLE_KERNEL
+    if (true) {  // variant build: K3 + K6 + K4 in one kernel (measured slower)
         ProfScope ps(ctx, GB_K_FUSED);
         GB_CUDA(gb::launch_fused(cam->mode, s->grid.n, tiles, b->cfg.tile_size, b->ranges.as<uint2>(),
                                  b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
@@ -942,7 +930,9 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
                                  out ? out->last_rank : nullptr, image_grad, loss,
                                  K > 0 ? ctx->accum.as<float>() : nullptr, g->grid_values, stream));
         ctx->launches += 1;
-    } else {  // K3 with the loss in its epilogue, then K4: no image round trip, no K6 pass
+    }
+#else
+    {  // K3 with the loss in its epilogue, then K4: no image round trip, no K6 pass
         float* trans = out ? out->final_transmittance : nullptr;
         int32_t* last = out ? out->last_rank : nullptr;
         if (!out) {
@@ -972,6 +962,7 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
         }
         ctx->launches += 2;
     }
+#endif
     if (out) {
         out->splat_count = s->count;
         out->grid_n = s->grid.n;

@@ -62,7 +62,6 @@ struct RasterConst {
     float tex_scale;       // (n-1)/(2 sigma)
     float tex_offset;      // (n-1)/2
     float sigma;
-    int direct_lanes;      // K4: warp-entries with at most this many active lanes skip the warp reductions
 };
 
 // Thread -> pixel mapping inside a tile.  For tile sizes that are multiples
@@ -180,28 +179,19 @@ cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, CullRec* cull
 cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
                          cudaStream_t st);
 
-// gb_composite.cu: K3/K4 with sub-warp groups (tile sizes 8 and 16)
-bool grp_supported(int ts);
-cudaError_t launch_forward_grp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                               const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
-                               float* color, float* trans, int32_t* last, cudaStream_t st);
-cudaError_t launch_backward_grp(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
-                                const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
-                                const float* trans, const int32_t* last, const float* image_grad, float* accum,
-                                float* grid_grad, cudaStream_t st);
-
-// gb_raster.cu: K3 + K6 + K4 in one kernel (direct compositors only), or K3 + K6 then K4
-bool fused_available();
-bool fused_single_kernel();
+// gb_raster.cu: K3 with the photometric loss in its epilogue (K3 + K6); the single fused K3+K6+K4 kernel
+// exists only in the -DGB_FUSED_SINGLE_KERNEL variant build
 cudaError_t launch_forward_loss(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                                 const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                                 const RasterConst& rc, int kind, const float* target, float scale, float* color,
                                 float* trans, int32_t* last, float* image_grad, float* loss, cudaStream_t st);
+#ifdef GB_FUSED_SINGLE_KERNEL
 cudaError_t launch_fused(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                          const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                          const RasterConst& rc, int kind, const float* target, float scale, float* color, float* trans,
                          int32_t* last, float* image_grad, float* loss, float* accum, float* grid_grad,
                          cudaStream_t st);
+#endif
 
 __device__ __forceinline__ uint32_t float_order_key(float d) {
     uint32_t b = __float_as_uint(d == 0.0f ? 0.0f : d);  // -0 sorts as +0 (double compare)

@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(256, GB_K1_MINB) k_project(const ProjParams p,
 }
 
 // K5: chain the K4 screen-space sums to the raw parameters and ADD into the
-// gradient buffer.  Ortho: raster.hpp:350-360 with the per-eval products
+// gradient buffer with reds (red.global.add): several views' K5s run on
+// different streams into one buffer (the trainer's view lanes), so a plain
+// read-modify-write could lose updates.  Ortho: raster.hpp:350-360 with the per-eval products
 // (u_hat*u, ...) summed by K4.  Pinhole: dL/dM from (S_A, S_B, S_D) then the
 // camera/quaternion chain (oracle pinhole_chain()).
 // 8 CTAs of 128 threads per SM (64 registers, with spills): fp64 latency hides better with more warps
@@ -409,12 +411,13 @@ __global__ void __launch_bounds__(128, GB_K5_MINB) k_chain(const ProjParams p, c
     if (p.mode == GB_MODE_ORTHO) {
         const double su = A.x, sv = A.y, suv = A.z, svu = A.w, suu = B.x, svv = B.y, sop = B.z;
         const double inv_su = 1.0 / g.s_u, inv_sv = 1.0 / g.s_v;
-        g_out.position[2 * k + 0] += (float)(su * (-g.cos_t * inv_su) + sv * (g.sin_t * inv_sv));
-        g_out.position[2 * k + 1] += (float)(su * (-g.sin_t * inv_su) + sv * (-g.cos_t * inv_sv));
-        g_out.theta[k] += (float)(suv * (g.s_v * inv_su) - svu * (g.s_u * inv_sv));
-        if (!g.su_clamped) g_out.log_scale[2 * k + 0] += (float)(-suu);
-        if (!g.sv_clamped) g_out.log_scale[2 * k + 1] += (float)(-svv);
-        g_out.opacity_logit[k] += (float)(sop * (g.alpha_k * (1.0 - g.alpha_k)));
+        atomicAdd(reinterpret_cast<float2*>(g_out.position) + k,
+                  make_float2((float)(su * (-g.cos_t * inv_su) + sv * (g.sin_t * inv_sv)),
+                              (float)(su * (-g.sin_t * inv_su) + sv * (-g.cos_t * inv_sv))));
+        atomicAdd(g_out.theta + k, (float)(suv * (g.s_v * inv_su) - svu * (g.s_u * inv_sv)));
+        atomicAdd(reinterpret_cast<float2*>(g_out.log_scale) + k,
+                  make_float2(g.su_clamped ? 0.0f : (float)(-suu), g.sv_clamped ? 0.0f : (float)(-svv)));
+        atomicAdd(g_out.opacity_logit + k, (float)(sop * (g.alpha_k * (1.0 - g.alpha_k))));
         return;
     }
     if (!g.valid) return;
@@ -467,12 +470,12 @@ __global__ void __launch_bounds__(128, GB_K5_MINB) k_chain(const ProjParams p, c
     const double* R = p.R;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        g_out.position[3 * k + j] += (float)(R[0 + j] * g_pc[0] + R[3 + j] * g_pc[1] + R[6 + j] * g_pc[2]);
+        atomicAdd(g_out.position + 3 * k + j, (float)(R[0 + j] * g_pc[0] + R[3 + j] * g_pc[1] + R[6 + j] * g_pc[2]));
         g_tu[j] = g.s_u * (R[0 + j] * g_col0[0] + R[3 + j] * g_col0[1] + R[6 + j] * g_col0[2]);
         g_tv[j] = g.s_v * (R[0 + j] * g_col1[0] + R[3 + j] * g_col1[1] + R[6 + j] * g_col1[2]);
     }
-    if (!g.su_clamped) g_out.log_scale[2 * k + 0] += (float)(g_su * g.s_u);
-    if (!g.sv_clamped) g_out.log_scale[2 * k + 1] += (float)(g_sv * g.s_v);
+    atomicAdd(reinterpret_cast<float2*>(g_out.log_scale) + k,
+              make_float2(g.su_clamped ? 0.0f : (float)(g_su * g.s_u), g.sv_clamped ? 0.0f : (float)(g_sv * g.s_v)));
     const double w = g.qn[0], x = g.qn[1], y = g.qn[2], z = g.qn[3];
     double gq[4];
     gq[0] = g_tu[1] * 2 * z - g_tu[2] * 2 * y - g_tv[0] * 2 * z + g_tv[2] * 2 * x;
@@ -480,9 +483,10 @@ __global__ void __launch_bounds__(128, GB_K5_MINB) k_chain(const ProjParams p, c
     gq[2] = -g_tu[0] * 4 * y + g_tu[1] * 2 * x - g_tu[2] * 2 * w + g_tv[0] * 2 * x + g_tv[2] * 2 * z;
     gq[3] = -g_tu[0] * 4 * z + g_tu[1] * 2 * w + g_tu[2] * 2 * x - g_tv[0] * 2 * w - g_tv[1] * 4 * z + g_tv[2] * 2 * y;
     const double dot = w * gq[0] + x * gq[1] + y * gq[2] + z * gq[3];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) g_out.quat[4 * k + i] += (float)((gq[i] - g.qn[i] * dot) / g.qnorm);
-    g_out.opacity_logit[k] += (float)(sop * (g.alpha_k * (1.0 - g.alpha_k)));
+    atomicAdd(reinterpret_cast<float4*>(g_out.quat) + k,
+              make_float4((float)((gq[0] - g.qn[0] * dot) / g.qnorm), (float)((gq[1] - g.qn[1] * dot) / g.qnorm),
+                          (float)((gq[2] - g.qn[2] * dot) / g.qnorm), (float)((gq[3] - g.qn[3] * dot) / g.qnorm)));
+    atomicAdd(g_out.opacity_logit + k, (float)(sop * (g.alpha_k * (1.0 - g.alpha_k))));
 }
 
 }  // namespace gb

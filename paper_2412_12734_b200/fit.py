@@ -175,7 +175,7 @@ def _write_checkpoint(directory: str, it: int, splats: SplatSet, history: List[M
         with open(base + ".history.csv", "w") as fh:
             fh.write("iter,loss,psnr\n")
             for r in history:
-                fh.write(f"{r.iter},{r.loss!r},{r.psnr!r}\n")
+                fh.write("%d,%.17g,%.17g\n" % (r.iter, r.loss, r.psnr))  # train.hpp:149-165 writes %.17g
     except Exception as e:  # noqa: BLE001
         raise FitError(f"checkpoint write failed: {e}") from e
 

@@ -46,6 +46,8 @@ def reduce_gradients(grads: GradientBuffer, process_group=None) -> None:
             torch.distributed.all_reduce(grads.flat, op=torch.distributed.ReduceOp.SUM, group=process_group)
 
 
+PAIR_LIMIT = 2 ** 31 - 1  # the binning's pair-count limit (gb_binning.cu kPairLimit; capacities stay below it)
+
 _ADAM_GROUP = {"position": 0, "theta": 1, "quat": 1, "log_scale": 2, "opacity_logit": 3, "grid": 4}
 
 
@@ -351,7 +353,11 @@ class ViewShardedTrainer:
         self._on_lanes(body)
 
     def _set_capacity(self, pairs_max: int, exact: bool = False) -> None:
+        if pairs_max >= PAIR_LIMIT:
+            raise RuntimeError(f"view binning needs {pairs_max} tile/primitive pairs, more than the "
+                               f"{PAIR_LIMIT - 1} the sorts index")
         cap = pairs_max if exact else ((int(pairs_max * self.capacity_margin) + 4096 + 65535) & ~65535)
+        cap = min(cap, PAIR_LIMIT - 1)  # the margin never pushes the capacity past the C-ABI's limit
         for lane in self._lanes:
             lane.binning.set_capacity(cap, self._overflow)
         self.capacity = cap
@@ -373,9 +379,6 @@ class ViewShardedTrainer:
             self.overflows += 1
             self._overflow.zero_()
             need = int((self._pair_counts[: len(self.views)].to(torch.int64) & 0xFFFFFFFF).max().item())  # uint32
-            if need >= 2 ** 31:
-                raise RuntimeError(f"view binning needs {need} tile/primitive pairs, more than the 2^31 the "
-                                   "sort supports")
             self._set_capacity(need)
         else:
             raise RuntimeError("view binning kept outgrowing its pair capacity")
@@ -471,9 +474,6 @@ class ViewShardedTrainer:
         self.overflows += 1
         if int(self._overflow.item()):
             need = int((self._pair_counts[: len(self.views)].to(torch.int64) & 0xFFFFFFFF).max().item())  # uint32
-            if need >= 2 ** 31:
-                raise RuntimeError(f"view binning needs {need} tile/primitive pairs, more than the 2^31 the "
-                                   "sort supports")
             self._overflow.zero_()
             self._set_capacity(need)
 

@@ -175,34 +175,13 @@ def test_configs2_full():
 
 
 # ---------------------------------------------------------------------------------------------
-# the measured alternative compositors (GB_COMPOSITOR, read by the library at every launch)
-# ---------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("variant,group", [("staged", None), ("grp", "4"), ("grp", "8"), ("grp", "16")])
-def test_alternative_compositors(monkeypatch, variant, group):
-    import paper_2412_12734_b200.scenes as sc
-
-    monkeypatch.setenv("GB_COMPOSITOR", variant)
-    if group:
-        monkeypatch.setenv("GB_GROUP", group)
-    cfgs = _config(0, count=20_000, n=4)
-    _check(f"variant_{variant}{group or ''}_pinhole", cfgs.arrays(), O.MODE_PINHOLE, 4,
-           O.Cam.from_spec(cfgs.cameras[0]), O.Cfg())
-    arrays = sc.generate(O.MODE_ORTHO, 3000, 3, 31, width=120, height=88, scale_lo=0.5, scale_hi=8.0)
-    _check(f"variant_{variant}{group or ''}_ortho_n3", arrays, O.MODE_ORTHO, 3,
-           O.Cam(O.MODE_ORTHO, 120, 88, (0.2, 0.1, 0.3)), O.Cfg(tile_size=8))
-
-
-# ---------------------------------------------------------------------------------------------
-# render_loss_backward: K3 + K6 + K4 in one kernel (and its three-call fallback, GB_NO_FUSE)
+# render_loss_backward: K3 with the loss in its epilogue, then K4
 # ---------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("loss", ["l1", "mse"])
-@pytest.mark.parametrize("fallback", [False, True])
-def test_fused_forward_loss_backward(monkeypatch, loss, fallback):
+def test_fused_forward_loss_backward(loss):
     import paper_2412_12734_b200.scenes as sc
 
-    if fallback:
-        monkeypatch.setenv("GB_NO_FUSE", "1")
-    tag = f"fused_{loss}{'_fallback' if fallback else ''}"
+    tag = f"fused_{loss}"
     cfgs = _config(0, count=20_000, n=8)
     _check(f"{tag}_pinhole", cfgs.arrays(), O.MODE_PINHOLE, 8, O.Cam.from_spec(cfgs.cameras[0]), O.Cfg(),
            fused=loss)

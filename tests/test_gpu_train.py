@@ -432,3 +432,38 @@ def test_host_step_overflow_vetoes_adam_and_redoes():
     np.testing.assert_allclose(got.numpy(), want.numpy(), rtol=1e-5)
     for k, w in ref.splats.tensors().items():
         np.testing.assert_allclose(tr.splats.tensors()[k].cpu().numpy(), w.cpu().numpy(), atol=2e-3, err_msg=k)
+
+
+def test_view_lanes_match_one_lane_at_configs3_size():
+    """configs[3] shape (1M surfels, 8x8 textures, 8 Fibonacci views at 1600x1064): the step's gradients with
+    four view lanes (concurrent K4/K5 on four streams into one buffer) equal the one-lane step's, up to
+    atomics order.  A lost update (a K5 read-modify-write racing another lane's) would move an entry by a
+    whole view's contribution."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+    from paper_2412_12734_b200.train import ViewShardedTrainer
+
+    cfg3 = sc.baseline_config(3)
+    arrays = cfg3.arrays()
+    cams = [gb.PinholeCamera.from_spec(c) for c in cfg3.cameras]
+    views = list(range(8))
+    tg = [torch.from_numpy(cfg3.target(v)).cuda() for v in views]
+
+    def grads(lanes):
+        s = gb.SplatSet.from_numpy(cfg3.mode, gb.ColorGridConfig(cfg3.n), **arrays)
+        tr = ViewShardedTrainer(s, cams, views, lanes=lanes, async_binning=False)
+        tr._views_checked(lambda: tr._run_views(tg))
+        torch.cuda.synchronize()
+        out = {k: v.cpu().numpy().astype(np.float64) for k, v in tr.grads.tensors().items() if v is not None}
+        del tr, s
+        torch.cuda.empty_cache()
+        return out
+
+    one = grads(1)
+    four = grads(4)
+    for k, w in one.items():
+        rms = float(np.sqrt(np.mean(w * w))) + 1e-30
+        bad = np.abs(four[k] - w) > 1e-3 * np.abs(w) + 1e-3 * rms
+        assert int(bad.sum()) == 0, (k, int(bad.sum()), float(np.abs(four[k] - w).max()), rms)

@@ -1,5 +1,5 @@
 """A small end-to-end case for compute-sanitizer (memcheck / racecheck / synccheck), one tool per run:
-binning, forward, L1, backward (every compositor variant), Adam, SSIM/PSNR, GBIL save/load, downsample.
+binning, forward, L1, backward, Adam, SSIM/PSNR, GBIL save/load, downsample.
 
     compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_case.py
 """
@@ -17,8 +17,7 @@ import paper_2412_12734_b200.fit as F
 import paper_2412_12734_b200.scenes as sc
 
 
-def run(mode, n, variant):
-    os.environ["GB_COMPOSITOR"] = variant
+def run(mode, n):
     if mode == gb.raster.MODE_PINHOLE:
         arrays = sc.generate(mode, 1500, n, 3, scale_lo=0.02, scale_hi=0.15)
         cam = gb.PinholeCamera.from_spec(sc.look_at((0.3, -0.2, -3.0), (0, 0, 0), 90, 70, 80.0, 80.0, 45.0, 35.0))
@@ -37,10 +36,9 @@ def run(mode, n, variant):
 
 
 def main():
-    for variant in ("direct", "staged", "grp"):
-        for mode in (gb.raster.MODE_PINHOLE, gb.raster.MODE_ORTHO):
-            for n in (1, 3, 8):
-                s, out, target = run(mode, n, variant)
+    for mode in (gb.raster.MODE_PINHOLE, gb.raster.MODE_ORTHO):
+        for n in (1, 3, 8):
+            s, out, target = run(mode, n)
     F.ssim_with_gradient(out.color, target)
     F.psnr(out.color, target)
     D.downsample_set(s, 2)
