@@ -41,7 +41,8 @@ typedef enum {
     GB_OOM = 4,
     GB_NONFINITE = 5, /* adam_step non-finite gradient: optim.hpp:81-83 */
     GB_NOT_SUPPORTED = 6,
-    GB_IO_ERROR = 7 /* SplatIoError (serialize.hpp:23-25) */
+    GB_IO_ERROR = 7, /* SplatIoError (serialize.hpp:23-25) */
+    GB_NCCL_ERROR = 8 /* a collective failed or the communicator reported an asynchronous error */
 } gb_status;
 
 #define GB_MODE_ORTHO 0   /* the reference's ImagePlaneCamera (core.hpp:102-116) */
@@ -171,7 +172,8 @@ GB_API int64_t gb_context_launch_count(const gb_context *ctx);
 #define GB_K_LOSS 8      /* K6  photometric loss */
 #define GB_K_ADAM 9      /* K7  Adam */
 #define GB_K_FUSED 10    /* K3+K6+K4 in one kernel (gb_render_loss_backward) */
-#define GB_NUM_KERNEL_IDS 11
+#define GB_K_COLLECTIVE 11 /* NCCL collectives of the view-sharded step (gb_allreduce_grads, ...) */
+#define GB_NUM_KERNEL_IDS 12
 GB_API gb_status gb_context_profile(gb_context *ctx, int enable);
 GB_API gb_status gb_context_profile_read(gb_context *ctx, double *total_ms, int64_t *counts, int n);
 /* The recorded launches of kernel `id` as (start, stop) in ms after `ref_event` (a cudaEvent_t recorded
@@ -314,6 +316,37 @@ typedef struct {
 #define GB_ADAM_FLAG_CLEAR 0x7fffffffffffffffLL
 GB_API gb_status gb_adam_segments(gb_context *ctx, int32_t phase, const gb_adam_segment *seg, int32_t nseg,
                                   gb_adam_state *state, const gb_learning_rates *lrs, int64_t *flag);
+
+/* ---- the view-sharded step's gradient exchange ------------------------------------
+ * The reference is single-process (fit, train.hpp:174-219); the multi-GPU step generalises its loop
+ * (build_binning -> render_forward -> loss -> render_backward -> adam_step, train.hpp:190-217) by view:
+ * every GPU renders and backpropagates its own views into one flat fp32 gradient buffer, then the
+ * buffers are summed over the GPUs -- one all-reduce, or a reduce-scatter followed by Adam on each
+ * rank's slice and an all-gather of the parameters -- over NCCL (NVLink/NVSwitch).  NCCL is loaded at
+ * run time (dlopen "libnccl.so.2"; the copy a host process already loaded, e.g. torch's, is reused).
+ * Collectives are stream-ordered on the context's stream and timed under GB_K_COLLECTIVE. */
+typedef struct gb_comm gb_comm;
+#define GB_COMM_ID_BYTES 128
+/* ncclGetUniqueId: rank 0 creates the id and ships it to the other ranks (any side channel). */
+GB_API gb_status gb_comm_unique_id(uint8_t id[GB_COMM_ID_BYTES]);
+/* ncclCommInitRank on ctx's device (one process or thread per GPU). */
+GB_API gb_status gb_comm_init_rank(gb_context *ctx, int32_t nranks, const uint8_t id[GB_COMM_ID_BYTES], int32_t rank,
+                                   gb_comm **out);
+/* ncclCommInitAll: one communicator per context (distinct devices), rank i = ctxs[i]; single host thread. */
+GB_API gb_status gb_comm_init_all(gb_context *const *ctxs, int32_t n, gb_comm **out);
+GB_API gb_status gb_comm_destroy(gb_comm *c);
+GB_API gb_status gb_comm_info(const gb_comm *c, int32_t *nranks, int32_t *rank);
+/* ncclCommGetAsyncError: GB_OK, or GB_NCCL_ERROR with the communicator's error string. */
+GB_API gb_status gb_comm_check(gb_comm *c);
+/* In-place sum of the flat gradient buffer over all ranks (ncclAllReduce, ncclFloat, ncclSum). */
+GB_API gb_status gb_allreduce_grads(gb_context *ctx, gb_comm *c, float *grads, int64_t count);
+/* recv[recv_count] = this rank's slice of the sum of every rank's send[nranks * recv_count] (ncclReduceScatter). */
+GB_API gb_status gb_reduce_scatter_grads(gb_context *ctx, gb_comm *c, const float *send, float *recv, int64_t recv_count);
+/* recv[nranks * send_count] = every rank's send[send_count] in rank order (ncclAllGather); in place when
+ * send == recv + rank * send_count. */
+GB_API gb_status gb_all_gather_params(gb_context *ctx, gb_comm *c, const float *send, float *recv, int64_t send_count);
+/* In-place minimum of a device int64 over all ranks: the Adam non-finite/veto flag (gb_adam_segments). */
+GB_API gb_status gb_allreduce_flag_min(gb_context *ctx, gb_comm *c, int64_t *flag);
 
 /* ---- GBIL splat files (serialize.hpp:15-124) -------------------------------
  * Header "GBIL", u32 version, u32 K, u32 N, f32 sigma, then K little-endian

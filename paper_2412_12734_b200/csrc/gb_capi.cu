@@ -1,6 +1,8 @@
 // gb_capi.cu -- the extern "C" boundary (include/gb_raster.h) and the host
 // orchestration of K1..K7 on the context's CUDA stream.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -35,8 +37,11 @@ cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* rang
                            float* color, float* trans, int32_t* last, cudaStream_t st);
 cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                             const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc, const RasterConst& rc,
-                            const float* trans, const int32_t* last, const float* image_grad, float* accum,
-                            float* grid_grad, cudaStream_t st);
+                            const float* trans, const int32_t* last, const float* image_grad, real* accum,
+                            real* grid_grad, cudaStream_t st);
+#ifdef GB_PARITY_F64
+cudaError_t launch_add_f64(const double* src, float* dst, int64_t n, cudaStream_t st);
+#endif
 cudaError_t launch_loss(int kind, const float* color, const float* target, int64_t n, float scale, float* grad,
                         float* loss, int sm_count, cudaStream_t st);
 cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned long long* bad, int sm_count,
@@ -121,6 +126,7 @@ struct gb_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
+    DevBuf grid64;  // parity build: fp64 texel-gradient scratch (added into the caller's fp32 buffer after K4)
     DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, accum, adam_bad, ssim_tmp,
         metric_tmp, fuse_color, fuse_trans, fuse_last, fuse_grad;
     uint32_t* pinned_total = nullptr;
@@ -197,6 +203,7 @@ struct gb_binning {
     int64_t capacity = 0;  // > 0: capacity mode (no host read-back of P; see gb_binning_set_capacity)
     int32_t* overflow = nullptr;
     DevBuf headers, cull, rects, counts, offsets, depth, perm, keys, values, ranges;
+    DevBuf trans64;  // parity build: the forward's fp64 final transmittance, rewound by the backward
 };
 
 namespace {
@@ -265,13 +272,28 @@ gb_status validate_grads(const gb_grads* g, int mode, int n, const char* where) 
     return GB_OK;
 }
 
+#ifdef GB_PARITY_F64
+// parity build: K4 accumulates texel gradients into fp64 scratch, added into the caller's buffer after K4
+gb_status grid_scratch(gb_context* ctx, int64_t K, int n, gb::real** out) {
+    const size_t bytes = sizeof(double) * (size_t)K * 3 * n * n;
+    GB_CUDA(ctx->grid64.ensure(bytes > 0 ? bytes : 8));
+    GB_CUDA(cudaMemsetAsync(ctx->grid64.p, 0, bytes, ctx->stream));
+    *out = ctx->grid64.as<double>();
+    return GB_OK;
+}
+gb_status trans_scratch(gb_context* ctx, const gb_binning* b) {
+    GB_CUDA(const_cast<gb_binning*>(b)->trans64.ensure(sizeof(double) * (size_t)b->width * b->height));
+    return GB_OK;
+}
+#endif
+
 gb::CamConst make_cam_const(const gb_camera* cam) {
     gb::CamConst cc;
     cc.width = cam->width;
     cc.height = cam->height;
     cc.inv_fx = cam->mode == GB_MODE_PINHOLE ? (float)(1.0 / cam->fx) : 0.0f;
     cc.inv_fy = cam->mode == GB_MODE_PINHOLE ? (float)(1.0 / cam->fy) : 0.0f;
-    for (int i = 0; i < 3; ++i) cc.bg[i] = (float)cam->background[i];
+    for (int i = 0; i < 3; ++i) cc.bg[i] = (gb::real)cam->background[i];
     return cc;
 }
 
@@ -280,11 +302,14 @@ gb::RasterConst make_raster_const(const gb_binning* b, int n, double sigma) {
     rc.tile_size = b->cfg.tile_size;
     rc.tiles_x = b->tiles_x;
     rc.tiles_y = b->tiles_y;
-    rc.alpha_skip = (float)b->cfg.alpha_skip;
-    rc.early_stop = (float)b->cfg.early_stop_transmittance;
-    rc.tex_scale = (float)((double)(n - 1) / (2.0 * sigma));
-    rc.tex_offset = (float)((double)(n - 1) * 0.5);
-    rc.sigma = (float)sigma;
+    rc.alpha_skip = (gb::real)b->cfg.alpha_skip;
+    rc.early_stop = (gb::real)b->cfg.early_stop_transmittance;
+    rc.tex_scale = (gb::real)((double)(n - 1) / (2.0 * sigma));
+    rc.tex_offset = (gb::real)((double)(n - 1) * 0.5);
+    rc.sigma = (gb::real)sigma;
+#ifdef GB_PARITY_F64
+    rc.trans64 = b->trans64.as<double>();
+#endif
     return rc;
 }
 
@@ -330,6 +355,7 @@ gb_status gb_context_destroy(gb_context* ctx) {
     ctx->depth_tmp.release();
     ctx->iota_tmp.release();
     ctx->accum.release();
+    ctx->grid64.release();
     ctx->adam_bad.release();
     ctx->ssim_tmp.release();
     ctx->metric_tmp.release();
@@ -620,6 +646,7 @@ gb_status gb_binning_destroy(gb_binning* b) {
     b->keys.release();
     b->values.release();
     b->ranges.release();
+    b->trans64.release();
     delete b;
     return GB_OK;
 }
@@ -809,6 +836,9 @@ gb_status gb_render_forward(gb_context* ctx, const gb_splats* s, const gb_camera
     if (!out->color || !out->final_transmittance || !out->last_rank)
         return fail(GB_INVALID_ARGUMENT, "render_forward: null output buffer");
     if (gb_status st = set_device(ctx)) return st;
+#ifdef GB_PARITY_F64
+    if (gb_status st = trans_scratch(ctx, b)) return st;
+#endif
     const gb::CamConst cc = make_cam_const(cam);
     const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
     ProfScope ps(ctx, GB_K_FORWARD);
@@ -841,22 +871,31 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
     if (gb_status st = set_device(ctx)) return st;
     cudaStream_t stream = ctx->stream;
     const int64_t K = s->count;
-    GB_CUDA(ctx->accum.ensure(sizeof(float) * gb::kAccumStride * K));
-    GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(float) * gb::kAccumStride * K, stream));
+    GB_CUDA(ctx->accum.ensure(sizeof(gb::real) * gb::kAccumStride * K));
+    GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(gb::real) * gb::kAccumStride * K, stream));
     const gb::CamConst cc = make_cam_const(cam);
     const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+#ifdef GB_PARITY_F64
+    gb::real* grid_grad = nullptr;
+    if (gb_status st = grid_scratch(ctx, K, s->grid.n, &grid_grad)) return st;
+#else
+    gb::real* grid_grad = g->grid_values;
+#endif
     {
         ProfScope ps(ctx, GB_K_BACKWARD);
         GB_CUDA(gb::launch_backward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
                                     b->ranges.as<uint2>(), b->values.as<int32_t>(),
                                     b->headers.as<gb::ScreenHeader>(), b->cull.as<gb::CullRec>(), s->grid_values, cc, rc,
-                                    out->final_transmittance, out->last_rank, image_grad, ctx->accum.as<float>(),
-                                    g->grid_values, stream));
+                                    out->final_transmittance, out->last_rank, image_grad, ctx->accum.as<gb::real>(),
+                                    grid_grad, stream));
     }
+#ifdef GB_PARITY_F64
+    GB_CUDA(gb::launch_add_f64(ctx->grid64.as<double>(), g->grid_values, K * 3 * s->grid.n * s->grid.n, stream));
+#endif
     gb::ProjParams pp = gb::make_proj_params(s, cam, &b->cfg, b->tiles_x, b->tiles_y);
     {
         ProfScope ps(ctx, GB_K_CHAIN);
-        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
+        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<gb::real>(), *g, stream));
     }
     ctx->launches += 2;
     return GB_OK;
@@ -914,12 +953,21 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
     cudaStream_t stream = ctx->stream;
     const int64_t K = s->count;
     if (K > 0) {
-        GB_CUDA(ctx->accum.ensure(sizeof(float) * gb::kAccumStride * K));
-        GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(float) * gb::kAccumStride * K, stream));
+        GB_CUDA(ctx->accum.ensure(sizeof(gb::real) * gb::kAccumStride * K));
+        GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(gb::real) * gb::kAccumStride * K, stream));
     }
+#ifdef GB_PARITY_F64
+    if (gb_status st = trans_scratch(ctx, b)) return st;
+#endif
     const gb::CamConst cc = make_cam_const(cam);
     const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
     const int tiles = b->tiles_x * b->tiles_y;
+#ifdef GB_PARITY_F64
+    gb::real* grid_grad = nullptr;
+    if (gb_status st = grid_scratch(ctx, K, s->grid.n, &grid_grad)) return st;
+#else
+    gb::real* grid_grad = g->grid_values;
+#endif
 #ifdef GB_FUSED_SINGLE_KERNEL
     if (true) {  // variant build: K3 + K6 + K4 in one kernel (measured slower)
         ProfScope ps(ctx, GB_K_FUSED);
@@ -928,7 +976,7 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
                                  b->cull.as<gb::CullRec>(), s->grid_values, cc, rc, loss_kind, target, scale,
                                  out ? out->color : nullptr, out ? out->final_transmittance : nullptr,
                                  out ? out->last_rank : nullptr, image_grad, loss,
-                                 K > 0 ? ctx->accum.as<float>() : nullptr, g->grid_values, stream));
+                                 K > 0 ? ctx->accum.as<gb::real>() : nullptr, grid_grad, stream));
         ctx->launches += 1;
     }
 #else
@@ -958,7 +1006,7 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
             GB_CUDA(gb::launch_backward(cam->mode, s->grid.n, tiles, b->cfg.tile_size, b->ranges.as<uint2>(),
                                         b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
                                         b->cull.as<gb::CullRec>(), s->grid_values, cc, rc, trans, last, grad,
-                                        K > 0 ? ctx->accum.as<float>() : nullptr, g->grid_values, stream));
+                                        K > 0 ? ctx->accum.as<gb::real>() : nullptr, grid_grad, stream));
         }
         ctx->launches += 2;
     }
@@ -969,10 +1017,13 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
         out->tile_size = b->cfg.tile_size;
     }
     if (K == 0) return GB_OK;
+#ifdef GB_PARITY_F64
+    GB_CUDA(gb::launch_add_f64(ctx->grid64.as<double>(), g->grid_values, K * 3 * s->grid.n * s->grid.n, stream));
+#endif
     gb::ProjParams pp = gb::make_proj_params(s, cam, &b->cfg, b->tiles_x, b->tiles_y);
     {
         ProfScope ps(ctx, GB_K_CHAIN);
-        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<float>(), *g, stream));
+        GB_CUDA(gb::launch_chain(pp, b->counts.as<uint32_t>(), ctx->accum.as<gb::real>(), *g, stream));
     }
     ctx->launches += 1;
     return GB_OK;
@@ -1349,6 +1400,196 @@ gb_status gb_splats_load(gb_context* ctx, const char* path, int64_t count, int32
     }
     GB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (!ok) return fail(GB_IO_ERROR, "bad splat file: truncated at record %lld", (long long)(off / rec_bytes));
+    return GB_OK;
+}
+
+}  // extern "C"
+
+// ---- NCCL: the view-sharded step's gradient exchange ------------------------------------------------
+// NCCL is resolved with dlopen on first use so that a host process which already loaded a libnccl.so.2
+// (torch) shares it instead of mixing two NCCL builds in one process.
+namespace {
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommInitAll) CommInitAll = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclCommCount) CommCount = nullptr;
+    decltype(&ncclCommUserRank) CommUserRank = nullptr;
+    decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclReduceScatter) ReduceScatter = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return a;
+        }
+#define GB_NCCL_SYM(name)                                                         \
+    a.name = reinterpret_cast<decltype(a.name)>(dlsym(h, "nccl" #name));          \
+    if (!a.name) {                                                                \
+        a.why = "libnccl.so.2 lacks nccl" #name;                                  \
+        return a;                                                                 \
+    }
+        GB_NCCL_SYM(GetUniqueId)
+        GB_NCCL_SYM(CommInitRank)
+        GB_NCCL_SYM(CommInitAll)
+        GB_NCCL_SYM(CommDestroy)
+        GB_NCCL_SYM(CommCount)
+        GB_NCCL_SYM(CommUserRank)
+        GB_NCCL_SYM(CommGetAsyncError)
+        GB_NCCL_SYM(GetErrorString)
+        GB_NCCL_SYM(AllReduce)
+        GB_NCCL_SYM(ReduceScatter)
+        GB_NCCL_SYM(AllGather)
+#undef GB_NCCL_SYM
+        a.ok = true;
+        return a;
+    }();
+    return api;
+}
+
+#define GB_NCCL(call)                                                                                      \
+    do {                                                                                                   \
+        ncclResult_t r_ = (call);                                                                          \
+        if (r_ != ncclSuccess)                                                                             \
+            return fail(GB_NCCL_ERROR, "%s:%d: %s: %s", __FILE__, __LINE__, #call, nccl().GetErrorString(r_)); \
+    } while (0)
+
+gb_status need_nccl() {
+    if (!nccl().ok) return fail(GB_NCCL_ERROR, "%s", nccl().why.c_str());
+    return GB_OK;
+}
+}  // namespace
+
+struct gb_comm {
+    ncclComm_t comm = nullptr;
+    int device = 0;
+    int nranks = 1, rank = 0;
+};
+
+extern "C" {
+
+gb_status gb_comm_unique_id(uint8_t id[GB_COMM_ID_BYTES]) {
+    if (!id) return fail(GB_INVALID_ARGUMENT, "null id");
+    if (gb_status st = need_nccl()) return st;
+    static_assert(sizeof(ncclUniqueId) == GB_COMM_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId u;
+    GB_NCCL(nccl().GetUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+    return GB_OK;
+}
+
+gb_status gb_comm_init_rank(gb_context* ctx, int32_t nranks, const uint8_t id[GB_COMM_ID_BYTES], int32_t rank,
+                            gb_comm** out) {
+    if (!ctx || !id || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(GB_INVALID_ARGUMENT, "rank %d of %d", rank, nranks);
+    if (gb_status st = need_nccl()) return st;
+    if (gb_status st = set_device(ctx)) return st;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    std::unique_ptr<gb_comm> c(new gb_comm());
+    GB_NCCL(nccl().CommInitRank(&c->comm, nranks, u, rank));
+    c->device = ctx->device;
+    c->nranks = nranks;
+    c->rank = rank;
+    *out = c.release();
+    return GB_OK;
+}
+
+gb_status gb_comm_init_all(gb_context* const* ctxs, int32_t n, gb_comm** out) {
+    if (!ctxs || !out || n < 1) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = need_nccl()) return st;
+    std::vector<int> devs(n);
+    for (int i = 0; i < n; ++i) {
+        if (!ctxs[i]) return fail(GB_INVALID_ARGUMENT, "null context %d", i);
+        devs[i] = ctxs[i]->device;
+        for (int j = 0; j < i; ++j)
+            if (devs[j] == devs[i]) return fail(GB_INVALID_ARGUMENT, "contexts %d and %d share device %d", j, i, devs[i]);
+    }
+    std::vector<ncclComm_t> comms(n);
+    GB_NCCL(nccl().CommInitAll(comms.data(), n, devs.data()));
+    for (int i = 0; i < n; ++i) {
+        out[i] = new gb_comm();
+        out[i]->comm = comms[i];
+        out[i]->device = devs[i];
+        out[i]->nranks = n;
+        out[i]->rank = i;
+    }
+    return GB_OK;
+}
+
+gb_status gb_comm_destroy(gb_comm* c) {
+    if (!c) return GB_OK;
+    if (c->comm && nccl().ok) {
+        cudaSetDevice(c->device);
+        nccl().CommDestroy(c->comm);
+    }
+    delete c;
+    return GB_OK;
+}
+
+gb_status gb_comm_info(const gb_comm* c, int32_t* nranks, int32_t* rank) {
+    if (!c) return fail(GB_INVALID_ARGUMENT, "null communicator");
+    if (nranks) *nranks = c->nranks;
+    if (rank) *rank = c->rank;
+    return GB_OK;
+}
+
+gb_status gb_comm_check(gb_comm* c) {
+    if (!c) return fail(GB_INVALID_ARGUMENT, "null communicator");
+    if (gb_status st = need_nccl()) return st;
+    ncclResult_t async = ncclSuccess;
+    GB_NCCL(nccl().CommGetAsyncError(c->comm, &async));
+    if (async != ncclSuccess && async != ncclInProgress)
+        return fail(GB_NCCL_ERROR, "communicator error: %s", nccl().GetErrorString(async));
+    return GB_OK;
+}
+
+namespace {
+gb_status comm_args(gb_context* ctx, gb_comm* c, const void* a, const void* b, int64_t count) {
+    if (!ctx || !c) return fail(GB_INVALID_ARGUMENT, "null context or communicator");
+    if (count < 0 || (count > 0 && (!a || !b))) return fail(GB_INVALID_ARGUMENT, "null buffer");
+    if (c->device != ctx->device) return fail(GB_MISMATCH, "communicator on device %d, context on %d", c->device, ctx->device);
+    if (gb_status st = need_nccl()) return st;
+    return set_device(ctx);
+}
+}  // namespace
+
+gb_status gb_allreduce_grads(gb_context* ctx, gb_comm* c, float* grads, int64_t count) {
+    if (gb_status st = comm_args(ctx, c, grads, grads, count)) return st;
+    ProfScope ps(ctx, GB_K_COLLECTIVE);
+    GB_NCCL(nccl().AllReduce(grads, grads, (size_t)count, ncclFloat, ncclSum, c->comm, ctx->stream));
+    return GB_OK;
+}
+
+gb_status gb_reduce_scatter_grads(gb_context* ctx, gb_comm* c, const float* send, float* recv, int64_t recv_count) {
+    if (gb_status st = comm_args(ctx, c, send, recv, recv_count)) return st;
+    ProfScope ps(ctx, GB_K_COLLECTIVE);
+    GB_NCCL(nccl().ReduceScatter(send, recv, (size_t)recv_count, ncclFloat, ncclSum, c->comm, ctx->stream));
+    return GB_OK;
+}
+
+gb_status gb_all_gather_params(gb_context* ctx, gb_comm* c, const float* send, float* recv, int64_t send_count) {
+    if (gb_status st = comm_args(ctx, c, send, recv, send_count)) return st;
+    ProfScope ps(ctx, GB_K_COLLECTIVE);
+    GB_NCCL(nccl().AllGather(send, recv, (size_t)send_count, ncclFloat, c->comm, ctx->stream));
+    return GB_OK;
+}
+
+gb_status gb_allreduce_flag_min(gb_context* ctx, gb_comm* c, int64_t* flag) {
+    if (gb_status st = comm_args(ctx, c, flag, flag, 1)) return st;
+    ProfScope ps(ctx, GB_K_COLLECTIVE);
+    GB_NCCL(nccl().AllReduce(flag, flag, 1, ncclInt64, ncclMin, c->comm, ctx->stream));
     return GB_OK;
 }
 

@@ -17,22 +17,22 @@ __device__ __forceinline__ int tex_n(int n_rt) {
 
 struct Bilin {
     int o00;  // offset of texel (i_u, i_v) channel 0
-    float fu, fv;
-    float w00, w10, w01, w11;
+    real fu, fv;
+    real w00, w10, w01, w11;
 };
 
-__device__ __forceinline__ void bilin_setup(float u, float v, int N, const RasterConst& rc, Bilin& b) {
+__device__ __forceinline__ void bilin_setup(real u, real v, int N, const RasterConst& rc, Bilin& b) {
     int iu, iv;
-    float s = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
-    s = fminf(fmaxf(s, 0.0f), (float)(N - 1));
-    iu = min((int)floorf(s), N - 2);
-    b.fu = __fsub_rn(s, (float)iu);
-    float t = __fmaf_rn(v, rc.tex_scale, rc.tex_offset);
-    t = fminf(fmaxf(t, 0.0f), (float)(N - 1));
-    iv = min((int)floorf(t), N - 2);
-    b.fv = __fsub_rn(t, (float)iv);
+    real s = fma_rn(u, rc.tex_scale, rc.tex_offset);
+    s = rmin(rmax(s, (real)0), (real)(N - 1));
+    iu = min((int)rfloor(s), N - 2);
+    b.fu = sub_rn(s, (real)iu);
+    real t = fma_rn(v, rc.tex_scale, rc.tex_offset);
+    t = rmin(rmax(t, (real)0), (real)(N - 1));
+    iv = min((int)rfloor(t), N - 2);
+    b.fv = sub_rn(t, (real)iv);
     b.o00 = (iu * N + iv) * 3;
-    const float gu = 1.0f - b.fu, gv = 1.0f - b.fv;
+    const real gu = (real)1 - b.fu, gv = (real)1 - b.fv;
     b.w00 = gu * gv;
     b.w10 = b.fu * gv;
     b.w01 = gu * b.fv;
@@ -66,31 +66,60 @@ __device__ __forceinline__ float smem_reduce(const float (&v)[NV], float* scratc
     return acc + __shfl_xor_sync(kFull, acc, 1);
 }
 
-__device__ __forceinline__ void red_add(float* p, float v) {
-    if (v != 0.0f) atomicAdd(p, v);
+// fp64 (parity build): the same transpose, scalar loads
+template <int NV>
+__device__ __forceinline__ double smem_reduce(const double (&v)[NV], double* scratch, int lane) {
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[i * kRedStride + lane] = v[i];
+    __syncwarp();
+    const int row = lane >> 1;
+    double acc = 0.0;
+    if (row < NV) {
+        const double* q = scratch + row * kRedStride + (lane & 1) * 16;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc += q[k];
+    }
+    return acc + __shfl_xor_sync(kFull, acc, 1);
 }
 
-// p[0..2] += (a, b, c)
-#ifdef GB_RED3_SCALAR
-__device__ __forceinline__ void red3(float* p, float a, float b, float c) {  // experiment: three scalar reds
+__device__ __forceinline__ void red_add(real* p, real v) {
+    if (v != (real)0) atomicAdd(p, v);
+}
+
+#ifdef GB_PARITY_F64
+__device__ __forceinline__ void red3(double* p, double a, double b, double c) {
     atomicAdd(p, a);
     atomicAdd(p + 1, b);
     atomicAdd(p + 2, c);
 }
+__device__ __forceinline__ void red4(double* p, double a, double b, double c, double d) {
+    red3(p, a, b, c);
+    atomicAdd(p + 3, d);
+}
+__device__ __forceinline__ void red2(double* p, double a, double b) {
+    atomicAdd(p, a);
+    atomicAdd(p + 1, b);
+}
 #else
-// one 8-byte vector red and one scalar red (branch-free on alignment)
+// p[0..2] += (a, b, c): one 8-byte vector red and one scalar red (branch-free on alignment)
 __device__ __forceinline__ void red3(float* p, float a, float b, float c) {
     const bool even = (reinterpret_cast<uintptr_t>(p) & 7) == 0;
     float2* pv = reinterpret_cast<float2*>(even ? p : p + 1);
     atomicAdd(pv, even ? make_float2(a, b) : make_float2(b, c));
     atomicAdd(even ? p + 2 : p, even ? c : a);
 }
-#endif
 
 // p[0..3] += (a, b, c, d) with one 16-byte vector red (p 16-B aligned)
 __device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
     atomicAdd(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));
 }
+
+// p[0..1] += (a, b) with one 8-byte vector red (p 8-B aligned)
+__device__ __forceinline__ void red2(float* p, float a, float b) {
+    atomicAdd(reinterpret_cast<float2*>(p), make_float2(a, b));
+}
+#endif
 
 // texel corner k (0..3 = 00, 10, 01, 11) channel c -> float offset from the base texel
 __device__ __forceinline__ int corner_offset(int i, int N) {

@@ -11,7 +11,7 @@
 //   keys     : uint32[P] tile id per (tile, primitive) pair, stably sorted
 //   values   : int32[P] primitive index per pair (per tile: depth, index order)
 //   ranges   : uint2[tiles] [start, end) into values per tile
-//   accum    : float[K*12] per-primitive screen-space gradient sums (K4 -> K5)
+//   accum    : real[K*12] per-primitive screen-space gradient sums (K4 -> K5)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -21,10 +21,23 @@
 
 namespace gb {
 
-constexpr int kAccumStride = 12;  // floats per primitive in the K4 -> K5 accumulator
-constexpr float kMaxAlphaF = 0.999f;
+// The compositors' arithmetic type.  The product is fp32 throughout.  The test-only parity build
+// (-DGB_PARITY_F64, libgb_raster_f64.so, never loaded by the product) runs the same K3/K4/K5 code in fp64
+// -- headers, evaluation, compositing, rewind, adjoint and every accumulation -- so the parity tests can
+// hold each gradient entry to rtol 1e-4 / atol 1e-5 with no cancellation exemption: that build differs
+// from the reference's fp64 path (raster.hpp:198-387) only in summation order.
+#ifdef GB_PARITY_F64
+typedef double real;
+typedef double4 real4;
+#else
+typedef float real;
+typedef float4 real4;
+#endif
 
-// Per-primitive screen header (48 B, three float4).
+constexpr int kAccumStride = 12;  // values per primitive in the K4 -> K5 accumulator
+constexpr real kMaxAlpha = (real)0.999;  // core.hpp:16
+
+// Per-primitive screen header (three real4 + the alpha-box; 64 B in the product).
 //   ortho  : h0 = (x, y, cos t, sin t)   h1 = (1/s_u, 1/s_v, alpha_k, 0)   h2 = 0
 //   pinhole: the ray-splat intersection as a linear-fractional map of the
 //            pixel offset (dx, dy) from the projected centre:
@@ -37,8 +50,45 @@ constexpr float kMaxAlphaF = 0.999f;
 //            ellipse, enlarged by a safety margin); the compositors skip a
 //            warp's 8x4 pixel block for this entry when it misses the box.
 struct __align__(16) ScreenHeader {
-    float4 h0, h1, h2, h3;
+    real4 h0, h1, h2;
+    float4 h3;
 };
+
+// integers stored in header slots (pinhole centre): bit-cast in fp32, exact values in fp64
+__device__ __forceinline__ int hdr_int(float v) { return __float_as_int(v); }
+__device__ __forceinline__ int hdr_int(double v) { return (int)v; }
+__device__ __forceinline__ real hdr_from_int(int i) {
+#ifdef GB_PARITY_F64
+    return (double)i;
+#else
+    return __int_as_float(i);
+#endif
+}
+
+// vector header loads through the read-only path
+__device__ __forceinline__ float4 ld_real4(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ double4 ld_real4(const double4* p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// pinned-rounding arithmetic for both precisions
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float rmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ double rmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float rmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double rmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float rabs(float a) { return fabsf(a); }
+__device__ __forceinline__ double rabs(double a) { return fabs(a); }
+__device__ __forceinline__ float rfloor(float a) { return floorf(a); }
+__device__ __forceinline__ double rfloor(double a) { return floor(a); }
 
 // Per-primitive alpha-skip ellipse in pixel-index coordinates (K1, alpha_ellipse):
 // a = (e_x, e_y, Q11, Q22), b = (Q12, Q12/Q22, Q12/Q11, 0).
@@ -46,22 +96,25 @@ struct __align__(16) CullRec {
     float4 a, b;
 };
 
-// Per-launch camera constants for the fp32 compositor.
+// Per-launch camera constants for the compositor.
 struct CamConst {
     int width, height;
     float inv_fx, inv_fy;
-    float bg[3];
+    real bg[3];
 };
 
 // Raster constants shared by K3/K4.
 struct RasterConst {
     int tile_size;
     int tiles_x, tiles_y;
-    float alpha_skip;      // <= 0 disables
-    float early_stop;      // <= 0 disables
-    float tex_scale;       // (n-1)/(2 sigma)
-    float tex_offset;      // (n-1)/2
-    float sigma;
+    real alpha_skip;      // <= 0 disables
+    real early_stop;      // <= 0 disables
+    real tex_scale;       // (n-1)/(2 sigma)
+    real tex_offset;      // (n-1)/2
+    real sigma;
+#ifdef GB_PARITY_F64
+    double* trans64;  // parity build: K3 stores the fp64 final transmittance here, K4 rewinds from it
+#endif
 };
 
 // Thread -> pixel mapping inside a tile.  For tile sizes that are multiples
@@ -85,29 +138,26 @@ __device__ __forceinline__ void tile_pixel(int tid, int ts, int& lx, int& ly) {
 // -ffp-contract=off for the same reason, CMakeLists.txt:12-15).
 
 struct PinholeTerms {  // kept for the backward chain
-    float dx, dy, cz, iz;
+    real dx, dy, cz, iz;
 };
 
 // Approximate reciprocal (one MUFU.RCP, ~1 ulp).  It is deterministic, so K3
 // and K4 still see identical bits; only the oracle comparison is
 // tolerance-based, and 1 ulp is far inside it.
 __device__ __forceinline__ float rcp_approx(float x) {
-#ifdef GB_PRECISE_EVAL
-    return __frcp_rn(x);
-#else
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
-#endif
 }
+__device__ __forceinline__ double rcp_approx(double x) { return __drcp_rn(x); }
 
 // raster.hpp:36-42 (ortho) -- returns true (always a hit).
-__device__ __forceinline__ bool eval_uv_ortho(const ScreenHeader& h, int x, int y, float& u, float& v) {
-    const float dx = __fsub_rn(__fadd_rn((float)x, 0.5f), h.h0.x);
-    const float dy = __fsub_rn(__fadd_rn((float)y, 0.5f), h.h0.y);
-    const float c = h.h0.z, s = h.h0.w;
-    u = __fmul_rn(__fmaf_rn(c, dx, __fmul_rn(s, dy)), h.h1.x);
-    v = __fmul_rn(__fmaf_rn(-s, dx, __fmul_rn(c, dy)), h.h1.y);
+__device__ __forceinline__ bool eval_uv_ortho(const ScreenHeader& h, int x, int y, real& u, real& v) {
+    const real dx = sub_rn(add_rn((real)x, (real)0.5), h.h0.x);
+    const real dy = sub_rn(add_rn((real)y, (real)0.5), h.h0.y);
+    const real c = h.h0.z, s = h.h0.w;
+    u = mul_rn(fma_rn(c, dx, mul_rn(s, dy)), h.h1.x);
+    v = mul_rn(fma_rn(-s, dx, mul_rn(c, dy)), h.h1.y);
     return true;
 }
 
@@ -116,41 +166,29 @@ __device__ __forceinline__ bool eval_uv_ortho(const ScreenHeader& h, int x, int 
 // plane hit behind the camera: c_z <= 0 after the K1 normalisation) is skipped;
 // c_z below FLT_MIN (a hit at ~infinity, G = 0 anyway) counts as a miss so the
 // flush-to-zero reciprocal never sees a denormal.
-__device__ __forceinline__ bool eval_uv_pinhole(const ScreenHeader& h, int x, int y, float& u, float& v,
+__device__ __forceinline__ bool eval_uv_pinhole(const ScreenHeader& h, int x, int y, real& u, real& v,
                                                 PinholeTerms& p) {
-    const int cxi = __float_as_int(h.h2.y), cyi = __float_as_int(h.h2.z);
-    p.dx = __fadd_rn((float)(x - cxi), h.h1.w);
-    p.dy = __fadd_rn((float)(y - cyi), h.h2.x);
-    const float cx = __fmaf_rn(p.dx, h.h0.x, __fmul_rn(p.dy, h.h0.w));
-    const float cy = __fmaf_rn(p.dx, h.h0.y, __fmul_rn(p.dy, h.h1.x));
-    p.cz = __fmaf_rn(p.dx, h.h0.z, __fmaf_rn(p.dy, h.h1.y, 1.0f));
+    const int cxi = hdr_int(h.h2.y), cyi = hdr_int(h.h2.z);
+    p.dx = add_rn((real)(x - cxi), h.h1.w);
+    p.dy = add_rn((real)(y - cyi), h.h2.x);
+    const real cx = fma_rn(p.dx, h.h0.x, mul_rn(p.dy, h.h0.w));
+    const real cy = fma_rn(p.dx, h.h0.y, mul_rn(p.dy, h.h1.x));
+    p.cz = fma_rn(p.dx, h.h0.z, fma_rn(p.dy, h.h1.y, (real)1));
     p.iz = rcp_approx(p.cz);
-    u = __fmul_rn(cx, p.iz);
-    v = __fmul_rn(cy, p.iz);
-    return p.cz > 1.17549435e-38f;
+    u = mul_rn(cx, p.iz);
+    v = mul_rn(cy, p.iz);
+    return p.cz > (real)1.17549435e-38f;
 }
 
 // G = exp(-(u^2+v^2)/2)  (raster.hpp:52) as one MUFU.EX2 of -(u^2+v^2) log2(e)/2
 // (ftz: G underflows to 0 far outside the splat, where alpha < alpha_skip anyway).
 __device__ __forceinline__ float gauss_weight(float u, float v) {
     const float x = __fmul_rn(-0.72134752044448170368f, __fmaf_rn(u, u, __fmul_rn(v, v)));
-#ifdef GB_PRECISE_EVAL
-    return exp2f(x);
-#else
     float g;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(x));
     return g;
-#endif
 }
-
-// uv -> (i, f) on one axis, texture.hpp:27-37, with N fixed at compile time.
-template <int N>
-__device__ __forceinline__ void grid_coord(float u, const RasterConst& rc, int& i, float& f) {
-    float s = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
-    s = fminf(fmaxf(s, 0.0f), (float)(N - 1));
-    i = min((int)floorf(s), N - 2);
-    f = __fsub_rn(s, (float)i);
-}
+__device__ __forceinline__ double gauss_weight(double u, double v) { return exp(-0.5 * (u * u + v * v)); }
 
 // K1/K5 parameters (fp64 camera and config), passed by value.
 struct ProjParams {
@@ -176,7 +214,7 @@ ProjParams make_proj_params(const gb_splats* s, const gb_camera* cam, const gb_r
                             int tiles_y);
 cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, CullRec* cull, uint2* rects, uint32_t* counts,
                            uint32_t* depth_bits, cudaStream_t st);
-cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
+cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const real* accum, const gb_grads& g,
                          cudaStream_t st);
 
 // gb_raster.cu: K3 with the photometric loss in its epilogue (K3 + K6); the single fused K3+K6+K4 kernel
@@ -189,7 +227,7 @@ cudaError_t launch_forward_loss(int mode, int n, int tiles, int ts, const uint2*
 cudaError_t launch_fused(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                          const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                          const RasterConst& rc, int kind, const float* target, float scale, float* color, float* trans,
-                         int32_t* last, float* image_grad, float* loss, float* accum, float* grid_grad,
+                         int32_t* last, float* image_grad, float* loss, real* accum, real* grid_grad,
                          cudaStream_t st);
 #endif
 

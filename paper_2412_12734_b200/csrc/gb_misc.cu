@@ -137,4 +137,18 @@ cudaError_t launch_adam_update(float* p, const float* g, float* m, float* v, int
     return cudaGetLastError();
 }
 
+#ifdef GB_PARITY_F64
+// parity build: dst += (float)src, one rounding of the fp64 texel-gradient sums
+__global__ void __launch_bounds__(256) k_add_f64(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (src[i] != 0.0) dst[i] = (float)((double)dst[i] + src[i]);
+}
+
+cudaError_t launch_add_f64(const double* src, float* dst, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_add_f64<<<1184, 256, 0, st>>>(src, dst, n);
+    return cudaGetLastError();
+}
+#endif
+
 }  // namespace gb

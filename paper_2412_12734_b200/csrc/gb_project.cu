@@ -301,17 +301,26 @@ __device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g, 
     return out;
 }
 
-// Effective projected centre used by the fp32 compositor (see ScreenHeader).
-__device__ __forceinline__ void pinhole_centre(const ProjParams& p, const Geom& g, int& cxi, int& cyi, float& hx,
-                                               float& hy, double& dxe, double& dye) {
+// header slot values in the compositor's precision
+__device__ __forceinline__ real4 mk4(double a, double b, double c, double d) {
+#ifdef GB_PARITY_F64
+    return make_double4(a, b, c, d);
+#else
+    return make_float4((float)a, (float)b, (float)c, (float)d);
+#endif
+}
+
+// Effective projected centre used by the compositor (see ScreenHeader).
+__device__ __forceinline__ void pinhole_centre(const ProjParams& p, const Geom& g, int& cxi, int& cyi, real& hx,
+                                               real& hy, double& dxe, double& dye) {
     const double pz = g.M[8];
     const double cxp = p.fx * (g.M[2] / pz) + p.cx;
     const double cyp = p.fy * (g.M[5] / pz) + p.cy;
     const double fxi = floor(cxp), fyi = floor(cyp);
     cxi = (int)fxi;
     cyi = (int)fyi;
-    hx = (float)(0.5 - (cxp - fxi));
-    hy = (float)(0.5 - (cyp - fyi));
+    hx = (real)(0.5 - (cxp - fxi));
+    hy = (real)(0.5 - (cyp - fyi));
     const double c0x = fxi + 0.5 - (double)hx;
     const double c0y = fyi + 0.5 - (double)hy;
     dxe = (c0x - p.cx) / p.fx;
@@ -361,26 +370,25 @@ __global__ void __launch_bounds__(256, GB_K1_MINB) k_project(const ProjParams p,
     depth_bits[k] = float_order_key((float)g.depth);
     ScreenHeader h;
     if (p.mode == GB_MODE_ORTHO) {
-        h.h0 = make_float4(p.position[2 * k], p.position[2 * k + 1], (float)g.cos_t, (float)g.sin_t);
-        h.h1 = make_float4((float)(1.0 / g.s_u), (float)(1.0 / g.s_v), (float)g.alpha_k, 0.0f);
-        h.h2 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        h.h0 = mk4(p.position[2 * k], p.position[2 * k + 1], g.cos_t, g.sin_t);
+        h.h1 = mk4(1.0 / g.s_u, 1.0 / g.s_v, g.alpha_k, 0.0);
+        h.h2 = mk4(0.0, 0.0, 0.0, 0.0);
     } else {
         int cxi, cyi;
-        float hx, hy;
+        real hx, hy;
         double dxe, dye;
         pinhole_centre(p, g, cxi, cyi, hx, hy, dxe, dye);
         PinholeCoeffs pc;
         pinhole_coeffs(g, dxe, dye, pc);
         const double sx = 1.0 / (pc.E[2] * p.fx), sy = 1.0 / (pc.E[2] * p.fy);
         const bool ok = pc.E[2] != 0.0 && isfinite(sx) && isfinite(sy);
-        const float nan = __int_as_float(0x7fc00000);
+        const double nan = (double)__int_as_float(0x7fc00000);
         // X = Cx/(E_z fx), Y = Cy/(E_z fy); a degenerate plane (through the camera centre) misses everywhere
-        h.h0 = ok ? make_float4((float)(pc.Cx[0] * sx), (float)(pc.Cx[1] * sx), (float)(pc.Cx[2] * sx),
-                                (float)(pc.Cy[0] * sy))
-                  : make_float4(0.f, 0.f, nan, 0.f);
-        h.h1 = ok ? make_float4((float)(pc.Cy[1] * sy), (float)(pc.Cy[2] * sy), (float)g.alpha_k, hx)
-                  : make_float4(0.f, nan, (float)g.alpha_k, hx);
-        h.h2 = make_float4(hy, __int_as_float(cxi), __int_as_float(cyi), 0.0f);
+        h.h0 = ok ? mk4(pc.Cx[0] * sx, pc.Cx[1] * sx, pc.Cx[2] * sx, pc.Cy[0] * sy) : mk4(0.0, 0.0, nan, 0.0);
+        h.h1 = ok ? mk4(pc.Cy[1] * sy, pc.Cy[2] * sy, g.alpha_k, hx) : mk4(0.0, nan, g.alpha_k, hx);
+        h.h2 = mk4(hy, 0.0, 0.0, 0.0);
+        h.h2.y = hdr_from_int(cxi);
+        h.h2.z = hdr_from_int(cyi);
     }
     const double ar = p.alpha_skip > 0.0 && g.alpha_k > p.alpha_skip ? alpha_radius(p, g) : 0.0;
     h.h3 = alpha_box(p, k, g, ar);
@@ -400,12 +408,12 @@ __global__ void __launch_bounds__(256, GB_K1_MINB) k_project(const ProjParams p,
 #define GB_K5_MINB 8
 #endif
 __global__ void __launch_bounds__(128, GB_K5_MINB) k_chain(const ProjParams p, const uint32_t* __restrict__ counts,
-                                               const float* __restrict__ accum, gb_grads g_out) {
+                                               const real* __restrict__ accum, gb_grads g_out) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= p.K) return;
     if (counts[k] == 0) return;
-    const float4* a4 = reinterpret_cast<const float4*>(accum + k * kAccumStride);
-    const float4 A = a4[0], B = a4[1], C = a4[2];
+    const real4* a4 = reinterpret_cast<const real4*>(accum + k * kAccumStride);
+    const real4 A = a4[0], B = a4[1], C = a4[2];
     Geom g;
     build_geom(p, k, g);
     if (p.mode == GB_MODE_ORTHO) {
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(128, GB_K5_MINB) k_chain(const ProjParams p, c
     }
     if (!g.valid) return;
     int cxi, cyi;
-    float hx, hy;
+    real hx, hy;
     double dxe, dye;
     pinhole_centre(p, g, cxi, cyi, hx, hy, dxe, dye);
     // K4 sums over pixels of gc' = dL/dc' (c' = c / E_z):  S_E = sum gc', S_X = sum dx gc', S_Y = sum dy gc'
@@ -532,7 +540,7 @@ cudaError_t launch_project(const ProjParams& p, ScreenHeader* hdr, CullRec* cull
     return cudaGetLastError();
 }
 
-cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const float* accum, const gb_grads& g,
+cudaError_t launch_chain(const ProjParams& p, const uint32_t* counts, const real* accum, const gb_grads& g,
                          cudaStream_t st) {
     if (p.K == 0) return cudaSuccess;
     const int threads = 128;  // 96 fp64-heavy registers per thread: finer blocks fill the SMs better (+1 %)

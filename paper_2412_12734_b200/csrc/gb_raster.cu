@@ -86,31 +86,31 @@ __device__ __forceinline__ int cell_offset(int i, int N) {
 // One backward entry for the calling warp, after the evaluation: rewind the pixel's state, form the
 // adjoints and reduce/scatter the gradients (raster.hpp:324-363).
 template <int MODE, int NT, int CELL>
-__device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, bool on, unsigned act, float u,
-                                          float v, float G, float alpha, float araw, const PinholeTerms& pt,
-                                          float& T, float g0, float g1, float g2, float& bh0, float& bh1,
-                                          float& bh2, const RasterConst& rc, int N, int lane, float* wscratch,
-                                          float* __restrict__ accum, float* __restrict__ grid_grad) {
+__device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, bool on, unsigned act, real u,
+                                          real v, real G, real alpha, real araw, const PinholeTerms& pt,
+                                          real& T, real g0, real g1, real g2, real& bh0, real& bh1,
+                                          real& bh2, const RasterConst& rc, int N, int lane, real* wscratch,
+                                          real* __restrict__ accum, real* __restrict__ grid_grad) {
     constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
     constexpr int NX = CellShape<CELL>::texels;
     const int F = 3 * N * N;
-    const float sigma = rc.sigma;
-    float red[16];  // screen-space sums (NS of 16 slots)
+    const real sigma = rc.sigma;
+    real red[16];  // screen-space sums (NS of 16 slots)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) red[i] = 0.0f;
-    float tg[3 * NX];
+    for (int i = 0; i < 16; ++i) red[i] = (real)0;
+    real tg[3 * NX];
 #pragma unroll
-    for (int i = 0; i < 3 * NX; ++i) tg[i] = 0.0f;
+    for (int i = 0; i < 3 * NX; ++i) tg[i] = (real)0;
     int tbase = -1;
-    float wk[NX];  // corner weights
+    real wk[NX];  // corner weights
 #pragma unroll
-    for (int k = 0; k < NX; ++k) wk[k] = 0.0f;
+    for (int k = 0; k < NX; ++k) wk[k] = (real)0;
     if (on) {
-        T = __fmul_rn(T, rcp_approx(__fsub_rn(1.0f, alpha)));  // raster.hpp:333
-        float c0, c1, c2, fu_hat = 0.0f, fv_hat = 0.0f;
-        const float aT = alpha * T;
-        const float chat[3] = {aT * g0, aT * g1, aT * g2};  // c_hat (raster.hpp:338-340)
-        float cc_[3];
+        T = mul_rn(T, rcp_approx(sub_rn((real)1, alpha)));  // raster.hpp:333
+        real c0, c1, c2, fu_hat = (real)0, fv_hat = (real)0;
+        const real aT = alpha * T;
+        const real chat[3] = {aT * g0, aT * g1, aT * g2};  // c_hat (raster.hpp:338-340)
+        real cc_[3];
         if (CELL == kCellFull) {
             Bilin b;
             bilin_setup(u, v, N, rc, b);
@@ -118,7 +118,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             const float* p10 = p00 + 3 * N;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
+                const real c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
                 cc_[c] = c00 * b.w00 + c10 * b.w10 + c01 * b.w01 + c11 * b.w11;
                 tg[c] = chat[c] * b.w00;
                 tg[3 + c] = chat[c] * b.w10;
@@ -126,9 +126,9 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
                 tg[9 + c] = chat[c] * b.w11;
                 // texture.hpp:102-103: (C10 - C00)(1 - f_v) + (C11 - C01) f_v = du + f_v e and
                 // (C01 - C00)(1 - f_u) + (C11 - C10) f_u = dv + f_u e, e = C11 - C10 - C01 + C00
-                const float du = c10 - c00, dv = c01 - c00, e = (c11 - c10) - dv;
-                fu_hat = fmaf(chat[c], fmaf(b.fv, e, du), fu_hat);
-                fv_hat = fmaf(chat[c], fmaf(b.fu, e, dv), fv_hat);
+                const real du = c10 - c00, dv = c01 - c00, e = (c11 - c10) - dv;
+                fu_hat = fma_rn(chat[c], fma_rn(b.fv, e, du), fu_hat);
+                fv_hat = fma_rn(chat[c], fma_rn(b.fu, e, dv), fv_hat);
             }
             tbase = b.o00;
             wk[0] = b.w00;
@@ -137,24 +137,24 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             wk[3] = b.w11;
         } else if (CELL == kCellU || CELL == kCellV) {
             // interpolation along one axis; the other sits on texel 0 or n-1
-            const float w = CELL == kCellU ? u : v;
-            float sx = __fmaf_rn(w, rc.tex_scale, rc.tex_offset);
-            sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
-            const int i0 = min((int)floorf(sx), N - 2);
-            const float f = __fsub_rn(sx, (float)i0);
-            const float gf = 1.0f - f;
-            const int other = (CELL == kCellU ? v : u) > 0.0f ? N - 1 : 0;
+            const real w = CELL == kCellU ? u : v;
+            real sx = fma_rn(w, rc.tex_scale, rc.tex_offset);
+            sx = rmin(rmax(sx, (real)0), (real)(N - 1));
+            const int i0 = min((int)rfloor(sx), N - 2);
+            const real f = sub_rn(sx, (real)i0);
+            const real gf = (real)1 - f;
+            const int other = (CELL == kCellU ? v : u) > (real)0 ? N - 1 : 0;
             tbase = (CELL == kCellU ? i0 * N + other : other * N + i0) * 3;
             const float* pa = t + tbase;
             const float* pb = pa + (CELL == kCellU ? 3 * N : 3);
-            float fh = 0.0f;
+            real fh = (real)0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float ca = pa[c], cb = pb[c];
-                cc_[c] = fmaf(cb, f, ca * gf);  // = the four-corner blend with two zero weights
+                const real ca = pa[c], cb = pb[c];
+                cc_[c] = fma_rn(cb, f, ca * gf);  // = the four-corner blend with two zero weights
                 tg[c] = chat[c] * gf;
                 tg[3 + c] = chat[c] * f;
-                fh = fmaf(chat[c], cb - ca, fh);
+                fh = fma_rn(chat[c], cb - ca, fh);
             }
             if (CELL == kCellU)
                 fu_hat = fh;
@@ -163,27 +163,27 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             wk[0] = gf;
             wk[1] = f;
         } else {  // kCellOne (and n = 1): a single texel with weight 1
-            const int iu = N > 1 && u > 0.0f ? N - 1 : 0, iv = N > 1 && v > 0.0f ? N - 1 : 0;
+            const int iu = N > 1 && u > (real)0 ? N - 1 : 0, iv = N > 1 && v > (real)0 ? N - 1 : 0;
             tbase = (iu * N + iv) * 3;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 cc_[c] = t[tbase + c];
                 tg[c] = chat[c];
             }
-            wk[0] = 1.0f;
+            wk[0] = (real)1;
         }
         c0 = cc_[0];
         c1 = cc_[1];
         c2 = cc_[2];
         // texture.hpp:106-109 (strict mask)
-        float u_hat = (CELL != kCellV && CELL != kCellOne && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : 0.0f;
-        float v_hat = (CELL != kCellU && CELL != kCellOne && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : 0.0f;
+        real u_hat = (CELL != kCellV && CELL != kCellOne && u > -sigma && u < sigma) ? rc.tex_scale * fu_hat : (real)0;
+        real v_hat = (CELL != kCellU && CELL != kCellOne && v > -sigma && v < sigma) ? rc.tex_scale * fv_hat : (real)0;
         // raster.hpp:344-346
-        const float alpha_hat = T * (g0 * (c0 - bh0) + g1 * (c1 - bh1) + g2 * (c2 - bh2));
-        float op = 0.0f;
-        if (araw < kMaxAlphaF) {  // raster.hpp:350-354
+        const real alpha_hat = T * (g0 * (c0 - bh0) + g1 * (c1 - bh1) + g2 * (c2 - bh2));
+        real op = (real)0;
+        if (araw < kMaxAlpha) {  // raster.hpp:350-354
             op = alpha_hat * G;
-            const float aa = alpha_hat * alpha;
+            const real aa = alpha_hat * alpha;
             u_hat -= aa * u;
             v_hat -= aa * v;
         }
@@ -197,8 +197,8 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             red[6] = op;
         } else {
             // (u, v) = (c_x, c_y) / c_z with c = E' + dx X + dy Y (K1 header)
-            const float iz = pt.iz;
-            const float gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
+            const real iz = pt.iz;
+            const real gc0 = u_hat * iz, gc1 = v_hat * iz, gc2 = -(u_hat * u + v_hat * v) * iz;
             red[0] = gc0;
             red[1] = gc1;
             red[2] = gc2;
@@ -211,30 +211,30 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             red[9] = op;
         }
         // raster.hpp:362
-        const float om = 1.0f - alpha;
+        const real om = (real)1 - alpha;
         bh0 = alpha * c0 + om * bh0;
         bh1 = alpha * c1 + om * bh1;
         bh2 = alpha * c2 + om * bh2;
     }
-    float* gg = grid_grad + (size_t)id * F;
-    // this lane's non-zero texels straight to memory: one float2 + one float red each
+    real* gg = grid_grad + (size_t)id * F;
+    // this lane's non-zero texels straight to memory: one float2 + one float red each (fp32)
     auto texel_reds = [&]() {
 #pragma unroll
         for (int k = 0; k < NX; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
-            if (wk[k] != 0.0f)
+            if (wk[k] != (real)0)
                 red3(gg + tbase + cell_offset<CELL>(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
     };
     if (__popc(act) <= kDirectLanes) {
         // few active lanes: each adds its own terms with vector reds -- ~20 instructions for the warp
         // instead of two ~35-instruction warp reductions (12 % of warp-entries have one active lane)
         if (on) {
-            float* a = accum + (size_t)id * kAccumStride;  // 48-B records: 16-B aligned
+            real* a = accum + (size_t)id * kAccumStride;  // 48-B records: 16-B aligned
             red4(a, red[0], red[1], red[2], red[3]);
             if (NS == 10) {
                 red4(a + 4, red[4], red[5], red[6], red[7]);
-                atomicAdd(reinterpret_cast<float2*>(a + 8), make_float2(red[8], red[9]));
+                red2(a + 8, red[8], red[9]);
             } else {
-                atomicAdd(reinterpret_cast<float2*>(a + 4), make_float2(red[4], red[5]));
+                red2(a + 4, red[4], red[5]);
                 atomicAdd(a + 6, red[6]);
             }
             texel_reds();
@@ -242,20 +242,20 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         return;
     }
     {  // screen-space sums: lane l owns value l >> 1
-        float sv[NS];
+        real sv[NS];
 #pragma unroll
         for (int i = 0; i < NS; ++i) sv[i] = red[i];
-        const float r2 = smem_reduce<NS>(sv, wscratch, lane);
+        const real r2 = smem_reduce<NS>(sv, wscratch, lane);
         if ((lane & 1) == 0 && (lane >> 1) < NS) red_add(accum + (size_t)id * kAccumStride + (lane >> 1), r2);
     }
     if (CELL == kCellOne && NT != 1 && N > 1) {
         // one texel per lane, and it is one of the four grid corners (by the signs of u, v): one warp
         // reduction over the 4 corners x 3 channels instead of up to 32 reds on at most 4 addresses
-        const int q = on ? ((u > 0.0f) ? 2 : 0) + ((v > 0.0f) ? 1 : 0) : -1;
-        float tq[12];
+        const int q = on ? ((u > (real)0) ? 2 : 0) + ((v > (real)0) ? 1 : 0) : -1;
+        real tq[12];
 #pragma unroll
-        for (int i = 0; i < 12; ++i) tq[i] = (q == i / 3) ? tg[i % 3] : 0.0f;
-        const float r2 = smem_reduce<12>(tq, wscratch, lane);
+        for (int i = 0; i < 12; ++i) tq[i] = (q == i / 3) ? tg[i % 3] : (real)0;
+        const real r2 = smem_reduce<12>(tq, wscratch, lane);
         const int row = lane >> 1, qc = row / 3;
         if ((lane & 1) == 0 && row < 12)
             red_add(gg + 3 * (((qc >> 1) ? N - 1 : 0) * N + ((qc & 1) ? N - 1 : 0)) + row % 3, r2);
@@ -266,7 +266,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
     const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
     if (__all_sync(kFull, !on || tbase == b0)) {
         if (lane == 0) GB_DBG(4, 1);
-        const float r2 = smem_reduce<3 * NX>(tg, wscratch, lane);
+        const real r2 = smem_reduce<3 * NX>(tg, wscratch, lane);
         if ((lane & 1) == 0 && (lane >> 1) < 3 * NX) red_add(gg + b0 + cell_offset<CELL>(lane >> 1, N), r2);
     } else if (on) {
         if (lane == 0) GB_DBG(5, 1);
@@ -278,13 +278,13 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
 // bwd_shade (raster.hpp:324-363).
 template <int MODE, int NT>
 __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __restrict__ t, int id, int rank,
-                                          int last, int x, int y, float& T, float g0, float g1, float g2,
-                                          float& bh0, float& bh1, float& bh2, const RasterConst& rc, int N,
-                                          int lane, float* wscratch, float* __restrict__ accum,
-                                          float* __restrict__ grid_grad) {
-    const float sigma = rc.sigma;
+                                          int last, int x, int y, real& T, real g0, real g1, real g2,
+                                          real& bh0, real& bh1, real& bh2, const RasterConst& rc, int N,
+                                          int lane, real* wscratch, real* __restrict__ accum,
+                                          real* __restrict__ grid_grad) {
+    const real sigma = rc.sigma;
     bool on = rank <= last;
-    float u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
+    real u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
     PinholeTerms pt;
     if (on) {
         bool hit;
@@ -295,8 +295,8 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
         }
         if (hit) {
             G = gauss_weight(u, v);
-            araw = __fmul_rn(h.h1.z, G);
-            alpha = fminf(araw, kMaxAlphaF);
+            araw = mul_rn(h.h1.z, G);
+            alpha = rmin(araw, kMaxAlpha);
             on = !(alpha < rc.alpha_skip);
         } else {
             on = false;
@@ -387,17 +387,17 @@ template <int MODE, int NT>
 __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __restrict__ values,
                                          const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                          const float* __restrict__ tex, const RasterConst& rc, int N,
-                                         const WarpPixel& wp, float& T, float& acc0, float& acc1, float& acc2,
+                                         const WarpPixel& wp, real& T, real& acc0, real& acc1, real& acc2,
                                          int& last) {
     const int F = 3 * N * N;
     const int lane = threadIdx.x & 31;
     const int total = (int)(range.y - range.x);
     const int x = wp.x, y = wp.y;
-    T = 1.0f;
-    acc0 = acc1 = acc2 = 0.0f;
+    T = (real)1;
+    acc0 = acc1 = acc2 = (real)0;
     last = -1;
     bool done = !wp.inside;
-    const float early = rc.early_stop > 0.0f ? rc.early_stop : -1.0f;  // T >= 0: a disabled stop never fires
+    const real early = rc.early_stop > (real)0 ? rc.early_stop : -(real)1;  // T >= 0: a disabled stop never fires
     for (int c0 = 0; c0 < total && !__all_sync(kFull, done); c0 += 32) {
         const WarpPixel lr = live_rect(wp, !done);
         int idl = -1;
@@ -413,11 +413,11 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             const int id = __shfl_sync(kFull, idl, bit);
             // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not
             // composite -- no branch around the evaluation
-            float u, v;
+            real u, v;
             ScreenHeader h;
-            h.h0 = __ldg(&hdr[id].h0);
-            h.h1 = __ldg(&hdr[id].h1);
-            h.h2 = __ldg(&hdr[id].h2);
+            h.h0 = ld_real4(&hdr[id].h0);
+            h.h1 = ld_real4(&hdr[id].h1);
+            h.h2 = ld_real4(&hdr[id].h2);
             bool hit;
             if (MODE == GB_MODE_ORTHO) {
                 hit = eval_uv_ortho(h, x, y, u, v);
@@ -425,16 +425,16 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
                 PinholeTerms pt;
                 hit = eval_uv_pinhole(h, x, y, u, v, pt);
             }
-            const float G = gauss_weight(u, v);
-            const float alpha = fminf(__fmul_rn(h.h1.z, G), kMaxAlphaF);  // raster.hpp:241
+            const real G = gauss_weight(u, v);
+            const real alpha = rmin(mul_rn(h.h1.z, G), kMaxAlpha);  // raster.hpp:241
             const bool comp = !done && hit && !(alpha < rc.alpha_skip);     // raster.hpp:242
             // texel footprint class of the warp (see bwd_shade): clamped axes read one texel row
-            const float sigma = rc.sigma;
+            const real sigma = rc.sigma;
             const bool au = N > 1 && __any_sync(kFull, comp && u > -sigma && u < sigma);
             const bool av = N > 1 && __any_sync(kFull, comp && v > -sigma && v < sigma);
             if (comp) {
                 const float* t = tex + (size_t)id * F;
-                float c0_, c1_, c2_;
+                real c0_, c1_, c2_;
                 if (au && av) {
                     Bilin b;
                     bilin_setup(u, v, N, rc, b);
@@ -449,37 +449,37 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
                     // (separate uniform branches: each keeps its index arithmetic free of selects)
                     const float* pa;
                     const float* pb;
-                    float f;
+                    real f;
                     if (au) {
-                        float sx = __fmaf_rn(u, rc.tex_scale, rc.tex_offset);
-                        sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
-                        const int i0 = min((int)floorf(sx), N - 2);
-                        f = __fsub_rn(sx, (float)i0);
-                        pa = t + (i0 * N + (v > 0.0f ? N - 1 : 0)) * 3;
+                        real sx = fma_rn(u, rc.tex_scale, rc.tex_offset);
+                        sx = rmin(rmax(sx, (real)0), (real)(N - 1));
+                        const int i0 = min((int)rfloor(sx), N - 2);
+                        f = sub_rn(sx, (real)i0);
+                        pa = t + (i0 * N + (v > (real)0 ? N - 1 : 0)) * 3;
                         pb = pa + 3 * N;
                     } else {
-                        float sx = __fmaf_rn(v, rc.tex_scale, rc.tex_offset);
-                        sx = fminf(fmaxf(sx, 0.0f), (float)(N - 1));
-                        const int i0 = min((int)floorf(sx), N - 2);
-                        f = __fsub_rn(sx, (float)i0);
-                        pa = t + ((u > 0.0f ? N - 1 : 0) * N + i0) * 3;
+                        real sx = fma_rn(v, rc.tex_scale, rc.tex_offset);
+                        sx = rmin(rmax(sx, (real)0), (real)(N - 1));
+                        const int i0 = min((int)rfloor(sx), N - 2);
+                        f = sub_rn(sx, (real)i0);
+                        pa = t + ((u > (real)0 ? N - 1 : 0) * N + i0) * 3;
                         pb = pa + 3;
                     }
-                    const float gf = 1.0f - f;
-                    c0_ = fmaf(__ldg(pb), f, __ldg(pa) * gf);
-                    c1_ = fmaf(__ldg(pb + 1), f, __ldg(pa + 1) * gf);
-                    c2_ = fmaf(__ldg(pb + 2), f, __ldg(pa + 2) * gf);
+                    const real gf = (real)1 - f;
+                    c0_ = fma_rn(__ldg(pb), f, __ldg(pa) * gf);
+                    c1_ = fma_rn(__ldg(pb + 1), f, __ldg(pa + 1) * gf);
+                    c2_ = fma_rn(__ldg(pb + 2), f, __ldg(pa + 2) * gf);
                 } else {  // one texel (and n = 1)
-                    const float* p = t + (N > 1 ? ((u > 0.0f ? N - 1 : 0) * N + (v > 0.0f ? N - 1 : 0)) * 3 : 0);
+                    const float* p = t + (N > 1 ? ((u > (real)0 ? N - 1 : 0) * N + (v > (real)0 ? N - 1 : 0)) * 3 : 0);
                     c0_ = __ldg(p);
                     c1_ = __ldg(p + 1);
                     c2_ = __ldg(p + 2);
                 }
-                const float w = alpha * T;  // raster.hpp:244-249
-                acc0 = fmaf(c0_, w, acc0);
-                acc1 = fmaf(c1_, w, acc1);
-                acc2 = fmaf(c2_, w, acc2);
-                T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+                const real w = alpha * T;  // raster.hpp:244-249
+                acc0 = fma_rn(c0_, w, acc0);
+                acc1 = fma_rn(c1_, w, acc1);
+                acc2 = fma_rn(c2_, w, acc2);
+                T = mul_rn(T, sub_rn((real)1, alpha));
                 last = c0 + bit;
                 if (T < early) done = true;  // raster.hpp:250
             }
@@ -493,12 +493,12 @@ template <int MODE, int NT>
 __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __restrict__ values,
                                          const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                          const float* __restrict__ tex, const CamConst& cc, const RasterConst& rc,
-                                         int N, const WarpPixel& wp, int last, float T, float g0, float g1, float g2,
-                                         float* wscratch, float* __restrict__ accum, float* __restrict__ grid_grad) {
+                                         int N, const WarpPixel& wp, int last, real T, real g0, real g1, real g2,
+                                         real* wscratch, real* __restrict__ accum, real* __restrict__ grid_grad) {
     const int F = 3 * N * N;
     const int lane = threadIdx.x & 31;
-    if (g0 == 0.0f && g1 == 0.0f && g2 == 0.0f) last = -1;  // raster.hpp:315-317
-    float bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
+    if (g0 == (real)0 && g1 == (real)0 && g2 == (real)0) last = -1;  // raster.hpp:315-317
+    real bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
     const int wlast = __reduce_max_sync(kFull, last);
     for (int c0 = wlast & ~31; c0 >= 0; c0 -= 32) {
         // (a live rectangle here -- lanes with last >= c0 -- measured 1 % slower: few entries drop out)
@@ -516,9 +516,9 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
             mask &= ~(1u << bit);
             const int id = __shfl_sync(kFull, idl, bit);
             ScreenHeader h;
-            h.h0 = __ldg(&hdr[id].h0);
-            h.h1 = __ldg(&hdr[id].h1);
-            h.h2 = __ldg(&hdr[id].h2);
+            h.h0 = ld_real4(&hdr[id].h0);
+            h.h1 = ld_real4(&hdr[id].h1);
+            h.h2 = ld_real4(&hdr[id].h2);
             bwd_entry<MODE, NT>(h, tex + (size_t)id * F, id, c0 + bit, last, wp.x, wp.y, T, g0, g1, g2, bh0, bh1,
                                 bh2, rc, N, lane, wscratch, accum, grid_grad);
         }
@@ -534,15 +534,18 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
                                                         float* __restrict__ out_color, float* __restrict__ out_trans,
                                                         int32_t* __restrict__ out_last) {
     const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
-    float T, a0, a1, a2;
+    real T, a0, a1, a2;
     int last;
     fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
     if (wp.inside) {  // raster.hpp:253-254
         const size_t p = (size_t)wp.y * cc.width + wp.x;
-        out_color[p * 3 + 0] = fmaf(T, cc.bg[0], a0);
-        out_color[p * 3 + 1] = fmaf(T, cc.bg[1], a1);
-        out_color[p * 3 + 2] = fmaf(T, cc.bg[2], a2);
+        out_color[p * 3 + 0] = fma_rn(T, cc.bg[0], a0);
+        out_color[p * 3 + 1] = fma_rn(T, cc.bg[1], a1);
+        out_color[p * 3 + 2] = fma_rn(T, cc.bg[2], a2);
         out_trans[p] = T;
+#ifdef GB_PARITY_F64
+        if (rc.trans64) rc.trans64[p] = T;
+#endif
         out_last[p] = last;
     }
 }
@@ -561,33 +564,36 @@ __global__ void __launch_bounds__(256) k_forward_loss(const uint2* __restrict__ 
                                                       int32_t* __restrict__ out_last, float* __restrict__ out_grad,
                                                       float* __restrict__ loss) {
     const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
-    float T, a0, a1, a2;
+    real T, a0, a1, a2;
     int last;
     fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
-    float l = 0.0f;
+    real l = (real)0;
     if (wp.inside) {
         const size_t p = (size_t)wp.y * cc.width + wp.x;
-        const float c[3] = {fmaf(T, cc.bg[0], a0), fmaf(T, cc.bg[1], a1), fmaf(T, cc.bg[2], a2)};
+        const real c[3] = {fma_rn(T, cc.bg[0], a0), fma_rn(T, cc.bg[1], a1), fma_rn(T, cc.bg[2], a2)};
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {  // K6 (gb_misc.cu k_loss), per pixel
-            const float d = c[ch] - target[p * 3 + ch];
-            float g;
+            const real d = c[ch] - target[p * 3 + ch];
+            real g;
             if (KIND == 0) {
-                l += fabsf(d);
-                g = scale * (float)((d > 0.0f) - (d < 0.0f));
+                l += rabs(d);
+                g = scale * (real)((d > (real)0) - (d < (real)0));
             } else {
-                l = fmaf(d, d, l);
-                g = 2.0f * scale * d;
+                l = fma_rn(d, d, l);
+                g = (real)2 * scale * d;
             }
             out_grad[p * 3 + ch] = g;
             if (out_color) out_color[p * 3 + ch] = c[ch];
         }
         out_trans[p] = T;
+#ifdef GB_PARITY_F64
+        if (rc.trans64) rc.trans64[p] = T;
+#endif
         out_last[p] = last;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
-    if ((threadIdx.x & 31) == 0 && loss && l != 0.0f) atomicAdd(loss, l * scale);
+    if ((threadIdx.x & 31) == 0 && loss && l != (real)0) atomicAdd(loss, (float)(l * scale));
 }
 
 // <= 48 registers: 5 CTAs (40 warps) per SM -- with 32 B of spills, measured 1.3 % faster than 64
@@ -604,11 +610,11 @@ __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2
                                                          const float* __restrict__ in_trans,
                                                          const int32_t* __restrict__ in_last,
                                                          const float* __restrict__ image_grad,
-                                                         float* __restrict__ accum, float* __restrict__ grid_grad) {
-    extern __shared__ __align__(16) float red_scratch[];
+                                                         real* __restrict__ accum, real* __restrict__ grid_grad) {
+    extern __shared__ __align__(16) real red_scratch[];
     const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
     int last = -1;
-    float T = 1.0f, g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
+    real T = (real)1, g0 = (real)0, g1 = (real)0, g2 = (real)0;
     if (wp.inside) {  // raster.hpp:313-322
         const size_t p = (size_t)wp.y * cc.width + wp.x;
         last = in_last[p];
@@ -616,6 +622,9 @@ __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2
         g1 = image_grad[p * 3 + 1];
         g2 = image_grad[p * 3 + 2];
         T = in_trans[p];
+#ifdef GB_PARITY_F64
+        if (rc.trans64) T = rc.trans64[p];
+#endif
     }
     bwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1, g2,
                        red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad);
@@ -636,29 +645,29 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
                                                       const float* __restrict__ target, float scale,
                                                       float* __restrict__ out_color, float* __restrict__ out_trans,
                                                       int32_t* __restrict__ out_last, float* __restrict__ out_grad,
-                                                      float* __restrict__ loss, float* __restrict__ accum,
-                                                      float* __restrict__ grid_grad) {
-    extern __shared__ __align__(16) float red_scratch[];
+                                                      float* __restrict__ loss, real* __restrict__ accum,
+                                                      real* __restrict__ grid_grad) {
+    extern __shared__ __align__(16) real red_scratch[];
     const int N = tex_n<NT>(n_rt);
     const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
     const uint2 range = ranges[blockIdx.x];
-    float T, a0, a1, a2;
+    real T, a0, a1, a2;
     int last;
     fwd_walk<MODE, NT>(range, values, hdr, cull, tex, rc, N, wp, T, a0, a1, a2, last);
-    float g0 = 0.0f, g1 = 0.0f, g2 = 0.0f, l = 0.0f;
+    real g0 = (real)0, g1 = (real)0, g2 = (real)0, l = (real)0;
     if (wp.inside) {
         const size_t p = (size_t)wp.y * cc.width + wp.x;
-        const float c[3] = {fmaf(T, cc.bg[0], a0), fmaf(T, cc.bg[1], a1), fmaf(T, cc.bg[2], a2)};
-        float g[3];
+        const real c[3] = {fma_rn(T, cc.bg[0], a0), fma_rn(T, cc.bg[1], a1), fma_rn(T, cc.bg[2], a2)};
+        real g[3];
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {  // K6 (gb_misc.cu k_loss), per pixel
-            const float d = c[ch] - target[p * 3 + ch];
+            const real d = c[ch] - target[p * 3 + ch];
             if (KIND == 0) {
-                l += fabsf(d);
-                g[ch] = scale * (float)((d > 0.0f) - (d < 0.0f));
+                l += rabs(d);
+                g[ch] = scale * (real)((d > (real)0) - (d < (real)0));
             } else {
-                l = fmaf(d, d, l);
-                g[ch] = 2.0f * scale * d;
+                l = fma_rn(d, d, l);
+                g[ch] = (real)2 * scale * d;
             }
         }
         g0 = g[0];
@@ -669,6 +678,9 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
             out_color[p * 3 + 1] = c[1];
             out_color[p * 3 + 2] = c[2];
             out_trans[p] = T;
+#ifdef GB_PARITY_F64
+        if (rc.trans64) rc.trans64[p] = T;
+#endif
             out_last[p] = last;
         }
         if (out_grad) {
@@ -679,7 +691,7 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
-    if ((threadIdx.x & 31) == 0 && loss && l != 0.0f) atomicAdd(loss, l * scale);
+    if ((threadIdx.x & 31) == 0 && loss && l != (real)0) atomicAdd(loss, (float)(l * scale));
     bwd_walk<MODE, NT>(range, values, hdr, cull, tex, cc, rc, N, wp, last, T, g0, g1, g2,
                        red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad);
 }
@@ -699,7 +711,7 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
     }
 
 static int tile_threads(int ts) { return ((ts * ts + 31) / 32) * 32; }
-static size_t red_smem(int threads) { return (size_t)(threads / 32) * kRedRows * kRedStride * 4; }
+static size_t red_smem(int threads) { return (size_t)(threads / 32) * kRedRows * kRedStride * sizeof(real); }
 
 template <int MODE, int NT>
 static cudaError_t fwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
@@ -713,7 +725,7 @@ template <int MODE, int NT>
 static cudaError_t bwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                           const RasterConst& rc, int n, const float* trans, const int32_t* last,
-                          const float* image_grad, float* accum, float* grid_grad) {
+                          const float* image_grad, real* accum, real* grid_grad) {
     k_backward_direct<MODE, NT><<<tiles, threads, red_smem(threads), st>>>(ranges, values, hdr, cull, tex, cc, rc, n,
                                                                            trans, last, image_grad, accum, grid_grad);
     return cudaGetLastError();
@@ -736,7 +748,7 @@ cudaError_t launch_forward(int mode, int n, int tiles, int ts, const uint2* rang
 cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                             const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                             const RasterConst& rc, const float* trans, const int32_t* last, const float* image_grad,
-                            float* accum, float* grid_grad, cudaStream_t st) {
+                            real* accum, real* grid_grad, cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
     const int threads = tile_threads(ts);
     if (mode == GB_MODE_ORTHO) {
@@ -783,8 +795,8 @@ template <int MODE, int NT>
 static cudaError_t fused_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
                            const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                            const RasterConst& rc, int n, int kind, const float* target, float scale, float* color,
-                           float* trans, int32_t* last, float* image_grad, float* loss, float* accum,
-                           float* grid_grad) {
+                           float* trans, int32_t* last, float* image_grad, float* loss, real* accum,
+                           real* grid_grad) {
     if (kind == 0)
         k_fused_direct<MODE, NT, 0><<<tiles, threads, red_smem(threads), st>>>(
             ranges, values, hdr, cull, tex, cc, rc, n, target, scale, color, trans, last, image_grad, loss, accum,
@@ -799,7 +811,7 @@ static cudaError_t fused_t(int tiles, int threads, cudaStream_t st, const uint2*
 cudaError_t launch_fused(int mode, int n, int tiles, int ts, const uint2* ranges, const int32_t* values,
                          const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                          const RasterConst& rc, int kind, const float* target, float scale, float* color, float* trans,
-                         int32_t* last, float* image_grad, float* loss, float* accum, float* grid_grad,
+                         int32_t* last, float* image_grad, float* loss, real* accum, real* grid_grad,
                          cudaStream_t st) {
     if (tiles == 0) return cudaSuccess;
     const int threads = tile_threads(ts);

@@ -148,3 +148,98 @@ def compare_grads(gpu: dict, orc: dict, rtol=RTOL, atol=ATOL, model_c=MODEL_C) -
                       max_abs_err=float(d.max()) if d.size else 0.0,
                       max_rel_to_scale=float(d.max() / scale) if scale > 0 else 0.0)
     return out
+
+
+# ---------------------------------------------------------------------------------------------
+# Tile-row subsets: parity at sizes whose full fp64 backward does not fit the host.
+# The binning is compared in full (every pair); the forward and backward are compared on every
+# `stride`-th tile row (plus the last, ragged row).  The GPU renders the WHOLE scene and backpropagates
+# an image_grad that is zero outside those rows, so its gradients hold exactly the subset tiles'
+# contributions (zero-cotangent pixels are skipped, raster.hpp:315-317).  The oracle runs on the subset
+# tiles' lists over the primitives they reference, compacted in index order (so per-tile order is kept).
+# ---------------------------------------------------------------------------------------------
+def subset_rows(tiles_y: int, stride: int):
+    return sorted(set(range(0, tiles_y, stride)) | {tiles_y - 1})
+
+
+def run_rows(arrays: dict, mode: int, n: int, cam: "O.Cam", cfg: "O.Cfg", image_grad, stride: int = 8,
+             sigma=0.5, device="cuda"):
+    """-> (gpu, orc, info) shaped for compare_binning / compare_image / compare_grads."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+
+    K = int(arrays["opacity_logit"].shape[0])
+    geo = {f: (None if f == "grid" else arrays.get(f)) for f in O.FIELDS}
+    geo["grid"] = np.zeros((K, 3), np.float32)
+    offsets, values, tiles = O.build_binning(O.Scene64(geo, 1, sigma), cam, cfg)
+    tx, ty = tiles
+    ts = cfg.tile_size
+    rows = subset_rows(ty, stride)
+    px_rows = np.zeros(cam.height, bool)
+    for r in rows:
+        px_rows[r * ts:min(cam.height, (r + 1) * ts)] = True
+    ig = np.where(px_rows[:, None, None], np.asarray(image_grad, np.float64), 0.0)
+    # subset lists and the primitives they reference, compacted in index order
+    keep_t = np.zeros(tx * ty, bool)
+    for r in rows:
+        keep_t[r * tx:(r + 1) * tx] = True
+    counts = np.diff(offsets)
+    sub_counts = np.where(keep_t, counts, 0)
+    mask = np.repeat(keep_t, counts)
+    sub_vals = values[mask]
+    ids = np.unique(sub_vals)
+    remap = np.full(K, -1, np.int64)
+    remap[ids] = np.arange(len(ids))
+    sub_off = np.zeros(tx * ty + 1, np.int64)
+    sub_off[1:] = np.cumsum(sub_counts)
+    sub_bin = (sub_off, remap[sub_vals].astype(np.int32), tiles)
+
+    # GPU: the whole scene
+    splats = gb.SplatSet.from_numpy(mode, gb.ColorGridConfig(n, sigma), device=device, **arrays)
+    camera = (gb.ImagePlaneCamera(cam.width, cam.height, tuple(cam.background)) if mode == O.MODE_ORTHO
+              else gb.PinholeCamera.from_spec(cam))
+    rc = gb.RasterConfig(cfg.tile_size, cfg.cutoff_radius, cfg.alpha_skip, cfg.early_stop, 1)
+    binning = gb.build_binning(splats, camera, rc)
+    out = gb.render_forward(splats, camera, binning)
+    g = gb.render_backward(splats, camera, binning, out,
+                           torch.as_tensor(np.ascontiguousarray(ig, np.float32), device=device))
+    torch.cuda.synchronize()
+    gpu = {}
+    gpu["offsets"], gpu["values"] = binning.csr()
+    gpu["color"] = out.color.cpu().numpy().astype(np.float64)[px_rows]
+    gpu["trans"] = out.final_transmittance.cpu().numpy().astype(np.float64)[px_rows]
+    gpu["last"] = out.last_rank.cpu().numpy()[px_rows]
+    tid = torch.as_tensor(ids, device=device)
+    gpu["grads"] = {}
+    outside = {}
+    for f, t in g.tensors().items():
+        if t is None:
+            continue
+        t2 = t.reshape(K, -1)
+        gpu["grads"][f] = t2.index_select(0, tid).cpu().numpy().astype(np.float64)
+        others = torch.ones(K, dtype=torch.bool, device=device)
+        others[tid] = False
+        outside[f] = int((t2[others] != 0).sum())
+    del splats, binning, out, g
+    torch.cuda.empty_cache()
+
+    # oracle: the subset tiles over the compacted primitives
+    sub_arrays = {f: (None if arrays.get(f) is None else np.ascontiguousarray(arrays[f][ids])) for f in O.FIELDS}
+    scene = O.Scene64(sub_arrays, n, sigma)
+    f = O.render_forward(scene, cam, cfg, sub_bin)
+    gr, mag, slack = O.render_backward(scene, cam, cfg, sub_bin, f, ig)
+    orc = dict(offsets=offsets, values=values, color=f["color"][px_rows], trans=f["trans"][px_rows],
+               last=f["last"][px_rows], kink=f["kink"][px_rows],
+               grads={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in gr.items()},
+               mag={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in mag.items()},
+               slack={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in slack.items()})
+    info = dict(tile_rows=len(rows), tiles_y=ty, subset_pairs=int(len(sub_vals)), pairs=int(len(values)),
+                subset_primitives=int(len(ids)), gpu_nonzero_outside_subset=outside,
+                max_list=int(counts.max()) if counts.size else 0, mean_list=float(counts.mean()))
+    return gpu, orc, info
+
+
+def strict_summary(grads_stats: dict) -> dict:
+    """Per field: entries beyond rtol/atol + kink slack with NO cancellation exemption."""
+    return {f: st["strict_violations"] for f, st in grads_stats.items()}
