@@ -29,10 +29,12 @@
 #include <cstdio>
 #include <cmath>
 #include <cstdint>
+#include <exception>
 #include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gb_raster.h"
@@ -839,5 +841,332 @@ inline FitResult fit(const Image& target, const TrainConfig& cfg) {
     set.grid = detail::download(*p.grid, K * F);
     return result;
 }
+
+// ---- the view-sharded multi-GPU training step (BASELINE configs[3]) ------------------
+// fit's loop (train.hpp:190-217: build_binning -> render_forward -> loss -> render_backward -> adam_step),
+// generalised to many camera views sharded over GPUs.  Every rank keeps a replica of the primitives,
+// renders and backpropagates its own views into one flat fp32 gradient buffer (gb_render_loss_backward:
+// K3 with the L1 loss in its epilogue, K4, K5), then the ranks exchange gradients over NCCL through the
+// C-ABI -- reduce-scatter, Adam on the rank's 1/N slice (gb_adam_segments, the non-finite guard agreed by
+// a min-all-reduce of its flag), all-gather of the parameters; or one all-reduce and a replicated Adam.
+// One host thread per GPU, communicators from ncclCommInitAll (train) or ncclCommInitRank (one process
+// per GPU: Rank + gb_comm_init_rank).  Pinhole surfels (the BASELINE configs' camera; no reference).
+namespace multiview {
+
+struct PinholeCamera {
+    int width = 0, height = 0;
+    double fx = 1000.0, fy = 1000.0, cx = 0.0, cy = 0.0;
+    std::array<double, 9> rot{1, 0, 0, 0, 1, 0, 0, 0, 1};  // world -> camera
+    std::array<double, 3> trans{0, 0, 0};
+    double near_plane = 0.01;
+    std::array<double, 3> background{0, 0, 0};
+    gb_camera to_c() const {
+        gb_camera c{};
+        c.mode = GB_MODE_PINHOLE;
+        c.width = width;
+        c.height = height;
+        for (int i = 0; i < 3; ++i) c.background[i] = background[i];
+        c.fx = fx;
+        c.fy = fy;
+        c.cx = cx;
+        c.cy = cy;
+        for (int i = 0; i < 9; ++i) c.rot[i] = rot[i];
+        for (int i = 0; i < 3; ++i) c.trans[i] = trans[i];
+        c.near_plane = near_plane;
+        return c;
+    }
+};
+
+// Host fp32 scene in the C-ABI layout: position 3K (world mean), quat 4K (w,x,y,z), log_scale 2K,
+// opacity_logit K, grid K * 3n^2 in (i_u, i_v, channel) order.
+struct PinholeScene {
+    std::int64_t count = 0;
+    int n = 1;
+    double sigma = 0.5;
+    std::vector<float> position, quat, log_scale, opacity_logit, grid;
+};
+
+struct StepConfig {
+    LearningRates lrs;
+    AdamConfig adam;
+    RasterConfig raster;
+    bool sharded_adam = true;  // reduce-scatter + Adam on the rank's slice + all-gather; else all-reduce
+};
+
+namespace detail {
+inline void check(gb_status st, const char* where) { gbil_b200::detail::check(st, where); }
+
+// flat groups, 16-B aligned, padded to a multiple of 4 * nranks floats (one collective covers them)
+struct FlatLayout {
+    std::int64_t position = 0, quat = 0, log_scale = 0, opacity = 0, grid = 0, total = 0;
+    FlatLayout(std::int64_t K, int n, int nranks) {
+        auto up = [](std::int64_t v) { return (v + 3) & ~std::int64_t(3); };
+        position = 0;
+        quat = up(position + 3 * K);
+        log_scale = up(quat + 4 * K);
+        opacity = up(log_scale + 2 * K);
+        grid = up(opacity + K);
+        const std::int64_t end = grid + K * 3 * n * n, q = 4 * nranks;
+        total = (end + q - 1) / q * q;
+    }
+};
+
+struct Buffer {  // device memory of one rank's context
+    gb_context* ctx = nullptr;
+    void* ptr = nullptr;
+    Buffer() = default;
+    Buffer(gb_context* c, std::size_t bytes) : ctx(c) { check(gb_device_alloc(c, bytes, &ptr), "gb_device_alloc"); }
+    Buffer(const Buffer&) = delete;
+    Buffer& operator=(const Buffer&) = delete;
+    ~Buffer() {
+        if (ptr) gb_device_free(ctx, ptr);
+    }
+    float* f() const { return static_cast<float*>(ptr); }
+};
+}  // namespace detail
+
+// One rank: a GPU, its views, a parameter replica, the flat gradient buffer and its slice of Adam.
+class Rank {
+public:
+    Rank(int device, const PinholeScene& scene, std::vector<PinholeCamera> cameras, std::vector<int> views,
+         const StepConfig& cfg, int nranks, int rank)
+        : cams_(std::move(cameras)), views_(std::move(views)), cfg_(cfg), nranks_(nranks), rank_(rank),
+          layout_(scene.count, scene.n, nranks) {
+        cfg_.lrs.validate();
+        detail::check(gb_context_create(device, &ctx_), "gb_context_create");
+        const std::int64_t K = scene.count, n = scene.n, T = layout_.total;
+        K_ = K;
+        n_ = scene.n;
+        sigma_ = scene.sigma;
+        params_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * T);
+        grads_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * T);
+        detail::check(gb_memset_device(ctx_, params_->ptr, 0, sizeof(float) * T), "gb_memset_device");
+        auto put = [&](std::int64_t off, const std::vector<float>& v, std::int64_t want, const char* what) {
+            if (static_cast<std::int64_t>(v.size()) != want)
+                throw std::invalid_argument(std::string("PinholeScene: wrong size of ") + what);
+            detail::check(gb_copy_h2d(ctx_, params_->f() + off, v.data(), sizeof(float) * v.size(), 1), "gb_copy_h2d");
+        };
+        put(layout_.position, scene.position, 3 * K, "position");
+        put(layout_.quat, scene.quat, 4 * K, "quat");
+        put(layout_.log_scale, scene.log_scale, 2 * K, "log_scale");
+        put(layout_.opacity, scene.opacity_logit, K, "opacity_logit");
+        put(layout_.grid, scene.grid, K * 3 * n * n, "grid");
+        // this rank's slice of the flat buffer and its Adam moments
+        S_ = cfg_.sharded_adam ? T / nranks : T;
+        lo_ = cfg_.sharded_adam ? rank * S_ : 0;
+        m_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * S_);
+        v_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * S_);
+        detail::check(gb_memset_device(ctx_, m_->ptr, 0, sizeof(float) * S_), "gb_memset_device");
+        detail::check(gb_memset_device(ctx_, v_->ptr, 0, sizeof(float) * S_), "gb_memset_device");
+        if (cfg_.sharded_adam && nranks > 1) gshard_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * S_);
+        flag_ = std::make_unique<detail::Buffer>(ctx_, 16);
+        loss_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * std::max<std::size_t>(1, views_.size()));
+        detail::check(gb_binning_create(ctx_, &bin_), "gb_binning_create");
+        build_segments();
+    }
+    Rank(const Rank&) = delete;
+    Rank& operator=(const Rank&) = delete;
+    ~Rank() {
+        if (bin_) gb_binning_destroy(bin_);
+        params_.reset();
+        grads_.reset();
+        m_.reset();
+        v_.reset();
+        gshard_.reset();
+        flag_.reset();
+        loss_.reset();
+        if (ctx_) gb_context_destroy(ctx_);
+    }
+
+    gb_context* context() const { return ctx_; }
+    void attach(gb_comm* c) { comm_ = c; }
+    const std::vector<int>& views() const { return views_; }
+
+    // One step over this rank's views; targets[i] is view i's HWC fp32 target on this rank's device.
+    // Returns the sum of the views' mean-L1 losses (one host read per step, after the update is queued).
+    double step(const std::vector<const float*>& targets) {
+        if (targets.size() != views_.size()) throw std::invalid_argument("step: one target per owned view");
+        const std::int64_t T = layout_.total;
+        detail::check(gb_memset_device(ctx_, grads_->ptr, 0, sizeof(float) * T), "step");
+        detail::check(gb_memset_device(ctx_, loss_->ptr, 0, sizeof(float) * std::max<std::size_t>(1, views_.size())),
+                      "step");
+        const gb_splats s = splats();
+        gb_grads g = view_of(grads_->f());
+        const gb_raster_config rc{cfg_.raster.tile_size, cfg_.raster.threads, cfg_.raster.cutoff_radius,
+                                  cfg_.raster.alpha_skip, cfg_.raster.early_stop_transmittance};
+        for (std::size_t i = 0; i < views_.size(); ++i) {  // train.hpp:191-199 per view
+            const gb_camera cam = cams_.at(views_[i]).to_c();
+            const float scale = 1.0f / (3.0f * cam.width * cam.height);  // mean L1
+            detail::check(gb_build_binning(ctx_, &s, &cam, &rc, bin_), "step: build_binning");
+            detail::check(gb_render_loss_backward(ctx_, &s, &cam, bin_, targets[i], GB_LOSS_L1, scale, nullptr,
+                                                  nullptr, loss_->f() + i, &g),
+                          "step: render_loss_backward");
+        }
+        update();
+        std::vector<float> l(std::max<std::size_t>(1, views_.size()));
+        detail::check(gb_copy_d2h(ctx_, l.data(), loss_->ptr, sizeof(float) * l.size(), 1), "step");
+        double sum = 0.0;
+        for (std::size_t i = 0; i < views_.size(); ++i) sum += l[i];
+        if (comm_) detail::check(gb_comm_check(comm_), "step: NCCL");
+        return sum;
+    }
+
+    std::vector<float> download_params() const {  // flat layout
+        std::vector<float> out(static_cast<std::size_t>(layout_.total));
+        detail::check(gb_copy_d2h(ctx_, out.data(), params_->ptr, sizeof(float) * out.size(), 1), "download");
+        return out;
+    }
+    std::vector<float> download_grads() const {  // the summed gradients of the last step (all-reduce mode)
+        std::vector<float> out(static_cast<std::size_t>(layout_.total));
+        detail::check(gb_copy_d2h(ctx_, out.data(), grads_->ptr, sizeof(float) * out.size(), 1), "download");
+        return out;
+    }
+    const detail::FlatLayout& layout() const { return layout_; }
+    std::int64_t adam_t() const { return t_; }
+
+private:
+    gb_splats splats() const {
+        gb_splats s{};
+        s.count = K_;
+        s.grid.n = n_;
+        s.grid.sigma = sigma_;
+        const float* p = params_->f();
+        s.position = p + layout_.position;
+        s.quat = p + layout_.quat;
+        s.log_scale = p + layout_.log_scale;
+        s.opacity_logit = p + layout_.opacity;
+        s.grid_values = p + layout_.grid;
+        return s;
+    }
+    gb_grads view_of(float* base) const {
+        return gb_grads{base + layout_.position, nullptr, nullptr, base + layout_.quat, base + layout_.log_scale,
+                        base + layout_.opacity, base + layout_.grid};
+    }
+    void build_segments() {  // optim.hpp:96-117 groups intersected with this rank's slice
+        struct G {
+            std::int64_t off, len;
+            int group;
+        };
+        const G groups[] = {{layout_.position, 3 * K_, 0},
+                            {layout_.quat, 4 * K_, 1},
+                            {layout_.log_scale, 2 * K_, 2},
+                            {layout_.opacity, K_, 3},
+                            {layout_.grid, K_ * 3 * n_ * n_, 4}};
+        const bool shard = cfg_.sharded_adam && nranks_ > 1;
+        float* gbase = shard ? gshard_->f() : grads_->f() + lo_;
+        for (const G& gr : groups) {
+            const std::int64_t a = std::max(gr.off, lo_), b = std::min(gr.off + gr.len, lo_ + S_);
+            if (a >= b) continue;
+            segs_.push_back(gb_adam_segment{params_->f() + a, gbase + (a - lo_), m_->f() + (a - lo_),
+                                            v_->f() + (a - lo_), b - a, gr.group, 0});
+        }
+    }
+    void update() {
+        const std::int64_t T = layout_.total;
+        const bool multi = comm_ && nranks_ > 1;
+        if (multi) {
+            if (cfg_.sharded_adam)
+                detail::check(gb_reduce_scatter_grads(ctx_, comm_, grads_->f(), gshard_->f(), S_), "step: reduce-scatter");
+            else
+                detail::check(gb_allreduce_grads(ctx_, comm_, grads_->f(), T), "step: all-reduce");
+        }
+        detail::check(gb_copy_h2d(ctx_, flag_->ptr, &kClear, sizeof(kClear), 0), "step");
+        gb_adam_state st{t_, cfg_.adam.beta1, cfg_.adam.beta2, cfg_.adam.epsilon, {}, {}};
+        const gb_learning_rates l = cfg_.lrs.to_c();
+        auto* flag = static_cast<int64_t*>(flag_->ptr);
+        detail::check(gb_adam_segments(ctx_, 0, segs_.data(), static_cast<int32_t>(segs_.size()), &st, &l, flag),
+                      "step: adam");
+        if (multi) detail::check(gb_allreduce_flag_min(ctx_, comm_, flag), "step: flag");  // optim.hpp:81-83, agreed
+        detail::check(gb_adam_segments(ctx_, 1, segs_.data(), static_cast<int32_t>(segs_.size()), &st, &l, flag),
+                      "step: adam");
+        if (multi && cfg_.sharded_adam)
+            detail::check(gb_all_gather_params(ctx_, comm_, params_->f() + lo_, params_->f(), S_), "step: all-gather");
+        int64_t code = 0;
+        detail::check(gb_copy_d2h(ctx_, &code, flag_->ptr, sizeof(code), 1), "step");
+        if (code != kClear)
+            throw NonFiniteGradient("adam_step: non-finite gradient in group " + std::to_string(code >> 48) +
+                                    "; no parameter was updated");
+        t_ = st.t;
+    }
+
+    static constexpr int64_t kClear = GB_ADAM_FLAG_CLEAR;
+    gb_context* ctx_ = nullptr;
+    gb_comm* comm_ = nullptr;
+    gb_binning* bin_ = nullptr;
+    std::vector<PinholeCamera> cams_;
+    std::vector<int> views_;
+    StepConfig cfg_;
+    int nranks_, rank_;
+    detail::FlatLayout layout_;
+    std::int64_t K_ = 0, S_ = 0, lo_ = 0, t_ = 0;
+    int n_ = 1;
+    double sigma_ = 0.5;
+    std::unique_ptr<detail::Buffer> params_, grads_, m_, v_, gshard_, flag_, loss_;
+    std::vector<gb_adam_segment> segs_;
+};
+
+// Views split into contiguous near-equal blocks (strong scaling), as train.py shard_views.
+inline std::vector<int> shard_views(int n_views, int rank, int nranks) {
+    std::vector<int> v;
+    for (int i = n_views * rank / nranks; i < n_views * (rank + 1) / nranks; ++i) v.push_back(i);
+    return v;
+}
+
+// Single-process driver: one rank per device, one host thread each, communicators from ncclCommInitAll.
+// targets(view) gives view's HWC fp32 host target.  Returns every step's loss (summed over all views).
+template <typename TargetFn>
+std::vector<double> train(const std::vector<int>& devices, const PinholeScene& scene,
+                          const std::vector<PinholeCamera>& cameras, TargetFn targets, int steps,
+                          const StepConfig& cfg = {}, std::vector<std::vector<float>>* final_params = nullptr) {
+    const int N = static_cast<int>(devices.size());
+    if (N < 1) throw std::invalid_argument("train: no devices");
+    std::vector<std::unique_ptr<Rank>> ranks;
+    for (int r = 0; r < N; ++r)
+        ranks.push_back(std::make_unique<Rank>(devices[r], scene, cameras,
+                                               shard_views(static_cast<int>(cameras.size()), r, N), cfg, N, r));
+    std::vector<gb_context*> ctxs;
+    for (auto& r : ranks) ctxs.push_back(r->context());
+    std::vector<gb_comm*> comms(N, nullptr);
+    detail::check(gb_comm_init_all(ctxs.data(), N, comms.data()), "train: ncclCommInitAll");
+    for (int r = 0; r < N; ++r) ranks[r]->attach(comms[r]);
+    // per-rank device targets, uploaded once
+    std::vector<std::vector<std::unique_ptr<detail::Buffer>>> tbuf(N);
+    std::vector<std::vector<const float*>> tptr(N);
+    for (int r = 0; r < N; ++r)
+        for (int v : ranks[r]->views()) {
+            const std::vector<float> host = targets(v);
+            tbuf[r].push_back(std::make_unique<detail::Buffer>(ranks[r]->context(), sizeof(float) * host.size()));
+            detail::check(gb_copy_h2d(ranks[r]->context(), tbuf[r].back()->ptr, host.data(), sizeof(float) * host.size(), 1),
+                          "train: targets");
+            tptr[r].push_back(tbuf[r].back()->f());
+        }
+    std::vector<double> losses(steps, 0.0);
+    std::vector<std::vector<double>> per(N, std::vector<double>(steps, 0.0));
+    std::vector<std::exception_ptr> errs(N);
+    std::vector<std::thread> threads;
+    for (int r = 0; r < N; ++r)
+        threads.emplace_back([&, r] {
+            try {
+                for (int s = 0; s < steps; ++s) per[r][s] = ranks[r]->step(tptr[r]);
+            } catch (...) {
+                errs[r] = std::current_exception();
+            }
+        });
+    for (auto& t : threads) t.join();
+    for (auto& e : errs)
+        if (e) {
+            for (auto* c : comms) gb_comm_destroy(c);
+            std::rethrow_exception(e);
+        }
+    for (int s = 0; s < steps; ++s)
+        for (int r = 0; r < N; ++r) losses[s] += per[r][s];
+    if (final_params)
+        for (auto& r : ranks) final_params->push_back(r->download_params());
+    for (int r = 0; r < N; ++r) tbuf[r].clear();
+    for (auto* c : comms) gb_comm_destroy(c);
+    return losses;
+}
+
+}  // namespace multiview
 
 }  // namespace gbil_b200

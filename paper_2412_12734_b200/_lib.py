@@ -22,11 +22,14 @@ GB_NONFINITE = 5
 ADAM_FLAG_CLEAR = 0x7FFFFFFFFFFFFFFF  # GB_ADAM_FLAG_CLEAR
 GB_NOT_SUPPORTED = 6
 GB_IO_ERROR = 7
+GB_NCCL_ERROR = 8
+COMM_ID_BYTES = 128
 
 MODE_ORTHO = 0
 MODE_PINHOLE = 1
 
-KERNEL_NAMES = ("project", "scan", "duplicate", "sort", "ranges", "forward", "backward", "chain", "loss", "adam", "fused")
+KERNEL_NAMES = ("project", "scan", "duplicate", "sort", "ranges", "forward", "backward", "chain", "loss", "adam", "fused",
+                "collective")
 
 
 class GridConfig(C.Structure):
@@ -220,6 +223,16 @@ _SIGS = {
     "gb_uniform_fill": (C.c_int, [C.c_uint64, C.c_int64, P]),
     "gb_rng_uniform": (C.c_int, [C.c_uint64, C.c_int64, P]),
     "gb_rng_normal": (C.c_int, [C.c_uint64, C.c_int64, C.c_double, C.c_double, P]),
+    "gb_comm_unique_id": (C.c_int, [P]),
+    "gb_comm_init_rank": (C.c_int, [P, C.c_int32, P, C.c_int32, C.POINTER(P)]),
+    "gb_comm_init_all": (C.c_int, [P, C.c_int32, P]),
+    "gb_comm_destroy": (C.c_int, [P]),
+    "gb_comm_info": (C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "gb_comm_check": (C.c_int, [P]),
+    "gb_allreduce_grads": (C.c_int, [P, P, P, C.c_int64]),
+    "gb_reduce_scatter_grads": (C.c_int, [P, P, P, P, C.c_int64]),
+    "gb_all_gather_params": (C.c_int, [P, P, P, P, C.c_int64]),
+    "gb_allreduce_flag_min": (C.c_int, [P, P, P]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -265,6 +278,10 @@ class SplatIoError(GBError):
     """serialize.hpp:23-25"""
 
 
+class NcclError(GBError):
+    """a collective of the view-sharded step failed (GB_NCCL_ERROR)"""
+
+
 def check(status: int, where: str) -> None:
     if status == GB_OK:
         return
@@ -276,4 +293,6 @@ def check(status: int, where: str) -> None:
         raise NonFinite(status, where)
     if status == GB_IO_ERROR:
         raise SplatIoError(status, where)
+    if status == GB_NCCL_ERROR:
+        raise NcclError(status, where)
     raise GBError(status, where)

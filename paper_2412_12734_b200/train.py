@@ -39,8 +39,62 @@ def shard_views(n_views: int, rank: int, world: int, per_rank: Optional[int] = N
     return list(range(lo, hi))
 
 
-def reduce_gradients(grads: GradientBuffer, process_group=None) -> None:
+class Communicator:
+    """The step's NCCL communicator, created and driven through the C-ABI (gb_comm_init_rank,
+    gb_allreduce_grads, gb_reduce_scatter_grads, gb_all_gather_params, gb_allreduce_flag_min) on the
+    current stream's context; only its unique id travels over the torch process group."""
+
+    def __init__(self, device, process_group=None):
+        dist = torch.distributed
+        self.world = dist.get_world_size(process_group)
+        self.rank = dist.get_rank(process_group)
+        uid = (C.c_uint8 * _lib.COMM_ID_BYTES)()
+        if self.rank == 0:
+            check(lib.gb_comm_unique_id(uid), "gb_comm_unique_id")
+        obj = [bytes(uid)]
+        src = 0 if process_group is None else dist.get_global_rank(process_group, 0)
+        dist.broadcast_object_list(obj, src=src, group=process_group)
+        uid = (C.c_uint8 * _lib.COMM_ID_BYTES).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        check(lib.gb_comm_init_rank(context(device).handle, self.world, uid, self.rank, C.byref(h)),
+              "gb_comm_init_rank")
+        self.handle = h
+
+    @staticmethod
+    def wanted(process_group=None) -> bool:
+        """NCCL through the C-ABI when the ranks are CUDA processes (backend nccl); gloo/fake groups (CPU
+        tests, code-path checks) keep torch.distributed's collectives."""
+        dist = torch.distributed
+        return (dist.is_available() and dist.is_initialized() and dist.get_world_size(process_group) > 1
+                and dist.get_backend(process_group) == "nccl")
+
+    def all_reduce(self, t: torch.Tensor) -> None:
+        check(lib.gb_allreduce_grads(context(t.device).handle, self.handle, t.data_ptr(), t.numel()),
+              "gb_allreduce_grads")
+
+    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        check(lib.gb_reduce_scatter_grads(context(out.device).handle, self.handle, inp.data_ptr(), out.data_ptr(),
+                                          out.numel()), "gb_reduce_scatter_grads")
+
+    def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        check(lib.gb_all_gather_params(context(out.device).handle, self.handle, inp.data_ptr(), out.data_ptr(),
+                                       inp.numel()), "gb_all_gather_params")
+
+    def min_flag(self, flag: torch.Tensor) -> None:
+        check(lib.gb_allreduce_flag_min(context(flag.device).handle, self.handle, flag.data_ptr()),
+              "gb_allreduce_flag_min")
+
+    def close(self) -> None:
+        if self.handle:
+            lib.gb_comm_destroy(self.handle)
+            self.handle = None
+
+
+def reduce_gradients(grads: GradientBuffer, process_group=None, comm: "Communicator" = None) -> None:
     """The step's one collective: sum the flat gradient buffer over all ranks (NCCL on GPUs)."""
+    if comm is not None:
+        comm.all_reduce(grads.flat)
+        return
     if torch.distributed.is_available() and torch.distributed.is_initialized():
         if torch.distributed.get_world_size(process_group) > 1:
             torch.distributed.all_reduce(grads.flat, op=torch.distributed.ReduceOp.SUM, group=process_group)
@@ -61,12 +115,13 @@ class ShardedAdam:
     The splats' parameter tensors become views into ``flat`` (same layout as the gradient buffer)."""
 
     def __init__(self, splats: SplatSet, grads: GradientBuffer, state: AdamState, process_group=None,
-                 segment_update=None):
+                 segment_update=None, comm: "Communicator" = None):
         """``segment_update(phase, ranges, state, lrs, flag)``: replaces the gb_adam_segments call --
         a hook for the multi-process CPU tests only (there is no CPU optimiser in the product)."""
         dist = torch.distributed
         self._hook = segment_update
         self.pg = process_group
+        self.comm = comm
         self.world = dist.get_world_size(process_group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(process_group) if self.world > 1 else 0
         if grads.flat.numel() % (4 * self.world):
@@ -120,7 +175,10 @@ class ShardedAdam:
 
         dist = torch.distributed
         if self.world > 1:
-            dist.reduce_scatter_tensor(self.g_shard, self.grads.flat, op=dist.ReduceOp.SUM, group=self.pg)
+            if self.comm is not None:
+                self.comm.reduce_scatter(self.g_shard, self.grads.flat)
+            else:
+                dist.reduce_scatter_tensor(self.g_shard, self.grads.flat, op=dist.ReduceOp.SUM, group=self.pg)
         self.flag.fill_(_lib.ADAM_FLAG_CLEAR)
 
         def fold_veto():  # veto (a device int32, nonzero = skip the update on every rank)
@@ -141,7 +199,10 @@ class ShardedAdam:
                                        self.flag.data_ptr()), "adam_step")
             fold_veto()
             if self.world > 1:
-                dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
+                if self.comm is not None:
+                    self.comm.min_flag(self.flag)
+                else:
+                    dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
             if grid_stream is None or self.world > 1 or not self._grid_segs:
                 check(lib.gb_adam_segments(ctx.handle, 1, self._segs, self._nseg, C.byref(st), C.byref(c_lrs),
                                            self.flag.data_ptr()), "adam_step")
@@ -160,7 +221,10 @@ class ShardedAdam:
                     grid_done.record(grid_stream)
             self.state.t = st.t
         if self.world > 1:
-            dist.all_gather_into_tensor(self.flat, self.flat[self.lo:self.lo + self.S], group=self.pg)
+            if self.comm is not None:
+                self.comm.all_gather(self.flat, self.flat[self.lo:self.lo + self.S])
+            else:
+                dist.all_gather_into_tensor(self.flat, self.flat[self.lo:self.lo + self.S], group=self.pg)
         if check_finite:
             self.raise_if_nonfinite(int(self.flag.item()))
 
@@ -210,7 +274,10 @@ class ViewShardedTrainer:
         # sharded optimiser (reduce-scatter, Adam on 1/world of the parameters, all-gather) or the
         # replicated one (all-reduce, full Adam on every rank)
         self.state = AdamState(splats, adam, moments=not sharded_adam)
-        self.opt = ShardedAdam(splats, self.grads, self.state, process_group) if sharded_adam else None
+        # the gradient exchange runs through the C-ABI's NCCL layer on CUDA ranks (torch's for gloo/fake)
+        self.comm = Communicator(splats.device, process_group) if Communicator.wanted(process_group) else None
+        self.opt = (ShardedAdam(splats, self.grads, self.state, process_group, comm=self.comm) if sharded_adam
+                    else None)
         # world size 1: the texel half of Adam (90 % of it) runs on a side stream and overlaps the next
         # step's binning; each lane waits for it (and the texel-gradient zeroing that follows it) before
         # its first forward compositor.  Texels read on another stream right after step() returns need
@@ -439,7 +506,7 @@ class ViewShardedTrainer:
             self.opt.step(self.lrs, check_finite=self.check_finite,
                           grid_stream=self._adam_stream, grid_done=self._grid_done)
             return
-        reduce_gradients(self.grads, self.pg)
+        reduce_gradients(self.grads, self.pg, self.comm)
         adam_step(self.splats, self.grads, self.state, self.lrs, check_finite=self.check_finite)
 
     def step(self, targets: Sequence[torch.Tensor]) -> torch.Tensor:
