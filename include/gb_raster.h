@@ -314,6 +314,10 @@ typedef struct {
     int32_t _pad;
 } gb_adam_segment;
 #define GB_ADAM_FLAG_CLEAR 0x7fffffffffffffffLL
+#define GB_ADAM_FLAG_VETO (7LL << 48) /* a vetoed step: below every clear value, above every non-finite code */
+/* *flag = GB_ADAM_FLAG_VETO if veto != NULL and *veto != 0 (a device int32, e.g. the binning's overflow
+ * flag: skip this update on every rank), else GB_ADAM_FLAG_CLEAR -- on the stream, before phase 0. */
+GB_API gb_status gb_adam_flag_init(gb_context *ctx, int64_t *flag, const int32_t *veto);
 GB_API gb_status gb_adam_segments(gb_context *ctx, int32_t phase, const gb_adam_segment *seg, int32_t nseg,
                                   gb_adam_state *state, const gb_learning_rates *lrs, int64_t *flag);
 

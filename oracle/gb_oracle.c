@@ -547,8 +547,8 @@ typedef struct {
     /* backward */
     const double *image_grad;
     const uint8_t *kink_px_in;
-    double **partials, **mags, **slacks;
-    int want_mag, want_slack;
+    double **partials, **mags, **slacks, **tmags;
+    int want_mag, want_slack, want_tmag;
     size_t stride;
 } raster_ctx_t;
 
@@ -797,8 +797,10 @@ static void backward_tile(void *vctx, int tile) {
     double *pmag = c->want_mag ? calloc((size_t)len * stride, sizeof(double)) : NULL;
     double *pslk = c->want_slack ? calloc((size_t)len * stride, sizeof(double)) : NULL;
     c->partials[tile] = partial;
+    double *ptm = c->want_tmag ? calloc((size_t)len * stride, sizeof(double)) : NULL;
     if (pmag) c->mags[tile] = pmag;
     if (pslk) c->slacks[tile] = pslk;
+    if (ptm) c->tmags[tile] = ptm;
     const int ts = cfg->tile_size;
     const int tx = tile % c->b->tiles_x, ty = tile / c->b->tiles_x;
     const int x0 = tx * ts, y0 = ty * ts;
@@ -821,6 +823,22 @@ static void backward_tile(void *vctx, int tile) {
             const double px = x + 0.5, py = y + 0.5;
             double t = c->trans[p];
             const double t_final = t;
+            /* tmag: the transmittance-chain term of the fp32 error model.  Every composited entry j scales T by
+             * (1 - alpha_j) whose fp32 value carries a relative error ~ eps * alpha_j / (1 - alpha_j) (alpha_j
+             * itself is exact to a few eps), so the relative error of any T of this pixel is bounded by
+             * O(eps) * kappa, kappa = sum_j alpha_j / (1 - alpha_j), and it is shared -- not averaged out -- by
+             * the pixel's terms and by neighbouring pixels that see the same splats in front. */
+            double kappa = 0.0;
+            if (ptm) {
+                for (int32_t rank = 0; rank <= last; ++rank) {
+                    const geom_t *g = &c->geom[list[rank]];
+                    double u, v, a[3], b[3], cz = 0.0;
+                    if (!eval_uv(c, g, px, py, &u, &v, a, b, &cz)) continue;
+                    const double alpha = dmin(g->alpha_k * gaussian_weight(u, v), kMaxAlpha);
+                    if (alpha < cfg->alpha_skip) continue;
+                    kappa += alpha / (1.0 - alpha);
+                }
+            }
             double behind[3] = {c->cam->background[0], c->cam->background[1], c->cam->background[2]};
             if (pslk && (px_flag & 1) && kk && cfg->alpha_skip > 0.0 && !(cfg->early_stop > 0.0 && t < cfg->early_stop)) {
                 /* entries skipped just below the threshold AFTER the last composited one: fp32 may composite
@@ -891,7 +909,7 @@ static void backward_tile(void *vctx, int tile) {
                         rec[6 + j] += -dxn * ga[j] - dyn * gb[j];
                     }
                 }
-                if (pmag || pslk) {
+                if (pmag || pslk || ptm) {
                     double uh_t, vh_t;
                     uv_hat_tex_abs(n, sigma, u, v, gridk, c_hat, &uh_t, &vh_t);
                     double ah = 0.0;
@@ -905,6 +923,12 @@ static void backward_tile(void *vctx, int tile) {
                         double *rm = pmag + (size_t)rank * stride;
                         for (size_t j = 0; j < gs; ++j) rm[j] += d[j];
                         tex_abs(n, sigma, u, v, c_hat, rm + gs);
+                    }
+                    if (ptm) {
+                        double *rt = ptm + (size_t)rank * stride;
+                        for (size_t j = 0; j < gs; ++j) rt[j] += kappa * d[j];
+                        const double ck[3] = {kappa * c_hat[0], kappa * c_hat[1], kappa * c_hat[2]};
+                        tex_abs(n, sigma, u, v, ck, rt + gs);
                     }
                     if (pslk) {
                         double *rs = pslk + (size_t)rank * stride;
@@ -1104,6 +1128,13 @@ static void reduce_records(const orc_camera *cam, const orc_binning *b, const ge
 int orc_render_backward(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, const orc_binning *b,
                         const double *trans, const int32_t *last, const double *image_grad, orc_grads *gr,
                         const uint8_t *kink_px, orc_grads *mag, orc_grads *slack, const orc_kink *kink) {
+    return orc_render_backward_tm(s, cam, cfg, b, trans, last, image_grad, gr, kink_px, mag, slack, NULL, kink);
+}
+
+int orc_render_backward_tm(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, const orc_binning *b,
+                           const double *trans, const int32_t *last, const double *image_grad, orc_grads *gr,
+                           const uint8_t *kink_px, orc_grads *mag, orc_grads *slack, orc_grads *tmag,
+                           const orc_kink *kink) {
     int st = validate(cam, cfg, s);
     if (st) return st;
     if (b->tiles_x != (cam->width + cfg->tile_size - 1) / cfg->tile_size ||
@@ -1116,6 +1147,7 @@ int orc_render_backward(const orc_splats *s, const orc_camera *cam, const orc_co
     zero_grads(gr, K, tex_stride, pin);
     if (mag) zero_grads(mag, K, tex_stride, pin);
     if (slack) zero_grads(slack, K, tex_stride, pin);
+    if (tmag) zero_grads(tmag, K, tex_stride, pin);
 
     geom_t *geom = build_all_geom(s, cam);
     const int nt = b->tiles_x * b->tiles_y;
@@ -1123,11 +1155,13 @@ int orc_render_backward(const orc_splats *s, const orc_camera *cam, const orc_co
     double **partials = calloc(ntc, sizeof(double *));
     double **mags = mag ? calloc(ntc, sizeof(double *)) : NULL;
     double **slacks = slack ? calloc(ntc, sizeof(double *)) : NULL;
-    if (!geom || !partials || (mag && !mags) || (slack && !slacks)) {
+    double **tmags = tmag ? calloc(ntc, sizeof(double *)) : NULL;
+    if (!geom || !partials || (mag && !mags) || (slack && !slacks) || (tmag && !tmags)) {
         free(geom);
         free(partials);
         free(mags);
         free(slacks);
+        free(tmags);
         return ORC_OOM;
     }
     raster_ctx_t c;
@@ -1147,15 +1181,19 @@ int orc_render_backward(const orc_splats *s, const orc_camera *cam, const orc_co
     c.slacks = slacks;
     c.want_mag = mag != NULL;
     c.want_slack = slack != NULL;
+    c.tmags = tmags;
+    c.want_tmag = tmag != NULL;
     c.stride = geom_slots(cam) + tex_stride;
     for_each_tile(nt, cfg->threads, backward_tile, &c);
 
     reduce_records(cam, b, geom, K, tex_stride, c.stride, partials, gr, 0);
     if (mag) reduce_records(cam, b, geom, K, tex_stride, c.stride, mags, mag, 1);
     if (slack) reduce_records(cam, b, geom, K, tex_stride, c.stride, slacks, slack, 1);
+    if (tmag) reduce_records(cam, b, geom, K, tex_stride, c.stride, tmags, tmag, 1);
     free(partials);
     free(mags);
     free(slacks);
+    free(tmags);
     free(geom);
     return ORC_OK;
 }

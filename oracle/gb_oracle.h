@@ -118,6 +118,13 @@ int orc_render_backward(const orc_splats *s, const orc_camera *cam, const orc_co
                         const double *trans, const int32_t *last, const double *image_grad, orc_grads *g,
                         const uint8_t *kink_px, orc_grads *mag, orc_grads *slack, const orc_kink *kink);
 
+/* ... and tmag (nullable): the per-entry sum of |terms| * kappa, kappa = sum over the pixel's composited
+ * entries of alpha / (1 - alpha) -- the transmittance-chain term of the fp32 error model. */
+int orc_render_backward_tm(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, const orc_binning *b,
+                           const double *trans, const int32_t *last, const double *image_grad, orc_grads *g,
+                           const uint8_t *kink_px, orc_grads *mag, orc_grads *slack, orc_grads *tmag,
+                           const orc_kink *kink);
+
 int orc_render_naive(const orc_splats *s, const orc_camera *cam, double *color, double *trans);
 
 /* Central finite differences of L = sum(weights * render_naive(...).color)

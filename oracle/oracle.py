@@ -85,6 +85,7 @@ def oracle_lib():
         L.orc_project.argtypes = [P, P, P, P, P]
         L.orc_render_forward.argtypes = [P, P, P, C.POINTER(OrcBinning), P, P, P, P, P]
         L.orc_render_backward.argtypes = [P, P, P, C.POINTER(OrcBinning), P, P, P, P, P, P, P, P]
+        L.orc_render_backward_tm.argtypes = [P, P, P, C.POINTER(OrcBinning), P, P, P, P, P, P, P, P, P]
         L.orc_render_naive.argtypes = [P, P, P, P]
         L.orc_gradient_fd.argtypes = [P, P, P, C.c_double, P]
         L.orc_uv_to_grid.argtypes = [C.c_double, C.c_double, C.c_int, C.c_double, P, P, P, P]
@@ -270,6 +271,12 @@ def render_forward(scene: Scene64, cam: Cam, cfg: Cfg, binning, kink=DEFAULT_KIN
 
 def render_backward(scene: Scene64, cam: Cam, cfg: Cfg, binning, fwd: dict, image_grad, kink=DEFAULT_KINK,
                     want_mag: bool = True):
+    g, mag, slack, _ = render_backward_tm(scene, cam, cfg, binning, fwd, image_grad, kink, want_mag, False)
+    return g, mag, slack
+
+
+def render_backward_tm(scene: Scene64, cam: Cam, cfg: Cfg, binning, fwd: dict, image_grad, kink=DEFAULT_KINK,
+                       want_mag: bool = True, want_tmag: bool = True):
     """raster.hpp:277-387 in fp64 -> (grads, mag, slack) dicts.
 
     mag[f]   : sum of |terms| per gradient entry (fp32 accumulation-error scale)
@@ -281,6 +288,7 @@ def render_backward(scene: Scene64, cam: Cam, cfg: Cfg, binning, fwd: dict, imag
     g = scene.zeros_like()
     mag = scene.zeros_like() if want_mag else None
     slack = scene.zeros_like() if want_mag else None
+    tmag = scene.zeros_like() if want_tmag else None
     ig = np.ascontiguousarray(image_grad, np.float64)
     trans = np.ascontiguousarray(fwd["trans"], np.float64)
     last = np.ascontiguousarray(fwd["last"], np.int32)
@@ -290,11 +298,13 @@ def render_backward(scene: Scene64, cam: Cam, cfg: Cfg, binning, fwd: dict, imag
     gc = _grads_c(g)
     mc = _grads_c(mag) if mag is not None else None
     sc = _grads_c(slack) if slack is not None else None
-    _check(L.orc_render_backward(C.byref(s), C.byref(c), C.byref(k), C.byref(b), trans.ctypes.data,
-                                 last.ctypes.data, ig.ctypes.data, C.byref(gc), kpx.ctypes.data,
-                                 C.byref(mc) if mc is not None else None, C.byref(sc) if sc is not None else None,
-                                 C.byref(kk) if kk is not None else None), "orc_render_backward")
-    return g, mag, slack
+    tc = _grads_c(tmag) if tmag is not None else None
+    _check(L.orc_render_backward_tm(C.byref(s), C.byref(c), C.byref(k), C.byref(b), trans.ctypes.data,
+                                    last.ctypes.data, ig.ctypes.data, C.byref(gc), kpx.ctypes.data,
+                                    C.byref(mc) if mc is not None else None, C.byref(sc) if sc is not None else None,
+                                    C.byref(tc) if tc is not None else None,
+                                    C.byref(kk) if kk is not None else None), "orc_render_backward")
+    return g, mag, slack, tmag
 
 
 def project(scene: Scene64, cam: Cam, cfg: Cfg):

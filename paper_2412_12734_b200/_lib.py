@@ -20,6 +20,7 @@ GB_CUDA_ERROR = 3
 GB_OOM = 4
 GB_NONFINITE = 5
 ADAM_FLAG_CLEAR = 0x7FFFFFFFFFFFFFFF  # GB_ADAM_FLAG_CLEAR
+ADAM_FLAG_VETO = 7 << 48  # GB_ADAM_FLAG_VETO
 GB_NOT_SUPPORTED = 6
 GB_IO_ERROR = 7
 GB_NCCL_ERROR = 8
@@ -223,6 +224,7 @@ _SIGS = {
     "gb_uniform_fill": (C.c_int, [C.c_uint64, C.c_int64, P]),
     "gb_rng_uniform": (C.c_int, [C.c_uint64, C.c_int64, P]),
     "gb_rng_normal": (C.c_int, [C.c_uint64, C.c_int64, C.c_double, C.c_double, P]),
+    "gb_adam_flag_init": (C.c_int, [P, P, P]),
     "gb_comm_unique_id": (C.c_int, [P]),
     "gb_comm_init_rank": (C.c_int, [P, C.c_int32, P, C.c_int32, C.POINTER(P)]),
     "gb_comm_init_all": (C.c_int, [P, C.c_int32, P]),

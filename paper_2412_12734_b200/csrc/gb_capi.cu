@@ -42,6 +42,7 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
 #ifdef GB_PARITY_F64
 cudaError_t launch_add_f64(const double* src, float* dst, int64_t n, cudaStream_t st);
 #endif
+cudaError_t launch_adam_flag_init(int64_t* flag, const int32_t* veto, cudaStream_t st);
 cudaError_t launch_loss(int kind, const float* color, const float* target, int64_t n, float scale, float* grad,
                         float* loss, int sm_count, cudaStream_t st);
 cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned long long* bad, int sm_count,
@@ -1136,6 +1137,15 @@ gb_status gb_adam_step(gb_context* ctx, int32_t mode, int64_t count, int32_t n, 
                                        ctx->sm_count, stream));
         ctx->launches++;
     }
+    return GB_OK;
+}
+
+gb_status gb_adam_flag_init(gb_context* ctx, int64_t* flag, const int32_t* veto) {
+    if (!ctx || !flag) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    ProfScope ps(ctx, GB_K_ADAM);
+    GB_CUDA(gb::launch_adam_flag_init(flag, veto, ctx->stream));
+    ctx->launches++;
     return GB_OK;
 }
 

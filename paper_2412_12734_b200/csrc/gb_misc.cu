@@ -113,6 +113,15 @@ __global__ void __launch_bounds__(256) k_adam_update(float* __restrict__ p, cons
         adam_one(p[i], g[i], m[i], v[i], lr, b1, b2, omb1, omb2, eps, inv_bias1, inv_bias2);
 }
 
+__global__ void k_adam_flag_init(long long* __restrict__ flag, const int* __restrict__ veto) {
+    *flag = (veto && *veto) ? GB_ADAM_FLAG_VETO : GB_ADAM_FLAG_CLEAR;
+}
+
+cudaError_t launch_adam_flag_init(int64_t* flag, const int32_t* veto, cudaStream_t st) {
+    k_adam_flag_init<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(flag), veto);
+    return cudaGetLastError();
+}
+
 static unsigned grid_for(int64_t n, int sm_count) {
     int64_t blocks = (n + 255) / 256;
     const int64_t cap = (int64_t)sm_count * 8;

@@ -117,6 +117,15 @@ def all_contexts(device=None) -> list:
     return _Context.all(device if device is not None else "cuda")
 
 
+def memset_(t: torch.Tensor) -> None:
+    """Zero a contiguous device tensor with a stream-ordered memset on the current stream's context
+    (gb_memset_device: a memset node under graph capture, no framework kernel)."""
+    if not t.is_contiguous():
+        raise ValueError("memset_: tensor must be contiguous")
+    check(lib.gb_memset_device(context(t.device).handle, C.c_void_p(t.data_ptr()), 0, t.numel() * t.element_size()),
+          "memset_")
+
+
 def copy_h2d(dst: torch.Tensor, src: torch.Tensor) -> None:
     """Stream-ordered copy of host ``src`` into the front of device ``dst`` on the current stream
     (gb_copy_h2d; asynchronous when ``src`` is pinned)."""

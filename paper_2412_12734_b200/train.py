@@ -26,7 +26,7 @@ from ._lib import check, lib
 
 from .raster import (AdamConfig, AdamState, GradientBuffer, LearningRates, RasterConfig, RenderOutput, SplatSet,
                      StepGraph, TileBinning, adam_step, all_contexts, build_binning, context, l1_loss,
-                     copy_h2d, render_backward, render_forward, render_loss_backward)
+                     copy_h2d, memset_, render_backward, render_forward, render_loss_backward)
 
 
 def shard_views(n_views: int, rank: int, world: int, per_rank: Optional[int] = None) -> List[int]:
@@ -162,8 +162,8 @@ class ShardedAdam:
         self._other_segs = (_lib.AdamSegment * max(1, len(other)))(*other)
         self._names = [f for f in grads.offsets if f != "depth_key"]
 
-    VETO = 7 << 48  # flag value of a vetoed step: below every clear value, above every non-finite code
-    # (group <= 4), so a non-finite gradient still wins the min-reduction
+    VETO = _lib.ADAM_FLAG_VETO  # flag value of a vetoed step: below every clear value, above every non-finite
+    # code (group <= 4), so a non-finite gradient still wins the min-reduction
 
     def step(self, lrs: LearningRates, check_finite: bool = False, grid_stream=None, grid_done=None,
              veto: torch.Tensor = None) -> None:
@@ -179,15 +179,11 @@ class ShardedAdam:
                 self.comm.reduce_scatter(self.g_shard, self.grads.flat)
             else:
                 dist.reduce_scatter_tensor(self.g_shard, self.grads.flat, op=dist.ReduceOp.SUM, group=self.pg)
-        self.flag.fill_(_lib.ADAM_FLAG_CLEAR)
-
-        def fold_veto():  # veto (a device int32, nonzero = skip the update on every rank)
-            if veto is not None:
-                self.flag.copy_(torch.where(veto.to(torch.int64) != 0, self._veto, self.flag))
-
-        if self._hook is not None:
+        if self._hook is not None:  # CPU test stand-in (gloo): torch ops on host tensors
+            self.flag.fill_(_lib.ADAM_FLAG_CLEAR)
             self._hook(0, self, lrs)
-            fold_veto()
+            if veto is not None:  # veto (an int32, nonzero = skip the update on every rank)
+                self.flag.copy_(torch.where(veto.to(torch.int64) != 0, self._veto, self.flag))
             if self.world > 1:
                 dist.all_reduce(self.flag, op=dist.ReduceOp.MIN, group=self.pg)
             self._hook(1, self, lrs)
@@ -195,9 +191,12 @@ class ShardedAdam:
             ctx = context(self.flat.device)
             st = self.state.to_c()
             c_lrs = lrs.to_c()
+            # flag = VETO if the view work vetoed the step (a binning overflow), else CLEAR; phase 0 lowers it
+            # to the first non-finite gradient's code
+            check(lib.gb_adam_flag_init(ctx.handle, self.flag.data_ptr(),
+                                        None if veto is None else veto.data_ptr()), "gb_adam_flag_init")
             check(lib.gb_adam_segments(ctx.handle, 0, self._segs, self._nseg, C.byref(st), C.byref(c_lrs),
                                        self.flag.data_ptr()), "adam_step")
-            fold_veto()
             if self.world > 1:
                 if self.comm is not None:
                     self.comm.min_flag(self.flag)
@@ -314,8 +313,6 @@ class ViewShardedTrainer:
         self.capacity = 0
         self._overflow = torch.zeros(1, dtype=torch.int32, device=dev)
         self._pair_counts = torch.zeros(max(1, len(self.views)), dtype=torch.int32, device=dev)
-        self._pair_sum = torch.zeros(1, dtype=torch.int64, device=dev)
-        self._pair_views = 0
         self.use_graph = graph
         self.graph_host = False  # step_host views as a graph too (H2D copies as memcpy nodes)
         self._graph = None
@@ -369,10 +366,10 @@ class ViewShardedTrainer:
         main = self._lanes[0].stream
         if self.overlap_adam:
             o, _ = self.grads.offsets["grid"]
-            self.grads.flat[:o].zero_()
+            memset_(self.grads.flat[:o])
         else:
-            self.grads.zero_()
-        self.losses.zero_()
+            memset_(self.grads.flat)
+        memset_(self.losses)
         self._step_start.record(main)
         for lane in self._lanes[1:]:
             lane.stream.wait_event(self._step_start)  # parameters updated and gradients zeroed
@@ -384,7 +381,7 @@ class ViewShardedTrainer:
             with torch.cuda.stream(a):
                 check(lib.gb_stream_wait_event(context(self.splats.device).handle,
                                                C.c_void_p(self._grid_done.cuda_event), 1), "gb_stream_wait_event")
-                self.grads.grid.zero_()
+                memset_(self.grads.grid)
                 self._grid_ready.record(a)
             self._waited = set()
 
@@ -444,14 +441,11 @@ class ViewShardedTrainer:
             if not self.capacity or not int(self._overflow.item()):
                 break
             self.overflows += 1
-            self._overflow.zero_()
+            memset_(self._overflow)
             need = int((self._pair_counts[: len(self.views)].to(torch.int64) & 0xFFFFFFFF).max().item())  # uint32
             self._set_capacity(need)
         else:
             raise RuntimeError("view binning kept outgrowing its pair capacity")
-        if self.capacity:
-            self._pair_sum += self._pair_counts[: len(self.views)].sum()
-            self._pair_views += len(self.views)
 
     def _run_views(self, targets: Sequence[torch.Tensor]) -> None:
         self._run_graphed(lambda: self._views(targets), ("dev",) + tuple(t.data_ptr() for t in targets))
@@ -491,15 +485,16 @@ class ViewShardedTrainer:
         self._graphs[key] = g
 
     def pair_stats(self):
-        """(sum of P, views) over the views binned since reset_pair_stats() (roofline bytes)."""
+        """(sum of P, views): over the views of the last step in capacity mode (the builds store their pair
+        counts on the device; nothing is summed inside the step), else over the views binned since
+        reset_pair_stats() (roofline bytes)."""
         if self.capacity:
-            return int(self._pair_sum.item()), self._pair_views
+            nv = len(self.views)
+            return int((self._pair_counts[:nv].to(torch.int64) & 0xFFFFFFFF).sum().item()), nv
         return sum(self.pairs), len(self.pairs)
 
     def reset_pair_stats(self) -> None:
         self.pairs.clear()
-        self._pair_sum.zero_()
-        self._pair_views = 0
 
     def _finish(self) -> None:
         if self.opt is not None:
@@ -531,8 +526,6 @@ class ViewShardedTrainer:
             self._grow_after_overflow()
         else:
             raise RuntimeError("view binning kept outgrowing its pair capacity")
-        self._pair_sum += self._pair_counts[: len(self.views)].sum()
-        self._pair_views += len(self.views)
         if self.check_finite:
             ShardedAdam.raise_if_nonfinite(code)
         return self.losses
@@ -541,7 +534,7 @@ class ViewShardedTrainer:
         self.overflows += 1
         if int(self._overflow.item()):
             need = int((self._pair_counts[: len(self.views)].to(torch.int64) & 0xFFFFFFFF).max().item())  # uint32
-            self._overflow.zero_()
+            memset_(self._overflow)
             self._set_capacity(need)
 
     def step_host(self, targets_host: Sequence[torch.Tensor]) -> torch.Tensor:
@@ -572,8 +565,6 @@ class ViewShardedTrainer:
             self._grow_after_overflow()
         else:
             raise RuntimeError("view binning kept outgrowing its pair capacity")
-        self._pair_sum += self._pair_counts[: len(self.views)].sum()
-        self._pair_views += len(self.views)
         if self.check_finite:
             ShardedAdam.raise_if_nonfinite(code)
         return self._pinned_losses

@@ -7,8 +7,13 @@ SURVEY.md §8(c):
   except pixels the oracle flags as within fp32 error of a threshold kink;
 * gradients (same image_grad fed to both sides): |d| <= atol + rtol*|ref| +
   slack, where slack is the oracle's |terms| from kink-adjacent evaluations.
-  A second, error-model check adds C*eps32*mag (mag = sum of |terms|), the
-  rounding-error scale of fp32 accumulation; both counts are reported.
+  A second, error-model check adds C*eps32*(mag + tmag): mag = sum of |terms|,
+  the rounding-error scale of fp32 accumulation, and tmag = sum of |terms| x
+  kappa (kappa = sum of alpha/(1-alpha) over the pixel's composited entries),
+  the rounding-error scale of the fp32 transmittance chain; both counts are
+  reported.  Entries whose sums cancel beyond what fp32 can resolve are held to
+  the error model only; the fp64 parity build (tests/test_gpu_strict.py) holds
+  every entry to the strict bound.
 """
 from __future__ import annotations
 
@@ -90,8 +95,8 @@ def run_oracle(arrays: dict, n: int, cam: "O.Cam", cfg: "O.Cfg", image_grad=None
     f = O.render_forward(scene, cam, cfg, b)
     res = dict(offsets=b[0], values=b[1], color=f["color"], trans=f["trans"], last=f["last"], kink=f["kink"])
     if image_grad is not None:
-        g, mag, slack = O.render_backward(scene, cam, cfg, b, f, np.asarray(image_grad, np.float64))
-        res.update(grads=g, mag=mag, slack=slack)
+        g, mag, slack, tmag = O.render_backward_tm(scene, cam, cfg, b, f, np.asarray(image_grad, np.float64))
+        res.update(grads=g, mag=mag, slack=slack, tmag=tmag)
     return res
 
 
@@ -127,8 +132,11 @@ def compare_grads(gpu: dict, orc: dict, rtol=RTOL, atol=ATOL, model_c=MODEL_C) -
         d = np.abs(got - ref)
         slack = orc["slack"][f]
         mag = orc["mag"][f]
+        # fp32 error model: rounding of the sums (mag) plus the transmittance chain (tmag: |terms| x the pixel's
+        # sum of alpha/(1-alpha), the amplification of alpha's relative error through the (1 - alpha) factors)
+        tmag = orc["tmag"][f] if orc.get("tmag") is not None and orc["tmag"].get(f) is not None else 0.0
         strict = d > atol + rtol * np.abs(ref) + slack
-        model = d > atol + rtol * np.abs(ref) + slack + model_c * EPS32 * mag
+        model = d > atol + rtol * np.abs(ref) + slack + model_c * EPS32 * (mag + tmag)
         exempt = mag > CANCEL_MAX * np.maximum(np.abs(ref), atol)
         scale = float(np.abs(ref).max()) if ref.size else 0.0
         tol = atol + rtol * np.abs(ref) + slack
@@ -228,12 +236,13 @@ def run_rows(arrays: dict, mode: int, n: int, cam: "O.Cam", cfg: "O.Cfg", image_
     sub_arrays = {f: (None if arrays.get(f) is None else np.ascontiguousarray(arrays[f][ids])) for f in O.FIELDS}
     scene = O.Scene64(sub_arrays, n, sigma)
     f = O.render_forward(scene, cam, cfg, sub_bin)
-    gr, mag, slack = O.render_backward(scene, cam, cfg, sub_bin, f, ig)
+    gr, mag, slack, tmag = O.render_backward_tm(scene, cam, cfg, sub_bin, f, ig)
     orc = dict(offsets=offsets, values=values, color=f["color"][px_rows], trans=f["trans"][px_rows],
                last=f["last"][px_rows], kink=f["kink"][px_rows],
                grads={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in gr.items()},
                mag={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in mag.items()},
-               slack={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in slack.items()})
+               slack={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in slack.items()},
+               tmag={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in tmag.items()})
     info = dict(tile_rows=len(rows), tiles_y=ty, subset_pairs=int(len(sub_vals)), pairs=int(len(values)),
                 subset_primitives=int(len(ids)), gpu_nonzero_outside_subset=outside,
                 max_list=int(counts.max()) if counts.size else 0, mean_list=float(counts.mean()))
