@@ -1,13 +1,16 @@
 """Benchmark of the Gaussian Billboards hot path on B200 (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[3], weak scaling): 1,000,000 textured surfels
-with 8x8 RGB fp32 textures, 64 Fibonacci-sphere cameras (radius 6) at
-1600x1064; every GPU renders and backpropagates its own 8 views per step (L1
-loss against seeded-noise targets), gradients are summed by one NCCL
-all-reduce (N > 1) and Adam updates the replicated primitives.  One "step" is
-that whole training step; value = megapixels/s over all GPUs.
+Workload (BASELINE.json configs[3]): 1,000,000 textured surfels with 8x8 RGB
+fp32 textures, 64 Fibonacci-sphere cameras (radius 6) at 1600x1064.  Strong
+scaling (default, SURVEY §8(d)'s primary): the 64 views are split over the N
+GPUs; --scaling weak: every GPU renders and backpropagates its own 8 views.
+Per step every GPU renders and backpropagates its views (L1 loss against
+seeded-noise targets); for N > 1 the gradients are reduce-scattered over NCCL
+through the C-ABI, Adam updates each rank's slice and the parameters are
+all-gathered.  One "step" is that whole training step; value = megapixels/s
+over all GPUs.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scaling strong|weak]
 
 --impl reference times the reference algorithm's CPU implementation on the
 host cores (rank 0 only): the compiled reference has no perspective camera
@@ -43,6 +46,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the 64 configs[3] views split over the N ranks (SURVEY §8(d) primary); "
+                         "weak: --views-per-gpu views on every rank")
     ap.add_argument("--views-per-gpu", type=int, default=8)
     ap.add_argument("--count", type=int, default=1_000_000)
     ap.add_argument("--n", type=int, default=8)
@@ -58,6 +64,41 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def union_ms(ivs) -> float:
+    """Total length of the union of [a, b) intervals."""
+    busy, end = 0.0, -1e30
+    for a, b in sorted(ivs):
+        if b > end:
+            busy += b - max(a, end)
+            end = b
+    return busy
+
+
+def attribute_ms(ivs_by_kernel: dict) -> dict:
+    """Share of the timeline per kernel: every instant covered by k concurrent launches (any lanes, any
+    kernels) is split equally between them, so the shares sum to the union of all launches (<= the step)."""
+    ev = []
+    for name, ivs in ivs_by_kernel.items():
+        for a, b in ivs:
+            if b > a:
+                ev.append((a, 1, name))
+                ev.append((b, -1, name))
+    ev.sort(key=lambda e: (e[0], e[1]))
+    out = {k: 0.0 for k in ivs_by_kernel}
+    active = {}
+    t0 = None
+    for t, d, name in ev:
+        n = sum(active.values())
+        if t0 is not None and n > 0 and t > t0:
+            for k, c in active.items():
+                out[k] += (t - t0) * c / n
+        active[name] = active.get(name, 0) + d
+        if active[name] == 0:
+            del active[name]
+        t0 = t
+    return out
 
 
 def hbm_peak():
@@ -177,7 +218,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(mps, 4), "unit": "MP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
-        "ms_per_view": round(step_s * 1e3, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_view": round(step_s * 1e3, 1), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[3] shapes)",
         "config": {"workload": "configs[3] view: 1M surfels, 8x8 fp32 textures, 1600x1064, fwd+bwd+L1 (+1/8 Adam)",
                    "views_per_step": 1},
@@ -200,6 +241,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator sizes appear in the log
         torch.cuda.set_device(local)
         if os.environ.get("GB_BENCH_FAKE_PG") == "1":  # code-path check on one GPU: collectives move nothing
             from torch.testing._internal.distributed.fake_pg import FakeStore
@@ -220,7 +262,7 @@ def run_ours(args):
     arrays = cfg3.arrays()
     splats = gb.SplatSet.from_numpy(cfg3.mode, gb.ColorGridConfig(cfg3.n), device=device, **arrays)
     cams = [gb.PinholeCamera.from_spec(c) for c in cfg3.cameras]
-    views = shard_views(len(cams), rank, world, per_rank=args.views_per_gpu)
+    views = shard_views(len(cams), rank, world, per_rank=args.views_per_gpu if args.scaling == "weak" else None)
     lrs = gb.LearningRates()
     lrs.position *= 6.0  # position LR x scene extent
     use_graph = os.environ.get("GB_GRAPH", "1") != "0" and not args.no_graph
@@ -276,7 +318,7 @@ def run_ours(args):
     # launch intervals of the compositors on all lanes, relative to ev0: overlapping launches of the same
     # kernel on different lanes are merged into busy time (a launch's own interval also holds its wait
     # for SMs held by the other lanes)
-    intervals = {k: [iv for c in ctxs for iv in c.profile_intervals(ev0, k)] for k in ("forward", "backward")}
+    intervals = {k: [iv for c in ctxs for iv in c.profile_intervals(ev0, k)] for k in gb._lib.KERNEL_NAMES}
     prof = {}
     for c in ctxs:
         c.profile(False)
@@ -289,7 +331,7 @@ def run_ours(args):
                  "; avg_launch_ms = union of the kernel's launch intervals over all lanes / launches")
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
     step_ms = elapsed_ms / args.steps
-    views_total = world * len(views)
+    views_total = world * len(views) if args.scaling == "weak" else len(cams)
     mpix = views_total * W * H / 1e6
     value = mpix / (step_ms / 1e3)
     pair_sum, pair_views = trainer.pair_stats()
@@ -369,11 +411,7 @@ def run_ours(args):
     dom = max(model, key=lambda k: prof[k][0])
     total_ms, count = prof[dom]
     bytes_per_launch = model[dom](mean_pairs)  # linear in P: the mean over the timed views
-    busy_ms, end = 0.0, -1e30
-    for a, b in sorted(intervals.get(dom, [])):  # union of the launch intervals
-        if b > end:
-            busy_ms += b - max(a, end)
-            end = b
+    busy_ms = union_ms(intervals.get(dom, []))  # union of the launch intervals
     avg_ms = (busy_ms if busy_ms > 0 else total_ms) / max(1, count)  # busy time per launch
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
     traffic = None
@@ -384,7 +422,10 @@ def run_ours(args):
         except Exception:
             traffic = None
 
-    kernel_ms = {k: round(v[0] / args.steps, 4) for k, v in prof.items() if v[1]}
+    share = attribute_ms({k: v for k, v in intervals.items() if v})
+    kernel_ms = {k: round(v / args.steps, 4) for k, v in share.items()}
+    kernel_busy = {k: round(union_ms(v) / args.steps, 4) for k, v in intervals.items() if v}
+    collective_ms = round(union_ms(intervals.get("collective", [])) / args.steps, 4)
     line = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -395,14 +436,16 @@ def run_ours(args):
         "ms_per_step": round(step_ms, 3),
         "ms_per_view": round(step_ms / len(views), 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded Rng, BASELINE configs[3] shapes; random-init surfels, noise targets)",
         "config": {"workload": "configs[3] view-sharded training step: 1M surfels, 8x8 fp32 RGB textures, "
-                               f"{args.views_per_gpu} Fibonacci-sphere views/GPU at 1600x1064, L1, "
-                               "Adam (N > 1: NCCL reduce-scatter, Adam on the rank's slice, all-gather)",
-                   "views_per_gpu": len(views), "surfels": cfg3.count, "texture": f"{n}x{n}",
+                               + (f"the 64 Fibonacci-sphere views split over {world} GPU(s)" if args.scaling == "strong"
+                                  else f"{args.views_per_gpu} Fibonacci-sphere views/GPU") +
+                               " at 1600x1064, L1, Adam (N > 1: NCCL reduce-scatter through the C-ABI, Adam on "
+                               "the rank's slice, all-gather)",
+                   "views_per_gpu": len(views), "views_total": views_total, "surfels": cfg3.count, "texture": f"{n}x{n}",
                    "image": f"{W}x{H}", "tile": 16,
                    "compositor": ("fused " if trainer.fused else "") + "direct (one warp per 8x4 pixel block)",
                    "mean_pairs_per_view": int(mean_pairs),
@@ -418,8 +461,14 @@ def run_ours(args):
                      "avg_launch_ms_events": round(total_ms / max(1, count), 4),
                      "peak_source": peak_src, "timing": prof_note},
         "kernel_ms_per_step": kernel_ms,
-        "kernel_ms_note": "sum of event intervals per launch site; the two view lanes overlap, so an interval "
-                          "includes waiting for SMs held by the other lane (small kernels most)",
+        "kernel_ms_note": "each kernel's share of the timeline from CUDA events around every launch on all view "
+                          "lanes: an instant covered by k concurrent launches counts 1/k to each, so the shares "
+                          "sum to the busy time (<= ms_per_step); kernel_busy_ms_per_step is each kernel's own "
+                          "union of launch intervals (overlaps other kernels)",
+        "kernel_busy_ms_per_step": kernel_busy,
+        "collective_ms": collective_ms,
+        "comm": ({"nranks": world, "path": "C-ABI gb_comm (NCCL; reduce-scatter + all-gather + flag min)"}
+                 if world > 1 else {"nranks": 1, "path": "none (one GPU)"}),
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "e2e": e2e,

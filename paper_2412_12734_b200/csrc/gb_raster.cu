@@ -382,6 +382,81 @@ __device__ __forceinline__ WarpPixel live_rect(const WarpPixel& wp, bool live) {
     return r;
 }
 
+// One forward entry for the calling warp (raster.hpp:238-250): evaluate, pick the warp's texel footprint
+// class (see bwd_shade), composite into the lanes that are not done.
+template <int MODE, int NT>
+__device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __restrict__ tex, int id, int rank, int x,
+                                          int y, const RasterConst& rc, int N, real early, bool& done, real& T,
+                                          real& acc0, real& acc1, real& acc2, int& last) {
+    const int F = 3 * N * N;
+    real u, v;
+    bool hit;
+    if (MODE == GB_MODE_ORTHO) {
+        hit = eval_uv_ortho(h, x, y, u, v);
+    } else {
+        PinholeTerms pt;
+        hit = eval_uv_pinhole(h, x, y, u, v, pt);
+    }
+    const real G = gauss_weight(u, v);
+    const real alpha = rmin(mul_rn(h.h1.z, G), kMaxAlpha);  // raster.hpp:241
+    const bool comp = !done && hit && !(alpha < rc.alpha_skip);     // raster.hpp:242
+    // texel footprint class of the warp (see bwd_shade): clamped axes read one texel row
+    const real sigma = rc.sigma;
+    const bool au = N > 1 && __any_sync(kFull, comp && u > -sigma && u < sigma);
+    const bool av = N > 1 && __any_sync(kFull, comp && v > -sigma && v < sigma);
+    if (comp) {
+        const float* t = tex + (size_t)id * F;
+        real c0_, c1_, c2_;
+        if (au && av) {
+            Bilin b;
+            bilin_setup(u, v, N, rc, b);
+            const float* p00 = t + b.o00;
+            const float* p10 = p00 + 3 * N;
+            c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 + __ldg(p10 + 3) * b.w11;
+            c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
+                  __ldg(p10 + 4) * b.w11;
+            c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
+                  __ldg(p10 + 5) * b.w11;
+        } else if (au || av) {  // the four-corner blend with two zero weights
+            // (separate uniform branches: each keeps its index arithmetic free of selects)
+            const float* pa;
+            const float* pb;
+            real f;
+            if (au) {
+                real sx = fma_rn(u, rc.tex_scale, rc.tex_offset);
+                sx = rmin(rmax(sx, (real)0), (real)(N - 1));
+                const int i0 = min((int)rfloor(sx), N - 2);
+                f = sub_rn(sx, (real)i0);
+                pa = t + (i0 * N + (v > (real)0 ? N - 1 : 0)) * 3;
+                pb = pa + 3 * N;
+            } else {
+                real sx = fma_rn(v, rc.tex_scale, rc.tex_offset);
+                sx = rmin(rmax(sx, (real)0), (real)(N - 1));
+                const int i0 = min((int)rfloor(sx), N - 2);
+                f = sub_rn(sx, (real)i0);
+                pa = t + ((u > (real)0 ? N - 1 : 0) * N + i0) * 3;
+                pb = pa + 3;
+            }
+            const real gf = (real)1 - f;
+            c0_ = fma_rn(__ldg(pb), f, __ldg(pa) * gf);
+            c1_ = fma_rn(__ldg(pb + 1), f, __ldg(pa + 1) * gf);
+            c2_ = fma_rn(__ldg(pb + 2), f, __ldg(pa + 2) * gf);
+        } else {  // one texel (and n = 1)
+            const float* p = t + (N > 1 ? ((u > (real)0 ? N - 1 : 0) * N + (v > (real)0 ? N - 1 : 0)) * 3 : 0);
+            c0_ = __ldg(p);
+            c1_ = __ldg(p + 1);
+            c2_ = __ldg(p + 2);
+        }
+        const real w = alpha * T;  // raster.hpp:244-249
+        acc0 = fma_rn(c0_, w, acc0);
+        acc1 = fma_rn(c1_, w, acc1);
+        acc2 = fma_rn(c2_, w, acc2);
+        T = mul_rn(T, sub_rn((real)1, alpha));
+        last = rank;
+        if (T < early) done = true;  // raster.hpp:250
+    }
+}
+
 // render_forward's per-pixel loop (raster.hpp:237-250) for the calling warp's pixels
 template <int MODE, int NT>
 __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __restrict__ values,
@@ -389,7 +464,6 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
                                          const float* __restrict__ tex, const RasterConst& rc, int N,
                                          const WarpPixel& wp, real& T, real& acc0, real& acc1, real& acc2,
                                          int& last) {
-    const int F = 3 * N * N;
     const int lane = threadIdx.x & 31;
     const int total = (int)(range.y - range.x);
     const int x = wp.x, y = wp.y;
@@ -411,78 +485,12 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             const int bit = __ffs(mask) - 1;
             mask &= mask - 1;
             const int id = __shfl_sync(kFull, idl, bit);
-            // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not
-            // composite -- no branch around the evaluation
-            real u, v;
             ScreenHeader h;
             h.h0 = ld_real4(&hdr[id].h0);
             h.h1 = ld_real4(&hdr[id].h1);
             h.h2 = ld_real4(&hdr[id].h2);
-            bool hit;
-            if (MODE == GB_MODE_ORTHO) {
-                hit = eval_uv_ortho(h, x, y, u, v);
-            } else {
-                PinholeTerms pt;
-                hit = eval_uv_pinhole(h, x, y, u, v, pt);
-            }
-            const real G = gauss_weight(u, v);
-            const real alpha = rmin(mul_rn(h.h1.z, G), kMaxAlpha);  // raster.hpp:241
-            const bool comp = !done && hit && !(alpha < rc.alpha_skip);     // raster.hpp:242
-            // texel footprint class of the warp (see bwd_shade): clamped axes read one texel row
-            const real sigma = rc.sigma;
-            const bool au = N > 1 && __any_sync(kFull, comp && u > -sigma && u < sigma);
-            const bool av = N > 1 && __any_sync(kFull, comp && v > -sigma && v < sigma);
-            if (comp) {
-                const float* t = tex + (size_t)id * F;
-                real c0_, c1_, c2_;
-                if (au && av) {
-                    Bilin b;
-                    bilin_setup(u, v, N, rc, b);
-                    const float* p00 = t + b.o00;
-                    const float* p10 = p00 + 3 * N;
-                    c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 + __ldg(p10 + 3) * b.w11;
-                    c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
-                          __ldg(p10 + 4) * b.w11;
-                    c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
-                          __ldg(p10 + 5) * b.w11;
-                } else if (au || av) {  // the four-corner blend with two zero weights
-                    // (separate uniform branches: each keeps its index arithmetic free of selects)
-                    const float* pa;
-                    const float* pb;
-                    real f;
-                    if (au) {
-                        real sx = fma_rn(u, rc.tex_scale, rc.tex_offset);
-                        sx = rmin(rmax(sx, (real)0), (real)(N - 1));
-                        const int i0 = min((int)rfloor(sx), N - 2);
-                        f = sub_rn(sx, (real)i0);
-                        pa = t + (i0 * N + (v > (real)0 ? N - 1 : 0)) * 3;
-                        pb = pa + 3 * N;
-                    } else {
-                        real sx = fma_rn(v, rc.tex_scale, rc.tex_offset);
-                        sx = rmin(rmax(sx, (real)0), (real)(N - 1));
-                        const int i0 = min((int)rfloor(sx), N - 2);
-                        f = sub_rn(sx, (real)i0);
-                        pa = t + ((u > (real)0 ? N - 1 : 0) * N + i0) * 3;
-                        pb = pa + 3;
-                    }
-                    const real gf = (real)1 - f;
-                    c0_ = fma_rn(__ldg(pb), f, __ldg(pa) * gf);
-                    c1_ = fma_rn(__ldg(pb + 1), f, __ldg(pa + 1) * gf);
-                    c2_ = fma_rn(__ldg(pb + 2), f, __ldg(pa + 2) * gf);
-                } else {  // one texel (and n = 1)
-                    const float* p = t + (N > 1 ? ((u > (real)0 ? N - 1 : 0) * N + (v > (real)0 ? N - 1 : 0)) * 3 : 0);
-                    c0_ = __ldg(p);
-                    c1_ = __ldg(p + 1);
-                    c2_ = __ldg(p + 2);
-                }
-                const real w = alpha * T;  // raster.hpp:244-249
-                acc0 = fma_rn(c0_, w, acc0);
-                acc1 = fma_rn(c1_, w, acc1);
-                acc2 = fma_rn(c2_, w, acc2);
-                T = mul_rn(T, sub_rn((real)1, alpha));
-                last = c0 + bit;
-                if (T < early) done = true;  // raster.hpp:250
-            }
+            // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not composite
+            fwd_entry<MODE, NT>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
             if (__all_sync(kFull, done)) break;
         }
     }
@@ -525,6 +533,145 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
     }
 }
 
+#ifdef GB_STAGE_HEADERS
+#ifdef GB_PARITY_F64
+#error "GB_STAGE_HEADERS is an fp32 A/B variant"
+#endif
+// ---------------------------------------------------------------------------
+// Variant build (-DGB_STAGE_HEADERS; A/B only): CTA-cooperative staging of the list
+// entries' ids, cull records and headers (84 B per entry) in a double-buffered shared-memory ring of
+// 32-entry chunks.  Warp 0 copies chunk i+1 with cp.async (16-B LDGSTS, one entry per lane) while every
+// warp composites chunk i from shared memory; one CTA barrier per chunk.  Texels stay on L1.  Versus the
+// direct walk each entry's id/cull/header is read from L2/L1 once per tile instead of once per warp.
+// ---------------------------------------------------------------------------
+struct __align__(16) StageChunk {
+    float4 cull[32][2];
+    float4 hdr[32][3];
+    int id[32];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// warp 0: entries [c0, c0 + n) of the tile list into chunk buffer b (n <= 32)
+__device__ __forceinline__ void stage_chunk(StageChunk& b, const int32_t* __restrict__ values, uint32_t base, int c0,
+                                            int n, const ScreenHeader* __restrict__ hdr,
+                                            const CullRec* __restrict__ cull) {
+    const int lane = threadIdx.x & 31;
+    const int id = lane < n ? __ldg(&values[base + c0 + lane]) : -1;
+    b.id[lane] = id;
+    if (id >= 0) {
+        cp_async16(&b.cull[lane][0], &cull[id].a);
+        cp_async16(&b.cull[lane][1], &cull[id].b);
+        cp_async16(&b.hdr[lane][0], &hdr[id].h0);
+        cp_async16(&b.hdr[lane][1], &hdr[id].h1);
+        cp_async16(&b.hdr[lane][2], &hdr[id].h2);
+    }
+    cp_async_commit();
+}
+
+__device__ __forceinline__ bool staged_meets(const StageChunk& b, int j, const WarpPixel& w) {
+    return ellipse_meets_rect(b.cull[j][0], b.cull[j][1], w.bx0 - 0.05f, w.bx1 + 0.05f, w.by0 - 0.05f, w.by1 + 0.05f);
+}
+
+__device__ __forceinline__ ScreenHeader staged_header(const StageChunk& b, int j) {
+    ScreenHeader h;
+    h.h0 = b.hdr[j][0];
+    h.h1 = b.hdr[j][1];
+    h.h2 = b.hdr[j][2];
+    return h;
+}
+
+template <int MODE, int NT>
+__device__ __forceinline__ void fwd_walk_staged(const uint2 range, const int32_t* __restrict__ values,
+                                                const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
+                                                const float* __restrict__ tex, const RasterConst& rc, int N,
+                                                const WarpPixel& wp, real& T, real& acc0, real& acc1, real& acc2,
+                                                int& last, StageChunk* ring) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int total = (int)(range.y - range.x);
+    T = (real)1;
+    acc0 = acc1 = acc2 = (real)0;
+    last = -1;
+    bool done = !wp.inside;
+    const real early = rc.early_stop > (real)0 ? rc.early_stop : -(real)1;
+    if (total == 0) return;
+    if (warp == 0) {
+        stage_chunk(ring[0], values, range.x, 0, min(32, total), hdr, cull);
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    int buf = 0;
+    for (int c0 = 0; c0 < total; c0 += 32) {
+        if (warp == 0 && c0 + 32 < total) stage_chunk(ring[buf ^ 1], values, range.x, c0 + 32, min(32, total - c0 - 32), hdr, cull);
+        const StageChunk& b = ring[buf];
+        if (!__all_sync(kFull, done)) {
+            const WarpPixel lr = live_rect(wp, !done);
+            const bool pass = c0 + lane < total && staged_meets(b, lane, lr);
+            unsigned mask = __ballot_sync(kFull, pass);
+            while (mask) {
+                const int bit = __ffs(mask) - 1;
+                mask &= mask - 1;
+                fwd_entry<MODE, NT>(staged_header(b, bit), tex, b.id[bit], c0 + bit, wp.x, wp.y, rc, N, early, done, T,
+                                    acc0, acc1, acc2, last);
+                if (__all_sync(kFull, done)) break;
+            }
+        }
+        if (warp == 0) cp_async_wait_all();
+        if (__syncthreads_and(done)) break;  // every pixel of the tile terminated (raster.hpp:250)
+        buf ^= 1;
+    }
+}
+
+template <int MODE, int NT>
+__device__ __forceinline__ void bwd_walk_staged(const uint2 range, const int32_t* __restrict__ values,
+                                                const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
+                                                const float* __restrict__ tex, const CamConst& cc,
+                                                const RasterConst& rc, int N, const WarpPixel& wp, int last, real T,
+                                                real g0, real g1, real g2, real* wscratch, real* __restrict__ accum,
+                                                real* __restrict__ grid_grad, StageChunk* ring, int* s_top) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (g0 == (real)0 && g1 == (real)0 && g2 == (real)0) last = -1;  // raster.hpp:315-317
+    real bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
+    const int wlast = __reduce_max_sync(kFull, last);
+    if (threadIdx.x == 0) *s_top = -1;
+    __syncthreads();
+    if (lane == 0 && wlast >= 0) atomicMax(s_top, wlast);
+    __syncthreads();
+    const int top = *s_top;  // the CTA walks ranks [0, top] back to front in 32-entry chunks
+    if (top < 0) return;
+    int c0 = top & ~31;
+    if (warp == 0) {
+        stage_chunk(ring[0], values, range.x, c0, top - c0 + 1, hdr, cull);
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    int buf = 0;
+    for (; c0 >= 0; c0 -= 32) {
+        if (warp == 0 && c0 >= 32) stage_chunk(ring[buf ^ 1], values, range.x, c0 - 32, 32, hdr, cull);
+        const StageChunk& b = ring[buf];
+        if (c0 <= wlast) {
+            const bool pass = c0 + lane <= wlast && staged_meets(b, lane, wp);
+            unsigned mask = __ballot_sync(kFull, pass);
+            while (mask) {
+                const int bit = 31 - __clz(mask);
+                mask &= ~(1u << bit);
+                const int id = b.id[bit];
+                bwd_entry<MODE, NT>(staged_header(b, bit), tex + (size_t)id * 3 * N * N, id, c0 + bit, last, wp.x,
+                                    wp.y, T, g0, g1, g2, bh0, bh1, bh2, rc, N, lane, wscratch, accum, grid_grad);
+            }
+        }
+        if (warp == 0) cp_async_wait_all();
+        __syncthreads();
+        buf ^= 1;
+    }
+}
+#endif  // GB_STAGE_HEADERS
+
 template <int MODE, int NT>
 __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict__ ranges,
                                                         const int32_t* __restrict__ values,
@@ -536,7 +683,13 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
     const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
     real T, a0, a1, a2;
     int last;
+#ifdef GB_STAGE_HEADERS
+    __shared__ StageChunk ring[2];
+    fwd_walk_staged<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
+                              ring);
+#else
     fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
+#endif
     if (wp.inside) {  // raster.hpp:253-254
         const size_t p = (size_t)wp.y * cc.width + wp.x;
         out_color[p * 3 + 0] = fma_rn(T, cc.bg[0], a0);
@@ -566,7 +719,13 @@ __global__ void __launch_bounds__(256) k_forward_loss(const uint2* __restrict__ 
     const WarpPixel wp = warp_pixel(rc, cc, blockIdx.x);
     real T, a0, a1, a2;
     int last;
+#ifdef GB_STAGE_HEADERS
+    __shared__ StageChunk ring[2];
+    fwd_walk_staged<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
+                              ring);
+#else
     fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
+#endif
     real l = (real)0;
     if (wp.inside) {
         const size_t p = (size_t)wp.y * cc.width + wp.x;
@@ -626,8 +785,16 @@ __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2
         if (rc.trans64) T = rc.trans64[p];
 #endif
     }
+#ifdef GB_STAGE_HEADERS
+    __shared__ StageChunk ring[2];
+    __shared__ int s_top;
+    bwd_walk_staged<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1,
+                              g2, red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad, ring,
+                              &s_top);
+#else
     bwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1, g2,
                        red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad);
+#endif
 }
 
 #ifdef GB_FUSED_SINGLE_KERNEL

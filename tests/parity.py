@@ -148,11 +148,18 @@ def compare_grads(gpu: dict, orc: dict, rtol=RTOL, atol=ATOL, model_c=MODEL_C) -
                                   slack=float(slack.ravel()[i]), mag=float(mag.ravel()[i]), ratio=float(ratio[i])))
         # error-model ratio of the strict violations: |d| / (eps32 * sum|terms|)
         em = (d / (EPS32 * np.maximum(mag, 1e-300)))[strict]
+        tm = np.broadcast_to(tmag, d.shape) if np.ndim(tmag) else np.zeros_like(d)
+
+        def listing(sel, k=4):
+            idx = np.flatnonzero(sel.ravel())[:k]
+            return [dict(index=int(i), got=float(got.ravel()[i]), ref=float(ref.ravel()[i]), mag=float(mag.ravel()[i]),
+                         tmag=float(tm.ravel()[i]), slack=float(slack.ravel()[i])) for i in idx]
         out[f] = dict(entries=int(ref.size), strict_violations=int(strict.sum()), worst=worst,
                       strict_violations_applicable=int((strict & ~exempt).sum()),
                       cancellation_exempt=int(exempt.sum()),
                       eps_mag_ratio_max=float(em.max()) if em.size else 0.0,
                       model_violations=int(model.sum()), kink_entries=int((slack > 0).sum()),
+                      applicable=listing(strict & ~exempt), model_list=listing(model),
                       max_abs_err=float(d.max()) if d.size else 0.0,
                       max_rel_to_scale=float(d.max() / scale) if scale > 0 else 0.0)
     return out

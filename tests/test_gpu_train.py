@@ -467,3 +467,39 @@ def test_view_lanes_match_one_lane_at_configs3_size():
         rms = float(np.sqrt(np.mean(w * w))) + 1e-30
         bad = np.abs(four[k] - w) > 1e-3 * np.abs(w) + 1e-3 * rms
         assert int(bad.sum()) == 0, (k, int(bad.sum()), float(np.abs(four[k] - w).max()), rms)
+
+
+def test_comm_c_abi_single_rank():
+    """The C-ABI NCCL layer at world size 1 (ncclCommInitRank over one GPU): every collective of the step
+    runs on the context's stream and is the identity; the communicator reports no asynchronous error."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2412_12734_b200 import _lib
+    from paper_2412_12734_b200._lib import check, lib
+    from paper_2412_12734_b200.raster import context
+
+    ctx = context("cuda")
+    uid = (C.c_uint8 * _lib.COMM_ID_BYTES)()
+    check(lib.gb_comm_unique_id(uid), "gb_comm_unique_id")
+    h = C.c_void_p()
+    check(lib.gb_comm_init_rank(ctx.handle, 1, uid, 0, C.byref(h)), "gb_comm_init_rank")
+    n, r = C.c_int32(), C.c_int32()
+    check(lib.gb_comm_info(h, C.byref(n), C.byref(r)), "gb_comm_info")
+    assert (n.value, r.value) == (1, 0)
+    x = torch.arange(1000, dtype=torch.float32, device="cuda")
+    want = x.clone()
+    check(lib.gb_allreduce_grads(ctx.handle, h, x.data_ptr(), x.numel()), "allreduce")
+    y = torch.empty_like(x)
+    check(lib.gb_reduce_scatter_grads(ctx.handle, h, x.data_ptr(), y.data_ptr(), x.numel()), "reduce_scatter")
+    z = torch.empty_like(x)
+    check(lib.gb_all_gather_params(ctx.handle, h, y.data_ptr(), z.data_ptr(), y.numel()), "all_gather")
+    f = torch.tensor([12345], dtype=torch.int64, device="cuda")
+    check(lib.gb_allreduce_flag_min(ctx.handle, h, f.data_ptr()), "flag")
+    check(lib.gb_sync(ctx.handle), "sync")
+    assert torch.equal(x, want) and torch.equal(y, want) and torch.equal(z, want) and int(f) == 12345
+    check(lib.gb_comm_check(h), "gb_comm_check")
+    bad = lib.gb_allreduce_grads(ctx.handle, None, x.data_ptr(), 4)
+    assert bad == _lib.GB_INVALID_ARGUMENT
+    check(lib.gb_comm_destroy(h), "gb_comm_destroy")
