@@ -569,7 +569,7 @@ static int eval_uv(const raster_ctx_t *c, const geom_t *g, double px, double py,
  * beyond the tolerance (thin, grazing splats), so it is treated like a kink. */
 static const double kEps32 = 5.9604644775390625e-08;
 
-static double uv_error32(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
+static double uv_error32_raw(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
     double eu, ev;
     if (c->cam->mode == ORC_MODE_ORTHO) {
         const double dx = px - g->x, dy = py - g->y;
@@ -582,10 +582,21 @@ static double uv_error32(const raster_ctx_t *c, const geom_t *g, double px, doub
         eu = 4.0 * kEps32 * (fabs(g->X[0] * dx) + fabs(g->Y[0] * dy) + fabs(u) * czt + fabs(g->X[0]) + fabs(g->Y[0])) / cz;
         ev = 4.0 * kEps32 * (fabs(g->X[1] * dx) + fabs(g->Y[1] * dy) + fabs(v) * czt + fabs(g->X[1]) + fabs(g->Y[1])) / cz;
     }
+    return eu > ev ? eu : ev;
+}
+
+static double uv_error32(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
     const int n = c->s->n;
     const double grid = n > 1 ? (double)(n - 1) / (2.0 * c->s->sigma) : 1.0;
-    const double e = (eu > ev ? eu : ev);
-    return e * (grid > 1.0 ? grid : 1.0);
+    return uv_error32_raw(c, g, px, py, u, v) * (grid > 1.0 ? grid : 1.0);
+}
+
+/* Relative margin of an alpha threshold decision (alpha-skip, the 0.999 cap): the fixed kink margin, or
+ * the evaluation's own fp32 uncertainty when larger -- dalpha/alpha = |u| du + |v| dv (G = exp(-(u^2+v^2)/2))
+ * plus the exponential's and the product's rounding -- which dominates for thin, grazing splats. */
+static double alpha_margin(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
+    const double e = 2.0 * ((fabs(u) + fabs(v)) * uv_error32_raw(c, g, px, py, u, v) + 8.0 * kEps32);
+    return e > c->kink->alpha_rel ? e : c->kink->alpha_rel;
 }
 
 static int sensitive(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
@@ -618,9 +629,9 @@ static void forward_tile(void *vctx, int tile) {
                 const double alpha_raw = g->alpha_k * gaussian_weight(u, v);
                 const double alpha = dmin(alpha_raw, kMaxAlpha);
                 if (kk) {
-                    if (cfg->alpha_skip > 0.0 && fabs(alpha - cfg->alpha_skip) <= kk->alpha_rel * cfg->alpha_skip)
-                        flag |= 1;
-                    if (fabs(alpha_raw - kMaxAlpha) <= kk->alpha_rel * kMaxAlpha) flag |= 1;
+                    const double am = alpha_margin(c, g, px, py, u, v);
+                    if (cfg->alpha_skip > 0.0 && fabs(alpha - cfg->alpha_skip) <= am * cfg->alpha_skip) flag |= 1;
+                    if (fabs(alpha_raw - kMaxAlpha) <= am * kMaxAlpha) flag |= 1;
                     if (alpha >= cfg->alpha_skip && sensitive(c, g, px, py, u, v)) flag |= 4;
                 }
                 if (alpha < cfg->alpha_skip) continue;
@@ -850,7 +861,7 @@ static void backward_tile(void *vctx, int tile) {
                     if (!eval_uv(c, g, px, py, &u, &v, a, b, &cz)) continue;
                     const double weight = gaussian_weight(u, v);
                     const double alpha = dmin(g->alpha_k * weight, kMaxAlpha);
-                    if (fabs(alpha - cfg->alpha_skip) <= kk->alpha_rel * cfg->alpha_skip)
+                    if (fabs(alpha - cfg->alpha_skip) <= alpha_margin(c, g, px, py, u, v) * cfg->alpha_skip)
                         add_abs_terms(c, g, px, py, u, v, alpha, weight, t, gacc, behind,
                                       c->s->grid + (size_t)id * tex_stride, a, b, cz, pslk + (size_t)rank * stride);
                 }
@@ -867,7 +878,7 @@ static void backward_tile(void *vctx, int tile) {
                 if (alpha < cfg->alpha_skip) {
                     /* an entry skipped just below the threshold may be composited in fp32 */
                     if (pslk && (px_flag & 1) && kk &&
-                        fabs(alpha - cfg->alpha_skip) <= kk->alpha_rel * cfg->alpha_skip)
+                        fabs(alpha - cfg->alpha_skip) <= alpha_margin(c, g, px, py, u, v) * cfg->alpha_skip)
                         add_abs_terms(c, g, px, py, u, v, alpha, weight, t, gacc, behind, gridk, a, b, cz,
                                       pslk + (size_t)rank * stride);
                     continue;

@@ -457,13 +457,45 @@ __device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __
     }
 }
 
+// Per-warp header staging (default; -DGB_WARP_STAGE=0 for the A/B): after the 32-entry ballot every
+// passing lane copies its entry's header into the warp's shared-memory slot (structure of arrays, so the
+// stores are conflict-free and each entry's read is a broadcast).  The warp then waits on the header
+// loads once per chunk -- all issued together -- instead of once per entry right before its evaluation
+// (the evaluation's first header use was the top stall site of K3 and K4 under ncu).  Warp-private: no CTA
+// barrier, only __syncwarp.
+#ifndef GB_WARP_STAGE
+#define GB_WARP_STAGE 1
+#endif
+struct WarpHeaders {
+    real4 h[3][32];
+};
+
+__device__ __forceinline__ void stage_headers(WarpHeaders& wh, const ScreenHeader* __restrict__ hdr, bool pass,
+                                              int idl, int lane) {
+    __syncwarp();  // the previous chunk's readers are done
+    if (pass) {
+        wh.h[0][lane] = ld_real4(&hdr[idl].h0);
+        wh.h[1][lane] = ld_real4(&hdr[idl].h1);
+        wh.h[2][lane] = ld_real4(&hdr[idl].h2);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ ScreenHeader staged_hdr(const WarpHeaders& wh, int j) {
+    ScreenHeader h;
+    h.h0 = wh.h[0][j];
+    h.h1 = wh.h[1][j];
+    h.h2 = wh.h[2][j];
+    return h;
+}
+
 // render_forward's per-pixel loop (raster.hpp:237-250) for the calling warp's pixels
 template <int MODE, int NT>
 __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __restrict__ values,
                                          const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                          const float* __restrict__ tex, const RasterConst& rc, int N,
                                          const WarpPixel& wp, real& T, real& acc0, real& acc1, real& acc2,
-                                         int& last) {
+                                         int& last, WarpHeaders* wh) {
     const int lane = threadIdx.x & 31;
     const int total = (int)(range.y - range.x);
     const int x = wp.x, y = wp.y;
@@ -481,14 +513,21 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             pass = entry_meets_warp(hdr, cull, idl, lr);
         }
         unsigned mask = __ballot_sync(kFull, pass);
+#if GB_WARP_STAGE
+        if (mask) stage_headers(*wh, hdr, pass, idl, lane);
+#endif
         while (mask) {
             const int bit = __ffs(mask) - 1;
             mask &= mask - 1;
             const int id = __shfl_sync(kFull, idl, bit);
+#if GB_WARP_STAGE
+            const ScreenHeader h = staged_hdr(*wh, bit);
+#else
             ScreenHeader h;
             h.h0 = ld_real4(&hdr[id].h0);
             h.h1 = ld_real4(&hdr[id].h1);
             h.h2 = ld_real4(&hdr[id].h2);
+#endif
             // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not composite
             fwd_entry<MODE, NT>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
             if (__all_sync(kFull, done)) break;
@@ -502,7 +541,8 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
                                          const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                          const float* __restrict__ tex, const CamConst& cc, const RasterConst& rc,
                                          int N, const WarpPixel& wp, int last, real T, real g0, real g1, real g2,
-                                         real* wscratch, real* __restrict__ accum, real* __restrict__ grid_grad) {
+                                         real* wscratch, real* __restrict__ accum, real* __restrict__ grid_grad,
+                                         WarpHeaders* wh) {
     const int F = 3 * N * N;
     const int lane = threadIdx.x & 31;
     if (g0 == (real)0 && g1 == (real)0 && g2 == (real)0) last = -1;  // raster.hpp:315-317
@@ -519,14 +559,21 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
         }
         unsigned mask = __ballot_sync(kFull, pass);
         if (lane == 0) GB_DBG(1, __popc(mask));
+#if GB_WARP_STAGE
+        if (mask) stage_headers(*wh, hdr, pass, idl, lane);
+#endif
         while (mask) {
             const int bit = 31 - __clz(mask);
             mask &= ~(1u << bit);
             const int id = __shfl_sync(kFull, idl, bit);
+#if GB_WARP_STAGE
+            const ScreenHeader h = staged_hdr(*wh, bit);
+#else
             ScreenHeader h;
             h.h0 = ld_real4(&hdr[id].h0);
             h.h1 = ld_real4(&hdr[id].h1);
             h.h2 = ld_real4(&hdr[id].h2);
+#endif
             bwd_entry<MODE, NT>(h, tex + (size_t)id * F, id, c0 + bit, last, wp.x, wp.y, T, g0, g1, g2, bh0, bh1,
                                 bh2, rc, N, lane, wscratch, accum, grid_grad);
         }
@@ -688,7 +735,9 @@ __global__ void __launch_bounds__(256) k_forward_direct(const uint2* __restrict_
     fwd_walk_staged<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
                               ring);
 #else
-    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
+    __shared__ WarpHeaders whs[8];
+    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
+                       &whs[threadIdx.x >> 5]);
 #endif
     if (wp.inside) {  // raster.hpp:253-254
         const size_t p = (size_t)wp.y * cc.width + wp.x;
@@ -724,7 +773,9 @@ __global__ void __launch_bounds__(256) k_forward_loss(const uint2* __restrict__ 
     fwd_walk_staged<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
                               ring);
 #else
-    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last);
+    __shared__ WarpHeaders whs[8];
+    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
+                       &whs[threadIdx.x >> 5]);
 #endif
     real l = (real)0;
     if (wp.inside) {
@@ -792,8 +843,10 @@ __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2
                               g2, red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad, ring,
                               &s_top);
 #else
+    __shared__ WarpHeaders whs[8];
     bwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1, g2,
-                       red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad);
+                       red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad,
+                       &whs[threadIdx.x >> 5]);
 #endif
 }
 
@@ -820,7 +873,8 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
     const uint2 range = ranges[blockIdx.x];
     real T, a0, a1, a2;
     int last;
-    fwd_walk<MODE, NT>(range, values, hdr, cull, tex, rc, N, wp, T, a0, a1, a2, last);
+    __shared__ WarpHeaders whs[8];
+    fwd_walk<MODE, NT>(range, values, hdr, cull, tex, rc, N, wp, T, a0, a1, a2, last, &whs[threadIdx.x >> 5]);
     real g0 = (real)0, g1 = (real)0, g2 = (real)0, l = (real)0;
     if (wp.inside) {
         const size_t p = (size_t)wp.y * cc.width + wp.x;
@@ -860,7 +914,8 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
     if ((threadIdx.x & 31) == 0 && loss && l != (real)0) atomicAdd(loss, (float)(l * scale));
     bwd_walk<MODE, NT>(range, values, hdr, cull, tex, cc, rc, N, wp, last, T, g0, g1, g2,
-                       red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad);
+                       red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad,
+                       &whs[threadIdx.x >> 5]);
 }
 #endif  // GB_FUSED_SINGLE_KERNEL
 

@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
+python -m pytest tests/test_gpu_configs4.py -x -q -k "4000000-1" > gpurun_out/r2_c4_t1b.log 2>&1; echo "c4 t1 rc=$?"; tail -3 gpurun_out/r2_c4_t1b.log
 B="python bench.py --steps 20 --warmup 5 --no-cpu-baseline"
 $B > gpurun_out/r2_b6_direct_a.json 2>gpurun_out/r2_b6_direct_a.err; echo "direct a rc=$?"
 GB_LIB_PATH=variants/stage/libgb_raster.so $B > gpurun_out/r2_b6_stage_a.json 2>gpurun_out/r2_b6_stage_a.err; echo "stage a rc=$?"
