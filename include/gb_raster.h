@@ -248,6 +248,17 @@ GB_API gb_status gb_render_backward(gb_context *ctx, const gb_splats *s, const g
 GB_API gb_status gb_render(gb_context *ctx, const gb_splats *s, const gb_camera *cam, const gb_raster_config *cfg,
                     gb_binning *scratch, gb_render_out *out);
 
+/* Texel-gradient layout of this context's backwards (no reference counterpart; the default is the
+ * reference's).  stride 3: gb_grads.grid_values is K x n x n x 3 in (i_u, i_v, channel) order
+ * (core.hpp:44-48).  stride 4: K x n x n x 4, RGBA-padded (the 4th float of each texel is never written and
+ * stays as the caller left it; 16-B aligned), so K4 adds each texel's three channels with one 16-byte
+ * vector red instead of an 8-byte and a 4-byte one.  A training loop accumulating many views keeps a
+ * padded buffer and converts it once per step with gb_texel_grads_unpad. */
+GB_API gb_status gb_context_set_texel_grad_stride(gb_context *ctx, int32_t stride);
+/* dst[3t + c] (+)= padded[4t + c] for t < texels, c < 3 (accumulate = 0: overwrite). */
+GB_API gb_status gb_texel_grads_unpad(gb_context *ctx, const float *padded, float *dst, int64_t texels,
+                                      int32_t accumulate);
+
 /* ---- losses (train.hpp:120-133; L1 is the BASELINE configs' loss) --------- */
 /* grad[i] = scale*sign(color-target) (sign(0) = 0); *loss += scale*sum|color-target|. */
 GB_API gb_status gb_l1_loss(gb_context *ctx, const float *color, const float *target, int64_t n, float scale, float *grad,

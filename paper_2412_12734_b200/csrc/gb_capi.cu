@@ -43,6 +43,8 @@ cudaError_t launch_backward(int mode, int n, int tiles, int ts, const uint2* ran
 cudaError_t launch_add_f64(const double* src, float* dst, int64_t n, cudaStream_t st);
 #endif
 cudaError_t launch_adam_flag_init(int64_t* flag, const int32_t* veto, cudaStream_t st);
+cudaError_t launch_texel_unpad(const float* padded, float* dst, int64_t texels, bool accumulate, int sm_count,
+                               cudaStream_t st);
 cudaError_t launch_loss(int kind, const float* color, const float* target, int64_t n, float scale, float* grad,
                         float* loss, int sm_count, cudaStream_t st);
 cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned long long* bad, int sm_count,
@@ -127,6 +129,7 @@ struct gb_context {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
+    int texel_grad_stride = 3;  // gb_context_set_texel_grad_stride
     DevBuf grid64;  // parity build: fp64 texel-gradient scratch (added into the caller's fp32 buffer after K4)
     DevBuf scan_temp, sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp, accum, adam_bad, ssim_tmp,
         metric_tmp, fuse_color, fuse_trans, fuse_last, fuse_grad;
@@ -261,14 +264,14 @@ gb_status validate_splats(const gb_splats* s, int mode) {
 }
 
 // gradient buffers take vector reds (K4/K5): ortho position and log_scale 8-B aligned, quat and even-n grids 16-B
-gb_status validate_grads(const gb_grads* g, int mode, int n, const char* where) {
+gb_status validate_grads(const gb_grads* g, int mode, int n, const char* where, int texel_stride = 3) {
     if (!g->position || !g->log_scale || !g->opacity_logit || !g->grid_values ||
         (mode == GB_MODE_ORTHO && !g->theta) || (mode == GB_MODE_PINHOLE && !g->quat))
         return fail(GB_INVALID_ARGUMENT, "%s: null gradient buffer", where);
     const bool bad = (reinterpret_cast<uintptr_t>(g->log_scale) & 7) ||
                      (mode == GB_MODE_ORTHO && (reinterpret_cast<uintptr_t>(g->position) & 7)) ||
                      (mode == GB_MODE_PINHOLE && (reinterpret_cast<uintptr_t>(g->quat) & 15)) ||
-                     ((n % 2) == 0 && (reinterpret_cast<uintptr_t>(g->grid_values) & 15));
+                     (((n % 2) == 0 || texel_stride == 4) && (reinterpret_cast<uintptr_t>(g->grid_values) & 15));
     if (bad) return fail(GB_INVALID_ARGUMENT, "%s: misaligned gradient buffer", where);
     return GB_OK;
 }
@@ -298,7 +301,7 @@ gb::CamConst make_cam_const(const gb_camera* cam) {
     return cc;
 }
 
-gb::RasterConst make_raster_const(const gb_binning* b, int n, double sigma) {
+gb::RasterConst make_raster_const(const gb_context* ctx, const gb_binning* b, int n, double sigma) {
     gb::RasterConst rc;
     rc.tile_size = b->cfg.tile_size;
     rc.tiles_x = b->tiles_x;
@@ -310,6 +313,9 @@ gb::RasterConst make_raster_const(const gb_binning* b, int n, double sigma) {
     rc.sigma = (gb::real)sigma;
 #ifdef GB_PARITY_F64
     rc.trans64 = b->trans64.as<double>();
+    rc.tgs = 3;  // the parity build's fp64 texel scratch keeps the reference layout
+#else
+    rc.tgs = ctx->texel_grad_stride;
 #endif
     return rc;
 }
@@ -841,7 +847,7 @@ gb_status gb_render_forward(gb_context* ctx, const gb_splats* s, const gb_camera
     if (gb_status st = trans_scratch(ctx, b)) return st;
 #endif
     const gb::CamConst cc = make_cam_const(cam);
-    const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+    const gb::RasterConst rc = make_raster_const(ctx, b, s->grid.n, s->grid.sigma);
     ProfScope ps(ctx, GB_K_FORWARD);
     GB_CUDA(gb::launch_forward(cam->mode, s->grid.n, b->tiles_x * b->tiles_y, b->cfg.tile_size,
                                b->ranges.as<uint2>(), b->values.as<int32_t>(), b->headers.as<gb::ScreenHeader>(),
@@ -868,14 +874,14 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
         return fail(GB_MISMATCH, "render_backward: image size mismatch");
     if (!image_grad) return fail(GB_MISMATCH, "render_backward: image_grad size mismatch");
     if (s->count == 0) return GB_OK;
-    if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_backward")) return st;
+    if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_backward", ctx->texel_grad_stride)) return st;
     if (gb_status st = set_device(ctx)) return st;
     cudaStream_t stream = ctx->stream;
     const int64_t K = s->count;
     GB_CUDA(ctx->accum.ensure(sizeof(gb::real) * gb::kAccumStride * K));
     GB_CUDA(cudaMemsetAsync(ctx->accum.p, 0, sizeof(gb::real) * gb::kAccumStride * K, stream));
     const gb::CamConst cc = make_cam_const(cam);
-    const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+    const gb::RasterConst rc = make_raster_const(ctx, b, s->grid.n, s->grid.sigma);
 #ifdef GB_PARITY_F64
     gb::real* grid_grad = nullptr;
     if (gb_status st = grid_scratch(ctx, K, s->grid.n, &grid_grad)) return st;
@@ -948,7 +954,7 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
             return fail(GB_INVALID_ARGUMENT, "render_loss_backward: null output buffer");
     }
     if (s->count > 0)
-        if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_loss_backward")) return st;
+        if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_loss_backward", ctx->texel_grad_stride)) return st;
     if (gb_status st = set_device(ctx)) return st;
     const int64_t npix = (int64_t)cam->width * cam->height;
     cudaStream_t stream = ctx->stream;
@@ -961,7 +967,7 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
     if (gb_status st = trans_scratch(ctx, b)) return st;
 #endif
     const gb::CamConst cc = make_cam_const(cam);
-    const gb::RasterConst rc = make_raster_const(b, s->grid.n, s->grid.sigma);
+    const gb::RasterConst rc = make_raster_const(ctx, b, s->grid.n, s->grid.sigma);
     const int tiles = b->tiles_x * b->tiles_y;
 #ifdef GB_PARITY_F64
     gb::real* grid_grad = nullptr;
@@ -1137,6 +1143,24 @@ gb_status gb_adam_step(gb_context* ctx, int32_t mode, int64_t count, int32_t n, 
                                        ctx->sm_count, stream));
         ctx->launches++;
     }
+    return GB_OK;
+}
+
+gb_status gb_context_set_texel_grad_stride(gb_context* ctx, int32_t stride) {
+    if (!ctx) return fail(GB_INVALID_ARGUMENT, "null context");
+    if (stride != 3 && stride != 4) return fail(GB_INVALID_ARGUMENT, "texel gradient stride must be 3 or 4");
+    ctx->texel_grad_stride = stride;
+    return GB_OK;
+}
+
+gb_status gb_texel_grads_unpad(gb_context* ctx, const float* padded, float* dst, int64_t texels, int32_t accumulate) {
+    if (!ctx || (texels > 0 && (!padded || !dst))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (texels < 0) return fail(GB_INVALID_ARGUMENT, "texel count must be >= 0");
+    if (reinterpret_cast<uintptr_t>(padded) & 15) return fail(GB_INVALID_ARGUMENT, "padded texel gradients must be 16-byte aligned");
+    if (gb_status st = set_device(ctx)) return st;
+    ProfScope ps(ctx, GB_K_CHAIN);
+    GB_CUDA(gb::launch_texel_unpad(padded, dst, texels, accumulate != 0, ctx->sm_count, ctx->stream));
+    ctx->launches += texels > 0;
     return GB_OK;
 }
 

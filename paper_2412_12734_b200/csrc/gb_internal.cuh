@@ -112,6 +112,7 @@ struct RasterConst {
     real tex_scale;       // (n-1)/(2 sigma)
     real tex_offset;      // (n-1)/2
     real sigma;
+    int tgs;  // K4 texel-gradient stride: 3 = the reference layout, 4 = RGBA-padded (one 16-B red per texel)
 #ifdef GB_PARITY_F64
     double* trans64;  // parity build: K3 stores the fp64 final transmittance here, K4 rewinds from it
 #endif

@@ -113,6 +113,33 @@ __global__ void __launch_bounds__(256) k_adam_update(float* __restrict__ p, cons
         adam_one(p[i], g[i], m[i], v[i], lr, b1, b2, omb1, omb2, eps, inv_bias1, inv_bias2);
 }
 
+// RGBA-padded texel gradients (K4 with gb_context_set_texel_grad_stride(4)) into the reference layout
+__global__ void __launch_bounds__(256) k_texel_unpad(const float4* __restrict__ padded, float* __restrict__ dst,
+                                                     int64_t texels, bool accumulate) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < texels; t += (int64_t)gridDim.x * blockDim.x) {
+        const float4 g = padded[t];
+        float* d = dst + 3 * t;
+        if (accumulate) {
+            d[0] += g.x;
+            d[1] += g.y;
+            d[2] += g.z;
+        } else {
+            d[0] = g.x;
+            d[1] = g.y;
+            d[2] = g.z;
+        }
+    }
+}
+
+cudaError_t launch_texel_unpad(const float* padded, float* dst, int64_t texels, bool accumulate, int sm_count,
+                               cudaStream_t st) {
+    if (texels <= 0) return cudaSuccess;
+    int64_t blocks = (texels + 255) / 256;
+    if (blocks > (int64_t)sm_count * 16) blocks = (int64_t)sm_count * 16;
+    k_texel_unpad<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(padded), dst, texels, accumulate);
+    return cudaGetLastError();
+}
+
 __global__ void k_adam_flag_init(long long* __restrict__ flag, const int* __restrict__ veto) {
     *flag = (veto && *veto) ? GB_ADAM_FLAG_VETO : GB_ADAM_FLAG_CLEAR;
 }

@@ -76,6 +76,11 @@ struct CellShape {
 };
 
 // offset of reduced texel-gradient value i (corner i / 3, channel i % 3) from the class's base texel
+// Texel-gradient float offset in the gradient buffer's layout for an offset f = 3 * texel + channel of the
+// reference layout (core.hpp:44-48): identity for stride 3, texel * 4 + channel for the RGBA-padded layout
+// (gb_context_set_texel_grad_stride), whose 16-B texel records take one vector red.
+__device__ __forceinline__ int gofs(int f, int S) { return S == 4 ? f + f / 3 : f; }
+
 template <int CELL>
 __device__ __forceinline__ int cell_offset(int i, int N) {
     if (CELL == kCellFull) return corner_offset(i, N);
@@ -85,7 +90,7 @@ __device__ __forceinline__ int cell_offset(int i, int N) {
 
 // One backward entry for the calling warp, after the evaluation: rewind the pixel's state, form the
 // adjoints and reduce/scatter the gradients (raster.hpp:324-363).
-template <int MODE, int NT, int CELL>
+template <int MODE, int NT, int CELL, int S>
 __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, bool on, unsigned act, real u,
                                           real v, real G, real alpha, real araw, const PinholeTerms& pt,
                                           real& T, real g0, real g1, real g2, real& bh0, real& bh1,
@@ -216,13 +221,18 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         bh1 = alpha * c1 + om * bh1;
         bh2 = alpha * c2 + om * bh2;
     }
-    real* gg = grid_grad + (size_t)id * F;
+    // S: the texel-gradient stride, 3 (reference layout) or 4 (RGBA-padded, gb_context_set_texel_grad_stride)
+    real* gg = grid_grad + (size_t)id * (S == 4 ? 4 * N * N : F);
     // this lane's non-zero texels straight to memory: one float2 + one float red each (fp32)
     auto texel_reds = [&]() {
 #pragma unroll
         for (int k = 0; k < NX; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
             if (wk[k] != (real)0)
-                red3(gg + tbase + cell_offset<CELL>(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
+                if (S == 4)
+                    red4(gg + gofs(tbase + cell_offset<CELL>(3 * k, N), 4), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2],
+                         (real)0);
+                else
+                    red3(gg + tbase + cell_offset<CELL>(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
     };
     if (__popc(act) <= kDirectLanes) {
         // few active lanes: each adds its own terms with vector reds -- ~20 instructions for the warp
@@ -258,7 +268,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         const real r2 = smem_reduce<12>(tq, wscratch, lane);
         const int row = lane >> 1, qc = row / 3;
         if ((lane & 1) == 0 && row < 12)
-            red_add(gg + 3 * (((qc >> 1) ? N - 1 : 0) * N + ((qc & 1) ? N - 1 : 0)) + row % 3, r2);
+            red_add(gg + gofs(3 * (((qc >> 1) ? N - 1 : 0) * N + ((qc & 1) ? N - 1 : 0)) + row % 3, S), r2);
         return;
     }
     // texel gradients: one warp reduction when every active lane has the same base texel;
@@ -267,7 +277,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
     if (__all_sync(kFull, !on || tbase == b0)) {
         if (lane == 0) GB_DBG(4, 1);
         const real r2 = smem_reduce<3 * NX>(tg, wscratch, lane);
-        if ((lane & 1) == 0 && (lane >> 1) < 3 * NX) red_add(gg + b0 + cell_offset<CELL>(lane >> 1, N), r2);
+        if ((lane & 1) == 0 && (lane >> 1) < 3 * NX) red_add(gg + gofs(b0 + cell_offset<CELL>(lane >> 1, N), S), r2);
     } else if (on) {
         if (lane == 0) GB_DBG(5, 1);
         texel_reds();
@@ -276,7 +286,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
 
 // One backward entry for the calling warp: evaluate, pick the warp's texel footprint class, then
 // bwd_shade (raster.hpp:324-363).
-template <int MODE, int NT>
+template <int MODE, int NT, int S>
 __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __restrict__ t, int id, int rank,
                                           int last, int x, int y, real& T, real g0, real g1, real g2,
                                           real& bh0, real& bh1, real& bh2, const RasterConst& rc, int N,
@@ -311,7 +321,7 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
         GB_DBG(7, (act & 0x0000FFFFu) && (act & 0xFFFF0000u));  // both 8x2 halves active
     }
 #define GB_SHADE(CELL)                                                                                          \
-    bwd_shade<MODE, NT, CELL>(t, id, on, act, u, v, G, alpha, araw, pt, T, g0, g1, g2, bh0, bh1, bh2, rc, N, \
+    bwd_shade<MODE, NT, CELL, S>(t, id, on, act, u, v, G, alpha, araw, pt, T, g0, g1, g2, bh0, bh1, bh2, rc, N, \
                               lane, wscratch, accum, grid_grad)
     if (N == 1) {
         GB_SHADE(kCellOne);
@@ -536,7 +546,7 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
 }
 
 // render_backward's per-pixel loop (raster.hpp:313-364) for the calling warp's pixels
-template <int MODE, int NT>
+template <int MODE, int NT, int S>
 __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __restrict__ values,
                                          const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                          const float* __restrict__ tex, const CamConst& cc, const RasterConst& rc,
@@ -574,7 +584,7 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
             h.h1 = ld_real4(&hdr[id].h1);
             h.h2 = ld_real4(&hdr[id].h2);
 #endif
-            bwd_entry<MODE, NT>(h, tex + (size_t)id * F, id, c0 + bit, last, wp.x, wp.y, T, g0, g1, g2, bh0, bh1,
+            bwd_entry<MODE, NT, S>(h, tex + (size_t)id * F, id, c0 + bit, last, wp.x, wp.y, T, g0, g1, g2, bh0, bh1,
                                 bh2, rc, N, lane, wscratch, accum, grid_grad);
         }
     }
@@ -674,7 +684,7 @@ __device__ __forceinline__ void fwd_walk_staged(const uint2 range, const int32_t
     }
 }
 
-template <int MODE, int NT>
+template <int MODE, int NT, int S>
 __device__ __forceinline__ void bwd_walk_staged(const uint2 range, const int32_t* __restrict__ values,
                                                 const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                                 const float* __restrict__ tex, const CamConst& cc,
@@ -708,7 +718,7 @@ __device__ __forceinline__ void bwd_walk_staged(const uint2 range, const int32_t
                 const int bit = 31 - __clz(mask);
                 mask &= ~(1u << bit);
                 const int id = b.id[bit];
-                bwd_entry<MODE, NT>(staged_header(b, bit), tex + (size_t)id * 3 * N * N, id, c0 + bit, last, wp.x,
+                bwd_entry<MODE, NT, S>(staged_header(b, bit), tex + (size_t)id * 3 * N * N, id, c0 + bit, last, wp.x,
                                     wp.y, T, g0, g1, g2, bh0, bh1, bh2, rc, N, lane, wscratch, accum, grid_grad);
             }
         }
@@ -811,7 +821,7 @@ __global__ void __launch_bounds__(256) k_forward_loss(const uint2* __restrict__ 
 #ifndef GB_K4_MINB
 #define GB_K4_MINB 5
 #endif
-template <int MODE, int NT>
+template <int MODE, int NT, int S>
 __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2* __restrict__ ranges,
                                                          const int32_t* __restrict__ values,
                                                          const ScreenHeader* __restrict__ hdr,
@@ -839,14 +849,14 @@ __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2
 #ifdef GB_STAGE_HEADERS
     __shared__ StageChunk ring[2];
     __shared__ int s_top;
-    bwd_walk_staged<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1,
+    bwd_walk_staged<MODE, NT, S>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1,
                               g2, red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad, ring,
                               &s_top);
 #else
     __shared__ WarpHeaders whs[8];
-    bwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1, g2,
-                       red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad,
-                       &whs[threadIdx.x >> 5]);
+    bwd_walk<MODE, NT, S>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1,
+                          g2, red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad,
+                          &whs[threadIdx.x >> 5]);
 #endif
 }
 
@@ -913,7 +923,7 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
     if ((threadIdx.x & 31) == 0 && loss && l != (real)0) atomicAdd(loss, (float)(l * scale));
-    bwd_walk<MODE, NT>(range, values, hdr, cull, tex, cc, rc, N, wp, last, T, g0, g1, g2,
+    bwd_walk<MODE, NT, 3>(range, values, hdr, cull, tex, cc, rc, N, wp, last, T, g0, g1, g2,
                        red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad,
                        &whs[threadIdx.x >> 5]);
 }
@@ -948,8 +958,14 @@ static cudaError_t bwdd_t(int tiles, int threads, cudaStream_t st, const uint2* 
                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                           const RasterConst& rc, int n, const float* trans, const int32_t* last,
                           const float* image_grad, real* accum, real* grid_grad) {
-    k_backward_direct<MODE, NT><<<tiles, threads, red_smem(threads), st>>>(ranges, values, hdr, cull, tex, cc, rc, n,
-                                                                           trans, last, image_grad, accum, grid_grad);
+    if (rc.tgs == 4)
+        k_backward_direct<MODE, NT, 4><<<tiles, threads, red_smem(threads), st>>>(ranges, values, hdr, cull, tex, cc,
+                                                                                  rc, n, trans, last, image_grad,
+                                                                                  accum, grid_grad);
+    else
+        k_backward_direct<MODE, NT, 3><<<tiles, threads, red_smem(threads), st>>>(ranges, values, hdr, cull, tex, cc,
+                                                                                  rc, n, trans, last, image_grad,
+                                                                                  accum, grid_grad);
     return cudaGetLastError();
 }
 

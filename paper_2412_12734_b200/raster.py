@@ -502,9 +502,32 @@ def render_forward(splats: SplatSet, camera, binning: TileBinning, out: RenderOu
     return out
 
 
+class _TexelStride:
+    """Within the block, the context's backwards write texel gradients into ``padded`` (RGBA, stride 4:
+    gb_context_set_texel_grad_stride) instead of the gradient buffer's reference-layout grid group."""
+
+    def __init__(self, ctx, g, padded, grid_numel):
+        self.ctx, self.g, self.padded, self.grid_numel = ctx, g, padded, grid_numel
+
+    def __enter__(self):
+        if self.padded is not None:
+            if self.padded.numel() * 3 != 4 * self.grid_numel or self.padded.data_ptr() % 16:
+                raise ValueError("texel_grad: padded buffer must hold K*n*n*4 floats, 16-byte aligned")
+            self.g.grid_values = self.padded.data_ptr()
+            check(lib.gb_context_set_texel_grad_stride(self.ctx.handle, 4), "gb_context_set_texel_grad_stride")
+        return self.g
+
+    def __exit__(self, *a):
+        if self.padded is not None:
+            check(lib.gb_context_set_texel_grad_stride(self.ctx.handle, 3), "gb_context_set_texel_grad_stride")
+
+
 def render_backward(splats: SplatSet, camera, binning: TileBinning, output: RenderOutput,
-                    image_grad: torch.Tensor, grads: GradientBuffer = None) -> GradientBuffer:
-    """raster.hpp:277-387.  Accumulates into ``grads`` (a fresh zeroed buffer by default)."""
+                    image_grad: torch.Tensor, grads: GradientBuffer = None,
+                    texel_grad: torch.Tensor = None) -> GradientBuffer:
+    """raster.hpp:277-387.  Accumulates into ``grads`` (a fresh zeroed buffer by default).  ``texel_grad``: an
+    RGBA-padded (K*n*n*4) buffer that receives the texel gradients instead of ``grads.grid`` (convert with
+    texel_grads_unpad)."""
     ctx = context(splats.device)
     if grads is None:
         grads = GradientBuffer(splats)
@@ -512,14 +535,24 @@ def render_backward(splats: SplatSet, camera, binning: TileBinning, output: Rend
         raise ValueError("render_backward: image_grad size mismatch")
     image_grad = image_grad.contiguous()
     s, cam, g = splats.to_c(), camera.to_c(), grads.to_c()
-    check(lib.gb_render_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(output._c),
-                                 _ptr(image_grad), C.byref(g)), "render_backward")
+    with _TexelStride(ctx, g, texel_grad, grads.grid.numel()) as g:
+        check(lib.gb_render_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(output._c),
+                                     _ptr(image_grad), C.byref(g)), "render_backward")
     return grads
+
+
+def texel_grads_unpad(padded: torch.Tensor, dst: torch.Tensor, accumulate: bool = False) -> None:
+    """dst (reference layout, K*n*n*3) (+)= the RGBA-padded texel gradients (K*n*n*4), on the current stream."""
+    if padded.numel() * 3 != dst.numel() * 4:
+        raise ValueError("texel_grads_unpad: size mismatch")
+    check(lib.gb_texel_grads_unpad(context(dst.device).handle, _ptr(padded), _ptr(dst), padded.numel() // 4,
+                                   int(accumulate)), "gb_texel_grads_unpad")
 
 
 def render_loss_backward(splats: SplatSet, camera, binning: TileBinning, target: torch.Tensor, loss: str = "l1",
                          scale: float = None, grads: GradientBuffer = None, loss_acc: torch.Tensor = None,
-                         output: RenderOutput = None, image_grad: torch.Tensor = None):
+                         output: RenderOutput = None, image_grad: torch.Tensor = None,
+                         texel_grad: torch.Tensor = None):
     """render_forward + l1_loss / mse_loss + render_backward of one view in one pass
     (train.hpp:120-133 around raster.hpp:201-387).  Returns (loss_acc, grads); ``loss_acc``
     (a device float, zero by default) and ``grads`` accumulate.  ``output`` / ``image_grad``,
@@ -540,10 +573,11 @@ def render_loss_backward(splats: SplatSet, camera, binning: TileBinning, target:
         raise ValueError("render_loss_backward: image_grad size mismatch")
     target = target.contiguous()
     s, cam, g = splats.to_c(), camera.to_c(), grads.to_c()
-    check(lib.gb_render_loss_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, _ptr(target),
-                                      kinds[loss], scale, C.byref(output._c) if output is not None else None,
-                                      _ptr(image_grad) if image_grad is not None else None, _ptr(loss_acc),
-                                      C.byref(g)), "render_loss_backward")
+    with _TexelStride(ctx, g, texel_grad, grads.grid.numel()) as g:
+        check(lib.gb_render_loss_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, _ptr(target),
+                                          kinds[loss], scale, C.byref(output._c) if output is not None else None,
+                                          _ptr(image_grad) if image_grad is not None else None, _ptr(loss_acc),
+                                          C.byref(g)), "render_loss_backward")
     return loss_acc, grads
 
 

@@ -26,7 +26,7 @@ from ._lib import check, lib
 
 from .raster import (AdamConfig, AdamState, GradientBuffer, LearningRates, RasterConfig, RenderOutput, SplatSet,
                      StepGraph, TileBinning, adam_step, all_contexts, build_binning, context, l1_loss,
-                     copy_h2d, memset_, render_backward, render_forward, render_loss_backward)
+                     copy_h2d, memset_, render_backward, render_forward, render_loss_backward, texel_grads_unpad)
 
 
 def shard_views(n_views: int, rank: int, world: int, per_rank: Optional[int] = None) -> List[int]:
@@ -260,7 +260,8 @@ class ViewShardedTrainer:
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
                  lanes: int = 4, fused: bool = False, async_binning: bool = True, graph: bool = False,
-                 capacity_margin: float = 1.1, sharded_adam: bool = True, overlap_adam: bool = True):
+                 capacity_margin: float = 1.1, sharded_adam: bool = True, overlap_adam: bool = True,
+                 texel_pad: bool = True):
         self.splats = splats
         self.cameras = list(cameras)
         self.views = list(views)
@@ -291,6 +292,10 @@ class ViewShardedTrainer:
         self.check_finite = check_finite
         self.fused = fused
         dev = splats.device
+        # the views' K4s add texel gradients into an RGBA-padded scratch (one 16-B red per texel), converted into
+        # the flat buffer's reference-layout grid group once per step (gb_texel_grads_unpad)
+        self._tex_pad = (torch.zeros(self.grads.grid.numel() // 3 * 4, dtype=torch.float32, device=dev)
+                         if texel_pad else None)
         # lane 0 is the caller's stream, except under graph capture (which needs a side stream)
         main = torch.cuda.Stream(device=dev) if graph else torch.cuda.current_stream(dev)
         self._lanes = [_Lane(dev, main if i == 0 else torch.cuda.Stream(device=dev)) for i in range(max(1, lanes))]
@@ -352,10 +357,10 @@ class ViewShardedTrainer:
         lane = self._lane(i)
         if self.fused:
             render_loss_backward(self.splats, cam, lane.binning, target, "l1", grads=self.grads,
-                                 loss_acc=self.losses[i:i + 1])
+                                 loss_acc=self.losses[i:i + 1], texel_grad=self._tex_pad)
             return
         l1_loss(out.color, target.view(cam.height, cam.width, 3), grad=gimg, loss=self.losses[i:i + 1])
-        render_backward(self.splats, cam, lane.binning, out, gimg, self.grads)
+        render_backward(self.splats, cam, lane.binning, out, gimg, self.grads, texel_grad=self._tex_pad)
 
     def wait_adam(self) -> None:
         """Order the current stream after the step's texel update (overlap_adam)."""
@@ -369,6 +374,8 @@ class ViewShardedTrainer:
             memset_(self.grads.flat[:o])
         else:
             memset_(self.grads.flat)
+        if self._tex_pad is not None:
+            memset_(self._tex_pad)
         memset_(self.losses)
         self._step_start.record(main)
         for lane in self._lanes[1:]:
@@ -381,7 +388,8 @@ class ViewShardedTrainer:
             with torch.cuda.stream(a):
                 check(lib.gb_stream_wait_event(context(self.splats.device).handle,
                                                C.c_void_p(self._grid_done.cuda_event), 1), "gb_stream_wait_event")
-                memset_(self.grads.grid)
+                if self._tex_pad is None:  # (padded: the grid group is overwritten by the unpad at the join)
+                    memset_(self.grads.grid)
                 self._grid_ready.record(a)
             self._waited = set()
 
@@ -392,6 +400,8 @@ class ViewShardedTrainer:
             main.wait_event(lane.done)
         if self.overlap_adam:
             main.wait_event(self._grid_ready)  # the side stream rejoins (a graph capture needs it)
+        if self._tex_pad is not None:  # after the previous step's texel update read the grid group
+            texel_grads_unpad(self._tex_pad, self.grads.grid.view(-1), accumulate=False)
 
     def _on_lanes(self, body) -> None:
         """Run body() with lane 0 as the current stream, ordered after and before the caller's stream."""

@@ -503,3 +503,35 @@ def test_comm_c_abi_single_rank():
     bad = lib.gb_allreduce_grads(ctx.handle, None, x.data_ptr(), 4)
     assert bad == _lib.GB_INVALID_ARGUMENT
     check(lib.gb_comm_destroy(h), "gb_comm_destroy")
+
+
+def test_padded_texel_gradients_match_reference_layout():
+    """K4 with the RGBA-padded texel-gradient layout (gb_context_set_texel_grad_stride(4), then
+    gb_texel_grads_unpad) gives the reference layout's texel gradients (atomics order aside) and leaves the
+    other groups unchanged; the padding floats are never written."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+
+    for n in (3, 8):
+        c = sc.baseline_config(0, count=20_000, n=n)
+        s = gb.SplatSet.from_numpy(c.mode, gb.ColorGridConfig(n), **c.arrays())
+        cam = gb.PinholeCamera.from_spec(c.cameras[0])
+        b = gb.build_binning(s, cam)
+        out = gb.render_forward(s, cam, b)
+        ig = torch.sign(torch.randn((cam.height, cam.width, 3), device="cuda"))
+        ref = gb.render_backward(s, cam, b, out, ig)
+        pad = torch.full((ref.grid.numel() // 3 * 4,), 7.0, device="cuda")
+        pad.view(-1, 4)[:, :3] = 0.0
+        got = gb.render_backward(s, cam, b, out, ig, texel_grad=pad)
+        torch.cuda.synchronize()
+        assert bool((pad.view(-1, 4)[:, 3] == 7.0).all())
+        assert float(got.grid.abs().max()) == 0.0  # the reference-layout group was not touched
+        pad.view(-1, 4)[:, 3] = 0.0
+        gb.raster.texel_grads_unpad(pad, got.grid.view(-1))
+        torch.cuda.synchronize()
+        for k, v in ref.tensors().items():
+            w = got.tensors()[k]
+            scale = float(v.abs().max()) + 1e-30
+            assert float((w - v).abs().max()) <= 1e-5 * scale, (n, k)
