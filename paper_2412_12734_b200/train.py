@@ -305,10 +305,13 @@ class ViewShardedTrainer:
         self.losses = torch.zeros(max(1, len(self.views)), dtype=torch.float32, device=dev)
         self._pinned_losses = torch.zeros(max(1, len(self.views)), dtype=torch.float32, pin_memory=True)
         self._pinned_flag = torch.zeros(1, dtype=torch.int64, pin_memory=True)
-        self._target_buf = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+        # two target buffers per view lane: every lane's view can have its target landed while the copy stream
+        # runs ahead (with two buffers for four lanes, lanes 3-4 waited for a free buffer)
+        nbuf = 2 * len(self._lanes)
+        self._target_buf = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(nbuf)]
         self._copy_stream = torch.cuda.Stream(device=dev)
-        self._copy_done = [torch.cuda.Event() for _ in range(2)]
-        self._buf_free = [torch.cuda.Event() for _ in range(2)]
+        self._copy_done = [torch.cuda.Event() for _ in range(nbuf)]
+        self._buf_free = [torch.cuda.Event() for _ in range(nbuf)]
         self._step_start = torch.cuda.Event()
         self.pairs: List[int] = []  # blocking mode: pair count P of every view binned (roofline bytes)
         # capacity mode (async_binning): after one blocking step sizes the pair buffers, builds never read P
@@ -584,8 +587,10 @@ class ViewShardedTrainer:
         self._begin()
         n = len(self.views)
 
+        nbuf = len(self._target_buf)
+
         def issue(i):
-            b = i % 2
+            b = i % nbuf
             with torch.cuda.stream(self._copy_stream):
                 self._copy_stream.wait_event(self._buf_free[b])
                 t = targets_host[i]
@@ -595,14 +600,15 @@ class ViewShardedTrainer:
                 copy_h2d(self._target_buf[b], t)
                 self._copy_done[b].record(self._copy_stream)
 
-        for b in range(2):
+        for b in range(nbuf):
             self._buf_free[b].record(main)
-        if n:
-            issue(0)
+        ahead = nbuf - 1  # copies in flight ahead of the view being issued
+        for i in range(min(n, ahead)):
+            issue(i)
         for i in range(n):
-            b = i % 2
-            if i + 1 < n:
-                issue(i + 1)
+            b = i % nbuf
+            if i + ahead < n:
+                issue(i + ahead)
             s = self._lane(i).stream
             with torch.cuda.stream(s):
                 cam, out, gimg = self._view_forward(i)
