@@ -353,10 +353,12 @@ def run_ours(args):
         ev3.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        e2e_dev = ev2.elapsed_time(ev3) / args.steps
         e2e_ms = max_over_ranks(max(ev2.elapsed_time(ev3), wall * 1e3)) / args.steps
         h2d = sum(t.numel() * 4 for t in host_targets)
         e2e = {"value": round(mpix / (e2e_ms / 1e3), 3), "unit": "MP/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": len(views) * 4, "ms_per_step": round(e2e_ms, 3)}
+               "d2h_bytes_per_step": len(views) * 4, "ms_per_step": round(e2e_ms, 3),
+               "device_ms_per_step": round(e2e_dev, 3), "wall_ms_per_step": round(wall * 1e3 / args.steps, 3)}
 
     # ---- forward only (render: K1 + K2 + K3 per view, one stream), SURVEY §8(d)'s "fwd" figure ----
     fwd = None

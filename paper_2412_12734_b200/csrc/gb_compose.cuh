@@ -16,6 +16,7 @@ __device__ __forceinline__ int tex_n(int n_rt) {
 }
 
 struct Bilin {
+    int t00;  // texel index of (i_u, i_v)
     int o00;  // offset of texel (i_u, i_v) channel 0
     real fu, fv;
     real w00, w10, w01, w11;
@@ -31,7 +32,8 @@ __device__ __forceinline__ void bilin_setup(real u, real v, int N, const RasterC
     t = rmin(rmax(t, (real)0), (real)(N - 1));
     iv = min((int)rfloor(t), N - 2);
     b.fv = sub_rn(t, (real)iv);
-    b.o00 = (iu * N + iv) * 3;
+    b.t00 = iu * N + iv;
+    b.o00 = b.t00 * 3;
     const real gu = (real)1 - b.fu, gv = (real)1 - b.fv;
     b.w00 = gu * gv;
     b.w10 = b.fu * gv;

@@ -76,16 +76,12 @@ struct CellShape {
 };
 
 // offset of reduced texel-gradient value i (corner i / 3, channel i % 3) from the class's base texel
-// Texel-gradient float offset in the gradient buffer's layout for an offset f = 3 * texel + channel of the
-// reference layout (core.hpp:44-48): identity for stride 3, texel * 4 + channel for the RGBA-padded layout
-// (gb_context_set_texel_grad_stride), whose 16-B texel records take one vector red.
-__device__ __forceinline__ int gofs(int f, int S) { return S == 4 ? f + f / 3 : f; }
-
+// texel-index offset of the class's corner k from its base texel (texel index i_u * n + i_v, core.hpp:44-48)
 template <int CELL>
-__device__ __forceinline__ int cell_offset(int i, int N) {
-    if (CELL == kCellFull) return corner_offset(i, N);
-    if (CELL == kCellU) return i < 3 ? i : 3 * N + i - 3;  // (i_u, i_v'), (i_u + 1, i_v')
-    return i;                                              // kCellV: (i_u', i_v), (i_u', i_v + 1); kCellOne
+__device__ __forceinline__ int cell_texel(int k, int N) {
+    if (CELL == kCellFull) return ((k & 1) ? N : 0) + ((k & 2) ? 1 : 0);  // 00, 10, 01, 11
+    if (CELL == kCellU) return k ? N : 0;                                  // (i_u, i_v'), (i_u + 1, i_v')
+    return k;                                                              // kCellV: (i_u', i_v), (i_u', i_v + 1)
 }
 
 // One backward entry for the calling warp, after the evaluation: rewind the pixel's state, form the
@@ -98,7 +94,6 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
                                           real* __restrict__ accum, real* __restrict__ grid_grad) {
     constexpr int NS = MODE == GB_MODE_ORTHO ? 7 : 10;  // screen-space sums per entry
     constexpr int NX = CellShape<CELL>::texels;
-    const int F = 3 * N * N;
     const real sigma = rc.sigma;
     real red[16];  // screen-space sums (NS of 16 slots)
 #pragma unroll
@@ -106,7 +101,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
     real tg[3 * NX];
 #pragma unroll
     for (int i = 0; i < 3 * NX; ++i) tg[i] = (real)0;
-    int tbase = -1;
+    int tt = -1;  // base texel index of the entry's footprint class
     real wk[NX];  // corner weights
 #pragma unroll
     for (int k = 0; k < NX; ++k) wk[k] = (real)0;
@@ -135,7 +130,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
                 fu_hat = fma_rn(chat[c], fma_rn(b.fv, e, du), fu_hat);
                 fv_hat = fma_rn(chat[c], fma_rn(b.fu, e, dv), fv_hat);
             }
-            tbase = b.o00;
+            tt = b.t00;
             wk[0] = b.w00;
             wk[1] = b.w10;
             wk[2] = b.w01;
@@ -149,8 +144,8 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             const real f = sub_rn(sx, (real)i0);
             const real gf = (real)1 - f;
             const int other = (CELL == kCellU ? v : u) > (real)0 ? N - 1 : 0;
-            tbase = (CELL == kCellU ? i0 * N + other : other * N + i0) * 3;
-            const float* pa = t + tbase;
+            tt = CELL == kCellU ? i0 * N + other : other * N + i0;
+            const float* pa = t + 3 * tt;
             const float* pb = pa + (CELL == kCellU ? 3 * N : 3);
             real fh = (real)0;
 #pragma unroll
@@ -169,10 +164,10 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             wk[1] = f;
         } else {  // kCellOne (and n = 1): a single texel with weight 1
             const int iu = N > 1 && u > (real)0 ? N - 1 : 0, iv = N > 1 && v > (real)0 ? N - 1 : 0;
-            tbase = (iu * N + iv) * 3;
+            tt = iu * N + iv;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                cc_[c] = t[tbase + c];
+                cc_[c] = t[3 * tt + c];
                 tg[c] = chat[c];
             }
             wk[0] = (real)1;
@@ -221,18 +216,20 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         bh1 = alpha * c1 + om * bh1;
         bh2 = alpha * c2 + om * bh2;
     }
-    // S: the texel-gradient stride, 3 (reference layout) or 4 (RGBA-padded, gb_context_set_texel_grad_stride)
-    real* gg = grid_grad + (size_t)id * (S == 4 ? 4 * N * N : F);
-    // this lane's non-zero texels straight to memory: one float2 + one float red each (fp32)
+    // S: the texel-gradient stride, 3 (reference layout (i_u, i_v, channel)) or 4 (RGBA-padded,
+    // gb_context_set_texel_grad_stride: texel records 16-B aligned, one vector red each)
+    real* gg = grid_grad + (size_t)id * (S * N * N);
+    // this lane's non-zero texels straight to memory: one 16-B red (S = 4) or an 8-B + 4-B pair (S = 3)
     auto texel_reds = [&]() {
 #pragma unroll
         for (int k = 0; k < NX; ++k)  // a zero corner weight (clamped or on-grid uv) adds nothing
-            if (wk[k] != (real)0)
+            if (wk[k] != (real)0) {
+                real* p = gg + S * (tt + cell_texel<CELL>(k, N));
                 if (S == 4)
-                    red4(gg + gofs(tbase + cell_offset<CELL>(3 * k, N), 4), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2],
-                         (real)0);
+                    red4(p, tg[3 * k], tg[3 * k + 1], tg[3 * k + 2], (real)0);
                 else
-                    red3(gg + tbase + cell_offset<CELL>(3 * k, N), tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
+                    red3(p, tg[3 * k], tg[3 * k + 1], tg[3 * k + 2]);
+            }
     };
     if (__popc(act) <= kDirectLanes) {
         // few active lanes: each adds its own terms with vector reds -- ~20 instructions for the warp
@@ -268,16 +265,17 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         const real r2 = smem_reduce<12>(tq, wscratch, lane);
         const int row = lane >> 1, qc = row / 3;
         if ((lane & 1) == 0 && row < 12)
-            red_add(gg + gofs(3 * (((qc >> 1) ? N - 1 : 0) * N + ((qc & 1) ? N - 1 : 0)) + row % 3, S), r2);
+            red_add(gg + S * (((qc >> 1) ? N - 1 : 0) * N + ((qc & 1) ? N - 1 : 0)) + row % 3, r2);
         return;
     }
     // texel gradients: one warp reduction when every active lane has the same base texel;
     // otherwise each lane adds its own texels -- cheaper than a reduction per distinct cell
-    const int b0 = __shfl_sync(kFull, tbase, __ffs(act) - 1);
-    if (__all_sync(kFull, !on || tbase == b0)) {
+    const int b0 = __shfl_sync(kFull, tt, __ffs(act) - 1);
+    if (__all_sync(kFull, !on || tt == b0)) {
         if (lane == 0) GB_DBG(4, 1);
         const real r2 = smem_reduce<3 * NX>(tg, wscratch, lane);
-        if ((lane & 1) == 0 && (lane >> 1) < 3 * NX) red_add(gg + gofs(b0 + cell_offset<CELL>(lane >> 1, N), S), r2);
+        const int i = lane >> 1;
+        if ((lane & 1) == 0 && i < 3 * NX) red_add(gg + S * (b0 + cell_texel<CELL>(i / 3, N)) + i % 3, r2);
     } else if (on) {
         if (lane == 0) GB_DBG(5, 1);
         texel_reds();
@@ -958,6 +956,14 @@ static cudaError_t bwdd_t(int tiles, int threads, cudaStream_t st, const uint2* 
                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                           const RasterConst& rc, int n, const float* trans, const int32_t* last,
                           const float* image_grad, real* accum, real* grid_grad) {
+    // the fp64 parity build's scratch (static header slots + dynamic reduction rows) exceeds the 48 KB default
+    static const cudaError_t opt_in =
+        cudaFuncSetAttribute(k_backward_direct<MODE, NT, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)red_smem(256)) == cudaSuccess
+            ? cudaFuncSetAttribute(k_backward_direct<MODE, NT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)red_smem(256))
+            : cudaErrorInvalidValue;
+    if (opt_in != cudaSuccess) return opt_in;
     if (rc.tgs == 4)
         k_backward_direct<MODE, NT, 4><<<tiles, threads, red_smem(threads), st>>>(ranges, values, hdr, cull, tex, cc,
                                                                                   rc, n, trans, last, image_grad,
