@@ -595,7 +595,10 @@ static double uv_error32(const raster_ctx_t *c, const geom_t *g, double px, doub
  * the evaluation's own fp32 uncertainty when larger -- dalpha/alpha = |u| du + |v| dv (G = exp(-(u^2+v^2)/2))
  * plus the exponential's and the product's rounding -- which dominates for thin, grazing splats. */
 static double alpha_margin(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
-    const double e = 2.0 * ((fabs(u) + fabs(v)) * uv_error32_raw(c, g, px, py, u, v) + 8.0 * kEps32);
+    double e = 2.0 * ((fabs(u) + fabs(v)) * uv_error32_raw(c, g, px, py, u, v) + 8.0 * kEps32);
+    /* first-order in the relative error of alpha: capped, so that an evaluation whose alpha is far below
+     * the threshold (huge |u|, G ~ 0) is never taken for one near it */
+    if (e > 0.5) e = 0.5;
     return e > c->kink->alpha_rel ? e : c->kink->alpha_rel;
 }
 

@@ -535,3 +535,27 @@ def test_padded_texel_gradients_match_reference_layout():
             w = got.tensors()[k]
             scale = float(v.abs().max()) + 1e-30
             assert float((w - v).abs().max()) <= 1e-5 * scale, (n, k)
+
+
+def test_pair_capacity_limits():
+    """The pair count is indexed with int by the sorts: the C-ABI rejects capacities >= 2^31 - 1 and the
+    trainer never inflates a capacity past it (the 1.1 margin could overflow the sort's int)."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200._lib import InvalidArgument
+    from paper_2412_12734_b200.train import PAIR_LIMIT, ViewShardedTrainer
+
+    b = gb.TileBinning()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with pytest.raises(InvalidArgument):
+        b.set_capacity(2 ** 31 - 1, flag)
+    b.set_capacity(2 ** 31 - 2, flag)  # the largest accepted
+    b.set_capacity(0, flag)
+    n, arrays, specs, targets = _trainer_scene()
+    s = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    tr = ViewShardedTrainer(s, [gb.PinholeCamera.from_spec(c) for c in specs], [0, 1, 2])
+    tr._set_capacity(PAIR_LIMIT - 100)  # the 1.1x margin is clamped below the limit
+    assert tr.capacity == PAIR_LIMIT - 1
+    with pytest.raises(RuntimeError):
+        tr._set_capacity(PAIR_LIMIT)

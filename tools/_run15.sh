@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+python -m pytest tests/test_gpu_configs4.py tests/test_gpu_parity.py -x -q > gpurun_out/r2_p15.log 2>&1; echo "parity rc=$?"; tail -3 gpurun_out/r2_p15.log
+python -c "
+import json
+for f in ['parity_configs4_K4000000_T1','parity_configs4_K4000000_T16','parity_configs4_K1000000_T4','parity_configs2_fwd_bwd','parity_configs1_fwd_bwd']:
+    d=json.load(open('gpurun_out/'+f+'.json')); print(f, d['image']['kink_pixels'], {k:(v['strict_violations_applicable'],v['model_violations']) for k,v in d['grads'].items()})
+"
