@@ -168,8 +168,9 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------------
 # CPU legs (oracle = test infrastructure; only the cpu_baseline and --impl reference legs use it)
 # ---------------------------------------------------------------------------------------------
-def cpu_view(scene64, cam, target, step_frac_adam=0.125):
-    """One view of the workload on the host: binning + forward + L1 + backward (+ 1/8 of Adam)."""
+def cpu_view(scene64, cam, target, step_frac_adam=1.0 / 64):
+    """One view of the workload on the host: binning + forward + L1 + backward (+ its 1/64 share of the
+    step's Adam: one update per 64-view step)."""
     from oracle import oracle as O
 
     cfg = O.Cfg()
@@ -220,10 +221,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
         "ms_per_view": round(step_s * 1e3, 1), "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[3] shapes)",
-        "config": {"workload": "configs[3] view: 1M surfels, 8x8 fp32 textures, 1600x1064, fwd+bwd+L1 (+1/8 Adam)",
+        "config": {"workload": "configs[3] view: 1M surfels, 8x8 fp32 textures, 1600x1064, fwd+bwd+L1 (+1/64 of the step's Adam)",
                    "views_per_step": 1},
         "cpu_baseline": {"value": round(mps, 4), "unit": "MP/s", "cores": cores, "kind": "port",
-                         "sample": "one full configs[3] view per step (binning + forward + L1 + backward + 1/8 "
+                         "sample": "one full configs[3] view per step (binning + forward + L1 + backward + 1/64 of the step's "
                                    "Adam), fp64 C restatement of the reference algorithm (oracle/gb_oracle.c), "
                                    f"{cores} threads; the compiled reference has no perspective path"},
         "e2e": {"value": round(mps, 4), "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -487,7 +488,7 @@ def run_ours(args):
             cores = os.cpu_count() or 1
             line["cpu_baseline"] = {
                 "value": round(W * H / 1e6 / dt, 4), "unit": "MP/s", "cores": cores, "kind": "port",
-                "sample": f"1 view of the workload (binning+forward+L1+backward+1/8 Adam) in {dt:.1f} s, fp64 C "
+                "sample": f"1 view of the workload (binning+forward+L1+backward+1/64 of the step's Adam) in {dt:.1f} s, fp64 C "
                           f"restatement of the reference algorithm (oracle/gb_oracle.c), {cores} threads"}
         except Exception as e:  # the baseline never blocks the GPU number
             line["cpu_baseline"] = {"value": None, "unit": "MP/s", "cores": os.cpu_count(), "kind": "port",

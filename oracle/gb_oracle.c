@@ -595,12 +595,14 @@ static double uv_error32(const raster_ctx_t *c, const geom_t *g, double px, doub
  * the evaluation's own fp32 uncertainty when larger -- dalpha/alpha = |u| du + |v| dv (G = exp(-(u^2+v^2)/2))
  * plus the exponential's and the product's rounding -- which dominates for thin, grazing splats. */
 static double alpha_margin(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
-    double e = 2.0 * ((fabs(u) + fabs(v)) * uv_error32_raw(c, g, px, py, u, v) + 8.0 * kEps32);
-    /* first-order in the relative error of alpha: capped, so that an evaluation whose alpha is far below
-     * the threshold (huge |u|, G ~ 0) is never taken for one near it */
-    if (e > 0.5) e = 0.5;
+    const double e = 2.0 * ((fabs(u) + fabs(v)) * uv_error32_raw(c, g, px, py, u, v) + 8.0 * kEps32);
     return e > c->kink->alpha_rel ? e : c->kink->alpha_rel;
 }
+
+/* alpha within the relative uncertainty m of threshold t, in log space (|ln(alpha / t)| <= m): for small m
+ * the usual |alpha - t| <= m t; for a large m (an fp32-ill-conditioned evaluation) a factor e^m either way,
+ * and never an alpha that underflowed far below the threshold. */
+static int near_threshold(double alpha, double t, double m) { return alpha > 0.0 && fabs(log(alpha / t)) <= m; }
 
 static int sensitive(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
     return c->kink && c->kink->cond_min > 0.0 && uv_error32(c, g, px, py, u, v) > c->kink->cond_min;
@@ -633,8 +635,8 @@ static void forward_tile(void *vctx, int tile) {
                 const double alpha = dmin(alpha_raw, kMaxAlpha);
                 if (kk) {
                     const double am = alpha_margin(c, g, px, py, u, v);
-                    if (cfg->alpha_skip > 0.0 && fabs(alpha - cfg->alpha_skip) <= am * cfg->alpha_skip) flag |= 1;
-                    if (fabs(alpha_raw - kMaxAlpha) <= am * kMaxAlpha) flag |= 1;
+                    if (cfg->alpha_skip > 0.0 && near_threshold(alpha, cfg->alpha_skip, am)) flag |= 1;
+                    if (near_threshold(alpha_raw, kMaxAlpha, am)) flag |= 1;
                     if (alpha >= cfg->alpha_skip && sensitive(c, g, px, py, u, v)) flag |= 4;
                 }
                 if (alpha < cfg->alpha_skip) continue;
@@ -864,7 +866,7 @@ static void backward_tile(void *vctx, int tile) {
                     if (!eval_uv(c, g, px, py, &u, &v, a, b, &cz)) continue;
                     const double weight = gaussian_weight(u, v);
                     const double alpha = dmin(g->alpha_k * weight, kMaxAlpha);
-                    if (fabs(alpha - cfg->alpha_skip) <= alpha_margin(c, g, px, py, u, v) * cfg->alpha_skip)
+                    if (near_threshold(alpha, cfg->alpha_skip, alpha_margin(c, g, px, py, u, v)))
                         add_abs_terms(c, g, px, py, u, v, alpha, weight, t, gacc, behind,
                                       c->s->grid + (size_t)id * tex_stride, a, b, cz, pslk + (size_t)rank * stride);
                 }
@@ -881,7 +883,7 @@ static void backward_tile(void *vctx, int tile) {
                 if (alpha < cfg->alpha_skip) {
                     /* an entry skipped just below the threshold may be composited in fp32 */
                     if (pslk && (px_flag & 1) && kk &&
-                        fabs(alpha - cfg->alpha_skip) <= alpha_margin(c, g, px, py, u, v) * cfg->alpha_skip)
+                        near_threshold(alpha, cfg->alpha_skip, alpha_margin(c, g, px, py, u, v)))
                         add_abs_terms(c, g, px, py, u, v, alpha, weight, t, gacc, behind, gridk, a, b, cz,
                                       pslk + (size_t)rank * stride);
                     continue;
