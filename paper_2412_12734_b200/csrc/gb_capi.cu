@@ -317,6 +317,9 @@ gb::RasterConst make_raster_const(const gb_context* ctx, const gb_binning* b, in
 #else
     rc.tgs = ctx->texel_grad_stride;
 #endif
+#ifdef GB_DEBUG_CHECKS
+    rc.dbg_K = b->K;
+#endif
     return rc;
 }
 

@@ -34,6 +34,7 @@ __device__ __forceinline__ void bilin_setup(real u, real v, int N, const RasterC
     b.fv = sub_rn(t, (real)iv);
     b.t00 = iu * N + iv;
     b.o00 = b.t00 * 3;
+    GB_CHECK(N >= 2 && b.t00 >= 0 && b.t00 + N + 1 < N * N);
     const real gu = (real)1 - b.fu, gv = (real)1 - b.fv;
     b.w00 = gu * gv;
     b.w10 = b.fu * gv;

@@ -34,6 +34,20 @@ typedef float real;
 typedef float4 real4;
 #endif
 
+// Debug build (-DGB_DEBUG_CHECKS, libgb_raster_debug.so; tests/test_gpu_debug_checks.py): bounds checks on
+// list entries, primitive ids, tile keys and texel indices that trap (a launch error) instead of reading or
+// writing out of range.  compute-sanitizer is closed on the GPU pool, so this is the memory-safety net.
+#ifdef GB_DEBUG_CHECKS
+#define GB_CHECK(c)          \
+    do {                     \
+        if (!(c)) __trap();  \
+    } while (0)
+#else
+#define GB_CHECK(c) \
+    do {            \
+    } while (0)
+#endif
+
 constexpr int kAccumStride = 12;  // values per primitive in the K4 -> K5 accumulator
 constexpr real kMaxAlpha = (real)0.999;  // core.hpp:16
 
@@ -113,6 +127,9 @@ struct RasterConst {
     real tex_offset;      // (n-1)/2
     real sigma;
     int tgs;  // K4 texel-gradient stride: 3 = the reference layout, 4 = RGBA-padded (one 16-B red per texel)
+#ifdef GB_DEBUG_CHECKS
+    int64_t dbg_K;  // primitives: every list entry must be in [0, K)
+#endif
 #ifdef GB_PARITY_F64
     double* trans64;  // parity build: K3 stores the fp64 final transmittance here, K4 rewinds from it
 #endif

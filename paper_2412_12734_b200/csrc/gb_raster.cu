@@ -172,6 +172,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             }
             wk[0] = (real)1;
         }
+        GB_CHECK(tt >= 0 && tt + cell_texel<CELL>(NX - 1, N) < N * N);
         c0 = cc_[0];
         c1 = cc_[1];
         c2 = cc_[2];
@@ -518,6 +519,7 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
         bool pass = false;
         if (c0 + lane < total) {
             idl = __ldg(&values[range.x + c0 + lane]);
+            GB_CHECK(idl >= 0 && idl < rc.dbg_K);
             pass = entry_meets_warp(hdr, cull, idl, lr);
         }
         unsigned mask = __ballot_sync(kFull, pass);
@@ -563,6 +565,7 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
         bool pass = false;
         if (c0 + lane <= wlast) {
             idl = __ldg(&values[range.x + c0 + lane]);
+            GB_CHECK(idl >= 0 && idl < rc.dbg_K);
             pass = entry_meets_warp(hdr, cull, idl, lr);
         }
         unsigned mask = __ballot_sync(kFull, pass);
