@@ -595,6 +595,7 @@ static double uv_error32(const raster_ctx_t *c, const geom_t *g, double px, doub
  * the evaluation's own fp32 uncertainty when larger -- dalpha/alpha = |u| du + |v| dv (G = exp(-(u^2+v^2)/2))
  * plus the exponential's and the product's rounding -- which dominates for thin, grazing splats. */
 static double alpha_margin(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
+    if (!(c->kink->uv_rel > 0.0)) return c->kink->alpha_rel;
     const double e = 2.0 * ((fabs(u) + fabs(v)) * uv_error32_raw(c, g, px, py, u, v) + 8.0 * kEps32);
     return e > c->kink->alpha_rel ? e : c->kink->alpha_rel;
 }
@@ -603,6 +604,17 @@ static double alpha_margin(const raster_ctx_t *c, const geom_t *g, double px, do
  * the usual |alpha - t| <= m t; for a large m (an fp32-ill-conditioned evaluation) a factor e^m either way,
  * and never an alpha that underflowed far below the threshold. */
 static int near_threshold(double alpha, double t, double m) { return alpha > 0.0 && fabs(log(alpha / t)) <= m; }
+
+/* relative fp32 error of the u- and v-proportional terms of an evaluation: uv_rel delta (1/|u| + 1/|v|) with |u|, |v|
+ * floored at 0.05 and the result capped at 1; 0 when it is below eps32 (negligible) */
+static double uv_rel_error(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
+    if (!c->kink || !(c->kink->uv_rel > 0.0)) return 0.0;
+    const double d = uv_error32_raw(c, g, px, py, u, v);
+    const double au = fabs(u) > 0.05 ? fabs(u) : 0.05, av = fabs(v) > 0.05 ? fabs(v) : 0.05;
+    double f = c->kink->uv_rel * d * (1.0 / au + 1.0 / av);
+    if (f > 1.0) f = 1.0;
+    return f > kEps32 ? f : 0.0;
+}
 
 static int sensitive(const raster_ctx_t *c, const geom_t *g, double px, double py, double u, double v) {
     return c->kink && c->kink->cond_min > 0.0 && uv_error32(c, g, px, py, u, v) > c->kink->cond_min;
@@ -954,7 +966,17 @@ static void backward_tile(void *vctx, int tile) {
                             /* decision kink in this pixel, or an fp32-ill-conditioned evaluation */
                             for (size_t j = 0; j < gs; ++j) rs[j] += d[j];
                             tex_abs(n, sigma, u, v, c_hat, rs + gs);
-                        } else if (grid_kink(u, n, sigma, margin) || grid_kink(v, n, sigma, margin)) {
+                        } else if (uv_rel_error(c, g, px, py, u, v) > 0.0) {
+                            /* the fp32 (u, v) carry the absolute error delta of uv_error32_raw; terms proportional
+                             * to u or v then carry delta / |u|, delta / |v| relative -- large where u or v is small
+                             * (thin, grazing surfels).  Slack: the evaluation's |terms| times that, floored */
+                            const double f = uv_rel_error(c, g, px, py, u, v);
+                            for (size_t j = 0; j < gs; ++j) rs[j] += f * d[j];
+                            const double cf[3] = {f * c_hat[0], f * c_hat[1], f * c_hat[2]};
+                            tex_abs(n, sigma, u, v, cf, rs + gs);
+                        }
+                        if (!((px_flag & 3) || sensitive(c, g, px, py, u, v)) &&
+                            (grid_kink(u, n, sigma, margin) || grid_kink(v, n, sigma, margin))) {
                             /* only the texture part of (u_hat, v_hat) jumps across a texel
                              * boundary: bound the jump by both sides' magnitudes */
                             const double du = 2.0 * margin * (2.0 * sigma) / (n - 1);

@@ -99,6 +99,8 @@ typedef struct {
     double trans_rel; /* |T - early_stop| <= trans_rel*early_stop at any composite */
     double grid_abs;  /* |u' - k| <= grid_abs for an interior texel boundary k; ||u|-sigma| <= grid_abs*2sigma/(n-1) */
     double cond_min;  /* fp32 sensitivity: estimated |error| of (u,v) in texel units above this */
+    double uv_rel;    /* > 0: fp32 (u,v) error propagation -- alpha-threshold margins from the evaluation's
+                         uncertainty and slack uv_rel * delta * (1/|u| + 1/|v|) * |terms|; 0 for an fp64 GPU build */
 } orc_kink;
 
 int orc_build_binning(const orc_splats *s, const orc_camera *cam, const orc_config *cfg, orc_binning *out);

@@ -64,10 +64,13 @@ class OrcBinning(C.Structure):
 
 class OrcKink(C.Structure):
     _fields_ = [("alpha_rel", C.c_double), ("trans_rel", C.c_double), ("grid_abs", C.c_double),
-                ("cond_min", C.c_double)]
+                ("cond_min", C.c_double), ("uv_rel", C.c_double)]
 
 
-DEFAULT_KINK = (2e-5, 1e-3, 1e-4, 1e-4)
+# kink margins of the fp32 product (parity protocol)
+DEFAULT_KINK = (2e-5, 1e-3, 1e-4, 1e-4, 4.0)
+# for the fp64 parity build: decision kinks only (its (u, v) are fp64, so no fp32 (u, v) error propagation)
+STRICT_KINK = (2e-5, 1e-3, 1e-4, 0.0, 0.0)
 
 _oracle = None
 _ref = None

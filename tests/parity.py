@@ -89,13 +89,14 @@ def run_gpu(arrays: dict, mode: int, n: int, cam_spec, cfg: "O.Cfg", image_grad=
     return res
 
 
-def run_oracle(arrays: dict, n: int, cam: "O.Cam", cfg: "O.Cfg", image_grad=None, sigma=0.5):
+def run_oracle(arrays: dict, n: int, cam: "O.Cam", cfg: "O.Cfg", image_grad=None, sigma=0.5, kink=O.DEFAULT_KINK):
     scene = O.Scene64(arrays, n, sigma)
     b = O.build_binning(scene, cam, cfg)
-    f = O.render_forward(scene, cam, cfg, b)
+    f = O.render_forward(scene, cam, cfg, b, kink=kink)
     res = dict(offsets=b[0], values=b[1], color=f["color"], trans=f["trans"], last=f["last"], kink=f["kink"])
     if image_grad is not None:
-        g, mag, slack, tmag = O.render_backward_tm(scene, cam, cfg, b, f, np.asarray(image_grad, np.float64))
+        g, mag, slack, tmag = O.render_backward_tm(scene, cam, cfg, b, f, np.asarray(image_grad, np.float64),
+                                                   kink=kink)
         res.update(grads=g, mag=mag, slack=slack, tmag=tmag)
     return res
 
@@ -178,7 +179,7 @@ def subset_rows(tiles_y: int, stride: int):
 
 
 def run_rows(arrays: dict, mode: int, n: int, cam: "O.Cam", cfg: "O.Cfg", image_grad, stride: int = 8,
-             sigma=0.5, device="cuda"):
+             sigma=0.5, device="cuda", kink=O.DEFAULT_KINK):
     """-> (gpu, orc, info) shaped for compare_binning / compare_image / compare_grads."""
     import torch
 
@@ -242,8 +243,8 @@ def run_rows(arrays: dict, mode: int, n: int, cam: "O.Cam", cfg: "O.Cfg", image_
     # oracle: the subset tiles over the compacted primitives
     sub_arrays = {f: (None if arrays.get(f) is None else np.ascontiguousarray(arrays[f][ids])) for f in O.FIELDS}
     scene = O.Scene64(sub_arrays, n, sigma)
-    f = O.render_forward(scene, cam, cfg, sub_bin)
-    gr, mag, slack, tmag = O.render_backward_tm(scene, cam, cfg, sub_bin, f, ig)
+    f = O.render_forward(scene, cam, cfg, sub_bin, kink=kink)
+    gr, mag, slack, tmag = O.render_backward_tm(scene, cam, cfg, sub_bin, f, ig, kink=kink)
     orc = dict(offsets=offsets, values=values, color=f["color"][px_rows], trans=f["trans"][px_rows],
                last=f["last"][px_rows], kink=f["kink"][px_rows],
                grads={k: (None if v is None else v.reshape(len(ids), -1)) for k, v in gr.items()},

@@ -48,11 +48,12 @@ def main():
     arrays, mode, n, cam, stride = case(name)
     ig = image_grad(0, cam.height, cam.width)
     cfg = O.Cfg()
+    # decision kinks only: the parity build evaluates (u, v) in fp64, so no fp32 (u, v) error is propagated
     if stride:
-        gpu, orc, info = run_rows(arrays, mode, n, cam, cfg, ig, stride=stride)
+        gpu, orc, info = run_rows(arrays, mode, n, cam, cfg, ig, stride=stride, kink=O.STRICT_KINK)
     else:
         gpu = run_gpu(arrays, mode, n, cam, cfg, ig)
-        orc = run_oracle(arrays, n, cam, cfg, ig)
+        orc = run_oracle(arrays, n, cam, cfg, ig, kink=O.STRICT_KINK)
         info = {}
     import paper_2412_12734_b200._lib as L
 
