@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--count", type=int, default=1_000_000)
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpp-host", action="store_true",
+                    help="skip the C++-host measurement (gbil_b200::multiview::Rank through libgb_mvhost.so)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true",
                     help="issue each step's view work eagerly instead of replaying it as one CUDA graph")
@@ -235,6 +237,56 @@ def run_reference(args):
 # ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
+def run_cpp_host(args, arrays, cams, views, dev_targets, W, H):
+    """The same device-resident step through the C++ host (gbil_b200::multiview::Rank: four view lanes,
+    capacity binning, one CUDA graph per step, padded texel gradients; Adam on one stream), timed by wall
+    clock around K steps (each step ends with its synchronous loss and flag read)."""
+    import ctypes as C
+
+    import torch
+
+    lib = C.CDLL(os.path.join(ROOT, "paper_2412_12734_b200", "libgb_mvhost.so"))
+    P = C.c_void_p
+    lib.gb_mv_create.argtypes = [C.c_int, C.c_int64, C.c_int] + [P] * 5 + [C.c_int] * 3 + [P, C.c_int, P, C.c_int,
+                                                                                          C.c_int, C.c_double,
+                                                                                          C.POINTER(P)]
+    lib.gb_mv_step.argtypes = [P, C.c_int, P, C.POINTER(C.c_double)]
+    lib.gb_mv_destroy.argtypes = [P]
+    lib.gb_mv_error.restype = C.c_char_p
+    a = {k: np.ascontiguousarray(arrays[k], np.float32) for k in ("position", "quat", "log_scale", "opacity_logit",
+                                                                   "grid")}
+    cam16 = np.ascontiguousarray(np.array([[c.fx, c.fy, c.cx, c.cy, *np.asarray(c.rot).ravel(), *np.asarray(c.trans)]
+                                           for c in cams], np.float64))
+    vv = np.ascontiguousarray(np.array(views, np.int32))
+    h = P()
+    K = a["opacity_logit"].shape[0]
+    n = int(round((a["grid"].shape[1] // 3) ** 0.5))
+    rc = lib.gb_mv_create(torch.cuda.current_device(), K, n, *[a[k].ctypes.data for k in ("position", "quat",
+                                                                                            "log_scale",
+                                                                                            "opacity_logit", "grid")],
+                          W, H, len(cams), cam16.ctypes.data, len(vv), vv.ctypes.data, 4, 1, 6.0, C.byref(h))
+    if rc:
+        raise RuntimeError(lib.gb_mv_error().decode())
+    tp = (P * len(dev_targets))(*[t.data_ptr() for t in dev_targets])
+    loss = C.c_double()
+    try:
+        for _ in range(max(3, args.warmup)):
+            if lib.gb_mv_step(h, len(dev_targets), tp, C.byref(loss)):
+                raise RuntimeError(lib.gb_mv_error().decode())
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            if lib.gb_mv_step(h, len(dev_targets), tp, C.byref(loss)):
+                raise RuntimeError(lib.gb_mv_error().decode())
+        dt = (time.perf_counter() - t0) / args.steps
+    finally:
+        lib.gb_mv_destroy(h)
+    return {"value": round(len(views) * W * H / 1e6 / dt, 3), "unit": "MP/s", "ms_per_step": round(dt * 1e3, 3),
+            "what": "the same device-resident step driven by the C++ host (gbil_b200::multiview::Rank via "
+                    "libgb_mvhost.so): four view lanes, capacity binning, one CUDA graph per step, padded texel "
+                    "gradients, Adam on one stream; wall clock around K steps, each ending with its loss read",
+            "last_loss": round(loss.value, 6)}
+
+
 def run_ours(args):
     import torch
 
@@ -382,6 +434,14 @@ def run_ours(args):
         fwd = {"ms_per_view": round(f_ms, 4), "value": round(W * H / 1e6 / (f_ms / 1e3), 3), "unit": "MP/s",
                "what": "build_binning + render_forward per view, one stream, CUDA events"}
 
+    # ---- the same step driven by the C++ host (include/gbil_b200.hpp multiview::Rank, libgb_mvhost.so) ----
+    cpp_host = None
+    if rank == 0 and world == 1 and not args.no_cpp_host:
+        try:
+            cpp_host = run_cpp_host(args, arrays, cams, views, dev_targets, W, H)
+        except Exception as e:  # an extra measurement never blocks the headline
+            cpp_host = {"failed": str(e)[:200]}
+
     # ---- replicas stay in sync: every rank holds bit-identical parameters ----
     in_sync = True
     if world > 1:
@@ -478,6 +538,7 @@ def run_ours(args):
         "e2e": e2e,
         "replicas_in_sync": in_sync,
         "forward_only": fwd,
+        "cpp_host": cpp_host,
     }
     if world == 1 and not args.no_cpu_baseline:
         try:

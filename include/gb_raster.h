@@ -200,6 +200,13 @@ GB_API gb_status gb_graph_destroy(gb_graph *g);
  * graph then waits for the event's record made outside it, at every launch (ignored outside a capture). */
 GB_API gb_status gb_stream_wait_event(gb_context *ctx, void *event, int32_t external);
 
+/* Events for a host without CUDA headers (fork/join of several contexts' streams, e.g. view lanes inside
+ * a gb_graph capture): a timing-disabled cudaEvent_t recorded on / waited for by a context's stream
+ * (gb_stream_wait_event). */
+GB_API gb_status gb_event_create(gb_context *ctx, void **event);
+GB_API gb_status gb_event_record(gb_context *ctx, void *event);
+GB_API gb_status gb_event_destroy(gb_context *ctx, void *event);
+
 /* ---- device memory helpers (so a C/C++ host needs no CUDA headers) -------- */
 GB_API gb_status gb_device_alloc(gb_context *ctx, uint64_t bytes, void **out);
 GB_API gb_status gb_device_free(gb_context *ctx, void *ptr);

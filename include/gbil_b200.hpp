@@ -926,20 +926,38 @@ struct Buffer {  // device memory of one rank's context
 }  // namespace detail
 
 // One rank: a GPU, its views, a parameter replica, the flat gradient buffer and its slice of Adam.
+// The views are dealt round-robin to `lanes` contexts (one CUDA stream each), so the binning, sorts and
+// compositors of different views overlap; after a first blocking step has sized them, the binnings run
+// in capacity mode (no host read-back) and the step's view work -- zeroing, every lane's binning and
+// forward + loss + backward, the fork/join, the texel-gradient unpad -- replays as one CUDA graph
+// (gb_graph_*).  K4 writes texel gradients into an RGBA-padded scratch (gb_context_set_texel_grad_stride).
+// A view that outgrows its pair buffers vetoes the step's update (gb_adam_flag_init) and the step is
+// redone with larger buffers.  The same design as the Python trainer (train.py ViewShardedTrainer).
 class Rank {
 public:
     Rank(int device, const PinholeScene& scene, std::vector<PinholeCamera> cameras, std::vector<int> views,
-         const StepConfig& cfg, int nranks, int rank)
+         const StepConfig& cfg, int nranks, int rank, int lanes = 4, bool graph = true)
         : cams_(std::move(cameras)), views_(std::move(views)), cfg_(cfg), nranks_(nranks), rank_(rank),
-          layout_(scene.count, scene.n, nranks) {
+          layout_(scene.count, scene.n, nranks), use_graph_(graph) {
         cfg_.lrs.validate();
-        detail::check(gb_context_create(device, &ctx_), "gb_context_create");
+        if (lanes < 1) throw std::invalid_argument("Rank: lanes must be >= 1");
+        for (int i = 0; i < lanes; ++i) {
+            Lane l;
+            detail::check(gb_context_create(device, &l.ctx), "gb_context_create");
+            detail::check(gb_binning_create(l.ctx, &l.bin), "gb_binning_create");
+            detail::check(gb_context_set_texel_grad_stride(l.ctx, 4), "gb_context_set_texel_grad_stride");
+            detail::check(gb_event_create(l.ctx, &l.done), "gb_event_create");
+            lanes_.push_back(l);
+        }
+        ctx_ = lanes_[0].ctx;
+        detail::check(gb_event_create(ctx_, &ev_start_), "gb_event_create");
         const std::int64_t K = scene.count, n = scene.n, T = layout_.total;
         K_ = K;
         n_ = scene.n;
         sigma_ = scene.sigma;
         params_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * T);
         grads_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * T);
+        pad_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * 4 * K * n * n + 16);
         detail::check(gb_memset_device(ctx_, params_->ptr, 0, sizeof(float) * T), "gb_memset_device");
         auto put = [&](std::int64_t off, const std::vector<float>& v, std::int64_t want, const char* what) {
             if (static_cast<std::int64_t>(v.size()) != want)
@@ -960,22 +978,35 @@ public:
         detail::check(gb_memset_device(ctx_, v_->ptr, 0, sizeof(float) * S_), "gb_memset_device");
         if (cfg_.sharded_adam && nranks > 1) gshard_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * S_);
         flag_ = std::make_unique<detail::Buffer>(ctx_, 16);
-        loss_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * std::max<std::size_t>(1, views_.size()));
-        detail::check(gb_binning_create(ctx_, &bin_), "gb_binning_create");
+        const std::size_t nv = std::max<std::size_t>(1, views_.size());
+        loss_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * nv);
+        pairs_ = std::make_unique<detail::Buffer>(ctx_, sizeof(uint32_t) * nv);
+        overflow_ = std::make_unique<detail::Buffer>(ctx_, 16);
+        detail::check(gb_memset_device(ctx_, overflow_->ptr, 0, 16), "gb_memset_device");
+        detail::check(gb_sync(ctx_), "gb_sync");
         build_segments();
     }
     Rank(const Rank&) = delete;
     Rank& operator=(const Rank&) = delete;
     ~Rank() {
-        if (bin_) gb_binning_destroy(bin_);
+        if (graph_) gb_graph_destroy(graph_);
+        for (Lane& l : lanes_) gb_sync(l.ctx);
         params_.reset();
         grads_.reset();
+        pad_.reset();
         m_.reset();
         v_.reset();
         gshard_.reset();
         flag_.reset();
         loss_.reset();
-        if (ctx_) gb_context_destroy(ctx_);
+        pairs_.reset();
+        overflow_.reset();
+        if (ev_start_) gb_event_destroy(ctx_, ev_start_);
+        for (std::size_t i = lanes_.size(); i-- > 0;) {
+            gb_event_destroy(lanes_[i].ctx, lanes_[i].done);
+            gb_binning_destroy(lanes_[i].bin);
+            gb_context_destroy(lanes_[i].ctx);
+        }
     }
 
     gb_context* context() const { return ctx_; }
@@ -986,29 +1017,34 @@ public:
     // Returns the sum of the views' mean-L1 losses (one host read per step, after the update is queued).
     double step(const std::vector<const float*>& targets) {
         if (targets.size() != views_.size()) throw std::invalid_argument("step: one target per owned view");
-        const std::int64_t T = layout_.total;
-        detail::check(gb_memset_device(ctx_, grads_->ptr, 0, sizeof(float) * T), "step");
-        detail::check(gb_memset_device(ctx_, loss_->ptr, 0, sizeof(float) * std::max<std::size_t>(1, views_.size())),
-                      "step");
-        const gb_splats s = splats();
-        gb_grads g = view_of(grads_->f());
-        const gb_raster_config rc{cfg_.raster.tile_size, cfg_.raster.threads, cfg_.raster.cutoff_radius,
-                                  cfg_.raster.alpha_skip, cfg_.raster.early_stop_transmittance};
-        for (std::size_t i = 0; i < views_.size(); ++i) {  // train.hpp:191-199 per view
-            const gb_camera cam = cams_.at(views_[i]).to_c();
-            const float scale = 1.0f / (3.0f * cam.width * cam.height);  // mean L1
-            detail::check(gb_build_binning(ctx_, &s, &cam, &rc, bin_), "step: build_binning");
-            detail::check(gb_render_loss_backward(ctx_, &s, &cam, bin_, targets[i], GB_LOSS_L1, scale, nullptr,
-                                                  nullptr, loss_->f() + i, &g),
-                          "step: render_loss_backward");
+        if (!capacity_) {  // blocking builds learn the pair counts, then capacity mode
+            run_views(targets, true);
+            set_capacity(max_pairs_);
         }
-        update();
-        std::vector<float> l(std::max<std::size_t>(1, views_.size()));
-        detail::check(gb_copy_d2h(ctx_, l.data(), loss_->ptr, sizeof(float) * l.size(), 1), "step");
-        double sum = 0.0;
-        for (std::size_t i = 0; i < views_.size(); ++i) sum += l[i];
-        if (comm_) detail::check(gb_comm_check(comm_), "step: NCCL");
-        return sum;
+        for (int attempt = 0; attempt < 4; ++attempt) {
+            if (use_graph_ && graph_ && graph_key_ == targets) {
+                detail::check(gb_graph_launch(graph_), "step: graph");
+            } else {
+                run_views(targets, false);  // eager (sizes every buffer), then captured for the next steps
+                if (use_graph_) capture(targets);
+            }
+            const std::int64_t code = update();
+            std::vector<float> l(std::max<std::size_t>(1, views_.size()));
+            detail::check(gb_copy_d2h(ctx_, l.data(), loss_->ptr, sizeof(float) * l.size(), 1), "step");
+            if (comm_) detail::check(gb_comm_check(comm_), "step: NCCL");
+            if (code == GB_ADAM_FLAG_VETO) {  // a view outgrew its pair buffers: nothing was updated
+                grow();
+                continue;
+            }
+            if (code != kClear)
+                throw NonFiniteGradient("adam_step: non-finite gradient in group " + std::to_string(code >> 48) +
+                                        "; no parameter was updated");
+            t_ += 1;
+            double sum = 0.0;
+            for (std::size_t i = 0; i < views_.size(); ++i) sum += l[i];
+            return sum;
+        }
+        throw std::runtime_error("step: view binning kept outgrowing its pair capacity");
     }
 
     std::vector<float> download_params() const {  // flat layout
@@ -1023,8 +1059,16 @@ public:
     }
     const detail::FlatLayout& layout() const { return layout_; }
     std::int64_t adam_t() const { return t_; }
+    std::int64_t capacity() const { return capacity_; }
+    int overflows() const { return overflows_; }
 
 private:
+    struct Lane {
+        gb_context* ctx = nullptr;
+        gb_binning* bin = nullptr;
+        void* done = nullptr;
+    };
+
     gb_splats splats() const {
         gb_splats s{};
         s.count = K_;
@@ -1041,6 +1085,77 @@ private:
     gb_grads view_of(float* base) const {
         return gb_grads{base + layout_.position, nullptr, nullptr, base + layout_.quat, base + layout_.log_scale,
                         base + layout_.opacity, base + layout_.grid};
+    }
+    // fit's per-view loop (train.hpp:191-199) for every owned view, dealt to the lanes; capturable when
+    // `blocking` is false (capacity mode: no allocation, no host read).
+    void run_views(const std::vector<const float*>& targets, bool blocking) {
+        const std::int64_t T = layout_.total, K = K_, n = n_;
+        const std::size_t nv = std::max<std::size_t>(1, views_.size());
+        detail::check(gb_memset_device(ctx_, grads_->ptr, 0, sizeof(float) * T), "step");
+        detail::check(gb_memset_device(ctx_, pad_->ptr, 0, sizeof(float) * 4 * K * n * n), "step");
+        detail::check(gb_memset_device(ctx_, loss_->ptr, 0, sizeof(float) * nv), "step");
+        detail::check(gb_event_record(ctx_, ev_start_), "step");
+        for (std::size_t i = 1; i < lanes_.size(); ++i)
+            detail::check(gb_stream_wait_event(lanes_[i].ctx, ev_start_, 0), "step");
+        const gb_splats s = splats();
+        gb_grads g = view_of(grads_->f());
+        g.grid_values = pad_->f();  // K4's RGBA-padded texel gradients
+        const gb_raster_config rc{cfg_.raster.tile_size, cfg_.raster.threads, cfg_.raster.cutoff_radius,
+                                  cfg_.raster.alpha_skip, cfg_.raster.early_stop_transmittance};
+        max_pairs_ = 0;
+        for (std::size_t i = 0; i < views_.size(); ++i) {  // train.hpp:191-199 per view
+            const Lane& l = lanes_[i % lanes_.size()];
+            const gb_camera cam = cams_.at(views_[i]).to_c();
+            const float scale = 1.0f / (3.0f * cam.width * cam.height);  // mean L1
+            detail::check(gb_build_binning(l.ctx, &s, &cam, &rc, l.bin), "step: build_binning");
+            if (blocking) {
+                std::int64_t P = 0;
+                detail::check(gb_binning_info(l.bin, nullptr, nullptr, &P), "step");
+                max_pairs_ = std::max(max_pairs_, P);
+            } else {
+                detail::check(gb_binning_store_total(l.ctx, l.bin, static_cast<uint32_t*>(pairs_->ptr) + i), "step");
+            }
+            detail::check(gb_render_loss_backward(l.ctx, &s, &cam, l.bin, targets[i], GB_LOSS_L1, scale, nullptr,
+                                                  nullptr, loss_->f() + i, &g),
+                          "step: render_loss_backward");
+        }
+        for (std::size_t i = 1; i < lanes_.size(); ++i) {
+            detail::check(gb_event_record(lanes_[i].ctx, lanes_[i].done), "step");
+            detail::check(gb_stream_wait_event(ctx_, lanes_[i].done, 0), "step");
+        }
+        detail::check(gb_texel_grads_unpad(ctx_, pad_->f(), grads_->f() + layout_.grid, K * n * n, 0), "step");
+    }
+    void capture(const std::vector<const float*>& targets) {
+        if (graph_) {
+            gb_graph_destroy(graph_);
+            graph_ = nullptr;
+        }
+        std::vector<gb_context*> ctxs;
+        for (const Lane& l : lanes_) ctxs.push_back(l.ctx);
+        detail::check(gb_graph_begin(ctxs.data(), static_cast<int32_t>(ctxs.size())), "step: graph_begin");
+        run_views(targets, false);
+        detail::check(gb_graph_end(ctxs.data(), static_cast<int32_t>(ctxs.size()), &graph_), "step: graph_end");
+        graph_key_ = targets;
+    }
+    void set_capacity(std::int64_t pairs) {
+        std::int64_t cap = (static_cast<std::int64_t>(pairs * 1.1) + 4096 + 65535) & ~std::int64_t(65535);
+        cap = std::min<std::int64_t>(cap, 0x7ffffffeLL);
+        for (const Lane& l : lanes_)
+            detail::check(gb_binning_set_capacity(l.bin, cap, static_cast<int32_t*>(overflow_->ptr)), "capacity");
+        capacity_ = cap;
+        if (graph_) {
+            gb_graph_destroy(graph_);
+            graph_ = nullptr;
+        }
+    }
+    void grow() {  // after a vetoed step: the largest view's pair count sizes the new capacity
+        ++overflows_;
+        std::vector<uint32_t> p(std::max<std::size_t>(1, views_.size()));
+        detail::check(gb_copy_d2h(ctx_, p.data(), pairs_->ptr, sizeof(uint32_t) * p.size(), 1), "grow");
+        detail::check(gb_memset_device(ctx_, overflow_->ptr, 0, 16), "grow");
+        std::int64_t need = 0;
+        for (uint32_t v : p) need = std::max<std::int64_t>(need, v);
+        set_capacity(need);
     }
     void build_segments() {  // optim.hpp:96-117 groups intersected with this rank's slice
         struct G {
@@ -1061,7 +1176,8 @@ private:
                                             v_->f() + (a - lo_), b - a, gr.group, 0});
         }
     }
-    void update() {
+    // the exchange and Adam on the main context; returns the agreed flag (CLEAR, VETO or a non-finite code)
+    std::int64_t update() {
         const std::int64_t T = layout_.total;
         const bool multi = comm_ && nranks_ > 1;
         if (multi) {
@@ -1070,10 +1186,12 @@ private:
             else
                 detail::check(gb_allreduce_grads(ctx_, comm_, grads_->f(), T), "step: all-reduce");
         }
-        detail::check(gb_copy_h2d(ctx_, flag_->ptr, &kClear, sizeof(kClear), 0), "step");
+        auto* flag = static_cast<int64_t*>(flag_->ptr);
+        // CLEAR, or VETO when a view outgrew its pair buffers; phase 0 lowers it to a non-finite gradient's code
+        detail::check(gb_adam_flag_init(ctx_, flag, capacity_ ? static_cast<const int32_t*>(overflow_->ptr) : nullptr),
+                      "step: adam");
         gb_adam_state st{t_, cfg_.adam.beta1, cfg_.adam.beta2, cfg_.adam.epsilon, {}, {}};
         const gb_learning_rates l = cfg_.lrs.to_c();
-        auto* flag = static_cast<int64_t*>(flag_->ptr);
         detail::check(gb_adam_segments(ctx_, 0, segs_.data(), static_cast<int32_t>(segs_.size()), &st, &l, flag),
                       "step: adam");
         if (multi) detail::check(gb_allreduce_flag_min(ctx_, comm_, flag), "step: flag");  // optim.hpp:81-83, agreed
@@ -1083,25 +1201,27 @@ private:
             detail::check(gb_all_gather_params(ctx_, comm_, params_->f() + lo_, params_->f(), S_), "step: all-gather");
         int64_t code = 0;
         detail::check(gb_copy_d2h(ctx_, &code, flag_->ptr, sizeof(code), 1), "step");
-        if (code != kClear)
-            throw NonFiniteGradient("adam_step: non-finite gradient in group " + std::to_string(code >> 48) +
-                                    "; no parameter was updated");
-        t_ = st.t;
+        return code;
     }
 
     static constexpr int64_t kClear = GB_ADAM_FLAG_CLEAR;
+    std::vector<Lane> lanes_;
     gb_context* ctx_ = nullptr;
     gb_comm* comm_ = nullptr;
-    gb_binning* bin_ = nullptr;
+    void* ev_start_ = nullptr;
     std::vector<PinholeCamera> cams_;
     std::vector<int> views_;
     StepConfig cfg_;
     int nranks_, rank_;
     detail::FlatLayout layout_;
-    std::int64_t K_ = 0, S_ = 0, lo_ = 0, t_ = 0;
+    bool use_graph_ = true;
+    gb_graph* graph_ = nullptr;
+    std::vector<const float*> graph_key_;
+    std::int64_t K_ = 0, S_ = 0, lo_ = 0, t_ = 0, capacity_ = 0, max_pairs_ = 0;
+    int overflows_ = 0;
     int n_ = 1;
     double sigma_ = 0.5;
-    std::unique_ptr<detail::Buffer> params_, grads_, m_, v_, gshard_, flag_, loss_;
+    std::unique_ptr<detail::Buffer> params_, grads_, pad_, m_, v_, gshard_, flag_, loss_, pairs_, overflow_;
     std::vector<gb_adam_segment> segs_;
 };
 

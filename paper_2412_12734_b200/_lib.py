@@ -225,6 +225,9 @@ _SIGS = {
     "gb_rng_uniform": (C.c_int, [C.c_uint64, C.c_int64, P]),
     "gb_rng_normal": (C.c_int, [C.c_uint64, C.c_int64, C.c_double, C.c_double, P]),
     "gb_adam_flag_init": (C.c_int, [P, P, P]),
+    "gb_event_create": (C.c_int, [P, C.POINTER(P)]),
+    "gb_event_record": (C.c_int, [P, P]),
+    "gb_event_destroy": (C.c_int, [P, P]),
     "gb_context_set_texel_grad_stride": (C.c_int, [P, C.c_int32]),
     "gb_texel_grads_unpad": (C.c_int, [P, P, P, C.c_int64, C.c_int32]),
     "gb_comm_unique_id": (C.c_int, [P]),

@@ -596,6 +596,29 @@ gb_status gb_stream_wait_event(gb_context* ctx, void* event, int32_t external) {
     return GB_OK;
 }
 
+gb_status gb_event_create(gb_context* ctx, void** event) {
+    if (!ctx || !event) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    cudaEvent_t e = nullptr;
+    GB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    *event = e;
+    return GB_OK;
+}
+
+gb_status gb_event_record(gb_context* ctx, void* event) {
+    if (!ctx || !event) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), ctx->stream));
+    return GB_OK;
+}
+
+gb_status gb_event_destroy(gb_context* ctx, void* event) {
+    if (!ctx || !event) return GB_OK;
+    if (gb_status st = set_device(ctx)) return st;
+    GB_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+    return GB_OK;
+}
+
 gb_status gb_device_alloc(gb_context* ctx, uint64_t bytes, void** out) {
     if (!ctx || !out) return fail(GB_INVALID_ARGUMENT, "null argument");
     *out = nullptr;

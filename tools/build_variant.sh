@@ -7,6 +7,6 @@ set -e
 NAME=$1; shift
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 mkdir -p "$ROOT/variants/$NAME" "$ROOT/build/var_$NAME"
-make -C "$ROOT/paper_2412_12734_b200/csrc" -j8 OUT="$ROOT/variants/$NAME/libgb_raster.so" \
+make -C "$ROOT/paper_2412_12734_b200/csrc" -j8 OUT="$ROOT/variants/$NAME/libgb_raster.so" MVHOST_OUT= \
   OBJDIR="$ROOT/build/var_$NAME" EXTRA="$*" 2>&1 | grep -E "error|spill.*k_backward_direct|spill.*k_forward_direct" || true
 ls -la "$ROOT/variants/$NAME/libgb_raster.so"
