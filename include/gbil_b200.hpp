@@ -940,6 +940,7 @@ public:
         : cams_(std::move(cameras)), views_(std::move(views)), cfg_(cfg), nranks_(nranks), rank_(rank),
           layout_(scene.count, scene.n, nranks), use_graph_(graph) {
         cfg_.lrs.validate();
+        device_ = device;
         if (lanes < 1) throw std::invalid_argument("Rank: lanes must be >= 1");
         for (int i = 0; i < lanes; ++i) {
             Lane l;
@@ -951,6 +952,11 @@ public:
         }
         ctx_ = lanes_[0].ctx;
         detail::check(gb_event_create(ctx_, &ev_start_), "gb_event_create");
+        // Adam's texel-group update runs on its own stream and overlaps the next step's binning
+        detail::check(gb_context_create(device, &adam_ctx_), "gb_context_create");
+        detail::check(gb_event_create(ctx_, &ev_scan_), "gb_event_create");
+        detail::check(gb_event_create(adam_ctx_, &ev_grid_done_), "gb_event_create");
+        detail::check(gb_event_record(adam_ctx_, ev_grid_done_), "gb_event_record");  // complete before the first wait
         const std::int64_t K = scene.count, n = scene.n, T = layout_.total;
         K_ = K;
         n_ = scene.n;
@@ -1001,6 +1007,19 @@ public:
         loss_.reset();
         pairs_.reset();
         overflow_.reset();
+        for (auto& b : host_bufs_) b.reset();
+        for (void* e : copy_done_) gb_event_destroy(copy_ctx_, e);
+        for (void* e : buf_free_) gb_event_destroy(ctx_, e);
+        if (copy_ctx_) {
+            gb_sync(copy_ctx_);
+            gb_context_destroy(copy_ctx_);
+        }
+        if (adam_ctx_) {
+            gb_sync(adam_ctx_);
+            gb_event_destroy(adam_ctx_, ev_grid_done_);
+            gb_context_destroy(adam_ctx_);
+        }
+        if (ev_scan_) gb_event_destroy(ctx_, ev_scan_);
         if (ev_start_) gb_event_destroy(ctx_, ev_start_);
         for (std::size_t i = lanes_.size(); i-- > 0;) {
             gb_event_destroy(lanes_[i].ctx, lanes_[i].done);
@@ -1015,17 +1034,27 @@ public:
 
     // One step over this rank's views; targets[i] is view i's HWC fp32 target on this rank's device.
     // Returns the sum of the views' mean-L1 losses (one host read per step, after the update is queued).
-    double step(const std::vector<const float*>& targets) {
+    double step(const std::vector<const float*>& targets) { return step_impl(targets, false); }
+
+    // The end-to-end step: targets[i] is view i's HWC fp32 target in (pinned) HOST memory.  The host->device
+    // copies run on a copy stream into two buffers per view lane, each view waiting for its own target only
+    // before its loss; eager (no graph), like the Python trainer's step_host.
+    double step_host(const std::vector<const float*>& host_targets) { return step_impl(host_targets, true); }
+
+private:
+    double step_impl(const std::vector<const float*>& targets, bool host) {
         if (targets.size() != views_.size()) throw std::invalid_argument("step: one target per owned view");
         if (!capacity_) {  // blocking builds learn the pair counts, then capacity mode
-            run_views(targets, true);
+            run_views(targets, true, host);
             set_capacity(max_pairs_);
         }
         for (int attempt = 0; attempt < 4; ++attempt) {
-            if (use_graph_ && graph_ && graph_key_ == targets) {
+            if (host) {
+                run_views(targets, false, true);
+            } else if (use_graph_ && graph_ && graph_key_ == targets) {
                 detail::check(gb_graph_launch(graph_), "step: graph");
             } else {
-                run_views(targets, false);  // eager (sizes every buffer), then captured for the next steps
+                run_views(targets, false, false);  // eager (sizes every buffer), then captured for the next steps
                 if (use_graph_) capture(targets);
             }
             const std::int64_t code = update();
@@ -1047,12 +1076,15 @@ public:
         throw std::runtime_error("step: view binning kept outgrowing its pair capacity");
     }
 
+public:
     std::vector<float> download_params() const {  // flat layout
+        detail::check(gb_sync(adam_ctx_), "download");  // the texel update is on the Adam stream
         std::vector<float> out(static_cast<std::size_t>(layout_.total));
         detail::check(gb_copy_d2h(ctx_, out.data(), params_->ptr, sizeof(float) * out.size(), 1), "download");
         return out;
     }
     std::vector<float> download_grads() const {  // the summed gradients of the last step (all-reduce mode)
+        detail::check(gb_sync(adam_ctx_), "download");
         std::vector<float> out(static_cast<std::size_t>(layout_.total));
         detail::check(gb_copy_d2h(ctx_, out.data(), grads_->ptr, sizeof(float) * out.size(), 1), "download");
         return out;
@@ -1088,15 +1120,32 @@ private:
     }
     // fit's per-view loop (train.hpp:191-199) for every owned view, dealt to the lanes; capturable when
     // `blocking` is false (capacity mode: no allocation, no host read).
-    void run_views(const std::vector<const float*>& targets, bool blocking) {
-        const std::int64_t T = layout_.total, K = K_, n = n_;
+    void run_views(const std::vector<const float*>& targets, bool blocking, bool host) {
+        const std::int64_t K = K_, n = n_;
         const std::size_t nv = std::max<std::size_t>(1, views_.size());
-        detail::check(gb_memset_device(ctx_, grads_->ptr, 0, sizeof(float) * T), "step");
+        // the grid group is overwritten by the unpad below -- and may still be read by the previous step's
+        // texel update on the Adam stream -- so only the groups in front of it are zeroed
+        detail::check(gb_memset_device(ctx_, grads_->ptr, 0, sizeof(float) * layout_.grid), "step");
         detail::check(gb_memset_device(ctx_, pad_->ptr, 0, sizeof(float) * 4 * K * n * n), "step");
         detail::check(gb_memset_device(ctx_, loss_->ptr, 0, sizeof(float) * nv), "step");
         detail::check(gb_event_record(ctx_, ev_start_), "step");
         for (std::size_t i = 1; i < lanes_.size(); ++i)
             detail::check(gb_stream_wait_event(lanes_[i].ctx, ev_start_, 0), "step");
+        if (host) prepare_copies();
+        std::size_t nbuf = host_bufs_.size(), ahead = nbuf - 1;
+        auto issue = [&](std::size_t i) {  // copy view i's target into buffer i % nbuf on the copy stream
+            const std::size_t b = i % nbuf;
+            detail::check(gb_stream_wait_event(copy_ctx_, buf_free_[b], 0), "step");
+            const gb_camera cam = cams_.at(views_[i]).to_c();
+            detail::check(gb_copy_h2d(copy_ctx_, host_bufs_[b]->ptr, targets[i],
+                                      sizeof(float) * 3 * (std::size_t)cam.width * cam.height, 0),
+                          "step: copy");
+            detail::check(gb_event_record(copy_ctx_, copy_done_[b]), "step");
+        };
+        if (host) {
+            for (std::size_t b = 0; b < nbuf; ++b) detail::check(gb_event_record(ctx_, buf_free_[b]), "step");
+            for (std::size_t i = 0; i < std::min(views_.size(), ahead); ++i) issue(i);
+        }
         const gb_splats s = splats();
         gb_grads g = view_of(grads_->f());
         g.grid_values = pad_->f();  // K4's RGBA-padded texel gradients
@@ -1107,6 +1156,7 @@ private:
             const Lane& l = lanes_[i % lanes_.size()];
             const gb_camera cam = cams_.at(views_[i]).to_c();
             const float scale = 1.0f / (3.0f * cam.width * cam.height);  // mean L1
+            if (host && i + ahead < views_.size()) issue(i + ahead);
             detail::check(gb_build_binning(l.ctx, &s, &cam, &rc, l.bin), "step: build_binning");
             if (blocking) {
                 std::int64_t P = 0;
@@ -1115,9 +1165,18 @@ private:
             } else {
                 detail::check(gb_binning_store_total(l.ctx, l.bin, static_cast<uint32_t*>(pairs_->ptr) + i), "step");
             }
-            detail::check(gb_render_loss_backward(l.ctx, &s, &cam, l.bin, targets[i], GB_LOSS_L1, scale, nullptr,
-                                                  nullptr, loss_->f() + i, &g),
+            // the texels this view reads were updated by the previous step's texel Adam on the Adam stream
+            // (an external wait inside a graph capture: the graph waits for the record made outside it)
+            if (i < lanes_.size()) detail::check(gb_stream_wait_event(l.ctx, ev_grid_done_, 1), "step");
+            const float* tgt = targets[i];
+            if (host) {
+                detail::check(gb_stream_wait_event(l.ctx, copy_done_[i % nbuf], 0), "step");
+                tgt = host_bufs_[i % nbuf]->f();
+            }
+            detail::check(gb_render_loss_backward(l.ctx, &s, &cam, l.bin, tgt, GB_LOSS_L1, scale, nullptr, nullptr,
+                                                  loss_->f() + i, &g),
                           "step: render_loss_backward");
+            if (host) detail::check(gb_event_record(l.ctx, buf_free_[i % nbuf]), "step");
         }
         for (std::size_t i = 1; i < lanes_.size(); ++i) {
             detail::check(gb_event_record(lanes_[i].ctx, lanes_[i].done), "step");
@@ -1125,6 +1184,25 @@ private:
         }
         detail::check(gb_texel_grads_unpad(ctx_, pad_->f(), grads_->f() + layout_.grid, K * n * n, 0), "step");
     }
+    void prepare_copies() {  // two device target buffers per view lane, their events and the copy stream
+        if (copy_ctx_) return;
+        detail::check(gb_context_create(device_of_ctx(), &copy_ctx_), "gb_context_create");
+        std::size_t W = 1, H = 1;
+        for (int v : views_) {
+            W = std::max<std::size_t>(W, cams_.at(v).width);
+            H = std::max<std::size_t>(H, cams_.at(v).height);
+        }
+        for (std::size_t b = 0; b < 2 * lanes_.size(); ++b) {
+            host_bufs_.push_back(std::make_unique<detail::Buffer>(ctx_, sizeof(float) * 3 * W * H));
+            void* e = nullptr;
+            detail::check(gb_event_create(copy_ctx_, &e), "gb_event_create");
+            copy_done_.push_back(e);
+            detail::check(gb_event_create(ctx_, &e), "gb_event_create");
+            buf_free_.push_back(e);
+        }
+    }
+    int device_of_ctx() const { return device_; }
+
     void capture(const std::vector<const float*>& targets) {
         if (graph_) {
             gb_graph_destroy(graph_);
@@ -1133,7 +1211,7 @@ private:
         std::vector<gb_context*> ctxs;
         for (const Lane& l : lanes_) ctxs.push_back(l.ctx);
         detail::check(gb_graph_begin(ctxs.data(), static_cast<int32_t>(ctxs.size())), "step: graph_begin");
-        run_views(targets, false);
+        run_views(targets, false, false);
         detail::check(gb_graph_end(ctxs.data(), static_cast<int32_t>(ctxs.size()), &graph_), "step: graph_end");
         graph_key_ = targets;
     }
@@ -1195,8 +1273,22 @@ private:
         detail::check(gb_adam_segments(ctx_, 0, segs_.data(), static_cast<int32_t>(segs_.size()), &st, &l, flag),
                       "step: adam");
         if (multi) detail::check(gb_allreduce_flag_min(ctx_, comm_, flag), "step: flag");  // optim.hpp:81-83, agreed
-        detail::check(gb_adam_segments(ctx_, 1, segs_.data(), static_cast<int32_t>(segs_.size()), &st, &l, flag),
+        // phase 1: the small groups on the main stream, the texel group (90 % of Adam's bytes) on the Adam
+        // stream, overlapping the next step's binning (one GPU: the all-gather below needs every group)
+        std::vector<gb_adam_segment> main_segs, grid_segs;
+        for (const gb_adam_segment& sg : segs_) (sg.group == 4 && !multi ? grid_segs : main_segs).push_back(sg);
+        gb_adam_state st_grid = st;
+        detail::check(gb_adam_segments(ctx_, 1, main_segs.data(), static_cast<int32_t>(main_segs.size()), &st, &l,
+                                       flag),
                       "step: adam");
+        if (!grid_segs.empty()) {
+            detail::check(gb_event_record(ctx_, ev_scan_), "step");
+            detail::check(gb_stream_wait_event(adam_ctx_, ev_scan_, 0), "step");
+            detail::check(gb_adam_segments(adam_ctx_, 1, grid_segs.data(), static_cast<int32_t>(grid_segs.size()),
+                                           &st_grid, &l, flag),
+                          "step: adam");
+            detail::check(gb_event_record(adam_ctx_, ev_grid_done_), "step");
+        }
         if (multi && cfg_.sharded_adam)
             detail::check(gb_all_gather_params(ctx_, comm_, params_->f() + lo_, params_->f(), S_), "step: all-gather");
         int64_t code = 0;
@@ -1207,8 +1299,15 @@ private:
     static constexpr int64_t kClear = GB_ADAM_FLAG_CLEAR;
     std::vector<Lane> lanes_;
     gb_context* ctx_ = nullptr;
+    gb_context* adam_ctx_ = nullptr;
+    gb_context* copy_ctx_ = nullptr;
     gb_comm* comm_ = nullptr;
     void* ev_start_ = nullptr;
+    void* ev_scan_ = nullptr;
+    void* ev_grid_done_ = nullptr;
+    std::vector<std::unique_ptr<detail::Buffer>> host_bufs_;
+    std::vector<void*> copy_done_, buf_free_;
+    int device_ = 0;
     std::vector<PinholeCamera> cams_;
     std::vector<int> views_;
     StepConfig cfg_;

@@ -70,6 +70,20 @@ __attribute__((visibility("default"))) int gb_mv_step(void* h, int nviews, const
     }
 }
 
+// The end-to-end step: targets in (pinned) host memory, copied every step inside the call.
+__attribute__((visibility("default"))) int gb_mv_step_host(void* h, int nviews, const float* const* host_targets,
+                                                           double* loss) {
+    try {
+        auto* r = static_cast<mv::Rank*>(h);
+        const double l = r->step_host(std::vector<const float*>(host_targets, host_targets + nviews));
+        if (loss) *loss = l;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 __attribute__((visibility("default"))) int gb_mv_params(void* h, float* out, int64_t cap) {
     try {
         const std::vector<float> p = static_cast<mv::Rank*>(h)->download_params();
