@@ -105,11 +105,17 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
     real wk[NX];  // corner weights
 #pragma unroll
     for (int k = 0; k < NX; ++k) wk[k] = (real)0;
-    if (on) {
-        T = mul_rn(T, rcp_approx(sub_rn((real)1, alpha)));  // raster.hpp:333
+    {
+        // Branch-free: every lane runs the arithmetic (the warp issues it anyway), lanes that are not on
+        // skip the texel loads (predicated) and select zeros / their old state at the end -- no divergent
+        // region, no BSSY/BSYNC reconvergence per entry.  Off lanes' u, v may be non-finite (a missed
+        // plane): the texel addresses are clamped, and every value they reach is masked below.
+        const real Tn = mul_rn(T, rcp_approx(sub_rn((real)1, alpha)));  // raster.hpp:333
+        T = on ? Tn : T;
         real c0, c1, c2, fu_hat = (real)0, fv_hat = (real)0;
         const real aT = alpha * T;
-        const real chat[3] = {aT * g0, aT * g1, aT * g2};  // c_hat (raster.hpp:338-340)
+        const real chat[3] = {on ? aT * g0 : (real)0, on ? aT * g1 : (real)0,
+                              on ? aT * g2 : (real)0};  // c_hat (raster.hpp:338-340)
         real cc_[3];
         if (CELL == kCellFull) {
             Bilin b;
@@ -118,7 +124,8 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             const float* p10 = p00 + 3 * N;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const real c00 = p00[c], c10 = p10[c], c01 = p00[3 + c], c11 = p10[3 + c];
+                const real c00 = on ? p00[c] : 0.f, c10 = on ? p10[c] : 0.f, c01 = on ? p00[3 + c] : 0.f,
+                           c11 = on ? p10[3 + c] : 0.f;
                 cc_[c] = c00 * b.w00 + c10 * b.w10 + c01 * b.w01 + c11 * b.w11;
                 tg[c] = chat[c] * b.w00;
                 tg[3 + c] = chat[c] * b.w10;
@@ -150,7 +157,7 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             real fh = (real)0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const real ca = pa[c], cb = pb[c];
+                const real ca = on ? pa[c] : 0.f, cb = on ? pb[c] : 0.f;
                 cc_[c] = fma_rn(cb, f, ca * gf);  // = the four-corner blend with two zero weights
                 tg[c] = chat[c] * gf;
                 tg[3 + c] = chat[c] * f;
@@ -167,12 +174,12 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             tt = iu * N + iv;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                cc_[c] = t[3 * tt + c];
+                cc_[c] = on ? t[3 * tt + c] : 0.f;
                 tg[c] = chat[c];
             }
             wk[0] = (real)1;
         }
-        GB_CHECK(tt >= 0 && tt + cell_texel<CELL>(NX - 1, N) < N * N);
+        GB_CHECK(!on || (tt >= 0 && tt + cell_texel<CELL>(NX - 1, N) < N * N));
         c0 = cc_[0];
         c1 = cc_[1];
         c2 = cc_[2];
@@ -211,11 +218,13 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             red[8] = pt.dy * gc2;
             red[9] = op;
         }
+#pragma unroll
+        for (int i = 0; i < NS; ++i) red[i] = on ? red[i] : (real)0;
         // raster.hpp:362
         const real om = (real)1 - alpha;
-        bh0 = alpha * c0 + om * bh0;
-        bh1 = alpha * c1 + om * bh1;
-        bh2 = alpha * c2 + om * bh2;
+        bh0 = on ? alpha * c0 + om * bh0 : bh0;
+        bh1 = on ? alpha * c1 + om * bh1 : bh1;
+        bh2 = on ? alpha * c2 + om * bh2 : bh2;
     }
     // S: the texel-gradient stride, 3 (reference layout (i_u, i_v, channel)) or 4 (RGBA-padded,
     // gb_context_set_texel_grad_stride: texel records 16-B aligned, one vector red each)
@@ -292,25 +301,19 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
                                           int lane, real* wscratch, real* __restrict__ accum,
                                           real* __restrict__ grid_grad) {
     const real sigma = rc.sigma;
-    bool on = rank <= last;
-    real u = 0.f, v = 0.f, G = 0.f, alpha = 0.f, araw = 0.f;
+    // evaluated on every lane (branch-free; lanes past their last rank or missing the plane are masked)
+    real u, v;
     PinholeTerms pt;
-    if (on) {
-        bool hit;
-        if (MODE == GB_MODE_ORTHO) {
-            hit = eval_uv_ortho(h, x, y, u, v);
-        } else {
-            hit = eval_uv_pinhole(h, x, y, u, v, pt);
-        }
-        if (hit) {
-            G = gauss_weight(u, v);
-            araw = mul_rn(h.h1.z, G);
-            alpha = rmin(araw, kMaxAlpha);
-            on = !(alpha < rc.alpha_skip);
-        } else {
-            on = false;
-        }
+    bool hit;
+    if (MODE == GB_MODE_ORTHO) {
+        hit = eval_uv_ortho(h, x, y, u, v);
+    } else {
+        hit = eval_uv_pinhole(h, x, y, u, v, pt);
     }
+    const real G = gauss_weight(u, v);
+    const real araw = mul_rn(h.h1.z, G);
+    const real alpha = rmin(araw, kMaxAlpha);
+    const bool on = rank <= last && hit && !(alpha < rc.alpha_skip);
     const unsigned act = __ballot_sync(kFull, on);
     if (act == 0) return;
     if (lane == 0) {
