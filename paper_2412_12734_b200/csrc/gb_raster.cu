@@ -820,10 +820,11 @@ __global__ void __launch_bounds__(256) k_forward_loss(const uint2* __restrict__ 
     if ((threadIdx.x & 31) == 0 && loss && l != (real)0) atomicAdd(loss, (float)(l * scale));
 }
 
-// <= 48 registers: 5 CTAs (40 warps) per SM -- with 32 B of spills, measured 1.3 % faster than 64
-// registers at 4 CTAs (6 CTAs at 40 registers: no gain)
+// <= 64 registers: 4 CTAs (32 warps) per SM, no spills -- with the branch-free entry, measured 1.0 %
+// faster than 5 CTAs at 48 registers (16 B of spills) and 7 % faster than 6 CTAs at 40 (56 B)
+// (before it, 5 CTAs with 32 B of spills had been 1.3 % faster than 4)
 #ifndef GB_K4_MINB
-#define GB_K4_MINB 5
+#define GB_K4_MINB 4
 #endif
 template <int MODE, int NT, int S>
 __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2* __restrict__ ranges,
