@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (markdown + the JSON bench.py reads for roofline.traffic).
 
-    python tools/ncu_summary.py <tag> <launches.csv> <kernel>=<report.ncu-rep> [...]
+    python tools/ncu_summary.py <tag> <launches.csv> <kernel>=<report.ncu-rep>[@<kernel regex>] [...]
 
 Writes profiles/ncu_<tag>.md and updates profiles/ncu_summary.json with
 {kernel: {"dram_bytes_per_launch": ..., ...}} for each full capture.
@@ -47,7 +47,10 @@ def to_bytes(unit, val):
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # "<report>@<kernel regex>": the first launch of that kernel in a multi-kernel report
+    rep, _, pat = rep.partition("@")
+    flt = ["--kernel-name", "regex:" + pat] if pat else []
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"] + flt, capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     res = []
@@ -93,7 +96,7 @@ def main():
     for kern, rep in caps.items():
         for d in raw(rep)[:1]:
             name = d.get("Kernel Name", ("", kern))[1]
-            md += [f"## `{kern}` — full capture (`{os.path.basename(rep)}`)", "", f"`{name[:150]}`", "",
+            md += [f"## `{kern}` — full capture (`{os.path.basename(rep.partition('@')[0])}`)", "", f"`{name[:150]}`", "",
                    "| metric | value | unit |", "|---|---|---|"]
             for key, label in METRICS:
                 if key in d:
@@ -102,7 +105,7 @@ def main():
             rd = to_bytes(*[d["dram__bytes_read.sum"][0], float(d["dram__bytes_read.sum"][1].replace(",", ""))])
             wr = to_bytes(*[d["dram__bytes_write.sum"][0], float(d["dram__bytes_write.sum"][1].replace(",", ""))])
             sj[kern] = {"dram_bytes_per_launch": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
-                        "kernel": name[:200], "source": f"profiles/ncu_{tag}.md", "report": os.path.basename(rep)}
+                        "kernel": name[:200], "source": f"profiles/ncu_{tag}.md", "report": os.path.basename(rep.partition("@")[0])}
     open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w").write("\n".join(md) + "\n")
     json.dump(sj, open(sj_path, "w"), indent=1)
     print("\n".join(md))
