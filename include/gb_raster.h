@@ -162,10 +162,10 @@ GB_API int64_t gb_context_launch_count(const gb_context *ctx);
  * enabled, every launch site is bracketed by two events; _read synchronises,
  * returns total milliseconds and launch counts per kernel id, and resets. */
 #define GB_K_PROJECT 0   /* K1  per-primitive projection + cull + tile rect */
-#define GB_K_SCAN 1      /* K2a tile-count scan (CUB) */
-#define GB_K_DUPLICATE 2 /* K2b (tile|depth) key duplication */
-#define GB_K_SORT 3      /* K2c radix sort (CUB) */
-#define GB_K_RANGES 4    /* K2d per-tile ranges */
+#define GB_K_SCAN 1      /* K2a per-tile pair counts + their scan (CUB) */
+#define GB_K_DUPLICATE 2 /* K2b scatter of the (depth, id) keys into the tile buckets */
+#define GB_K_SORT 3      /* K2c per-tile bucket sort -> lists and ranges */
+#define GB_K_RANGES 4    /* (no separate pass since the tile-bucket build: ranges come with K2c) */
 #define GB_K_FORWARD 5   /* K3  forward compositor */
 #define GB_K_BACKWARD 6  /* K4  backward compositor */
 #define GB_K_CHAIN 7     /* K5  per-primitive gradient chain */

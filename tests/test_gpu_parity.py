@@ -90,6 +90,15 @@ def test_ortho_tile_sizes(ts):
     _check(f"ortho_ts{ts}", arrays, O.MODE_ORTHO, 4, cam, O.Cfg(tile_size=ts))
 
 
+def test_ortho_many_tiles():
+    # 128 x 100 = 12800 tiles: past the binning's shared-memory tile counters (12288), so the build takes
+    # its global-atomic path (the other cases take the privatised one)
+    W, H = 256, 200
+    arrays = _ortho_scene(3000, 4, 21, W, H, 0.5, 4.0)
+    cam = O.Cam(O.MODE_ORTHO, W, H, (0.2, 0.2, 0.2))
+    _check("ortho_many_tiles", arrays, O.MODE_ORTHO, 4, cam, O.Cfg(tile_size=2))
+
+
 def test_ortho_thresholds_disabled():
     W, H = 64, 48
     arrays = _ortho_scene(300, 4, 5, W, H, 1.0, 6.0)

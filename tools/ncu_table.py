@@ -74,11 +74,19 @@ def main(rep, P, Kv, out_md, peak=None):
         elif name == "cub::DeviceRadixSortHistogramKernel":
             model = 4 * K if onesweep < 4 else 4 * P
         elif name == "cub::DeviceScanKernel":
-            model = 12 * K
+            model = 8 * nt
         elif name == "k_duplicate":
             model = 12 * P + 16 * Kv
         elif name == "k_ranges":
             model = 8 * P + 8 * nt
+        elif name == "k_tile_count":  # counts + rects of K primitives, the per-CTA count rows
+            model = 12 * K + 4 * 148 * nt
+        elif name == "k_tile_prefix":
+            model = 8 * 148 * nt + 4 * nt
+        elif name == "k_scatter_priv":  # counts, rects, depth of K primitives, one 8-B key per pair
+            model = 16 * K + 8 * P + 8 * 148 * nt
+        elif name == "k_tile_lists":  # keys in (and, past 128 keys, merge passes), ids and ranges out
+            model = 8 * P + 4 * P + 12 * nt
         elif name == "k_forward_direct":
             model = P * (4 + Bh + Bt) + 8 * nt + 20 * npx
         elif name == "k_backward_direct":
