@@ -22,7 +22,8 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns
 
 
 def short(name):
-    for k in ("k_project", "k_iota", "k_duplicate", "k_ranges", "k_pad", "k_forward_direct", "k_forward_loss",
+    for k in ("k_project", "k_tile_count", "k_tile_prefix", "k_scatter_priv", "k_tile_lists", "k_tile_hist",
+              "k_scatter", "k_forward_direct", "k_forward_loss",
               "k_backward_direct", "k_chain", "k_loss", "k_adam_check", "k_adam_update", "k_adam_flag_init"):
         if k in name:
             return k
