@@ -1,6 +1,8 @@
-"""Print the K4 development counters for one configs[2]-like view (needs tools/_dbg/libgb_raster.so from tools/dbg_counters.sh)."""
+"""Print the K4 development counters for one configs[3] view (needs variants/dbg/libgb_raster.so from
+tools/dbg_counters.sh, or GB_LIB_PATH pointing at another -DGB_DEBUG_COUNTERS build)."""
 import ctypes as C, os, sys
-os.environ["GB_LIB_PATH"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "_dbg", "libgb_raster.so")
+os.environ.setdefault("GB_LIB_PATH", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "variants",
+                                                 "dbg", "libgb_raster.so"))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2412_12734_b200 as gb, paper_2412_12734_b200.scenes as sc
