@@ -10,9 +10,13 @@
 //                   index) to every tile it overlaps (shared-memory cursors:
 //                   arbitrary order inside the bucket)
 //   k_tile_lists  : one CTA per tile sorts its bucket by that key -- a bitonic
-//                   sort of kSortChunk-key chunks (registers + shuffles for the
-//                   in-warp stages), then merge-path passes through global
-//                   memory -- and writes the primitive ids and the tile's range
+//                   sort of 128- or 2048-key chunks by the mean bucket length
+//                   (registers + shuffles for the in-warp stages), then
+//                   merge-path passes through global memory -- and writes the
+//                   primitive ids and the tile's range
+//
+// Deep scenes (more than kDeepBucket pairs per tile on average) take the two
+// stable radix sorts at the end of this file instead.
 //
 // (depth_bits, index) keys are unique, so every tile's list is in (depth_key,
 // index) order -- the reference's per-tile order (raster.hpp:141-145) -- bit for
@@ -28,7 +32,10 @@
 // key buffer holds `cap` slots; pairs past it are dropped, the lists clipped at
 // it and the overflow flagged (the caller redoes the step with more room), so
 // the whole build can be captured into a CUDA graph.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "gb_internal.cuh"
 
@@ -82,9 +89,6 @@ __global__ void __launch_bounds__(256) k_scatter(int64_t K, int tiles_x, const u
 #endif
 #ifndef GB_BIN_THREADS
 #define GB_BIN_THREADS 512
-#endif
-#ifndef GB_SORT_THREADS
-#define GB_SORT_THREADS 128
 #endif
 constexpr int kBinCtas = GB_BIN_CTAS;
 constexpr int kBinThreads = GB_BIN_THREADS;  // half an SM: co-resident with the compositors of other view lanes
@@ -165,11 +169,11 @@ __global__ void __launch_bounds__(kBinThreads) k_scatter_priv(int64_t K, int til
     }
 }
 
-constexpr int kSortThreads = GB_SORT_THREADS;
-#ifndef GB_SORT_CHUNK
-#define GB_SORT_CHUNK 128
-#endif
-constexpr int kSortChunk = GB_SORT_CHUNK;  // keys sorted in shared memory at once (8 B each)
+constexpr int kDeepBucket = 512;  // mean pairs per tile past which the radix build is used
+
+// Bucket sort <kSortChunk keys sorted in shared memory at once, kSortThreads>: 128-key chunks with 128
+// threads -- 1 KB of shared memory, so the sort's CTAs barely displace the other view lanes' compositors
+// (profiles/ab_r02.md s34-s36) -- then merge-path passes through global memory.
 
 // Ascending bitonic sort of s[0, np), np a power of two >= 64.  Each warp owns 64-key blocks (lane l holds
 // keys l and l + 32 of a block in registers): the stages with partner distance j <= 32 stay inside a block
@@ -199,6 +203,7 @@ __device__ __forceinline__ void block_stages(uint64_t& a, uint64_t& b, int pa, i
     }
 }
 
+template <int kSortThreads>
 __device__ __forceinline__ void bitonic_sort(uint64_t* s, int np) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarps = kSortThreads / 32;
@@ -234,16 +239,18 @@ __device__ __forceinline__ void bitonic_sort(uint64_t* s, int np) {
     }
 }
 
-// keys[0, n) (n <= kSortChunk) -> sorted in s
+// keys[0, n) (n <= the chunk) -> sorted in s
+template <int kSortThreads>
 __device__ __forceinline__ void sort_chunk(const uint64_t* __restrict__ keys, int n, uint64_t* s) {
     int np = 64;
     while (np < n) np <<= 1;
     for (int i = threadIdx.x; i < np; i += kSortThreads) s[i] = i < n ? keys[i] : ~0ull;
     __syncthreads();
-    bitonic_sort(s, np);
+    bitonic_sort<kSortThreads>(s, np);
 }
 
 // one pass of the bucket merge sort: runs of length L in src[0, n) merged pairwise into dst (merge path)
+template <int kSortThreads>
 __device__ void merge_pass(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, int n, int L) {
     constexpr int IT = 8;
     for (int base = 0; base < n; base += kSortThreads * IT) {
@@ -272,43 +279,58 @@ __device__ void merge_pass(const uint64_t* __restrict__ src, uint64_t* __restric
     __syncthreads();
 }
 
-// One CTA per tile: the tile's bucket [min(off[t], limit), min(off[t+1], limit)) sorted by key, the primitive
-// ids into values, the tile's range into ranges; tile 0 flags a total past the capacity.
+// tile t's bucket [min(off[t], limit), min(off[t+1], limit)) and range; tile 0 flags a total past the capacity
+__device__ __forceinline__ int tile_bucket(const uint32_t* __restrict__ tile_off, uint32_t limit, int n_tiles,
+                                           uint2* __restrict__ ranges, int32_t* __restrict__ overflow,
+                                           uint32_t& b) {
+    const int t = blockIdx.x;
+    b = min(tile_off[t], limit);
+    const uint32_t e = min(tile_off[t + 1], limit);
+    if (threadIdx.x == 0) {
+        ranges[t] = make_uint2(b, e);
+        if (t == 0 && overflow && tile_off[n_tiles] > limit) *overflow = 1;
+    }
+    return (int)(e - b);
+}
+
+// the global-memory tail of a bucket sort: runs of L sorted keys in keys[0, n) merged up to one run, the ids
+// written to values
+template <int kThreads>
+__device__ __forceinline__ void merge_runs(uint64_t* src, uint64_t* dst, int n, int L, int32_t* __restrict__ values) {
+    for (; L < n; L <<= 1) {
+        merge_pass<kThreads>(src, dst, n, L);
+        uint64_t* tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    for (int i = threadIdx.x; i < n; i += kThreads) values[i] = (int32_t)(uint32_t)src[i];
+}
+
+// One CTA per tile sorts its bucket in 128-key register/shared bitonic chunks, then merges them in global
+// memory; the primitive ids go to values, the range to ranges.
+template <int kSortChunk, int kSortThreads>
 __global__ void __launch_bounds__(kSortThreads) k_tile_lists(const uint32_t* __restrict__ tile_off, uint32_t limit,
                                                              int n_tiles, uint64_t* __restrict__ keys,
                                                              uint64_t* __restrict__ scratch,
                                                              int32_t* __restrict__ values, uint2* __restrict__ ranges,
                                                              int32_t* __restrict__ overflow) {
     __shared__ uint64_t s[kSortChunk];
-    const int t = blockIdx.x;
-    const uint32_t b = min(tile_off[t], limit), e = min(tile_off[t + 1], limit);
-    if (threadIdx.x == 0) {
-        ranges[t] = make_uint2(b, e);
-        if (t == 0 && overflow && tile_off[n_tiles] > limit) *overflow = 1;
-    }
-    const int n = (int)(e - b);
+    uint32_t b;
+    const int n = tile_bucket(tile_off, limit, n_tiles, ranges, overflow, b);
     if (n == 0) return;
     if (n <= kSortChunk) {
-        sort_chunk(keys + b, n, s);
+        sort_chunk<kSortThreads>(keys + b, n, s);
         for (int i = threadIdx.x; i < n; i += kSortThreads) values[b + i] = (int32_t)(uint32_t)s[i];
         return;
     }
-    // large bucket: sorted chunks of kSortChunk, then merge passes between keys and scratch
     uint64_t* src = keys + b;
-    uint64_t* dst = scratch + b;
     for (int c = 0; c < n; c += kSortChunk) {
         const int m = min(kSortChunk, n - c);
-        sort_chunk(src + c, m, s);
+        sort_chunk<kSortThreads>(src + c, m, s);
         for (int i = threadIdx.x; i < m; i += kSortThreads) src[c + i] = s[i];
         __syncthreads();
     }
-    for (int L = kSortChunk; L < n; L <<= 1) {
-        merge_pass(src, dst, n, L);
-        uint64_t* tmp = src;
-        src = dst;
-        dst = tmp;
-    }
-    for (int i = threadIdx.x; i < n; i += kSortThreads) values[b + i] = (int32_t)(uint32_t)src[i];
+    merge_runs<kSortThreads>(src, scratch + b, n, kSortChunk, values + b);
 }
 
 size_t tile_scan_temp_bytes(int n_tiles) {
@@ -370,7 +392,155 @@ int tile_offsets_launches(int64_t K, int n_tiles) {
 cudaError_t launch_tile_lists(int n_tiles, const uint32_t* tile_off, uint32_t limit, uint64_t* keys,
                               uint64_t* scratch, int32_t* values, uint2* ranges, int32_t* overflow, cudaStream_t st) {
     if (n_tiles == 0) return cudaSuccess;
-    k_tile_lists<<<n_tiles, kSortThreads, 0, st>>>(tile_off, limit, n_tiles, keys, scratch, values, ranges, overflow);
+    k_tile_lists<128, 128><<<n_tiles, 128, 0, st>>>(tile_off, limit, n_tiles, keys, scratch, values, ranges,
+                                                    overflow);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Deep scenes (mean tile list > kDeepBucket pairs, e.g. configs[4] at 4M surfels: ~2000 per tile, up to
+// ~7.7K): two stable CUB radix sorts.  The primitives' 32-bit depth keys are sorted once (culled ones carry
+// ~0 and sort last), the tile counts scanned in that order, each primitive's (tile id, primitive) pairs
+// emitted in that order and stably sorted on the ceil(log2 tiles) tile-id bits only -- bit-identical to a
+// sort of (tile << 32 | depth) keys.  At these list lengths the per-tile bucket sorts above cost more than
+// the bandwidth-bound radix passes (4M x 1: 1.36 vs 1.00 ms per build).  Capacity mode pads the slots past
+// P with the key n_tiles, which sorts after every tile and k_ranges skips.
+// ---------------------------------------------------------------------------
+int deep_bucket_mean() { return kDeepBucket; }
+
+__global__ void __launch_bounds__(256) k_iota(int64_t K, int32_t* __restrict__ out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < K) out[k] = (int32_t)k;
+}
+
+// cap: pair capacity of keys/values.  Pairs at or beyond it are dropped and flagged in *overflow
+// (capacity mode only; the blocking mode sizes the buffers to P exactly).
+__global__ void __launch_bounds__(256) k_duplicate(int64_t K, int tiles_x, const int32_t* __restrict__ perm,
+                                                   const uint32_t* __restrict__ offsets,
+                                                   const uint2* __restrict__ rects, uint32_t* __restrict__ keys,
+                                                   int32_t* __restrict__ values, uint32_t cap,
+                                                   int32_t* __restrict__ overflow) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const uint32_t end = min(offsets[i + 1], cap);
+    uint32_t o = offsets[i];
+    if (i == K - 1 && offsets[K] > cap && overflow) *overflow = 1;
+    if (o >= end) return;
+    const int32_t k = perm[i];
+    const uint2 r = rects[k];
+    const int tx0 = r.x & 0xffff, ty0 = r.x >> 16, tx1 = r.y & 0xffff, ty1 = r.y >> 16;
+    for (int ty = ty0; ty <= ty1 && o < end; ++ty)
+        for (int tx = tx0; tx <= tx1 && o < end; ++tx) {
+            keys[o] = (uint32_t)(ty * tiles_x + tx);
+            values[o] = k;
+            ++o;
+        }
+}
+
+// capacity mode: slots [P, cap) get the pad tile key n_tiles, which sorts after every real tile
+__global__ void __launch_bounds__(256) k_pad(uint32_t cap, const uint32_t* __restrict__ total, uint32_t pad,
+                                             uint32_t* __restrict__ keys, int32_t* __restrict__ values) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cap || i < *total) return;
+    keys[i] = pad;
+    values[i] = -1;
+}
+
+// pairs with a pad key (>= n_tiles) belong to no tile
+__global__ void __launch_bounds__(256) k_ranges(int64_t P, const uint32_t* __restrict__ keys,
+                                                uint2* __restrict__ ranges, uint32_t n_tiles) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const uint32_t tile = keys[i];
+    if (tile >= n_tiles) return;
+    if (i == 0 || keys[i - 1] != tile) ranges[tile].x = (uint32_t)i;
+    if (i == P - 1 || keys[i + 1] != tile) ranges[tile].y = (uint32_t)(i + 1);
+}
+
+static int bits_for(uint32_t v) {
+    int b = 0;
+    while (b < 32 && (1ull << b) < (uint64_t)v) ++b;
+    return b;
+}
+
+// key bits covering tile keys 0 .. n_keys - 1 (n_keys = n_tiles, + 1 for the capacity mode's pad key)
+int tile_sort_bits(int n_keys) {
+    const int b = bits_for((uint32_t)n_keys);
+    return b ? b : 1;
+}
+
+// counts[perm[i]]: the tile counts read in depth order straight into the scan (no gather pass)
+struct PermutedCount {
+    const int32_t* perm;
+    const uint32_t* counts;
+    __host__ __device__ uint32_t operator()(int64_t i) const { return counts[perm[i]]; }
+};
+using CountIter = thrust::transform_iterator<PermutedCount, thrust::counting_iterator<int64_t>, uint32_t>;
+
+size_t scan_temp_bytes(int64_t K) {
+    size_t bytes = 0;
+    CountIter it(thrust::counting_iterator<int64_t>(0), PermutedCount{nullptr, nullptr});
+    cub::DeviceScan::InclusiveScan(nullptr, bytes, it, (uint32_t*)nullptr, SatAdd{}, (int)K);
+    return bytes;
+}
+
+size_t sort_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)n);
+    return bytes;
+}
+
+// Radix passes CUB launches for a sort over `bits` key bits (histogram + exclusive sum + one per 8-bit digit).
+int sort_launches(int bits) { return bits > 0 ? 2 + (bits + 7) / 8 : 0; }
+
+// perm = primitive indices in stable (depth_bits, index) order; depth_sorted is scratch.
+cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* depth_bits, uint32_t* depth_sorted,
+                              int32_t* iota, int32_t* perm, int64_t K, cudaStream_t st) {
+    if (K == 0) return cudaSuccess;
+    k_iota<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, iota);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, depth_bits, depth_sorted, iota, perm, (int)K, 0, 32, st);
+}
+
+// offsets (K+1 entries) = exclusive scan of the counts in perm order; offsets[K] = P (saturated at 2^31 - 1).
+cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
+                        uint32_t* offsets, int64_t K, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(offsets, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess || K == 0) return e;
+    CountIter it(thrust::counting_iterator<int64_t>(0), PermutedCount{perm, counts});
+    return cub::DeviceScan::InclusiveScan(temp, temp_bytes, it, offsets + 1, SatAdd{}, (int)K, st);
+}
+
+cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,
+                             uint32_t* keys, int32_t* values, uint32_t cap, int32_t* overflow, cudaStream_t st) {
+    if (K == 0) return cudaSuccess;
+    k_duplicate<<<(unsigned)((K + 255) / 256), 256, 0, st>>>(K, tiles_x, perm, offsets, rects, keys, values, cap,
+                                                             overflow);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad(uint32_t cap, const uint32_t* total, int n_tiles, uint32_t* keys, int32_t* values,
+                       cudaStream_t st) {
+    if (cap == 0) return cudaSuccess;
+    k_pad<<<(cap + 255) / 256, 256, 0, st>>>(cap, total, (uint32_t)n_tiles, keys, values);
+    return cudaGetLastError();
+}
+
+// Stable sort of (tile id, primitive) pairs on the tile-id bits.
+cudaError_t launch_tile_sort(void* temp, size_t temp_bytes, uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_in,
+                             int32_t* vals_out, int64_t P, int n_keys, cudaStream_t st) {
+    if (P == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)P, 0,
+                                           tile_sort_bits(n_keys), st);
+}
+
+
+cudaError_t launch_ranges(int64_t P, const uint32_t* keys, uint2* ranges, int n_tiles, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)n_tiles, st);
+    if (e != cudaSuccess || P == 0) return e;
+    k_ranges<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, keys, ranges, (uint32_t)n_tiles);
     return cudaGetLastError();
 }
 

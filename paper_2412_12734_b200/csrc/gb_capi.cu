@@ -17,6 +17,22 @@
 #include "gb_io.cuh"
 
 namespace gb {
+size_t scan_temp_bytes(int64_t K);
+size_t sort_temp_bytes(int64_t n);
+int sort_launches(int bits);
+int tile_sort_bits(int n_keys);
+cudaError_t launch_depth_sort(void* temp, size_t temp_bytes, const uint32_t* depth_bits, uint32_t* depth_sorted,
+                              int32_t* iota, int32_t* perm, int64_t K, cudaStream_t st);
+cudaError_t launch_scan(void* temp, size_t temp_bytes, const int32_t* perm, const uint32_t* counts,
+                        uint32_t* offsets, int64_t K, cudaStream_t st);
+cudaError_t launch_duplicate(int64_t K, int tiles_x, const int32_t* perm, const uint32_t* offsets, const uint2* rects,
+                             uint32_t* keys, int32_t* values, uint32_t cap, int32_t* overflow, cudaStream_t st);
+cudaError_t launch_pad(uint32_t cap, const uint32_t* total, int n_tiles, uint32_t* keys, int32_t* values,
+                       cudaStream_t st);
+cudaError_t launch_tile_sort(void* temp, size_t temp_bytes, uint32_t* keys_in, uint32_t* keys_out, int32_t* vals_in,
+                             int32_t* vals_out, int64_t P, int n_keys, cudaStream_t st);
+cudaError_t launch_ranges(int64_t P, const uint32_t* keys, uint2* ranges, int n_tiles, cudaStream_t st);
+int deep_bucket_mean();
 size_t tile_scan_temp_bytes(int n_tiles);
 size_t tile_scratch_words(int n_tiles);
 int tile_offsets_launches(int64_t K, int n_tiles);
@@ -128,6 +144,7 @@ struct gb_context {
     int texel_grad_stride = 3;  // gb_context_set_texel_grad_stride
     DevBuf grid64;  // parity build: fp64 texel-gradient scratch (added into the caller's fp32 buffer after K4)
     DevBuf tile_hist, keys64_tmp;  // binning scratch (per-tile counts and CTA bases, bucket merge passes)
+    DevBuf sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp;  // radix build scratch
     DevBuf scan_temp, accum, adam_bad, ssim_tmp,
         metric_tmp, fuse_color, fuse_trans, fuse_last, fuse_grad;
     uint32_t* pinned_total = nullptr;
@@ -204,7 +221,9 @@ struct gb_binning {
     int64_t capacity = 0;  // > 0: capacity mode (no host read-back of P; see gb_binning_set_capacity)
     int32_t* overflow = nullptr;
     DevBuf headers, cull, rects, counts, depth, values, ranges;
-    DevBuf tile_off, keys64;  // tile offsets (n_tiles + 1; [n_tiles] = P), (depth_bits << 32 | id) keys
+    DevBuf tile_off, keys64;  // tile-bucket build: tile offsets (n_tiles + 1; [n_tiles] = P), (depth << 32 | id) keys
+    DevBuf offsets, perm, keys;  // radix build (deep scenes): per-primitive pair offsets ([K] = P), depth order
+    bool radix = false;          // the last build took the radix path
     DevBuf trans64;  // parity build: the forward's fp64 final transmittance, rewound by the backward
 };
 
@@ -358,6 +377,11 @@ gb_status gb_context_destroy(gb_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->scan_temp.release();
     ctx->tile_hist.release();
+    ctx->sort_temp.release();
+    ctx->keys_tmp.release();
+    ctx->vals_tmp.release();
+    ctx->depth_tmp.release();
+    ctx->iota_tmp.release();
     ctx->keys64_tmp.release();
     ctx->accum.release();
     ctx->grid64.release();
@@ -671,6 +695,9 @@ gb_status gb_binning_destroy(gb_binning* b) {
     b->depth.release();
     b->values.release();
     b->tile_off.release();
+    b->offsets.release();
+    b->perm.release();
+    b->keys.release();
     b->keys64.release();
     b->ranges.release();
     b->trans64.release();
@@ -702,12 +729,10 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
     GB_CUDA(b->cull.ensure(sizeof(gb::CullRec) * Kc));
     GB_CUDA(b->rects.ensure(sizeof(uint2) * Kc));
     GB_CUDA(b->counts.ensure(sizeof(uint32_t) * Kc));
-    // K1, then the tile-bucket build (gb_binning.cu): per-tile counts + scan, scatter, per-tile sort
+    // K1, then K2 (gb_binning.cu): tile buckets sorted in place, or -- deep scenes, more than
+    // deep_bucket_mean() pairs per tile on average -- the two stable radix sorts
     GB_CUDA(b->depth.ensure(sizeof(uint32_t) * Kc));
     GB_CUDA(b->ranges.ensure(sizeof(uint2) * (n_tiles > 0 ? n_tiles : 1)));
-    GB_CUDA(b->tile_off.ensure(sizeof(uint32_t) * ((size_t)n_tiles + 1)));
-    GB_CUDA(ctx->tile_hist.ensure(sizeof(uint32_t) * gb::tile_scratch_words(n_tiles)));
-    GB_CUDA(ctx->scan_temp.ensure(gb::tile_scan_temp_bytes(n_tiles)));
     gb::ProjParams pp = gb::make_proj_params(s, cam, cfg, b->tiles_x, b->tiles_y);
     {
         ProfScope ps(ctx, GB_K_PROJECT);
@@ -715,44 +740,112 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
                                    b->counts.as<uint32_t>(), b->depth.as<uint32_t>(), stream));
     }
     ctx->launches += K > 0;
+    const int64_t deep = (int64_t)gb::deep_bucket_mean() * n_tiles;
+    // capacity mode decides by the slots; the blocking mode by the pair count its tile scan reads back
+    bool radix = b->capacity > deep;
+    int64_t P = 0;  // pair slots the lists are built in: the exact count, or the capacity
+    if (!radix) {
+        GB_CUDA(b->tile_off.ensure(sizeof(uint32_t) * ((size_t)n_tiles + 1)));
+        GB_CUDA(ctx->tile_hist.ensure(sizeof(uint32_t) * gb::tile_scratch_words(n_tiles)));
+        GB_CUDA(ctx->scan_temp.ensure(gb::tile_scan_temp_bytes(n_tiles)));
+        {
+            ProfScope ps(ctx, GB_K_SCAN);
+            GB_CUDA(gb::launch_tile_offsets(ctx->scan_temp.p, ctx->scan_temp.cap, K, b->tiles_x, n_tiles,
+                                            b->counts.as<uint32_t>(), b->rects.as<uint2>(),
+                                            ctx->tile_hist.as<uint32_t>(), b->tile_off.as<uint32_t>(), stream));
+        }
+        ctx->launches += gb::tile_offsets_launches(K, n_tiles);
+        if (b->capacity > 0) {
+            P = b->capacity;
+            b->P = -1;
+        } else {
+            GB_CUDA(cudaMemcpyAsync(ctx->pinned_total, b->tile_off.as<uint32_t>() + n_tiles, sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, stream));
+            GB_CUDA(cudaStreamSynchronize(stream));
+            P = *ctx->pinned_total;
+            if (P >= 0x7fffffffll)
+                return fail(GB_NOT_SUPPORTED,
+                            "build_binning: %lld+ tile/primitive pairs exceed the 2^31 - 1 the lists index",
+                            (long long)P);
+            b->P = P;
+            radix = P > deep;
+        }
+    }
+    b->radix = radix;
+    if (!radix) {
+        const int64_t Pc = P > 0 ? P : 1;
+        GB_CUDA(b->keys64.ensure(sizeof(uint64_t) * Pc));
+        GB_CUDA(b->values.ensure(sizeof(int32_t) * Pc));
+        GB_CUDA(ctx->keys64_tmp.ensure(sizeof(uint64_t) * Pc));
+        {
+            ProfScope ps(ctx, GB_K_DUPLICATE);
+            GB_CUDA(gb::launch_scatter(K, b->tiles_x, n_tiles, b->counts.as<uint32_t>(), b->rects.as<uint2>(),
+                                       b->depth.as<uint32_t>(), b->tile_off.as<uint32_t>(),
+                                       ctx->tile_hist.as<uint32_t>(), b->keys64.as<uint64_t>(), (uint32_t)P, stream));
+        }
+        {
+            ProfScope ps(ctx, GB_K_SORT);
+            GB_CUDA(gb::launch_tile_lists(n_tiles, b->tile_off.as<uint32_t>(), (uint32_t)P, b->keys64.as<uint64_t>(),
+                                          ctx->keys64_tmp.as<uint64_t>(), b->values.as<int32_t>(),
+                                          b->ranges.as<uint2>(), b->capacity > 0 ? b->overflow : nullptr, stream));
+        }
+        ctx->launches += (K > 0 && n_tiles > 0) + (n_tiles > 0);
+        b->built = true;
+        return GB_OK;
+    }
+    // deep scenes: K2a primitives in (depth, index) order
+    GB_CUDA(b->offsets.ensure(sizeof(uint32_t) * (Kc + 1)));
+    GB_CUDA(b->perm.ensure(sizeof(int32_t) * Kc));
+    GB_CUDA(ctx->depth_tmp.ensure(sizeof(uint32_t) * Kc));
+    GB_CUDA(ctx->iota_tmp.ensure(sizeof(int32_t) * Kc));
+    GB_CUDA(ctx->scan_temp.ensure(gb::scan_temp_bytes(Kc)));
+    GB_CUDA(ctx->sort_temp.ensure(gb::sort_temp_bytes(Kc)));
+    {
+        ProfScope ps(ctx, GB_K_SORT);
+        GB_CUDA(gb::launch_depth_sort(ctx->sort_temp.p, ctx->sort_temp.cap, b->depth.as<uint32_t>(),
+                                      ctx->depth_tmp.as<uint32_t>(), ctx->iota_tmp.as<int32_t>(),
+                                      b->perm.as<int32_t>(), K, stream));
+    }
+    ctx->launches += K > 0 ? 1 + gb::sort_launches(32) : 0;
+    // K2b tile counts in that order, scanned -> P
     {
         ProfScope ps(ctx, GB_K_SCAN);
-        GB_CUDA(gb::launch_tile_offsets(ctx->scan_temp.p, ctx->scan_temp.cap, K, b->tiles_x, n_tiles,
-                                        b->counts.as<uint32_t>(), b->rects.as<uint2>(), ctx->tile_hist.as<uint32_t>(),
-                                        b->tile_off.as<uint32_t>(), stream));
+        GB_CUDA(gb::launch_scan(ctx->scan_temp.p, ctx->scan_temp.cap, b->perm.as<int32_t>(), b->counts.as<uint32_t>(),
+                                b->offsets.as<uint32_t>(), K, stream));
     }
-    ctx->launches += gb::tile_offsets_launches(K, n_tiles);
-    int64_t P;  // pair slots the lists are built in: the exact count, or the capacity
+    ctx->launches += K > 0 ? 2 : 0;  // CUB scan (init + scan) over the permuted counts
     if (b->capacity > 0) {
         P = b->capacity;
         b->P = -1;
-    } else {
-        GB_CUDA(cudaMemcpyAsync(ctx->pinned_total, b->tile_off.as<uint32_t>() + n_tiles, sizeof(uint32_t),
-                                cudaMemcpyDeviceToHost, stream));
-        GB_CUDA(cudaStreamSynchronize(stream));
-        P = *ctx->pinned_total;
-        if (P >= 0x7fffffffll)
-            return fail(GB_NOT_SUPPORTED, "build_binning: %lld+ tile/primitive pairs exceed the 2^31 - 1 the lists index",
-                        (long long)P);
-        b->P = P;
-    }
+    }  // (blocking: P and b->P from the tile scan above)
     const int64_t Pc = P > 0 ? P : 1;
-    GB_CUDA(b->keys64.ensure(sizeof(uint64_t) * Pc));
+    const int n_keys = n_tiles + (b->capacity > 0);
+    GB_CUDA(b->keys.ensure(sizeof(uint32_t) * Pc));
     GB_CUDA(b->values.ensure(sizeof(int32_t) * Pc));
-    GB_CUDA(ctx->keys64_tmp.ensure(sizeof(uint64_t) * Pc));
+    GB_CUDA(ctx->keys_tmp.ensure(sizeof(uint32_t) * Pc));
+    GB_CUDA(ctx->vals_tmp.ensure(sizeof(int32_t) * Pc));
+    GB_CUDA(ctx->sort_temp.ensure(gb::sort_temp_bytes(Pc)));
+    // K2c duplicate in depth order, K2d stable sort on the tile id, K2e ranges
     {
         ProfScope ps(ctx, GB_K_DUPLICATE);
-        GB_CUDA(gb::launch_scatter(K, b->tiles_x, n_tiles, b->counts.as<uint32_t>(), b->rects.as<uint2>(),
-                                   b->depth.as<uint32_t>(), b->tile_off.as<uint32_t>(), ctx->tile_hist.as<uint32_t>(),
-                                   b->keys64.as<uint64_t>(), (uint32_t)P, stream));
+        GB_CUDA(gb::launch_duplicate(K, b->tiles_x, b->perm.as<int32_t>(), b->offsets.as<uint32_t>(),
+                                     b->rects.as<uint2>(), ctx->keys_tmp.as<uint32_t>(), ctx->vals_tmp.as<int32_t>(),
+                                     (uint32_t)P, b->overflow, stream));
+        if (b->capacity > 0)
+            GB_CUDA(gb::launch_pad((uint32_t)P, b->offsets.as<uint32_t>() + K, n_tiles, ctx->keys_tmp.as<uint32_t>(),
+                                   ctx->vals_tmp.as<int32_t>(), stream));
     }
     {
         ProfScope ps(ctx, GB_K_SORT);
-        GB_CUDA(gb::launch_tile_lists(n_tiles, b->tile_off.as<uint32_t>(), (uint32_t)P, b->keys64.as<uint64_t>(),
-                                      ctx->keys64_tmp.as<uint64_t>(), b->values.as<int32_t>(), b->ranges.as<uint2>(),
-                                      b->capacity > 0 ? b->overflow : nullptr, stream));
+        GB_CUDA(gb::launch_tile_sort(ctx->sort_temp.p, ctx->sort_temp.cap, ctx->keys_tmp.as<uint32_t>(),
+                                     b->keys.as<uint32_t>(), ctx->vals_tmp.as<int32_t>(), b->values.as<int32_t>(), P,
+                                     n_keys, stream));
     }
-    ctx->launches += (K > 0 && n_tiles > 0) + (n_tiles > 0);
+    {
+        ProfScope ps(ctx, GB_K_RANGES);
+        GB_CUDA(gb::launch_ranges(P, b->keys.as<uint32_t>(), b->ranges.as<uint2>(), n_tiles, stream));
+    }
+    ctx->launches += (K > 0) + (b->capacity > 0) + (P > 0 ? 1 + gb::sort_launches(gb::tile_sort_bits(n_keys)) : 0);
     b->built = true;
     return GB_OK;
 }
@@ -760,7 +853,7 @@ gb_status gb_build_binning(gb_context* ctx, const gb_splats* s, const gb_camera*
 namespace {
 // the device word holding the build's pair count P
 const uint32_t* total_ptr(const gb_binning* b) {
-    return b->tile_off.as<uint32_t>() + (size_t)b->tiles_x * b->tiles_y;
+    return b->radix ? b->offsets.as<uint32_t>() + b->K : b->tile_off.as<uint32_t>() + (size_t)b->tiles_x * b->tiles_y;
 }
 
 // capacity mode: read the pair count back (synchronous); clamps to the capacity on overflow

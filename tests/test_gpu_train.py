@@ -173,7 +173,10 @@ def test_capacity_binning_matches_blocking():
     ref_csr = ref.csr()
     ref_img = gb.render_forward(splats, cam, ref).color.clone()
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
-    for cap in (P, P + 1, P + 70_000):
+    tx, ty = ref.tiles_x, ref.tiles_y
+    # the last capacity exceeds 512 slots per tile: the capacity build takes the radix path (deep scenes)
+    # while the blocking reference took the tile-bucket path -- the two K2 builds must agree bit for bit
+    for cap in (P, P + 1, P + 70_000, P + 600 * tx * ty):
         b = gb.TileBinning()
         b.set_capacity(cap, flag)
         gb.build_binning(splats, cam, out=b)
@@ -190,6 +193,43 @@ def test_capacity_binning_matches_blocking():
     assert int(flag) == 1 and small.total == P // 3
     off, val = small.csr()  # the first P/3 pairs in (depth, index) order, still tile-sorted
     assert off[-1] == P // 3 and np.all(np.diff(off) >= 0)
+
+
+def test_deep_scene_radix_binning():
+    """More than 512 pairs per tile on average: the build takes the two stable radix sorts (blocking and
+    capacity mode alike) -- the lists match the oracle's, capacity mode reproduces them, an undersized
+    capacity raises the overflow flag."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+    from parity import O, run_oracle
+
+    K, n, W, H = 30_000, 4, 96, 64
+    arrays = _pinhole_scene(K, n, 11)
+    spec = sc.look_at((0.0, 0.0, -4.0), (0.0, 0.0, 0.0), W, H, 120.0, 120.0, W / 2, H / 2)
+    splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    cam = gb.PinholeCamera.from_spec(spec)
+    ref = gb.build_binning(splats, cam)
+    P, tiles = ref.total, ref.tiles_x * ref.tiles_y
+    assert P > 512 * tiles, (P, tiles)  # a deep scene
+    off, val = ref.csr()
+    orc = run_oracle(arrays, n, O.Cam.from_spec(spec), O.Cfg(), None)
+    np.testing.assert_array_equal(off, orc["offsets"])
+    np.testing.assert_array_equal(val, orc["values"])
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for cap in (P, P + 4096):
+        b = gb.TileBinning()
+        b.set_capacity(cap, flag)
+        gb.build_binning(splats, cam, out=b)
+        assert int(flag) == 0 and b.total == P
+        o2, v2 = b.csr()
+        np.testing.assert_array_equal(o2, off)
+        np.testing.assert_array_equal(v2, val)
+    small = gb.TileBinning()
+    small.set_capacity(max(513 * tiles, P - 1000), flag)
+    gb.build_binning(splats, cam, out=small)
+    assert int(flag) == 1
 
 
 def _trainer_scene():
