@@ -93,6 +93,10 @@ __global__ void __launch_bounds__(256) k_scatter(int64_t K, int tiles_x, const u
 constexpr int kBinCtas = GB_BIN_CTAS;
 constexpr int kBinThreads = GB_BIN_THREADS;  // half an SM: co-resident with the compositors of other view lanes
 constexpr int kSmemTiles = 12288;  // 48 KB of per-CTA tile counters
+#ifndef GB_BIN_BATCH
+#define GB_BIN_BATCH 4
+#endif
+constexpr int kBinBatch = GB_BIN_BATCH;
 
 __device__ __forceinline__ void cta_range(int64_t K, int64_t& k0, int64_t& k1) {
     const int64_t chunk = (K + kBinCtas - 1) / kBinCtas;
@@ -109,12 +113,23 @@ __global__ void __launch_bounds__(kBinThreads) k_tile_count(int64_t K, int tiles
     __syncthreads();
     int64_t k0, k1;
     cta_range(K, k0, k1);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += kBinThreads) {
-        if (counts[k] == 0) continue;
-        const uint2 r = rects[k];
-        const int tx0 = r.x & 0xffff, ty0 = r.x >> 16, tx1 = r.y & 0xffff, ty1 = r.y >> 16;
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&sh[ty * tiles_x + tx], 1u);
+    // kBinBatch primitives per thread per round: their loads issue together (the pass is latency-bound)
+    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += (int64_t)kBinBatch * kBinThreads) {
+        uint32_t c[kBinBatch];
+        uint2 r[kBinBatch];
+#pragma unroll
+        for (int j = 0; j < kBinBatch; ++j) {
+            const int64_t k = kb + (int64_t)j * kBinThreads;
+            c[j] = k < k1 ? counts[k] : 0u;
+            r[j] = k < k1 ? rects[k] : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < kBinBatch; ++j) {
+            if (c[j] == 0) continue;
+            const int tx0 = r[j].x & 0xffff, ty0 = r[j].x >> 16, tx1 = r[j].y & 0xffff, ty1 = r[j].y >> 16;
+            for (int ty = ty0; ty <= ty1; ++ty)
+                for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&sh[ty * tiles_x + tx], 1u);
+        }
     }
     __syncthreads();
     uint32_t* row = mat + (size_t)blockIdx.x * n_tiles;
@@ -156,16 +171,28 @@ __global__ void __launch_bounds__(kBinThreads) k_scatter_priv(int64_t K, int til
     __syncthreads();
     int64_t k0, k1;
     cta_range(K, k0, k1);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += kBinThreads) {
-        if (counts[k] == 0) continue;
-        const uint2 r = rects[k];
-        const uint64_t key = ((uint64_t)depth_bits[k] << 32) | (uint32_t)k;
-        const int tx0 = r.x & 0xffff, ty0 = r.x >> 16, tx1 = r.y & 0xffff, ty1 = r.y >> 16;
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx) {
-                const uint32_t pos = atomicAdd(&cur[ty * tiles_x + tx], 1u);
-                if (pos < cap) keys[pos] = key;
-            }
+    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += (int64_t)kBinBatch * kBinThreads) {
+        uint32_t c[kBinBatch], d[kBinBatch];
+        uint2 r[kBinBatch];
+#pragma unroll
+        for (int j = 0; j < kBinBatch; ++j) {
+            const int64_t k = kb + (int64_t)j * kBinThreads;
+            c[j] = k < k1 ? counts[k] : 0u;
+            r[j] = k < k1 ? rects[k] : make_uint2(0u, 0u);
+            d[j] = k < k1 ? depth_bits[k] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kBinBatch; ++j) {
+            if (c[j] == 0) continue;
+            const int64_t k = kb + (int64_t)j * kBinThreads;
+            const uint64_t key = ((uint64_t)d[j] << 32) | (uint32_t)k;
+            const int tx0 = r[j].x & 0xffff, ty0 = r[j].x >> 16, tx1 = r[j].y & 0xffff, ty1 = r[j].y >> 16;
+            for (int ty = ty0; ty <= ty1; ++ty)
+                for (int tx = tx0; tx <= tx1; ++tx) {
+                    const uint32_t pos = atomicAdd(&cur[ty * tiles_x + tx], 1u);
+                    if (pos < cap) keys[pos] = key;
+                }
+        }
     }
 }
 
