@@ -216,3 +216,45 @@ def test_pinhole_few_huge_splats():
     spec = sc.look_at((0.0, 0.0, -2.0), (0.0, 0.0, 0.0), 96, 80, 90.0, 90.0, 48.0, 40.0)
     arrays = sc.generate(O.MODE_PINHOLE, 12, 8, 19, mean_lo=-0.3, mean_hi=0.3, scale_lo=0.5, scale_hi=2.0)
     _check("pinhole_huge", arrays, O.MODE_PINHOLE, 8, O.Cam.from_spec(spec), O.Cfg())
+
+
+def test_binning_randomised_vs_oracle():
+    """K2 on 24 seeded scenes of mixed depth (buckets from empty to several thousand pairs, both the
+    tile-bucket and the radix build, tile sizes 1-16, ortho and pinhole): lists bit-exact with the oracle."""
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+
+    rng = np.random.default_rng(2024)
+    seen_deep = seen_shallow = 0
+    for i in range(24):
+        mode = O.MODE_ORTHO if i % 2 == 0 else O.MODE_PINHOLE
+        W, H = int(rng.integers(16, 200)), int(rng.integers(16, 160))
+        ts = int(rng.choice([1, 4, 8, 16]))
+        K = int(rng.integers(0, 20_000))
+        n = int(rng.choice([1, 2, 4]))
+        if i == 0:  # one deep scene for certain: 4 tiles, 20k ortho surfels
+            W, H, ts, K = 32, 32, 16, 20_000
+        if mode == O.MODE_ORTHO:
+            arrays = sc.generate(mode, K, n, 100 + i, width=W, height=H, scale_lo=0.5, scale_hi=float(rng.uniform(1, 12)))
+            cam = O.Cam(O.MODE_ORTHO, W, H, (0.0, 0.0, 0.0))
+            camera = gb.ImagePlaneCamera(W, H, (0.0, 0.0, 0.0))
+        else:
+            arrays = sc.generate(mode, K, n, 100 + i, mean_lo=-1.0, mean_hi=1.0, scale_lo=0.005,
+                                 scale_hi=float(rng.uniform(0.02, 0.2)))
+            f = float(rng.uniform(0.5, 2.0)) * max(W, H)
+            spec = sc.look_at((0.0, 0.0, -4.0), (0.0, 0.0, 0.0), W, H, f, f, W / 2, H / 2)
+            cam = O.Cam.from_spec(spec)
+            camera = gb.PinholeCamera.from_spec(spec)
+        cfg = O.Cfg(tile_size=ts)
+        off, val, _ = O.build_binning(O.Scene64(arrays, n, 0.5), cam, cfg)
+        splats = gb.SplatSet.from_numpy(mode, gb.ColorGridConfig(n), **arrays)
+        b = gb.build_binning(splats, camera, gb.RasterConfig(ts, cfg.cutoff_radius, cfg.alpha_skip, cfg.early_stop, 1))
+        goff, gval = b.csr()
+        np.testing.assert_array_equal(goff, off, err_msg=f"scene {i}")
+        np.testing.assert_array_equal(gval, val, err_msg=f"scene {i}")
+        tiles = len(off) - 1
+        if len(val) > 512 * tiles:
+            seen_deep += 1
+        else:
+            seen_shallow += 1
+    assert seen_deep and seen_shallow, (seen_deep, seen_shallow)
