@@ -342,7 +342,8 @@ def run_ours(args):
                                  overlap_adam=os.environ.get("GB_OVERLAP_ADAM", "1") == "1",
                                  capacity_margin=float(os.environ.get("GB_CAP_MARGIN", "1.1")),
                                  fused=os.environ.get("GB_FUSED") == "1",
-                                 texel_pad=os.environ.get("GB_TEXEL_PAD", "1") == "1")
+                                 texel_pad=os.environ.get("GB_TEXEL_PAD", "1") == "1",
+                                 rgba_texels=os.environ.get("GB_RGBA_TEXELS", "1") == "1")
     trainer.graph_host = os.environ.get("GB_GRAPH_HOST", "0") == "1"
     if os.environ.get("GB_PRE_ADAM_READ") == "1":
         trainer.overlap_read = False

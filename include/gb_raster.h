@@ -262,6 +262,15 @@ GB_API gb_status gb_render(gb_context *ctx, const gb_splats *s, const gb_camera 
  * vector red instead of an 8-byte and a 4-byte one.  A training loop accumulating many views keeps a
  * padded buffer and converts it once per step with gb_texel_grads_unpad. */
 GB_API gb_status gb_context_set_texel_grad_stride(gb_context *ctx, int32_t stride);
+/* Texel layout the compositors read (no reference counterpart).  rgba == NULL (the default): the splats'
+ * grid_values, K x n x n x 3 (core.hpp:44-48).  Otherwise an RGBA-padded copy of them, K x n x n x 4 floats,
+ * 16-B aligned (gb_texels_pad writes one): K3/K4 fetch a texel with one 16-byte load -- the same values, so
+ * the same results.  The caller keeps the copy in step with grid_values; the backwards then need texel
+ * gradient stride 4 (gb_context_set_texel_grad_stride).  A training loop pads once per step, after the
+ * optimizer's texel update. */
+GB_API gb_status gb_context_set_texel_rgba(gb_context *ctx, const float *rgba);
+/* dst[4t + c] = src[3t + c], dst[4t + 3] = 0 for t < texels (dst 16-B aligned). */
+GB_API gb_status gb_texels_pad(gb_context *ctx, const float *src, float *dst, int64_t texels);
 /* dst[3t + c] (+)= padded[4t + c] for t < texels, c < 3 (accumulate = 0: overwrite). */
 GB_API gb_status gb_texel_grads_unpad(gb_context *ctx, const float *padded, float *dst, int64_t texels,
                                       int32_t accumulate);

@@ -230,6 +230,8 @@ _SIGS = {
     "gb_event_destroy": (C.c_int, [P, P]),
     "gb_context_set_texel_grad_stride": (C.c_int, [P, C.c_int32]),
     "gb_texel_grads_unpad": (C.c_int, [P, P, P, C.c_int64, C.c_int32]),
+    "gb_context_set_texel_rgba": (C.c_int, [P, P]),
+    "gb_texels_pad": (C.c_int, [P, P, P, C.c_int64]),
     "gb_comm_unique_id": (C.c_int, [P]),
     "gb_comm_init_rank": (C.c_int, [P, C.c_int32, P, C.c_int32, C.POINTER(P)]),
     "gb_comm_init_all": (C.c_int, [P, C.c_int32, P]),

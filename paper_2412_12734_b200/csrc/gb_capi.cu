@@ -57,6 +57,7 @@ cudaError_t launch_add_f64(const double* src, float* dst, int64_t n, cudaStream_
 cudaError_t launch_adam_flag_init(int64_t* flag, const int32_t* veto, cudaStream_t st);
 cudaError_t launch_texel_unpad(const float* padded, float* dst, int64_t texels, bool accumulate, int sm_count,
                                cudaStream_t st);
+cudaError_t launch_texel_pad(const float* src, float* dst, int64_t texels, int sm_count, cudaStream_t st);
 cudaError_t launch_loss(int kind, const float* color, const float* target, int64_t n, float scale, float* grad,
                         float* loss, int sm_count, cudaStream_t st);
 cudaError_t launch_adam_check(const float* g, int64_t n, int group, unsigned long long* bad, int sm_count,
@@ -142,6 +143,7 @@ struct gb_context {
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     int texel_grad_stride = 3;  // gb_context_set_texel_grad_stride
+    const float* tex_rgba = nullptr;  // gb_context_set_texel_rgba
     DevBuf grid64;  // parity build: fp64 texel-gradient scratch (added into the caller's fp32 buffer after K4)
     DevBuf tile_hist, keys64_tmp;  // binning scratch (per-tile counts and CTA bases, bucket merge passes)
     DevBuf sort_temp, keys_tmp, vals_tmp, depth_tmp, iota_tmp;  // radix build scratch
@@ -331,8 +333,10 @@ gb::RasterConst make_raster_const(const gb_context* ctx, const gb_binning* b, in
 #ifdef GB_PARITY_F64
     rc.trans64 = b->trans64.as<double>();
     rc.tgs = 3;  // the parity build's fp64 texel scratch keeps the reference layout
+    rc.tex4 = nullptr;
 #else
     rc.tgs = ctx->texel_grad_stride;
+    rc.tex4 = reinterpret_cast<const float4*>(ctx->tex_rgba);
 #endif
 #ifdef GB_DEBUG_CHECKS
     rc.dbg_K = b->K;
@@ -969,6 +973,8 @@ gb_status gb_render_backward(gb_context* ctx, const gb_splats* s, const gb_camer
     if (!image_grad) return fail(GB_MISMATCH, "render_backward: image_grad size mismatch");
     if (s->count == 0) return GB_OK;
     if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_backward", ctx->texel_grad_stride)) return st;
+    if (ctx->tex_rgba && ctx->texel_grad_stride != 4)
+        return fail(GB_INVALID_ARGUMENT, "render_backward: RGBA texels need texel gradient stride 4");
     if (gb_status st = set_device(ctx)) return st;
     cudaStream_t stream = ctx->stream;
     const int64_t K = s->count;
@@ -1049,6 +1055,8 @@ gb_status gb_render_loss_backward(gb_context* ctx, const gb_splats* s, const gb_
     }
     if (s->count > 0)
         if (gb_status st = validate_grads(g, cam->mode, s->grid.n, "render_loss_backward", ctx->texel_grad_stride)) return st;
+    if (ctx->tex_rgba && ctx->texel_grad_stride != 4)
+        return fail(GB_INVALID_ARGUMENT, "render_loss_backward: RGBA texels need texel gradient stride 4");
     if (gb_status st = set_device(ctx)) return st;
     const int64_t npix = (int64_t)cam->width * cam->height;
     cudaStream_t stream = ctx->stream;
@@ -1244,6 +1252,24 @@ gb_status gb_context_set_texel_grad_stride(gb_context* ctx, int32_t stride) {
     if (!ctx) return fail(GB_INVALID_ARGUMENT, "null context");
     if (stride != 3 && stride != 4) return fail(GB_INVALID_ARGUMENT, "texel gradient stride must be 3 or 4");
     ctx->texel_grad_stride = stride;
+    return GB_OK;
+}
+
+gb_status gb_context_set_texel_rgba(gb_context* ctx, const float* rgba) {
+    if (!ctx) return fail(GB_INVALID_ARGUMENT, "null context");
+    if (reinterpret_cast<uintptr_t>(rgba) & 15) return fail(GB_INVALID_ARGUMENT, "RGBA texels must be 16-byte aligned");
+    ctx->tex_rgba = rgba;
+    return GB_OK;
+}
+
+gb_status gb_texels_pad(gb_context* ctx, const float* src, float* dst, int64_t texels) {
+    if (!ctx || (texels > 0 && (!src || !dst))) return fail(GB_INVALID_ARGUMENT, "null argument");
+    if (texels < 0) return fail(GB_INVALID_ARGUMENT, "texel count must be >= 0");
+    if (reinterpret_cast<uintptr_t>(dst) & 15) return fail(GB_INVALID_ARGUMENT, "RGBA texels must be 16-byte aligned");
+    if (gb_status st = set_device(ctx)) return st;
+    ProfScope ps(ctx, GB_K_ADAM);
+    GB_CUDA(gb::launch_texel_pad(src, dst, texels, ctx->sm_count, ctx->stream));
+    ctx->launches += texels > 0;
     return GB_OK;
 }
 

@@ -127,6 +127,7 @@ struct RasterConst {
     real tex_offset;      // (n-1)/2
     real sigma;
     int tgs;  // K4 texel-gradient stride: 3 = the reference layout, 4 = RGBA-padded (one 16-B red per texel)
+    const float4* tex4;  // non-null: K3/K4 read the texels from this RGBA-padded copy (gb_context_set_texel_rgba)
 #ifdef GB_DEBUG_CHECKS
     int64_t dbg_K;  // primitives: every list entry must be in [0, K)
 #endif

@@ -140,6 +140,20 @@ cudaError_t launch_texel_unpad(const float* padded, float* dst, int64_t texels, 
     return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) k_texel_pad(const float* __restrict__ src, float4* __restrict__ dst,
+                                                   int64_t texels) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < texels; t += (int64_t)gridDim.x * blockDim.x)
+        dst[t] = make_float4(src[3 * t], src[3 * t + 1], src[3 * t + 2], 0.0f);
+}
+
+cudaError_t launch_texel_pad(const float* src, float* dst, int64_t texels, int sm_count, cudaStream_t st) {
+    if (texels <= 0) return cudaSuccess;
+    int64_t blocks = (texels + 255) / 256;
+    if (blocks > (int64_t)sm_count * 16) blocks = (int64_t)sm_count * 16;
+    k_texel_pad<<<(unsigned)blocks, 256, 0, st>>>(src, reinterpret_cast<float4*>(dst), texels);
+    return cudaGetLastError();
+}
+
 __global__ void k_adam_flag_init(long long* __restrict__ flag, const int* __restrict__ veto) {
     *flag = (veto && *veto) ? GB_ADAM_FLAG_VETO : GB_ADAM_FLAG_CLEAR;
 }

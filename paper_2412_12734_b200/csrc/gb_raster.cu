@@ -84,10 +84,35 @@ __device__ __forceinline__ int cell_texel(int k, int N) {
     return k;                                                              // kCellV: (i_u', i_v), (i_u', i_v + 1)
 }
 
+// An entry's texels (core.hpp:44-48, texel index i_u * n + i_v): TL = 3 reads the reference layout (three
+// scalar loads per texel), TL = 4 an RGBA-padded copy (one 16-B load per texel, every texel row in whole
+// 16-B words; gb_context_set_texel_rgba) -- the same values either way.
+template <int TL>
+struct TexelRef;
+template <>
+struct TexelRef<3> {
+    const float* t;
+    __device__ __forceinline__ TexelRef(const float* tex, const float4*, int id, int NN)
+        : t(tex + (size_t)id * (3 * NN)) {}
+    __device__ __forceinline__ float3 operator[](int i) const {
+        return make_float3(__ldg(t + 3 * i), __ldg(t + 3 * i + 1), __ldg(t + 3 * i + 2));
+    }
+};
+template <>
+struct TexelRef<4> {
+    const float4* t;
+    __device__ __forceinline__ TexelRef(const float*, const float4* tex4, int id, int NN) : t(tex4 + (size_t)id * NN) {}
+    __device__ __forceinline__ float3 operator[](int i) const {
+        const float4 q = __ldg(t + i);
+        return make_float3(q.x, q.y, q.z);
+    }
+};
+__device__ __forceinline__ float ch(const float3& q, int c) { return c == 0 ? q.x : (c == 1 ? q.y : q.z); }
+
 // One backward entry for the calling warp, after the evaluation: rewind the pixel's state, form the
 // adjoints and reduce/scatter the gradients (raster.hpp:324-363).
-template <int MODE, int NT, int CELL, int S>
-__device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, bool on, unsigned act, real u,
+template <int MODE, int NT, int CELL, int S, int TL>
+__device__ __forceinline__ void bwd_shade(const TexelRef<TL>& tx, int id, bool on, unsigned act, real u,
                                           real v, real G, real alpha, real araw, const PinholeTerms& pt,
                                           real& T, real g0, real g1, real g2, real& bh0, real& bh1,
                                           real& bh2, const RasterConst& rc, int N, int lane, real* wscratch,
@@ -120,12 +145,12 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         if (CELL == kCellFull) {
             Bilin b;
             bilin_setup(u, v, N, rc, b);
-            const float* p00 = t + b.o00;
-            const float* p10 = p00 + 3 * N;
+            const float3 z = make_float3(0.f, 0.f, 0.f);
+            const float3 q00 = on ? tx[b.t00] : z, q10 = on ? tx[b.t00 + N] : z, q01 = on ? tx[b.t00 + 1] : z,
+                         q11 = on ? tx[b.t00 + N + 1] : z;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const real c00 = on ? p00[c] : 0.f, c10 = on ? p10[c] : 0.f, c01 = on ? p00[3 + c] : 0.f,
-                           c11 = on ? p10[3 + c] : 0.f;
+                const real c00 = ch(q00, c), c10 = ch(q10, c), c01 = ch(q01, c), c11 = ch(q11, c);
                 cc_[c] = c00 * b.w00 + c10 * b.w10 + c01 * b.w01 + c11 * b.w11;
                 tg[c] = chat[c] * b.w00;
                 tg[3 + c] = chat[c] * b.w10;
@@ -152,12 +177,12 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
             const real gf = (real)1 - f;
             const int other = (CELL == kCellU ? v : u) > (real)0 ? N - 1 : 0;
             tt = CELL == kCellU ? i0 * N + other : other * N + i0;
-            const float* pa = t + 3 * tt;
-            const float* pb = pa + (CELL == kCellU ? 3 * N : 3);
+            const float3 z = make_float3(0.f, 0.f, 0.f);
+            const float3 qa = on ? tx[tt] : z, qb = on ? tx[tt + (CELL == kCellU ? N : 1)] : z;
             real fh = (real)0;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const real ca = on ? pa[c] : 0.f, cb = on ? pb[c] : 0.f;
+                const real ca = ch(qa, c), cb = ch(qb, c);
                 cc_[c] = fma_rn(cb, f, ca * gf);  // = the four-corner blend with two zero weights
                 tg[c] = chat[c] * gf;
                 tg[3 + c] = chat[c] * f;
@@ -172,9 +197,10 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
         } else {  // kCellOne (and n = 1): a single texel with weight 1
             const int iu = N > 1 && u > (real)0 ? N - 1 : 0, iv = N > 1 && v > (real)0 ? N - 1 : 0;
             tt = iu * N + iv;
+            const float3 q = on ? tx[tt] : make_float3(0.f, 0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                cc_[c] = on ? t[3 * tt + c] : 0.f;
+                cc_[c] = ch(q, c);
                 tg[c] = chat[c];
             }
             wk[0] = (real)1;
@@ -294,8 +320,8 @@ __device__ __forceinline__ void bwd_shade(const float* __restrict__ t, int id, b
 
 // One backward entry for the calling warp: evaluate, pick the warp's texel footprint class, then
 // bwd_shade (raster.hpp:324-363).
-template <int MODE, int NT, int S>
-__device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __restrict__ t, int id, int rank,
+template <int MODE, int NT, int S, int TL = 3>
+__device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __restrict__ tex, int id, int rank,
                                           int last, int x, int y, real& T, real g0, real g1, real g2,
                                           real& bh0, real& bh1, real& bh2, const RasterConst& rc, int N,
                                           int lane, real* wscratch, real* __restrict__ accum,
@@ -322,9 +348,10 @@ __device__ __forceinline__ void bwd_entry(const ScreenHeader& h, const float* __
         GB_DBG(6, (act & 0x0F0F0F0Fu) && (act & 0xF0F0F0F0u));  // both 4x4 halves active
         GB_DBG(7, (act & 0x0000FFFFu) && (act & 0xFFFF0000u));  // both 8x2 halves active
     }
-#define GB_SHADE(CELL)                                                                                          \
-    bwd_shade<MODE, NT, CELL, S>(t, id, on, act, u, v, G, alpha, araw, pt, T, g0, g1, g2, bh0, bh1, bh2, rc, N, \
-                              lane, wscratch, accum, grid_grad)
+    const TexelRef<TL> tx(tex, rc.tex4, id, N * N);
+#define GB_SHADE(CELL)                                                                                              \
+    bwd_shade<MODE, NT, CELL, S, TL>(tx, id, on, act, u, v, G, alpha, araw, pt, T, g0, g1, g2, bh0, bh1, bh2, rc, N, \
+                                     lane, wscratch, accum, grid_grad)
     if (N == 1) {
         GB_SHADE(kCellOne);
         return;
@@ -396,11 +423,10 @@ __device__ __forceinline__ WarpPixel live_rect(const WarpPixel& wp, bool live) {
 
 // One forward entry for the calling warp (raster.hpp:238-250): evaluate, pick the warp's texel footprint
 // class (see bwd_shade), composite into the lanes that are not done.
-template <int MODE, int NT>
+template <int MODE, int NT, int TL = 3>
 __device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __restrict__ tex, int id, int rank, int x,
                                           int y, const RasterConst& rc, int N, real early, bool& done, real& T,
                                           real& acc0, real& acc1, real& acc2, int& last) {
-    const int F = 3 * N * N;
     real u, v;
     bool hit;
     if (MODE == GB_MODE_ORTHO) {
@@ -417,47 +443,44 @@ __device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __
     const bool au = N > 1 && __any_sync(kFull, comp && u > -sigma && u < sigma);
     const bool av = N > 1 && __any_sync(kFull, comp && v > -sigma && v < sigma);
     if (comp) {
-        const float* t = tex + (size_t)id * F;
+        const TexelRef<TL> tx(tex, rc.tex4, id, N * N);
         real c0_, c1_, c2_;
         if (au && av) {
             Bilin b;
             bilin_setup(u, v, N, rc, b);
-            const float* p00 = t + b.o00;
-            const float* p10 = p00 + 3 * N;
-            c0_ = __ldg(p00) * b.w00 + __ldg(p10) * b.w10 + __ldg(p00 + 3) * b.w01 + __ldg(p10 + 3) * b.w11;
-            c1_ = __ldg(p00 + 1) * b.w00 + __ldg(p10 + 1) * b.w10 + __ldg(p00 + 4) * b.w01 +
-                  __ldg(p10 + 4) * b.w11;
-            c2_ = __ldg(p00 + 2) * b.w00 + __ldg(p10 + 2) * b.w10 + __ldg(p00 + 5) * b.w01 +
-                  __ldg(p10 + 5) * b.w11;
+            const float3 q00 = tx[b.t00], q10 = tx[b.t00 + N], q01 = tx[b.t00 + 1], q11 = tx[b.t00 + N + 1];
+            c0_ = q00.x * b.w00 + q10.x * b.w10 + q01.x * b.w01 + q11.x * b.w11;
+            c1_ = q00.y * b.w00 + q10.y * b.w10 + q01.y * b.w01 + q11.y * b.w11;
+            c2_ = q00.z * b.w00 + q10.z * b.w10 + q01.z * b.w01 + q11.z * b.w11;
         } else if (au || av) {  // the four-corner blend with two zero weights
             // (separate uniform branches: each keeps its index arithmetic free of selects)
-            const float* pa;
-            const float* pb;
+            int ta, tb;
             real f;
             if (au) {
                 real sx = fma_rn(u, rc.tex_scale, rc.tex_offset);
                 sx = rmin(rmax(sx, (real)0), (real)(N - 1));
                 const int i0 = min((int)rfloor(sx), N - 2);
                 f = sub_rn(sx, (real)i0);
-                pa = t + (i0 * N + (v > (real)0 ? N - 1 : 0)) * 3;
-                pb = pa + 3 * N;
+                ta = i0 * N + (v > (real)0 ? N - 1 : 0);
+                tb = ta + N;
             } else {
                 real sx = fma_rn(v, rc.tex_scale, rc.tex_offset);
                 sx = rmin(rmax(sx, (real)0), (real)(N - 1));
                 const int i0 = min((int)rfloor(sx), N - 2);
                 f = sub_rn(sx, (real)i0);
-                pa = t + ((u > (real)0 ? N - 1 : 0) * N + i0) * 3;
-                pb = pa + 3;
+                ta = (u > (real)0 ? N - 1 : 0) * N + i0;
+                tb = ta + 1;
             }
             const real gf = (real)1 - f;
-            c0_ = fma_rn(__ldg(pb), f, __ldg(pa) * gf);
-            c1_ = fma_rn(__ldg(pb + 1), f, __ldg(pa + 1) * gf);
-            c2_ = fma_rn(__ldg(pb + 2), f, __ldg(pa + 2) * gf);
+            const float3 qa = tx[ta], qb = tx[tb];
+            c0_ = fma_rn(qb.x, f, qa.x * gf);
+            c1_ = fma_rn(qb.y, f, qa.y * gf);
+            c2_ = fma_rn(qb.z, f, qa.z * gf);
         } else {  // one texel (and n = 1)
-            const float* p = t + (N > 1 ? ((u > (real)0 ? N - 1 : 0) * N + (v > (real)0 ? N - 1 : 0)) * 3 : 0);
-            c0_ = __ldg(p);
-            c1_ = __ldg(p + 1);
-            c2_ = __ldg(p + 2);
+            const float3 q = tx[N > 1 ? (u > (real)0 ? N - 1 : 0) * N + (v > (real)0 ? N - 1 : 0) : 0];
+            c0_ = q.x;
+            c1_ = q.y;
+            c2_ = q.z;
         }
         const real w = alpha * T;  // raster.hpp:244-249
         acc0 = fma_rn(c0_, w, acc0);
@@ -502,7 +525,7 @@ __device__ __forceinline__ ScreenHeader staged_hdr(const WarpHeaders& wh, int j)
 }
 
 // render_forward's per-pixel loop (raster.hpp:237-250) for the calling warp's pixels
-template <int MODE, int NT>
+template <int MODE, int NT, int TL>
 __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __restrict__ values,
                                          const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                          const float* __restrict__ tex, const RasterConst& rc, int N,
@@ -542,14 +565,14 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             h.h2 = ld_real4(&hdr[id].h2);
 #endif
             // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not composite
-            fwd_entry<MODE, NT>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
+            fwd_entry<MODE, NT, TL>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
             if (__all_sync(kFull, done)) break;
         }
     }
 }
 
 // render_backward's per-pixel loop (raster.hpp:313-364) for the calling warp's pixels
-template <int MODE, int NT, int S>
+template <int MODE, int NT, int S, int TL>
 __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __restrict__ values,
                                          const ScreenHeader* __restrict__ hdr, const CullRec* __restrict__ cull,
                                          const float* __restrict__ tex, const CamConst& cc, const RasterConst& rc,
@@ -588,8 +611,8 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
             h.h1 = ld_real4(&hdr[id].h1);
             h.h2 = ld_real4(&hdr[id].h2);
 #endif
-            bwd_entry<MODE, NT, S>(h, tex + (size_t)id * F, id, c0 + bit, last, wp.x, wp.y, T, g0, g1, g2, bh0, bh1,
-                                bh2, rc, N, lane, wscratch, accum, grid_grad);
+            bwd_entry<MODE, NT, S, TL>(h, tex, id, c0 + bit, last, wp.x, wp.y, T, g0, g1, g2, bh0, bh1, bh2, rc, N,
+                                       lane, wscratch, accum, grid_grad);
         }
     }
 }
@@ -722,7 +745,7 @@ __device__ __forceinline__ void bwd_walk_staged(const uint2 range, const int32_t
                 const int bit = 31 - __clz(mask);
                 mask &= ~(1u << bit);
                 const int id = b.id[bit];
-                bwd_entry<MODE, NT, S>(staged_header(b, bit), tex + (size_t)id * 3 * N * N, id, c0 + bit, last, wp.x,
+                bwd_entry<MODE, NT, S>(staged_header(b, bit), tex, id, c0 + bit, last, wp.x,
                                     wp.y, T, g0, g1, g2, bh0, bh1, bh2, rc, N, lane, wscratch, accum, grid_grad);
             }
         }
@@ -738,7 +761,7 @@ __device__ __forceinline__ void bwd_walk_staged(const uint2 range, const int32_t
 #ifndef GB_K3_MINB
 #define GB_K3_MINB 8
 #endif
-template <int MODE, int NT>
+template <int MODE, int NT, int TL>
 __global__ void __launch_bounds__(256, GB_K3_MINB) k_forward_direct(const uint2* __restrict__ ranges,
                                                         const int32_t* __restrict__ values,
                                                         const ScreenHeader* __restrict__ hdr,
@@ -755,7 +778,7 @@ __global__ void __launch_bounds__(256, GB_K3_MINB) k_forward_direct(const uint2*
                               ring);
 #else
     __shared__ WarpHeaders whs[8];
-    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
+    fwd_walk<MODE, NT, TL>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
                        &whs[threadIdx.x >> 5]);
 #endif
     if (wp.inside) {  // raster.hpp:253-254
@@ -774,7 +797,7 @@ __global__ void __launch_bounds__(256, GB_K3_MINB) k_forward_direct(const uint2*
 // render_forward with the photometric loss (KIND 0 = L1, 1 = MSE; K6) in its epilogue: the pixel's
 // colour turns into the loss cotangent in registers, so the image is written only when asked for and
 // no separate loss pass runs.  T and the last rank are always written (the backward rewinds from them).
-template <int MODE, int NT, int KIND>
+template <int MODE, int NT, int KIND, int TL>
 __global__ void __launch_bounds__(256, GB_K3_MINB) k_forward_loss(const uint2* __restrict__ ranges,
                                                       const int32_t* __restrict__ values,
                                                       const ScreenHeader* __restrict__ hdr,
@@ -793,7 +816,7 @@ __global__ void __launch_bounds__(256, GB_K3_MINB) k_forward_loss(const uint2* _
                               ring);
 #else
     __shared__ WarpHeaders whs[8];
-    fwd_walk<MODE, NT>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
+    fwd_walk<MODE, NT, TL>(ranges[blockIdx.x], values, hdr, cull, tex, rc, tex_n<NT>(n_rt), wp, T, a0, a1, a2, last,
                        &whs[threadIdx.x >> 5]);
 #endif
     real l = (real)0;
@@ -831,7 +854,7 @@ __global__ void __launch_bounds__(256, GB_K3_MINB) k_forward_loss(const uint2* _
 #ifndef GB_K4_MINB
 #define GB_K4_MINB 4
 #endif
-template <int MODE, int NT, int S>
+template <int MODE, int NT, int S, int TL>
 __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2* __restrict__ ranges,
                                                          const int32_t* __restrict__ values,
                                                          const ScreenHeader* __restrict__ hdr,
@@ -864,7 +887,7 @@ __global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2
                               &s_top);
 #else
     __shared__ WarpHeaders whs[8];
-    bwd_walk<MODE, NT, S>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1,
+    bwd_walk<MODE, NT, S, TL>(ranges[blockIdx.x], values, hdr, cull, tex, cc, rc, tex_n<NT>(n_rt), wp, last, T, g0, g1,
                           g2, red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad,
                           &whs[threadIdx.x >> 5]);
 #endif
@@ -894,7 +917,7 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
     real T, a0, a1, a2;
     int last;
     __shared__ WarpHeaders whs[8];
-    fwd_walk<MODE, NT>(range, values, hdr, cull, tex, rc, N, wp, T, a0, a1, a2, last, &whs[threadIdx.x >> 5]);
+    fwd_walk<MODE, NT, 3>(range, values, hdr, cull, tex, rc, N, wp, T, a0, a1, a2, last, &whs[threadIdx.x >> 5]);
     real g0 = (real)0, g1 = (real)0, g2 = (real)0, l = (real)0;
     if (wp.inside) {
         const size_t p = (size_t)wp.y * cc.width + wp.x;
@@ -933,7 +956,7 @@ __global__ void __launch_bounds__(256) k_fused_direct(const uint2* __restrict__ 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(kFull, l, o);
     if ((threadIdx.x & 31) == 0 && loss && l != (real)0) atomicAdd(loss, (float)(l * scale));
-    bwd_walk<MODE, NT, 3>(range, values, hdr, cull, tex, cc, rc, N, wp, last, T, g0, g1, g2,
+    bwd_walk<MODE, NT, 3, 3>(range, values, hdr, cull, tex, cc, rc, N, wp, last, T, g0, g1, g2,
                        red_scratch + (threadIdx.x >> 5) * kRedRows * kRedStride, accum, grid_grad,
                        &whs[threadIdx.x >> 5]);
 }
@@ -959,7 +982,12 @@ template <int MODE, int NT>
 static cudaError_t fwdd_t(int tiles, int threads, cudaStream_t st, const uint2* ranges, const int32_t* values,
                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                           const RasterConst& rc, int n, float* color, float* trans, int32_t* last) {
-    k_forward_direct<MODE, NT><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, color, trans, last);
+    if (rc.tex4)  // RGBA-padded texels (gb_context_set_texel_rgba)
+        k_forward_direct<MODE, NT, 4><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, color, trans,
+                                                                 last);
+    else
+        k_forward_direct<MODE, NT, 3><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, color, trans,
+                                                                 last);
     return cudaGetLastError();
 }
 
@@ -968,22 +996,32 @@ static cudaError_t bwdd_t(int tiles, int threads, cudaStream_t st, const uint2* 
                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                           const RasterConst& rc, int n, const float* trans, const int32_t* last,
                           const float* image_grad, real* accum, real* grid_grad) {
-    // the fp64 parity build's scratch (static header slots + dynamic reduction rows) exceeds the 48 KB default
-    static const cudaError_t opt_in =
-        cudaFuncSetAttribute(k_backward_direct<MODE, NT, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)red_smem(256)) == cudaSuccess
-            ? cudaFuncSetAttribute(k_backward_direct<MODE, NT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)red_smem(256))
-            : cudaErrorInvalidValue;
+    // the fp64 parity build's scratch (static header slots + dynamic reduction rows) exceeds the 48 KB default;
+    // (texel-gradient stride, texel layout) in {(3, 3), (4, 3), (4, 4)}
+    static const cudaError_t opt_in = [] {
+        const int bytes = (int)red_smem(256);
+        cudaError_t e = cudaFuncSetAttribute(k_backward_direct<MODE, NT, 3, 3>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_backward_direct<MODE, NT, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_backward_direct<MODE, NT, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     bytes);
+        return e;
+    }();
     if (opt_in != cudaSuccess) return opt_in;
-    if (rc.tgs == 4)
-        k_backward_direct<MODE, NT, 4><<<tiles, threads, red_smem(threads), st>>>(ranges, values, hdr, cull, tex, cc,
-                                                                                  rc, n, trans, last, image_grad,
-                                                                                  accum, grid_grad);
+    if (rc.tex4 && rc.tgs != 4) return cudaErrorNotSupported;  // RGBA texels come with RGBA texel gradients
+    const size_t smem = red_smem(threads);
+    if (rc.tex4)
+        k_backward_direct<MODE, NT, 4, 4><<<tiles, threads, smem, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, trans,
+                                                                        last, image_grad, accum, grid_grad);
+    else if (rc.tgs == 4)
+        k_backward_direct<MODE, NT, 4, 3><<<tiles, threads, smem, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, trans,
+                                                                        last, image_grad, accum, grid_grad);
     else
-        k_backward_direct<MODE, NT, 3><<<tiles, threads, red_smem(threads), st>>>(ranges, values, hdr, cull, tex, cc,
-                                                                                  rc, n, trans, last, image_grad,
-                                                                                  accum, grid_grad);
+        k_backward_direct<MODE, NT, 3, 3><<<tiles, threads, smem, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, trans,
+                                                                        last, image_grad, accum, grid_grad);
     return cudaGetLastError();
 }
 
@@ -1021,12 +1059,21 @@ static cudaError_t fwdl_t(int tiles, int threads, cudaStream_t st, const uint2* 
                           const ScreenHeader* hdr, const CullRec* cull, const float* tex, const CamConst& cc,
                           const RasterConst& rc, int n, int kind, const float* target, float scale, float* color,
                           float* trans, int32_t* last, float* image_grad, float* loss) {
-    if (kind == 0)
-        k_forward_loss<MODE, NT, 0><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, target,
-                                                               scale, color, trans, last, image_grad, loss);
-    else
-        k_forward_loss<MODE, NT, 1><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, target,
-                                                               scale, color, trans, last, image_grad, loss);
+#define GB_FWDL(KIND_, TL_)                                                                                     \
+    k_forward_loss<MODE, NT, KIND_, TL_><<<tiles, threads, 0, st>>>(ranges, values, hdr, cull, tex, cc, rc, n, target, \
+                                                                    scale, color, trans, last, image_grad, loss)
+    if (kind == 0) {
+        if (rc.tex4)
+            GB_FWDL(0, 4);
+        else
+            GB_FWDL(0, 3);
+    } else {
+        if (rc.tex4)
+            GB_FWDL(1, 4);
+        else
+            GB_FWDL(1, 3);
+    }
+#undef GB_FWDL
     return cudaGetLastError();
 }
 

@@ -492,13 +492,43 @@ class RenderOutput:
         return 1.0 - self.final_transmittance
 
 
-def render_forward(splats: SplatSet, camera, binning: TileBinning, out: RenderOutput = None) -> RenderOutput:
-    """raster.hpp:201-261"""
+class _TexelRGBA:
+    """Within the block, the context's compositors read the texels from ``rgba`` (an RGBA-padded copy of the
+    splats' grid, gb_context_set_texel_rgba; see texels_pad) instead of the reference layout."""
+
+    def __init__(self, ctx, rgba, grid_numel):
+        self.ctx, self.rgba, self.grid_numel = ctx, rgba, grid_numel
+
+    def __enter__(self):
+        if self.rgba is not None:
+            if self.rgba.numel() * 3 != 4 * self.grid_numel or self.rgba.data_ptr() % 16:
+                raise ValueError("texels_rgba: padded buffer must hold K*n*n*4 floats, 16-byte aligned")
+            check(lib.gb_context_set_texel_rgba(self.ctx.handle, C.c_void_p(self.rgba.data_ptr())),
+                  "gb_context_set_texel_rgba")
+
+    def __exit__(self, *a):
+        if self.rgba is not None:
+            check(lib.gb_context_set_texel_rgba(self.ctx.handle, None), "gb_context_set_texel_rgba")
+
+
+def texels_pad(grid: torch.Tensor, rgba: torch.Tensor) -> None:
+    """rgba <- the RGBA-padded copy of a reference-layout texel grid (K*n*n*3 -> K*n*n*4 floats; gb_texels_pad),
+    on the current stream."""
+    if rgba.numel() * 3 != grid.numel() * 4:
+        raise ValueError("texels_pad: size mismatch")
+    check(lib.gb_texels_pad(context(grid.device).handle, _ptr(grid), _ptr(rgba), grid.numel() // 3), "gb_texels_pad")
+
+
+def render_forward(splats: SplatSet, camera, binning: TileBinning, out: RenderOutput = None,
+                   texels_rgba: torch.Tensor = None) -> RenderOutput:
+    """raster.hpp:201-261.  ``texels_rgba``: an RGBA-padded copy of the splats' texels (texels_pad) that K3
+    reads with one 16-byte load per texel -- the same image."""
     ctx = context(splats.device)
     out = out if out is not None else RenderOutput(camera.width, camera.height, splats.device)
     s, cam = splats.to_c(), camera.to_c()
-    check(lib.gb_render_forward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(out._c)),
-          "render_forward")
+    with _TexelRGBA(ctx, texels_rgba, splats.count * 3 * splats.grid_config.n ** 2):
+        check(lib.gb_render_forward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(out._c)),
+              "render_forward")
     return out
 
 
@@ -524,7 +554,7 @@ class _TexelStride:
 
 def render_backward(splats: SplatSet, camera, binning: TileBinning, output: RenderOutput,
                     image_grad: torch.Tensor, grads: GradientBuffer = None,
-                    texel_grad: torch.Tensor = None) -> GradientBuffer:
+                    texel_grad: torch.Tensor = None, texels_rgba: torch.Tensor = None) -> GradientBuffer:
     """raster.hpp:277-387.  Accumulates into ``grads`` (a fresh zeroed buffer by default).  ``texel_grad``: an
     RGBA-padded (K*n*n*4) buffer that receives the texel gradients instead of ``grads.grid`` (convert with
     texel_grads_unpad)."""
@@ -535,7 +565,7 @@ def render_backward(splats: SplatSet, camera, binning: TileBinning, output: Rend
         raise ValueError("render_backward: image_grad size mismatch")
     image_grad = image_grad.contiguous()
     s, cam, g = splats.to_c(), camera.to_c(), grads.to_c()
-    with _TexelStride(ctx, g, texel_grad, grads.grid.numel()) as g:
+    with _TexelStride(ctx, g, texel_grad, grads.grid.numel()) as g, _TexelRGBA(ctx, texels_rgba, grads.grid.numel()):
         check(lib.gb_render_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, C.byref(output._c),
                                      _ptr(image_grad), C.byref(g)), "render_backward")
     return grads
@@ -552,7 +582,7 @@ def texel_grads_unpad(padded: torch.Tensor, dst: torch.Tensor, accumulate: bool 
 def render_loss_backward(splats: SplatSet, camera, binning: TileBinning, target: torch.Tensor, loss: str = "l1",
                          scale: float = None, grads: GradientBuffer = None, loss_acc: torch.Tensor = None,
                          output: RenderOutput = None, image_grad: torch.Tensor = None,
-                         texel_grad: torch.Tensor = None):
+                         texel_grad: torch.Tensor = None, texels_rgba: torch.Tensor = None):
     """render_forward + l1_loss / mse_loss + render_backward of one view in one pass
     (train.hpp:120-133 around raster.hpp:201-387).  Returns (loss_acc, grads); ``loss_acc``
     (a device float, zero by default) and ``grads`` accumulate.  ``output`` / ``image_grad``,
@@ -573,7 +603,7 @@ def render_loss_backward(splats: SplatSet, camera, binning: TileBinning, target:
         raise ValueError("render_loss_backward: image_grad size mismatch")
     target = target.contiguous()
     s, cam, g = splats.to_c(), camera.to_c(), grads.to_c()
-    with _TexelStride(ctx, g, texel_grad, grads.grid.numel()) as g:
+    with _TexelStride(ctx, g, texel_grad, grads.grid.numel()) as g, _TexelRGBA(ctx, texels_rgba, grads.grid.numel()):
         check(lib.gb_render_loss_backward(ctx.handle, C.byref(s), C.byref(cam), binning.handle, _ptr(target),
                                           kinds[loss], scale, C.byref(output._c) if output is not None else None,
                                           _ptr(image_grad) if image_grad is not None else None, _ptr(loss_acc),

@@ -26,7 +26,8 @@ from ._lib import check, lib
 
 from .raster import (AdamConfig, AdamState, GradientBuffer, LearningRates, RasterConfig, RenderOutput, SplatSet,
                      StepGraph, TileBinning, adam_step, all_contexts, build_binning, context, l1_loss,
-                     copy_h2d, memset_, render_backward, render_forward, render_loss_backward, texel_grads_unpad)
+                     copy_h2d, memset_, render_backward, render_forward, render_loss_backward, texel_grads_unpad,
+                     texels_pad)
 
 
 def shard_views(n_views: int, rank: int, world: int, per_rank: Optional[int] = None) -> List[int]:
@@ -261,7 +262,7 @@ class ViewShardedTrainer:
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
                  lanes: int = 4, fused: bool = False, async_binning: bool = True, graph: bool = False,
                  capacity_margin: float = 1.1, sharded_adam: bool = True, overlap_adam: bool = True,
-                 texel_pad: bool = True):
+                 texel_pad: bool = True, rgba_texels: bool = True):
         self.splats = splats
         self.cameras = list(cameras)
         self.views = list(views)
@@ -296,6 +297,10 @@ class ViewShardedTrainer:
         # the flat buffer's reference-layout grid group once per step (gb_texel_grads_unpad)
         self._tex_pad = (torch.zeros(self.grads.grid.numel() // 3 * 4, dtype=torch.float32, device=dev)
                          if texel_pad else None)
+        # ... and the compositors read the texels from an RGBA-padded copy (one 16-B load per texel), refreshed
+        # once per step after the texel update (gb_texels_pad; rgba_texels needs texel_pad)
+        self._tex_rgba = (torch.zeros(self.grads.grid.numel() // 3 * 4, dtype=torch.float32, device=dev)
+                          if texel_pad and rgba_texels else None)
         # lane 0 is the caller's stream, except under graph capture (which needs a side stream)
         main = torch.cuda.Stream(device=dev) if graph else torch.cuda.current_stream(dev)
         self._lanes = [_Lane(dev, main if i == 0 else torch.cuda.Stream(device=dev)) for i in range(max(1, lanes))]
@@ -353,17 +358,18 @@ class ViewShardedTrainer:
             self._waited.add(id(lane))
             lane.stream.wait_event(self._grid_ready)
         if not self.fused:
-            render_forward(self.splats, cam, lane.binning, out)
+            render_forward(self.splats, cam, lane.binning, out, texels_rgba=self._tex_rgba)
         return cam, out, gimg
 
     def _view_backward(self, i: int, cam, out, gimg, target: torch.Tensor) -> None:
         lane = self._lane(i)
         if self.fused:
             render_loss_backward(self.splats, cam, lane.binning, target, "l1", grads=self.grads,
-                                 loss_acc=self.losses[i:i + 1], texel_grad=self._tex_pad)
+                                 loss_acc=self.losses[i:i + 1], texel_grad=self._tex_pad, texels_rgba=self._tex_rgba)
             return
         l1_loss(out.color, target.view(cam.height, cam.width, 3), grad=gimg, loss=self.losses[i:i + 1])
-        render_backward(self.splats, cam, lane.binning, out, gimg, self.grads, texel_grad=self._tex_pad)
+        render_backward(self.splats, cam, lane.binning, out, gimg, self.grads, texel_grad=self._tex_pad,
+                        texels_rgba=self._tex_rgba)
 
     def wait_adam(self) -> None:
         """Order the current stream after the step's texel update (overlap_adam)."""
@@ -380,6 +386,8 @@ class ViewShardedTrainer:
         if self._tex_pad is not None:
             memset_(self._tex_pad)
         memset_(self.losses)
+        if self._tex_rgba is not None and not self.overlap_adam:
+            texels_pad(self.splats.grid.view(-1), self._tex_rgba)  # (the last step's Adam ran on this stream)
         self._step_start.record(main)
         for lane in self._lanes[1:]:
             lane.stream.wait_event(self._step_start)  # parameters updated and gradients zeroed
@@ -393,6 +401,8 @@ class ViewShardedTrainer:
                                                C.c_void_p(self._grid_done.cuda_event), 1), "gb_stream_wait_event")
                 if self._tex_pad is None:  # (padded: the grid group is overwritten by the unpad at the join)
                     memset_(self.grads.grid)
+                if self._tex_rgba is not None:
+                    texels_pad(self.splats.grid.view(-1), self._tex_rgba)
                 self._grid_ready.record(a)
             self._waited = set()
 

@@ -599,3 +599,40 @@ def test_pair_capacity_limits():
     assert tr.capacity == PAIR_LIMIT - 1
     with pytest.raises(RuntimeError):
         tr._set_capacity(PAIR_LIMIT)
+
+
+def test_rgba_texels_same_results():
+    """gb_context_set_texel_rgba: K3/K4 reading the RGBA-padded texel copy (gb_texels_pad) give the same
+    image and gradients as the reference layout, bit for bit; the backward insists on stride-4 texel
+    gradients with it."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+    from paper_2412_12734_b200.raster import GBError, texel_grads_unpad, texels_pad
+
+    n, K, W, H = 4, 4000, 128, 96
+    arrays = _pinhole_scene(K, n, 21)
+    import paper_2412_12734_b200.scenes as sc
+
+    spec = sc.look_at((0.0, 0.3, -3.5), (0.0, 0.0, 0.0), W, H, 110.0, 110.0, W / 2, H / 2)
+    splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    cam = gb.PinholeCamera.from_spec(spec)
+    b = gb.build_binning(splats, cam)
+    rgba = torch.zeros(splats.grid.numel() // 3 * 4, dtype=torch.float32, device="cuda")
+    texels_pad(splats.grid.view(-1), rgba)
+    out3 = gb.render_forward(splats, cam, b)
+    out4 = gb.render_forward(splats, cam, b, texels_rgba=rgba)
+    assert torch.equal(out3.color, out4.color) and torch.equal(out3.last_rank, out4.last_rank)
+    ig = torch.sign(torch.randn(H, W, 3, device="cuda", generator=torch.Generator("cuda").manual_seed(3)))
+    pad3 = torch.zeros_like(rgba)
+    pad4 = torch.zeros_like(rgba)
+    g3 = gb.render_backward(splats, cam, b, out3, ig, texel_grad=pad3)
+    g4 = gb.render_backward(splats, cam, b, out4, ig, texel_grad=pad4, texels_rgba=rgba)
+    # same arithmetic; float atomics may order the adds differently
+    for k, v in g3.tensors().items():
+        if k == "grid":
+            continue
+        np.testing.assert_allclose(g4.tensors()[k].cpu().numpy(), v.cpu().numpy(), rtol=1e-5, atol=1e-7, err_msg=k)
+    np.testing.assert_allclose(pad4.cpu().numpy(), pad3.cpu().numpy(), rtol=1e-5, atol=1e-7)
+    with pytest.raises(GBError):
+        gb.render_backward(splats, cam, b, out4, ig, texels_rgba=rgba)  # stride-3 gradients with RGBA texels
