@@ -964,6 +964,10 @@ public:
         params_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * T);
         grads_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * T);
         pad_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * 4 * K * n * n + 16);
+        // the compositors read the texels from an RGBA-padded copy (gb_context_set_texel_rgba), refreshed after
+        // every texel update
+        rgba_ = std::make_unique<detail::Buffer>(ctx_, sizeof(float) * 4 * K * n * n + 16);
+        for (Lane& l : lanes_) detail::check(gb_context_set_texel_rgba(l.ctx, rgba_->f()), "gb_context_set_texel_rgba");
         detail::check(gb_memset_device(ctx_, params_->ptr, 0, sizeof(float) * T), "gb_memset_device");
         auto put = [&](std::int64_t off, const std::vector<float>& v, std::int64_t want, const char* what) {
             if (static_cast<std::int64_t>(v.size()) != want)
@@ -989,6 +993,7 @@ public:
         pairs_ = std::make_unique<detail::Buffer>(ctx_, sizeof(uint32_t) * nv);
         overflow_ = std::make_unique<detail::Buffer>(ctx_, 16);
         detail::check(gb_memset_device(ctx_, overflow_->ptr, 0, 16), "gb_memset_device");
+        detail::check(gb_texels_pad(ctx_, params_->f() + layout_.grid, rgba_->f(), K * n * n), "gb_texels_pad");
         detail::check(gb_sync(ctx_), "gb_sync");
         build_segments();
     }
@@ -997,9 +1002,11 @@ public:
     ~Rank() {
         if (graph_) gb_graph_destroy(graph_);
         for (Lane& l : lanes_) gb_sync(l.ctx);
+        if (adam_ctx_) gb_sync(adam_ctx_);
         params_.reset();
         grads_.reset();
         pad_.reset();
+        rgba_.reset();
         m_.reset();
         v_.reset();
         gshard_.reset();
@@ -1287,10 +1294,13 @@ private:
             detail::check(gb_adam_segments(adam_ctx_, 1, grid_segs.data(), static_cast<int32_t>(grid_segs.size()),
                                            &st_grid, &l, flag),
                           "step: adam");
+            detail::check(gb_texels_pad(adam_ctx_, params_->f() + layout_.grid, rgba_->f(), K_ * n_ * n_), "step");
             detail::check(gb_event_record(adam_ctx_, ev_grid_done_), "step");
         }
         if (multi && cfg_.sharded_adam)
             detail::check(gb_all_gather_params(ctx_, comm_, params_->f() + lo_, params_->f(), S_), "step: all-gather");
+        if (grid_segs.empty())  // (several ranks: the texels are final on the main stream)
+            detail::check(gb_texels_pad(ctx_, params_->f() + layout_.grid, rgba_->f(), K_ * n_ * n_), "step");
         int64_t code = 0;
         detail::check(gb_copy_d2h(ctx_, &code, flag_->ptr, sizeof(code), 1), "step");
         return code;
@@ -1320,7 +1330,7 @@ private:
     int overflows_ = 0;
     int n_ = 1;
     double sigma_ = 0.5;
-    std::unique_ptr<detail::Buffer> params_, grads_, pad_, m_, v_, gshard_, flag_, loss_, pairs_, overflow_;
+    std::unique_ptr<detail::Buffer> params_, grads_, pad_, rgba_, m_, v_, gshard_, flag_, loss_, pairs_, overflow_;
     std::vector<gb_adam_segment> segs_;
 };
 

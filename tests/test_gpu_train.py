@@ -628,11 +628,10 @@ def test_rgba_texels_same_results():
     pad4 = torch.zeros_like(rgba)
     g3 = gb.render_backward(splats, cam, b, out3, ig, texel_grad=pad3)
     g4 = gb.render_backward(splats, cam, b, out4, ig, texel_grad=pad4, texels_rgba=rgba)
-    # same arithmetic; float atomics may order the adds differently
-    for k, v in g3.tensors().items():
-        if k == "grid":
-            continue
-        np.testing.assert_allclose(g4.tensors()[k].cpu().numpy(), v.cpu().numpy(), rtol=1e-5, atol=1e-7, err_msg=k)
-    np.testing.assert_allclose(pad4.cpu().numpy(), pad3.cpu().numpy(), rtol=1e-5, atol=1e-7)
+    # same arithmetic; float atomics may order the adds differently (the last bits, relative to the field)
+    pairs = [(k, g4.tensors()[k], v) for k, v in g3.tensors().items() if k != "grid"] + [("texels", pad4, pad3)]
+    for k, a, r in pairs:
+        err = float((a - r).abs().max()) / (1e-12 + float(r.abs().max()))
+        assert err < 1e-5, (k, err)
     with pytest.raises(GBError):
         gb.render_backward(splats, cam, b, out4, ig, texels_rgba=rgba)  # stride-3 gradients with RGBA texels
