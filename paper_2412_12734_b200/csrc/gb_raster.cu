@@ -32,9 +32,10 @@ namespace gb {
 
 // K4 warp-entries with at most this many active lanes add per lane instead of reducing first (B200 sweep
 // of 0..32 at configs[3]: 0 = always reduce 575 MP/s, 8 = 605, 12 = 607, 16 = 605, 24 = 586, 32 = 453;
-// re-swept after the footprint classes: 10 -> 719.1, 12 -> 718.8, 14 -> 716.1, 16 -> 712.1)
+// re-swept after the footprint classes: 10 -> 719.1, 12 -> 718.8, 14 -> 716.1, 16 -> 712.1; with RGBA texels
+// at 5 CTAs/SM: 10 -> 859.8, 12 -> 858.6, 14 -> 854.7)
 #ifndef GB_K4_DIRECT_LANES
-#define GB_K4_DIRECT_LANES 12
+#define GB_K4_DIRECT_LANES 10
 #endif
 constexpr int kDirectLanes = GB_K4_DIRECT_LANES;
 
@@ -848,14 +849,18 @@ __global__ void __launch_bounds__(256, GB_K3_MINB) k_forward_loss(const uint2* _
     if ((threadIdx.x & 31) == 0 && loss && l != (real)0) atomicAdd(loss, (float)(l * scale));
 }
 
-// <= 64 registers: 4 CTAs (32 warps) per SM, no spills -- with the branch-free entry, measured 1.0 %
-// faster than 5 CTAs at 48 registers (16 B of spills) and 7 % faster than 6 CTAs at 40 (56 B)
-// (before it, 5 CTAs with 32 B of spills had been 1.3 % faster than 4)
+// K4 register caps.  Reference texel layout (TL = 3): <= 64 registers, 4 CTAs (32 warps) per SM, no spills --
+// with the branch-free entry, 1.0 % faster than 5 CTAs at 48 registers (16 B of spills) and 7 % faster than 6
+// CTAs at 40 (56 B).  RGBA texels (TL = 4, one 16-B load per texel, fewer live registers): <= 48 registers,
+// 5 CTAs per SM (16 B of spills) -- 2.7 % faster than 4 CTAs, 7 % faster than 6 (profiles/ab_r02.md s44).
 #ifndef GB_K4_MINB
 #define GB_K4_MINB 4
 #endif
+#ifndef GB_K4_MINB_RGBA
+#define GB_K4_MINB_RGBA 5
+#endif
 template <int MODE, int NT, int S, int TL>
-__global__ void __launch_bounds__(256, GB_K4_MINB) k_backward_direct(const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(256, TL == 4 ? GB_K4_MINB_RGBA : GB_K4_MINB) k_backward_direct(const uint2* __restrict__ ranges,
                                                          const int32_t* __restrict__ values,
                                                          const ScreenHeader* __restrict__ hdr,
                                                          const CullRec* __restrict__ cull, const float* __restrict__ tex,
