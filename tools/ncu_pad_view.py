@@ -22,11 +22,14 @@ def main(view=0):
     grads = gb.GradientBuffer(s)
     state = gb.AdamState(s)
     torch.cuda.synchronize()
+    # the trainer's configuration: RGBA-padded texels (one 16-B load per texel) and texel gradients
+    rgba = torch.zeros(grads.grid.numel() // 3 * 4, device="cuda")
+    gb.raster.texels_pad(s.grid.view(-1), rgba)
     b = gb.build_binning(s, cam)
-    out = gb.render_forward(s, cam, b)
+    out = gb.render_forward(s, cam, b, texels_rgba=rgba)
     loss, ig = gb.l1_loss(out.color, target)
     pad = torch.zeros(grads.grid.numel() // 3 * 4, device="cuda")
-    gb.render_backward(s, cam, b, out, ig, grads, texel_grad=pad)
+    gb.render_backward(s, cam, b, out, ig, grads, texel_grad=pad, texels_rgba=rgba)
     gb.adam_step(s, grads, state, gb.LearningRates())
     torch.cuda.synchronize()
     print("ncu_view ok: P =", b.total, "loss =", float(loss))

@@ -39,6 +39,10 @@ def cell(K, T, iters):
     W, H = cam.width, cam.height
     target = torch.rand((H, W, 3), generator=g, device="cuda", dtype=torch.float32)
     grads = gb.GradientBuffer(splats)
+    # the trainer's configuration: RGBA-padded texels and texel gradients
+    rgba = torch.zeros(splats.grid.numel() // 3 * 4, device="cuda")
+    gb.raster.texels_pad(splats.grid.view(-1), rgba)
+    pad = torch.zeros_like(rgba)
     b = gb.TileBinning()
     out = gb.RenderOutput(W, H, "cuda")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
@@ -47,12 +51,13 @@ def cell(K, T, iters):
         ev[0].record()
         gb.build_binning(splats, cam, gb.RasterConfig(), out=b)
         ev[1].record()
-        gb.render_forward(splats, cam, b, out)
+        gb.render_forward(splats, cam, b, out, texels_rgba=rgba)
         ev[2].record()
         _, ig = gb.l1_loss(out.color, target)
         grads.zero_()
+        pad.zero_()
         ev[3].record()
-        gb.render_backward(splats, cam, b, out, ig, grads)
+        gb.render_backward(splats, cam, b, out, ig, grads, texel_grad=pad, texels_rgba=rgba)
         ev[4].record()
         torch.cuda.synchronize()
         if it >= 2:
