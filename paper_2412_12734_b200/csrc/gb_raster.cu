@@ -277,9 +277,8 @@ __device__ __forceinline__ void bwd_shade(const TexelRef<TL>& tx, int id, bool o
             if (NS == 10) {
                 red4(a + 4, red[4], red[5], red[6], red[7]);
                 red2(a + 8, red[8], red[9]);
-            } else {
-                red2(a + 4, red[4], red[5]);
-                atomicAdd(a + 6, red[6]);
+            } else {  // slot 7 is padding in the ortho record: one 16-B red for slots 4..7
+                red4(a + 4, red[4], red[5], red[6], (real)0);
             }
             texel_reds();
         }
