@@ -222,6 +222,7 @@ struct ProjParams {
     const float* opacity;
     int W, H;
     double fx, fy, cx, cy;
+    double inv_fx, inv_fy;  // 1/fx, 1/fy (K5)
     double R[9];
     double t[3];
     double near_plane;
