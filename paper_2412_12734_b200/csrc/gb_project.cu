@@ -132,9 +132,9 @@ __device__ float4 alpha_box(const ProjParams& p, int64_t k, const Geom& g, doubl
         const double C22 = r2 * (H2[0] * H2[0] + H2[1] * H2[1]) - H2[2] * H2[2];
         const double dx = C02 * C02 - C00 * C22, dy = C12 * C12 - C11 * C22;
         if (!(dx >= 0.0) || !(dy >= 0.0) || !(C22 < 0.0)) return all;
-        const double sx = sqrt(dx), sy = sqrt(dy);
-        const double xa = (C02 - sx) / C22, xb = (C02 + sx) / C22;
-        const double ya = (C12 - sy) / C22, yb = (C12 + sy) / C22;
+        const double sx = sqrt(dx), sy = sqrt(dy), ic = 1.0 / C22;  // product-only box: reciprocal, not 4 divisions
+        const double xa = (C02 - sx) * ic, xb = (C02 + sx) * ic;
+        const double ya = (C12 - sy) * ic, yb = (C12 + sy) * ic;
         min_x = dmin_(xa, xb);
         max_x = dmax_(xa, xb);
         min_y = dmin_(ya, yb);
@@ -197,13 +197,15 @@ __device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g, 
         // C is over p = (x, y, 1) with x, y continuous pixel coordinates
         const double det2 = C[0][0] * C[1][1] - C[0][1] * C[0][1];
         if (!(C[0][0] > 0.0) || !(det2 > 0.0)) return all;
-        const double cx = -(C[1][1] * C[0][2] - C[0][1] * C[1][2]) / det2;
-        const double cy = -(C[0][0] * C[1][2] - C[0][1] * C[0][2]) / det2;
+        const double idet = 1.0 / det2;  // product-only ellipse: reciprocals instead of divisions
+        const double cx = -(C[1][1] * C[0][2] - C[0][1] * C[1][2]) * idet;
+        const double cy = -(C[0][0] * C[1][2] - C[0][1] * C[0][2]) * idet;
         const double kk = -(C[2][2] + C[0][2] * cx + C[1][2] * cy);
         if (!(kk > 0.0)) return all;
-        A11 = C[0][0] / kk;
-        A12 = C[0][1] / kk;
-        A22 = C[1][1] / kk;
+        const double ikk = 1.0 / kk;
+        A11 = C[0][0] * ikk;
+        A12 = C[0][1] * ikk;
+        A22 = C[1][1] * ikk;
         ex = cx - 0.5;
         ey = cy - 0.5;
     }
@@ -263,10 +265,12 @@ __global__ void __launch_bounds__(256, GB_K1_MINB) k_project(const ProjParams p,
         int cxi, cyi;
         real hx, hy;
         double dxe, dye;
-        pinhole_centre<false>(p, g, cxi, cyi, hx, hy, dxe, dye);
+        // the header is product-only (no binning decision reads it): reciprocals instead of divisions
+        pinhole_centre<true>(p, g, cxi, cyi, hx, hy, dxe, dye);
         PinholeCoeffs pc;
         pinhole_coeffs(g, dxe, dye, pc);
-        const double sx = 1.0 / (pc.E[2] * p.fx), sy = 1.0 / (pc.E[2] * p.fy);
+        const double iez = 1.0 / pc.E[2];
+        const double sx = iez * p.inv_fx, sy = iez * p.inv_fy;
         const bool ok = pc.E[2] != 0.0 && isfinite(sx) && isfinite(sy);
         const double nan = (double)__int_as_float(0x7fc00000);
         // X = Cx/(E_z fx), Y = Cy/(E_z fy); a degenerate plane (through the camera centre) misses everywhere
