@@ -2,6 +2,7 @@
 # Interleaved A/B of library variants on one box: bash tools/ab_run.sh ROUNDS name[=libpath] ...
 # ("default" = the in-tree libgb_raster.so).  One bench line per (round, variant) in gpurun_out/ab_<name>_<r>.json.
 R=$1; shift
+rm -f gpurun_out/ab_*.json gpurun_out/ab_*.err
 for r in $(seq 1 "$R"); do
   for v in "$@"; do
     name=${v%%=*}; lib=${v#*=}
