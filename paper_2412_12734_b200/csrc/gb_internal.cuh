@@ -61,8 +61,9 @@ constexpr real kMaxAlpha = (real)0.999;  // core.hpp:16
 //            h2 = (hy, int cxi, int cyi, 0); dx = (x - cxi) + hx, dy = (y - cyi) + hy.
 //   both   : h3 = (x0, x1, y0, y1) the inclusive pixel box outside which
 //            alpha < alpha_skip for certain (fp64 AABB of the alpha-skip
-//            ellipse, enlarged by a safety margin); the compositors skip a
-//            warp's 8x4 pixel block for this entry when it misses the box.
+//            ellipse, enlarged by a safety margin) -- filled only in the
+//            -DGB_CULL_BOX variant, whose compositors test it; the product
+//            tests the alpha-skip ellipse of the cull record instead.
 struct __align__(16) ScreenHeader {
     real4 h0, h1, h2;
     float4 h3;

@@ -154,7 +154,7 @@ __device__ float4 alpha_box(const ProjParams& p, int64_t k, const Geom& g, doubl
 // alpha_box.  Record: a = (e_x, e_y, Q11, Q22), b = (Q12, Q12/Q22, Q12/Q11, 0).
 // All-zero Q passes everything (threshold disabled, or the region reaches
 // behind the camera and is not an ellipse); e = +inf-like passes nothing.
-__device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g, double r, const float4 box) {
+__device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g, double r) {
     const CullRec all = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
     const CullRec none = {make_float4(1e30f, 1e30f, 1.f, 1.f), make_float4(0.f, 0.f, 0.f, 0.f)};
     if (!(p.alpha_skip > 0.0)) return all;
@@ -217,6 +217,7 @@ __device__ CullRec alpha_ellipse(const ProjParams& p, int64_t k, const Geom& g, 
     // circumscribing the alpha-box (axis-aligned, no cancellation).
     const double tr = 0.5 * (A11 + A22), dq = sqrt(fmax(tr * tr - (A11 * A22 - A12 * A12), 0.0));
     if (!(tr - dq > 0.0) || (tr + dq) > 4096.0 * (tr - dq)) {
+        const float4 box = alpha_box(p, k, g, r);  // only here: the compositors test the ellipse
         if (box.x > box.y || box.z > box.w) return none;
         if (box.x < -1e29f || box.y > 1e29f || box.z < -1e29f || box.w > 1e29f) return all;
         const double hx = 0.5 * ((double)box.y - (double)box.x) + 0.5, hy = 0.5 * ((double)box.w - (double)box.z) + 0.5;
@@ -281,9 +282,13 @@ __global__ void __launch_bounds__(256, GB_K1_MINB) k_project(const ProjParams p,
         h.h2.z = hdr_from_int(cyi);
     }
     const double ar = p.alpha_skip > 0.0 && g.alpha_k > p.alpha_skip ? alpha_radius(p, g) : 0.0;
-    h.h3 = alpha_box(p, k, g, ar);
+#ifdef GB_CULL_BOX
+    h.h3 = alpha_box(p, k, g, ar);  // A/B variant: the compositors test the box
+#else
+    h.h3 = make_float4(0.f, 0.f, 0.f, 0.f);  // unread: the compositors test the ellipse (cull record)
+#endif
     hdr[k] = h;
-    cull[k] = alpha_ellipse(p, k, g, ar, h.h3);
+    cull[k] = alpha_ellipse(p, k, g, ar);
 }
 
 
