@@ -503,7 +503,19 @@ __device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __
 #endif
 struct WarpHeaders {
     real4 h[3][32];
+    int id[32];   // the chunk's primitive ids (read per entry instead of a shuffle of a register held through the loop)
+    float4 rect;  // K4: the warp's pixel rectangle for the cull test, +-0.05 px (re-read per chunk, see bwd_walk)
 };
+
+// the warp rectangle kept in shared memory: re-read once per 32-entry chunk instead of holding four registers
+// through the entry loop (at K4's 48-register cap they spilled: three local loads per warp-entry)
+__device__ __forceinline__ float4 ld_rect(const float4* r) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"((uint32_t)__cvta_generic_to_shared(r)));
+    return v;
+}
 
 __device__ __forceinline__ void stage_headers(WarpHeaders& wh, const ScreenHeader* __restrict__ hdr, bool pass,
                                               int idl, int lane) {
@@ -512,6 +524,7 @@ __device__ __forceinline__ void stage_headers(WarpHeaders& wh, const ScreenHeade
         wh.h[0][lane] = ld_real4(&hdr[idl].h0);
         wh.h[1][lane] = ld_real4(&hdr[idl].h1);
         wh.h[2][lane] = ld_real4(&hdr[idl].h2);
+        wh.id[lane] = idl;
     }
     __syncwarp();
 }
@@ -555,10 +568,11 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
         while (mask) {
             const int bit = __ffs(mask) - 1;
             mask &= mask - 1;
-            const int id = __shfl_sync(kFull, idl, bit);
 #if GB_WARP_STAGE
+            const int id = wh->id[bit];
             const ScreenHeader h = staged_hdr(*wh, bit);
 #else
+            const int id = __shfl_sync(kFull, idl, bit);
             ScreenHeader h;
             h.h0 = ld_real4(&hdr[id].h0);
             h.h1 = ld_real4(&hdr[id].h1);
@@ -584,15 +598,23 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
     if (g0 == (real)0 && g1 == (real)0 && g2 == (real)0) last = -1;  // raster.hpp:315-317
     real bh0 = cc.bg[0], bh1 = cc.bg[1], bh2 = cc.bg[2];
     const int wlast = __reduce_max_sync(kFull, last);
+#if GB_WARP_STAGE && !defined(GB_CULL_BOX)
+    if (lane == 0) wh->rect = make_float4(wp.bx0 - 0.05f, wp.bx1 + 0.05f, wp.by0 - 0.05f, wp.by1 + 0.05f);
+    __syncwarp();
+#endif
     for (int c0 = wlast & ~31; c0 >= 0; c0 -= 32) {
         // (a live rectangle here -- lanes with last >= c0 -- measured 1 % slower: few entries drop out)
-        const WarpPixel& lr = wp;
         int idl = -1;
         bool pass = false;
         if (c0 + lane <= wlast) {
             idl = __ldg(&values[range.x + c0 + lane]);
             GB_CHECK(idl >= 0 && idl < rc.dbg_K);
-            pass = entry_meets_warp(hdr, cull, idl, lr);
+#if GB_WARP_STAGE && !defined(GB_CULL_BOX)
+            const float4 r = ld_rect(&wh->rect);
+            pass = ellipse_meets_rect(__ldg(&cull[idl].a), __ldg(&cull[idl].b), r.x, r.y, r.z, r.w);
+#else
+            pass = entry_meets_warp(hdr, cull, idl, wp);
+#endif
         }
         unsigned mask = __ballot_sync(kFull, pass);
         if (lane == 0) GB_DBG(1, __popc(mask));
@@ -602,10 +624,11 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
         while (mask) {
             const int bit = 31 - __clz(mask);
             mask &= ~(1u << bit);
-            const int id = __shfl_sync(kFull, idl, bit);
 #if GB_WARP_STAGE
+            const int id = wh->id[bit];
             const ScreenHeader h = staged_hdr(*wh, bit);
 #else
+            const int id = __shfl_sync(kFull, idl, bit);
             ScreenHeader h;
             h.h0 = ld_real4(&hdr[id].h0);
             h.h1 = ld_real4(&hdr[id].h1);
