@@ -238,7 +238,7 @@ def run_reference(args):
 # our arm
 # ---------------------------------------------------------------------------------------------
 def run_cpp_host(args, arrays, cams, views, dev_targets, W, H, host_targets=None):
-    """The same device-resident step through the C++ host (gbil_b200::multiview::Rank: four view lanes,
+    """The same device-resident step through the C++ host (gbil_b200::multiview::Rank: six view lanes,
     capacity binning, one CUDA graph per step, padded texel gradients; Adam on one stream), timed by wall
     clock around K steps (each step ends with its synchronous loss and flag read)."""
     import ctypes as C
@@ -265,7 +265,8 @@ def run_cpp_host(args, arrays, cams, views, dev_targets, W, H, host_targets=None
     rc = lib.gb_mv_create(torch.cuda.current_device(), K, n, *[a[k].ctypes.data for k in ("position", "quat",
                                                                                             "log_scale",
                                                                                             "opacity_logit", "grid")],
-                          W, H, len(cams), cam16.ctypes.data, len(vv), vv.ctypes.data, 4, 1, 6.0, C.byref(h))
+                          W, H, len(cams), cam16.ctypes.data, len(vv), vv.ctypes.data, int(os.environ.get("GB_LANES", "6")), 1, 6.0,
+                          C.byref(h))
     if rc:
         raise RuntimeError(lib.gb_mv_error().decode())
     tp = (P * len(dev_targets))(*[t.data_ptr() for t in dev_targets])
@@ -298,7 +299,7 @@ def run_cpp_host(args, arrays, cams, views, dev_targets, W, H, host_targets=None
     return {"value": round(len(views) * W * H / 1e6 / dt, 3), "unit": "MP/s", "ms_per_step": round(dt * 1e3, 3),
             "e2e": e2e,
             "what": "the same device-resident step driven by the C++ host (gbil_b200::multiview::Rank via "
-                    "libgb_mvhost.so): four view lanes, capacity binning, one CUDA graph per step, padded texel "
+                    "libgb_mvhost.so): six view lanes, capacity binning, one CUDA graph per step, padded texel "
                     "gradients, Adam's texel update overlapped with the next binning; wall clock around K steps, "
                     "each ending with its loss read (e2e: pinned host targets copied inside every step)",
             "last_loss": round(loss.value, 6)}
@@ -338,7 +339,7 @@ def run_ours(args):
     use_graph = os.environ.get("GB_GRAPH", "1") != "0" and not args.no_graph
     blocking = os.environ.get("GB_BLOCKING_BINNING") == "1"
     trainer = ViewShardedTrainer(splats, cams, views, lrs=lrs, graph=use_graph, async_binning=not blocking,
-                                 lanes=int(os.environ.get("GB_LANES", "4")),
+                                 lanes=int(os.environ.get("GB_LANES", "6")),
                                  overlap_adam=os.environ.get("GB_OVERLAP_ADAM", "1") == "1",
                                  capacity_margin=float(os.environ.get("GB_CAP_MARGIN", "1.1")),
                                  fused=os.environ.get("GB_FUSED") == "1",

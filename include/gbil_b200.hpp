@@ -936,7 +936,7 @@ struct Buffer {  // device memory of one rank's context
 class Rank {
 public:
     Rank(int device, const PinholeScene& scene, std::vector<PinholeCamera> cameras, std::vector<int> views,
-         const StepConfig& cfg, int nranks, int rank, int lanes = 4, bool graph = true)
+         const StepConfig& cfg, int nranks, int rank, int lanes = 6, bool graph = true)
         : cams_(std::move(cameras)), views_(std::move(views)), cfg_(cfg), nranks_(nranks), rank_(rank),
           layout_(scene.count, scene.n, nranks), use_graph_(graph) {
         cfg_.lrs.validate();

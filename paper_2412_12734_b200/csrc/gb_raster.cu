@@ -33,9 +33,10 @@ namespace gb {
 // K4 warp-entries with at most this many active lanes add per lane instead of reducing first (B200 sweep
 // of 0..32 at configs[3]: 0 = always reduce 575 MP/s, 8 = 605, 12 = 607, 16 = 605, 24 = 586, 32 = 453;
 // re-swept after the footprint classes: 10 -> 719.1, 12 -> 718.8, 14 -> 716.1, 16 -> 712.1; with RGBA texels
-// at 5 CTAs/SM: 10 -> 859.8, 12 -> 858.6, 14 -> 854.7)
+// at 5 CTAs/SM: 10 -> 859.8, 12 -> 858.6, 14 -> 854.7; after the shared-memory id staging: 8 -> 888.2,
+// 10 -> 892.2, 12 -> 893.3, 14 -> 891.5)
 #ifndef GB_K4_DIRECT_LANES
-#define GB_K4_DIRECT_LANES 10
+#define GB_K4_DIRECT_LANES 12
 #endif
 constexpr int kDirectLanes = GB_K4_DIRECT_LANES;
 
@@ -580,7 +581,9 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
 #endif
             // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not composite
             fwd_entry<MODE, NT, TL>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
+#ifndef GB_K3_CHUNK_EXIT
             if (__all_sync(kFull, done)) break;
+#endif
         }
     }
 }

@@ -260,7 +260,7 @@ class ViewShardedTrainer:
 
     def __init__(self, splats: SplatSet, cameras: Sequence, views: Sequence[int], lrs: LearningRates = None,
                  adam: AdamConfig = None, raster: RasterConfig = None, process_group=None, check_finite=False,
-                 lanes: int = 4, fused: bool = False, async_binning: bool = True, graph: bool = False,
+                 lanes: int = 6, fused: bool = False, async_binning: bool = True, graph: bool = False,
                  capacity_margin: float = 1.1, sharded_adam: bool = True, overlap_adam: bool = True,
                  texel_pad: bool = True, rgba_texels: bool = True):
         self.splats = splats
