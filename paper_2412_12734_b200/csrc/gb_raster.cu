@@ -580,10 +580,9 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             h.h2 = ld_real4(&hdr[id].h2);
 #endif
             // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not composite
+            // (no per-entry all-done vote: early termination is checked once per chunk by the outer loop --
+            // the rest of a chunk after every pixel finished composites nothing; +0.65 %, ab_r02 s53)
             fwd_entry<MODE, NT, TL>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
-#ifndef GB_K3_CHUNK_EXIT
-            if (__all_sync(kFull, done)) break;
-#endif
         }
     }
 }
