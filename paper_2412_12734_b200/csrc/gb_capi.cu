@@ -236,6 +236,8 @@ gb_status set_device(gb_context* ctx) {
     return GB_OK;
 }
 
+constexpr int kMaxImageSide = 65536 - 16;
+
 gb_status validate_camera(const gb_camera* cam) {
     if (!cam) return fail(GB_INVALID_ARGUMENT, "camera is null");
     if (cam->width < 1 || cam->height < 1)
@@ -248,8 +250,9 @@ gb_status validate_camera(const gb_camera* cam) {
     if (cam->mode == GB_MODE_PINHOLE && !(cam->fx != 0.0 && cam->fy != 0.0 && std::isfinite(cam->fx) &&
                                           std::isfinite(cam->fy)))
         return fail(GB_INVALID_ARGUMENT, "pinhole camera: fx and fy must be finite and non-zero");
-    if (cam->width > 65535 * 16 || cam->height > 65535 * 16)
-        return fail(GB_NOT_SUPPORTED, "image too large");
+    // the compositors pack a pixel's (x, y) into 16 + 16 bits (tiles overhang the image by < 16 px)
+    if (cam->width > kMaxImageSide || cam->height > kMaxImageSide)
+        return fail(GB_NOT_SUPPORTED, "image too large (at most 65520 pixels per side)");
     return GB_OK;
 }
 

@@ -635,3 +635,23 @@ def test_rgba_texels_same_results():
         assert err < 1e-5, (k, err)
     with pytest.raises(GBError):
         gb.render_backward(splats, cam, b, out4, ig, texels_rgba=rgba)  # stride-3 gradients with RGBA texels
+
+
+def test_image_side_limit():
+    """K4 packs a pixel's (x, y) into 16 + 16 bits, so the C-ABI rejects images wider or taller than
+    65536 - 16 pixels (tiles overhang the image by < 16 px) with GB_NOT_SUPPORTED, before any launch."""
+    import paper_2412_12734_b200 as gb
+    import paper_2412_12734_b200.scenes as sc
+    from paper_2412_12734_b200.raster import GBError
+
+    n, K = 2, 64
+    arrays = _pinhole_scene(K, n, 5)
+    splats = gb.SplatSet.from_numpy(O.MODE_PINHOLE, gb.ColorGridConfig(n), **arrays)
+    for W, H, ok in ((65520, 8, True), (65521, 8, False), (8, 65521, False)):
+        spec = sc.look_at((0.0, 0.3, -3.5), (0.0, 0.0, 0.0), W, H, 110.0, 110.0, W / 2, H / 2)
+        cam = gb.PinholeCamera.from_spec(spec)
+        if ok:
+            gb.build_binning(splats, cam)
+        else:
+            with pytest.raises(GBError, match="too large"):
+                gb.build_binning(splats, cam)
