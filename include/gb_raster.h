@@ -96,7 +96,8 @@ typedef struct {
 
 /* ImagePlaneCamera (core.hpp:104-116) plus the pinhole extension:
  * OpenCV convention, x_pix = fx*X/Z + cx with pixel centres at i + 0.5,
- * world->camera [rot | trans]. */
+ * world->camera [rot | trans].  width, height <= 65520 (GB_NOT_SUPPORTED past it:
+ * the compositors pack a pixel's coordinates into 16 + 16 bits). */
 typedef struct {
     int32_t mode;
     int32_t width;
