@@ -311,7 +311,7 @@ class ViewShardedTrainer:
         self._pinned_losses = torch.zeros(max(1, len(self.views)), dtype=torch.float32, pin_memory=True)
         self._pinned_flag = torch.zeros(1, dtype=torch.int64, pin_memory=True)
         # two target buffers per view lane: every lane's view can have its target landed while the copy stream
-        # runs ahead (with two buffers for four lanes, lanes 3-4 waited for a free buffer)
+        # runs ahead (with two buffers for four lanes, lanes 3-4 had waited for a free buffer)
         nbuf = 2 * len(self._lanes)
         self._target_buf = [torch.empty((H, W, 3), dtype=torch.float32, device=dev) for _ in range(nbuf)]
         self._copy_stream = torch.cuda.Stream(device=dev)
