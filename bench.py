@@ -237,6 +237,41 @@ def run_reference(args):
 # ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
+def k4_isolated(trainer, cams, views, dev_targets, W, H, device):
+    """Average K4 launch time of `views` run one after another on one stream (trainer's configuration:
+    RGBA-padded texels and texel gradients), with the pair count P of each view for the algorithmic bytes."""
+    import torch
+
+    import paper_2412_12734_b200 as gb
+
+    splats = trainer.splats
+    ctx = gb.raster.context(device)
+    rb = gb.TileBinning(device)
+    out = gb.RenderOutput(W, H, device)
+    grads = gb.GradientBuffer(splats)
+    rgba = torch.empty(splats.grid.numel() // 3 * 4, dtype=torch.float32, device=device)
+    gb.raster.texels_pad(splats.grid.view(-1), rgba)
+    pad = torch.zeros_like(rgba)
+    pairs, ms, cnt = 0, 0.0, 0
+    for rep in range(2):  # the first pass warms up
+        for v in views:
+            b = gb.build_binning(splats, cams[v], out=rb)
+            o = gb.render_forward(splats, cams[v], b, out, texels_rgba=rgba)
+            _, ig = gb.l1_loss(o.color, dev_targets[v])
+            torch.cuda.synchronize()
+            ctx.profile(True)
+            ctx.profile_read()
+            gb.render_backward(splats, cams[v], b, o, ig, grads, texel_grad=pad, texels_rgba=rgba)
+            t, n = ctx.profile_read()["backward"]
+            ctx.profile(False)
+            if rep == 1:
+                pairs, ms, cnt = pairs + b.total, ms + t, cnt + n
+    del pad, rgba, grads
+    return {"avg_launch_ms": round(ms / max(1, cnt), 4), "mean_pairs": pairs // max(1, len(views)),
+            "launches": cnt, "what": "K4 of %d configs[3] views one at a time on one stream after the timed "
+                                     "region (CUDA events at the C-ABI launch site)" % len(views)}
+
+
 def run_cpp_host(args, arrays, cams, views, dev_targets, W, H, host_targets=None):
     """The same device-resident step through the C++ host (gbil_b200::multiview::Rank: six view lanes,
     capacity binning, one CUDA graph per step, padded texel gradients; Adam on one stream), timed by wall
@@ -453,6 +488,15 @@ def run_ours(args):
         fwd = {"ms_per_view": round(f_ms, 4), "value": round(W * H / 1e6 / (f_ms / 1e3), 3), "unit": "MP/s",
                "what": "build_binning + render_forward per view, one stream, CUDA events"}
 
+    # ---- K4 alone: the backward compositor of a few views on one stream, no other lane sharing the SMs
+    # (the roofline above times it inside the overlapped step) -- per-launch-site CUDA events of the C-ABI ----
+    k4_alone = None
+    if rank == 0:
+        try:
+            k4_alone = k4_isolated(trainer, cams, views[:8], dev_targets, W, H, device)
+        except Exception as e:  # an extra measurement never blocks the headline
+            k4_alone = {"failed": str(e)[:200]}
+
     # ---- the same step driven by the C++ host (include/gbil_b200.hpp multiview::Rank, libgb_mvhost.so) ----
     cpp_host = None
     if rank == 0 and world == 1 and not args.no_cpp_host:
@@ -543,7 +587,11 @@ def run_ours(args):
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(bytes_per_launch), "avg_launch_ms": round(avg_ms, 4),
                      "avg_launch_ms_events": round(total_ms / max(1, count), 4),
-                     "peak_source": peak_src, "timing": prof_note},
+                     "peak_source": peak_src, "timing": prof_note,
+                     "alone": (dict(k4_alone, frac=round(model["backward"](k4_alone["mean_pairs"])
+                                                        / (k4_alone["avg_launch_ms"] / 1e3) / 1e9 / peak, 4))
+                               if k4_alone and "avg_launch_ms" in k4_alone and k4_alone["avg_launch_ms"] > 0
+                               else k4_alone)},
         "kernel_ms_per_step": kernel_ms,
         "kernel_ms_note": "each kernel's share of the timeline from CUDA events around every launch on all view "
                           "lanes: an instant covered by k concurrent launches counts 1/k to each, so the shares "
