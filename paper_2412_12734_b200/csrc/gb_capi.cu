@@ -329,7 +329,9 @@ gb::RasterConst make_raster_const(const gb_context* ctx, const gb_binning* b, in
     rc.tiles_x = b->tiles_x;
     rc.tiles_y = b->tiles_y;
     rc.alpha_skip = (gb::real)b->cfg.alpha_skip;
-    rc.early_stop = (gb::real)b->cfg.early_stop_transmittance;
+    // <= 0 disables the stop (raster.hpp:250); folded here so the compositors compare against a kernel
+    // parameter (a constant-bank operand) instead of re-deriving the threshold in registers
+    rc.early_stop = b->cfg.early_stop_transmittance > 0.0 ? (gb::real)b->cfg.early_stop_transmittance : (gb::real)-1;
     rc.tex_scale = (gb::real)((double)(n - 1) / (2.0 * sigma));
     rc.tex_offset = (gb::real)((double)(n - 1) * 0.5);
     rc.sigma = (gb::real)sigma;

@@ -123,7 +123,7 @@ struct RasterConst {
     int tile_size;
     int tiles_x, tiles_y;
     real alpha_skip;      // <= 0 disables
-    real early_stop;      // <= 0 disables
+    real early_stop;      // the early-termination threshold, or -1 when disabled (T >= 0 never falls below it)
     real tex_scale;       // (n-1)/(2 sigma)
     real tex_offset;      // (n-1)/2
     real sigma;

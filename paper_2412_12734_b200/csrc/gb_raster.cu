@@ -552,7 +552,7 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
     acc0 = acc1 = acc2 = (real)0;
     last = -1;
     bool done = !wp.inside;
-    const real early = rc.early_stop > (real)0 ? rc.early_stop : -(real)1;  // T >= 0: a disabled stop never fires
+    const real early = rc.early_stop;  // -1 when disabled (gb_capi.cu): T >= 0 never falls below it
     for (int c0 = 0; c0 < total && !__all_sync(kFull, done); c0 += 32) {
         const WarpPixel lr = live_rect(wp, !done);
         int idl = -1;
@@ -713,7 +713,7 @@ __device__ __forceinline__ void fwd_walk_staged(const uint2 range, const int32_t
     acc0 = acc1 = acc2 = (real)0;
     last = -1;
     bool done = !wp.inside;
-    const real early = rc.early_stop > (real)0 ? rc.early_stop : -(real)1;
+    const real early = rc.early_stop;
     if (total == 0) return;
     if (warp == 0) {
         stage_chunk(ring[0], values, range.x, 0, min(32, total), hdr, cull);
