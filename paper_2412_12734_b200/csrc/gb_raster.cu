@@ -424,7 +424,7 @@ __device__ __forceinline__ WarpPixel live_rect(const WarpPixel& wp, bool live) {
 
 // One forward entry for the calling warp (raster.hpp:238-250): evaluate, pick the warp's texel footprint
 // class (see bwd_shade), composite into the lanes that are not done.
-template <int MODE, int NT, int TL = 3>
+template <int MODE, int NT, int TL = 3, bool DERIVED_DONE = false>
 __device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __restrict__ tex, int id, int rank, int x,
                                           int y, const RasterConst& rc, int N, real early, bool& done, real& T,
                                           real& acc0, real& acc1, real& acc2, int& last) {
@@ -438,7 +438,10 @@ __device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __
     }
     const real G = gauss_weight(u, v);
     const real alpha = rmin(mul_rn(h.h1.z, G), kMaxAlpha);  // raster.hpp:241
-    const bool comp = !done && hit && !(alpha < rc.alpha_skip);     // raster.hpp:242
+    // DERIVED_DONE: a pixel is done once it composited (last >= 0) and T fell below the threshold -- the same
+    // state as the flag (T and last change only when compositing), without a flag to keep
+    const bool fin = DERIVED_DONE ? (last >= 0 && T < early) : done;
+    const bool comp = !fin && hit && !(alpha < rc.alpha_skip);     // raster.hpp:242
     // texel footprint class of the warp (see bwd_shade): clamped axes read one texel row
     const real sigma = rc.sigma;
     const bool au = N > 1 && __any_sync(kFull, comp && u > -sigma && u < sigma);
@@ -489,7 +492,7 @@ __device__ __forceinline__ void fwd_entry(const ScreenHeader& h, const float* __
         acc2 = fma_rn(c2_, w, acc2);
         T = mul_rn(T, sub_rn((real)1, alpha));
         last = rank;
-        if (T < early) done = true;  // raster.hpp:250
+        if (!DERIVED_DONE && T < early) done = true;  // raster.hpp:250
     }
 }
 
@@ -551,10 +554,19 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
     T = (real)1;
     acc0 = acc1 = acc2 = (real)0;
     last = -1;
-    bool done = !wp.inside;
     const real early = rc.early_stop;  // -1 when disabled (gb_capi.cu): T >= 0 never falls below it
-    for (int c0 = 0; c0 < total && !__all_sync(kFull, done); c0 += 32) {
-        const WarpPixel lr = live_rect(wp, !done);
+    // No per-pixel done flag (a byte-packed bool cost three instructions per entry at the 32-register cap): a
+    // pixel is done once it composited and T fell below the threshold (fwd_entry<..., true>).  Pixels outside
+    // the image start finished -- last 0, T -2 below any threshold >= -1 -- and are never stored.  +0.5 %
+    // (ab_r02 s60).
+    if (!wp.inside) {
+        T = (real)-2;
+        last = 0;
+    }
+    bool done = false;  // unused by the derived test
+#define GB_K3_DONE (last >= 0 && T < early)
+    for (int c0 = 0; c0 < total && !__all_sync(kFull, GB_K3_DONE); c0 += 32) {
+        const WarpPixel lr = live_rect(wp, !(GB_K3_DONE));
         int idl = -1;
         bool pass = false;
         if (c0 + lane < total) {
@@ -582,9 +594,10 @@ __device__ __forceinline__ void fwd_walk(const uint2 range, const int32_t* __res
             // every lane evaluates (the warp runs the instructions anyway); finished pixels just do not composite
             // (no per-entry all-done vote: early termination is checked once per chunk by the outer loop --
             // the rest of a chunk after every pixel finished composites nothing; +0.65 %, ab_r02 s53)
-            fwd_entry<MODE, NT, TL>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
+            fwd_entry<MODE, NT, TL, true>(h, tex, id, c0 + bit, x, y, rc, N, early, done, T, acc0, acc1, acc2, last);
         }
     }
+#undef GB_K3_DONE
 }
 
 // render_backward's per-pixel loop (raster.hpp:313-364) for the calling warp's pixels
