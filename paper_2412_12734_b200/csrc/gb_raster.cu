@@ -521,14 +521,15 @@ __device__ __forceinline__ float4 ld_rect(const float4* r) {
     return v;
 }
 
+// (slot: the lane for K3, 31 - lane for K4's back-to-front walk)
 __device__ __forceinline__ void stage_headers(WarpHeaders& wh, const ScreenHeader* __restrict__ hdr, bool pass,
-                                              int idl, int lane) {
+                                              int idl, int slot) {
     __syncwarp();  // the previous chunk's readers are done
     if (pass) {
-        wh.h[0][lane] = ld_real4(&hdr[idl].h0);
-        wh.h[1][lane] = ld_real4(&hdr[idl].h1);
-        wh.h[2][lane] = ld_real4(&hdr[idl].h2);
-        wh.id[lane] = idl;
+        wh.h[0][slot] = ld_real4(&hdr[idl].h0);
+        wh.h[1][slot] = ld_real4(&hdr[idl].h1);
+        wh.h[2][slot] = ld_real4(&hdr[idl].h2);
+        wh.id[slot] = idl;
     }
     __syncwarp();
 }
@@ -635,15 +636,20 @@ __device__ __forceinline__ void bwd_walk(const uint2 range, const int32_t* __res
         unsigned mask = __ballot_sync(kFull, pass);
         if (lane == 0) GB_DBG(1, __popc(mask));
 #if GB_WARP_STAGE
-        if (mask) stage_headers(*wh, hdr, pass, idl, lane);
-#endif
+        // entries staged in reverse slot order (slot 31 - lane), so the back-to-front walk takes the lowest set
+        // bit of the reversed ballot: a shorter per-entry index computation (+0.3 %, ab_r02 s61)
+        if (mask) stage_headers(*wh, hdr, pass, idl, 31 - lane);
+        unsigned rmask = __brev(mask);
+        while (rmask) {
+            const int slot = __ffs(rmask) - 1;
+            rmask &= rmask - 1;
+            const int bit = 31 - slot;
+            const int id = wh->id[slot];
+            const ScreenHeader h = staged_hdr(*wh, slot);
+#else
         while (mask) {
             const int bit = 31 - __clz(mask);
             mask &= ~(1u << bit);
-#if GB_WARP_STAGE
-            const int id = wh->id[bit];
-            const ScreenHeader h = staged_hdr(*wh, bit);
-#else
             const int id = __shfl_sync(kFull, idl, bit);
             ScreenHeader h;
             h.h0 = ld_real4(&hdr[id].h0);
